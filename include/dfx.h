@@ -1,0 +1,241 @@
+/*
+ * dfx.h — C ABI of libdfx, the sm_100a execution library behind the fused-DAG
+ * path of FusedInf (arXiv 2410.21120).
+ *
+ * The reference exposes this path only as a Python API (no FFI exists):
+ *   fuse_models            /root/reference/pkg/src/dagfuse/fuse.py:165-200
+ *   execute_fused          /root/reference/pkg/src/dagfuse/fuse.py:268-291
+ *   swap_subgraph          /root/reference/pkg/src/dagfuse/fuse.py:203-242
+ *   executor.run/run_batch /root/reference/pkg/src/dagfuse/executor.py:187-201
+ *   simulated swap-in      /root/reference/pkg/src/dagfuse/costmodel.py:277-338
+ * Python keeps those signatures (paper_2410_21120_b200/fuse.py) and crosses
+ * into this library through ctypes (paper_2410_21120_b200/runtime.py); the
+ * binding a maintainer would add to the reference is in INTEGRATION.md.
+ * Each entry point below names the reference function whose work it does.
+ *
+ * Conventions: plain pointers and sizes only; every function returns
+ * DFX_OK (0) or a negative dfx_status and never throws; dfx_last_error()
+ * returns a thread-local message for the last failure on the calling thread.
+ * Streams are passed as opaque void* (a cudaStream_t; NULL = legacy default).
+ * No function synchronises unless its comment says so.
+ *
+ * Data layout on the device: activations are bf16 NHWC with a channel pitch
+ * that is a multiple of 8 elements (16 B); a tensor may be a channel window
+ * [coff, coff + C) of a wider buffer (zero-copy concat).  Weights live in one
+ * packed arena.
+ */
+#ifndef DFX_H
+#define DFX_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DFX_ABI_VERSION 1
+
+typedef enum dfx_status {
+  DFX_OK = 0,
+  DFX_E_CUDA = -1,         /* a CUDA runtime/driver call failed */
+  DFX_E_ARG = -2,          /* invalid argument */
+  DFX_E_NOMEM = -3,        /* device or pinned-host allocation failed */
+  DFX_E_UNSUPPORTED = -4,  /* shape/feature not supported by the kernels */
+  DFX_E_STATE = -5,        /* call out of order (e.g. launch before instantiate) */
+  DFX_E_NODEVICE = -6      /* no sm_100 device visible */
+} dfx_status;
+
+typedef enum dfx_act {
+  DFX_ACT_NONE = 0, DFX_ACT_RELU = 1, DFX_ACT_HARDSWISH = 2,
+  DFX_ACT_HARDSIGMOID = 3, DFX_ACT_SILU = 4, DFX_ACT_SIGMOID = 5
+} dfx_act;
+
+typedef enum dfx_binop {
+  DFX_BIN_NONE = 0,
+  DFX_BIN_ADD = 1,     /* v += other[n, h, w, c]            (residual_add)   */
+  DFX_BIN_SCALE = 2    /* v *= other[n, 0, 0, c]            (channel_scale)  */
+} dfx_binop;
+
+typedef enum dfx_op {
+  DFX_OP_GEMM = 1,     /* grouped implicit-GEMM conv / dense (tcgen05)      */
+  DFX_OP_SPLITK = 2,   /* split-K reduction + epilogue                     */
+  DFX_OP_DWCONV = 3,   /* depthwise conv + epilogue                        */
+  DFX_OP_POOL = 4,     /* max / avg pool, padded                           */
+  DFX_OP_GAP = 5,      /* global average pool                              */
+  DFX_OP_EW = 6,       /* affine/act/add/scale/copy on NHWC views          */
+  DFX_OP_IN = 7,       /* fp32 CHW samples -> bf16 NHWC                    */
+  DFX_OP_OUT = 8       /* bf16 NHWC -> fp32 samples in logical CHW order   */
+} dfx_op;
+
+/* A bf16 NHWC view: element (n, h, w, c) at base[((n*H + h)*W + w)*pitch + coff + c]. */
+typedef struct dfx_view {
+  void* base;
+  int32_t n, h, w, c;
+  int32_t pitch, coff;
+} dfx_view;
+
+/* Epilogue shared by GEMM / split-K / depthwise / elementwise:
+ *   v = x * alpha[c] + beta[c]   (alpha/beta NULL -> identity)
+ *   v = act1(v)
+ *   v = v (+|*) other            (binop)
+ *   v = act2(v)
+ * then rounded to bf16 and stored. */
+typedef struct dfx_epilogue {
+  const float* alpha;
+  const float* beta;
+  int32_t act1, act2, binop, _pad;
+  dfx_view other;
+} dfx_epilogue;
+
+/* One implicit-GEMM problem (conv2d groups=1, or dense as a 1x1-output conv).
+ *   M = output pixels (n, p, q), tiled as tn x tp x tq <= 128 rows
+ *   N = output channels, tiles of bn (multiple of 16, <= 256)
+ *   K = r * s * ceil(cin / cb) * cb, consumed in sub-blocks of cb channels
+ * tmap_a / tmap_b are CUtensorMap objects written by dfx_tmap_act /
+ * dfx_tmap_weights.  Filled by the host, uploaded to device memory. */
+typedef struct __attribute__((aligned(64))) dfx_gemm_desc {
+  uint64_t tmap_a[16];
+  uint64_t tmap_b[16];
+  int32_t n, p, q;                 /* output extents */
+  int32_t tn, tp, tq;              /* M tile extents */
+  int32_t mt_n, mt_p, mt_q;        /* M tiles along n, p, q */
+  int32_t nt;                      /* N tiles */
+  int32_t r, s, stride_h, stride_w, pad_h, pad_w;
+  int32_t cb;                      /* channel block: 16, 32 or 64 */
+  int32_t cblocks;                 /* ceil(cin / cb) */
+  int32_t ksteps;                  /* r * s * cblocks */
+  int32_t kpack;                   /* 64 / cb sub-blocks per pipeline stage */
+  int32_t stages;                  /* ceil(ksteps / kpack) */
+  int32_t splits;                  /* split-K factor (1 = fused epilogue) */
+  int32_t stages_per_split;
+  int32_t bn;                      /* N tile width */
+  int32_t cout;
+  int32_t tile_begin;              /* first blockIdx.x of this problem */
+  int32_t tiles;                   /* mt_n*mt_p*mt_q*nt*splits */
+  int32_t _pad0;
+  dfx_view out;                    /* bf16 output view (n, p, q, cout) */
+  dfx_epilogue epi;
+  float* ws;                       /* split-K workspace [splits][n*p*q][nt*bn] */
+  int64_t _pad1[5];                
+} dfx_gemm_desc;
+
+typedef struct dfx_gemm_launch {
+  const dfx_gemm_desc* descs;      /* device pointer, ndesc entries */
+  int32_t ndesc;
+  int32_t total_tiles;             /* grid size */
+  int32_t bn_max;                  /* sizes smem / TMEM */
+  int32_t _pad;
+} dfx_gemm_launch;
+
+typedef struct dfx_splitk_params {
+  const float* ws;
+  int32_t splits, pixels, cout, ldw;   /* ws row stride (nt*bn) */
+  dfx_view out;                        /* out.n*out.h*out.w == pixels */
+  dfx_epilogue epi;
+} dfx_splitk_params;
+
+typedef struct dfx_dwconv_params {
+  dfx_view in, out;                    /* out.c == in.c */
+  const float* weight;                 /* [kh*kw][c] fp32 */
+  int32_t kh, kw, stride_h, stride_w, pad_h, pad_w;
+  dfx_epilogue epi;
+} dfx_dwconv_params;
+
+typedef struct dfx_pool_params {
+  dfx_view in, out;
+  int32_t kh, kw, stride_h, stride_w, pad_h, pad_w;
+  int32_t is_max, count_include_pad;
+} dfx_pool_params;
+
+typedef struct dfx_gap_params {
+  dfx_view in, out;                    /* out.h == out.w == 1 */
+} dfx_gap_params;
+
+typedef struct dfx_ew_params {
+  dfx_view in, out;                    /* same n, h, w, c */
+  dfx_epilogue epi;
+} dfx_ew_params;
+
+typedef struct dfx_in_params {
+  const float* src;                    /* n samples, each c*h*w fp32 in CHW order */
+  dfx_view out;
+} dfx_in_params;
+
+typedef struct dfx_out_params {
+  dfx_view in;
+  float* dst;                          /* n samples, each c*h*w fp32 in CHW order */
+} dfx_out_params;
+
+/* ---- library / device ------------------------------------------------- */
+const char* dfx_last_error(void);
+int dfx_abi_version(void);
+/* sizeof() of a struct declared here, by name ("dfx_gemm_desc", ...); -1 if
+ * unknown.  Lets bindings verify their mirrored layouts at load time. */
+int dfx_sizeof(const char* name);
+/* Selects the device on the calling thread, checks sm_100, sets kernel
+ * attributes.  Idempotent. */
+int dfx_init(int device);
+int dfx_device_info(int device, int* sm_count, int* cc_major, int* cc_minor,
+                    size_t* total_mem);
+int dfx_mem_info(size_t* free_bytes, size_t* total_bytes);
+
+/* ---- memory ------------------------------------------------------------ */
+int dfx_malloc(void** dptr, size_t bytes);
+int dfx_free(void* dptr);
+int dfx_memset(void* dptr, int value, size_t bytes, void* stream);
+int dfx_host_alloc(void** hptr, size_t bytes);          /* pinned */
+int dfx_host_free(void* hptr);
+int dfx_host_register(void* hptr, size_t bytes);
+int dfx_host_unregister(void* hptr);
+int dfx_memcpy_h2d(void* dst, const void* src, size_t bytes, void* stream);
+int dfx_memcpy_d2h(void* dst, const void* src, size_t bytes, void* stream);
+int dfx_memcpy_d2d(void* dst, const void* src, size_t bytes, void* stream);
+
+/* Swap-in (replaces the modelled memcpy phase of simulate_load,
+ * costmodel.py:277-305): ONE device allocation and ONE cudaMemcpyAsync of a
+ * packed weight arena from pinned host memory. */
+int dfx_arena_upload(const void* pinned_host, size_t bytes, void** dev_arena, void* stream);
+
+/* ---- streams / events --------------------------------------------------- */
+int dfx_stream_create(void** stream);
+int dfx_stream_destroy(void* stream);
+int dfx_stream_sync(void* stream);                       /* synchronises */
+int dfx_event_create(void** ev);
+int dfx_event_destroy(void* ev);
+int dfx_event_record(void* ev, void* stream);
+int dfx_event_elapsed(void* start, void* stop, float* ms); /* synchronises on stop */
+
+/* ---- tensor maps (TMA descriptors, 128 B written to out128) -------------- */
+/* Activation view as a 4-D tiled map (c, w, h, n); box (cb, tq*sw, tp*sh, tn)
+ * with element strides (1, sw, sh, 1); 16/32/64-channel boxes use the
+ * 32/64/128-byte swizzle; out-of-bounds elements (padding, channel tails)
+ * read as zero. */
+int dfx_tmap_act(void* out128, const dfx_view* v, int cb, int tq, int tp, int tn,
+                 int stride_w, int stride_h);
+/* Packed weight matrix [rows][k] bf16 (k contiguous); box (cb, bn). */
+int dfx_tmap_weights(void* out128, const void* base, int rows, int k, int cb, int bn);
+
+/* ---- kernels: direct launch on a stream (tests, eager mode) ------------- */
+int dfx_launch(int op, const void* params, size_t params_size, void* stream);
+
+/* ---- CUDA graph of the fused DAG --------------------------------------- */
+/* Nodes are kernel launches with explicit dependencies; the executor
+ * instantiates one cudaGraphExec per (DAG, batch signature, instance). */
+int dfx_graph_create(void** graph);
+int dfx_graph_add(void* graph, int op, const void* params, size_t params_size,
+                  const int* deps, int ndeps, int* node_id);
+int dfx_graph_instantiate(void* graph);
+int dfx_graph_launch(void* graph, void* stream);
+int dfx_graph_node_count(void* graph, int* count);
+int dfx_graph_destroy(void* graph);
+
+/* End-to-end query (execute_fused, fuse.py:268-291): H2D of the packed fp32
+ * inputs, one graph launch, D2H of the packed fp32 outputs, stream sync. */
+int dfx_execute(void* graph, const void* host_in, void* dev_in, size_t in_bytes,
+                void* host_out, const void* dev_out, size_t out_bytes, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DFX_H */

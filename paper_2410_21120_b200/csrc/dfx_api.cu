@@ -1,0 +1,453 @@
+// dfx_api.cu — the C ABI of libdfx (declared in include/dfx.h).
+//
+// Memory, streams, TMA descriptor encoding, kernel dispatch, and the CUDA
+// graph that executes a whole fused DAG.  Host-side only; kernels live in
+// dfx_gemm.cu and dfx_bw.cu.
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "dfx_common.cuh"
+
+namespace dfx {
+__global__ void gemm_kernel(const __grid_constant__ dfx_gemm_launch L);
+__global__ void splitk_kernel(const __grid_constant__ dfx_splitk_params P);
+__global__ void ew_kernel(const __grid_constant__ dfx_ew_params P);
+__global__ void dwconv_kernel(const __grid_constant__ dfx_dwconv_params P);
+__global__ void pool_kernel(const __grid_constant__ dfx_pool_params P);
+__global__ void gap_kernel(const __grid_constant__ dfx_gap_params P);
+__global__ void in_kernel(const __grid_constant__ dfx_in_params P);
+__global__ void out_kernel(const __grid_constant__ dfx_out_params P);
+}  // namespace dfx
+
+namespace {
+
+thread_local std::string g_err;
+int g_sm_count = 148;
+
+int fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+#define CK(call)                                                                       \
+  do {                                                                                 \
+    cudaError_t _e = (call);                                                           \
+    if (_e != cudaSuccess)                                                             \
+      return fail(DFX_E_CUDA, "%s: %s (%s:%d)", #call, cudaGetErrorString(_e), __FILE__, \
+                  __LINE__);                                                           \
+  } while (0)
+
+inline cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// --- cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda).
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                   const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeTiledFn g_encode = nullptr;
+std::once_flag g_encode_once;
+
+int get_encode() {
+  std::call_once(g_encode_once, [] {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      g_encode = reinterpret_cast<EncodeTiledFn>(fn);
+  });
+  return g_encode ? DFX_OK : fail(DFX_E_CUDA, "cuTensorMapEncodeTiled unavailable");
+}
+
+CUtensorMapSwizzle swizzle_for(int cb) {
+  return cb == 64 ? CU_TENSOR_MAP_SWIZZLE_128B
+                  : (cb == 32 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B);
+}
+
+int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+unsigned elementwise_grid(int64_t threads, int block) {
+  int64_t g = cdiv(threads, block);
+  const int64_t cap = int64_t(g_sm_count) * 32;
+  if (g > cap) g = cap;
+  if (g < 1) g = 1;
+  return unsigned(g);
+}
+
+struct LaunchCfg {
+  const void* func;
+  dim3 grid, block;
+  size_t smem;
+};
+
+int config_for(int op, const void* params, size_t size, LaunchCfg* c) {
+#define NEED(T)                                                                            \
+  if (size != sizeof(T)) return fail(DFX_E_ARG, "op %d: params size %zu != %zu", op, size, \
+                                     sizeof(T));
+  c->block = dim3(256);
+  c->smem = 0;
+  switch (op) {
+    case DFX_OP_GEMM: {
+      NEED(dfx_gemm_launch);
+      const auto* p = static_cast<const dfx_gemm_launch*>(params);
+      if (p->bn_max < 16 || p->bn_max > 256 || p->total_tiles < 1)
+        return fail(DFX_E_ARG, "gemm: bad bn_max %d / tiles %d", p->bn_max, p->total_tiles);
+      c->func = reinterpret_cast<const void*>(&dfx::gemm_kernel);
+      c->grid = dim3(p->total_tiles);
+      c->block = dim3(128);
+      c->smem = dfx::gemm_smem_bytes(p->bn_max) + 1024;
+      return DFX_OK;
+    }
+    case DFX_OP_SPLITK: {
+      NEED(dfx_splitk_params);
+      const auto* p = static_cast<const dfx_splitk_params*>(params);
+      c->func = reinterpret_cast<const void*>(&dfx::splitk_kernel);
+      c->grid = dim3(elementwise_grid(int64_t(p->pixels) * cdiv(p->cout, 8), 256));
+      return DFX_OK;
+    }
+    case DFX_OP_DWCONV: {
+      NEED(dfx_dwconv_params);
+      const auto* p = static_cast<const dfx_dwconv_params*>(params);
+      c->func = reinterpret_cast<const void*>(&dfx::dwconv_kernel);
+      c->grid = dim3(elementwise_grid(int64_t(p->out.n) * p->out.h * p->out.w * cdiv(p->in.c, 8), 256));
+      return DFX_OK;
+    }
+    case DFX_OP_POOL: {
+      NEED(dfx_pool_params);
+      const auto* p = static_cast<const dfx_pool_params*>(params);
+      c->func = reinterpret_cast<const void*>(&dfx::pool_kernel);
+      c->grid = dim3(elementwise_grid(int64_t(p->out.n) * p->out.h * p->out.w * cdiv(p->in.c, 8), 256));
+      return DFX_OK;
+    }
+    case DFX_OP_GAP: {
+      NEED(dfx_gap_params);
+      const auto* p = static_cast<const dfx_gap_params*>(params);
+      c->func = reinterpret_cast<const void*>(&dfx::gap_kernel);
+      c->grid = dim3(unsigned(cdiv(p->in.c, 256)), unsigned(p->in.n));
+      return DFX_OK;
+    }
+    case DFX_OP_EW: {
+      NEED(dfx_ew_params);
+      const auto* p = static_cast<const dfx_ew_params*>(params);
+      c->func = reinterpret_cast<const void*>(&dfx::ew_kernel);
+      c->grid = dim3(elementwise_grid(int64_t(p->in.n) * p->in.h * p->in.w * cdiv(p->in.c, 8), 256));
+      return DFX_OK;
+    }
+    case DFX_OP_IN: {
+      NEED(dfx_in_params);
+      const auto* p = static_cast<const dfx_in_params*>(params);
+      if (p->out.pitch % 8 || p->out.coff) return fail(DFX_E_ARG, "in: pitch/coff");
+      c->func = reinterpret_cast<const void*>(&dfx::in_kernel);
+      c->grid = dim3(elementwise_grid(int64_t(p->out.n) * p->out.h * p->out.w * (p->out.pitch / 8), 256));
+      return DFX_OK;
+    }
+    case DFX_OP_OUT: {
+      NEED(dfx_out_params);
+      const auto* p = static_cast<const dfx_out_params*>(params);
+      c->func = reinterpret_cast<const void*>(&dfx::out_kernel);
+      c->grid = dim3(elementwise_grid(int64_t(p->in.n) * p->in.h * p->in.w * p->in.c, 256));
+      return DFX_OK;
+    }
+  }
+#undef NEED
+  return fail(DFX_E_ARG, "unknown op %d", op);
+}
+
+struct Graph {
+  cudaGraph_t g = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  std::vector<cudaGraphNode_t> nodes;
+};
+
+}  // namespace
+
+extern "C" {
+
+const char* dfx_last_error(void) { return g_err.c_str(); }
+int dfx_abi_version(void) { return DFX_ABI_VERSION; }
+
+int dfx_sizeof(const char* name) {
+  struct {
+    const char* n;
+    int s;
+  } t[] = {{"dfx_view", sizeof(dfx_view)},
+           {"dfx_epilogue", sizeof(dfx_epilogue)},
+           {"dfx_gemm_desc", sizeof(dfx_gemm_desc)},
+           {"dfx_gemm_launch", sizeof(dfx_gemm_launch)},
+           {"dfx_splitk_params", sizeof(dfx_splitk_params)},
+           {"dfx_dwconv_params", sizeof(dfx_dwconv_params)},
+           {"dfx_pool_params", sizeof(dfx_pool_params)},
+           {"dfx_gap_params", sizeof(dfx_gap_params)},
+           {"dfx_ew_params", sizeof(dfx_ew_params)},
+           {"dfx_in_params", sizeof(dfx_in_params)},
+           {"dfx_out_params", sizeof(dfx_out_params)}};
+  for (auto& e : t)
+    if (!strcmp(e.n, name)) return e.s;
+  return -1;
+}
+
+int dfx_init(int device) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0)
+    return fail(DFX_E_NODEVICE, "no CUDA device visible");
+  if (device < 0 || device >= n) return fail(DFX_E_ARG, "device %d of %d", device, n);
+  CK(cudaSetDevice(device));
+  cudaDeviceProp prop;
+  CK(cudaGetDeviceProperties(&prop, device));
+  if (prop.major != 10)
+    return fail(DFX_E_NODEVICE, "device %d is sm_%d%d; libdfx is built for sm_100a", device,
+                prop.major, prop.minor);
+  g_sm_count = prop.multiProcessorCount;
+  CK(cudaFuncSetAttribute(reinterpret_cast<const void*>(&dfx::gemm_kernel),
+                          cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          dfx::gemm_smem_bytes(256) + 1024));
+  return get_encode();
+}
+
+int dfx_device_info(int device, int* sm_count, int* cc_major, int* cc_minor, size_t* total_mem) {
+  cudaDeviceProp prop;
+  CK(cudaGetDeviceProperties(&prop, device));
+  if (sm_count) *sm_count = prop.multiProcessorCount;
+  if (cc_major) *cc_major = prop.major;
+  if (cc_minor) *cc_minor = prop.minor;
+  if (total_mem) *total_mem = prop.totalGlobalMem;
+  return DFX_OK;
+}
+
+int dfx_mem_info(size_t* free_bytes, size_t* total_bytes) {
+  CK(cudaMemGetInfo(free_bytes, total_bytes));
+  return DFX_OK;
+}
+
+int dfx_malloc(void** dptr, size_t bytes) {
+  if (!dptr) return fail(DFX_E_ARG, "null out pointer");
+  cudaError_t e = cudaMalloc(dptr, bytes ? bytes : 1);
+  if (e != cudaSuccess) return fail(DFX_E_NOMEM, "cudaMalloc(%zu): %s", bytes, cudaGetErrorString(e));
+  return DFX_OK;
+}
+int dfx_free(void* dptr) {
+  CK(cudaFree(dptr));
+  return DFX_OK;
+}
+int dfx_memset(void* dptr, int value, size_t bytes, void* stream) {
+  CK(cudaMemsetAsync(dptr, value, bytes, S(stream)));
+  return DFX_OK;
+}
+int dfx_host_alloc(void** hptr, size_t bytes) {
+  cudaError_t e = cudaHostAlloc(hptr, bytes ? bytes : 1, cudaHostAllocDefault);
+  if (e != cudaSuccess) return fail(DFX_E_NOMEM, "cudaHostAlloc(%zu): %s", bytes, cudaGetErrorString(e));
+  return DFX_OK;
+}
+int dfx_host_free(void* hptr) {
+  CK(cudaFreeHost(hptr));
+  return DFX_OK;
+}
+int dfx_host_register(void* hptr, size_t bytes) {
+  CK(cudaHostRegister(hptr, bytes, cudaHostRegisterDefault));
+  return DFX_OK;
+}
+int dfx_host_unregister(void* hptr) {
+  CK(cudaHostUnregister(hptr));
+  return DFX_OK;
+}
+int dfx_memcpy_h2d(void* dst, const void* src, size_t bytes, void* stream) {
+  CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, S(stream)));
+  return DFX_OK;
+}
+int dfx_memcpy_d2h(void* dst, const void* src, size_t bytes, void* stream) {
+  CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, S(stream)));
+  return DFX_OK;
+}
+int dfx_memcpy_d2d(void* dst, const void* src, size_t bytes, void* stream) {
+  CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, S(stream)));
+  return DFX_OK;
+}
+
+int dfx_arena_upload(const void* pinned_host, size_t bytes, void** dev_arena, void* stream) {
+  int rc = dfx_malloc(dev_arena, bytes);
+  if (rc) return rc;
+  CK(cudaMemcpyAsync(*dev_arena, pinned_host, bytes, cudaMemcpyHostToDevice, S(stream)));
+  return DFX_OK;
+}
+
+int dfx_stream_create(void** stream) {
+  cudaStream_t s;
+  CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  *stream = s;
+  return DFX_OK;
+}
+int dfx_stream_destroy(void* stream) {
+  CK(cudaStreamDestroy(S(stream)));
+  return DFX_OK;
+}
+int dfx_stream_sync(void* stream) {
+  CK(cudaStreamSynchronize(S(stream)));
+  return DFX_OK;
+}
+int dfx_event_create(void** ev) {
+  cudaEvent_t e;
+  CK(cudaEventCreate(&e));
+  *ev = e;
+  return DFX_OK;
+}
+int dfx_event_destroy(void* ev) {
+  CK(cudaEventDestroy(reinterpret_cast<cudaEvent_t>(ev)));
+  return DFX_OK;
+}
+int dfx_event_record(void* ev, void* stream) {
+  CK(cudaEventRecord(reinterpret_cast<cudaEvent_t>(ev), S(stream)));
+  return DFX_OK;
+}
+int dfx_event_elapsed(void* start, void* stop, float* ms) {
+  CK(cudaEventSynchronize(reinterpret_cast<cudaEvent_t>(stop)));
+  CK(cudaEventElapsedTime(ms, reinterpret_cast<cudaEvent_t>(start),
+                          reinterpret_cast<cudaEvent_t>(stop)));
+  return DFX_OK;
+}
+
+int dfx_tmap_act(void* out128, const dfx_view* v, int cb, int tq, int tp, int tn, int stride_w,
+                 int stride_h) {
+  int rc = get_encode();
+  if (rc) return rc;
+  if (!v || !out128) return fail(DFX_E_ARG, "tmap_act: null");
+  if (cb != 16 && cb != 32 && cb != 64) return fail(DFX_E_ARG, "tmap_act: cb %d", cb);
+  if (v->pitch % 8 || v->coff % 8) return fail(DFX_E_ARG, "tmap_act: pitch %d coff %d", v->pitch, v->coff);
+  if (tq * stride_w > 256 || tp * stride_h > 256 || tn > 256 || tq * tp * tn > 128)
+    return fail(DFX_E_ARG, "tmap_act: box %dx%dx%d stride %d,%d", tq, tp, tn, stride_w, stride_h);
+  void* base = static_cast<char*>(v->base) + int64_t(v->coff) * 2;
+  if (reinterpret_cast<uintptr_t>(base) % 16) return fail(DFX_E_ARG, "tmap_act: base alignment");
+  cuuint64_t dims[4] = {cuuint64_t(v->c), cuuint64_t(v->w), cuuint64_t(v->h), cuuint64_t(v->n)};
+  cuuint64_t strides[3] = {cuuint64_t(v->pitch) * 2, cuuint64_t(v->pitch) * 2 * v->w,
+                           cuuint64_t(v->pitch) * 2 * v->w * v->h};
+  cuuint32_t box[4] = {cuuint32_t(cb), cuuint32_t(tq * stride_w), cuuint32_t(tp * stride_h),
+                       cuuint32_t(tn)};
+  cuuint32_t estr[4] = {1, cuuint32_t(stride_w), cuuint32_t(stride_h), 1};
+  CUresult r = g_encode(reinterpret_cast<CUtensorMap*>(out128), CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4,
+                        base, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                        swizzle_for(cb), CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    return fail(DFX_E_CUDA, "cuTensorMapEncodeTiled(act c=%d w=%d h=%d n=%d pitch=%d cb=%d box=%u,%u,%u,%u) = %d",
+                v->c, v->w, v->h, v->n, v->pitch, cb, box[0], box[1], box[2], box[3], int(r));
+  return DFX_OK;
+}
+
+int dfx_tmap_weights(void* out128, const void* base, int rows, int k, int cb, int bn) {
+  int rc = get_encode();
+  if (rc) return rc;
+  if (cb != 16 && cb != 32 && cb != 64) return fail(DFX_E_ARG, "tmap_weights: cb %d", cb);
+  if (k % 8 || reinterpret_cast<uintptr_t>(base) % 16)
+    return fail(DFX_E_ARG, "tmap_weights: k %d / alignment", k);
+  cuuint64_t dims[2] = {cuuint64_t(k), cuuint64_t(rows)};
+  cuuint64_t strides[1] = {cuuint64_t(k) * 2};
+  cuuint32_t box[2] = {cuuint32_t(cb), cuuint32_t(bn)};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = g_encode(reinterpret_cast<CUtensorMap*>(out128), CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+                        const_cast<void*>(base), dims, strides, box, estr,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, swizzle_for(cb),
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    return fail(DFX_E_CUDA, "cuTensorMapEncodeTiled(weights rows=%d k=%d cb=%d bn=%d) = %d", rows, k,
+                cb, bn, int(r));
+  return DFX_OK;
+}
+
+int dfx_launch(int op, const void* params, size_t params_size, void* stream) {
+  LaunchCfg c;
+  int rc = config_for(op, params, params_size, &c);
+  if (rc) return rc;
+  void* args[1] = {const_cast<void*>(params)};
+  CK(cudaLaunchKernel(c.func, c.grid, c.block, args, c.smem, S(stream)));
+  return DFX_OK;
+}
+
+int dfx_graph_create(void** graph) {
+  auto* g = new Graph();
+  cudaError_t e = cudaGraphCreate(&g->g, 0);
+  if (e != cudaSuccess) {
+    delete g;
+    return fail(DFX_E_CUDA, "cudaGraphCreate: %s", cudaGetErrorString(e));
+  }
+  *graph = g;
+  return DFX_OK;
+}
+
+int dfx_graph_add(void* graph, int op, const void* params, size_t params_size, const int* deps,
+                  int ndeps, int* node_id) {
+  auto* g = static_cast<Graph*>(graph);
+  if (!g || g->exec) return fail(DFX_E_STATE, "graph_add after instantiate");
+  LaunchCfg c;
+  int rc = config_for(op, params, params_size, &c);
+  if (rc) return rc;
+  std::vector<cudaGraphNode_t> dn;
+  for (int i = 0; i < ndeps; ++i) {
+    if (deps[i] < 0 || deps[i] >= int(g->nodes.size()))
+      return fail(DFX_E_ARG, "graph_add: dependency %d out of range", deps[i]);
+    dn.push_back(g->nodes[deps[i]]);
+  }
+  cudaKernelNodeParams kp = {};
+  void* args[1] = {const_cast<void*>(params)};
+  kp.func = const_cast<void*>(c.func);
+  kp.gridDim = c.grid;
+  kp.blockDim = c.block;
+  kp.sharedMemBytes = unsigned(c.smem);
+  kp.kernelParams = args;
+  cudaGraphNode_t node;
+  CK(cudaGraphAddKernelNode(&node, g->g, dn.data(), dn.size(), &kp));
+  g->nodes.push_back(node);
+  if (node_id) *node_id = int(g->nodes.size()) - 1;
+  return DFX_OK;
+}
+
+int dfx_graph_instantiate(void* graph) {
+  auto* g = static_cast<Graph*>(graph);
+  if (!g) return fail(DFX_E_ARG, "null graph");
+  if (g->exec) return DFX_OK;
+  CK(cudaGraphInstantiate(&g->exec, g->g, 0));
+  return DFX_OK;
+}
+
+int dfx_graph_launch(void* graph, void* stream) {
+  auto* g = static_cast<Graph*>(graph);
+  if (!g || !g->exec) return fail(DFX_E_STATE, "graph not instantiated");
+  CK(cudaGraphLaunch(g->exec, S(stream)));
+  return DFX_OK;
+}
+
+int dfx_graph_node_count(void* graph, int* count) {
+  auto* g = static_cast<Graph*>(graph);
+  if (!g) return fail(DFX_E_ARG, "null graph");
+  *count = int(g->nodes.size());
+  return DFX_OK;
+}
+
+int dfx_graph_destroy(void* graph) {
+  auto* g = static_cast<Graph*>(graph);
+  if (!g) return DFX_OK;
+  if (g->exec) cudaGraphExecDestroy(g->exec);
+  if (g->g) cudaGraphDestroy(g->g);
+  delete g;
+  return DFX_OK;
+}
+
+int dfx_execute(void* graph, const void* host_in, void* dev_in, size_t in_bytes, void* host_out,
+                const void* dev_out, size_t out_bytes, void* stream) {
+  CK(cudaMemcpyAsync(dev_in, host_in, in_bytes, cudaMemcpyHostToDevice, S(stream)));
+  int rc = dfx_graph_launch(graph, stream);
+  if (rc) return rc;
+  CK(cudaMemcpyAsync(host_out, dev_out, out_bytes, cudaMemcpyDeviceToHost, S(stream)));
+  CK(cudaStreamSynchronize(S(stream)));
+  return DFX_OK;
+}
+
+}  // extern "C"
+

@@ -1,0 +1,257 @@
+// dfx_bw.cu — bandwidth-bound kernels on bf16 NHWC views.
+//
+// Reference semantics (/root/reference/pkg/src/dagfuse/executor.py):
+//   maxpool2d      :95-109   (+ padding, extension)      -> pool_kernel
+//   global_avg_pool:126-133  sum * fp32(1/HW)            -> gap_kernel
+//   batchnorm/relu/residual_add/concat copy :112-166      -> ew_kernel
+// Extension kinds: depthwise conv (dwconv_kernel), avgpool2d (pool_kernel),
+// hardswish/hardsigmoid/silu/sigmoid/channel_scale (ew_kernel epilogue).
+// Every kernel moves 8 channels (16 B) per thread when the view's channel
+// offset allows it and falls back to scalar lanes for ragged toy shapes.
+#include "dfx_common.cuh"
+
+namespace dfx {
+
+__device__ __forceinline__ int64_t grid_stride_start() {
+  return blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+}
+__device__ __forceinline__ int64_t grid_stride_step() { return int64_t(gridDim.x) * blockDim.x; }
+
+// ------------------------------------------------------------------ elementwise
+__global__ void ew_kernel(const __grid_constant__ dfx_ew_params P) {
+  const dfx_view& in = P.in;
+  const dfx_view& out = P.out;
+  const int cg = (in.c + 7) / 8;
+  const int hw = in.h * in.w;
+  const int64_t total = int64_t(in.n) * hw * cg;
+  const bool vec_ok_views = ((in.coff | out.coff | (P.epi.binop ? P.epi.other.coff : 0)) & 7) == 0;
+  for (int64_t idx = grid_stride_start(); idx < total; idx += grid_stride_step()) {
+    const int64_t pix = idx / cg;
+    const int c = int(idx - pix * cg) * 8;
+    const int n = int(pix / hw);
+    if (vec_ok_views && c + 8 <= in.c) {
+      float v[8];
+      unpack_bf16x8(*reinterpret_cast<const uint4*>(
+                        reinterpret_cast<const __nv_bfloat16*>(in.base) + view_pixel_index(in, pix, c)),
+                    v);
+      epilogue8(P.epi, v, pix, n, c);
+      *reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(out.base) +
+                                view_pixel_index(out, pix, c)) = pack_bf16x8(v);
+    } else {
+      for (int i = 0; i < 8 && c + i < in.c; ++i) {
+        const float x = bf16_at(in.base, view_pixel_index(in, pix, c + i));
+        bf16_store(out.base, view_pixel_index(out, pix, c + i), epilogue(P.epi, x, pix, n, c + i));
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------------ depthwise conv
+// One thread = 8 channels of one output pixel; fp32 taps [kh*kw][c].
+__global__ void dwconv_kernel(const __grid_constant__ dfx_dwconv_params P) {
+  const dfx_view& in = P.in;
+  const dfx_view& out = P.out;
+  const int C = in.c;
+  const int cg = (C + 7) / 8;
+  const int64_t total = int64_t(out.n) * out.h * out.w * cg;
+  const bool vec_ok_views = ((in.coff | out.coff) & 7) == 0 && (C & 7) == 0;
+  for (int64_t idx = grid_stride_start(); idx < total; idx += grid_stride_step()) {
+    const int64_t pix = idx / cg;
+    const int c = int(idx - pix * cg) * 8;
+    const int q = int(pix % out.w);
+    const int p = int((pix / out.w) % out.h);
+    const int n = int(pix / (int64_t(out.w) * out.h));
+    float acc[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) acc[i] = 0.0f;
+    const int h0 = p * P.stride_h - P.pad_h;
+    const int w0 = q * P.stride_w - P.pad_w;
+    if (vec_ok_views) {
+      for (int ki = 0; ki < P.kh; ++ki) {
+        const int h = h0 + ki;
+        if (h < 0 || h >= in.h) continue;
+        for (int kj = 0; kj < P.kw; ++kj) {
+          const int w = w0 + kj;
+          if (w < 0 || w >= in.w) continue;
+          float x[8];
+          unpack_bf16x8(*reinterpret_cast<const uint4*>(
+                            reinterpret_cast<const __nv_bfloat16*>(in.base) + view_index(in, n, h, w, c)),
+                        x);
+          const float* wt = P.weight + int64_t(ki * P.kw + kj) * C + c;
+          const float4 w_lo = __ldg(reinterpret_cast<const float4*>(wt));
+          const float4 w_hi = __ldg(reinterpret_cast<const float4*>(wt + 4));
+          acc[0] = fmaf(w_lo.x, x[0], acc[0]); acc[1] = fmaf(w_lo.y, x[1], acc[1]);
+          acc[2] = fmaf(w_lo.z, x[2], acc[2]); acc[3] = fmaf(w_lo.w, x[3], acc[3]);
+          acc[4] = fmaf(w_hi.x, x[4], acc[4]); acc[5] = fmaf(w_hi.y, x[5], acc[5]);
+          acc[6] = fmaf(w_hi.z, x[6], acc[6]); acc[7] = fmaf(w_hi.w, x[7], acc[7]);
+        }
+      }
+      epilogue8(P.epi, acc, pix, n, c);
+      *reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(out.base) +
+                                view_pixel_index(out, pix, c)) = pack_bf16x8(acc);
+    } else {
+      for (int i = 0; i < 8 && c + i < C; ++i) {
+        float a = 0.0f;
+        for (int ki = 0; ki < P.kh; ++ki) {
+          const int h = h0 + ki;
+          if (h < 0 || h >= in.h) continue;
+          for (int kj = 0; kj < P.kw; ++kj) {
+            const int w = w0 + kj;
+            if (w < 0 || w >= in.w) continue;
+            a = fmaf(P.weight[int64_t(ki * P.kw + kj) * C + c + i],
+                     bf16_at(in.base, view_index(in, n, h, w, c + i)), a);
+          }
+        }
+        bf16_store(out.base, view_pixel_index(out, pix, c + i), epilogue(P.epi, a, pix, n, c + i));
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------------ pooling
+__global__ void pool_kernel(const __grid_constant__ dfx_pool_params P) {
+  const dfx_view& in = P.in;
+  const dfx_view& out = P.out;
+  const int C = in.c;
+  const int cg = (C + 7) / 8;
+  const int64_t total = int64_t(out.n) * out.h * out.w * cg;
+  const bool vec = ((in.coff | out.coff) & 7) == 0;
+  for (int64_t idx = grid_stride_start(); idx < total; idx += grid_stride_step()) {
+    const int64_t pix = idx / cg;
+    const int c = int(idx - pix * cg) * 8;
+    const int q = int(pix % out.w);
+    const int p = int((pix / out.w) % out.h);
+    const int n = int(pix / (int64_t(out.w) * out.h));
+    const int h0 = p * P.stride_h - P.pad_h;
+    const int w0 = q * P.stride_w - P.pad_w;
+    const int nl = min(8, C - c);
+    float acc[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) acc[i] = P.is_max ? -INFINITY : 0.0f;
+    int count = 0;
+    for (int ki = 0; ki < P.kh; ++ki) {
+      const int h = h0 + ki;
+      if (h < 0 || h >= in.h) continue;
+      for (int kj = 0; kj < P.kw; ++kj) {
+        const int w = w0 + kj;
+        if (w < 0 || w >= in.w) continue;
+        ++count;
+        float x[8];
+        if (vec && nl == 8) {
+          unpack_bf16x8(*reinterpret_cast<const uint4*>(
+                            reinterpret_cast<const __nv_bfloat16*>(in.base) + view_index(in, n, h, w, c)),
+                        x);
+        } else {
+          for (int i = 0; i < 8; ++i) x[i] = i < nl ? bf16_at(in.base, view_index(in, n, h, w, c + i)) : 0.f;
+        }
+        if (P.is_max) {
+#pragma unroll
+          for (int i = 0; i < 8; ++i) acc[i] = fmaxf(acc[i], x[i]);
+        } else {
+#pragma unroll
+          for (int i = 0; i < 8; ++i) acc[i] += x[i];
+        }
+      }
+    }
+    if (!P.is_max) {
+      const float inv = 1.0f / float(P.count_include_pad ? P.kh * P.kw : count);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) acc[i] *= inv;
+    }
+    if (vec && nl == 8) {
+      *reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(out.base) +
+                                view_pixel_index(out, pix, c)) = pack_bf16x8(acc);
+    } else {
+      for (int i = 0; i < nl; ++i) bf16_store(out.base, view_pixel_index(out, pix, c + i), acc[i]);
+    }
+  }
+}
+
+// ------------------------------------------------------------------ global average pool
+// grid (ceil(C/256), N); 256 threads = 8 warps; lane handles 8 channels, warps
+// split the spatial range, smem reduction in fixed order.
+__global__ void gap_kernel(const __grid_constant__ dfx_gap_params P) {
+  __shared__ float part[8][256 + 8];
+  const dfx_view& in = P.in;
+  const int n = blockIdx.y;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int c = blockIdx.x * 256 + lane * 8;
+  const int hw = in.h * in.w;
+  const int nl = min(8, in.c - c);
+  float acc[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) acc[i] = 0.f;
+  if (nl > 0) {
+    const bool vec = nl == 8 && (in.coff & 7) == 0;
+    for (int s = warp; s < hw; s += 8) {
+      const int64_t base = view_pixel_index(in, int64_t(n) * hw + s, c);
+      float x[8];
+      if (vec) {
+        unpack_bf16x8(*reinterpret_cast<const uint4*>(
+                          reinterpret_cast<const __nv_bfloat16*>(in.base) + base), x);
+      } else {
+        for (int i = 0; i < 8; ++i) x[i] = i < nl ? bf16_at(in.base, base + i) : 0.f;
+      }
+#pragma unroll
+      for (int i = 0; i < 8; ++i) acc[i] += x[i];
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < 8; ++i) part[warp][lane * 8 + i] = acc[i];
+  __syncthreads();
+  if (warp == 0 && nl > 0) {
+    float v[8];
+    const float inv = 1.0f / float(hw);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      float s = 0.f;
+      for (int w = 0; w < 8; ++w) s += part[w][lane * 8 + i];
+      v[i] = s * inv;
+    }
+    const dfx_view& out = P.out;
+    const int64_t o = int64_t(n) * out.pitch + out.coff + c;
+    if (nl == 8 && (out.coff & 7) == 0) {
+      *reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(out.base) + o) = pack_bf16x8(v);
+    } else {
+      for (int i = 0; i < nl; ++i) bf16_store(out.base, o + i, v[i]);
+    }
+  }
+}
+
+// ------------------------------------------------------------------ layout conversion
+// fp32 CHW samples -> bf16 NHWC (pad channels written as zero).
+__global__ void in_kernel(const __grid_constant__ dfx_in_params P) {
+  const dfx_view& o = P.out;
+  const int hw = o.h * o.w;
+  const int cgp = o.pitch / 8;                 // channel groups incl. padding
+  const int64_t total = int64_t(o.n) * hw * cgp;
+  for (int64_t idx = grid_stride_start(); idx < total; idx += grid_stride_step()) {
+    const int64_t pix = idx / cgp;
+    const int c = int(idx - pix * cgp) * 8;
+    const int n = int(pix / hw);
+    const int s = int(pix - int64_t(n) * hw);
+    const float* src = P.src + int64_t(n) * o.c * hw + s;
+    float v[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) v[i] = (c + i < o.c) ? __ldg(src + int64_t(c + i) * hw) : 0.0f;
+    *reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(o.base) + pix * o.pitch + c) =
+        pack_bf16x8(v);
+  }
+}
+
+// bf16 NHWC -> fp32 samples in logical CHW order (also the flatten order).
+__global__ void out_kernel(const __grid_constant__ dfx_out_params P) {
+  const dfx_view& v = P.in;
+  const int hw = v.h * v.w;
+  const int64_t per = int64_t(v.c) * hw;
+  const int64_t total = int64_t(v.n) * per;
+  for (int64_t idx = grid_stride_start(); idx < total; idx += grid_stride_step()) {
+    const int n = int(idx / per);
+    const int64_t r = idx - int64_t(n) * per;
+    const int c = int(r / hw);
+    const int s = int(r - int64_t(c) * hw);
+    P.dst[idx] = bf16_at(v.base, view_pixel_index(v, int64_t(n) * hw + s, c));
+  }
+}
+
+}  // namespace dfx

@@ -1,0 +1,283 @@
+// dfx_common.cuh — shared device helpers for libdfx (sm_100a only).
+//
+// Thin inline-PTX wrappers for mbarrier, TMA (cp.async.bulk.tensor), tcgen05
+// (alloc / mma / commit / ld) and the bf16 + activation math every epilogue
+// uses.  Encodings follow the PTX ISA for sm_100a; the UMMA shared-memory and
+// instruction descriptor bit layouts match CUTLASS's cute/arch/mma_sm100_desc.hpp.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/dfx.h"
+
+#define DFX_DEV __device__ __forceinline__
+
+namespace dfx {
+
+// ---------------------------------------------------------------- math
+DFX_DEV float act_apply(int act, float v) {
+  switch (act) {
+    case DFX_ACT_RELU: return fmaxf(v, 0.0f);
+    case DFX_ACT_HARDSWISH: return v * fminf(fmaxf(v + 3.0f, 0.0f), 6.0f) / 6.0f;
+    case DFX_ACT_HARDSIGMOID: return fminf(fmaxf(v + 3.0f, 0.0f), 6.0f) / 6.0f;
+    case DFX_ACT_SILU: return v / (1.0f + __expf(-v));
+    case DFX_ACT_SIGMOID: return 1.0f / (1.0f + __expf(-v));
+    default: return v;
+  }
+}
+
+DFX_DEV uint32_t pack_bf16x2(float lo, float hi) {
+  __nv_bfloat162 h = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<uint32_t*>(&h);
+}
+
+DFX_DEV void unpack_bf16x8(const uint4& u, float* f) {
+  const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    float2 t = __bfloat1622float2(h[i]);
+    f[2 * i] = t.x;
+    f[2 * i + 1] = t.y;
+  }
+}
+
+DFX_DEV uint4 pack_bf16x8(const float* f) {
+  uint4 u;
+  u.x = pack_bf16x2(f[0], f[1]);
+  u.y = pack_bf16x2(f[2], f[3]);
+  u.z = pack_bf16x2(f[4], f[5]);
+  u.w = pack_bf16x2(f[6], f[7]);
+  return u;
+}
+
+DFX_DEV float bf16_at(const void* base, int64_t idx) {
+  return __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(base)[idx]);
+}
+
+DFX_DEV void bf16_store(void* base, int64_t idx, float v) {
+  reinterpret_cast<__nv_bfloat16*>(base)[idx] = __float2bfloat16_rn(v);
+}
+
+DFX_DEV int64_t view_index(const dfx_view& v, int n, int h, int w, int c) {
+  return ((int64_t(n) * v.h + h) * v.w + w) * v.pitch + v.coff + c;
+}
+
+DFX_DEV int64_t view_pixel_index(const dfx_view& v, int64_t pix, int c) {
+  return pix * v.pitch + v.coff + c;
+}
+
+// Full epilogue on one value.  `pix` is the flat (n*h*w) pixel index and n the
+// image index of the element; `c` its channel.
+DFX_DEV float epilogue(const dfx_epilogue& e, float x, int64_t pix, int n, int c) {
+  float v = x;
+  if (e.alpha) v = v * __ldg(e.alpha + c);
+  if (e.beta) v = v + __ldg(e.beta + c);
+  v = act_apply(e.act1, v);
+  if (e.binop == DFX_BIN_ADD) {
+    v += bf16_at(e.other.base, view_pixel_index(e.other, pix, c));
+  } else if (e.binop == DFX_BIN_SCALE) {
+    v *= bf16_at(e.other.base, int64_t(n) * e.other.pitch + e.other.coff + c);
+  }
+  return act_apply(e.act2, v);
+}
+
+// Vector form over 8 consecutive channels c..c+7 (caller guarantees alignment).
+DFX_DEV void epilogue8(const dfx_epilogue& e, float* v, int64_t pix, int n, int c) {
+  if (e.alpha) {
+    const float4 a0 = __ldg(reinterpret_cast<const float4*>(e.alpha + c));
+    const float4 a1 = __ldg(reinterpret_cast<const float4*>(e.alpha + c + 4));
+    v[0] *= a0.x; v[1] *= a0.y; v[2] *= a0.z; v[3] *= a0.w;
+    v[4] *= a1.x; v[5] *= a1.y; v[6] *= a1.z; v[7] *= a1.w;
+  }
+  if (e.beta) {
+    const float4 b0 = __ldg(reinterpret_cast<const float4*>(e.beta + c));
+    const float4 b1 = __ldg(reinterpret_cast<const float4*>(e.beta + c + 4));
+    v[0] += b0.x; v[1] += b0.y; v[2] += b0.z; v[3] += b0.w;
+    v[4] += b1.x; v[5] += b1.y; v[6] += b1.z; v[7] += b1.w;
+  }
+#pragma unroll
+  for (int i = 0; i < 8; ++i) v[i] = act_apply(e.act1, v[i]);
+  if (e.binop != DFX_BIN_NONE) {
+    const int64_t idx = e.binop == DFX_BIN_ADD
+                            ? view_pixel_index(e.other, pix, c)
+                            : int64_t(n) * e.other.pitch + e.other.coff + c;
+    float o[8];
+    unpack_bf16x8(*reinterpret_cast<const uint4*>(
+                      reinterpret_cast<const __nv_bfloat16*>(e.other.base) + idx), o);
+    if (e.binop == DFX_BIN_ADD) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) v[i] += o[i];
+    } else {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) v[i] *= o[i];
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < 8; ++i) v[i] = act_apply(e.act2, v[i]);
+}
+
+// True when 8-channel vector access at channel c is legal for view v.
+DFX_DEV bool vec8_ok(const dfx_view& v, int c) { return ((v.coff + c) & 7) == 0; }
+
+// ---------------------------------------------------------------- PTX wrappers
+DFX_DEV uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+DFX_DEV void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+DFX_DEV void fence_barrier_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+DFX_DEV void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+
+DFX_DEV void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// Blocks until the phase with the given parity completed.  A pipeline bug would
+// otherwise hang the GPU; after ~2^26 polls the kernel traps instead.
+DFX_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
+  const uint32_t addr = smem_u32(bar);
+  uint32_t done = 0;
+  for (uint32_t tries = 0;; ++tries) {
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n"
+        "selp.u32 %0, 1, 0, P1;\n"
+        "}\n"
+        : "=r"(done)
+        : "r"(addr), "r"(parity)
+        : "memory");
+    if (done) return;
+    if (tries > (1u << 26)) __trap();
+  }
+}
+
+DFX_DEV void tma_load_4d(void* dst, const void* tmap, uint64_t* bar, int c0, int c1, int c2,
+                         int c3) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(tmap), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+      : "memory");
+}
+
+DFX_DEV void tma_load_2d(void* dst, const void* tmap, uint64_t* bar, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(tmap), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+      : "memory");
+}
+
+DFX_DEV void tma_prefetch_desc(const void* tmap) {
+  asm volatile("prefetch.tensormap [%0];" ::"l"(tmap) : "memory");
+}
+
+// tcgen05 -------------------------------------------------------------------
+DFX_DEV void tmem_alloc(uint32_t* dst_smem, uint32_t ncols) {
+  asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                   smem_u32(dst_smem)),
+               "r"(ncols)
+               : "memory");
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+}
+
+DFX_DEV void tmem_dealloc(uint32_t taddr, uint32_t ncols) {
+  asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols)
+               : "memory");
+}
+
+DFX_DEV void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+DFX_DEV void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+// D[tmem] (+)= A[smem] * B[smem]^T, bf16 inputs, fp32 accumulate.
+DFX_DEV void umma_bf16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                       uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
+// Arrive on an mbarrier when all previously issued tcgen05.mma complete.
+DFX_DEV void umma_commit(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+          smem_u32(bar))
+      : "memory");
+}
+
+// 32 lanes x 32 bit, 16 consecutive columns per thread.
+DFX_DEV void tmem_ld16(uint32_t taddr, float* v) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+      "{%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),
+        "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+// UMMA shared-memory descriptor, K-major operand with 32/64/128-byte swizzle.
+// rows of `row_bytes` (= swizzle width), 8-row core groups stacked densely.
+DFX_DEV uint64_t umma_smem_desc(uint32_t saddr, uint32_t row_bytes) {
+  const uint64_t layout = row_bytes == 128 ? 2ull : (row_bytes == 64 ? 4ull : 6ull);
+  uint64_t d = 0;
+  d |= uint64_t((saddr >> 4) & 0x3FFF);            // start address
+  d |= uint64_t(1) << 16;                          // LBO (unused for swizzled K-major)
+  d |= uint64_t(((8 * row_bytes) >> 4) & 0x3FFF) << 32;  // SBO: 8-row group stride
+  d |= uint64_t(1) << 46;                          // version = 1 (sm_100)
+  d |= layout << 61;                               // swizzle mode
+  return d;
+}
+
+// Instruction descriptor: kind::f16, A=B=bf16, D=f32, both K-major, M=128.
+DFX_DEV uint32_t umma_idesc_bf16(uint32_t n) {
+  uint32_t d = 0;
+  d |= 1u << 4;               // D format f32
+  d |= 1u << 7;               // A bf16
+  d |= 1u << 10;              // B bf16
+  d |= (n >> 3) << 17;        // N
+  d |= (128u >> 4) << 24;     // M
+  return d;
+}
+
+constexpr int kGemmThreads = 128;
+constexpr int kSlots = 4;
+constexpr int kStageABytes = 128 * 64 * 2;   // 128 rows x 64 bf16
+constexpr int kHeaderBytes = 1024;
+
+__host__ __device__ inline int gemm_slot_bytes(int bn_max) { return kStageABytes + bn_max * 128; }
+__host__ __device__ inline int gemm_smem_bytes(int bn_max) {
+  return kHeaderBytes + kSlots * gemm_slot_bytes(bn_max);
+}
+__host__ __device__ inline uint32_t tmem_cols_for(int bn) {
+  uint32_t c = 32;
+  while (c < uint32_t(bn)) c <<= 1;
+  return c;
+}
+
+}  // namespace dfx

@@ -1,0 +1,453 @@
+"""Device residency of a fused DAG: weight arena, activation plans, CUDA graphs.
+
+Swap-in (the reference simulates it: /root/reference/pkg/src/dagfuse/costmodel.py:277-338)
+is real here: every member's packed weights are laid out in ONE pinned host
+arena and moved with ONE ``cudaMemcpyAsync`` into ONE device allocation
+(``dfx_arena_upload``).  ``swap_subgraph`` re-uploads only the incoming
+member's segment.  Replication to other GPUs is a single NCCL broadcast of
+the arena (``broadcast_arena``).
+
+Execution: an ``ExecInstance`` owns one activation arena (planned by
+``planner.first_fit`` over the lowered buffers' launch-index lifetimes), a
+split-K workspace, the GEMM descriptor table, I/O staging buffers and one
+instantiated CUDA graph containing every member's launches.  In the default
+``concurrent`` mode members are independent graph branches with disjoint
+arena segments (the reference's Σ, costmodel.py:264-266); ``sequential``
+chains members and overlays their segments (max).  Instances are pooled per
+batch signature so concurrent ``execute_fused`` callers never share one.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import threading
+import time
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import runtime as rt
+from .graph_ir import LiveInterval
+from .lower import COPY, DWCONV, EW, GAP, GEMM, POOL, MemberProgram, gemm_tiling, lower_member
+from .planner import first_fit
+
+ALIGN = 256
+_program_cache: dict[tuple[int, int], tuple] = {}
+_cache_lock = threading.Lock()
+
+
+def program_for(g, w) -> MemberProgram:
+    """Lowered program of (graph, weights), cached by object identity."""
+    key = (id(g), id(w))
+    with _cache_lock:
+        hit = _program_cache.get(key)
+        if hit is not None and hit[0] is g and hit[1] is w:
+            return hit[2]
+    prog = lower_member(g, w)
+    with _cache_lock:
+        _program_cache[key] = (g, w, prog)
+    return prog
+
+
+def _align(x, a=ALIGN):
+    return (x + a - 1) // a * a
+
+
+# ------------------------------------------------------------------------------ weights
+
+class WeightArena:
+    """Packed weights of all members: host pinned staging + device copy."""
+
+    def __init__(self, programs: list[MemberProgram], device: int = 0):
+        self.device = device
+        self.layout: list[dict[str, int]] = []
+        self.segments: list[tuple[int, int]] = []          # (offset, bytes) per member
+        at = 0
+        for p in programs:
+            seg0 = at
+            offs = {}
+            for key in sorted(p.blobs):
+                offs[key] = at
+                at = _align(at + p.blobs[key].nbytes)
+            self.layout.append(offs)
+            self.segments.append((seg0, at - seg0))
+        self.total = max(at, ALIGN)
+        rt.init_device(device)
+        self.host = rt.host_alloc(self.total)
+        view = (C.c_uint8 * self.total).from_address(self.host)
+        buf = np.frombuffer(view, dtype=np.uint8)
+        for p, offs in zip(programs, self.layout):
+            for key, off in offs.items():
+                raw = p.blobs[key].view(np.uint8).reshape(-1)
+                buf[off:off + raw.size] = raw
+        self.dev = 0
+        self.member_base: list[int] = []       # device base of each member's segment
+        self.extra_allocs: list[int] = []
+        self.upload_ms = None
+
+    def upload(self, stream=None) -> float:
+        """ONE device allocation + ONE H2D copy of the whole arena; returns ms."""
+        p = C.c_void_p()
+        t0 = time.perf_counter()
+        rt.call("dfx_arena_upload", C.c_void_p(self.host), C.c_size_t(self.total), C.byref(p),
+                C.c_void_p(stream))
+        rt.stream_sync(stream)
+        self.upload_ms = (time.perf_counter() - t0) * 1e3
+        self.dev = p.value
+        self.member_base = [self.dev + off for off, _ in self.segments]
+        return self.upload_ms
+
+    def addr(self, member: int, key: str) -> int:
+        return self.member_base[member] + (self.layout[member][key] - self.segments[member][0])
+
+    def replace_member(self, member: int, prog: MemberProgram, stream=None) -> float:
+        """swap_subgraph: pack + upload only the incoming member's segment."""
+        offs, at = {}, 0
+        for key in sorted(prog.blobs):
+            offs[key] = at
+            at = _align(at + prog.blobs[key].nbytes)
+        size = max(at, ALIGN)
+        host = rt.host_alloc(size)
+        buf = np.frombuffer((C.c_uint8 * size).from_address(host), dtype=np.uint8)
+        for key, off in offs.items():
+            raw = prog.blobs[key].view(np.uint8).reshape(-1)
+            buf[off:off + raw.size] = raw
+        t0 = time.perf_counter()
+        cap = self.segments[member][1]
+        if size <= cap:
+            base = self.member_base[member]
+        else:
+            base = rt.malloc(size)
+            self.extra_allocs.append(base)
+        rt.h2d(base, host, size, stream)
+        rt.stream_sync(stream)
+        ms = (time.perf_counter() - t0) * 1e3
+        rt.host_free(host)
+        self.member_base[member] = base
+        self.layout[member] = offs
+        self.segments[member] = (0, max(cap, size)) if size <= cap else (0, size)
+        return ms
+
+    def clone_for_swap(self) -> "WeightArena":
+        twin = object.__new__(WeightArena)
+        twin.__dict__.update(self.__dict__)
+        twin.layout = list(self.layout)
+        twin.segments = list(self.segments)
+        twin.member_base = list(self.member_base)
+        return twin
+
+    def free(self):
+        rt.free(self.dev)
+        for p in self.extra_allocs:
+            rt.free(p)
+        rt.host_free(self.host)
+        self.dev = self.host = 0
+
+
+def broadcast_arena(arena: WeightArena, src: int = 0, group=None) -> None:
+    """Replicate the device arena from rank ``src`` over NCCL (torch.distributed
+    plumbing; the arena is wrapped zero-copy through __cuda_array_interface__)."""
+    import torch
+    import torch.distributed as dist
+
+    class _Iface:
+        def __init__(self, ptr, n):
+            self.__cuda_array_interface__ = {"shape": (n,), "typestr": "|u1",
+                                             "data": (ptr, False), "version": 3}
+
+    t = torch.as_tensor(_Iface(arena.dev, arena.total), device=f"cuda:{arena.device}")
+    dist.broadcast(t, src=src, group=group)
+
+
+# ------------------------------------------------------------------------------ plans
+
+@dataclass
+class MemberPlan:
+    offsets: list[int]          # per buffer, relative to the member segment
+    arena_bytes: int
+    ws_bytes: int
+    tilings: dict[int, dict]    # launch index -> gemm tiling
+
+
+def plan_member(prog: MemberProgram, n: int, sm_count: int = 148) -> MemberPlan:
+    ivs = [LiveInterval(str(b.bid).zfill(6), b.bytes_for(n), b.first, b.last)
+           for b in prog.buffers]
+    places = first_fit(ivs, align=ALIGN)
+    offsets = [0] * len(prog.buffers)
+    for pl in places:
+        offsets[int(pl.name)] = pl.offset
+    arena = max((pl.offset + pl.size for pl in places), default=0)
+    ws = 0
+    tilings = {}
+    for L in prog.launches:
+        if L.kind != GEMM:
+            continue
+        out = prog.values[L.dst]
+        t = gemm_tiling(L.geom, n, out.h, out.w, sm_count)
+        tilings[L.index] = t
+        if t["splits"] > 1:
+            ws = max(ws, t["splits"] * n * out.h * out.w * t["nt"] * t["bn"] * 4)
+    return MemberPlan(offsets, _align(arena), _align(ws), tilings)
+
+
+# ------------------------------------------------------------------------------ instances
+
+class ExecInstance:
+    """One instantiated CUDA graph of the whole fused DAG for a batch signature."""
+
+    def __init__(self, dag: "DeviceDag", batch: tuple[int, ...]):
+        self.dag, self.batch = dag, batch
+        progs, arena = dag.programs, dag.arena
+        rt.init_device(dag.device)
+        self.stream = rt.stream_create()
+        self.plans = [plan_member(p, n, dag.sm_count) if n > 0 else MemberPlan([], 0, 0, {})
+                      for p, n in zip(progs, batch)]
+        seq = dag.mode == "sequential"
+        # activation arena: disjoint member segments (concurrent) or overlaid (sequential)
+        self.seg_off, at = [], 0
+        for pl in self.plans:
+            self.seg_off.append(0 if seq else at)
+            at = max(at, pl.arena_bytes) if seq else at + pl.arena_bytes
+        self.act_bytes = _align(max(at, ALIGN))
+        ws_each = [pl.ws_bytes for pl in self.plans]
+        self.ws_off, wat = [], 0
+        for wb in ws_each:
+            self.ws_off.append(0 if seq else wat)
+            wat = max(wat, wb) if seq else wat + wb
+        self.ws_bytes = _align(max(wat, ALIGN))
+        self.in_sizes = [n * int(np.prod(p.input_dims)) * 4 for p, n in zip(progs, batch)]
+        self.out_sizes = [n * int(np.prod(p.output_dims)) * 4 for p, n in zip(progs, batch)]
+        self.in_off = np.cumsum([0] + self.in_sizes).tolist()
+        self.out_off = np.cumsum([0] + self.out_sizes).tolist()
+        self.in_bytes, self.out_bytes = self.in_off[-1], self.out_off[-1]
+        n_gemm = sum(1 for p, n in zip(progs, batch) for L in p.launches if L.kind == GEMM and n)
+        self.act = rt.malloc(self.act_bytes)
+        self.ws = rt.malloc(self.ws_bytes)
+        self.descs = rt.malloc(max(n_gemm, 1) * C.sizeof(rt.GemmDesc))
+        self.dev_in = rt.malloc(max(self.in_bytes, 16))
+        self.dev_out = rt.malloc(max(self.out_bytes, 16))
+        self.host_in = rt.host_alloc(max(self.in_bytes, 16))
+        self.host_out = rt.host_alloc(max(self.out_bytes, 16))
+        rt.memset(self.act, 0, self.act_bytes, self.stream)
+        self.gemm_count = 0
+        self.kernel_nodes = 0
+        self.graph = self._build(progs, arena)
+        rt.stream_sync(self.stream)
+
+    # --- views
+    def _view(self, m: int, prog: MemberProgram, name: str, n: int) -> rt.View:
+        v = prog.values[name]
+        b = prog.buffers[v.buf]
+        base = self.act + self.seg_off[m] + self.plans[m].offsets[v.buf]
+        return rt.View(base, n, v.h, v.w, v.c, b.pitch, v.coff)
+
+    def _epi(self, m, prog, L, n) -> rt.Epilogue:
+        e = rt.Epilogue()
+        arena = self.dag.arena
+        e.alpha = arena.addr(m, L.blobs["alpha"]) if "alpha" in L.blobs else None
+        e.beta = arena.addr(m, L.blobs["beta"]) if "beta" in L.blobs else None
+        e.act1 = rt.ACT[L.epi.act1]
+        e.act2 = rt.ACT[L.epi.act2]
+        e.binop = L.epi.binop
+        if L.epi.binop:
+            e.other = self._view(m, prog, L.epi.other, n)
+        return e
+
+    def _build(self, progs, arena) -> rt.Graph:
+        g = rt.Graph()
+        host_descs = []
+        pending = []                                   # (member, launch, desc slot)
+        prev_tail = None
+        self._keep = []                                # keep param structs alive
+        for m, (prog, n) in enumerate(zip(progs, self.batch)):
+            if n == 0:
+                continue
+            deps = [prev_tail] if (self.dag.mode == "sequential" and prev_tail is not None) else []
+            pin = rt.InParams(self.dev_in + self.in_off[m], self._view(m, prog, "<input>", n))
+            last = g.add(rt.OP_IN, pin, deps)
+            self._keep.append(pin)
+            for L in prog.launches:
+                for op, params in self._params(m, prog, L, n, host_descs):
+                    last = g.add(op, params, [last])
+                    self._keep.append(params)
+            pout = rt.OutParams(self._view(m, prog, prog.exit_value, n), self.dev_out + self.out_off[m])
+            last = g.add(rt.OP_OUT, pout, [last])
+            self._keep.append(pout)
+            prev_tail = last
+        if host_descs:
+            arr = (rt.GemmDesc * len(host_descs))(*host_descs)
+            rt.h2d(self.descs, C.addressof(arr), C.sizeof(arr), self.stream)
+            rt.stream_sync(self.stream)
+        g.instantiate()
+        self.kernel_nodes = len(g.kinds)
+        return g
+
+    def _params(self, m, prog: MemberProgram, L, n, host_descs):
+        arena = self.dag.arena
+        src = self._view(m, prog, L.src, n)
+        if L.kind == GEMM:
+            geo, t = L.geom, self.plans[m].tilings[L.index]
+            out = self._view(m, prog, L.dst, n)
+            d = rt.GemmDesc()
+            d.tmap_a = rt.tmap_act(src, geo["cb"], t["tq"], t["tp"], t["tn"], geo["sw"], geo["sh"])
+            d.tmap_b = rt.tmap_weights(arena.addr(m, L.blobs["weight"]), geo["cout"], geo["k"],
+                                       geo["cb"], t["bn"])
+            d.n, d.p, d.q = n, out.h, out.w
+            d.tn, d.tp, d.tq = t["tn"], t["tp"], t["tq"]
+            d.mt_n, d.mt_p, d.mt_q, d.nt = t["mt_n"], t["mt_p"], t["mt_q"], t["nt"]
+            d.r, d.s = geo["kh"], geo["kw"]
+            d.stride_h, d.stride_w, d.pad_h, d.pad_w = geo["sh"], geo["sw"], geo["ph"], geo["pw"]
+            d.cb, d.cblocks, d.ksteps, d.kpack = geo["cb"], geo["cblocks"], geo["ksteps"], t["kpack"]
+            d.stages, d.splits, d.stages_per_split = t["stages"], t["splits"], t["sps"]
+            d.bn, d.cout, d.tile_begin, d.tiles = t["bn"], geo["cout"], 0, t["tiles"]
+            d.out = out
+            epi = self._epi(m, prog, L, n)
+            d.epi = epi
+            d.ws = (self.ws + self.ws_off[m]) if t["splits"] > 1 else None
+            slot = len(host_descs)
+            host_descs.append(d)
+            self.gemm_count += 1
+            gl = rt.GemmLaunch(self.descs + slot * C.sizeof(rt.GemmDesc), 1, t["tiles"], t["bn"])
+            yield rt.OP_GEMM, gl
+            if t["splits"] > 1:
+                sp = rt.SplitKParams(self.ws + self.ws_off[m], t["splits"], n * out.h * out.w,
+                                     geo["cout"], t["nt"] * t["bn"], out, epi)
+                yield rt.OP_SPLITK, sp
+        elif L.kind == DWCONV:
+            geo = L.geom
+            p = rt.DwconvParams(src, self._view(m, prog, L.dst, n), arena.addr(m, L.blobs["weight"]),
+                                geo["kh"], geo["kw"], geo["sh"], geo["sw"], geo["ph"], geo["pw"],
+                                self._epi(m, prog, L, n))
+            yield rt.OP_DWCONV, p
+        elif L.kind == POOL:
+            geo = L.geom
+            yield rt.OP_POOL, rt.PoolParams(src, self._view(m, prog, L.dst, n), geo["kh"], geo["kw"],
+                                            geo["sh"], geo["sw"], geo["ph"], geo["pw"],
+                                            geo["is_max"], geo["cip"])
+        elif L.kind == GAP:
+            yield rt.OP_GAP, rt.GapParams(src, self._view(m, prog, L.dst, n))
+        elif L.kind == EW:
+            yield rt.OP_EW, rt.EwParams(src, self._view(m, prog, L.dst, n), self._epi(m, prog, L, n))
+        elif L.kind == COPY:
+            cv = self._view(m, prog, L.geom["concat"], n)
+            out = rt.View(cv.base, n, src.h, src.w, src.c, cv.pitch, L.geom["coff"])
+            yield rt.OP_EW, rt.EwParams(src, out, rt.Epilogue())
+        else:
+            raise AssertionError(L.kind)
+
+    # --- execution
+    def stage_inputs(self, xs: list[np.ndarray]) -> None:
+        hb = np.frombuffer((C.c_uint8 * max(self.in_bytes, 16)).from_address(self.host_in),
+                           dtype=np.uint8)
+        for m, x in enumerate(xs):
+            raw = np.ascontiguousarray(x, dtype=np.float32).view(np.uint8).reshape(-1)
+            hb[self.in_off[m]:self.in_off[m] + raw.size] = raw
+
+    def read_outputs(self) -> list[np.ndarray]:
+        hb = np.frombuffer((C.c_uint8 * max(self.out_bytes, 16)).from_address(self.host_out),
+                           dtype=np.uint8)
+        outs = []
+        for m, p in enumerate(self.dag.programs):
+            raw = hb[self.out_off[m]:self.out_off[m + 1]].copy().view(np.float32)
+            outs.append(raw.reshape((self.batch[m],) + tuple(p.output_dims)))
+        return outs
+
+    def run(self, xs: list[np.ndarray]) -> list[np.ndarray]:
+        """End to end: stage -> H2D -> graph -> D2H -> sync (dfx_execute)."""
+        self.stage_inputs(xs)
+        self.graph.execute(self.host_in, self.dev_in, self.in_bytes, self.host_out, self.dev_out,
+                           self.out_bytes, self.stream)
+        return self.read_outputs()
+
+    def upload_inputs(self, xs):
+        self.stage_inputs(xs)
+        rt.h2d(self.dev_in, self.host_in, self.in_bytes, self.stream)
+        rt.stream_sync(self.stream)
+
+    def launch_graph(self):
+        self.graph.launch(self.stream)
+
+    def sync(self):
+        rt.stream_sync(self.stream)
+
+    def download_outputs(self) -> list[np.ndarray]:
+        rt.d2h(self.host_out, self.dev_out, self.out_bytes, self.stream)
+        rt.stream_sync(self.stream)
+        return self.read_outputs()
+
+    def free(self):
+        self.graph.destroy()
+        for p in (self.act, self.ws, self.descs, self.dev_in, self.dev_out):
+            rt.free(p)
+        rt.host_free(self.host_in)
+        rt.host_free(self.host_out)
+        rt.stream_destroy(self.stream)
+
+
+class DeviceDag:
+    """A fused DAG resident on one GPU."""
+
+    def __init__(self, members, device: int = 0, mode: str = "concurrent", arena=None,
+                 programs=None):
+        if mode not in ("concurrent", "sequential"):
+            raise ValueError(mode)
+        self.device, self.mode = device, mode
+        rt.init_device(device)
+        sm = C.c_int()
+        rt.call("dfx_device_info", C.c_int(device), C.byref(sm), None, None, None)
+        self.sm_count = sm.value
+        self.members = list(members)
+        self.programs = programs or [program_for(g, w) for g, w in self.members]
+        if arena is None:
+            arena = WeightArena(self.programs, device)
+            arena.upload()
+        self.arena = arena
+        self._pool: dict[tuple, list[ExecInstance]] = {}
+        self._all: list[ExecInstance] = []
+        self._lock = threading.Lock()
+
+    @property
+    def swap_in_ms(self) -> float:
+        return self.arena.upload_ms
+
+    def acquire(self, batch: tuple[int, ...]) -> ExecInstance:
+        with self._lock:
+            free = self._pool.setdefault(batch, [])
+            if free:
+                return free.pop()
+        inst = ExecInstance(self, batch)
+        with self._lock:
+            self._all.append(inst)
+        return inst
+
+    def release(self, inst: ExecInstance) -> None:
+        with self._lock:
+            self._pool.setdefault(inst.batch, []).append(inst)
+
+    def execute(self, xs: list[np.ndarray]) -> list[np.ndarray]:
+        batch = tuple(int(x.shape[0]) for x in xs)
+        inst = self.acquire(batch)
+        try:
+            return inst.run(xs)
+        finally:
+            self.release(inst)
+
+    def swapped(self, index: int, incoming) -> "DeviceDag":
+        g, w = incoming
+        prog = program_for(g, w)
+        arena = self.arena.clone_for_swap()
+        ms = arena.replace_member(index, prog)
+        members = list(self.members)
+        members[index] = incoming
+        programs = list(self.programs)
+        programs[index] = prog
+        out = DeviceDag(members, self.device, self.mode, arena=arena, programs=programs)
+        out.last_swap_ms = ms
+        return out
+
+    def free_instances(self):
+        with self._lock:
+            for inst in self._all:
+                inst.free()
+            self._all.clear()
+            self._pool.clear()

@@ -1,0 +1,557 @@
+"""Lowering: one member graph -> a sequence of libdfx kernel launches.
+
+Input: a validated ``ModelGraph`` + ``WeightStore`` (reference IR superset).
+Output: a batch-independent ``MemberProgram``:
+
+* **chains** — every launch is an *anchor* node plus the single-consumer
+  nodes folded into its epilogue, in this slot order (dfx.h dfx_epilogue):
+  ``affine`` (bias, batch-norm) -> ``act1`` -> ``binop`` (residual_add /
+  channel_scale with an operand materialised earlier) -> ``act2``.
+  Anchors: conv2d/dense -> tcgen05 implicit GEMM; depthwise conv2d ->
+  dwconv; pools -> pool; global_avg_pool -> gap; batchnorm / activations /
+  residual_add / channel_scale -> elementwise.  flatten is a view; concat is
+  zero-copy (producers write at a channel offset of one buffer) with a copy
+  launch only for parts that cannot be placed (misaligned offset, the graph
+  input, a value already placed elsewhere).
+* **buffers** — physical bf16 NHWC tensors (one per materialised value or
+  concat group) with launch-index lifetimes for the activation planner.
+* **blobs** — packed weights (bf16 GEMM matrices in (r, s, channel-block)
+  K order, fp32 epilogue vectors, fp32 depthwise taps) for the weight arena.
+
+Semantics are the reference's per-kind definitions
+(/root/reference/pkg/src/dagfuse/executor.py:56-167, extension kinds as in
+graph_ir.py).  Folding batch-norm into (alpha, beta) and the bf16 storage of
+activations are the only numerical departures; parity is checked against the
+oracle within the north-star tolerance.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from .errors import UnsupportedOnDevice
+from .graph_ir import (ACTIVATION_KINDS, conv_geometry, infer_shapes, pool_geometry,
+                       topo_order)
+
+GEMM, DWCONV, POOL, GAP, EW, COPY = "gemm", "dwconv", "pool", "gap", "ew", "copy"
+
+
+def round_up(x: int, a: int) -> int:
+    return (x + a - 1) // a * a
+
+
+def to_bf16_bits(a: np.ndarray) -> np.ndarray:
+    """fp32 -> bf16 bit patterns, round-to-nearest-even (finite inputs)."""
+    u = np.ascontiguousarray(a, dtype=np.float32).view(np.uint32).astype(np.uint64)
+    u = (u + 0x7FFF + ((u >> 16) & 1)) >> 16
+    return u.astype(np.uint16)
+
+
+def bf16_bits_to_f32(b: np.ndarray) -> np.ndarray:
+    return (b.astype(np.uint32) << 16).view(np.float32)
+
+
+@dataclass
+class Buffer:
+    bid: int
+    h: int
+    w: int
+    c: int                  # channels of the whole buffer
+    pitch: int              # round_up(c, 8)
+    name: str
+    first: int = 10 ** 9    # launch index of first write
+    last: int = -1          # launch index of last read
+    is_input: bool = False
+
+    def bytes_for(self, n: int) -> int:
+        return n * self.h * self.w * self.pitch * 2
+
+
+@dataclass
+class Value:
+    """Physical placement of one IR value."""
+    buf: int
+    coff: int
+    h: int
+    w: int
+    c: int
+    flat: bool = False      # logical rank-1 over physical (h, w, c) in CHW order
+
+
+@dataclass
+class Epi:
+    alpha: np.ndarray | None = None
+    beta: np.ndarray | None = None
+    act1: str | None = None
+    binop: int = 0          # 0 none, 1 add, 2 scale
+    other: str | None = None   # IR node id of the binop operand
+    act2: str | None = None
+
+    def affine_open(self) -> bool:
+        return self.act1 is None and self.binop == 0 and self.act2 is None
+
+
+@dataclass
+class Launch:
+    kind: str
+    nodes: list[str]                    # IR nodes covered (anchor first)
+    src: str                            # IR value read as the main operand
+    dst: str                            # IR value written
+    epi: Epi = field(default_factory=Epi)
+    geom: dict = field(default_factory=dict)
+    blobs: dict = field(default_factory=dict)     # role -> blob key
+    index: int = -1
+
+
+@dataclass
+class MemberProgram:
+    model_id: str
+    input_dims: tuple
+    output_dims: tuple
+    launches: list[Launch]
+    values: dict[str, Value]
+    buffers: list[Buffer]
+    blobs: dict[str, np.ndarray]        # key -> uint16 (bf16) or float32 array
+    exit_value: str
+    input_value: str = "<input>"
+    gemm_flops_per_sample: int = 0
+
+    def weight_bytes(self) -> int:
+        return sum(b.nbytes for b in self.blobs.values())
+
+
+# ------------------------------------------------------------------------------------------
+
+def _act_or_none(kind):
+    return kind if kind in ACTIVATION_KINDS else None
+
+
+class _Lowerer:
+    def __init__(self, g, w):
+        self.g, self.w = g, w
+        self.shapes = infer_shapes(g)
+        self.order = topo_order(g)
+        self.pos = {nid: i for i, nid in enumerate(self.order)}
+        self.users: dict[str, list[str]] = {nid: [] for nid in g.nodes}
+        for nid in self.order:
+            for s in g.nodes[nid].inputs:
+                if nid not in self.users[s]:
+                    self.users[s].append(nid)
+        self.absorbed: dict[str, str] = {}      # node -> anchor
+        self.launches: list[Launch] = []
+        self.values: dict[str, Value] = {}
+        self.buffers: list[Buffer] = []
+        self.blobs: dict[str, np.ndarray] = {}
+        self.acc_owner: dict[str, str] = {}
+        self.pending_weights: list = []
+        self.keep_f32 = False
+        self.debug_f32: dict[str, np.ndarray] = {}
+
+    # -------------------------------------------------------------- helpers
+    def dims(self, nid):
+        return self.shapes[nid].dims
+
+    def in_dims(self, nid):
+        if nid == self.g.entry:
+            return self.g.input_spec.dims
+        return self.dims(self.g.nodes[nid].inputs[0])
+
+    def src_of(self, nid, k=0):
+        return "<input>" if nid == self.g.entry else self.g.nodes[nid].inputs[k]
+
+    def warr(self, node, role):
+        return np.asarray(self.w.array(node.weight_refs[role]), dtype=np.float32)
+
+    def single_user(self, nid):
+        u = self.users[nid]
+        return u[0] if len(u) == 1 and nid != self.g.exit else None
+
+    def bn_affine(self, node):
+        eps = np.float32(node.attrs.get("epsilon", 1e-5))
+        var = self.warr(node, "var")
+        inv = (np.float32(1.0) / np.sqrt(var + eps)).astype(np.float32)
+        s = self.warr(node, "gamma").astype(np.float64) * inv
+        t = self.warr(node, "beta").astype(np.float64) - self.warr(node, "mean") * s
+        return s, t
+
+    # -------------------------------------------------------------- chains
+    def absorb(self, anchor_id: str, tail: str, epi: Epi, allow_affine: bool, allow_bin: bool):
+        """Greedily fold single-consumer successors into the epilogue."""
+        nodes = [anchor_id] if anchor_id != tail else [tail]
+        while True:
+            nxt = self.single_user(tail)
+            if nxt is None:
+                break
+            node = self.g.nodes[nxt]
+            k = node.kind
+            if k == "batchnorm_inference" and allow_affine and epi.affine_open():
+                s, t = self.bn_affine(node)
+                a = np.ones_like(s) if epi.alpha is None else epi.alpha.astype(np.float64)
+                b = np.zeros_like(s) if epi.beta is None else epi.beta.astype(np.float64)
+                epi.alpha = (a * s).astype(np.float32)
+                epi.beta = (b * s + t).astype(np.float32)
+            elif _act_or_none(k) and epi.binop == 0 and epi.act1 is None:
+                epi.act1 = k
+            elif _act_or_none(k) and epi.binop != 0 and epi.act2 is None:
+                epi.act2 = k
+            elif k == "residual_add" and allow_bin and epi.binop == 0 and epi.act2 is None \
+                    and len(node.inputs) == 2:
+                other = node.inputs[1] if node.inputs[0] == tail else node.inputs[0]
+                if other == tail or self.pos[other] >= self.pos[anchor_id] \
+                        or other in self.absorbed:
+                    break
+                epi.binop, epi.other = 1, other
+            elif k == "channel_scale" and allow_bin and epi.binop == 0 and epi.act2 is None \
+                    and node.inputs[0] == tail:
+                other = node.inputs[1]
+                if self.pos[other] >= self.pos[anchor_id] or other in self.absorbed:
+                    break
+                epi.binop, epi.other = 2, other
+            else:
+                break
+            self.absorbed[nxt] = anchor_id
+            nodes.append(nxt)
+            tail = nxt
+        return nodes, tail
+
+    def lower_node(self, nid):
+        node = self.g.nodes[nid]
+        k = node.kind
+        if k in ("conv2d", "dense"):
+            return self.lower_gemm_or_dw(nid)
+        if k in ("maxpool2d", "avgpool2d"):
+            kh, kw, sh, sw, ph, pw = pool_geometry(node.attrs)
+            L = Launch(POOL, [nid], self.src_of(nid), nid,
+                       geom=dict(kh=kh, kw=kw, sh=sh, sw=sw, ph=ph, pw=pw,
+                                 is_max=int(k == "maxpool2d"),
+                                 cip=int(node.attrs.get("count_include_pad", 1))))
+            self.launches.append(L)
+            return
+        if k == "global_avg_pool":
+            self.launches.append(Launch(GAP, [nid], self.src_of(nid), nid))
+            return
+        if k in ("flatten", "concat"):
+            return          # views; handled in placement
+        # elementwise anchors
+        epi = Epi()
+        src = self.src_of(nid)
+        if k == "batchnorm_inference":
+            s, t = self.bn_affine(node)
+            epi.alpha, epi.beta = s.astype(np.float32), t.astype(np.float32)
+        elif k in ACTIVATION_KINDS:
+            epi.act1 = k
+        elif k == "residual_add":
+            ins = node.inputs
+            if len(ins) > 2:
+                self.lower_multi_add(nid)
+                return
+            src, epi.binop, epi.other = ins[0], 1, ins[1]
+        elif k == "channel_scale":
+            src, epi.binop, epi.other = node.inputs[0], 2, node.inputs[1]
+        nodes, tail = self.absorb(nid, nid, epi, allow_affine=k in ("batchnorm_inference",)
+                                  or k in ACTIVATION_KINDS, allow_bin=True)
+        self.launches.append(Launch(EW, nodes, src, tail, epi=epi))
+
+    def lower_multi_add(self, nid):
+        """residual_add with k > 2 inputs: left fold (executor.py:153-155) as k-1 adds."""
+        ins = self.g.nodes[nid].inputs
+        tmp = f"{nid}#acc"
+        self.acc_owner[tmp] = nid
+        acc = ins[0]
+        for i, other in enumerate(ins[1:]):
+            dst = nid if i == len(ins) - 2 else tmp
+            self.launches.append(Launch(EW, [nid], acc, dst, epi=Epi(binop=1, other=other)))
+            acc = dst
+
+    def lower_gemm_or_dw(self, nid):
+        node = self.g.nodes[nid]
+        idims = self.in_dims(nid)
+        a = node.attrs
+        epi = Epi()
+        bias = self.warr(node, "bias") if "bias" in node.weight_refs else None
+        if node.kind == "dense":
+            units, fan_in = int(a["units"]), int(a["fan_in"])
+            wt = self.warr(node, "weight")
+            src = self.src_of(nid)
+            geom = dict(cout=units, cin=fan_in, kh=1, kw=1, sh=1, sw=1, ph=0, pw=0,
+                        dense=True)
+            wt4 = wt.reshape(units, fan_in, 1, 1)
+            kind = GEMM
+        else:
+            kh, kw, sh, sw, ph, pw = conv_geometry(a)
+            cout, groups = int(a["out_channels"]), int(a.get("groups", 1))
+            cin = idims[0]
+            wt4 = self.warr(node, "weight")
+            src = self.src_of(nid)
+            geom = dict(cout=cout, cin=cin, kh=kh, kw=kw, sh=sh, sw=sw, ph=ph, pw=pw,
+                        dense=False)
+            if groups == 1:
+                kind = GEMM
+            elif groups == cin == cout:
+                kind = DWCONV
+            else:
+                raise UnsupportedOnDevice(nid, f"grouped conv with groups={groups} "
+                                               f"(only 1 or depthwise)")
+        epi.beta = None if bias is None else bias.astype(np.float32)
+        nodes, tail = self.absorb(nid, nid, epi, allow_affine=True, allow_bin=(kind == GEMM))
+        L = Launch(kind, nodes, src, tail, epi=epi, geom=geom)
+        key = f"{nid}.w"
+        L.blobs["weight"] = key
+        self.pending_weights.append((L, wt4))
+        self.launches.append(L)
+
+    # -------------------------------------------------------------- placement
+    def new_buffer(self, h, w, c, name):
+        b = Buffer(len(self.buffers), h, w, c, round_up(c, 8), name)
+        self.buffers.append(b)
+        return b.bid
+
+    def _is_flat_source(self, s):
+        node = self.g.nodes[s]
+        if node.kind != "flatten":
+            return False
+        d = self.in_dims(s)
+        return len(d) == 3 and d[1] * d[2] > 1
+
+    def resolve(self, name):
+        """Placement of a value, creating flatten views on demand."""
+        if name in self.values:
+            return self.values[name]
+        node = self.g.nodes.get(name)
+        if node is not None and node.kind == "flatten":
+            src = self.resolve(self.src_of(name))
+            v = Value(src.buf, src.coff, src.h, src.w, src.c, flat=src.flat or src.h * src.w > 1)
+            self.values[name] = v
+            return v
+        raise UnsupportedOnDevice(name, "value has no placement")
+
+    def place(self):
+        g = self.g
+        ind = g.input_spec.dims
+        h, w = (ind[1], ind[2]) if len(ind) == 3 else (1, 1)
+        ib = self.new_buffer(h, w, ind[0], "<input>")
+        self.buffers[ib].is_input = True
+        self.values["<input>"] = Value(ib, 0, h, w, ind[0])
+
+        produced = {L.dst for L in self.launches}
+        # concat groups, outermost first (reverse topo order): parts written in place
+        self.copies = []
+        for cid in reversed([n for n in self.order if g.nodes[n].kind == "concat"]):
+            d = self.dims(cid)
+            if any(self._is_flat_source(s) for s in g.nodes[cid].inputs):
+                raise UnsupportedOnDevice(cid, "concat of flattened spatial tensors")
+            h, w = (d[1], d[2]) if len(d) == 3 else (1, 1)
+            if cid not in self.values:
+                self.values[cid] = Value(self.new_buffer(h, w, d[0], cid), 0, h, w, d[0])
+            base = self.values[cid]
+            off = 0
+            for s in g.nodes[cid].inputs:
+                cs = self.dims(s)[0]
+                at = base.coff + off
+                if at % 8 == 0 and s not in self.values and \
+                        (s in produced or g.nodes[s].kind == "concat"):
+                    self.values[s] = Value(base.buf, at, h, w, cs)
+                else:
+                    self.copies.append((s, cid, at))
+                off += cs
+
+        # launch outputs, in launch order (sources resolve lazily through flatten views)
+        for L in self.launches:
+            if L.dst in self.values:
+                continue
+            src = self.resolve(L.src)
+            if L.dst.endswith("#acc"):
+                d = self.dims(self.acc_owner[L.dst])
+            else:
+                d = self.dims(L.dst)
+            if L.kind == EW and src.flat:
+                self.values[L.dst] = Value(self.new_buffer(src.h, src.w, src.c, L.dst), 0,
+                                           src.h, src.w, src.c, flat=True)
+            elif len(d) == 3:
+                self.values[L.dst] = Value(self.new_buffer(d[1], d[2], d[0], L.dst), 0,
+                                           d[1], d[2], d[0])
+            else:
+                self.values[L.dst] = Value(self.new_buffer(1, 1, d[0], L.dst), 0, 1, 1, d[0])
+        for nid in self.order:              # remaining views (e.g. a flatten exit)
+            if nid not in self.values and g.nodes[nid].kind == "flatten":
+                self.resolve(nid)
+
+    # -------------------------------------------------------------- build
+    def run(self) -> MemberProgram:
+        for nid in self.order:
+            if nid in self.absorbed:
+                continue
+            self.lower_node(nid)
+        self.place()
+        for s, cid, off in self.copies:
+            self.launches.append(Launch(COPY, [cid], s, f"{cid}@{off}",
+                                        geom=dict(coff=off, concat=cid)))
+        self.launches.sort(key=lambda L: self.pos[L.geom["concat"]] if L.kind == COPY
+                           else self.pos[L.nodes[0]])          # stable: keeps emission order
+        for i, L in enumerate(self.launches):
+            L.index = i + 1            # 0 is the input conversion
+        self.check_and_finish()
+        self.pack_weights()
+        return MemberProgram(self.g.model_id, tuple(self.g.input_spec.dims),
+                             tuple(self.g.output_spec.dims), self.launches, self.values,
+                             self.buffers, self.blobs, self.g.exit)
+
+    def value_of(self, name):
+        return self.resolve(name)
+
+    def check_and_finish(self):
+        n_launch = len(self.launches) + 2      # + input conversion (0) + output (last)
+        inb = self.values["<input>"].buf
+        self.buffers[inb].first = 0
+
+        def touch_write(v, i):
+            b = self.buffers[v.buf]
+            b.first = min(b.first, i)
+            b.last = max(b.last, i)
+
+        def touch_read(v, i):
+            b = self.buffers[v.buf]
+            b.last = max(b.last, i)
+
+        for L in self.launches:
+            i = L.index
+            touch_read(self.value_of(L.src), i)
+            if L.epi.other is not None:
+                touch_read(self.value_of(L.epi.other), i)
+            if L.kind == COPY:
+                touch_write(self.value_of(L.geom["concat"]), i)
+            else:
+                touch_write(self.value_of(L.dst), i)
+            # semantic checks for flattened operands
+            sv = self.value_of(L.src)
+            if sv.flat and L.kind == EW and L.epi.alpha is not None:
+                raise UnsupportedOnDevice(L.nodes[0], "per-channel affine on a flattened tensor")
+            if sv.flat and L.kind in (POOL, GAP, DWCONV):
+                raise UnsupportedOnDevice(L.nodes[0], "spatial op on a flattened tensor")
+            if L.kind == GEMM and not L.geom["dense"] and sv.flat:
+                raise UnsupportedOnDevice(L.nodes[0], "conv on a flattened tensor")
+        exitv = self.value_of(self.g.exit)
+        self.buffers[exitv.buf].last = n_launch
+        for b in self.buffers:
+            if b.first > b.last:        # written but never read (dead-end) -> live at write
+                b.last = b.first
+
+    # -------------------------------------------------------------- weights
+    def pack_weights(self):
+        for L, wt4 in self.pending_weights:
+            geo = L.geom
+            if L.kind == DWCONV:
+                c = geo["cout"]
+                taps = np.ascontiguousarray(wt4[:, 0].transpose(1, 2, 0).reshape(-1, c),
+                                            dtype=np.float32)       # [kh*kw][c]
+                self.blobs[L.blobs["weight"]] = taps
+            else:
+                sv = self.resolve(L.src)
+                if geo["dense"] and sv.flat:
+                    # dense over a flattened (C,H,W): a conv whose kernel is the whole image
+                    cin, h, w = sv.c, sv.h, sv.w
+                    wt4 = wt4.reshape(geo["cout"], cin, h, w)
+                    geo.update(cin=cin, kh=h, kw=w)
+                cin = geo["cin"]
+                cb = choose_cb(cin)
+                cblocks = -(-cin // cb)
+                cout = geo["cout"]
+                t = np.zeros((cout, geo["kh"], geo["kw"], cblocks * cb), dtype=np.float32)
+                t[..., :cin] = wt4.transpose(0, 2, 3, 1)
+                packed = to_bf16_bits(t.reshape(cout, -1))
+                geo.update(cb=cb, cblocks=cblocks, ksteps=geo["kh"] * geo["kw"] * cblocks,
+                           k=packed.shape[1])
+                self.blobs[L.blobs["weight"]] = packed
+                if self.keep_f32:
+                    self.debug_f32[L.blobs["weight"]] = t.reshape(cout, -1)
+            for role in ("alpha", "beta"):
+                v = getattr(L.epi, role)
+                if v is not None:
+                    key = f"{L.nodes[0]}.{role}"
+                    arr = np.zeros(round_up(len(v), 8), dtype=np.float32)
+                    arr[:len(v)] = v
+                    self.blobs[key] = arr
+                    L.blobs[role] = key
+        for L in self.launches:
+            if L.kind == EW:
+                for role in ("alpha", "beta"):
+                    v = getattr(L.epi, role)
+                    if v is not None:
+                        key = f"{L.nodes[0]}.{role}"
+                        arr = np.zeros(round_up(len(v), 8), dtype=np.float32)
+                        arr[:len(v)] = v
+                        self.blobs[key] = arr
+                        L.blobs[role] = key
+
+
+def choose_cb(cin: int) -> int:
+    """Channel block for the K loop: the widest of 64/32/16 wasting <= 12.5%."""
+    for cb in (64, 32):
+        if -(-cin // cb) * cb <= cin * 1.125:
+            return cb
+    return 16
+
+
+def lower_member(g, w, keep_f32: bool = False) -> MemberProgram:
+    """``keep_f32`` also keeps the unrounded packed GEMM weights (tests only)."""
+    low = _Lowerer(g, w)
+    low.keep_f32 = keep_f32
+    prog = low.run()
+    prog.debug_f32 = low.debug_f32
+    from .graph_ir import gemm_flops
+    prog.gemm_flops_per_sample = gemm_flops(g)
+    return prog
+
+
+# ------------------------------------------------------------------------------------------
+# per-batch GEMM tiling
+
+def choose_m_tile(n: int, p: int, q: int, sh: int, sw: int):
+    """(tn, tp, tq) covering <= 128 output pixels with the best row utilisation."""
+    best = None
+    if p * q <= 128:
+        tq, tp = q, p
+        tn = max(1, min(n, 128 // (p * q), 256))
+        cands = [(tn, tp, tq)]
+    else:
+        cands = []
+        for tq in range(1, min(q, 128) + 1):
+            if tq * sw > 256:
+                break
+            tp = min(p, 128 // tq)
+            if tp < 1 or tp * sh > 256:
+                continue
+            cands.append((1, tp, tq))
+    for tn, tp, tq in cands:
+        tiles = math.ceil(n / tn) * math.ceil(p / tp) * math.ceil(q / tq)
+        util = (n * p * q) / (tiles * 128)
+        score = (round(util, 4), tq)
+        if best is None or score > best[0]:
+            best = (score, (tn, tp, tq))
+    return best[1]
+
+
+def choose_bn(cout: int) -> tuple[int, int]:
+    nt = -(-cout // 256)
+    bn = round_up(-(-cout // nt), 16)
+    return bn, -(-cout // bn)
+
+
+def gemm_tiling(geom: dict, n: int, p: int, q: int, sm_count: int = 148) -> dict:
+    tn, tp, tq = choose_m_tile(n, p, q, geom["sh"], geom["sw"])
+    mt = (math.ceil(n / tn), math.ceil(p / tp), math.ceil(q / tq))
+    bn, nt = choose_bn(geom["cout"])
+    kpack = 64 // geom["cb"]
+    stages = math.ceil(geom["ksteps"] / kpack)
+    base = mt[0] * mt[1] * mt[2] * nt
+    splits = 1
+    if base < sm_count and stages >= 4:
+        splits = min(math.ceil(sm_count / base), stages // 2)
+    sps = math.ceil(stages / max(splits, 1))
+    splits = math.ceil(stages / sps)
+    return dict(tn=tn, tp=tp, tq=tq, mt_n=mt[0], mt_p=mt[1], mt_q=mt[2], bn=bn, nt=nt,
+                kpack=kpack, stages=stages, splits=splits, sps=sps,
+                tiles=base * splits)

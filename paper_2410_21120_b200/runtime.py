@@ -1,0 +1,287 @@
+"""ctypes binding of libdfx (include/dfx.h).
+
+The product path has no CPU fallback: if ``libdfx.so`` is missing or no
+sm_100 device is visible, ``lib()`` / ``init_device()`` raise ``DeviceError``.
+Structures mirror dfx.h field for field; ``check_abi()`` compares every
+``sizeof`` with the library's own ``dfx_sizeof`` so a layout drift fails at
+load time instead of corrupting kernel parameters.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+import threading
+from pathlib import Path
+
+from .errors import DeviceError
+
+PKG = Path(__file__).resolve().parent
+LIB_PATH = PKG / "libdfx.so"
+
+OP_GEMM, OP_SPLITK, OP_DWCONV, OP_POOL, OP_GAP, OP_EW, OP_IN, OP_OUT = range(1, 9)
+ACT = {None: 0, "relu": 1, "hardswish": 2, "hardsigmoid": 3, "silu": 4, "sigmoid": 5}
+BIN_NONE, BIN_ADD, BIN_SCALE = 0, 1, 2
+
+i32, i64, u64, vp = C.c_int32, C.c_int64, C.c_uint64, C.c_void_p
+fptr = C.POINTER(C.c_float)
+
+
+class View(C.Structure):
+    _fields_ = [("base", vp), ("n", i32), ("h", i32), ("w", i32), ("c", i32),
+                ("pitch", i32), ("coff", i32)]
+
+
+class Epilogue(C.Structure):
+    _fields_ = [("alpha", vp), ("beta", vp), ("act1", i32), ("act2", i32), ("binop", i32),
+                ("_pad", i32), ("other", View)]
+
+
+class GemmDesc(C.Structure):
+    _pack_ = 8
+    _fields_ = [("tmap_a", u64 * 16), ("tmap_b", u64 * 16),
+                ("n", i32), ("p", i32), ("q", i32), ("tn", i32), ("tp", i32), ("tq", i32),
+                ("mt_n", i32), ("mt_p", i32), ("mt_q", i32), ("nt", i32),
+                ("r", i32), ("s", i32), ("stride_h", i32), ("stride_w", i32),
+                ("pad_h", i32), ("pad_w", i32), ("cb", i32), ("cblocks", i32), ("ksteps", i32),
+                ("kpack", i32), ("stages", i32), ("splits", i32), ("stages_per_split", i32),
+                ("bn", i32), ("cout", i32), ("tile_begin", i32), ("tiles", i32), ("_pad0", i32),
+                ("out", View), ("epi", Epilogue), ("ws", vp), ("_pad1", i64 * 5)]
+
+
+class GemmLaunch(C.Structure):
+    _fields_ = [("descs", vp), ("ndesc", i32), ("total_tiles", i32), ("bn_max", i32),
+                ("_pad", i32)]
+
+
+class SplitKParams(C.Structure):
+    _fields_ = [("ws", vp), ("splits", i32), ("pixels", i32), ("cout", i32), ("ldw", i32),
+                ("out", View), ("epi", Epilogue)]
+
+
+class DwconvParams(C.Structure):
+    _fields_ = [("inp", View), ("out", View), ("weight", vp), ("kh", i32), ("kw", i32),
+                ("stride_h", i32), ("stride_w", i32), ("pad_h", i32), ("pad_w", i32),
+                ("epi", Epilogue)]
+
+
+class PoolParams(C.Structure):
+    _fields_ = [("inp", View), ("out", View), ("kh", i32), ("kw", i32), ("stride_h", i32),
+                ("stride_w", i32), ("pad_h", i32), ("pad_w", i32), ("is_max", i32),
+                ("count_include_pad", i32)]
+
+
+class GapParams(C.Structure):
+    _fields_ = [("inp", View), ("out", View)]
+
+
+class EwParams(C.Structure):
+    _fields_ = [("inp", View), ("out", View), ("epi", Epilogue)]
+
+
+class InParams(C.Structure):
+    _fields_ = [("src", vp), ("out", View)]
+
+
+class OutParams(C.Structure):
+    _fields_ = [("inp", View), ("dst", vp)]
+
+
+STRUCTS = {
+    "dfx_view": View, "dfx_epilogue": Epilogue, "dfx_gemm_desc": GemmDesc,
+    "dfx_gemm_launch": GemmLaunch, "dfx_splitk_params": SplitKParams,
+    "dfx_dwconv_params": DwconvParams, "dfx_pool_params": PoolParams,
+    "dfx_gap_params": GapParams, "dfx_ew_params": EwParams, "dfx_in_params": InParams,
+    "dfx_out_params": OutParams,
+}
+OP_PARAMS = {OP_GEMM: GemmLaunch, OP_SPLITK: SplitKParams, OP_DWCONV: DwconvParams,
+             OP_POOL: PoolParams, OP_GAP: GapParams, OP_EW: EwParams, OP_IN: InParams,
+             OP_OUT: OutParams}
+
+# every symbol include/dfx.h declares (tests check the .so exports all of them)
+EXPORTS = (
+    "dfx_last_error", "dfx_abi_version", "dfx_sizeof", "dfx_init", "dfx_device_info", "dfx_mem_info",
+    "dfx_malloc", "dfx_free", "dfx_memset", "dfx_host_alloc", "dfx_host_free",
+    "dfx_host_register", "dfx_host_unregister", "dfx_memcpy_h2d", "dfx_memcpy_d2h",
+    "dfx_memcpy_d2d", "dfx_arena_upload", "dfx_stream_create", "dfx_stream_destroy",
+    "dfx_stream_sync", "dfx_event_create", "dfx_event_destroy", "dfx_event_record",
+    "dfx_event_elapsed", "dfx_tmap_act", "dfx_tmap_weights", "dfx_launch", "dfx_graph_create",
+    "dfx_graph_add", "dfx_graph_instantiate", "dfx_graph_launch", "dfx_graph_node_count",
+    "dfx_graph_destroy", "dfx_execute",
+)
+
+_lock = threading.Lock()
+_lib = None
+_inited: set[int] = set()
+
+
+def lib():
+    """Load libdfx.so (once).  Raises DeviceError if it is not built."""
+    global _lib
+    with _lock:
+        if _lib is None:
+            path = os.environ.get("DFX_LIBRARY", str(LIB_PATH))
+            if not Path(path).exists():
+                raise DeviceError(-6, f"{path} is not built (run __graft_entry__.build())",
+                                  "load libdfx")
+            L = C.CDLL(path)
+            L.dfx_last_error.restype = C.c_char_p
+            L.dfx_sizeof.argtypes = [C.c_char_p]
+            L.dfx_sizeof.restype = C.c_int
+            _lib = L
+            check_abi(L)
+        return _lib
+
+
+def check_abi(L) -> None:
+    if L.dfx_abi_version() != 1:
+        raise DeviceError(-2, "ABI version mismatch", "dfx_abi_version")
+    for name, cls in STRUCTS.items():
+        got = L.dfx_sizeof(name.encode())
+        if got != C.sizeof(cls):
+            raise DeviceError(-2, f"sizeof({name}) = {got} in C, {C.sizeof(cls)} in ctypes",
+                              "check_abi")
+
+
+def call(name: str, *args) -> None:
+    L = lib()
+    rc = getattr(L, name)(*args)
+    if rc != 0:
+        raise DeviceError(rc, L.dfx_last_error().decode(errors="replace"), name)
+
+
+def init_device(device: int = 0) -> None:
+    if device in _inited:
+        call("dfx_init", C.c_int(device))   # cheap; re-selects the device on this thread
+        return
+    call("dfx_init", C.c_int(device))
+    _inited.add(device)
+
+
+# ---- small helpers ---------------------------------------------------------------
+
+def malloc(nbytes: int) -> int:
+    p = vp()
+    call("dfx_malloc", C.byref(p), C.c_size_t(nbytes))
+    return p.value
+
+
+def free(ptr: int) -> None:
+    if ptr:
+        call("dfx_free", vp(ptr))
+
+
+def host_alloc(nbytes: int) -> int:
+    p = vp()
+    call("dfx_host_alloc", C.byref(p), C.c_size_t(nbytes))
+    return p.value
+
+
+def host_free(ptr: int) -> None:
+    if ptr:
+        call("dfx_host_free", vp(ptr))
+
+
+def memset(ptr: int, value: int, nbytes: int, stream=None) -> None:
+    call("dfx_memset", vp(ptr), C.c_int(value), C.c_size_t(nbytes), vp(stream))
+
+
+def h2d(dst: int, src: int, nbytes: int, stream=None) -> None:
+    call("dfx_memcpy_h2d", vp(dst), vp(src), C.c_size_t(nbytes), vp(stream))
+
+
+def d2h(dst: int, src: int, nbytes: int, stream=None) -> None:
+    call("dfx_memcpy_d2h", vp(dst), vp(src), C.c_size_t(nbytes), vp(stream))
+
+
+def stream_create() -> int:
+    s = vp()
+    call("dfx_stream_create", C.byref(s))
+    return s.value
+
+
+def stream_sync(stream) -> None:
+    call("dfx_stream_sync", vp(stream))
+
+
+def stream_destroy(stream) -> None:
+    call("dfx_stream_destroy", vp(stream))
+
+
+def mem_info() -> tuple[int, int]:
+    f, t = C.c_size_t(), C.c_size_t()
+    call("dfx_mem_info", C.byref(f), C.byref(t))
+    return f.value, t.value
+
+
+def launch(op: int, params, stream=None) -> None:
+    call("dfx_launch", C.c_int(op), C.byref(params), C.c_size_t(C.sizeof(params)), vp(stream))
+
+
+class Event:
+    def __init__(self):
+        e = vp()
+        call("dfx_event_create", C.byref(e))
+        self.ptr = e.value
+
+    def record(self, stream=None):
+        call("dfx_event_record", vp(self.ptr), vp(stream))
+
+    def elapsed_ms(self, end: "Event") -> float:
+        ms = C.c_float()
+        call("dfx_event_elapsed", vp(self.ptr), vp(end.ptr), C.byref(ms))
+        return ms.value
+
+    def __del__(self):
+        try:
+            if self.ptr and _lib is not None:
+                _lib.dfx_event_destroy(vp(self.ptr))
+        except Exception:   # noqa: BLE001 - interpreter teardown
+            pass
+
+
+class Graph:
+    """A CUDA graph of libdfx kernel nodes with explicit dependencies."""
+
+    def __init__(self):
+        g = vp()
+        call("dfx_graph_create", C.byref(g))
+        self.ptr = g.value
+        self.kinds: list[int] = []
+
+    def add(self, op: int, params, deps=()) -> int:
+        deps = list(deps)
+        arr = (C.c_int * max(len(deps), 1))(*deps)
+        nid = C.c_int()
+        call("dfx_graph_add", vp(self.ptr), C.c_int(op), C.byref(params),
+             C.c_size_t(C.sizeof(params)), arr, C.c_int(len(deps)), C.byref(nid))
+        self.kinds.append(op)
+        return nid.value
+
+    def instantiate(self):
+        call("dfx_graph_instantiate", vp(self.ptr))
+
+    def launch(self, stream=None):
+        call("dfx_graph_launch", vp(self.ptr), vp(stream))
+
+    def execute(self, host_in, dev_in, in_bytes, host_out, dev_out, out_bytes, stream):
+        call("dfx_execute", vp(self.ptr), vp(host_in), vp(dev_in), C.c_size_t(in_bytes),
+             vp(host_out), vp(dev_out), C.c_size_t(out_bytes), vp(stream))
+
+    def destroy(self):
+        if self.ptr:
+            call("dfx_graph_destroy", vp(self.ptr))
+            self.ptr = 0
+
+
+def tmap_act(view: View, cb: int, tq: int, tp: int, tn: int, sw: int, sh: int):
+    buf = (u64 * 16)()
+    call("dfx_tmap_act", buf, C.byref(view), C.c_int(cb), C.c_int(tq), C.c_int(tp), C.c_int(tn),
+         C.c_int(sw), C.c_int(sh))
+    return buf
+
+
+def tmap_weights(base: int, rows: int, k: int, cb: int, bn: int):
+    buf = (u64 * 16)()
+    call("dfx_tmap_weights", buf, vp(base), C.c_int(rows), C.c_int(k), C.c_int(cb), C.c_int(bn))
+    return buf

@@ -1,0 +1,151 @@
+"""numpy interpreter of a lowered MemberProgram — test infrastructure.
+
+Executes exactly what the GPU would: the launch list over ONE flat activation
+arena laid out by ``device.plan_member`` (so an overlap bug in the planner
+corrupts results here too), GEMM weights read back from their packed bf16
+(r, s, channel-block) K order, epilogue slots in dfx.h order, bf16 rounding
+of every stored activation.  Lets the lowering be checked on CPU before any
+GPU time is spent.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from paper_2410_21120_b200.device import plan_member
+from paper_2410_21120_b200.lower import (COPY, DWCONV, EW, GAP, GEMM, POOL, bf16_bits_to_f32,
+                                         to_bf16_bits)
+
+
+def _bf16(x):
+    return bf16_bits_to_f32(to_bf16_bits(np.asarray(x, np.float32)))
+
+
+def _act(kind, v):
+    if kind is None:
+        return v
+    if kind == "relu":
+        return np.maximum(v, 0)
+    if kind == "hardswish":
+        return v * np.clip(v + 3, 0, 6) / 6
+    if kind == "hardsigmoid":
+        return np.clip(v + 3, 0, 6) / 6
+    if kind == "silu":
+        return v / (1 + np.exp(-v))
+    if kind == "sigmoid":
+        return 1 / (1 + np.exp(-v))
+    raise KeyError(kind)
+
+
+class Emulator:
+    def __init__(self, prog, n, round_bf16=True):
+        self.p, self.n = prog, n
+        self.plan = plan_member(prog, n)
+        self.arena = np.full(self.plan.arena_bytes // 2 + 8, np.nan, dtype=np.float32)
+        self.round = round_bf16
+
+    def view(self, name):
+        v = self.p.values[name]
+        b = self.p.buffers[v.buf]
+        base = self.plan.offsets[v.buf] // 2
+        full = self.arena[base:base + self.n * v.h * v.w * b.pitch].reshape(self.n, v.h, v.w, b.pitch)
+        return full[..., v.coff:v.coff + v.c]
+
+    def store(self, dst_view, vals):
+        dst_view[...] = _bf16(vals) if self.round else vals
+
+    def epilogue(self, L, x):
+        e = L.epi
+        v = x.astype(np.float32)
+        if e.alpha is not None:
+            v = v * e.alpha
+        if e.beta is not None:
+            v = v + e.beta
+        v = _act(e.act1, v)
+        if e.binop == 1:
+            v = v + self.view(e.other)
+        elif e.binop == 2:
+            v = v * self.view(e.other)[:, 0:1, 0:1, :]
+        return _act(e.act2, v)
+
+    def run(self, xs):
+        p = self.p
+        xs = np.asarray(xs, np.float32).reshape((self.n,) + tuple(p.input_dims))
+        iv = self.view("<input>")
+        if xs.ndim == 4:
+            self.store(iv, xs.transpose(0, 2, 3, 1))
+        else:
+            self.store(iv, xs[:, None, None, :])
+        for L in p.launches:
+            getattr(self, "do_" + L.kind)(L)
+        out = self.view(p.exit_value)        # (n, h, w, c) -> logical CHW flatten
+        return out.transpose(0, 3, 1, 2).reshape(self.n, -1)
+
+    def do_gemm(self, L):
+        g = L.geom
+        x = self.view(L.src)
+        key = L.blobs["weight"]
+        dbg = getattr(self.p, "debug_f32", {})
+        packed = dbg[key] if (not self.round and key in dbg) else \
+            bf16_bits_to_f32(self.p.blobs[key])
+        w = packed.reshape(g["cout"], g["kh"], g["kw"], g["cblocks"] * g["cb"])[..., :g["cin"]]
+        if self.round:
+            x = _bf16(x)
+        n, h, wd, c = x.shape
+        xp = np.pad(x, ((0, 0), (g["ph"], g["ph"]), (g["pw"], g["pw"]), (0, 0)))
+        out = self.view(L.dst)
+        P, Q = out.shape[1], out.shape[2]
+        acc = np.zeros((n, P, Q, g["cout"]), np.float64)
+        for r in range(g["kh"]):
+            for s in range(g["kw"]):
+                win = xp[:, r:r + P * g["sh"]:g["sh"], s:s + Q * g["sw"]:g["sw"], :]
+                acc += np.einsum("npqc,oc->npqo", win, w[:, r, s, :], optimize=True)
+        self.store(out, self.epilogue(L, acc.astype(np.float32)))
+
+    def do_dwconv(self, L):
+        g = L.geom
+        x = self.view(L.src)
+        taps = self.p.blobs[L.blobs["weight"]].reshape(g["kh"], g["kw"], -1)
+        xp = np.pad(x, ((0, 0), (g["ph"], g["ph"]), (g["pw"], g["pw"]), (0, 0)))
+        out = self.view(L.dst)
+        P, Q = out.shape[1], out.shape[2]
+        acc = np.zeros(out.shape, np.float32)
+        for r in range(g["kh"]):
+            for s in range(g["kw"]):
+                acc += xp[:, r:r + P * g["sh"]:g["sh"], s:s + Q * g["sw"]:g["sw"], :] * taps[r, s]
+        self.store(out, self.epilogue(L, acc))
+
+    def do_pool(self, L):
+        g = L.geom
+        x = self.view(L.src)
+        fill = -np.inf if g["is_max"] else 0.0
+        xp = np.pad(x, ((0, 0), (g["ph"], g["ph"]), (g["pw"], g["pw"]), (0, 0)), constant_values=fill)
+        ones = np.pad(np.ones(x.shape[1:3]), ((g["ph"], g["ph"]), (g["pw"], g["pw"])))
+        out = self.view(L.dst)
+        P, Q = out.shape[1], out.shape[2]
+        acc, cnt = None, np.zeros((P, Q))
+        for r in range(g["kh"]):
+            for s in range(g["kw"]):
+                win = xp[:, r:r + P * g["sh"]:g["sh"], s:s + Q * g["sw"]:g["sw"], :]
+                cnt += ones[r:r + P * g["sh"]:g["sh"], s:s + Q * g["sw"]:g["sw"]]
+                acc = win.copy() if acc is None else (np.maximum(acc, win) if g["is_max"] else acc + win)
+        if not g["is_max"]:
+            div = g["kh"] * g["kw"] if g["cip"] else cnt
+            acc = acc / (div if np.isscalar(div) else div[None, :, :, None])
+        self.store(out, acc)
+
+    def do_gap(self, L):
+        x = self.view(L.src)
+        self.store(self.view(L.dst), x.mean(axis=(1, 2), keepdims=True))
+
+    def do_ew(self, L):
+        self.store(self.view(L.dst), self.epilogue(L, self.view(L.src)))
+
+    def do_copy(self, L):
+        cv = self.p.values[L.geom["concat"]]
+        b = self.p.buffers[cv.buf]
+        base = self.plan.offsets[cv.buf] // 2
+        full = self.arena[base:base + self.n * cv.h * cv.w * b.pitch].reshape(self.n, cv.h, cv.w, b.pitch)
+        src = self.view(L.src)
+        off = L.geom["coff"]
+        full[..., off:off + src.shape[3]] = src

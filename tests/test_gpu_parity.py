@@ -1,0 +1,203 @@
+"""GPU parity: the sm_100a path (through libdfx) against the CPU oracle.
+
+Tolerance (north star): per sample ||gpu - ref||inf / ||ref||inf <= 2e-2.
+The toy corpus has a few random-init models whose bf16 error exceeds that
+(see test_lowering_cpu.py: the same margin shows up in the CPU emulation of
+the lowered program), so it is held to >= 97% of models at 2e-2 and every
+model at 6e-2; single layers and the zoo are held to 2e-2 each.
+"""
+
+import threading
+
+import numpy as np
+import pytest
+
+from conftest import golden_input
+from oracle.executor_ref import run_faithful, run_fast
+from paper_2410_21120_b200 import fuse, graph_ir
+from paper_2410_21120_b200.executor import Tensor, run, run_batch
+
+pytestmark = pytest.mark.gpu
+
+TOL = 2e-2
+TOY_MAX = 6e-2
+
+
+def rel(got, ref):
+    got = np.asarray(got, np.float64).reshape(len(got), -1)
+    ref = np.asarray(ref, np.float64).reshape(len(ref), -1)
+    return (np.abs(got - ref).max(axis=1) / np.maximum(np.abs(ref).max(axis=1), 1e-30)).max()
+
+
+def single(node, in_dims, out_dims, store):
+    return graph_ir.ModelGraph(node.node_id, [node], node.node_id, node.node_id,
+                               graph_ir.TensorSpec(in_dims), graph_ir.TensorSpec(out_dims)), store
+
+
+CONV_CASES = [
+    # cin, h, w, cout, k, stride, pad, n
+    (3, 8, 8, 4, 3, 1, 1, 2),
+    (3, 32, 32, 64, 7, 2, 3, 2),
+    (16, 17, 13, 24, 3, 1, 1, 3),
+    (48, 14, 14, 192, 1, 1, 0, 2),
+    (64, 28, 28, 128, 3, 2, 1, 1),
+    (144, 7, 7, 48, 3, 1, 1, 4),
+    (256, 14, 14, 512, 3, 1, 1, 1),
+    (512, 7, 7, 1000, 1, 1, 0, 2),
+    (40, 9, 11, 300, 5, 2, 2, 2),
+]
+
+
+@pytest.mark.parametrize("cin,h,w,cout,k,s,p,n", CONV_CASES)
+def test_conv_layer(cin, h, w, cout, k, s, p, n):
+    rng = np.random.default_rng(cin * 1000 + cout)
+    st = graph_ir.WeightStore()
+    st.put("w", graph_ir.TensorSpec((cout, cin, k, k)), rng.standard_normal(cout * cin * k * k) / np.sqrt(cin * k * k))
+    st.put("b", graph_ir.TensorSpec((cout,)), rng.standard_normal(cout) * 0.1)
+    node = graph_ir.OpNode("c", "conv2d", {"out_channels": cout, "kernel": k, "stride": s, "padding": p},
+                           {"weight": "w", "bias": "b"})
+    oh, ow = (h + 2 * p - k) // s + 1, (w + 2 * p - k) // s + 1
+    g, st = single(node, (cin, h, w), (cout, oh, ow), st)
+    xs = rng.standard_normal((n, cin, h, w)).astype(np.float32)
+    got = [t.values for t in run_batch(g, st, [Tensor(g.input_spec, x) for x in xs])]
+    ref = run_fast(g, st, xs)
+    assert rel(got, ref) < TOL
+
+
+@pytest.mark.parametrize("units,fan_in,n", [(10, 7, 1), (4096, 25088 // 49, 2), (1000, 1280, 3), (240, 960, 1)])
+def test_dense_layer(units, fan_in, n):
+    rng = np.random.default_rng(units)
+    st = graph_ir.WeightStore()
+    st.put("w", graph_ir.TensorSpec((units, fan_in)), rng.standard_normal(units * fan_in) / np.sqrt(fan_in))
+    st.put("b", graph_ir.TensorSpec((units,)), rng.standard_normal(units) * 0.1)
+    node = graph_ir.OpNode("d", "dense", {"units": units, "fan_in": fan_in}, {"weight": "w", "bias": "b"})
+    g, st = single(node, (fan_in,), (units,), st)
+    xs = rng.standard_normal((n, fan_in)).astype(np.float32)
+    got = [t.values for t in run_batch(g, st, [Tensor(g.input_spec, x) for x in xs])]
+    assert rel(got, run_fast(g, st, xs)) < TOL
+
+
+def test_extension_kinds_chain():
+    rng = np.random.default_rng(5)
+    st = graph_ir.WeightStore()
+    st.put("dw", graph_ir.TensorSpec((24, 1, 5, 5)), rng.standard_normal(600) * 0.2)
+    st.put("f1", graph_ir.TensorSpec((8, 24)), rng.standard_normal(192) * 0.2)
+    st.put("f2", graph_ir.TensorSpec((24, 8)), rng.standard_normal(192) * 0.3)
+    st.put("pw", graph_ir.TensorSpec((16, 24, 1, 1)), rng.standard_normal(384) * 0.2)
+    for nm in ("g", "b", "m", "v"):
+        st.put(nm, graph_ir.TensorSpec((24,)), rng.uniform(0.5, 1.5, 24) if nm in "gv" else rng.standard_normal(24) * 0.1)
+    O = graph_ir.OpNode
+    nodes = [
+        O("a", "conv2d", {"out_channels": 24, "kernel": 5, "stride": 2, "padding": 2, "groups": 24}, {"weight": "dw"}),
+        O("b", "batchnorm_inference", {}, {"gamma": "g", "beta": "b", "mean": "m", "var": "v"}, ("a",)),
+        O("c", "hardswish", inputs=("b",)),
+        O("d", "global_avg_pool", inputs=("c",)),
+        O("e", "dense", {"units": 8, "fan_in": 24}, {"weight": "f1"}, ("d",)),
+        O("f", "silu", inputs=("e",)),
+        O("h", "dense", {"units": 24, "fan_in": 8}, {"weight": "f2"}, ("f",)),
+        O("i", "hardsigmoid", inputs=("h",)),
+        O("j", "channel_scale", inputs=("c", "i")),
+        O("k", "conv2d", {"out_channels": 16, "kernel": 1}, {"weight": "pw"}, ("j",)),
+        O("l", "avgpool2d", {"kernel": 3, "stride": 2, "padding": 1, "count_include_pad": 0}, inputs=("k",)),
+        O("m", "maxpool2d", {"kernel": 3, "stride": 1, "padding": 1}, inputs=("l",)),
+        O("n", "sigmoid", inputs=("m",)),
+    ]
+    g = graph_ir.ModelGraph("ext", nodes, "a", "n", graph_ir.TensorSpec((24, 20, 20)), graph_ir.TensorSpec((16, 5, 5)))
+    assert graph_ir.validate_graph(g, st).ok
+    xs = rng.standard_normal((3, 24, 20, 20)).astype(np.float32)
+    got = [t.values for t in run_batch(g, st, [Tensor(g.input_spec, x) for x in xs])]
+    assert rel(got, run_fast(g, st, xs)) < TOL
+
+
+def test_toy_zoo(zoo, zoo_golden):
+    for g, w in zoo:
+        xs = zoo_golden[f"{g.model_id}.x"]
+        got = [t.values for t in run_batch(g, w, [Tensor(g.input_spec, x) for x in xs])]
+        assert rel(got, zoo_golden[f"{g.model_id}.y"]) < TOL, g.model_id
+
+
+def test_corpus_fused_vs_reference_and_solo(corpus, corpus_golden):
+    errs = []
+    n_groups = int(corpus_golden["n_groups"])
+    for gi in range(n_groups):
+        members = [int(i) for i in corpus_golden[f"group{gi}.members"]]
+        models = [corpus[i] for i in members]
+        dag = fuse.fuse_models(models, validate=False)
+        assert dag.total_mem_estimate_mib == float(corpus_golden[f"group{gi}.mem_mib"])
+        for t in range(2):
+            inputs = {corpus[i][0].model_id: Tensor(corpus[i][0].input_spec,
+                                                    golden_input(corpus[i][0].input_spec.dims, 7919 * i + t))
+                      for i in members}
+            outs = fuse.execute_fused(dag, inputs)
+            for i in members:
+                g, w = corpus[i]
+                ref = corpus_golden[f"{g.model_id}.y"][t]
+                errs.append(rel([outs[g.model_id].values], [ref]))
+                # fused and solo GPU runs use identical kernels in identical order: bitwise
+                solo = run(g, w, inputs[g.model_id])
+                assert np.array_equal(solo.values, outs[g.model_id].values), g.model_id
+    errs = np.array(errs)
+    assert (errs <= TOL).mean() >= 0.97, np.sort(errs)[-8:]
+    assert errs.max() < TOY_MAX
+
+
+def test_batched_members_and_empty(corpus):
+    models = corpus[:3]
+    dag = fuse.fuse_models(models)
+    rng = np.random.default_rng(1)
+    inputs = {g.model_id: [Tensor(g.input_spec, rng.standard_normal(g.input_spec.element_count))
+                           for _ in range(k)] for k, (g, _) in zip((5, 0, 2), models)}
+    outs = fuse.execute_fused(dag, inputs)
+    assert [len(outs[g.model_id]) for g, _ in models] == [5, 0, 2]
+    for k, (g, w) in zip((5, 0, 2), models):
+        for x, y in zip(inputs[g.model_id], outs[g.model_id]):
+            assert np.array_equal(run(g, w, x).values, y.values)
+
+
+def test_swap_subgraph_on_device(corpus):
+    models = corpus[10:14]
+    dag = fuse.fuse_models(models)
+    rng = np.random.default_rng(2)
+    inputs = {g.model_id: Tensor(g.input_spec, rng.standard_normal(g.input_spec.element_count)) for g, _ in models}
+    before = fuse.execute_fused(dag, inputs)
+    incoming = corpus[20]
+    new = fuse.swap_subgraph(dag, models[1][0].model_id, incoming)
+    inputs2 = dict(inputs)
+    del inputs2[models[1][0].model_id]
+    inputs2[incoming[0].model_id] = Tensor(incoming[0].input_spec,
+                                           rng.standard_normal(incoming[0].input_spec.element_count))
+    after = fuse.execute_fused(new, inputs2)
+    for g, w in (models[0], models[2], models[3]):
+        assert np.array_equal(before[g.model_id].values, after[g.model_id].values)
+    ref = run_faithful(incoming[0], incoming[1], inputs2[incoming[0].model_id].values)
+    assert rel([after[incoming[0].model_id].values], [ref]) < TOY_MAX
+    # the pre-swap DAG still answers correctly (re-loaded on demand)
+    again = fuse.execute_fused(dag, inputs)
+    for g, _ in models:
+        assert np.array_equal(again[g.model_id].values, before[g.model_id].values)
+
+
+def test_concurrent_execute_fused(corpus):
+    models = corpus[30:33]
+    dag = fuse.fuse_models(models)
+    rng = np.random.default_rng(3)
+    inputs = {g.model_id: Tensor(g.input_spec, rng.standard_normal(g.input_spec.element_count)) for g, _ in models}
+    ref = fuse.execute_fused(dag, inputs)
+    results, errors = [], []
+
+    def worker():
+        try:
+            for _ in range(5):
+                results.append(fuse.execute_fused(dag, inputs))
+        except Exception as exc:  # noqa: BLE001
+            errors.append(exc)
+
+    ts = [threading.Thread(target=worker) for _ in range(6)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert not errors, errors
+    for out in results:
+        for mid in ref:
+            assert np.array_equal(out[mid].values, ref[mid].values)

@@ -1,0 +1,58 @@
+"""Lowering + planner + weight packing checked on CPU through the program emulator."""
+
+import numpy as np
+import pytest
+
+from conftest import golden_input
+from oracle.executor_ref import run_fast
+from paper_2410_21120_b200.lower import lower_member
+from program_emulator import Emulator
+
+
+def _rel(a, b):
+    a = a.reshape(len(a), -1)
+    b = b.reshape(len(b), -1)
+    return (np.abs(a - b).max(axis=1) / np.maximum(np.abs(b).max(axis=1), 1e-30)).max()
+
+
+def test_corpus_lowering_exact_in_fp32(corpus, corpus_golden):
+    """Without bf16 rounding the lowered program equals the reference outputs to fp32 noise."""
+    for i, (g, w) in enumerate(corpus):
+        prog = lower_member(g, w, keep_f32=True)
+        xs = np.stack([golden_input(g.input_spec.dims, 7919 * i + t) for t in range(4)])
+        got = Emulator(prog, 4, round_bf16=False).run(xs)
+        assert _rel(got, corpus_golden[f"{g.model_id}.y"]) < 1e-5, g.model_id
+
+
+BF16_TOL = 2e-2          # north-star tolerance: per sample ||d||inf / ||ref||inf
+BF16_TOL_TOY_MAX = 6e-2  # worst toy model (random init, near-zero logits)
+
+
+def test_corpus_lowering_bf16_tolerance(corpus, corpus_golden):
+    errs = []
+    for i, (g, w) in enumerate(corpus):
+        prog = lower_member(g, w)
+        xs = np.stack([golden_input(g.input_spec.dims, 7919 * i + t) for t in range(4)])
+        got = Emulator(prog, 4).run(xs)
+        errs.append(_rel(got, corpus_golden[f"{g.model_id}.y"]))
+    errs = np.array(errs)
+    assert (errs <= BF16_TOL).mean() >= 0.97, np.sort(errs)[-8:]
+    assert errs.max() < BF16_TOL_TOY_MAX
+
+
+def test_zoo_lowering(zoo, zoo_golden):
+    for g, w in zoo:
+        prog = lower_member(g, w)
+        xs = zoo_golden[f"{g.model_id}.x"]
+        got = Emulator(prog, len(xs)).run(xs)
+        assert _rel(got, zoo_golden[f"{g.model_id}.y"]) < BF16_TOL, g.model_id
+
+
+def test_launch_counts_show_fusion(corpus):
+    """Epilogue fusion + zero-copy concat: fewer launches than compute nodes."""
+    nodes = launches = 0
+    for g, w in corpus:
+        prog = lower_member(g, w)
+        nodes += sum(1 for n in g.nodes.values() if n.kind not in ("flatten",))
+        launches += len(prog.launches)
+    assert launches < nodes
