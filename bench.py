@@ -1,0 +1,441 @@
+#!/usr/bin/env python3
+"""Benchmark of the fused multi-CNN DAG on B200 (BASELINE.json metric).
+
+Workload (BASELINE.json configs[1]): VGG16 + MobileNetV3-L + DenseNet161 +
+EfficientNetV2-L fused into one DAG, batch 1 per member, synthetic N(0,1)
+3x224x224 inputs, calibrated synthetic weights (zoo/, no checkpoints offline).
+One step = one fused query = one image through every member (4 images).
+
+  value   images/s of the whole job, device-timed with CUDA events per step
+          (inputs resident in HBM); the weights (587 MB packed) exceed the
+          126 MB L2, and an L2-flush write of 256 MB runs between timed steps
+          outside the events
+  e2e     the same metric through the public API ``execute_fused`` with host
+          Tensors: pinned H2D of the inputs, graph, D2H of the logits
+  + swap-in (one arena, one H2D) vs the unfused per-tensor loader, peak HBM
+    fused vs unfused, per-kernel-class roofline, CPU oracle baseline.
+
+Usage: python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+N>1 runs under torchrun: rank 0 does the single H2D, the arena is broadcast
+over NCCL, every rank runs its own queries (weak scaling), time = max over
+ranks.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+PEAKS_PATH = ROOT / "MEASURED_PEAKS.json"
+FALLBACK_PEAKS = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
+
+
+def peaks():
+    try:
+        d = json.loads(PEAKS_PATH.read_text())
+        return d, "measured"
+    except Exception:  # noqa: BLE001
+        return FALLBACK_PEAKS, "fallback"
+
+
+# ----------------------------------------------------------------------------- clocks
+
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index, self.rows, self.proc = index, [], None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            threading.Thread(target=self._read, daemon=True).start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 8:
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+        time.sleep(0.05)
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        reasons = sorted({n for r in self.rows for n, v in zip(names, r[4:8]) if v.lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+# ----------------------------------------------------------------------------- helpers
+
+def build_models(names):
+    from paper_2410_21120_b200 import zoo
+    return [zoo.build(n) for n in names]
+
+
+def make_inputs(models, batch, seed=1234):
+    rng = np.random.default_rng(seed)
+    return [rng.standard_normal((batch,) + tuple(g.input_spec.dims)).astype(np.float32) for g, _ in models]
+
+
+def cpu_port_time(models, xs, budget_s=30.0):
+    """The reference algorithm (numpy port, BLAS on all host threads) on a bounded sample."""
+    from oracle.executor_ref import run_fast
+    t0 = time.perf_counter()
+    imgs = 0
+    while True:
+        for (g, w), x in zip(models, xs):
+            run_fast(g, w, x[:1])
+            imgs += 1
+        el = time.perf_counter() - t0
+        if el > budget_s / 3 or imgs >= 4 * len(models):
+            return imgs / el, imgs, el
+
+
+def measure_pinned_h2d(rt, nbytes=1 << 30, reps=5):
+    host = rt.host_alloc(nbytes)
+    dev = rt.malloc(nbytes)
+    s = rt.stream_create()
+    best = float("inf")
+    for _ in range(reps):
+        e0, e1 = rt.Event(), rt.Event()
+        e0.record(s)
+        rt.h2d(dev, host, nbytes, s)
+        e1.record(s)
+        best = min(best, e0.elapsed_ms(e1))
+    rt.free(dev)
+    rt.host_free(host)
+    rt.stream_destroy(s)
+    return nbytes / (best * 1e-3) / 1e9
+
+
+# ----------------------------------------------------------------------------- reference arm
+
+def run_reference(args, world, rank):
+    """--impl reference: the reference's CPU algorithm (oracle port) on host cores."""
+    if rank != 0:
+        return
+    from oracle.executor_ref import run_fast
+    models = build_models(args.models)
+    xs = make_inputs(models, args.batch)
+    cores = os.cpu_count() or 1
+
+    def step():
+        for (g, w), x in zip(models, xs):
+            run_fast(g, w, x)
+
+    for _ in range(args.warmup):
+        step()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        step()
+    el = time.perf_counter() - t0
+    imgs = args.steps * len(models) * args.batch
+    value = imgs / el
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "images/s",
+        "n_gpus": 0, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": el / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": config_dict(args),
+        "cpu_baseline": {"value": value, "unit": "images/s", "cores": cores, "kind": "port",
+                         "sample": f"{args.steps} full fused queries ({len(models)} members x batch "
+                                   f"{args.batch}) through oracle/executor_ref.run_fast (numpy fp32, "
+                                   f"BLAS on {cores} host threads)"},
+        "e2e": {"value": value, "unit": "images/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+METRIC = "fused 4-model DAG images/s (batch 1 per member), with latency ms, peak HBM GB, swap-in ms"
+
+
+def config_dict(args):
+    return {"workload": "4-model fused DAG (configs[1])" if args.batch == 1 else
+            f"4-model fused DAG, batch {args.batch} per member",
+            "models": list(args.models), "batch_per_member": args.batch,
+            "input": "3x224x224 fp32 N(0,1)", "precision": args.precision, "mode": args.mode,
+            "l2": "weights 587 MB > 126 MB L2; 256 MB L2-flush write between timed steps (untimed)"}
+
+
+# ----------------------------------------------------------------------------- our arm
+
+def run_ours(args, world, rank, local_rank):
+    from paper_2410_21120_b200 import fuse, runtime as rt
+    from paper_2410_21120_b200.device import DeviceDag, PerTensorArena, WeightArena, program_for
+    from paper_2410_21120_b200.executor import Tensor
+
+    dist = None
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl")
+    rt.init_device(local_rank)
+    P, peak_kind = peaks()
+
+    models = build_models(args.models)
+    dag = fuse.fuse_models(models)
+    members = [(sg, sg.weight_binding) for sg in dag.subgraphs]
+    programs = [program_for(g, w, args.precision) for g, w in members]
+
+    # ---------------- unfused baseline: per-tensor loads, per-model graphs run one after another
+    unfused = None
+    if not args.skip_unfused and world == 1:
+        free_u0, _ = rt.mem_info()
+        pt = PerTensorArena(programs, local_rank)
+        solos = [DeviceDag([m], local_rank, "sequential", arena=_SubArena(pt, i), programs=[p],
+                           precision=args.precision)
+                 for i, (m, p) in enumerate(zip(members, programs))]
+        insts = [d.acquire((args.batch,)) for d in solos]
+        for si, x in zip(insts, make_inputs(models, args.batch, seed=1234 + rank)):
+            si.upload_inputs([x])
+        free_u1, _ = rt.mem_info()
+        u_ms = []
+        for _ in range(max(3, args.steps // 2)):
+            e0, e1 = rt.Event(), rt.Event()
+            e0.record(insts[0].stream)
+            for si in insts:          # one model after another, each its own graph
+                si.launch_graph()
+                si.sync()
+            e1.record(insts[-1].stream)
+            u_ms.append(e0.elapsed_ms(e1))
+        unfused = {"swap_in_ms": pt.upload_ms, "weight_tensors": pt.tensors,
+                   "peak_hbm_gb": (free_u0 - free_u1) / 1e9,
+                   "ms_per_query": float(np.median(u_ms)),
+                   "note": "per-tensor cudaMalloc+cudaMemcpyAsync from pageable memory; "
+                           "one CUDA graph per model, launched one after another"}
+        for d in solos:
+            d.free_instances()
+        pt.free()
+
+
+    # ---------------- swap-in: one pinned arena, ONE H2D (rank 0), NCCL broadcast to replicas
+    free0, _ = rt.mem_info()
+    arena = WeightArena(programs, local_rank)
+    if world > 1:
+        if rank == 0:
+            arena.upload()
+        else:
+            arena.allocate()
+        t0 = time.perf_counter()
+        from paper_2410_21120_b200.device import broadcast_arena
+        broadcast_arena(arena, src=0)
+        torch.cuda.synchronize()
+        bcast_ms = (time.perf_counter() - t0) * 1e3
+    else:
+        arena.upload()
+        bcast_ms = None
+    img = DeviceDag(members, local_rank, args.mode, arena=arena, programs=programs,
+                    precision=args.precision)
+    batch = tuple([args.batch] * len(members))
+    inst = img.acquire(batch)
+    xs = make_inputs(models, args.batch, seed=1234 + rank)
+    inst.upload_inputs(xs)
+    inst.launch_graph()
+    inst.sync()
+    free1, _ = rt.mem_info()
+    fused_peak = free0 - free1
+
+    flush = rt.malloc(256 << 20)
+    clocks = ClockSampler(local_rank)
+
+    # ---------------- device-timed steps
+    for _ in range(args.warmup):
+        inst.launch_graph()
+    inst.sync()
+    if dist is not None:
+        dist.barrier()
+    clocks.start()
+    step_ms = []
+    for _ in range(args.steps):
+        rt.memset(flush, rank & 0xFF, 256 << 20, inst.stream)       # L2 flush, outside the events
+        e0, e1 = rt.Event(), rt.Event()
+        e0.record(inst.stream)
+        inst.launch_graph()
+        e1.record(inst.stream)
+        step_ms.append(e0.elapsed_ms(e1))
+    inst.sync()
+    clk = clocks.stop()
+    total_ms = float(np.sum(step_ms))
+    if dist is not None:
+        import torch
+        t = torch.tensor([total_ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+        dist.barrier()
+    imgs_per_step = len(members) * args.batch
+    value = world * imgs_per_step * args.steps / (total_ms * 1e-3)
+    ms_per_step = total_ms / args.steps
+
+    # ---------------- e2e through the public API (host tensors, pinned H2D + D2H inside)
+    fuse.attach_image(dag, img)
+    host_inputs = {sg.model_id: ([Tensor(sg.input_spec, x[i]) for i in range(args.batch)]
+                                 if args.batch > 1 else Tensor(sg.input_spec, x[0]))
+                   for sg, x in zip(dag.subgraphs, xs)}
+    for _ in range(max(args.warmup, 1)):
+        fuse.execute_fused(dag, host_inputs)
+    if dist is not None:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        outs = fuse.execute_fused(dag, host_inputs)
+    e2e_s = time.perf_counter() - t0
+    if dist is not None:
+        import torch
+        t = torch.tensor([e2e_s], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    e2e_value = world * imgs_per_step * args.steps / e2e_s
+
+    if rank != 0:
+        if dist is not None:
+            dist.destroy_process_group()
+        return
+
+    # ---------------- per-kernel-class roofline (eager replay, CUDA events per launch)
+    prof = inst.profile_nodes(reps=3)
+    classes = {}
+    for r in prof:
+        c = classes.setdefault(r["kind"], {"ms": 0.0, "bytes": 0, "flops": 0, "launches": 0})
+        c["ms"] += r["ms"]
+        c["bytes"] += r["bytes"]
+        c["flops"] += r["flops"]
+        c["launches"] += 1
+    eager_total = sum(c["ms"] for c in classes.values())
+    dom = max(classes, key=lambda k: classes[k]["ms"])
+    g = classes["gemm"]
+    gemm_gbs = g["bytes"] / (g["ms"] * 1e-3) / 1e9
+    gemm_tflops = g["flops"] / (g["ms"] * 1e-3) / 1e12
+    hbm_peak = float(P["hbm_gbs"])
+    tc_peak = float(P.get("bf16_tflops", 1590.0))
+    hbm_frac, tc_frac = gemm_gbs / hbm_peak, gemm_tflops / tc_peak
+    bound = "hbm" if hbm_frac >= tc_frac else "tensor"
+    roofline = {
+        "kernel": "dfx::gemm_kernel (tcgen05 implicit-GEMM conv/dense, all launches of one step)",
+        "bound": bound,
+        "achieved": gemm_gbs if bound == "hbm" else gemm_tflops,
+        "peak": hbm_peak if bound == "hbm" else tc_peak,
+        "unit": "GB/s" if bound == "hbm" else "TFLOP/s",
+        "frac": hbm_frac if bound == "hbm" else tc_frac,
+        "traffic": None,
+        "peak_source": f"MEASURED_PEAKS.json ({peak_kind}; burst figures, kernels timed alone)",
+        "other_view": ({"achieved_tflops": gemm_tflops, "frac_of_bf16_peak": tc_frac} if bound == "hbm"
+                       else {"achieved_gbs": gemm_gbs, "frac_of_hbm_peak": hbm_frac}),
+        "gemm_share_of_eager_step": g["ms"] / eager_total,
+        "gemm_launches_per_step": g["launches"],
+        "classes": {k: {"ms": round(v["ms"], 4), "launches": v["launches"],
+                        "GB/s": round(v["bytes"] / (v["ms"] * 1e-3) / 1e9, 1) if v["ms"] else None,
+                        "TFLOP/s": round(v["flops"] / (v["ms"] * 1e-3) / 1e12, 2) if v["ms"] else None}
+                    for k, v in sorted(classes.items(), key=lambda kv: -kv[1]["ms"])},
+        "dominant_class": dom,
+    }
+
+    h2d_gbs = measure_pinned_h2d(rt)
+    cpu_ips, cpu_imgs, cpu_s = cpu_port_time(models, xs)
+    cores = os.cpu_count() or 1
+    # check the logits of the e2e run against the CPU oracle (4 members, 1 image)
+    from oracle.executor_ref import run_fast
+    parity = {}
+    for (gph, w), sg, x in zip(models, dag.subgraphs, xs):
+        ref = run_fast(gph, w, x[:1])[0]
+        got = outs[sg.model_id] if args.batch == 1 else outs[sg.model_id][0]
+        parity[sg.model_id] = float(np.abs(got.values - ref).max() / np.abs(ref).max())
+
+    line = {
+        "metric": METRIC, "value": value, "unit": "images/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f16" if args.precision == "fp16" else "bf16",
+        "data": "synthetic (N(0,1) inputs, seeded calibrated random-init weights)",
+        "config": config_dict(args),
+        "latency_ms": ms_per_step,
+        "swap_in": {"fused_ms": arena.upload_ms, "arena_mb": arena.total / 1e6,
+                    "fused_h2d_gbs": arena.total / (arena.upload_ms * 1e-3) / 1e9 if arena.upload_ms else None,
+                    "pinned_h2d_peak_gbs": h2d_gbs, "nccl_broadcast_ms": bcast_ms,
+                    "unfused_ms": unfused["swap_in_ms"] if unfused else None},
+        "peak_hbm_gb": {"fused": fused_peak / 1e9, "unfused": unfused["peak_hbm_gb"] if unfused else None},
+        "unfused": unfused,
+        "e2e": {"value": e2e_value, "unit": "images/s",
+                "h2d_bytes_per_step": int(sum(x.nbytes for x in xs)),
+                "d2h_bytes_per_step": int(sum(sg.output_spec.element_count * 4 * args.batch
+                                              for sg in dag.subgraphs)),
+                "ms_per_step": e2e_s / args.steps * 1e3},
+        "gpu_launches": inst.kernel_nodes * args.steps,
+        "graph_nodes_per_step": inst.kernel_nodes,
+        "roofline": roofline,
+        "cpu_baseline": {"value": cpu_ips, "unit": "images/s", "cores": cores, "kind": "port",
+                         "sample": f"{cpu_imgs} member-images ({cpu_s:.1f} s) through "
+                                   f"oracle/executor_ref.run_fast (numpy fp32, BLAS on {cores} threads)"},
+        "parity_rel_err": parity,
+        "clocks": clk,
+    }
+    print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+class _SubArena:
+    """One member's view of a PerTensorArena (member index remapped to 0)."""
+
+    def __init__(self, pt, i):
+        self.pt, self.i = pt, i
+        self.upload_ms = None
+
+    def addr(self, member, key):
+        return self.pt.addr(self.i, key)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
+    ap.add_argument("--batch", type=int, default=1)
+    ap.add_argument("--precision", default="fp16", choices=("fp16", "bf16"))
+    ap.add_argument("--mode", default="concurrent", choices=("concurrent", "sequential"))
+    ap.add_argument("--models", nargs="+",
+                    default=["vgg16", "mobilenet_v3_large", "densenet161", "efficientnet_v2_l"])
+    ap.add_argument("--skip-unfused", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, world, rank)
+    else:
+        run_ours(args, world, rank, local_rank)
+
+
+if __name__ == "__main__":
+    main()

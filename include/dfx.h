@@ -19,7 +19,7 @@
  * Streams are passed as opaque void* (a cudaStream_t; NULL = legacy default).
  * No function synchronises unless its comment says so.
  *
- * Data layout on the device: activations are bf16 NHWC with a channel pitch
+ * Data layout on the device: activations are 16-bit (fp16 or bf16) NHWC with a channel pitch
  * that is a multiple of 8 elements (16 B); a tensor may be a channel window
  * [coff, coff + C) of a wider buffer (zero-copy concat).  Weights live in one
  * packed arena.
@@ -34,7 +34,7 @@
 extern "C" {
 #endif
 
-#define DFX_ABI_VERSION 1
+#define DFX_ABI_VERSION 2
 
 typedef enum dfx_status {
   DFX_OK = 0,
@@ -68,11 +68,18 @@ typedef enum dfx_op {
   DFX_OP_OUT = 8       /* bf16 NHWC -> fp32 samples in logical CHW order   */
 } dfx_op;
 
-/* A bf16 NHWC view: element (n, h, w, c) at base[((n*H + h)*W + w)*pitch + coff + c]. */
+typedef enum dfx_dtype {
+  DFX_BF16 = 0,        /* bfloat16 storage, kind::f16 MMA with BF16 operands */
+  DFX_F16 = 1          /* IEEE half storage (saturating stores), F16 operands */
+} dfx_dtype;
+
+/* A 16-bit NHWC view: element (n, h, w, c) at base[((n*H + h)*W + w)*pitch + coff + c].
+ * Every view of one launch has the same dtype. */
 typedef struct dfx_view {
   void* base;
   int32_t n, h, w, c;
   int32_t pitch, coff;
+  int32_t dtype, _pad;
 } dfx_view;
 
 /* Epilogue shared by GEMM / split-K / depthwise / elementwise:
@@ -117,7 +124,7 @@ typedef struct __attribute__((aligned(64))) dfx_gemm_desc {
   dfx_view out;                    /* bf16 output view (n, p, q, cout) */
   dfx_epilogue epi;
   float* ws;                       /* split-K workspace [splits][n*p*q][nt*bn] */
-  int64_t _pad1[5];                
+  int64_t _pad1[3];                
 } dfx_gemm_desc;
 
 typedef struct dfx_gemm_launch {
@@ -125,7 +132,7 @@ typedef struct dfx_gemm_launch {
   int32_t ndesc;
   int32_t total_tiles;             /* grid size */
   int32_t bn_max;                  /* sizes smem / TMEM */
-  int32_t _pad;
+  int32_t dtype;                   /* dfx_dtype of every problem */
 } dfx_gemm_launch;
 
 typedef struct dfx_splitk_params {
@@ -213,8 +220,8 @@ int dfx_event_elapsed(void* start, void* stop, float* ms); /* synchronises on st
  * read as zero. */
 int dfx_tmap_act(void* out128, const dfx_view* v, int cb, int tq, int tp, int tn,
                  int stride_w, int stride_h);
-/* Packed weight matrix [rows][k] bf16 (k contiguous); box (cb, bn). */
-int dfx_tmap_weights(void* out128, const void* base, int rows, int k, int cb, int bn);
+/* Packed weight matrix [rows][k] of `dtype` (k contiguous); box (cb, bn). */
+int dfx_tmap_weights(void* out128, const void* base, int rows, int k, int cb, int bn, int dtype);
 
 /* ---- kernels: direct launch on a stream (tests, eager mode) ------------- */
 int dfx_launch(int op, const void* params, size_t params_size, void* stream);

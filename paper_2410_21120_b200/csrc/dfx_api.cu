@@ -13,15 +13,20 @@
 #include "dfx_common.cuh"
 
 namespace dfx {
-__global__ void gemm_kernel(const __grid_constant__ dfx_gemm_launch L);
-__global__ void splitk_kernel(const __grid_constant__ dfx_splitk_params P);
-__global__ void ew_kernel(const __grid_constant__ dfx_ew_params P);
-__global__ void dwconv_kernel(const __grid_constant__ dfx_dwconv_params P);
-__global__ void pool_kernel(const __grid_constant__ dfx_pool_params P);
-__global__ void gap_kernel(const __grid_constant__ dfx_gap_params P);
-__global__ void in_kernel(const __grid_constant__ dfx_in_params P);
-__global__ void out_kernel(const __grid_constant__ dfx_out_params P);
+template <typename T> __global__ void gemm_kernel(const __grid_constant__ dfx_gemm_launch L);
+template <typename T> __global__ void splitk_kernel(const __grid_constant__ dfx_splitk_params P);
+template <typename T> __global__ void ew_kernel(const __grid_constant__ dfx_ew_params P);
+template <typename T> __global__ void dwconv_kernel(const __grid_constant__ dfx_dwconv_params P);
+template <typename T> __global__ void pool_kernel(const __grid_constant__ dfx_pool_params P);
+template <typename T> __global__ void gap_kernel(const __grid_constant__ dfx_gap_params P);
+template <typename T> __global__ void in_kernel(const __grid_constant__ dfx_in_params P);
+template <typename T> __global__ void out_kernel(const __grid_constant__ dfx_out_params P);
 }  // namespace dfx
+
+// kernel instantiation for a storage dtype (DFX_F16 / DFX_BF16)
+#define DFX_PICK(K, dt) \
+  ((dt) == DFX_F16 ? reinterpret_cast<const void*>(&dfx::K<__half>) \
+                   : reinterpret_cast<const void*>(&dfx::K<__nv_bfloat16>))
 
 namespace {
 
@@ -73,6 +78,10 @@ CUtensorMapSwizzle swizzle_for(int cb) {
                   : (cb == 32 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B);
 }
 
+CUtensorMapDataType tmap_dtype(int dt) {
+  return dt == DFX_F16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
+}
+
 int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
 unsigned elementwise_grid(int64_t threads, int block) {
@@ -101,7 +110,7 @@ int config_for(int op, const void* params, size_t size, LaunchCfg* c) {
       const auto* p = static_cast<const dfx_gemm_launch*>(params);
       if (p->bn_max < 16 || p->bn_max > 256 || p->total_tiles < 1)
         return fail(DFX_E_ARG, "gemm: bad bn_max %d / tiles %d", p->bn_max, p->total_tiles);
-      c->func = reinterpret_cast<const void*>(&dfx::gemm_kernel);
+      c->func = DFX_PICK(gemm_kernel, p->dtype);
       c->grid = dim3(p->total_tiles);
       c->block = dim3(128);
       c->smem = dfx::gemm_smem_bytes(p->bn_max) + 1024;
@@ -110,35 +119,35 @@ int config_for(int op, const void* params, size_t size, LaunchCfg* c) {
     case DFX_OP_SPLITK: {
       NEED(dfx_splitk_params);
       const auto* p = static_cast<const dfx_splitk_params*>(params);
-      c->func = reinterpret_cast<const void*>(&dfx::splitk_kernel);
+      c->func = DFX_PICK(splitk_kernel, p->out.dtype);
       c->grid = dim3(elementwise_grid(int64_t(p->pixels) * cdiv(p->cout, 8), 256));
       return DFX_OK;
     }
     case DFX_OP_DWCONV: {
       NEED(dfx_dwconv_params);
       const auto* p = static_cast<const dfx_dwconv_params*>(params);
-      c->func = reinterpret_cast<const void*>(&dfx::dwconv_kernel);
+      c->func = DFX_PICK(dwconv_kernel, p->in.dtype);
       c->grid = dim3(elementwise_grid(int64_t(p->out.n) * p->out.h * p->out.w * cdiv(p->in.c, 8), 256));
       return DFX_OK;
     }
     case DFX_OP_POOL: {
       NEED(dfx_pool_params);
       const auto* p = static_cast<const dfx_pool_params*>(params);
-      c->func = reinterpret_cast<const void*>(&dfx::pool_kernel);
+      c->func = DFX_PICK(pool_kernel, p->in.dtype);
       c->grid = dim3(elementwise_grid(int64_t(p->out.n) * p->out.h * p->out.w * cdiv(p->in.c, 8), 256));
       return DFX_OK;
     }
     case DFX_OP_GAP: {
       NEED(dfx_gap_params);
       const auto* p = static_cast<const dfx_gap_params*>(params);
-      c->func = reinterpret_cast<const void*>(&dfx::gap_kernel);
+      c->func = DFX_PICK(gap_kernel, p->in.dtype);
       c->grid = dim3(unsigned(cdiv(p->in.c, 256)), unsigned(p->in.n));
       return DFX_OK;
     }
     case DFX_OP_EW: {
       NEED(dfx_ew_params);
       const auto* p = static_cast<const dfx_ew_params*>(params);
-      c->func = reinterpret_cast<const void*>(&dfx::ew_kernel);
+      c->func = DFX_PICK(ew_kernel, p->in.dtype);
       c->grid = dim3(elementwise_grid(int64_t(p->in.n) * p->in.h * p->in.w * cdiv(p->in.c, 8), 256));
       return DFX_OK;
     }
@@ -146,14 +155,14 @@ int config_for(int op, const void* params, size_t size, LaunchCfg* c) {
       NEED(dfx_in_params);
       const auto* p = static_cast<const dfx_in_params*>(params);
       if (p->out.pitch % 8 || p->out.coff) return fail(DFX_E_ARG, "in: pitch/coff");
-      c->func = reinterpret_cast<const void*>(&dfx::in_kernel);
+      c->func = DFX_PICK(in_kernel, p->out.dtype);
       c->grid = dim3(elementwise_grid(int64_t(p->out.n) * p->out.h * p->out.w * (p->out.pitch / 8), 256));
       return DFX_OK;
     }
     case DFX_OP_OUT: {
       NEED(dfx_out_params);
       const auto* p = static_cast<const dfx_out_params*>(params);
-      c->func = reinterpret_cast<const void*>(&dfx::out_kernel);
+      c->func = DFX_PICK(out_kernel, p->in.dtype);
       c->grid = dim3(elementwise_grid(int64_t(p->in.n) * p->in.h * p->in.w * p->in.c, 256));
       return DFX_OK;
     }
@@ -207,9 +216,9 @@ int dfx_init(int device) {
     return fail(DFX_E_NODEVICE, "device %d is sm_%d%d; libdfx is built for sm_100a", device,
                 prop.major, prop.minor);
   g_sm_count = prop.multiProcessorCount;
-  CK(cudaFuncSetAttribute(reinterpret_cast<const void*>(&dfx::gemm_kernel),
-                          cudaFuncAttributeMaxDynamicSharedMemorySize,
-                          dfx::gemm_smem_bytes(256) + 1024));
+  for (int dt : {int(DFX_BF16), int(DFX_F16)})
+    CK(cudaFuncSetAttribute(DFX_PICK(gemm_kernel, dt), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            dfx::gemm_smem_bytes(256) + 1024));
   return get_encode();
 }
 
@@ -331,7 +340,7 @@ int dfx_tmap_act(void* out128, const dfx_view* v, int cb, int tq, int tp, int tn
   cuuint32_t box[4] = {cuuint32_t(cb), cuuint32_t(tq * stride_w), cuuint32_t(tp * stride_h),
                        cuuint32_t(tn)};
   cuuint32_t estr[4] = {1, cuuint32_t(stride_w), cuuint32_t(stride_h), 1};
-  CUresult r = g_encode(reinterpret_cast<CUtensorMap*>(out128), CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4,
+  CUresult r = g_encode(reinterpret_cast<CUtensorMap*>(out128), tmap_dtype(v->dtype), 4,
                         base, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                         swizzle_for(cb), CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
@@ -341,7 +350,7 @@ int dfx_tmap_act(void* out128, const dfx_view* v, int cb, int tq, int tp, int tn
   return DFX_OK;
 }
 
-int dfx_tmap_weights(void* out128, const void* base, int rows, int k, int cb, int bn) {
+int dfx_tmap_weights(void* out128, const void* base, int rows, int k, int cb, int bn, int dtype) {
   int rc = get_encode();
   if (rc) return rc;
   if (cb != 16 && cb != 32 && cb != 64) return fail(DFX_E_ARG, "tmap_weights: cb %d", cb);
@@ -351,7 +360,7 @@ int dfx_tmap_weights(void* out128, const void* base, int rows, int k, int cb, in
   cuuint64_t strides[1] = {cuuint64_t(k) * 2};
   cuuint32_t box[2] = {cuuint32_t(cb), cuuint32_t(bn)};
   cuuint32_t estr[2] = {1, 1};
-  CUresult r = g_encode(reinterpret_cast<CUtensorMap*>(out128), CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+  CUresult r = g_encode(reinterpret_cast<CUtensorMap*>(out128), tmap_dtype(dtype), 2,
                         const_cast<void*>(base), dims, strides, box, estr,
                         CU_TENSOR_MAP_INTERLEAVE_NONE, swizzle_for(cb),
                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);

@@ -1,4 +1,4 @@
-// dfx_bw.cu — bandwidth-bound kernels on bf16 NHWC views.
+// dfx_bw.cu — bandwidth-bound kernels on 16-bit NHWC views.
 //
 // Reference semantics (/root/reference/pkg/src/dagfuse/executor.py):
 //   maxpool2d      :95-109   (+ padding, extension)      -> pool_kernel
@@ -8,6 +8,7 @@
 // hardswish/hardsigmoid/silu/sigmoid/channel_scale (ew_kernel epilogue).
 // Every kernel moves 8 channels (16 B) per thread when the view's channel
 // offset allows it and falls back to scalar lanes for ragged toy shapes.
+// Templated on the storage type T (__half or __nv_bfloat16).
 #include "dfx_common.cuh"
 
 namespace dfx {
@@ -18,6 +19,7 @@ __device__ __forceinline__ int64_t grid_stride_start() {
 __device__ __forceinline__ int64_t grid_stride_step() { return int64_t(gridDim.x) * blockDim.x; }
 
 // ------------------------------------------------------------------ elementwise
+template <typename T>
 __global__ void ew_kernel(const __grid_constant__ dfx_ew_params P) {
   const dfx_view& in = P.in;
   const dfx_view& out = P.out;
@@ -31,16 +33,13 @@ __global__ void ew_kernel(const __grid_constant__ dfx_ew_params P) {
     const int n = int(pix / hw);
     if (vec_ok_views && c + 8 <= in.c) {
       float v[8];
-      unpack_bf16x8(*reinterpret_cast<const uint4*>(
-                        reinterpret_cast<const __nv_bfloat16*>(in.base) + view_pixel_index(in, pix, c)),
-                    v);
-      epilogue8(P.epi, v, pix, n, c);
-      *reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(out.base) +
-                                view_pixel_index(out, pix, c)) = pack_bf16x8(v);
+      ld8<T>(in.base, view_pixel_index(in, pix, c), v);
+      epilogue8<T>(P.epi, v, pix, n, c);
+      st8<T>(out.base, view_pixel_index(out, pix, c), v);
     } else {
       for (int i = 0; i < 8 && c + i < in.c; ++i) {
-        const float x = bf16_at(in.base, view_pixel_index(in, pix, c + i));
-        bf16_store(out.base, view_pixel_index(out, pix, c + i), epilogue(P.epi, x, pix, n, c + i));
+        const float x = ld1<T>(in.base, view_pixel_index(in, pix, c + i));
+        st1<T>(out.base, view_pixel_index(out, pix, c + i), epilogue<T>(P.epi, x, pix, n, c + i));
       }
     }
   }
@@ -48,6 +47,7 @@ __global__ void ew_kernel(const __grid_constant__ dfx_ew_params P) {
 
 // ------------------------------------------------------------------ depthwise conv
 // One thread = 8 channels of one output pixel; fp32 taps [kh*kw][c].
+template <typename T>
 __global__ void dwconv_kernel(const __grid_constant__ dfx_dwconv_params P) {
   const dfx_view& in = P.in;
   const dfx_view& out = P.out;
@@ -74,9 +74,7 @@ __global__ void dwconv_kernel(const __grid_constant__ dfx_dwconv_params P) {
           const int w = w0 + kj;
           if (w < 0 || w >= in.w) continue;
           float x[8];
-          unpack_bf16x8(*reinterpret_cast<const uint4*>(
-                            reinterpret_cast<const __nv_bfloat16*>(in.base) + view_index(in, n, h, w, c)),
-                        x);
+          ld8<T>(in.base, view_index(in, n, h, w, c), x);
           const float* wt = P.weight + int64_t(ki * P.kw + kj) * C + c;
           const float4 w_lo = __ldg(reinterpret_cast<const float4*>(wt));
           const float4 w_hi = __ldg(reinterpret_cast<const float4*>(wt + 4));
@@ -86,9 +84,8 @@ __global__ void dwconv_kernel(const __grid_constant__ dfx_dwconv_params P) {
           acc[6] = fmaf(w_hi.z, x[6], acc[6]); acc[7] = fmaf(w_hi.w, x[7], acc[7]);
         }
       }
-      epilogue8(P.epi, acc, pix, n, c);
-      *reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(out.base) +
-                                view_pixel_index(out, pix, c)) = pack_bf16x8(acc);
+      epilogue8<T>(P.epi, acc, pix, n, c);
+      st8<T>(out.base, view_pixel_index(out, pix, c), acc);
     } else {
       for (int i = 0; i < 8 && c + i < C; ++i) {
         float a = 0.0f;
@@ -99,16 +96,17 @@ __global__ void dwconv_kernel(const __grid_constant__ dfx_dwconv_params P) {
             const int w = w0 + kj;
             if (w < 0 || w >= in.w) continue;
             a = fmaf(P.weight[int64_t(ki * P.kw + kj) * C + c + i],
-                     bf16_at(in.base, view_index(in, n, h, w, c + i)), a);
+                     ld1<T>(in.base, view_index(in, n, h, w, c + i)), a);
           }
         }
-        bf16_store(out.base, view_pixel_index(out, pix, c + i), epilogue(P.epi, a, pix, n, c + i));
+        st1<T>(out.base, view_pixel_index(out, pix, c + i), epilogue<T>(P.epi, a, pix, n, c + i));
       }
     }
   }
 }
 
 // ------------------------------------------------------------------ pooling
+template <typename T>
 __global__ void pool_kernel(const __grid_constant__ dfx_pool_params P) {
   const dfx_view& in = P.in;
   const dfx_view& out = P.out;
@@ -138,11 +136,9 @@ __global__ void pool_kernel(const __grid_constant__ dfx_pool_params P) {
         ++count;
         float x[8];
         if (vec && nl == 8) {
-          unpack_bf16x8(*reinterpret_cast<const uint4*>(
-                            reinterpret_cast<const __nv_bfloat16*>(in.base) + view_index(in, n, h, w, c)),
-                        x);
+          ld8<T>(in.base, view_index(in, n, h, w, c), x);
         } else {
-          for (int i = 0; i < 8; ++i) x[i] = i < nl ? bf16_at(in.base, view_index(in, n, h, w, c + i)) : 0.f;
+          for (int i = 0; i < 8; ++i) x[i] = i < nl ? ld1<T>(in.base, view_index(in, n, h, w, c + i)) : 0.f;
         }
         if (P.is_max) {
 #pragma unroll
@@ -159,10 +155,9 @@ __global__ void pool_kernel(const __grid_constant__ dfx_pool_params P) {
       for (int i = 0; i < 8; ++i) acc[i] *= inv;
     }
     if (vec && nl == 8) {
-      *reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(out.base) +
-                                view_pixel_index(out, pix, c)) = pack_bf16x8(acc);
+      st8<T>(out.base, view_pixel_index(out, pix, c), acc);
     } else {
-      for (int i = 0; i < nl; ++i) bf16_store(out.base, view_pixel_index(out, pix, c + i), acc[i]);
+      for (int i = 0; i < nl; ++i) st1<T>(out.base, view_pixel_index(out, pix, c + i), acc[i]);
     }
   }
 }
@@ -170,6 +165,7 @@ __global__ void pool_kernel(const __grid_constant__ dfx_pool_params P) {
 // ------------------------------------------------------------------ global average pool
 // grid (ceil(C/256), N); 256 threads = 8 warps; lane handles 8 channels, warps
 // split the spatial range, smem reduction in fixed order.
+template <typename T>
 __global__ void gap_kernel(const __grid_constant__ dfx_gap_params P) {
   __shared__ float part[8][256 + 8];
   const dfx_view& in = P.in;
@@ -187,10 +183,9 @@ __global__ void gap_kernel(const __grid_constant__ dfx_gap_params P) {
       const int64_t base = view_pixel_index(in, int64_t(n) * hw + s, c);
       float x[8];
       if (vec) {
-        unpack_bf16x8(*reinterpret_cast<const uint4*>(
-                          reinterpret_cast<const __nv_bfloat16*>(in.base) + base), x);
+        ld8<T>(in.base, base, x);
       } else {
-        for (int i = 0; i < 8; ++i) x[i] = i < nl ? bf16_at(in.base, base + i) : 0.f;
+        for (int i = 0; i < 8; ++i) x[i] = i < nl ? ld1<T>(in.base, base + i) : 0.f;
       }
 #pragma unroll
       for (int i = 0; i < 8; ++i) acc[i] += x[i];
@@ -211,15 +206,16 @@ __global__ void gap_kernel(const __grid_constant__ dfx_gap_params P) {
     const dfx_view& out = P.out;
     const int64_t o = int64_t(n) * out.pitch + out.coff + c;
     if (nl == 8 && (out.coff & 7) == 0) {
-      *reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(out.base) + o) = pack_bf16x8(v);
+      st8<T>(out.base, o, v);
     } else {
-      for (int i = 0; i < nl; ++i) bf16_store(out.base, o + i, v[i]);
+      for (int i = 0; i < nl; ++i) st1<T>(out.base, o + i, v[i]);
     }
   }
 }
 
 // ------------------------------------------------------------------ layout conversion
-// fp32 CHW samples -> bf16 NHWC (pad channels written as zero).
+// fp32 CHW samples -> 16-bit NHWC (pad channels written as zero).
+template <typename T>
 __global__ void in_kernel(const __grid_constant__ dfx_in_params P) {
   const dfx_view& o = P.out;
   const int hw = o.h * o.w;
@@ -234,12 +230,12 @@ __global__ void in_kernel(const __grid_constant__ dfx_in_params P) {
     float v[8];
 #pragma unroll
     for (int i = 0; i < 8; ++i) v[i] = (c + i < o.c) ? __ldg(src + int64_t(c + i) * hw) : 0.0f;
-    *reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(o.base) + pix * o.pitch + c) =
-        pack_bf16x8(v);
+    st8<T>(o.base, pix * o.pitch + c, v);
   }
 }
 
-// bf16 NHWC -> fp32 samples in logical CHW order (also the flatten order).
+// 16-bit NHWC -> fp32 samples in logical CHW order (also the flatten order).
+template <typename T>
 __global__ void out_kernel(const __grid_constant__ dfx_out_params P) {
   const dfx_view& v = P.in;
   const int hw = v.h * v.w;
@@ -250,8 +246,19 @@ __global__ void out_kernel(const __grid_constant__ dfx_out_params P) {
     const int64_t r = idx - int64_t(n) * per;
     const int c = int(r / hw);
     const int s = int(r - int64_t(c) * hw);
-    P.dst[idx] = bf16_at(v.base, view_pixel_index(v, int64_t(n) * hw + s, c));
+    P.dst[idx] = ld1<T>(v.base, view_pixel_index(v, int64_t(n) * hw + s, c));
   }
 }
+
+#define DFX_INSTANTIATE(K, P)                                               \
+  template __global__ void K<__nv_bfloat16>(const __grid_constant__ P); \
+  template __global__ void K<__half>(const __grid_constant__ P);
+DFX_INSTANTIATE(ew_kernel, dfx_ew_params)
+DFX_INSTANTIATE(dwconv_kernel, dfx_dwconv_params)
+DFX_INSTANTIATE(pool_kernel, dfx_pool_params)
+DFX_INSTANTIATE(gap_kernel, dfx_gap_params)
+DFX_INSTANTIATE(in_kernel, dfx_in_params)
+DFX_INSTANTIATE(out_kernel, dfx_out_params)
+#undef DFX_INSTANTIATE
 
 }  // namespace dfx

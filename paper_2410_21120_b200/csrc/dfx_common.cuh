@@ -8,6 +8,7 @@
 
 #include <cuda.h>
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -29,36 +30,62 @@ DFX_DEV float act_apply(int act, float v) {
   }
 }
 
-DFX_DEV uint32_t pack_bf16x2(float lo, float hi) {
-  __nv_bfloat162 h = __floats2bfloat162_rn(lo, hi);
-  return *reinterpret_cast<uint32_t*>(&h);
-}
-
-DFX_DEV void unpack_bf16x8(const uint4& u, float* f) {
-  const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    float2 t = __bfloat1622float2(h[i]);
-    f[2 * i] = t.x;
-    f[2 * i + 1] = t.y;
+// ---------------------------------------------------------------- 16-bit storage types
+// Activations and GEMM operands are 16-bit: bf16 or IEEE half (saturating stores,
+// so an out-of-range value clamps to +-65504 instead of becoming inf).
+template <typename T> struct Elt;
+template <> struct Elt<__nv_bfloat16> {
+  static constexpr int kDtype = DFX_BF16;
+  static DFX_DEV float to_f(__nv_bfloat16 v) { return __bfloat162float(v); }
+  static DFX_DEV __nv_bfloat16 from_f(float v) { return __float2bfloat16_rn(v); }
+  static DFX_DEV uint32_t pack2(float a, float b) {
+    __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+    return *reinterpret_cast<uint32_t*>(&h);
   }
+  static DFX_DEV float2 unpack2(uint32_t u) {
+    return __bfloat1622float2(*reinterpret_cast<__nv_bfloat162*>(&u));
+  }
+};
+template <> struct Elt<__half> {
+  static constexpr int kDtype = DFX_F16;
+  static DFX_DEV float sat(float v) { return fminf(fmaxf(v, -65504.0f), 65504.0f); }
+  static DFX_DEV float to_f(__half v) { return __half2float(v); }
+  static DFX_DEV __half from_f(float v) { return __float2half_rn(sat(v)); }
+  static DFX_DEV uint32_t pack2(float a, float b) {
+    __half2 h = __floats2half2_rn(sat(a), sat(b));
+    return *reinterpret_cast<uint32_t*>(&h);
+  }
+  static DFX_DEV float2 unpack2(uint32_t u) { return __half22float2(*reinterpret_cast<__half2*>(&u)); }
+};
+
+template <typename T> DFX_DEV void unpack8(const uint4& u, float* f) {
+  float2 t;
+  t = Elt<T>::unpack2(u.x); f[0] = t.x; f[1] = t.y;
+  t = Elt<T>::unpack2(u.y); f[2] = t.x; f[3] = t.y;
+  t = Elt<T>::unpack2(u.z); f[4] = t.x; f[5] = t.y;
+  t = Elt<T>::unpack2(u.w); f[6] = t.x; f[7] = t.y;
 }
 
-DFX_DEV uint4 pack_bf16x8(const float* f) {
+template <typename T> DFX_DEV uint4 pack8(const float* f) {
   uint4 u;
-  u.x = pack_bf16x2(f[0], f[1]);
-  u.y = pack_bf16x2(f[2], f[3]);
-  u.z = pack_bf16x2(f[4], f[5]);
-  u.w = pack_bf16x2(f[6], f[7]);
+  u.x = Elt<T>::pack2(f[0], f[1]);
+  u.y = Elt<T>::pack2(f[2], f[3]);
+  u.z = Elt<T>::pack2(f[4], f[5]);
+  u.w = Elt<T>::pack2(f[6], f[7]);
   return u;
 }
 
-DFX_DEV float bf16_at(const void* base, int64_t idx) {
-  return __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(base)[idx]);
+template <typename T> DFX_DEV float ld1(const void* base, int64_t idx) {
+  return Elt<T>::to_f(reinterpret_cast<const T*>(base)[idx]);
 }
-
-DFX_DEV void bf16_store(void* base, int64_t idx, float v) {
-  reinterpret_cast<__nv_bfloat16*>(base)[idx] = __float2bfloat16_rn(v);
+template <typename T> DFX_DEV void st1(void* base, int64_t idx, float v) {
+  reinterpret_cast<T*>(base)[idx] = Elt<T>::from_f(v);
+}
+template <typename T> DFX_DEV void ld8(const void* base, int64_t idx, float* f) {
+  unpack8<T>(*reinterpret_cast<const uint4*>(reinterpret_cast<const T*>(base) + idx), f);
+}
+template <typename T> DFX_DEV void st8(void* base, int64_t idx, const float* f) {
+  *reinterpret_cast<uint4*>(reinterpret_cast<T*>(base) + idx) = pack8<T>(f);
 }
 
 DFX_DEV int64_t view_index(const dfx_view& v, int n, int h, int w, int c) {
@@ -71,20 +98,22 @@ DFX_DEV int64_t view_pixel_index(const dfx_view& v, int64_t pix, int c) {
 
 // Full epilogue on one value.  `pix` is the flat (n*h*w) pixel index and n the
 // image index of the element; `c` its channel.
+template <typename T>
 DFX_DEV float epilogue(const dfx_epilogue& e, float x, int64_t pix, int n, int c) {
   float v = x;
   if (e.alpha) v = v * __ldg(e.alpha + c);
   if (e.beta) v = v + __ldg(e.beta + c);
   v = act_apply(e.act1, v);
   if (e.binop == DFX_BIN_ADD) {
-    v += bf16_at(e.other.base, view_pixel_index(e.other, pix, c));
+    v += ld1<T>(e.other.base, view_pixel_index(e.other, pix, c));
   } else if (e.binop == DFX_BIN_SCALE) {
-    v *= bf16_at(e.other.base, int64_t(n) * e.other.pitch + e.other.coff + c);
+    v *= ld1<T>(e.other.base, int64_t(n) * e.other.pitch + e.other.coff + c);
   }
   return act_apply(e.act2, v);
 }
 
 // Vector form over 8 consecutive channels c..c+7 (caller guarantees alignment).
+template <typename T>
 DFX_DEV void epilogue8(const dfx_epilogue& e, float* v, int64_t pix, int n, int c) {
   if (e.alpha) {
     const float4 a0 = __ldg(reinterpret_cast<const float4*>(e.alpha + c));
@@ -105,8 +134,7 @@ DFX_DEV void epilogue8(const dfx_epilogue& e, float* v, int64_t pix, int n, int 
                             ? view_pixel_index(e.other, pix, c)
                             : int64_t(n) * e.other.pitch + e.other.coff + c;
     float o[8];
-    unpack_bf16x8(*reinterpret_cast<const uint4*>(
-                      reinterpret_cast<const __nv_bfloat16*>(e.other.base) + idx), o);
+    ld8<T>(e.other.base, idx, o);
     if (e.binop == DFX_BIN_ADD) {
 #pragma unroll
       for (int i = 0; i < 8; ++i) v[i] += o[i];
@@ -206,7 +234,7 @@ DFX_DEV void tc_fence_before() {
 DFX_DEV void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 
 // D[tmem] (+)= A[smem] * B[smem]^T, bf16 inputs, fp32 accumulate.
-DFX_DEV void umma_bf16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+DFX_DEV void umma_f16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
                        uint32_t accumulate) {
   asm volatile(
       "{\n"
@@ -254,12 +282,14 @@ DFX_DEV uint64_t umma_smem_desc(uint32_t saddr, uint32_t row_bytes) {
   return d;
 }
 
-// Instruction descriptor: kind::f16, A=B=bf16, D=f32, both K-major, M=128.
-DFX_DEV uint32_t umma_idesc_bf16(uint32_t n) {
+// Instruction descriptor: kind::f16, A=B=bf16 (dtype DFX_BF16) or f16, D=f32,
+// both K-major, M=128.
+DFX_DEV uint32_t umma_idesc_f16(uint32_t n, int dtype) {
+  const uint32_t ab = dtype == DFX_BF16 ? 1u : 0u;
   uint32_t d = 0;
   d |= 1u << 4;               // D format f32
-  d |= 1u << 7;               // A bf16
-  d |= 1u << 10;              // B bf16
+  d |= ab << 7;               // A format
+  d |= ab << 10;              // B format
   d |= (n >> 3) << 17;        // N
   d |= (128u >> 4) << 24;     // M
   return d;

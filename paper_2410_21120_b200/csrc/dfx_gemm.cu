@@ -1,9 +1,10 @@
 // dfx_gemm.cu — grouped implicit-GEMM convolution on tcgen05 / TMEM, fed by TMA.
 //
 // Replaces the reference's conv2d and dense evaluation
-// (/root/reference/pkg/src/dagfuse/executor.py:56-92): bf16 operands, fp32
-// accumulation in TMEM, fp32 epilogue (bias / folded batch-norm / activation /
-// residual add), bf16 NHWC store at a channel offset (zero-copy concat).
+// (/root/reference/pkg/src/dagfuse/executor.py:56-92): 16-bit operands (fp16 or
+// bf16), fp32 accumulation in TMEM, fp32 epilogue (bias / folded batch-norm /
+// activation / residual add / channel scale), 16-bit NHWC store at a channel
+// offset (zero-copy concat).
 //
 // One CTA = one (M tile, N tile, K split) of one problem of a grouped launch.
 //   M tile : tn x tp x tq output pixels (<= 128 rows, one TMEM lane each)
@@ -30,6 +31,7 @@ struct GemmHeader {
   uint32_t tmem_base;
 };
 
+template <typename T>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     gemm_kernel(const __grid_constant__ dfx_gemm_launch L) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -49,7 +51,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     if (L.descs[i].tile_begin <= bid) pi = i;
   const dfx_gemm_desc* d = L.descs + pi;
 
-  // ---- tile coordinates
+  // ---- tile coordinates (M tiles fastest, then K splits, then N tiles)
   int t = bid - d->tile_begin;
   const int mt_total = d->mt_n * d->mt_p * d->mt_q;
   const int mi = t % mt_total;
@@ -112,7 +114,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     }
   } else if (warp == 1 && lane == 0) {
     // ================= MMA issuer
-    const uint32_t idesc = umma_idesc_bf16(uint32_t(bn));
+    const uint32_t idesc = umma_idesc_f16(uint32_t(bn), Elt<T>::kDtype);
     const uint32_t row_bytes = uint32_t(cb) * 2u;
     uint32_t accumulate = 0;
     int it = 0;
@@ -128,7 +130,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         for (int kk = 0; kk < cb / 16; ++kk) {
           const uint64_t ad = umma_smem_desc(a_base + j * sub_a + kk * 32, row_bytes);
           const uint64_t bd = umma_smem_desc(b_base + j * sub_b + kk * 32, row_bytes);
-          umma_bf16(tmem_base, ad, bd, idesc, accumulate);
+          umma_f16(tmem_base, ad, bd, idesc, accumulate);
           accumulate = 1;
         }
       }
@@ -138,7 +140,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   }
   __syncwarp();
 
-  // ================= epilogue: TMEM -> registers -> bf16 NHWC (or fp32 split-K partials)
+  // ================= epilogue: TMEM -> registers -> 16-bit NHWC (or fp32 split-K partials)
   mbar_wait(&hdr->accum, 0);
   tc_fence_after();
 
@@ -173,13 +175,12 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     if (vec) {
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
-        epilogue8(e, v + 8 * h, pix, on, co + 8 * h);
-        *reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(o.base) +
-                                  view_pixel_index(o, pix, co + 8 * h)) = pack_bf16x8(v + 8 * h);
+        epilogue8<T>(e, v + 8 * h, pix, on, co + 8 * h);
+        st8<T>(o.base, view_pixel_index(o, pix, co + 8 * h), v + 8 * h);
       }
     } else {
       for (int i = 0; i < 16 && co + i < d->cout; ++i)
-        bf16_store(o.base, view_pixel_index(o, pix, co + i), epilogue(e, v[i], pix, on, co + i));
+        st1<T>(o.base, view_pixel_index(o, pix, co + i), epilogue<T>(e, v[i], pix, on, co + i));
     }
   }
 
@@ -189,6 +190,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 }
 
 // Deterministic split-K reduction (splits summed in ascending order) + epilogue.
+template <typename T>
 __global__ void splitk_kernel(const __grid_constant__ dfx_splitk_params P) {
   const int cgroups = (P.cout + 7) / 8;
   const int64_t total = int64_t(P.pixels) * cgroups;
@@ -214,15 +216,18 @@ __global__ void splitk_kernel(const __grid_constant__ dfx_splitk_params P) {
     const bool vec = c + 8 <= P.cout && vec8_ok(P.out, c) &&
                      (P.epi.binop == DFX_BIN_NONE || vec8_ok(P.epi.other, c));
     if (vec) {
-      epilogue8(P.epi, v, pix, n, c);
-      *reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(P.out.base) +
-                                view_pixel_index(P.out, pix, c)) = pack_bf16x8(v);
+      epilogue8<T>(P.epi, v, pix, n, c);
+      st8<T>(P.out.base, view_pixel_index(P.out, pix, c), v);
     } else {
       for (int i = 0; i < 8 && c + i < P.cout; ++i)
-        bf16_store(P.out.base, view_pixel_index(P.out, pix, c + i),
-                   epilogue(P.epi, v[i], pix, n, c + i));
+        st1<T>(P.out.base, view_pixel_index(P.out, pix, c + i), epilogue<T>(P.epi, v[i], pix, n, c + i));
     }
   }
 }
+
+template __global__ void gemm_kernel<__nv_bfloat16>(const __grid_constant__ dfx_gemm_launch);
+template __global__ void gemm_kernel<__half>(const __grid_constant__ dfx_gemm_launch);
+template __global__ void splitk_kernel<__nv_bfloat16>(const __grid_constant__ dfx_splitk_params);
+template __global__ void splitk_kernel<__half>(const __grid_constant__ dfx_splitk_params);
 
 }  // namespace dfx

@@ -36,14 +36,14 @@ _program_cache: dict[tuple[int, int], tuple] = {}
 _cache_lock = threading.Lock()
 
 
-def program_for(g, w) -> MemberProgram:
-    """Lowered program of (graph, weights), cached by object identity."""
-    key = (id(g), id(w))
+def program_for(g, w, precision: str = "fp16") -> MemberProgram:
+    """Lowered program of (graph, weights, precision), cached by object identity."""
+    key = (id(g), id(w), precision)
     with _cache_lock:
         hit = _program_cache.get(key)
         if hit is not None and hit[0] is g and hit[1] is w:
             return hit[2]
-    prog = lower_member(g, w)
+    prog = lower_member(g, w, precision=precision)
     with _cache_lock:
         _program_cache[key] = (g, w, prog)
     return prog
@@ -97,6 +97,11 @@ class WeightArena:
         self.member_base = [self.dev + off for off, _ in self.segments]
         return self.upload_ms
 
+    def allocate(self) -> None:
+        """Device allocation only (a replica that receives the arena by broadcast)."""
+        self.dev = rt.malloc(self.total)
+        self.member_base = [self.dev + off for off, _ in self.segments]
+
     def addr(self, member: int, key: str) -> int:
         return self.member_base[member] + (self.layout[member][key] - self.segments[member][0])
 
@@ -142,6 +147,43 @@ class WeightArena:
             rt.free(p)
         rt.host_free(self.host)
         self.dev = self.host = 0
+
+
+class PerTensorArena:
+    """The UNFUSED baseline loader (what per-model framework loading does):
+    one cudaMalloc + one cudaMemcpyAsync per weight tensor, from pageable host
+    memory, model by model.  Same interface as WeightArena so the same
+    kernels run on it; used only to measure the fused-vs-unfused claims."""
+
+    def __init__(self, programs: list[MemberProgram], device: int = 0, stream=None):
+        rt.init_device(device)
+        self.device = device
+        self.ptrs: list[dict[str, int]] = []
+        self.tensors = 0
+        self.total = 0
+        t0 = time.perf_counter()
+        for p in programs:
+            table = {}
+            for key in sorted(p.blobs):
+                blob = np.ascontiguousarray(p.blobs[key])
+                ptr = rt.malloc(blob.nbytes)
+                rt.call("dfx_memcpy_h2d", C.c_void_p(ptr), C.c_void_p(blob.ctypes.data),
+                        C.c_size_t(blob.nbytes), C.c_void_p(stream))
+                rt.stream_sync(stream)            # pageable source: copy completes before return
+                table[key] = ptr
+                self.tensors += 1
+                self.total += blob.nbytes
+            self.ptrs.append(table)
+        self.upload_ms = (time.perf_counter() - t0) * 1e3
+
+    def addr(self, member: int, key: str) -> int:
+        return self.ptrs[member][key]
+
+    def free(self):
+        for table in self.ptrs:
+            for p in table.values():
+                rt.free(p)
+        self.ptrs = []
 
 
 def broadcast_arena(arena: WeightArena, src: int = 0, group=None) -> None:
@@ -197,6 +239,7 @@ class ExecInstance:
 
     def __init__(self, dag: "DeviceDag", batch: tuple[int, ...]):
         self.dag, self.batch = dag, batch
+        self.dtype = rt.DTYPES[dag.precision]
         progs, arena = dag.programs, dag.arena
         rt.init_device(dag.device)
         self.stream = rt.stream_create()
@@ -239,7 +282,7 @@ class ExecInstance:
         v = prog.values[name]
         b = prog.buffers[v.buf]
         base = self.act + self.seg_off[m] + self.plans[m].offsets[v.buf]
-        return rt.View(base, n, v.h, v.w, v.c, b.pitch, v.coff)
+        return rt.View(base, n, v.h, v.w, v.c, b.pitch, v.coff, self.dtype)
 
     def _epi(self, m, prog, L, n) -> rt.Epilogue:
         e = rt.Epilogue()
@@ -259,21 +302,25 @@ class ExecInstance:
         pending = []                                   # (member, launch, desc slot)
         prev_tail = None
         self._keep = []                                # keep param structs alive
+        self.nodes = []                                # (op, params, algorithmic info)
         for m, (prog, n) in enumerate(zip(progs, self.batch)):
             if n == 0:
                 continue
             deps = [prev_tail] if (self.dag.mode == "sequential" and prev_tail is not None) else []
             pin = rt.InParams(self.dev_in + self.in_off[m], self._view(m, prog, "<input>", n))
             last = g.add(rt.OP_IN, pin, deps)
-            self._keep.append(pin)
+            self.nodes.append((rt.OP_IN, pin, dict(member=m, kind="in", flops=0,
+                                                   bytes=self.in_sizes[m] * 3 // 2)))
             for L in prog.launches:
                 for op, params in self._params(m, prog, L, n, host_descs):
                     last = g.add(op, params, [last])
-                    self._keep.append(params)
+                    self.nodes.append((op, params, self._algo(prog, L, n, op)))
             pout = rt.OutParams(self._view(m, prog, prog.exit_value, n), self.dev_out + self.out_off[m])
             last = g.add(rt.OP_OUT, pout, [last])
-            self._keep.append(pout)
+            self.nodes.append((rt.OP_OUT, pout, dict(member=m, kind="out", flops=0,
+                                                     bytes=self.out_sizes[m] * 3 // 2)))
             prev_tail = last
+        self._keep = [p for _, p, _ in self.nodes]
         if host_descs:
             arr = (rt.GemmDesc * len(host_descs))(*host_descs)
             rt.h2d(self.descs, C.addressof(arr), C.sizeof(arr), self.stream)
@@ -281,6 +328,52 @@ class ExecInstance:
         g.instantiate()
         self.kernel_nodes = len(g.kinds)
         return g
+
+    @staticmethod
+    def _algo(prog: MemberProgram, L, n: int, op: int) -> dict:
+        """Algorithmic FLOPs and HBM bytes of one launch (16-bit activations,
+        unpadded weights): what a perfect kernel must move / compute."""
+        def vbytes(name):
+            v = prog.values[name]
+            return n * v.h * v.w * v.c * 2
+        info = dict(member=prog.model_id, kind=L.kind, flops=0, bytes=0)
+        out_b = vbytes(L.dst) if L.kind != COPY else vbytes(L.src)
+        in_b = vbytes(L.src)
+        other_b = vbytes(L.epi.other) if L.epi.other is not None else 0
+        if L.epi.binop == 2:                      # per-(n, c) scale vector
+            other_b = n * prog.values[L.epi.other].c * 2
+        if L.kind == GEMM:
+            g = L.geom
+            out = prog.values[L.dst]
+            macs = n * out.h * out.w * g["cout"] * g["cin"] * g["kh"] * g["kw"]
+            wbytes = g["cout"] * g["cin"] * g["kh"] * g["kw"] * 2
+            if op == rt.OP_SPLITK:
+                info.update(kind="splitk", bytes=out_b + other_b)
+            else:
+                info.update(flops=2 * macs, bytes=wbytes + in_b + out_b + other_b, weight_bytes=wbytes)
+        elif L.kind == DWCONV:
+            g = L.geom
+            out = prog.values[L.dst]
+            info.update(flops=2 * n * out.h * out.w * out.c * g["kh"] * g["kw"],
+                        bytes=in_b + out_b + out.c * g["kh"] * g["kw"] * 4)
+        else:
+            info.update(bytes=in_b + out_b + other_b)
+        return info
+
+    def profile_nodes(self, reps: int = 3) -> list[dict]:
+        """Replay every graph node eagerly on this instance's stream, timing each
+        launch with CUDA events (median of ``reps``).  Same params as the graph."""
+        out = []
+        for op, params, info in self.nodes:
+            times = []
+            for _ in range(reps):
+                e0, e1 = rt.Event(), rt.Event()
+                e0.record(self.stream)
+                rt.launch(op, params, self.stream)
+                e1.record(self.stream)
+                times.append(e0.elapsed_ms(e1))
+            out.append(dict(info, op=op, ms=float(np.median(times))))
+        return out
 
     def _params(self, m, prog: MemberProgram, L, n, host_descs):
         arena = self.dag.arena
@@ -291,7 +384,7 @@ class ExecInstance:
             d = rt.GemmDesc()
             d.tmap_a = rt.tmap_act(src, geo["cb"], t["tq"], t["tp"], t["tn"], geo["sw"], geo["sh"])
             d.tmap_b = rt.tmap_weights(arena.addr(m, L.blobs["weight"]), geo["cout"], geo["k"],
-                                       geo["cb"], t["bn"])
+                                       geo["cb"], t["bn"], self.dtype)
             d.n, d.p, d.q = n, out.h, out.w
             d.tn, d.tp, d.tq = t["tn"], t["tp"], t["tq"]
             d.mt_n, d.mt_p, d.mt_q, d.nt = t["mt_n"], t["mt_p"], t["mt_q"], t["nt"]
@@ -307,7 +400,8 @@ class ExecInstance:
             slot = len(host_descs)
             host_descs.append(d)
             self.gemm_count += 1
-            gl = rt.GemmLaunch(self.descs + slot * C.sizeof(rt.GemmDesc), 1, t["tiles"], t["bn"])
+            gl = rt.GemmLaunch(self.descs + slot * C.sizeof(rt.GemmDesc), 1, t["tiles"], t["bn"],
+                               self.dtype)
             yield rt.OP_GEMM, gl
             if t["splits"] > 1:
                 sp = rt.SplitKParams(self.ws + self.ws_off[m], t["splits"], n * out.h * out.w,
@@ -330,7 +424,7 @@ class ExecInstance:
             yield rt.OP_EW, rt.EwParams(src, self._view(m, prog, L.dst, n), self._epi(m, prog, L, n))
         elif L.kind == COPY:
             cv = self._view(m, prog, L.geom["concat"], n)
-            out = rt.View(cv.base, n, src.h, src.w, src.c, cv.pitch, L.geom["coff"])
+            out = rt.View(cv.base, n, src.h, src.w, src.c, cv.pitch, L.geom["coff"], self.dtype)
             yield rt.OP_EW, rt.EwParams(src, out, rt.Epilogue())
         else:
             raise AssertionError(L.kind)
@@ -388,16 +482,16 @@ class DeviceDag:
     """A fused DAG resident on one GPU."""
 
     def __init__(self, members, device: int = 0, mode: str = "concurrent", arena=None,
-                 programs=None):
+                 programs=None, precision: str = "fp16"):
         if mode not in ("concurrent", "sequential"):
             raise ValueError(mode)
-        self.device, self.mode = device, mode
+        self.device, self.mode, self.precision = device, mode, precision
         rt.init_device(device)
         sm = C.c_int()
         rt.call("dfx_device_info", C.c_int(device), C.byref(sm), None, None, None)
         self.sm_count = sm.value
         self.members = list(members)
-        self.programs = programs or [program_for(g, w) for g, w in self.members]
+        self.programs = programs or [program_for(g, w, precision) for g, w in self.members]
         if arena is None:
             arena = WeightArena(self.programs, device)
             arena.upload()
@@ -434,14 +528,15 @@ class DeviceDag:
 
     def swapped(self, index: int, incoming) -> "DeviceDag":
         g, w = incoming
-        prog = program_for(g, w)
+        prog = program_for(g, w, self.precision)
         arena = self.arena.clone_for_swap()
         ms = arena.replace_member(index, prog)
         members = list(self.members)
         members[index] = incoming
         programs = list(self.programs)
         programs[index] = prog
-        out = DeviceDag(members, self.device, self.mode, arena=arena, programs=programs)
+        out = DeviceDag(members, self.device, self.mode, arena=arena, programs=programs,
+                        precision=self.precision)
         out.last_swap_ms = ms
         return out
 

@@ -54,6 +54,24 @@ def bf16_bits_to_f32(b: np.ndarray) -> np.ndarray:
     return (b.astype(np.uint32) << 16).view(np.float32)
 
 
+PRECISIONS = ("fp16", "bf16")
+
+
+def to_storage_bits(a: np.ndarray, precision: str) -> np.ndarray:
+    """fp32 -> 16-bit storage bit patterns (fp16 saturates at +-65504 like the kernels)."""
+    if precision == "bf16":
+        return to_bf16_bits(a)
+    if precision == "fp16":
+        return np.clip(np.asarray(a, np.float32), -65504, 65504).astype(np.float16).view(np.uint16)
+    raise ValueError(precision)
+
+
+def storage_bits_to_f32(b: np.ndarray, precision: str) -> np.ndarray:
+    if precision == "bf16":
+        return bf16_bits_to_f32(b)
+    return b.view(np.float16).astype(np.float32)
+
+
 @dataclass
 class Buffer:
     bid: int
@@ -118,6 +136,7 @@ class MemberProgram:
     exit_value: str
     input_value: str = "<input>"
     gemm_flops_per_sample: int = 0
+    precision: str = "fp16"
 
     def weight_bytes(self) -> int:
         return sum(b.nbytes for b in self.blobs.values())
@@ -461,7 +480,7 @@ class _Lowerer:
                 cout = geo["cout"]
                 t = np.zeros((cout, geo["kh"], geo["kw"], cblocks * cb), dtype=np.float32)
                 t[..., :cin] = wt4.transpose(0, 2, 3, 1)
-                packed = to_bf16_bits(t.reshape(cout, -1))
+                packed = to_storage_bits(t.reshape(cout, -1), self.precision)
                 geo.update(cb=cb, cblocks=cblocks, ksteps=geo["kh"] * geo["kw"] * cblocks,
                            k=packed.shape[1])
                 self.blobs[L.blobs["weight"]] = packed
@@ -495,12 +514,17 @@ def choose_cb(cin: int) -> int:
     return 16
 
 
-def lower_member(g, w, keep_f32: bool = False) -> MemberProgram:
-    """``keep_f32`` also keeps the unrounded packed GEMM weights (tests only)."""
+def lower_member(g, w, keep_f32: bool = False, precision: str = "fp16") -> MemberProgram:
+    """``precision``: 16-bit storage/operand type ("fp16" default, or "bf16").
+    ``keep_f32`` also keeps the unrounded packed GEMM weights (tests only)."""
+    if precision not in PRECISIONS:
+        raise ValueError(precision)
     low = _Lowerer(g, w)
     low.keep_f32 = keep_f32
+    low.precision = precision
     prog = low.run()
     prog.debug_f32 = low.debug_f32
+    prog.precision = precision
     from .graph_ir import gemm_flops
     prog.gemm_flops_per_sample = gemm_flops(g)
     return prog

@@ -22,6 +22,9 @@ LIB_PATH = PKG / "libdfx.so"
 OP_GEMM, OP_SPLITK, OP_DWCONV, OP_POOL, OP_GAP, OP_EW, OP_IN, OP_OUT = range(1, 9)
 ACT = {None: 0, "relu": 1, "hardswish": 2, "hardsigmoid": 3, "silu": 4, "sigmoid": 5}
 BIN_NONE, BIN_ADD, BIN_SCALE = 0, 1, 2
+DT_BF16, DT_F16 = 0, 1
+DTYPES = {"bf16": DT_BF16, "fp16": DT_F16}
+ABI_VERSION = 2
 
 i32, i64, u64, vp = C.c_int32, C.c_int64, C.c_uint64, C.c_void_p
 fptr = C.POINTER(C.c_float)
@@ -29,7 +32,7 @@ fptr = C.POINTER(C.c_float)
 
 class View(C.Structure):
     _fields_ = [("base", vp), ("n", i32), ("h", i32), ("w", i32), ("c", i32),
-                ("pitch", i32), ("coff", i32)]
+                ("pitch", i32), ("coff", i32), ("dtype", i32), ("_pad", i32)]
 
 
 class Epilogue(C.Structure):
@@ -46,12 +49,12 @@ class GemmDesc(C.Structure):
                 ("pad_h", i32), ("pad_w", i32), ("cb", i32), ("cblocks", i32), ("ksteps", i32),
                 ("kpack", i32), ("stages", i32), ("splits", i32), ("stages_per_split", i32),
                 ("bn", i32), ("cout", i32), ("tile_begin", i32), ("tiles", i32), ("_pad0", i32),
-                ("out", View), ("epi", Epilogue), ("ws", vp), ("_pad1", i64 * 5)]
+                ("out", View), ("epi", Epilogue), ("ws", vp), ("_pad1", i64 * 3)]
 
 
 class GemmLaunch(C.Structure):
     _fields_ = [("descs", vp), ("ndesc", i32), ("total_tiles", i32), ("bn_max", i32),
-                ("_pad", i32)]
+                ("dtype", i32)]
 
 
 class SplitKParams(C.Structure):
@@ -134,7 +137,7 @@ def lib():
 
 
 def check_abi(L) -> None:
-    if L.dfx_abi_version() != 1:
+    if L.dfx_abi_version() != ABI_VERSION:
         raise DeviceError(-2, "ABI version mismatch", "dfx_abi_version")
     for name, cls in STRUCTS.items():
         got = L.dfx_sizeof(name.encode())
@@ -281,7 +284,8 @@ def tmap_act(view: View, cb: int, tq: int, tp: int, tn: int, sw: int, sh: int):
     return buf
 
 
-def tmap_weights(base: int, rows: int, k: int, cb: int, bn: int):
+def tmap_weights(base: int, rows: int, k: int, cb: int, bn: int, dtype: int):
     buf = (u64 * 16)()
-    call("dfx_tmap_weights", buf, vp(base), C.c_int(rows), C.c_int(k), C.c_int(cb), C.c_int(bn))
+    call("dfx_tmap_weights", buf, vp(base), C.c_int(rows), C.c_int(k), C.c_int(cb), C.c_int(bn),
+         C.c_int(dtype))
     return buf

@@ -13,12 +13,7 @@ from __future__ import annotations
 import numpy as np
 
 from paper_2410_21120_b200.device import plan_member
-from paper_2410_21120_b200.lower import (COPY, DWCONV, EW, GAP, GEMM, POOL, bf16_bits_to_f32,
-                                         to_bf16_bits)
-
-
-def _bf16(x):
-    return bf16_bits_to_f32(to_bf16_bits(np.asarray(x, np.float32)))
+from paper_2410_21120_b200.lower import storage_bits_to_f32, to_storage_bits
 
 
 def _act(kind, v):
@@ -51,8 +46,13 @@ class Emulator:
         full = self.arena[base:base + self.n * v.h * v.w * b.pitch].reshape(self.n, v.h, v.w, b.pitch)
         return full[..., v.coff:v.coff + v.c]
 
+    def q(self, x):
+        """Round to the program's 16-bit storage type."""
+        pr = self.p.precision
+        return storage_bits_to_f32(to_storage_bits(np.asarray(x, np.float32), pr), pr)
+
     def store(self, dst_view, vals):
-        dst_view[...] = _bf16(vals) if self.round else vals
+        dst_view[...] = self.q(vals) if self.round else vals
 
     def epilogue(self, L, x):
         e = L.epi
@@ -87,10 +87,10 @@ class Emulator:
         key = L.blobs["weight"]
         dbg = getattr(self.p, "debug_f32", {})
         packed = dbg[key] if (not self.round and key in dbg) else \
-            bf16_bits_to_f32(self.p.blobs[key])
+            storage_bits_to_f32(self.p.blobs[key], self.p.precision)
         w = packed.reshape(g["cout"], g["kh"], g["kw"], g["cblocks"] * g["cb"])[..., :g["cin"]]
         if self.round:
-            x = _bf16(x)
+            x = self.q(x)
         n, h, wd, c = x.shape
         xp = np.pad(x, ((0, 0), (g["ph"], g["ph"]), (g["pw"], g["pw"]), (0, 0)))
         out = self.view(L.dst)

@@ -1,10 +1,10 @@
 """GPU parity: the sm_100a path (through libdfx) against the CPU oracle.
 
-Tolerance (north star): per sample ||gpu - ref||inf / ||ref||inf <= 2e-2.
-The toy corpus has a few random-init models whose bf16 error exceeds that
-(see test_lowering_cpu.py: the same margin shows up in the CPU emulation of
-the lowered program), so it is held to >= 97% of models at 2e-2 and every
-model at 6e-2; single layers and the zoo are held to 2e-2 each.
+Tolerance (north star): per sample ||gpu - ref||inf / ||ref||inf <= 2e-2 for
+every model at the default fp16 storage.  With bf16 storage a few random-init
+toy models exceed it (the CPU emulation of the lowered program shows the same
+margin, test_lowering_cpu.py), so the bf16 run is held to >= 97% of models at
+2e-2 and every model at 6e-2.
 """
 
 import threading
@@ -137,6 +137,24 @@ def test_corpus_fused_vs_reference_and_solo(corpus, corpus_golden):
                 solo = run(g, w, inputs[g.model_id])
                 assert np.array_equal(solo.values, outs[g.model_id].values), g.model_id
     errs = np.array(errs)
+    assert errs.max() <= TOL, np.sort(errs)[-8:]
+
+
+def test_corpus_bf16_storage(corpus, corpus_golden):
+    errs = []
+    n_groups = int(corpus_golden["n_groups"])
+    for gi in range(n_groups):
+        members = [int(i) for i in corpus_golden[f"group{gi}.members"]]
+        dag = fuse.fuse_models([corpus[i] for i in members], validate=False)
+        fuse.load_fused(dag, precision="bf16")
+        inputs = {corpus[i][0].model_id: Tensor(corpus[i][0].input_spec,
+                                                golden_input(corpus[i][0].input_spec.dims, 7919 * i))
+                  for i in members}
+        outs = fuse.execute_fused(dag, inputs)
+        for i in members:
+            mid = corpus[i][0].model_id
+            errs.append(rel([outs[mid].values], [corpus_golden[f"{mid}.y"][0]]))
+    errs = np.array(errs)
     assert (errs <= TOL).mean() >= 0.97, np.sort(errs)[-8:]
     assert errs.max() < TOY_MAX
 
@@ -170,7 +188,7 @@ def test_swap_subgraph_on_device(corpus):
     for g, w in (models[0], models[2], models[3]):
         assert np.array_equal(before[g.model_id].values, after[g.model_id].values)
     ref = run_faithful(incoming[0], incoming[1], inputs2[incoming[0].model_id].values)
-    assert rel([after[incoming[0].model_id].values], [ref]) < TOY_MAX
+    assert rel([after[incoming[0].model_id].values], [ref]) < TOL
     # the pre-swap DAG still answers correctly (re-loaded on demand)
     again = fuse.execute_fused(dag, inputs)
     for g, _ in models:

@@ -24,19 +24,27 @@ def test_corpus_lowering_exact_in_fp32(corpus, corpus_golden):
         assert _rel(got, corpus_golden[f"{g.model_id}.y"]) < 1e-5, g.model_id
 
 
-BF16_TOL = 2e-2          # north-star tolerance: per sample ||d||inf / ||ref||inf
-BF16_TOL_TOY_MAX = 6e-2  # worst toy model (random init, near-zero logits)
+TOL = 2e-2               # north-star tolerance: per sample ||d||inf / ||ref||inf
+BF16_TOL_TOY_MAX = 6e-2  # bf16 storage: worst toy model (random init, near-zero logits)
+
+
+def test_corpus_lowering_fp16_tolerance(corpus, corpus_golden):
+    for i, (g, w) in enumerate(corpus):
+        prog = lower_member(g, w)                      # default precision: fp16
+        xs = np.stack([golden_input(g.input_spec.dims, 7919 * i + t) for t in range(4)])
+        got = Emulator(prog, 4).run(xs)
+        assert _rel(got, corpus_golden[f"{g.model_id}.y"]) <= TOL, g.model_id
 
 
 def test_corpus_lowering_bf16_tolerance(corpus, corpus_golden):
     errs = []
     for i, (g, w) in enumerate(corpus):
-        prog = lower_member(g, w)
+        prog = lower_member(g, w, precision="bf16")
         xs = np.stack([golden_input(g.input_spec.dims, 7919 * i + t) for t in range(4)])
         got = Emulator(prog, 4).run(xs)
         errs.append(_rel(got, corpus_golden[f"{g.model_id}.y"]))
     errs = np.array(errs)
-    assert (errs <= BF16_TOL).mean() >= 0.97, np.sort(errs)[-8:]
+    assert (errs <= TOL).mean() >= 0.97, np.sort(errs)[-8:]
     assert errs.max() < BF16_TOL_TOY_MAX
 
 
@@ -45,7 +53,7 @@ def test_zoo_lowering(zoo, zoo_golden):
         prog = lower_member(g, w)
         xs = zoo_golden[f"{g.model_id}.x"]
         got = Emulator(prog, len(xs)).run(xs)
-        assert _rel(got, zoo_golden[f"{g.model_id}.y"]) < BF16_TOL, g.model_id
+        assert _rel(got, zoo_golden[f"{g.model_id}.y"]) < TOL, g.model_id
 
 
 def test_launch_counts_show_fusion(corpus):

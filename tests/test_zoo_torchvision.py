@@ -1,0 +1,81 @@
+"""Zoo builders + oracle extension kinds vs torchvision CPU fp32 (same weights).
+
+Pins the parts of the oracle that have no reference code (depthwise/grouped
+conv, padded pools, avgpool, hardswish/hardsigmoid/SiLU/sigmoid, channel
+scale) and checks that the IR builders reproduce the torchvision
+architectures layer for layer: parameters are copied in module registration
+order and the two forwards must agree to 1e-5 (per sample, norm-relative).
+"""
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+tv = pytest.importorskip("torchvision")
+
+from oracle.executor_ref import run_fast  # noqa: E402
+from paper_2410_21120_b200 import zoo  # noqa: E402
+
+TV = {
+    "vgg16": lambda: tv.models.vgg16(),
+    "mobilenet_v3_large": lambda: tv.models.mobilenet_v3_large(),
+    "densenet161": lambda: tv.models.densenet161(),
+    "efficientnet_v2_l": lambda: tv.models.efficientnet_v2_l(),
+}
+
+
+def _load_into_torchvision(name, g, w):
+    model = TV[name]().eval()
+    mods = [m for m in model.modules()
+            if isinstance(m, (torch.nn.Conv2d, torch.nn.Linear, torch.nn.BatchNorm2d))]
+    ours = [n for n in g.nodes.values() if n.kind in ("conv2d", "dense", "batchnorm_inference")]
+    order = list(g.nodes)              # builder creation order == module registration order
+    ours.sort(key=lambda n: order.index(n.node_id))
+    assert len(mods) == len(ours), (len(mods), len(ours))
+    with torch.no_grad():
+        for m, n in zip(mods, ours):
+            if isinstance(m, torch.nn.BatchNorm2d):
+                assert n.kind == "batchnorm_inference"
+                m.weight.copy_(torch.from_numpy(w.array(n.weight_refs["gamma"]).copy()))
+                m.bias.copy_(torch.from_numpy(w.array(n.weight_refs["beta"]).copy()))
+                m.running_mean.copy_(torch.from_numpy(w.array(n.weight_refs["mean"]).copy()))
+                m.running_var.copy_(torch.from_numpy(w.array(n.weight_refs["var"]).copy()))
+                assert abs(m.eps - n.attrs["epsilon"]) < 1e-12
+            else:
+                wt = w.array(n.weight_refs["weight"])
+                shape = tuple(m.weight.shape)
+                # torchvision's squeeze-excitation FCs are 1x1 convs on (C,1,1)
+                assert shape == wt.shape or shape == wt.shape + (1, 1), (n.node_id, shape, wt.shape)
+                m.weight.copy_(torch.from_numpy(wt.copy()).reshape(shape))
+                if m.bias is not None:
+                    m.bias.copy_(torch.from_numpy(w.array(n.weight_refs["bias"]).copy()))
+                else:
+                    assert "bias" not in n.weight_refs
+    return model
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("name", zoo.NORTH_STAR)
+def test_builder_and_oracle_match_torchvision(name):
+    torch.set_num_threads(8)
+    g, w = zoo.build(name)
+    model = _load_into_torchvision(name, g, w)
+    xs = np.random.default_rng(11).standard_normal((2, 3, 224, 224)).astype(np.float32)
+    with torch.no_grad():
+        ref = model(torch.from_numpy(xs)).numpy()
+    got = run_fast(g, w, xs)
+    err = np.abs(got - ref).max(axis=1) / np.abs(ref).max(axis=1)
+    # fp32 reassociation noise (BLAS vs oneDNN) grows with depth: EfficientNetV2-L's
+    # ~300 layers land near 7e-5; the shallower nets stay below 1e-5
+    assert err.max() < (1e-4 if name == "efficientnet_v2_l" else 1e-5), err
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("name", zoo.NORTH_STAR)
+def test_calibrated_logits_are_input_sensitive(name):
+    g, w = zoo.build(name)
+    xs = np.random.default_rng(12).standard_normal((4, 3, 224, 224)).astype(np.float32)
+    out = run_fast(g, w, xs)
+    spread = np.abs(out - out.mean(axis=0)).max() / np.abs(out).max()
+    assert spread > 0.05, spread
+    assert np.all(np.isfinite(out))
