@@ -322,7 +322,7 @@ def run_ours(args, world, rank, local_rank):
         return
 
     # ---------------- per-kernel-class roofline (eager replay, CUDA events per launch)
-    prof = inst.profile_nodes(reps=3)
+    prof = inst.profile_nodes(reps=8)
     classes = {}
     for r in prof:
         c = classes.setdefault(r["kind"], {"ms": 0.0, "bytes": 0, "flops": 0, "launches": 0})

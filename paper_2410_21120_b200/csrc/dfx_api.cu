@@ -175,6 +175,12 @@ struct Graph {
   cudaGraph_t g = nullptr;
   cudaGraphExec_t exec = nullptr;
   std::vector<cudaGraphNode_t> nodes;
+  // programmatic dependent launch between nodes; DFX_PDL=0 in the environment
+  // turns it off (A/B measurements)
+  bool pdl = [] {
+    const char* e = getenv("DFX_PDL");
+    return !(e && e[0] == '0');
+  }();
 };
 
 }  // namespace
@@ -411,7 +417,20 @@ int dfx_graph_add(void* graph, int op, const void* params, size_t params_size, c
   kp.sharedMemBytes = unsigned(c.smem);
   kp.kernelParams = args;
   cudaGraphNode_t node;
-  CK(cudaGraphAddKernelNode(&node, g->g, dn.data(), dn.size(), &kp));
+  if (g->pdl && !dn.empty()) {
+    // programmatic edges: the node may launch once every predecessor block has
+    // called griddepcontrol.launch_dependents; it griddepcontrol.wait()s for
+    // their completion before touching activations (see dfx_common.cuh)
+    CK(cudaGraphAddKernelNode(&node, g->g, nullptr, 0, &kp));
+    for (cudaGraphNode_t from : dn) {
+      cudaGraphEdgeData ed = {};
+      ed.from_port = cudaGraphKernelNodePortProgrammatic;
+      ed.type = cudaGraphDependencyTypeProgrammatic;
+      CK(cudaGraphAddDependencies_v2(g->g, &from, &node, &ed, 1));
+    }
+  } else {
+    CK(cudaGraphAddKernelNode(&node, g->g, dn.data(), dn.size(), &kp));
+  }
   g->nodes.push_back(node);
   if (node_id) *node_id = int(g->nodes.size()) - 1;
   return DFX_OK;

@@ -21,6 +21,8 @@ __device__ __forceinline__ int64_t grid_stride_step() { return int64_t(gridDim.x
 // ------------------------------------------------------------------ elementwise
 template <typename T>
 __global__ void ew_kernel(const __grid_constant__ dfx_ew_params P) {
+  griddep_wait();
+  griddep_launch();
   const dfx_view& in = P.in;
   const dfx_view& out = P.out;
   const int cg = (in.c + 7) / 8;
@@ -49,6 +51,8 @@ __global__ void ew_kernel(const __grid_constant__ dfx_ew_params P) {
 // One thread = 8 channels of one output pixel; fp32 taps [kh*kw][c].
 template <typename T>
 __global__ void dwconv_kernel(const __grid_constant__ dfx_dwconv_params P) {
+  griddep_wait();
+  griddep_launch();
   const dfx_view& in = P.in;
   const dfx_view& out = P.out;
   const int C = in.c;
@@ -108,6 +112,8 @@ __global__ void dwconv_kernel(const __grid_constant__ dfx_dwconv_params P) {
 // ------------------------------------------------------------------ pooling
 template <typename T>
 __global__ void pool_kernel(const __grid_constant__ dfx_pool_params P) {
+  griddep_wait();
+  griddep_launch();
   const dfx_view& in = P.in;
   const dfx_view& out = P.out;
   const int C = in.c;
@@ -167,6 +173,8 @@ __global__ void pool_kernel(const __grid_constant__ dfx_pool_params P) {
 // split the spatial range, smem reduction in fixed order.
 template <typename T>
 __global__ void gap_kernel(const __grid_constant__ dfx_gap_params P) {
+  griddep_wait();
+  griddep_launch();
   __shared__ float part[8][256 + 8];
   const dfx_view& in = P.in;
   const int n = blockIdx.y;
@@ -217,6 +225,8 @@ __global__ void gap_kernel(const __grid_constant__ dfx_gap_params P) {
 // fp32 CHW samples -> 16-bit NHWC (pad channels written as zero).
 template <typename T>
 __global__ void in_kernel(const __grid_constant__ dfx_in_params P) {
+  griddep_wait();
+  griddep_launch();
   const dfx_view& o = P.out;
   const int hw = o.h * o.w;
   const int cgp = o.pitch / 8;                 // channel groups incl. padding
@@ -237,6 +247,8 @@ __global__ void in_kernel(const __grid_constant__ dfx_in_params P) {
 // 16-bit NHWC -> fp32 samples in logical CHW order (also the flatten order).
 template <typename T>
 __global__ void out_kernel(const __grid_constant__ dfx_out_params P) {
+  griddep_wait();
+  griddep_launch();
   const dfx_view& v = P.in;
   const int hw = v.h * v.w;
   const int64_t per = int64_t(v.c) * hw;

@@ -30,6 +30,34 @@ DFX_DEV float act_apply(int act, float v) {
   }
 }
 
+// Activation over 8 values with the switch hoisted out of the element loop.
+DFX_DEV void act8(int act, float* v) {
+  switch (act) {
+    case DFX_ACT_RELU:
+#pragma unroll
+      for (int i = 0; i < 8; ++i) v[i] = fmaxf(v[i], 0.0f);
+      break;
+    case DFX_ACT_HARDSWISH:
+#pragma unroll
+      for (int i = 0; i < 8; ++i) v[i] = v[i] * fminf(fmaxf(v[i] + 3.0f, 0.0f), 6.0f) / 6.0f;
+      break;
+    case DFX_ACT_HARDSIGMOID:
+#pragma unroll
+      for (int i = 0; i < 8; ++i) v[i] = fminf(fmaxf(v[i] + 3.0f, 0.0f), 6.0f) / 6.0f;
+      break;
+    case DFX_ACT_SILU:
+#pragma unroll
+      for (int i = 0; i < 8; ++i) v[i] = v[i] / (1.0f + __expf(-v[i]));
+      break;
+    case DFX_ACT_SIGMOID:
+#pragma unroll
+      for (int i = 0; i < 8; ++i) v[i] = 1.0f / (1.0f + __expf(-v[i]));
+      break;
+    default:
+      break;
+  }
+}
+
 // ---------------------------------------------------------------- 16-bit storage types
 // Activations and GEMM operands are 16-bit: bf16 or IEEE half (saturating stores,
 // so an out-of-range value clamps to +-65504 instead of becoming inf).
@@ -127,8 +155,7 @@ DFX_DEV void epilogue8(const dfx_epilogue& e, float* v, int64_t pix, int n, int 
     v[0] += b0.x; v[1] += b0.y; v[2] += b0.z; v[3] += b0.w;
     v[4] += b1.x; v[5] += b1.y; v[6] += b1.z; v[7] += b1.w;
   }
-#pragma unroll
-  for (int i = 0; i < 8; ++i) v[i] = act_apply(e.act1, v[i]);
+  act8(e.act1, v);
   if (e.binop != DFX_BIN_NONE) {
     const int64_t idx = e.binop == DFX_BIN_ADD
                             ? view_pixel_index(e.other, pix, c)
@@ -143,12 +170,33 @@ DFX_DEV void epilogue8(const dfx_epilogue& e, float* v, int64_t pix, int n, int 
       for (int i = 0; i < 8; ++i) v[i] *= o[i];
     }
   }
-#pragma unroll
-  for (int i = 0; i < 8; ++i) v[i] = act_apply(e.act2, v[i]);
+  act8(e.act2, v);
+}
+
+// Scalar epilogue + store of `count` (<= 16) consecutive channels starting at c.
+// Out of line on purpose: it only serves ragged channel tails / unaligned
+// concat offsets, and inlining it per column bloats every kernel's I-cache
+// footprint (measured: stalled_no_instructions dominated small GEMMs).
+template <typename T>
+__device__ __noinline__ void epilogue_store_tail(const dfx_epilogue& e, const dfx_view& o,
+                                                 const float* v, int64_t pix, int n, int c,
+                                                 int count) {
+  for (int i = 0; i < count; ++i)
+    st1<T>(o.base, view_pixel_index(o, pix, c + i), epilogue<T>(e, v[i], pix, n, c + i));
 }
 
 // True when 8-channel vector access at channel c is legal for view v.
 DFX_DEV bool vec8_ok(const dfx_view& v, int c) { return ((v.coff + c) & 7) == 0; }
+
+// ---------------------------------------------------------------- programmatic dependent launch
+// Graph edges between libdfx kernels are programmatic: a kernel may start
+// (prologue, TMEM/barrier setup, weight prefetch) while its predecessor
+// finishes.  griddep_wait() blocks until the predecessor grid completed and
+// its writes are visible -- every read of activations and every write must
+// come after it.  griddep_launch() lets the successor start its prologue.
+// Both are no-ops without a programmatic dependency (eager launches).
+DFX_DEV void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+DFX_DEV void griddep_launch() { asm volatile("griddepcontrol.launch_dependents;" :::); }
 
 // ---------------------------------------------------------------- PTX wrappers
 DFX_DEV uint32_t smem_u32(const void* p) {

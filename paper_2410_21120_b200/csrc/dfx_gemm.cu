@@ -19,7 +19,10 @@
 //
 // Warp roles (128 threads): warp 0 lane 0 = TMA producer, warp 1 lane 0 =
 // MMA issuer, warp 2 = TMEM allocator; all four warps run the epilogue
-// (warp w owns TMEM lanes 32w..32w+31 = tile rows).
+// (warp w owns TMEM lanes 32w..32w+31 = tile rows).  The problem descriptor
+// is staged in shared memory once and every loop runs on register copies of
+// its fields (the PTX "memory" clobbers would otherwise force a global reload
+// of each field per iteration).
 #include "dfx_common.cuh"
 
 namespace dfx {
@@ -29,7 +32,10 @@ struct GemmHeader {
   uint64_t empty[kSlots];
   uint64_t accum;
   uint32_t tmem_base;
+  uint32_t _pad[5];
+  dfx_gemm_desc desc;     // 64-B aligned copy of this CTA's problem
 };
+static_assert(sizeof(GemmHeader) <= kHeaderBytes, "gemm smem header overflow");
 
 template <typename T>
 __global__ void __launch_bounds__(kGemmThreads, 1)
@@ -49,24 +55,13 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   int pi = 0;
   for (int i = 1; i < L.ndesc; ++i)
     if (L.descs[i].tile_begin <= bid) pi = i;
-  const dfx_gemm_desc* d = L.descs + pi;
+  const dfx_gemm_desc* gd = L.descs + pi;          // global copy: tensor maps live here
 
-  // ---- tile coordinates (M tiles fastest, then K splits, then N tiles)
-  int t = bid - d->tile_begin;
-  const int mt_total = d->mt_n * d->mt_p * d->mt_q;
-  const int mi = t % mt_total;
-  t /= mt_total;
-  const int split = t % d->splits;
-  const int ntile = t / d->splits;
-  const int mq = mi % d->mt_q;
-  const int mp = (mi / d->mt_q) % d->mt_p;
-  const int mn = mi / (d->mt_q * d->mt_p);
-  const int n0 = mn * d->tn, p0 = mp * d->tp, q0 = mq * d->tq;
-  const int bn = d->bn, cb = d->cb, kpack = d->kpack, ksteps = d->ksteps;
-  const int st_begin = split * d->stages_per_split;
-  const int st_end = min(d->stages, st_begin + d->stages_per_split);
+  // ---- stage the descriptor in smem (32 x 16 B), barriers, TMEM
+  if (threadIdx.x < sizeof(dfx_gemm_desc) / 16)
+    reinterpret_cast<uint4*>(&hdr->desc)[threadIdx.x] =
+        reinterpret_cast<const uint4*>(gd)[threadIdx.x];
   const uint32_t tmem_cols = tmem_cols_for(L.bn_max);
-
   if (threadIdx.x == 0) {
     for (int i = 0; i < kSlots; ++i) {
       mbar_init(&hdr->full[i], 1);
@@ -77,22 +72,72 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   }
   if (warp == 2) tmem_alloc(&hdr->tmem_base, tmem_cols);
   if (warp == 0 && lane == 0) {
-    tma_prefetch_desc(d->tmap_a);
-    tma_prefetch_desc(d->tmap_b);
+    tma_prefetch_desc(gd->tmap_a);
+    tma_prefetch_desc(gd->tmap_b);
   }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = hdr->tmem_base;
+  const dfx_gemm_desc& D = hdr->desc;
+
+  // ---- tile coordinates (M tiles fastest, then K splits, then N tiles)
+  const int mt_q = D.mt_q, mt_p = D.mt_p, splits = D.splits;
+  const int tn = D.tn, tp = D.tp, tq = D.tq;
+  int t = bid - D.tile_begin;
+  const int mt_total = D.mt_n * mt_p * mt_q;
+  const int mi = t % mt_total;
+  t /= mt_total;
+  const int split = t % splits;
+  const int ntile = t / splits;
+  const int mq = mi % mt_q;
+  const int mp = (mi / mt_q) % mt_p;
+  const int mn = mi / (mt_q * mt_p);
+  const int n0 = mn * tn, p0 = mp * tp, q0 = mq * tq;
+  const int bn = D.bn, cb = D.cb, kpack = D.kpack, ksteps = D.ksteps;
+  const int st_begin = split * D.stages_per_split;
+  const int st_end = min(D.stages, st_begin + D.stages_per_split);
 
   const int sub_a = 128 * cb * 2;     // bytes of one K-step A sub-tile
   const int sub_b = bn * cb * 2;      // bytes of one K-step B sub-tile
-  const uint32_t box_a_bytes = uint32_t(cb) * 2u * d->tq * d->tp * d->tn;
 
   if (warp == 0 && lane == 0) {
     // ================= TMA producer
-    int it = 0;
-    for (int st = st_begin; st < st_end; ++st, ++it) {
+    const int cblocks = D.cblocks, S = D.s;
+    const int qbase = q0 * D.stride_w - D.pad_w, pbase = p0 * D.stride_h - D.pad_h;
+    const uint32_t box_a_bytes = uint32_t(cb) * 2u * tq * tp * tn;
+    const void* tma = gd->tmap_a;
+    const void* tmb = gd->tmap_b;
+    const int nrow = ntile * bn;
+    // Weights are static: the first kSlots stages' B tiles are requested before
+    // the programmatic dependency resolves, overlapping the predecessor's tail.
+    const int npre = min(kSlots, st_end - st_begin);
+    for (int it = 0; it < npre; ++it) {
+      const int st = st_begin + it;
+      uint8_t* b_dst = slots + it * slot_bytes + kStageABytes;
+      const int k0 = st * kpack;
+      const int nk = min(kpack, ksteps - k0);
+      mbar_arrive_expect_tx(&hdr->full[it], nk * (box_a_bytes + uint32_t(sub_b)));
+      for (int j = 0; j < nk; ++j)
+        tma_load_2d(b_dst + j * sub_b, tmb, &hdr->full[it], (k0 + j) * cb, nrow);
+    }
+    griddep_wait();
+    for (int it = 0; it < npre; ++it) {
+      const int st = st_begin + it;
+      uint8_t* a_dst = slots + it * slot_bytes;
+      const int k0 = st * kpack;
+      const int nk = min(kpack, ksteps - k0);
+      for (int j = 0; j < nk; ++j) {
+        const int kstep = k0 + j;
+        const int rs = kstep / cblocks;
+        const int cblk = kstep - rs * cblocks;
+        const int r = rs / S;
+        const int s = rs - r * S;
+        tma_load_4d(a_dst + j * sub_a, tma, &hdr->full[it], cblk * cb, qbase + s, pbase + r, n0);
+      }
+    }
+    int it = npre;
+    for (int st = st_begin + npre; st < st_end; ++st, ++it) {
       const int slot = it % kSlots;
       const uint32_t par = (it / kSlots) & 1;
       mbar_wait(&hdr->empty[slot], par ^ 1);
@@ -103,19 +148,19 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       mbar_arrive_expect_tx(&hdr->full[slot], nk * (box_a_bytes + uint32_t(sub_b)));
       for (int j = 0; j < nk; ++j) {
         const int kstep = k0 + j;
-        const int rs = kstep / d->cblocks;
-        const int cblk = kstep - rs * d->cblocks;
-        const int r = rs / d->s;
-        const int s = rs - r * d->s;
-        tma_load_4d(a_dst + j * sub_a, d->tmap_a, &hdr->full[slot], cblk * cb,
-                    q0 * d->stride_w + s - d->pad_w, p0 * d->stride_h + r - d->pad_h, n0);
-        tma_load_2d(b_dst + j * sub_b, d->tmap_b, &hdr->full[slot], kstep * cb, ntile * bn);
+        const int rs = kstep / cblocks;
+        const int cblk = kstep - rs * cblocks;
+        const int r = rs / S;
+        const int s = rs - r * S;
+        tma_load_4d(a_dst + j * sub_a, tma, &hdr->full[slot], cblk * cb, qbase + s, pbase + r, n0);
+        tma_load_2d(b_dst + j * sub_b, tmb, &hdr->full[slot], kstep * cb, nrow);
       }
     }
   } else if (warp == 1 && lane == 0) {
     // ================= MMA issuer
     const uint32_t idesc = umma_idesc_f16(uint32_t(bn), Elt<T>::kDtype);
     const uint32_t row_bytes = uint32_t(cb) * 2u;
+    const int kk_n = cb / 16;
     uint32_t accumulate = 0;
     int it = 0;
     for (int st = st_begin; st < st_end; ++st, ++it) {
@@ -127,7 +172,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       const uint32_t b_base = a_base + kStageABytes;
       const int nk = min(kpack, ksteps - st * kpack);
       for (int j = 0; j < nk; ++j) {
-        for (int kk = 0; kk < cb / 16; ++kk) {
+        for (int kk = 0; kk < kk_n; ++kk) {
           const uint64_t ad = umma_smem_desc(a_base + j * sub_a + kk * 32, row_bytes);
           const uint64_t bd = umma_smem_desc(b_base + j * sub_b + kk * 32, row_bytes);
           umma_f16(tmem_base, ad, bd, idesc, accumulate);
@@ -141,46 +186,51 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   __syncwarp();
 
   // ================= epilogue: TMEM -> registers -> 16-bit NHWC (or fp32 split-K partials)
+  const dfx_epilogue e = D.epi;
+  const dfx_view o = D.out;
+  const int cout = D.cout, P = D.p, Q = D.q, N = D.n;
+  float* const ws = D.ws;
+  const int ldw = D.nt * bn;
+
+  griddep_wait();                              // residual / output buffers of predecessors
   mbar_wait(&hdr->accum, 0);
   tc_fence_after();
+  griddep_launch();                            // successor may start its prologue now
 
   const int row = threadIdx.x;                 // tile row == TMEM lane
-  const int qi = row % d->tq;
-  const int pi_ = (row / d->tq) % d->tp;
-  const int ni = row / (d->tq * d->tp);
+  const int qi = row % tq;
+  const int pi_ = (row / tq) % tp;
+  const int ni = row / (tq * tp);
   const int on = n0 + ni, op = p0 + pi_, oq = q0 + qi;
-  const bool valid = row < d->tn * d->tp * d->tq && on < d->n && op < d->p && oq < d->q;
-  const int64_t pix = (int64_t(on) * d->p + op) * d->q + oq;
+  const bool valid = row < tn * tp * tq && on < N && op < P && oq < Q;
+  const int64_t pix = (int64_t(on) * P + op) * Q + oq;
   const uint32_t lane_addr = tmem_base + (uint32_t(warp * 32) << 16);
   const int co_base = ntile * bn;
-  const int ncols = min(bn, ((d->cout - co_base) + 15) & ~15);
+  const int ncols = min(bn, ((cout - co_base) + 15) & ~15);
+  const bool views_vec = vec8_ok(o, 0) && (e.binop == DFX_BIN_NONE || vec8_ok(e.other, 0));
 
   for (int c0 = 0; c0 < ncols; c0 += 16) {
     float v[16];
     tmem_ld16(lane_addr + uint32_t(c0), v);
     if (!valid) continue;
     const int co = co_base + c0;
-    if (d->splits > 1) {
-      const int ldw = d->nt * bn;
-      float4* dst = reinterpret_cast<float4*>(
-          d->ws + (int64_t(split) * d->n * d->p * d->q + pix) * ldw + co);
+    if (splits > 1) {
+      float4* dst = reinterpret_cast<float4*>(ws + (int64_t(split) * N * P * Q + pix) * ldw + co);
 #pragma unroll
       for (int i = 0; i < 4; ++i) dst[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
       continue;
     }
-    const dfx_epilogue& e = d->epi;
-    const dfx_view& o = d->out;
-    const bool vec = co + 16 <= d->cout && vec8_ok(o, co) &&
-                     (e.binop == DFX_BIN_NONE || vec8_ok(e.other, co));
-    if (vec) {
+    if (views_vec && co + 16 <= cout) {
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         epilogue8<T>(e, v + 8 * h, pix, on, co + 8 * h);
         st8<T>(o.base, view_pixel_index(o, pix, co + 8 * h), v + 8 * h);
       }
     } else {
-      for (int i = 0; i < 16 && co + i < d->cout; ++i)
-        st1<T>(o.base, view_pixel_index(o, pix, co + i), epilogue<T>(e, v[i], pix, on, co + i));
+      float tail[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) tail[i] = v[i];
+      epilogue_store_tail<T>(e, o, tail, pix, on, co, min(16, cout - co));
     }
   }
 
@@ -192,9 +242,12 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 // Deterministic split-K reduction (splits summed in ascending order) + epilogue.
 template <typename T>
 __global__ void splitk_kernel(const __grid_constant__ dfx_splitk_params P) {
+  griddep_wait();
+  griddep_launch();
   const int cgroups = (P.cout + 7) / 8;
   const int64_t total = int64_t(P.pixels) * cgroups;
   const int hw = P.out.h * P.out.w;
+  const int64_t plane = int64_t(P.pixels) * P.ldw;
   for (int64_t idx = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; idx < total;
        idx += int64_t(gridDim.x) * blockDim.x) {
     const int64_t pix = idx / cgroups;
@@ -208,7 +261,7 @@ __global__ void splitk_kernel(const __grid_constant__ dfx_splitk_params P) {
       v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
     }
     for (int s = 1; s < P.splits; ++s) {
-      const float* p = src + int64_t(s) * P.pixels * P.ldw;
+      const float* p = src + s * plane;
       const float4 a = *reinterpret_cast<const float4*>(p);
       const float4 b = *reinterpret_cast<const float4*>(p + 4);
       v[0] += a.x; v[1] += a.y; v[2] += a.z; v[3] += a.w; v[4] += b.x; v[5] += b.y; v[6] += b.z; v[7] += b.w;
@@ -219,8 +272,7 @@ __global__ void splitk_kernel(const __grid_constant__ dfx_splitk_params P) {
       epilogue8<T>(P.epi, v, pix, n, c);
       st8<T>(P.out.base, view_pixel_index(P.out, pix, c), v);
     } else {
-      for (int i = 0; i < 8 && c + i < P.cout; ++i)
-        st1<T>(P.out.base, view_pixel_index(P.out, pix, c + i), epilogue<T>(P.epi, v[i], pix, n, c + i));
+      epilogue_store_tail<T>(P.epi, P.out, v, pix, n, c, min(8, P.cout - c));
     }
   }
 }

@@ -314,7 +314,12 @@ class ExecInstance:
             for L in prog.launches:
                 for op, params in self._params(m, prog, L, n, host_descs):
                     last = g.add(op, params, [last])
-                    self.nodes.append((op, params, self._algo(prog, L, n, op)))
+                    info = self._algo(prog, L, n, op)
+                    info["node"] = L.nodes[0]
+                    if op == rt.OP_GEMM:
+                        info["tiling"] = self.plans[m].tilings[L.index]
+                        info["geom"] = {k: L.geom[k] for k in ("cin", "cout", "kh", "kw", "cb")}
+                    self.nodes.append((op, params, info))
             pout = rt.OutParams(self._view(m, prog, prog.exit_value, n), self.dev_out + self.out_off[m])
             last = g.add(rt.OP_OUT, pout, [last])
             self.nodes.append((rt.OP_OUT, pout, dict(member=m, kind="out", flops=0,
@@ -360,19 +365,39 @@ class ExecInstance:
             info.update(bytes=in_b + out_b + other_b)
         return info
 
-    def profile_nodes(self, reps: int = 3) -> list[dict]:
-        """Replay every graph node eagerly on this instance's stream, timing each
-        launch with CUDA events (median of ``reps``).  Same params as the graph."""
+    def profile_nodes(self, reps: int = 8, kinds=None) -> list[dict]:
+        """Per-node device time: each graph node (same params as in the step) is
+        put ``reps`` times in a chain inside its own CUDA graph, launched once to
+        warm up and once between CUDA events on this instance's stream; the
+        node time is the event interval / reps (host launch gaps excluded, the
+        ~1 us graph node-to-node gap included, as inside the real step).
+        A GEMM node that uses split-K is timed together with its reduction."""
         out = []
-        for op, params, info in self.nodes:
-            times = []
+        i = 0
+        nodes = self.nodes
+        while i < len(nodes):
+            op, params, info = nodes[i]
+            group = [(op, params)]
+            if op == rt.OP_GEMM and i + 1 < len(nodes) and nodes[i + 1][0] == rt.OP_SPLITK:
+                group.append(nodes[i + 1][:2])
+                i += 1
+            i += 1
+            if kinds is not None and info["kind"] not in kinds:
+                continue
+            g = rt.Graph()
+            last = None
             for _ in range(reps):
-                e0, e1 = rt.Event(), rt.Event()
-                e0.record(self.stream)
-                rt.launch(op, params, self.stream)
-                e1.record(self.stream)
-                times.append(e0.elapsed_ms(e1))
-            out.append(dict(info, op=op, ms=float(np.median(times))))
+                for o, p in group:
+                    last = g.add(o, p, [] if last is None else [last])
+            g.instantiate()
+            g.launch(self.stream)
+            e0, e1 = rt.Event(), rt.Event()
+            e0.record(self.stream)
+            g.launch(self.stream)
+            e1.record(self.stream)
+            ms = e0.elapsed_ms(e1) / reps
+            g.destroy()
+            out.append(dict(info, op=op, ms=ms, split=len(group) > 1))
         return out
 
     def _params(self, m, prog: MemberProgram, L, n, host_descs):

@@ -568,9 +568,14 @@ def gemm_tiling(geom: dict, n: int, p: int, q: int, sm_count: int = 148) -> dict
     tn, tp, tq = choose_m_tile(n, p, q, geom["sh"], geom["sw"])
     mt = (math.ceil(n / tn), math.ceil(p / tp), math.ceil(q / tq))
     bn, nt = choose_bn(geom["cout"])
+    m_tiles = mt[0] * mt[1] * mt[2]
+    # small-M layers: narrower N tiles first (more CTAs, no extra kernel), split-K second
+    while m_tiles * nt < sm_count and bn > 64:
+        bn = max(64, round_up(bn // 2, 16))
+        nt = -(-geom["cout"] // bn)
     kpack = 64 // geom["cb"]
     stages = math.ceil(geom["ksteps"] / kpack)
-    base = mt[0] * mt[1] * mt[2] * nt
+    base = m_tiles * nt
     splits = 1
     if base < sm_count and stages >= 4:
         splits = min(math.ceil(sm_count / base), stages // 2)
