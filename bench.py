@@ -52,18 +52,47 @@ def peaks():
 # ----------------------------------------------------------------------------- clocks
 
 class ClockSampler:
-    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    """SM clock + clock-event reasons sampled DURING the timed region.
+
+    NVML (pynvml) polled every ~2 ms from a thread; falls back to
+    ``nvidia-smi -lms 20`` when NVML is unavailable."""
+
+    REASONS = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
 
     def __init__(self, index: int):
-        self.index, self.rows, self.proc = index, [], None
+        self.index, self.rows, self.proc, self.stop_flag = index, [], None, False
+        self.thread = None
+        try:
+            import pynvml as nv
+            nv.nvmlInit()
+            self.nv, self.h = nv, nv.nvmlDeviceGetHandleByIndex(index)
+            self.bits = {"hw_slowdown": nv.nvmlClocksEventReasonHwSlowdown,
+                         "hw_thermal_slowdown": nv.nvmlClocksEventReasonHwThermalSlowdown,
+                         "sw_thermal_slowdown": nv.nvmlClocksEventReasonSwThermalSlowdown,
+                         "sw_power_cap": nv.nvmlClocksEventReasonSwPowerCap}
+            self.max_mhz = nv.nvmlDeviceGetMaxClockInfo(self.h, nv.NVML_CLOCK_SM)
+        except Exception:  # noqa: BLE001
+            self.nv = None
 
     def start(self):
+        self.stop_flag = False
+        if self.nv is not None:
+            def poll():
+                nv = self.nv
+                while not self.stop_flag:
+                    sm = nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)
+                    rs = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                    self.rows.append((sm, [n for n, b in self.bits.items() if rs & b]))
+                    time.sleep(0.002)
+            self.thread = threading.Thread(target=poll, daemon=True)
+            self.thread.start()
+            return
         try:
             self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                ["nvidia-smi", "-i", str(self.index),
+                 "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+                 "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_power_cap", "--format=csv,noheader,nounits", "-lms", "20"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             threading.Thread(target=self._read, daemon=True).start()
         except OSError:
@@ -71,27 +100,28 @@ class ClockSampler:
 
     def _read(self):
         for line in self.proc.stdout:
-            parts = [p.strip() for p in line.split(",")]
-            if len(parts) == 8:
-                self.rows.append(parts)
+            p = [x.strip() for x in line.split(",")]
+            if len(p) == 6 and p[0].isdigit():
+                self.max_mhz = float(p[1])
+                self.rows.append((float(p[0]), [n for n, v in zip(self.REASONS, p[2:]) if v.lower() == "active"]))
 
     def stop(self):
+        self.stop_flag = True
+        if self.thread is not None:
+            self.thread.join(timeout=2)
         if self.proc is not None:
             self.proc.terminate()
             try:
                 self.proc.wait(timeout=5)
             except subprocess.TimeoutExpired:
                 self.proc.kill()
-        time.sleep(0.05)
         if not self.rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
-        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
-        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
-        reasons = sorted({n for r in self.rows for n, v in zip(names, r[4:8]) if v.lower() == "active"})
-        return {"sm_mhz": float(np.median(sm)) if sm else None,
-                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
-                "samples": len(self.rows)}
+        sm = [r[0] for r in self.rows]
+        reasons = sorted({n for r in self.rows for n in r[1]})
+        return {"sm_mhz": float(np.median(sm)), "sm_min_mhz": float(min(sm)),
+                "sm_max_mhz": float(getattr(self, "max_mhz", max(sm))), "reasons": reasons,
+                "samples": len(self.rows), "source": "nvml" if self.nv is not None else "nvidia-smi"}
 
 
 # ----------------------------------------------------------------------------- helpers
@@ -228,7 +258,8 @@ def run_ours(args, world, rank, local_rank):
                 si.sync()
             e1.record(insts[-1].stream)
             u_ms.append(e0.elapsed_ms(e1))
-        unfused = {"swap_in_ms": pt.upload_ms, "weight_tensors": pt.tensors,
+        unfused = {"swap_in_ms": pt.upload_ms, "malloc_ms": pt.malloc_ms, "memcpy_ms": pt.memcpy_ms,
+                   "weight_tensors": pt.tensors,
                    "peak_hbm_gb": (free_u0 - free_u1) / 1e9,
                    "ms_per_query": float(np.median(u_ms)),
                    "note": "per-tensor cudaMalloc+cudaMemcpyAsync from pageable memory; "
@@ -378,10 +409,18 @@ def run_ours(args, world, rank, local_rank):
         "data": "synthetic (N(0,1) inputs, seeded calibrated random-init weights)",
         "config": config_dict(args),
         "latency_ms": ms_per_step,
-        "swap_in": {"fused_ms": arena.upload_ms, "arena_mb": arena.total / 1e6,
-                    "fused_h2d_gbs": arena.total / (arena.upload_ms * 1e-3) / 1e9 if arena.upload_ms else None,
-                    "pinned_h2d_peak_gbs": h2d_gbs, "nccl_broadcast_ms": bcast_ms,
-                    "unfused_ms": unfused["swap_in_ms"] if unfused else None},
+        "swap_in": {"fused_ms": arena.upload_ms, "fused_malloc_ms": getattr(arena, "malloc_ms", None),
+                    "fused_memcpy_ms": getattr(arena, "memcpy_ms", None),
+                    "arena_mb": arena.total / 1e6, "cuda_mallocs": 1, "h2d_copies": 1,
+                    "fused_h2d_gbs": (arena.total / (arena.memcpy_ms * 1e-3) / 1e9
+                                      if getattr(arena, "memcpy_ms", None) else None),
+                    "pinned_h2d_peak_gbs": h2d_gbs,
+                    "h2d_frac_of_pinned_peak": (arena.total / (arena.memcpy_ms * 1e-3) / 1e9 / h2d_gbs
+                                                if getattr(arena, "memcpy_ms", None) else None),
+                    "nccl_broadcast_ms": bcast_ms,
+                    "unfused_ms": unfused["swap_in_ms"] if unfused else None,
+                    "unfused_malloc_ms": unfused["malloc_ms"] if unfused else None,
+                    "unfused_memcpy_ms": unfused["memcpy_ms"] if unfused else None},
         "peak_hbm_gb": {"fused": fused_peak / 1e9, "unfused": unfused["peak_hbm_gb"] if unfused else None},
         "unfused": unfused,
         "e2e": {"value": e2e_value, "unit": "images/s",
@@ -417,7 +456,7 @@ class _SubArena:
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
     ap.add_argument("--batch", type=int, default=1)

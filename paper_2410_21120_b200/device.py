@@ -55,45 +55,61 @@ def _align(x, a=ALIGN):
 
 # ------------------------------------------------------------------------------ weights
 
+def arena_layout(programs: list[MemberProgram]):
+    """Byte layout of the packed weight arena: member segments in member order,
+    blobs in sorted-key order inside a segment, every blob 256-B aligned (TMA
+    needs 16 B; 256 keeps every tensor on its own L2 sector group).
+    Returns (per-member {key: offset}, per-member (offset, bytes), total)."""
+    layout, segments, at = [], [], 0
+    for p in programs:
+        seg0, offs = at, {}
+        for key in sorted(p.blobs):
+            offs[key] = at
+            at = _align(at + p.blobs[key].nbytes)
+        layout.append(offs)
+        segments.append((seg0, at - seg0))
+    return layout, segments, max(at, ALIGN)
+
+
+def fill_arena(buf: np.ndarray, programs: list[MemberProgram], layout) -> None:
+    """Copy every blob into its slot of a uint8 arena buffer."""
+    for p, offs in zip(programs, layout):
+        for key, off in offs.items():
+            raw = p.blobs[key].view(np.uint8).reshape(-1)
+            buf[off:off + raw.size] = raw
+
+
 class WeightArena:
     """Packed weights of all members: host pinned staging + device copy."""
 
     def __init__(self, programs: list[MemberProgram], device: int = 0):
         self.device = device
-        self.layout: list[dict[str, int]] = []
-        self.segments: list[tuple[int, int]] = []          # (offset, bytes) per member
-        at = 0
-        for p in programs:
-            seg0 = at
-            offs = {}
-            for key in sorted(p.blobs):
-                offs[key] = at
-                at = _align(at + p.blobs[key].nbytes)
-            self.layout.append(offs)
-            self.segments.append((seg0, at - seg0))
-        self.total = max(at, ALIGN)
+        self.layout, self.segments, self.total = arena_layout(programs)
         rt.init_device(device)
         self.host = rt.host_alloc(self.total)
         view = (C.c_uint8 * self.total).from_address(self.host)
-        buf = np.frombuffer(view, dtype=np.uint8)
-        for p, offs in zip(programs, self.layout):
-            for key, off in offs.items():
-                raw = p.blobs[key].view(np.uint8).reshape(-1)
-                buf[off:off + raw.size] = raw
+        fill_arena(np.frombuffer(view, dtype=np.uint8), programs, self.layout)
         self.dev = 0
         self.member_base: list[int] = []       # device base of each member's segment
         self.extra_allocs: list[int] = []
         self.upload_ms = None
 
     def upload(self, stream=None) -> float:
-        """ONE device allocation + ONE H2D copy of the whole arena; returns ms."""
-        p = C.c_void_p()
+        """ONE device allocation + ONE H2D copy of the whole arena; returns ms.
+
+        The two phases are timed apart (the reference's cost model books them
+        as separate cudaMalloc / cudaMemcpyAsync rows, costmodel.py:297-300):
+        ``malloc_ms`` by wall clock, ``memcpy_ms`` by CUDA events."""
         t0 = time.perf_counter()
-        rt.call("dfx_arena_upload", C.c_void_p(self.host), C.c_size_t(self.total), C.byref(p),
-                C.c_void_p(stream))
+        self.dev = rt.malloc(self.total)
+        self.malloc_ms = (time.perf_counter() - t0) * 1e3
+        e0, e1 = rt.Event(), rt.Event()
+        e0.record(stream)
+        rt.h2d(self.dev, self.host, self.total, stream)
+        e1.record(stream)
+        self.memcpy_ms = e0.elapsed_ms(e1)
         rt.stream_sync(stream)
         self.upload_ms = (time.perf_counter() - t0) * 1e3
-        self.dev = p.value
         self.member_base = [self.dev + off for off, _ in self.segments]
         return self.upload_ms
 
@@ -161,15 +177,20 @@ class PerTensorArena:
         self.ptrs: list[dict[str, int]] = []
         self.tensors = 0
         self.total = 0
+        self.malloc_ms = self.memcpy_ms = 0.0
         t0 = time.perf_counter()
         for p in programs:
             table = {}
             for key in sorted(p.blobs):
                 blob = np.ascontiguousarray(p.blobs[key])
+                ta = time.perf_counter()
                 ptr = rt.malloc(blob.nbytes)
+                tb = time.perf_counter()
                 rt.call("dfx_memcpy_h2d", C.c_void_p(ptr), C.c_void_p(blob.ctypes.data),
                         C.c_size_t(blob.nbytes), C.c_void_p(stream))
                 rt.stream_sync(stream)            # pageable source: copy completes before return
+                self.malloc_ms += (tb - ta) * 1e3
+                self.memcpy_ms += (time.perf_counter() - tb) * 1e3
                 table[key] = ptr
                 self.tensors += 1
                 self.total += blob.nbytes
