@@ -124,7 +124,10 @@ typedef struct __attribute__((aligned(64))) dfx_gemm_desc {
   dfx_view out;                    /* bf16 output view (n, p, q, cout) */
   dfx_epilogue epi;
   float* ws;                       /* split-K workspace [splits][n*p*q][nt*bn] */
-  int64_t _pad1[3];                
+  uint32_t* counters;              /* split-K arrival counters, one per output tile, zeroed
+                                      once; the last-arriving CTA of a tile reduces all splits
+                                      in split order (deterministic) and resets its counter */
+  int64_t _pad1[2];                
 } dfx_gemm_desc;
 
 typedef struct dfx_gemm_launch {

@@ -141,7 +141,7 @@ int config_for(int op, const void* params, size_t size, LaunchCfg* c) {
       NEED(dfx_gap_params);
       const auto* p = static_cast<const dfx_gap_params*>(params);
       c->func = DFX_PICK(gap_kernel, p->in.dtype);
-      c->grid = dim3(unsigned(cdiv(p->in.c, 256)), unsigned(p->in.n));
+      c->grid = dim3(unsigned(cdiv(p->in.c, 64)), unsigned(p->in.n));
       return DFX_OK;
     }
     case DFX_OP_EW: {

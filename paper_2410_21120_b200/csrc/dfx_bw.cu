@@ -169,54 +169,56 @@ __global__ void pool_kernel(const __grid_constant__ dfx_pool_params P) {
 }
 
 // ------------------------------------------------------------------ global average pool
-// grid (ceil(C/256), N); 256 threads = 8 warps; lane handles 8 channels, warps
-// split the spatial range, smem reduction in fixed order.
+// grid (ceil(C/64), N), 256 threads: 8 lanes x 8 channels cover 64 channels,
+// 32 thread rows split the spatial range; fixed-order smem reduction over rows
+// (deterministic).  Sum * fp32(1/HW) as the reference (executor.py:129-133).
 template <typename T>
 __global__ void gap_kernel(const __grid_constant__ dfx_gap_params P) {
   griddep_wait();
   griddep_launch();
-  __shared__ float part[8][256 + 8];
+  __shared__ float part[32][64 + 4];
   const dfx_view& in = P.in;
   const int n = blockIdx.y;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int c = blockIdx.x * 256 + lane * 8;
+  const int tx = threadIdx.x & 7, ty = threadIdx.x >> 3;
+  const int c = blockIdx.x * 64 + tx * 8;
   const int hw = in.h * in.w;
   const int nl = min(8, in.c - c);
   float acc[8];
 #pragma unroll
   for (int i = 0; i < 8; ++i) acc[i] = 0.f;
   if (nl > 0) {
-    const bool vec = nl == 8 && (in.coff & 7) == 0;
-    for (int s = warp; s < hw; s += 8) {
-      const int64_t base = view_pixel_index(in, int64_t(n) * hw + s, c);
-      float x[8];
-      if (vec) {
-        ld8<T>(in.base, base, x);
-      } else {
-        for (int i = 0; i < 8; ++i) x[i] = i < nl ? ld1<T>(in.base, base + i) : 0.f;
-      }
+    const bool vec = nl == 8 && ((in.coff + c) & 7) == 0;
+    const int64_t base = view_pixel_index(in, int64_t(n) * hw, c);
+    if (vec) {
+      int s = ty;
+      for (; s + 32 < hw; s += 64) {            // two independent 16-B loads in flight
+        float x0[8], x1[8];
+        ld8<T>(in.base, base + int64_t(s) * in.pitch, x0);
+        ld8<T>(in.base, base + int64_t(s + 32) * in.pitch, x1);
 #pragma unroll
-      for (int i = 0; i < 8; ++i) acc[i] += x[i];
+        for (int i = 0; i < 8; ++i) acc[i] += x0[i] + x1[i];
+      }
+      for (; s < hw; s += 32) {
+        float x[8];
+        ld8<T>(in.base, base + int64_t(s) * in.pitch, x);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) acc[i] += x[i];
+      }
+    } else {
+      for (int s = ty; s < hw; s += 32)
+        for (int i = 0; i < nl; ++i) acc[i] += ld1<T>(in.base, base + int64_t(s) * in.pitch + i);
     }
   }
 #pragma unroll
-  for (int i = 0; i < 8; ++i) part[warp][lane * 8 + i] = acc[i];
+  for (int i = 0; i < 8; ++i) part[ty][tx * 8 + i] = acc[i];
   __syncthreads();
-  if (warp == 0 && nl > 0) {
-    float v[8];
-    const float inv = 1.0f / float(hw);
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      float s = 0.f;
-      for (int w = 0; w < 8; ++w) s += part[w][lane * 8 + i];
-      v[i] = s * inv;
-    }
-    const dfx_view& out = P.out;
-    const int64_t o = int64_t(n) * out.pitch + out.coff + c;
-    if (nl == 8 && (out.coff & 7) == 0) {
-      st8<T>(out.base, o, v);
-    } else {
-      for (int i = 0; i < nl; ++i) st1<T>(out.base, o + i, v[i]);
+  if (threadIdx.x < 64) {
+    const int cc = blockIdx.x * 64 + threadIdx.x;
+    if (cc < in.c) {
+      float sum = 0.f;
+      for (int r = 0; r < 32; ++r) sum += part[r][threadIdx.x];
+      const dfx_view& out = P.out;
+      st1<T>(out.base, int64_t(n) * out.pitch + out.coff + cc, sum * (1.0f / float(hw)));
     }
   }
 }

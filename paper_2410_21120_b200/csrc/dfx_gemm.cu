@@ -32,7 +32,8 @@ struct GemmHeader {
   uint64_t empty[kSlots];
   uint64_t accum;
   uint32_t tmem_base;
-  uint32_t _pad[5];
+  uint32_t last_split;    // split-K: this CTA arrived last for its output tile
+  uint32_t _pad[4];
   dfx_gemm_desc desc;     // 64-B aligned copy of this CTA's problem
 };
 static_assert(sizeof(GemmHeader) <= kHeaderBytes, "gemm smem header overflow");
@@ -209,13 +210,14 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   const int ncols = min(bn, ((cout - co_base) + 15) & ~15);
   const bool views_vec = vec8_ok(o, 0) && (e.binop == DFX_BIN_NONE || vec8_ok(e.other, 0));
 
+  const int64_t plane = int64_t(N) * P * Q * ldw;      // one split's partials
   for (int c0 = 0; c0 < ncols; c0 += 16) {
     float v[16];
     tmem_ld16(lane_addr + uint32_t(c0), v);
     if (!valid) continue;
     const int co = co_base + c0;
     if (splits > 1) {
-      float4* dst = reinterpret_cast<float4*>(ws + (int64_t(split) * N * P * Q + pix) * ldw + co);
+      float4* dst = reinterpret_cast<float4*>(ws + split * plane + pix * ldw + co);
 #pragma unroll
       for (int i = 0; i < 4; ++i) dst[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
       continue;
@@ -231,6 +233,58 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 #pragma unroll
       for (int i = 0; i < 16; ++i) tail[i] = v[i];
       epilogue_store_tail<T>(e, o, tail, pix, on, co, min(16, cout - co));
+    }
+  }
+
+  if (splits > 1 && D.counters != nullptr) {
+    // ---- in-kernel split-K fixup: the last CTA to arrive for this output tile sums
+    // all splits' partials in split order (deterministic), applies the epilogue and
+    // resets the tile's counter for the next graph replay.
+    const int tile_id = mi + mt_total * ntile;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0)
+      hdr->last_split = atomicAdd(D.counters + tile_id, 1u) == uint32_t(splits - 1);
+    __syncthreads();
+    if (hdr->last_split) {
+      __threadfence();
+      // all 128 threads cooperate: item = (tile row, 8-channel group); adjacent
+      // threads take adjacent groups of one row (coalesced); the split loop is
+      // unrolled so its loads are independent and in flight together
+      const int c8n = ncols / 8;
+      for (int item = threadIdx.x; item < 128 * c8n; item += kGemmThreads) {
+        const int r = item / c8n;
+        const int co = co_base + (item - r * c8n) * 8;
+        const int rq = r % tq, rp = (r / tq) % tp, rn = r / (tq * tp);
+        const int an = n0 + rn, ap = p0 + rp, aq = q0 + rq;
+        if (r >= tn * tp * tq || an >= N || ap >= P || aq >= Q || co >= cout) continue;
+        const int64_t rpix = (int64_t(an) * P + ap) * Q + aq;
+        const float4* src = reinterpret_cast<const float4*>(ws + rpix * ldw + co);
+        const int64_t step = plane / 4;
+        float4 a0 = __ldcg(src), a1 = __ldcg(src + 1);
+        int s = 1;
+        for (; s + 1 < splits; s += 2) {
+          const float4 b0 = __ldcg(src + s * step), b1 = __ldcg(src + s * step + 1);
+          const float4 c0 = __ldcg(src + (s + 1) * step), c1 = __ldcg(src + (s + 1) * step + 1);
+          a0.x += b0.x; a0.y += b0.y; a0.z += b0.z; a0.w += b0.w;
+          a1.x += b1.x; a1.y += b1.y; a1.z += b1.z; a1.w += b1.w;
+          a0.x += c0.x; a0.y += c0.y; a0.z += c0.z; a0.w += c0.w;
+          a1.x += c1.x; a1.y += c1.y; a1.z += c1.z; a1.w += c1.w;
+        }
+        if (s < splits) {
+          const float4 b0 = __ldcg(src + s * step), b1 = __ldcg(src + s * step + 1);
+          a0.x += b0.x; a0.y += b0.y; a0.z += b0.z; a0.w += b0.w;
+          a1.x += b1.x; a1.y += b1.y; a1.z += b1.z; a1.w += b1.w;
+        }
+        float v[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+        if (views_vec && co + 8 <= cout) {
+          epilogue8<T>(e, v, rpix, an, co);
+          st8<T>(o.base, view_pixel_index(o, rpix, co), v);
+        } else {
+          epilogue_store_tail<T>(e, o, v, rpix, an, co, min(8, cout - co));
+        }
+      }
+      if (threadIdx.x == 0) D.counters[tile_id] = 0u;
     }
   }
 

@@ -20,6 +20,7 @@ batch signature so concurrent ``execute_fused`` callers never share one.
 from __future__ import annotations
 
 import ctypes as C
+import os
 import threading
 import time
 from dataclasses import dataclass
@@ -32,6 +33,10 @@ from .lower import COPY, DWCONV, EW, GAP, GEMM, POOL, MemberProgram, gemm_tiling
 from .planner import first_fit
 
 ALIGN = 256
+# split-K reduction: "kernel" = a separate deterministic reduction node (default,
+# measured faster at batch 1: its launch overlaps via PDL and it is spread over
+# the whole GPU); "fixup" = the last-arriving CTA of each tile reduces in-kernel
+SPLITK_MODE = os.environ.get("DFX_SPLITK", "kernel")
 _program_cache: dict[tuple[int, int], tuple] = {}
 _cache_lock = threading.Lock()
 
@@ -287,12 +292,17 @@ class ExecInstance:
         n_gemm = sum(1 for p, n in zip(progs, batch) for L in p.launches if L.kind == GEMM and n)
         self.act = rt.malloc(self.act_bytes)
         self.ws = rt.malloc(self.ws_bytes)
+        n_ctr = sum(t["mt_n"] * t["mt_p"] * t["mt_q"] * t["nt"]
+                    for pl in self.plans for t in pl.tilings.values() if t["splits"] > 1)
+        self.counters = rt.malloc(max(4 * n_ctr, 16))
+        self._ctr_used = 0
         self.descs = rt.malloc(max(n_gemm, 1) * C.sizeof(rt.GemmDesc))
         self.dev_in = rt.malloc(max(self.in_bytes, 16))
         self.dev_out = rt.malloc(max(self.out_bytes, 16))
         self.host_in = rt.host_alloc(max(self.in_bytes, 16))
         self.host_out = rt.host_alloc(max(self.out_bytes, 16))
         rt.memset(self.act, 0, self.act_bytes, self.stream)
+        rt.memset(self.counters, 0, max(4 * n_ctr, 16), self.stream)
         self.gemm_count = 0
         self.kernel_nodes = 0
         self.graph = self._build(progs, arena)
@@ -443,16 +453,20 @@ class ExecInstance:
             epi = self._epi(m, prog, L, n)
             d.epi = epi
             d.ws = (self.ws + self.ws_off[m]) if t["splits"] > 1 else None
+            fixup = t["splits"] > 1 and SPLITK_MODE == "fixup"
+            if fixup:                  # per-output-tile arrival counters (in-kernel fixup)
+                d.counters = self.counters + 4 * self._ctr_used
+                self._ctr_used += t["mt_n"] * t["mt_p"] * t["mt_q"] * t["nt"]
             slot = len(host_descs)
             host_descs.append(d)
             self.gemm_count += 1
             gl = rt.GemmLaunch(self.descs + slot * C.sizeof(rt.GemmDesc), 1, t["tiles"], t["bn"],
                                self.dtype)
             yield rt.OP_GEMM, gl
-            if t["splits"] > 1:
-                sp = rt.SplitKParams(self.ws + self.ws_off[m], t["splits"], n * out.h * out.w,
-                                     geo["cout"], t["nt"] * t["bn"], out, epi)
-                yield rt.OP_SPLITK, sp
+            if t["splits"] > 1 and not fixup:
+                yield rt.OP_SPLITK, rt.SplitKParams(self.ws + self.ws_off[m], t["splits"],
+                                                    n * out.h * out.w, geo["cout"],
+                                                    t["nt"] * t["bn"], out, epi)
         elif L.kind == DWCONV:
             geo = L.geom
             p = rt.DwconvParams(src, self._view(m, prog, L.dst, n), arena.addr(m, L.blobs["weight"]),
@@ -517,7 +531,7 @@ class ExecInstance:
 
     def free(self):
         self.graph.destroy()
-        for p in (self.act, self.ws, self.descs, self.dev_in, self.dev_out):
+        for p in (self.act, self.ws, self.counters, self.descs, self.dev_in, self.dev_out):
             rt.free(p)
         rt.host_free(self.host_in)
         rt.host_free(self.host_out)

@@ -577,8 +577,8 @@ def gemm_tiling(geom: dict, n: int, p: int, q: int, sm_count: int = 148) -> dict
     stages = math.ceil(geom["ksteps"] / kpack)
     base = m_tiles * nt
     splits = 1
-    if base < sm_count and stages >= 4:
-        splits = min(math.ceil(sm_count / base), stages // 2)
+    if base < sm_count and stages >= 8:
+        splits = min(math.ceil(sm_count / base), stages // 4)      # >= 4 stages per split
     sps = math.ceil(stages / max(splits, 1))
     splits = math.ceil(stages / sps)
     return dict(tn=tn, tp=tp, tq=tq, mt_n=mt[0], mt_p=mt[1], mt_q=mt[2], bn=bn, nt=nt,

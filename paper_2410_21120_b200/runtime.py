@@ -49,7 +49,7 @@ class GemmDesc(C.Structure):
                 ("pad_h", i32), ("pad_w", i32), ("cb", i32), ("cblocks", i32), ("ksteps", i32),
                 ("kpack", i32), ("stages", i32), ("splits", i32), ("stages_per_split", i32),
                 ("bn", i32), ("cout", i32), ("tile_begin", i32), ("tiles", i32), ("_pad0", i32),
-                ("out", View), ("epi", Epilogue), ("ws", vp), ("_pad1", i64 * 3)]
+                ("out", View), ("epi", Epilogue), ("ws", vp), ("counters", vp), ("_pad1", i64 * 2)]
 
 
 class GemmLaunch(C.Structure):
