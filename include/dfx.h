@@ -65,7 +65,9 @@ typedef enum dfx_op {
   DFX_OP_GAP = 5,      /* global average pool                              */
   DFX_OP_EW = 6,       /* affine/act/add/scale/copy on NHWC views          */
   DFX_OP_IN = 7,       /* fp32 CHW samples -> bf16 NHWC                    */
-  DFX_OP_OUT = 8       /* bf16 NHWC -> fp32 samples in logical CHW order   */
+  DFX_OP_OUT = 8,      /* bf16 NHWC -> fp32 samples in logical CHW order   */
+  DFX_OP_SE = 9        /* squeeze-excitation gate: GAP -> FC -> act -> FC -> gate,
+                          one 8-CTA cluster per image sharing data over DSMEM */
 } dfx_op;
 
 typedef enum dfx_dtype {
@@ -176,6 +178,19 @@ typedef struct dfx_out_params {
   dfx_view in;
   float* dst;                          /* n samples, each c*h*w fp32 in CHW order */
 } dfx_out_params;
+
+/* gate[n, c] = act2(b2[c] + sum_j w2[c][j] * act1(b1[j] + sum_k w1[j][k] * mean_hw x[n, :, :, k]))
+ * (global_avg_pool -> dense -> act -> dense -> act of the reference IR).
+ * w1 [cr][c], w2 [c][cr]: 16-bit, dtype of the views, row-major. */
+typedef struct dfx_se_params {
+  dfx_view in;                         /* x (n, h, w, c) */
+  dfx_view out;                        /* gate (n, 1, 1, c) */
+  const void* w1;
+  const float* b1;                     /* may be NULL */
+  const void* w2;
+  const float* b2;                     /* may be NULL */
+  int32_t cr, act1, act2, _pad;
+} dfx_se_params;
 
 /* ---- library / device ------------------------------------------------- */
 const char* dfx_last_error(void);

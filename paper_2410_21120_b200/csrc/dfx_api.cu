@@ -21,6 +21,7 @@ template <typename T> __global__ void pool_kernel(const __grid_constant__ dfx_po
 template <typename T> __global__ void gap_kernel(const __grid_constant__ dfx_gap_params P);
 template <typename T> __global__ void in_kernel(const __grid_constant__ dfx_in_params P);
 template <typename T> __global__ void out_kernel(const __grid_constant__ dfx_out_params P);
+template <typename T> __global__ void se_kernel(const __grid_constant__ dfx_se_params P);
 }  // namespace dfx
 
 // kernel instantiation for a storage dtype (DFX_F16 / DFX_BF16)
@@ -166,6 +167,16 @@ int config_for(int op, const void* params, size_t size, LaunchCfg* c) {
       c->grid = dim3(elementwise_grid(int64_t(p->in.n) * p->in.h * p->in.w * p->in.c, 256));
       return DFX_OK;
     }
+    case DFX_OP_SE: {
+      NEED(dfx_se_params);
+      const auto* p = static_cast<const dfx_se_params*>(params);
+      if (p->in.c > 4096 || p->cr > 512 || p->cr < 1)
+        return fail(DFX_E_UNSUPPORTED, "se: c=%d cr=%d beyond the cluster kernel's limits",
+                    p->in.c, p->cr);
+      c->func = DFX_PICK(se_kernel, p->in.dtype);
+      c->grid = dim3(8, unsigned(p->in.n));      // one 8-CTA cluster (__cluster_dims__) per image
+      return DFX_OK;
+    }
   }
 #undef NEED
   return fail(DFX_E_ARG, "unknown op %d", op);
@@ -204,7 +215,8 @@ int dfx_sizeof(const char* name) {
            {"dfx_gap_params", sizeof(dfx_gap_params)},
            {"dfx_ew_params", sizeof(dfx_ew_params)},
            {"dfx_in_params", sizeof(dfx_in_params)},
-           {"dfx_out_params", sizeof(dfx_out_params)}};
+           {"dfx_out_params", sizeof(dfx_out_params)},
+           {"dfx_se_params", sizeof(dfx_se_params)}};
   for (auto& e : t)
     if (!strcmp(e.n, name)) return e.s;
   return -1;

@@ -29,7 +29,7 @@ import numpy as np
 
 from . import runtime as rt
 from .graph_ir import LiveInterval
-from .lower import COPY, DWCONV, EW, GAP, GEMM, POOL, MemberProgram, gemm_tiling, lower_member
+from .lower import COPY, DWCONV, EW, GAP, GEMM, POOL, SE, MemberProgram, gemm_tiling, lower_member
 from .planner import first_fit
 
 ALIGN = 256
@@ -392,6 +392,9 @@ class ExecInstance:
             out = prog.values[L.dst]
             info.update(flops=2 * n * out.h * out.w * out.c * g["kh"] * g["kw"],
                         bytes=in_b + out_b + out.c * g["kh"] * g["kw"] * 4)
+        elif L.kind == SE:
+            g = L.geom
+            info.update(flops=4 * n * g["c"] * g["cr"], bytes=in_b + out_b + 2 * 2 * g["c"] * g["cr"])
         else:
             info.update(bytes=in_b + out_b + other_b)
         return info
@@ -486,6 +489,12 @@ class ExecInstance:
             cv = self._view(m, prog, L.geom["concat"], n)
             out = rt.View(cv.base, n, src.h, src.w, src.c, cv.pitch, L.geom["coff"], self.dtype)
             yield rt.OP_EW, rt.EwParams(src, out, rt.Epilogue())
+        elif L.kind == SE:
+            geo = L.geom
+            addr = (lambda r: arena.addr(m, L.blobs[r]) if r in L.blobs else None)
+            yield rt.OP_SE, rt.SeParams(src, self._view(m, prog, L.dst, n), addr("w1"), addr("b1"),
+                                        addr("w2"), addr("b2"), geo["cr"], rt.ACT[geo["act1"]],
+                                        rt.ACT[geo["act2"]])
         else:
             raise AssertionError(L.kind)
 

@@ -36,7 +36,8 @@ from .errors import UnsupportedOnDevice
 from .graph_ir import (ACTIVATION_KINDS, conv_geometry, infer_shapes, pool_geometry,
                        topo_order)
 
-GEMM, DWCONV, POOL, GAP, EW, COPY = "gemm", "dwconv", "pool", "gap", "ew", "copy"
+GEMM, DWCONV, POOL, GAP, EW, COPY, SE = "gemm", "dwconv", "pool", "gap", "ew", "copy", "se"
+SE_MAX_C, SE_MAX_CR = 4096, 512          # limits of dfx_fused.cu se_kernel
 
 
 def round_up(x: int, a: int) -> int:
@@ -166,6 +167,8 @@ class _Lowerer:
         self.blobs: dict[str, np.ndarray] = {}
         self.acc_owner: dict[str, str] = {}
         self.pending_weights: list = []
+        self.pending_se: list = []
+        self.precision = "fp16"
         self.keep_f32 = False
         self.debug_f32: dict[str, np.ndarray] = {}
 
@@ -250,6 +253,10 @@ class _Lowerer:
             self.launches.append(L)
             return
         if k == "global_avg_pool":
+            se = self.match_se(nid)
+            if se is not None:
+                self.launches.append(se)
+                return
             self.launches.append(Launch(GAP, [nid], self.src_of(nid), nid))
             return
         if k in ("flatten", "concat"):
@@ -459,7 +466,48 @@ class _Lowerer:
                 b.last = b.first
 
     # -------------------------------------------------------------- weights
+    def match_se(self, gap_id: str):
+        """global_avg_pool -> dense -> [act] -> dense -> [act] (a squeeze-excitation
+        gate) with single consumers along the chain: ONE cluster launch."""
+        chain = [gap_id]
+        cur = gap_id
+        fcs, acts = [], [None, None]
+        for which in (0, 1):
+            nxt = self.single_user(cur)
+            if nxt is None or self.g.nodes[nxt].kind != "dense":
+                return None
+            fcs.append(nxt)
+            chain.append(nxt)
+            cur = nxt
+            a = self.single_user(cur)
+            if a is not None and self.g.nodes[a].kind in ACTIVATION_KINDS:
+                acts[which] = self.g.nodes[a].kind
+                chain.append(a)
+                cur = a
+        c = self.dims(gap_id)[0]
+        cr = int(self.g.nodes[fcs[0]].attrs["units"])
+        if int(self.g.nodes[fcs[1]].attrs["units"]) != c or c > SE_MAX_C or cr > SE_MAX_CR:
+            return None
+        for n in chain[1:]:
+            self.absorbed[n] = gap_id
+        L = Launch(SE, chain, self.src_of(gap_id), cur,
+                   geom=dict(c=c, cr=cr, act1=acts[0], act2=acts[1], fc1=fcs[0], fc2=fcs[1]))
+        self.pending_se.append(L)
+        return L
+
     def pack_weights(self):
+        for L in self.pending_se:
+            for role, fc in (("1", L.geom["fc1"]), ("2", L.geom["fc2"])):
+                node = self.g.nodes[fc]
+                key = f"{fc}.w"
+                self.blobs[key] = to_storage_bits(self.warr(node, "weight"), self.precision)
+                L.blobs["w" + role] = key
+                if "bias" in node.weight_refs:
+                    b = self.warr(node, "bias")
+                    arr = np.zeros(round_up(len(b), 8), dtype=np.float32)
+                    arr[:len(b)] = b
+                    self.blobs[f"{fc}.b"] = arr
+                    L.blobs["b" + role] = f"{fc}.b"
         for L, wt4 in self.pending_weights:
             geo = L.geom
             if L.kind == DWCONV:

@@ -19,7 +19,7 @@ from .errors import DeviceError
 PKG = Path(__file__).resolve().parent
 LIB_PATH = PKG / "libdfx.so"
 
-OP_GEMM, OP_SPLITK, OP_DWCONV, OP_POOL, OP_GAP, OP_EW, OP_IN, OP_OUT = range(1, 9)
+OP_GEMM, OP_SPLITK, OP_DWCONV, OP_POOL, OP_GAP, OP_EW, OP_IN, OP_OUT, OP_SE = range(1, 10)
 ACT = {None: 0, "relu": 1, "hardswish": 2, "hardsigmoid": 3, "silu": 4, "sigmoid": 5}
 BIN_NONE, BIN_ADD, BIN_SCALE = 0, 1, 2
 DT_BF16, DT_F16 = 0, 1
@@ -90,16 +90,21 @@ class OutParams(C.Structure):
     _fields_ = [("inp", View), ("dst", vp)]
 
 
+class SeParams(C.Structure):
+    _fields_ = [("inp", View), ("out", View), ("w1", vp), ("b1", vp), ("w2", vp), ("b2", vp),
+                ("cr", i32), ("act1", i32), ("act2", i32), ("_pad", i32)]
+
+
 STRUCTS = {
     "dfx_view": View, "dfx_epilogue": Epilogue, "dfx_gemm_desc": GemmDesc,
     "dfx_gemm_launch": GemmLaunch, "dfx_splitk_params": SplitKParams,
     "dfx_dwconv_params": DwconvParams, "dfx_pool_params": PoolParams,
     "dfx_gap_params": GapParams, "dfx_ew_params": EwParams, "dfx_in_params": InParams,
-    "dfx_out_params": OutParams,
+    "dfx_out_params": OutParams, "dfx_se_params": SeParams,
 }
 OP_PARAMS = {OP_GEMM: GemmLaunch, OP_SPLITK: SplitKParams, OP_DWCONV: DwconvParams,
              OP_POOL: PoolParams, OP_GAP: GapParams, OP_EW: EwParams, OP_IN: InParams,
-             OP_OUT: OutParams}
+             OP_OUT: OutParams, OP_SE: SeParams}
 
 # every symbol include/dfx.h declares (tests check the .so exports all of them)
 EXPORTS = (

@@ -138,6 +138,22 @@ class Emulator:
         x = self.view(L.src)
         self.store(self.view(L.dst), x.mean(axis=(1, 2), keepdims=True))
 
+    def do_se(self, L):
+        g = L.geom
+        x = self.view(L.src)                                   # (n, h, w, c)
+        pooled = x.astype(np.float64).mean(axis=(1, 2))
+        w1 = storage_bits_to_f32(self.p.blobs[L.blobs["w1"]], self.p.precision).reshape(g["cr"], g["c"])
+        w2 = storage_bits_to_f32(self.p.blobs[L.blobs["w2"]], self.p.precision).reshape(g["c"], g["cr"])
+        h = pooled @ w1.T.astype(np.float64)
+        if "b1" in L.blobs:
+            h = h + self.p.blobs[L.blobs["b1"]][:g["cr"]]
+        h = _act(g["act1"], h.astype(np.float32))
+        o = h.astype(np.float64) @ w2.T.astype(np.float64)
+        if "b2" in L.blobs:
+            o = o + self.p.blobs[L.blobs["b2"]][:g["c"]]
+        o = _act(g["act2"], o.astype(np.float32))
+        self.store(self.view(L.dst), o[:, None, None, :])
+
     def do_ew(self, L):
         self.store(self.view(L.dst), self.epilogue(L, self.view(L.src)))
 
