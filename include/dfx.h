@@ -132,12 +132,19 @@ typedef struct __attribute__((aligned(64))) dfx_gemm_desc {
   int64_t _pad1[2];                
 } dfx_gemm_desc;
 
-typedef struct dfx_gemm_launch {
-  const dfx_gemm_desc* descs;      /* device pointer, ndesc entries */
+/* Kernel parameter of one GEMM launch.  A single problem travels inline
+ * (desc0, ndesc == 1): descriptor and tensor maps then sit in kernel-parameter
+ * space, read at launch without a global-memory round trip.  A grouped launch
+ * (ndesc > 1) reads `descs` from device memory, sorted by tile_begin. */
+typedef struct __attribute__((aligned(64))) dfx_gemm_launch {
+  const dfx_gemm_desc* descs;      /* device pointer, ndesc entries (ndesc > 1) */
   int32_t ndesc;
   int32_t total_tiles;             /* grid size */
   int32_t bn_max;                  /* sizes smem / TMEM */
   int32_t dtype;                   /* dfx_dtype of every problem */
+  int32_t nslots;                  /* smem pipeline depth, 2..8 */
+  int32_t _pad[9];
+  dfx_gemm_desc desc0;             /* the problem when ndesc == 1 */
 } dfx_gemm_launch;
 
 typedef struct dfx_splitk_params {

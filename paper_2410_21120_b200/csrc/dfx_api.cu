@@ -21,7 +21,7 @@ template <typename T> __global__ void pool_kernel(const __grid_constant__ dfx_po
 template <typename T> __global__ void gap_kernel(const __grid_constant__ dfx_gap_params P);
 template <typename T> __global__ void in_kernel(const __grid_constant__ dfx_in_params P);
 template <typename T> __global__ void out_kernel(const __grid_constant__ dfx_out_params P);
-template <typename T> __global__ void se_kernel(const __grid_constant__ dfx_se_params P);
+template <typename T, int CL> __global__ void se_kernel(const __grid_constant__ dfx_se_params P);
 }  // namespace dfx
 
 // kernel instantiation for a storage dtype (DFX_F16 / DFX_BF16)
@@ -31,8 +31,17 @@ template <typename T> __global__ void se_kernel(const __grid_constant__ dfx_se_p
 
 namespace {
 
+const void* se_func(int dt, int cl) {
+  if (cl == 16)
+    return dt == DFX_F16 ? reinterpret_cast<const void*>(&dfx::se_kernel<__half, 16>)
+                         : reinterpret_cast<const void*>(&dfx::se_kernel<__nv_bfloat16, 16>);
+  return dt == DFX_F16 ? reinterpret_cast<const void*>(&dfx::se_kernel<__half, 8>)
+                       : reinterpret_cast<const void*>(&dfx::se_kernel<__nv_bfloat16, 8>);
+}
+
 thread_local std::string g_err;
 int g_sm_count = 148;
+constexpr int kGemmSmemLimit = 227 * 1024;     // opt-in dynamic smem per CTA on sm_100
 
 int fail(int code, const char* fmt, ...) {
   char buf[512];
@@ -114,7 +123,12 @@ int config_for(int op, const void* params, size_t size, LaunchCfg* c) {
       c->func = DFX_PICK(gemm_kernel, p->dtype);
       c->grid = dim3(p->total_tiles);
       c->block = dim3(128);
-      c->smem = dfx::gemm_smem_bytes(p->bn_max) + 1024;
+      if (p->nslots < 2 || p->nslots > dfx::kMaxSlots)
+        return fail(DFX_E_ARG, "gemm: nslots %d", p->nslots);
+      c->smem = dfx::gemm_smem_bytes(p->bn_max, p->nslots) + 1024;
+      if (c->smem > size_t(kGemmSmemLimit))
+        return fail(DFX_E_ARG, "gemm: %zu B of shared memory (bn %d x %d slots)", c->smem,
+                    p->bn_max, p->nslots);
       return DFX_OK;
     }
     case DFX_OP_SPLITK: {
@@ -173,8 +187,13 @@ int config_for(int op, const void* params, size_t size, LaunchCfg* c) {
       if (p->in.c > 4096 || p->cr > 512 || p->cr < 1)
         return fail(DFX_E_UNSUPPORTED, "se: c=%d cr=%d beyond the cluster kernel's limits",
                     p->in.c, p->cr);
-      c->func = DFX_PICK(se_kernel, p->in.dtype);
-      c->grid = dim3(8, unsigned(p->in.n));      // one 8-CTA cluster (__cluster_dims__) per image
+      // one cluster per image: 8 CTAs, or 16 when the weight slices would not fit in smem
+      const int cl = dfx::se_smem_bytes(p->in.c, p->cr, 8) <= dfx::kSeSmemBudget ? 8 : 16;
+      c->func = se_func(p->in.dtype, cl);
+      c->grid = dim3(unsigned(cl), unsigned(p->in.n));
+      c->smem = size_t(dfx::se_smem_bytes(p->in.c, p->cr, cl));
+      if (c->smem > size_t(dfx::kSeSmemBudget))
+        return fail(DFX_E_UNSUPPORTED, "se: c=%d cr=%d needs %zu B of smem", p->in.c, p->cr, c->smem);
       return DFX_OK;
     }
   }
@@ -234,9 +253,14 @@ int dfx_init(int device) {
     return fail(DFX_E_NODEVICE, "device %d is sm_%d%d; libdfx is built for sm_100a", device,
                 prop.major, prop.minor);
   g_sm_count = prop.multiProcessorCount;
-  for (int dt : {int(DFX_BF16), int(DFX_F16)})
+  for (int dt : {int(DFX_BF16), int(DFX_F16)}) {
     CK(cudaFuncSetAttribute(DFX_PICK(gemm_kernel, dt), cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            dfx::gemm_smem_bytes(256) + 1024));
+                            kGemmSmemLimit));
+    for (int cl : {8, 16})
+      CK(cudaFuncSetAttribute(se_func(dt, cl), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              dfx::kSeSmemBudget));
+    CK(cudaFuncSetAttribute(se_func(dt, 16), cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  }
   return get_encode();
 }
 

@@ -129,8 +129,8 @@ DFX_DEV int64_t view_pixel_index(const dfx_view& v, int64_t pix, int c) {
 template <typename T>
 DFX_DEV float epilogue(const dfx_epilogue& e, float x, int64_t pix, int n, int c) {
   float v = x;
-  if (e.alpha) v = v * __ldg(e.alpha + c);
-  if (e.beta) v = v + __ldg(e.beta + c);
+  if (e.alpha) v = v * e.alpha[c];           // generic loads: alpha/beta may be staged in smem
+  if (e.beta) v = v + e.beta[c];
   v = act_apply(e.act1, v);
   if (e.binop == DFX_BIN_ADD) {
     v += ld1<T>(e.other.base, view_pixel_index(e.other, pix, c));
@@ -144,14 +144,14 @@ DFX_DEV float epilogue(const dfx_epilogue& e, float x, int64_t pix, int n, int c
 template <typename T>
 DFX_DEV void epilogue8(const dfx_epilogue& e, float* v, int64_t pix, int n, int c) {
   if (e.alpha) {
-    const float4 a0 = __ldg(reinterpret_cast<const float4*>(e.alpha + c));
-    const float4 a1 = __ldg(reinterpret_cast<const float4*>(e.alpha + c + 4));
+    const float4 a0 = *reinterpret_cast<const float4*>(e.alpha + c);
+    const float4 a1 = *reinterpret_cast<const float4*>(e.alpha + c + 4);
     v[0] *= a0.x; v[1] *= a0.y; v[2] *= a0.z; v[3] *= a0.w;
     v[4] *= a1.x; v[5] *= a1.y; v[6] *= a1.z; v[7] *= a1.w;
   }
   if (e.beta) {
-    const float4 b0 = __ldg(reinterpret_cast<const float4*>(e.beta + c));
-    const float4 b1 = __ldg(reinterpret_cast<const float4*>(e.beta + c + 4));
+    const float4 b0 = *reinterpret_cast<const float4*>(e.beta + c);
+    const float4 b1 = *reinterpret_cast<const float4*>(e.beta + c + 4);
     v[0] += b0.x; v[1] += b0.y; v[2] += b0.z; v[3] += b0.w;
     v[4] += b1.x; v[5] += b1.y; v[6] += b1.z; v[7] += b1.w;
   }
@@ -187,6 +187,15 @@ __device__ __noinline__ void epilogue_store_tail(const dfx_epilogue& e, const df
 
 // True when 8-channel vector access at channel c is legal for view v.
 DFX_DEV bool vec8_ok(const dfx_view& v, int c) { return ((v.coff + c) & 7) == 0; }
+
+// ---------------------------------------------------------------- debug timeline
+// DFX_TL(i): a %globaltimer probe.  dfx_gemm.cu defines it (and the probe array)
+// when built with -DDFX_TIMELINE; everywhere else it compiles to nothing.
+#ifndef DFX_TL
+#define DFX_TL(i) \
+  do {            \
+  } while (0)
+#endif
 
 // ---------------------------------------------------------------- programmatic dependent launch
 // Graph edges between libdfx kernels are programmatic: a kernel may start
@@ -255,6 +264,15 @@ DFX_DEV void tma_load_2d(void* dst, const void* tmap, uint64_t* bar, int c0, int
       "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
       " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
       "l"(tmap), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+      : "memory");
+}
+
+// Non-tensor bulk copy global -> own CTA's shared memory (16-B aligned, size % 16 == 0).
+DFX_DEV void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
 }
 
@@ -344,14 +362,30 @@ DFX_DEV uint32_t umma_idesc_f16(uint32_t n, int dtype) {
 }
 
 constexpr int kGemmThreads = 128;
-constexpr int kSlots = 4;
-constexpr int kStageABytes = 128 * 64 * 2;   // 128 rows x 64 bf16
-constexpr int kHeaderBytes = 1024;
+constexpr int kMaxSlots = 8;                 // pipeline depth is a launch parameter, 2..8
+constexpr int kStageABytes = 128 * 64 * 2;   // 128 rows x 64 16-bit
+constexpr int kHeaderBytes = 1024;           // barriers + staged descriptor
+constexpr int kEpiBytes = 2048;              // alpha[256] + beta[256] fp32, staged
+constexpr int kSlotsOffset = kHeaderBytes + kEpiBytes;   // 1024-B aligned
 
 __host__ __device__ inline int gemm_slot_bytes(int bn_max) { return kStageABytes + bn_max * 128; }
-__host__ __device__ inline int gemm_smem_bytes(int bn_max) {
-  return kHeaderBytes + kSlots * gemm_slot_bytes(bn_max);
+__host__ __device__ inline int gemm_smem_bytes(int bn_max, int nslots) {
+  return kSlotsOffset + nslots * gemm_slot_bytes(bn_max);
 }
+// ---- squeeze-excitation cluster kernel geometry (dfx_fused.cu)
+constexpr int kSeThreads = 256;
+constexpr int kSeMaxC = 4096;      // pooled channels held per CTA
+constexpr int kSeMaxCr = 512;      // hidden units held per CTA
+constexpr int kSeSmemBudget = 190 * 1024;
+__host__ __device__ inline int se_chan_slice(int C, int cl) { return ((C + cl * 8 - 1) / (cl * 8)) * 8; }
+__host__ __device__ inline int se_hid_slice(int Cr, int cl) { return (Cr + cl - 1) / cl; }
+// dynamic smem of one CTA: fc1 slice + fc2 slice (16-bit), each 16-B aligned
+__host__ __device__ inline int se_smem_bytes(int C, int Cr, int cl) {
+  const int b1 = ((se_hid_slice(Cr, cl) * C * 2) + 15) & ~15;
+  const int b2 = ((se_chan_slice(C, cl) * Cr * 2) + 15) & ~15;
+  return b1 + b2;
+}
+
 __host__ __device__ inline uint32_t tmem_cols_for(int bn) {
   uint32_t c = 32;
   while (c < uint32_t(bn)) c <<= 1;

@@ -18,22 +18,56 @@
 // The B tile is a 2-D TMA box of the packed [cout][K] weight matrix.
 //
 // Warp roles (128 threads): warp 0 lane 0 = TMA producer, warp 1 lane 0 =
-// MMA issuer, warp 2 = TMEM allocator; all four warps run the epilogue
-// (warp w owns TMEM lanes 32w..32w+31 = tile rows).  The problem descriptor
-// is staged in shared memory once and every loop runs on register copies of
-// its fields (the PTX "memory" clobbers would otherwise force a global reload
-// of each field per iteration).
+// MMA issuer, warp 2 = TMEM allocator, warps 2-3 stage the epilogue vectors;
+// all four warps run the epilogue (warp w owns TMEM lanes 32w..32w+31 = tile
+// rows).  Latency structure (batch-1 layers are latency-bound, measured with
+// the DFX_TIMELINE probes below):
+//   * a single problem's descriptor and tensor maps are a __grid_constant__
+//     kernel parameter (no global round trip before the first TMA);
+//   * everything static -- weight tiles of the first `nslots` stages (up to 8
+//     deep), the epilogue's folded-BN/bias vectors -- is requested BEFORE
+//     griddepcontrol.wait, i.e. while the predecessor kernel still runs;
+//   * the descriptor is copied to smem and loops run on register copies of its
+//     fields (the PTX "memory" clobbers would otherwise reload them per step).
+#ifdef DFX_TIMELINE
+// block-0 %globaltimer probes (ns), read back with dfx_debug_timeline
+__device__ unsigned long long dfx_timeline[64];
+#define DFX_TL(i)                                                \
+  do {                                                           \
+    if (blockIdx.x == 0 && blockIdx.y == 0) {                    \
+      unsigned long long _t;                                     \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(_t));     \
+      dfx_timeline[i] = _t;                                      \
+    }                                                            \
+  } while (0)
+#endif
+
 #include "dfx_common.cuh"
+
+// Debug builds (-DDFX_TIMELINE): copy the kernel timeline probes (ns).  Not in
+// dfx.h: a development hook, not part of the ABI.
+extern "C" int dfx_debug_timeline(unsigned long long* out, int n) {
+#ifdef DFX_TIMELINE
+  return cudaMemcpyFromSymbol(out, dfx_timeline, sizeof(unsigned long long) * (n < 64 ? n : 64)) ==
+                 cudaSuccess
+             ? 0
+             : -1;
+#else
+  (void)out;
+  (void)n;
+  return -4;
+#endif
+}
 
 namespace dfx {
 
 struct GemmHeader {
-  uint64_t full[kSlots];
-  uint64_t empty[kSlots];
+  uint64_t full[kMaxSlots];
+  uint64_t empty[kMaxSlots];
   uint64_t accum;
   uint32_t tmem_base;
   uint32_t last_split;    // split-K: this CTA arrived last for its output tile
-  uint32_t _pad[4];
+  uint32_t _pad[12];
   dfx_gemm_desc desc;     // 64-B aligned copy of this CTA's problem
 };
 static_assert(sizeof(GemmHeader) <= kHeaderBytes, "gemm smem header overflow");
@@ -46,17 +80,29 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   GemmHeader* hdr = reinterpret_cast<GemmHeader*>(smem);
-  uint8_t* slots = smem + kHeaderBytes;
+  float* s_alpha = reinterpret_cast<float*>(smem + kHeaderBytes);
+  float* s_beta = s_alpha + 256;
+  uint8_t* slots = smem + kSlotsOffset;
   const int slot_bytes = gemm_slot_bytes(L.bn_max);
+  const int nslots = L.nslots;
+  if (threadIdx.x == 0) DFX_TL(0);                 // CTA start
+#ifdef DFX_TIMELINE
+  if (threadIdx.x == 0 && blockIdx.x == 0) dfx_timeline[40] = clock64();
+#endif
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const int bid = blockIdx.x;
 
-  int pi = 0;
-  for (int i = 1; i < L.ndesc; ++i)
-    if (L.descs[i].tile_begin <= bid) pi = i;
-  const dfx_gemm_desc* gd = L.descs + pi;          // global copy: tensor maps live here
+  const dfx_gemm_desc* gd;                         // tensor maps are read through this
+  if (L.ndesc == 1 && L._pad[0] == 0) {
+    gd = &L.desc0;                                 // kernel-parameter space
+  } else {
+    int pi = 0;
+    for (int i = 1; i < L.ndesc; ++i)
+      if (L.descs[i].tile_begin <= bid) pi = i;
+    gd = L.descs + pi;
+  }
 
   // ---- stage the descriptor in smem (32 x 16 B), barriers, TMEM
   if (threadIdx.x < sizeof(dfx_gemm_desc) / 16)
@@ -64,14 +110,19 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         reinterpret_cast<const uint4*>(gd)[threadIdx.x];
   const uint32_t tmem_cols = tmem_cols_for(L.bn_max);
   if (threadIdx.x == 0) {
-    for (int i = 0; i < kSlots; ++i) {
+    DFX_TL(7);                                     // descriptor copied
+    for (int i = 0; i < nslots; ++i) {
       mbar_init(&hdr->full[i], 1);
       mbar_init(&hdr->empty[i], 1);
     }
     mbar_init(&hdr->accum, 1);
     fence_barrier_init();
+    DFX_TL(8);                                     // barriers initialised
   }
-  if (warp == 2) tmem_alloc(&hdr->tmem_base, tmem_cols);
+  if (warp == 2) {
+    tmem_alloc(&hdr->tmem_base, tmem_cols);
+    if (lane == 0) DFX_TL(9);                      // TMEM allocated
+  }
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(gd->tmap_a);
     tma_prefetch_desc(gd->tmap_b);
@@ -79,6 +130,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  if (threadIdx.x == 0) DFX_TL(10);                // prologue barrier passed
   const uint32_t tmem_base = hdr->tmem_base;
   const dfx_gemm_desc& D = hdr->desc;
 
@@ -98,6 +150,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   const int bn = D.bn, cb = D.cb, kpack = D.kpack, ksteps = D.ksteps;
   const int st_begin = split * D.stages_per_split;
   const int st_end = min(D.stages, st_begin + D.stages_per_split);
+  const int co_base = ntile * bn;
+  const int cout = D.cout;
 
   const int sub_a = 128 * cb * 2;     // bytes of one K-step A sub-tile
   const int sub_b = bn * cb * 2;      // bytes of one K-step B sub-tile
@@ -109,10 +163,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     const uint32_t box_a_bytes = uint32_t(cb) * 2u * tq * tp * tn;
     const void* tma = gd->tmap_a;
     const void* tmb = gd->tmap_b;
-    const int nrow = ntile * bn;
-    // Weights are static: the first kSlots stages' B tiles are requested before
+    // Weights are static: the first nslots stages' B tiles are requested before
     // the programmatic dependency resolves, overlapping the predecessor's tail.
-    const int npre = min(kSlots, st_end - st_begin);
+    const int npre = min(nslots, st_end - st_begin);
     for (int it = 0; it < npre; ++it) {
       const int st = st_begin + it;
       uint8_t* b_dst = slots + it * slot_bytes + kStageABytes;
@@ -120,9 +173,12 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       const int nk = min(kpack, ksteps - k0);
       mbar_arrive_expect_tx(&hdr->full[it], nk * (box_a_bytes + uint32_t(sub_b)));
       for (int j = 0; j < nk; ++j)
-        tma_load_2d(b_dst + j * sub_b, tmb, &hdr->full[it], (k0 + j) * cb, nrow);
+        tma_load_2d(b_dst + j * sub_b, tmb, &hdr->full[it], (k0 + j) * cb, co_base);
+      if (it < 8) DFX_TL(30 + it);                 // B prefetch of stage `it` issued (30..37)
     }
+    DFX_TL(1);                                     // weight prefetch issued
     griddep_wait();
+    DFX_TL(2);                                     // dependency resolved
     for (int it = 0; it < npre; ++it) {
       const int st = st_begin + it;
       uint8_t* a_dst = slots + it * slot_bytes;
@@ -137,10 +193,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         tma_load_4d(a_dst + j * sub_a, tma, &hdr->full[it], cblk * cb, qbase + s, pbase + r, n0);
       }
     }
+    DFX_TL(29);                                    // all prefetched stages' A loads issued
     int it = npre;
     for (int st = st_begin + npre; st < st_end; ++st, ++it) {
-      const int slot = it % kSlots;
-      const uint32_t par = (it / kSlots) & 1;
+      const int slot = it % nslots;
+      const uint32_t par = (it / nslots) & 1;
       mbar_wait(&hdr->empty[slot], par ^ 1);
       uint8_t* a_dst = slots + slot * slot_bytes;
       uint8_t* b_dst = a_dst + kStageABytes;
@@ -154,7 +211,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         const int r = rs / S;
         const int s = rs - r * S;
         tma_load_4d(a_dst + j * sub_a, tma, &hdr->full[slot], cblk * cb, qbase + s, pbase + r, n0);
-        tma_load_2d(b_dst + j * sub_b, tmb, &hdr->full[slot], kstep * cb, nrow);
+        tma_load_2d(b_dst + j * sub_b, tmb, &hdr->full[slot], kstep * cb, co_base);
       }
     }
   } else if (warp == 1 && lane == 0) {
@@ -165,9 +222,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     uint32_t accumulate = 0;
     int it = 0;
     for (int st = st_begin; st < st_end; ++st, ++it) {
-      const int slot = it % kSlots;
-      const uint32_t par = (it / kSlots) & 1;
+      const int slot = it % nslots;
+      const uint32_t par = (it / nslots) & 1;
       mbar_wait(&hdr->full[slot], par);
+      if (it == 0) DFX_TL(3);                      // first stage landed
+      if (it > 0 && it < 9) DFX_TL(12 + it);       // later stages landed (13..20)
       tc_fence_after();
       const uint32_t a_base = smem_u32(slots + slot * slot_bytes);
       const uint32_t b_base = a_base + kStageABytes;
@@ -180,23 +239,41 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           accumulate = 1;
         }
       }
+      if (it < 8) DFX_TL(21 + it);                 // stage's MMAs issued (21..28)
       umma_commit(&hdr->empty[slot]);
     }
     umma_commit(&hdr->accum);
+    DFX_TL(4);                                     // last MMA issued
+  } else if (warp >= 2 && splits == 1) {
+    // ================= stage this N tile's epilogue vectors (static data) in smem
+    const int ti = threadIdx.x - 64;
+    const float* ga = D.epi.alpha;
+    const float* gb = D.epi.beta;
+    for (int i = ti; i < bn; i += 64) {
+      const int c = co_base + i;
+      if (ga) s_alpha[i] = c < cout ? ga[c] : 0.f;
+      if (gb) s_beta[i] = c < cout ? gb[c] : 0.f;
+    }
   }
   __syncwarp();
 
   // ================= epilogue: TMEM -> registers -> 16-bit NHWC (or fp32 split-K partials)
-  const dfx_epilogue e = D.epi;
+  dfx_epilogue e = D.epi;
+  if (splits == 1) {                          // read the smem copies (offset by the tile base)
+    if (e.alpha) e.alpha = s_alpha - co_base;
+    if (e.beta) e.beta = s_beta - co_base;
+  }
   const dfx_view o = D.out;
-  const int cout = D.cout, P = D.p, Q = D.q, N = D.n;
+  const int P = D.p, Q = D.q, N = D.n;
   float* const ws = D.ws;
   const int ldw = D.nt * bn;
 
   griddep_wait();                              // residual / output buffers of predecessors
   mbar_wait(&hdr->accum, 0);
+  if (threadIdx.x == 0) DFX_TL(5);             // accumulator complete
   tc_fence_after();
   griddep_launch();                            // successor may start its prologue now
+  __syncthreads();                             // staged epilogue vectors visible
 
   const int row = threadIdx.x;                 // tile row == TMEM lane
   const int qi = row % tq;
@@ -206,14 +283,15 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   const bool valid = row < tn * tp * tq && on < N && op < P && oq < Q;
   const int64_t pix = (int64_t(on) * P + op) * Q + oq;
   const uint32_t lane_addr = tmem_base + (uint32_t(warp * 32) << 16);
-  const int co_base = ntile * bn;
   const int ncols = min(bn, ((cout - co_base) + 15) & ~15);
   const bool views_vec = vec8_ok(o, 0) && (e.binop == DFX_BIN_NONE || vec8_ok(e.other, 0));
 
   const int64_t plane = int64_t(N) * P * Q * ldw;      // one split's partials
+  if (threadIdx.x == 0) DFX_TL(11);                    // epilogue starts
   for (int c0 = 0; c0 < ncols; c0 += 16) {
     float v[16];
     tmem_ld16(lane_addr + uint32_t(c0), v);
+    if (c0 == 0 && threadIdx.x == 0) DFX_TL(12);       // first TMEM load back
     if (!valid) continue;
     const int co = co_base + c0;
     if (splits > 1) {
@@ -237,9 +315,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   }
 
   if (splits > 1 && D.counters != nullptr) {
-    // ---- in-kernel split-K fixup: the last CTA to arrive for this output tile sums
-    // all splits' partials in split order (deterministic), applies the epilogue and
-    // resets the tile's counter for the next graph replay.
+    // ---- in-kernel split-K fixup (DFX_SPLITK=fixup): the last CTA to arrive for
+    // this output tile sums all splits' partials in split order (deterministic),
+    // applies the epilogue and resets the tile's counter for the next replay.
     const int tile_id = mi + mt_total * ntile;
     __threadfence();
     __syncthreads();
@@ -248,9 +326,6 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     __syncthreads();
     if (hdr->last_split) {
       __threadfence();
-      // all 128 threads cooperate: item = (tile row, 8-channel group); adjacent
-      // threads take adjacent groups of one row (coalesced); the split loop is
-      // unrolled so its loads are independent and in flight together
       const int c8n = ncols / 8;
       for (int item = threadIdx.x; item < 128 * c8n; item += kGemmThreads) {
         const int r = item / c8n;
@@ -262,16 +337,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         const float4* src = reinterpret_cast<const float4*>(ws + rpix * ldw + co);
         const int64_t step = plane / 4;
         float4 a0 = __ldcg(src), a1 = __ldcg(src + 1);
-        int s = 1;
-        for (; s + 1 < splits; s += 2) {
-          const float4 b0 = __ldcg(src + s * step), b1 = __ldcg(src + s * step + 1);
-          const float4 c0 = __ldcg(src + (s + 1) * step), c1 = __ldcg(src + (s + 1) * step + 1);
-          a0.x += b0.x; a0.y += b0.y; a0.z += b0.z; a0.w += b0.w;
-          a1.x += b1.x; a1.y += b1.y; a1.z += b1.z; a1.w += b1.w;
-          a0.x += c0.x; a0.y += c0.y; a0.z += c0.z; a0.w += c0.w;
-          a1.x += c1.x; a1.y += c1.y; a1.z += c1.z; a1.w += c1.w;
-        }
-        if (s < splits) {
+        for (int s = 1; s < splits; ++s) {
           const float4 b0 = __ldcg(src + s * step), b1 = __ldcg(src + s * step + 1);
           a0.x += b0.x; a0.y += b0.y; a0.z += b0.z; a0.w += b0.w;
           a1.x += b1.x; a1.y += b1.y; a1.z += b1.z; a1.w += b1.w;
@@ -290,6 +356,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 
   tc_fence_before();
   __syncthreads();
+  if (threadIdx.x == 0) DFX_TL(6);             // epilogue stored
+#ifdef DFX_TIMELINE
+  if (threadIdx.x == 0 && blockIdx.x == 0) dfx_timeline[41] = clock64();
+#endif
   if (warp == 2) tmem_dealloc(tmem_base, tmem_cols);
 }
 

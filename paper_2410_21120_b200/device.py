@@ -58,6 +58,20 @@ def _align(x, a=ALIGN):
     return (x + a - 1) // a * a
 
 
+GEMM_SMEM_LIMIT = 227 * 1024 - 1024          # minus the kernel's 1 KB alignment slack
+GEMM_SMEM_FIXED = 1024 + 2048                # barriers/descriptor + epilogue vectors
+
+
+def gemm_slots(bn: int, tiles: int, sm_count: int = 148) -> int:
+    """Pipeline depth of a GEMM launch: as deep as shared memory allows (<= 8)
+    when the grid fits in one wave -- every extra slot is another weight tile
+    requested before griddepcontrol.wait -- else 4, leaving room for two CTAs
+    per SM on narrow tiles."""
+    slot = 128 * 64 * 2 + bn * 128
+    fit = (GEMM_SMEM_LIMIT - GEMM_SMEM_FIXED) // slot
+    return max(2, min(8 if tiles <= sm_count else 4, fit))
+
+
 # ------------------------------------------------------------------------------ weights
 
 def arena_layout(programs: list[MemberProgram]):
@@ -464,7 +478,8 @@ class ExecInstance:
             host_descs.append(d)
             self.gemm_count += 1
             gl = rt.GemmLaunch(self.descs + slot * C.sizeof(rt.GemmDesc), 1, t["tiles"], t["bn"],
-                               self.dtype)
+                               self.dtype, gemm_slots(t["bn"], t["tiles"], self.dag.sm_count))
+            gl.desc0 = d                    # single problem: descriptor in kernel-param space
             yield rt.OP_GEMM, gl
             if t["splits"] > 1 and not fixup:
                 yield rt.OP_SPLITK, rt.SplitKParams(self.ws + self.ws_off[m], t["splits"],

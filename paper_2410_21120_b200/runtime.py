@@ -54,7 +54,7 @@ class GemmDesc(C.Structure):
 
 class GemmLaunch(C.Structure):
     _fields_ = [("descs", vp), ("ndesc", i32), ("total_tiles", i32), ("bn_max", i32),
-                ("dtype", i32)]
+                ("dtype", i32), ("nslots", i32), ("_pad", i32 * 9), ("desc0", GemmDesc)]
 
 
 class SplitKParams(C.Structure):
