@@ -379,11 +379,9 @@ constexpr int kSeMaxCr = 512;      // hidden units held per CTA
 constexpr int kSeSmemBudget = 190 * 1024;
 __host__ __device__ inline int se_chan_slice(int C, int cl) { return ((C + cl * 8 - 1) / (cl * 8)) * 8; }
 __host__ __device__ inline int se_hid_slice(int Cr, int cl) { return (Cr + cl - 1) / cl; }
-// dynamic smem of one CTA: fc1 slice + fc2 slice (16-bit), each 16-B aligned
+// dynamic smem of one CTA: its channel rows of fc1^T and of fc2 (16-bit, [rows][Cr])
 __host__ __device__ inline int se_smem_bytes(int C, int Cr, int cl) {
-  const int b1 = ((se_hid_slice(Cr, cl) * C * 2) + 15) & ~15;
-  const int b2 = ((se_chan_slice(C, cl) * Cr * 2) + 15) & ~15;
-  return b1 + b2;
+  return 2 * (((se_chan_slice(C, cl) * Cr * 2) + 15) & ~15);
 }
 
 __host__ __device__ inline uint32_t tmem_cols_for(int bn) {

@@ -6,34 +6,64 @@
 // extension activations) as ONE launch instead of 3-5 dependent nodes.
 //
 // One CL-CTA cluster per image (CL = 8, or 16 when the weight slices would not
-// fit in shared memory).  CTA r of the cluster
-//   0. before griddepcontrol.wait (weights are static): one thread bulk-copies
-//      its contiguous weight slices -- fc1 rows [h_lo, h_hi) and fc2 rows
-//      [c_lo, c_hi) -- into shared memory (cp.async.bulk + mbarrier),
-//   1. pools channel slice r of the image (fixed-order sums, fp32, x fp32(1/HW)),
-//   2. after cluster.sync, gathers the whole pooled vector from the peers'
-//      shared memory over DSMEM and computes hidden units [h_lo, h_hi) of fc1
-//      (+ bias, act1): one warp per unit, fixed-order warp reduction,
-//   3. after cluster.sync, gathers the hidden vector over DSMEM and computes
-//      gate channels [c_lo, c_hi) of fc2 (+ bias, act2), one thread per channel,
-//   4. writes its gate slice (16-bit) and waits for the cluster so no CTA's
-//      shared memory disappears while a peer still reads it.
-// Deterministic: fixed summation orders, no atomics.
+// fit in shared memory).  CTA r owns the channel slice [c_lo, c_hi):
+//   0. before griddepcontrol.wait (weights are static) one thread bulk-copies
+//      the slice's rows of fc1^T [C][Cr] and fc2 [C][Cr] -- both contiguous --
+//      into shared memory (cp.async.bulk + mbarrier);
+//   1. pools its channels: every thread's 16-B loads for all of its pixels are
+//      issued before any is summed, then a fixed-order smem reduction;
+//   2. computes fc1 PARTIAL sums over its own channels for every hidden unit
+//      (no gather of the pooled vector), publishes them in smem;
+//   3. cluster.sync; reads the CL partial vectors over DSMEM and sums them in
+//      rank order (the same order in every CTA -> identical hidden vectors),
+//      + bias, act1;
+//   4. computes the gate for its channels (8 lanes per channel, 16-B weight
+//      reads, shuffle reduction), + bias, act2, 16-bit store;
+//   5. cluster.sync so no CTA's smem disappears while a peer still reads it.
+// Deterministic: fixed summation orders, no atomics.  Timeline probes
+// (-DDFX_TIMELINE): dfx_debug_timeline_se.
 #include <cooperative_groups.h>
 
+#ifdef DFX_TIMELINE
+__device__ unsigned long long dfx_timeline_se[64];
+#define DFX_TL(i)                                                \
+  do {                                                           \
+    if (blockIdx.x == 0 && blockIdx.y == 0) {                    \
+      unsigned long long _t;                                     \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(_t));     \
+      dfx_timeline_se[i] = _t;                                   \
+    }                                                            \
+  } while (0)
+#endif
+
 #include "dfx_common.cuh"
+
+extern "C" int dfx_debug_timeline_se(unsigned long long* out, int n) {
+#ifdef DFX_TIMELINE
+  return cudaMemcpyFromSymbol(out, dfx_timeline_se, sizeof(unsigned long long) * (n < 64 ? n : 64)) ==
+                 cudaSuccess
+             ? 0
+             : -1;
+#else
+  (void)out;
+  (void)n;
+  return -4;
+#endif
+}
 
 namespace cg = cooperative_groups;
 
 namespace dfx {
 
+constexpr int kSeMaxSlice = 512;   // channels per CTA (C <= 4096 -> <= 512 at CL = 8)
 
 template <typename T, int CL>
 __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kSeThreads)
     se_kernel(const __grid_constant__ dfx_se_params P) {
-  __shared__ float pooled[kSeMaxC];          // full pooled vector (gathered)
-  __shared__ float hidden[kSeMaxCr];         // full hidden vector (gathered)
-  __shared__ float part[32][64 + 4];
+  __shared__ float pooled[kSeMaxSlice];      // this CTA's channels only
+  __shared__ float partial[kSeMaxCr];        // fc1 partial sums over this CTA's channels
+  __shared__ float hidden[kSeMaxCr];         // full hidden vector (rank-order reduction)
+  __shared__ float red[kSeThreads * 8 + 8];  // pooling reduction scratch
   __shared__ __align__(8) uint64_t wbar;
   extern __shared__ __align__(16) uint8_t wsm[];
   cg::cluster_group cluster = cg::this_cluster();
@@ -44,138 +74,149 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kSeThreads)
   const int hw = in.h * in.w;
   const int cs = se_chan_slice(C, CL);
   const int c_lo = min(C, rank * cs), c_hi = min(C, c_lo + cs);
-  const int hs = se_hid_slice(Cr, CL);
-  const int h_lo = min(Cr, rank * hs), h_hi = min(Cr, h_lo + hs);
-  const T* w1g = reinterpret_cast<const T*>(P.w1);
-  const T* w2g = reinterpret_cast<const T*>(P.w2);
-  // staged copies (weights rows are contiguous; C, Cr multiples of 8 keep every
-  // slice 16-B aligned, otherwise the kernel reads global memory directly)
-  const bool staged = (C & 7) == 0 && (Cr & 7) == 0;
-  const int b1 = ((hs * C * 2) + 15) & ~15;
-  const T* w1s = reinterpret_cast<const T*>(wsm);                 // rows [h_lo, h_hi)
-  const T* w2s = reinterpret_cast<const T*>(wsm + b1);            // rows [c_lo, c_hi)
+  const int nch = c_hi - c_lo;
+  const T* w1g = reinterpret_cast<const T*>(P.w1);    // fc1^T  [C][Cr]
+  const T* w2g = reinterpret_cast<const T*>(P.w2);    // fc2    [C][Cr]
+  const bool staged = (C & 7) == 0 && (Cr & 7) == 0;  // 16-B aligned slices
+  const int sb = ((cs * Cr * 2) + 15) & ~15;
+  const T* w1 = staged ? reinterpret_cast<const T*>(wsm) : w1g + int64_t(c_lo) * Cr;
+  const T* w2 = staged ? reinterpret_cast<const T*>(wsm + sb) : w2g + int64_t(c_lo) * Cr;
 
-  // ---- 0. weight slices -> smem, issued before the dependency resolves
+  // ---- 0. weight slices -> smem, before the dependency resolves
   if (threadIdx.x == 0) {
+    DFX_TL(0);
     mbar_init(&wbar, 1);
     fence_barrier_init();
-    if (staged) {
-      const uint32_t n1 = uint32_t(h_hi - h_lo) * C * 2, n2 = uint32_t(c_hi - c_lo) * Cr * 2;
-      mbar_arrive_expect_tx(&wbar, n1 + n2);
-      if (n1) bulk_load(wsm, w1g + int64_t(h_lo) * C, n1, &wbar);
-      if (n2) bulk_load(wsm + b1, w2g + int64_t(c_lo) * Cr, n2, &wbar);
+    const uint32_t bytes = uint32_t(nch) * Cr * 2;
+    if (staged && bytes) {
+      mbar_arrive_expect_tx(&wbar, 2 * bytes);
+      bulk_load(wsm, w1g + int64_t(c_lo) * Cr, bytes, &wbar);
+      bulk_load(wsm + sb, w2g + int64_t(c_lo) * Cr, bytes, &wbar);
     } else {
       mbar_arrive(&wbar);
     }
   }
   griddep_wait();
   griddep_launch();
+  if (threadIdx.x == 0) DFX_TL(1);
 
-  // ---- 1. pool channels [c_lo, c_hi): 64-channel chunks, 32 spatial rows
-  const int tx = threadIdx.x & 7, ty = threadIdx.x >> 3;
-  const bool vec_in = (in.coff & 7) == 0;
-  for (int cc = c_lo; cc < c_hi; cc += 64) {
-    const int c = cc + tx * 8;
-    const int nl = max(0, min(8, c_hi - c));
-    float acc[8];
+  // ---- 1. pool: thread = (channel group g, pixel stripe y); all loads in flight first
+  const int G = (nch + 7) / 8;                        // channel groups of this CTA
+  const int stripes = G ? kSeThreads / G : 1;
+  const int g = threadIdx.x % max(G, 1), y = threadIdx.x / max(G, 1);
+  float acc[8];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) acc[i] = 0.f;
-    if (nl > 0) {
-      const int64_t base = view_pixel_index(in, int64_t(n) * hw, c);
-      if (nl == 8 && vec_in) {
-        int s = ty;
-        for (; s + 32 < hw; s += 64) {
-          float x0[8], x1[8];
-          ld8<T>(in.base, base + int64_t(s) * in.pitch, x0);
-          ld8<T>(in.base, base + int64_t(s + 32) * in.pitch, x1);
+  for (int i = 0; i < 8; ++i) acc[i] = 0.f;
+  if (G && y < stripes) {
+    const int c = c_lo + g * 8;
+    const int nl = min(8, c_hi - c);
+    const int64_t base = view_pixel_index(in, int64_t(n) * hw, c);
+    if (nl == 8 && ((in.coff + c) & 7) == 0) {
+      int s = y;
+      for (; s + 3 * stripes < hw; s += 4 * stripes) {      // 4 independent 16-B loads
+        float x0[8], x1[8], x2[8], x3[8];
+        ld8<T>(in.base, base + int64_t(s) * in.pitch, x0);
+        ld8<T>(in.base, base + int64_t(s + stripes) * in.pitch, x1);
+        ld8<T>(in.base, base + int64_t(s + 2 * stripes) * in.pitch, x2);
+        ld8<T>(in.base, base + int64_t(s + 3 * stripes) * in.pitch, x3);
 #pragma unroll
-          for (int i = 0; i < 8; ++i) acc[i] += x0[i] + x1[i];
-        }
-        for (; s < hw; s += 32) {
-          float x[8];
-          ld8<T>(in.base, base + int64_t(s) * in.pitch, x);
-#pragma unroll
-          for (int i = 0; i < 8; ++i) acc[i] += x[i];
-        }
-      } else {
-        for (int s = ty; s < hw; s += 32)
-          for (int i = 0; i < nl; ++i) acc[i] += ld1<T>(in.base, base + int64_t(s) * in.pitch + i);
+        for (int i = 0; i < 8; ++i) acc[i] += (x0[i] + x1[i]) + (x2[i] + x3[i]);
       }
-    }
+      for (; s < hw; s += stripes) {
+        float x[8];
+        ld8<T>(in.base, base + int64_t(s) * in.pitch, x);
 #pragma unroll
-    for (int i = 0; i < 8; ++i) part[ty][tx * 8 + i] = acc[i];
-    __syncthreads();
-    if (threadIdx.x < 64 && cc + threadIdx.x < c_hi) {
-      float s = 0.f;
-      for (int r = 0; r < 32; ++r) s += part[r][threadIdx.x];
-      pooled[cc + threadIdx.x] = s * (1.0f / float(hw));
-    }
-    __syncthreads();
-  }
-  cluster.sync();
-
-  // ---- 2. gather the pooled vector, fc1 slice
-  for (int r = 0; r < CL; ++r) {
-    if (r == rank) continue;
-    const int lo = min(C, r * cs), hi = min(C, lo + cs);
-    const float* remote = cluster.map_shared_rank(pooled, r);
-    for (int c = lo + threadIdx.x; c < hi; c += kSeThreads) pooled[c] = remote[c];
-  }
-  mbar_wait(&wbar, 0);                       // weight slices landed
-  __syncthreads();
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int j = h_lo + warp; j < h_hi; j += kSeThreads / 32) {
-    float acc = 0.f;
-    if (staged) {
-      const T* row = w1s + int64_t(j - h_lo) * C;
-      for (int k = lane * 8; k < C; k += 256) {
-        float wv[8];
-        ld8<T>(row, k, wv);
-#pragma unroll
-        for (int i = 0; i < 8; ++i) acc = fmaf(wv[i], pooled[k + i], acc);
+        for (int i = 0; i < 8; ++i) acc[i] += x[i];
       }
     } else {
-      const T* row = w1g + int64_t(j) * C;
-      for (int k = lane; k < C; k += 32) acc = fmaf(Elt<T>::to_f(row[k]), pooled[k], acc);
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-    if (lane == 0) {
-      float a[8] = {acc + (P.b1 ? P.b1[j] : 0.f), 0, 0, 0, 0, 0, 0, 0};
-      act8(P.act1, a);
-      hidden[j] = a[0];
+      for (int s = y; s < hw; s += stripes)
+        for (int i = 0; i < nl; ++i) acc[i] += ld1<T>(in.base, base + int64_t(s) * in.pitch + i);
     }
   }
-  cluster.sync();
+#pragma unroll
+  for (int i = 0; i < 8; ++i) red[threadIdx.x * 8 + i] = acc[i];
+  __syncthreads();
+  for (int k = threadIdx.x; k < nch; k += kSeThreads) {      // fixed stripe order
+    const int gg = k / 8, ii = k % 8;
+    float s = 0.f;
+    for (int yy = 0; yy < stripes; ++yy) s += red[(yy * G + gg) * 8 + ii];
+    pooled[k] = s * (1.0f / float(hw));
+  }
+  if (threadIdx.x == 0) DFX_TL(2);
+  mbar_wait(&wbar, 0);                                       // weight slices landed
+  __syncthreads();
+  if (threadIdx.x == 0) DFX_TL(3);
 
-  // ---- 3. gather the hidden vector, fc2 slice -> gate
-  for (int r = 0; r < CL; ++r) {
-    if (r == rank) continue;
-    const int lo = min(Cr, r * hs), hi = min(Cr, lo + hs);
-    const float* remote = cluster.map_shared_rank(hidden, r);
-    for (int j = lo + threadIdx.x; j < hi; j += kSeThreads) hidden[j] = remote[j];
+  // ---- 2. fc1 partial sums over this CTA's channels: thread (unit j, k-quarter q);
+  // consecutive threads read consecutive units of one row (conflict-free), the
+  // KQ k-partitions are combined in fixed order through smem
+  {
+    const int KQ = Cr >= kSeThreads ? 1 : kSeThreads / Cr;
+    const int kq_len = (nch + KQ - 1) / KQ;
+    for (int t = threadIdx.x; t < Cr * KQ; t += kSeThreads) {
+      const int j = t % Cr, q = t / Cr;
+      const int k0 = q * kq_len, k1 = min(nch, k0 + kq_len);
+      float s0 = 0.f, s1 = 0.f;
+      int k = k0;
+      for (; k + 1 < k1; k += 2) {
+        s0 = fmaf(Elt<T>::to_f(w1[int64_t(k) * Cr + j]), pooled[k], s0);
+        s1 = fmaf(Elt<T>::to_f(w1[int64_t(k + 1) * Cr + j]), pooled[k + 1], s1);
+      }
+      if (k < k1) s0 = fmaf(Elt<T>::to_f(w1[int64_t(k) * Cr + j]), pooled[k], s0);
+      red[t] = s0 + s1;
+    }
+    __syncthreads();
+    for (int j = threadIdx.x; j < Cr; j += kSeThreads) {
+      float s = 0.f;
+      for (int q = 0; q < KQ; ++q) s += red[q * Cr + j];
+      partial[j] = s;
+    }
+  }
+  if (threadIdx.x == 0) DFX_TL(4);
+  cluster.sync();
+  if (threadIdx.x == 0) DFX_TL(5);
+
+  // ---- 3. hidden = act1(b1 + sum over ranks of the partials), rank order
+  for (int j = threadIdx.x; j < Cr; j += kSeThreads) {
+    float v[CL];
+#pragma unroll
+    for (int r = 0; r < CL; ++r) v[r] = cluster.map_shared_rank(partial, r)[j];
+    float s = 0.f;
+#pragma unroll
+    for (int r = 0; r < CL; ++r) s += v[r];
+    float a[8] = {s + (P.b1 ? P.b1[j] : 0.f), 0, 0, 0, 0, 0, 0, 0};
+    act8(P.act1, a);
+    hidden[j] = a[0];
   }
   __syncthreads();
+  if (threadIdx.x == 0) DFX_TL(6);
+
+  // ---- 4. gate for this CTA's channels: thread per channel, hidden vector
+  // broadcast from smem, weight rows read as 16-B vectors
   const dfx_view& out = P.out;
-  for (int c = c_lo + threadIdx.x; c < c_hi; c += kSeThreads) {
-    float acc = 0.f;
+  for (int k = threadIdx.x; k < nch; k += kSeThreads) {
+    const T* row = w2 + int64_t(k) * Cr;
+    float s0 = 0.f, s1 = 0.f;
     if (staged) {
-      const T* row = w2s + int64_t(c - c_lo) * Cr;
       for (int j = 0; j < Cr; j += 8) {
         float wv[8];
         ld8<T>(row, j, wv);
-#pragma unroll
-        for (int i = 0; i < 8; ++i) acc = fmaf(wv[i], hidden[j + i], acc);
+        s0 = fmaf(wv[0], hidden[j], s0); s1 = fmaf(wv[1], hidden[j + 1], s1);
+        s0 = fmaf(wv[2], hidden[j + 2], s0); s1 = fmaf(wv[3], hidden[j + 3], s1);
+        s0 = fmaf(wv[4], hidden[j + 4], s0); s1 = fmaf(wv[5], hidden[j + 5], s1);
+        s0 = fmaf(wv[6], hidden[j + 6], s0); s1 = fmaf(wv[7], hidden[j + 7], s1);
       }
     } else {
-      const T* row = w2g + int64_t(c) * Cr;
-      for (int j = 0; j < Cr; ++j) acc = fmaf(Elt<T>::to_f(row[j]), hidden[j], acc);
+      for (int j = 0; j < Cr; ++j) s0 = fmaf(Elt<T>::to_f(row[j]), hidden[j], s0);
     }
-    float a[8] = {acc + (P.b2 ? P.b2[c] : 0.f), 0, 0, 0, 0, 0, 0, 0};
+    const int c = c_lo + k;
+    float a[8] = {s0 + s1 + (P.b2 ? P.b2[c] : 0.f), 0, 0, 0, 0, 0, 0, 0};
     act8(P.act2, a);
     st1<T>(out.base, int64_t(n) * out.pitch + out.coff + c, a[0]);
   }
+  if (threadIdx.x == 0) DFX_TL(7);
   cluster.sync();        // keep this CTA's smem alive until every peer finished reading it
+  if (threadIdx.x == 0) DFX_TL(8);
 }
 
 #define DFX_SE_INST(T, CL) template __global__ void se_kernel<T, CL>(const __grid_constant__ dfx_se_params);

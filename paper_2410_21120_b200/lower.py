@@ -500,7 +500,11 @@ class _Lowerer:
             for role, fc in (("1", L.geom["fc1"]), ("2", L.geom["fc2"])):
                 node = self.g.nodes[fc]
                 key = f"{fc}.w"
-                self.blobs[key] = to_storage_bits(self.warr(node, "weight"), self.precision)
+                wt = self.warr(node, "weight")            # (out, in)
+                # fc1 is stored transposed ([C][Cr]) so each cluster CTA's channel
+                # slice of both FCs is one contiguous block (dfx_fused.cu se_kernel)
+                self.blobs[key] = to_storage_bits(np.ascontiguousarray(wt.T) if role == "1" else wt,
+                                                  self.precision)
                 L.blobs["w" + role] = key
                 if "bias" in node.weight_refs:
                     b = self.warr(node, "bias")

@@ -142,7 +142,7 @@ class Emulator:
         g = L.geom
         x = self.view(L.src)                                   # (n, h, w, c)
         pooled = x.astype(np.float64).mean(axis=(1, 2))
-        w1 = storage_bits_to_f32(self.p.blobs[L.blobs["w1"]], self.p.precision).reshape(g["cr"], g["c"])
+        w1 = storage_bits_to_f32(self.p.blobs[L.blobs["w1"]], self.p.precision).reshape(g["c"], g["cr"]).T
         w2 = storage_bits_to_f32(self.p.blobs[L.blobs["w2"]], self.p.precision).reshape(g["c"], g["cr"])
         h = pooled @ w1.T.astype(np.float64)
         if "b1" in L.blobs:
