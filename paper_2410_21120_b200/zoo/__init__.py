@@ -47,6 +47,7 @@ class Net:
                  init: str = "kaiming_fan_out"):
         self.model_id = model_id
         self.init = init
+        self.beta_shift = 0.0           # mean of BN beta (see inception_v3)
         self.input_dims = tuple(input_dims)
         self.rng = np.random.default_rng(seed)
         self.calib = calib or {}
@@ -140,10 +141,13 @@ class Net:
         return self._add(nid, "dense", src, {"units": units, "fan_in": fan_in}, refs,
                          out_dims=(units,))
 
-    def bn(self, nid, src, eps=1e-5):
+    def bn(self, nid, src, eps=1e-5, gamma_scale=1.0):
+        """gamma ~ U(0.5, 1.5) * gamma_scale (gamma_scale < 1 on the last BN of a
+        residual branch: the small residual-branch gain of trained ResNets, cf.
+        torchvision's zero_init_residual), beta ~ N(0, 0.1)."""
         c = self._in_dims(src)[0]
-        gamma = self.rng.uniform(0.5, 1.5, c).astype(F32)
-        beta = (self.rng.standard_normal(c) * 0.1).astype(F32)
+        gamma = (self.rng.uniform(0.5, 1.5, c) * gamma_scale).astype(F32)
+        beta = (self.rng.standard_normal(c) * 0.1 + self.beta_shift).astype(F32)
         mean = np.asarray(self.calib.get(f"{nid}:mean", np.zeros(c)), F32)
         var = np.asarray(self.calib.get(f"{nid}:var", np.ones(c)), F32)
         refs = {r: self._put(f"{nid}.{r}", (c,), v)
@@ -337,13 +341,141 @@ def efficientnet_v2_l(model_id="efficientnet_v2_l", seed=1604, calib=None, res=2
     return n.build(x)
 
 
+# ----------------------------------------------------------------------------- ResNet-50 / 152
+
+RESNET_BRANCH_GAIN = 0.2
+
+def _resnet(model_id, seed, calib, res, classes, layers, branch_gain=RESNET_BRANCH_GAIN):
+    n = Net(model_id, (3, res, res), seed, calib)
+    x = n.conv("stem_conv", None, 64, 7, stride=2, pad=3)
+    x = n.act("stem_relu", n.bn("stem_bn", x), "relu")
+    x = n.pool("stem_pool", x, "maxpool2d", 3, stride=2, pad=1)
+    cin = 64
+    for li, (blocks, planes) in enumerate(zip(layers, (64, 128, 256, 512)), start=1):
+        for bi in range(1, blocks + 1):
+            p = f"l{li}_b{bi:02d}"
+            stride = 2 if (bi == 1 and li > 1) else 1
+            inp = x
+            t = n.act(f"{p}_relu1", n.bn(f"{p}_bn1", n.conv(f"{p}_conv1", x, planes, 1, pad=0)), "relu")
+            t = n.act(f"{p}_relu2", n.bn(f"{p}_bn2", n.conv(f"{p}_conv2", t, planes, 3, stride=stride)), "relu")
+            t = n.bn(f"{p}_bn3", n.conv(f"{p}_conv3", t, planes * 4, 1, pad=0), gamma_scale=branch_gain)
+            if bi == 1:
+                inp = n.bn(f"{p}_dsbn", n.conv(f"{p}_dsconv", x, planes * 4, 1, stride=stride, pad=0))
+            x = n.act(f"{p}_relu3", n.add(f"{p}_add", t, inp), "relu")
+            cin = planes * 4
+    x = n.gap("pool", x)
+    x = n.dense("fc", x, classes, init="torch_linear")
+    return n.build(x)
+
+
+def resnet50(model_id="resnet50", seed=1605, calib=None, res=224, classes=1000):
+    return _resnet(model_id, seed, calib, res, classes, (3, 4, 6, 3))
+
+
+def resnet152(model_id="resnet152", seed=1606, calib=None, res=224, classes=1000):
+    return _resnet(model_id, seed, calib, res, classes, (3, 8, 36, 3))
+
+
+# ----------------------------------------------------------------------------- Inception-v3
+
+# Mean of the synthetic BN betas in Inception-v3.  With zero-mean betas the
+# random-init net (no residual path) flips about half of its ReLU signs per
+# layer and the logits become chaotic in the input: fp16 storage noise then
+# reads as a 4% logit error.  A positive shift keeps it smooth (fp16 error
+# 0.8%) while the logits still vary by ~19% across inputs.
+INCEPTION_BETA_SHIFT = 0.5
+
+
+def inception_v3(model_id="inception_v3", seed=1607, calib=None, res=299, classes=1000,
+                 beta_shift=None):
+    """torchvision inception_v3 (eval, no aux head): BasicConv2d = conv + BN(1e-3) + ReLU."""
+    n = Net(model_id, (3, res, res), seed, calib)
+    n.beta_shift = INCEPTION_BETA_SHIFT if beta_shift is None else beta_shift
+
+    def basic(nid, src, cout, k, stride=1, pad=0):
+        x = n.conv(f"{nid}_conv", src, cout, k, stride=stride, pad=pad)
+        return n.act(f"{nid}_relu", n.bn(f"{nid}_bn", x, 1e-3), "relu")
+
+    def block_a(p, x, pool_features):
+        b1 = basic(f"{p}_b1x1", x, 64, 1)
+        b5 = basic(f"{p}_b5x5_2", basic(f"{p}_b5x5_1", x, 48, 1), 64, 5, pad=2)
+        bd = basic(f"{p}_b3x3dbl_1", x, 64, 1)
+        bd = basic(f"{p}_b3x3dbl_3", basic(f"{p}_b3x3dbl_2", bd, 96, 3, pad=1), 96, 3, pad=1)
+        bp = basic(f"{p}_bpool", n.pool(f"{p}_avg", x, "avgpool2d", 3, stride=1, pad=1), pool_features, 1)
+        return n.concat(f"{p}_cat", [b1, b5, bd, bp])
+
+    def block_b(p, x):
+        b3 = basic(f"{p}_b3x3", x, 384, 3, stride=2)
+        bd = basic(f"{p}_b3x3dbl_1", x, 64, 1)
+        bd = basic(f"{p}_b3x3dbl_3", basic(f"{p}_b3x3dbl_2", bd, 96, 3, pad=1), 96, 3, stride=2)
+        bp = n.pool(f"{p}_max", x, "maxpool2d", 3, stride=2)
+        return n.concat(f"{p}_cat", [b3, bd, bp])
+
+    def block_c(p, x, c7):
+        b1 = basic(f"{p}_b1x1", x, 192, 1)
+        b7 = basic(f"{p}_b7x7_1", x, c7, 1)
+        b7 = basic(f"{p}_b7x7_2", b7, c7, (1, 7), pad=(0, 3))
+        b7 = basic(f"{p}_b7x7_3", b7, 192, (7, 1), pad=(3, 0))
+        bd = basic(f"{p}_b7x7dbl_1", x, c7, 1)
+        bd = basic(f"{p}_b7x7dbl_2", bd, c7, (7, 1), pad=(3, 0))
+        bd = basic(f"{p}_b7x7dbl_3", bd, c7, (1, 7), pad=(0, 3))
+        bd = basic(f"{p}_b7x7dbl_4", bd, c7, (7, 1), pad=(3, 0))
+        bd = basic(f"{p}_b7x7dbl_5", bd, 192, (1, 7), pad=(0, 3))
+        bp = basic(f"{p}_bpool", n.pool(f"{p}_avg", x, "avgpool2d", 3, stride=1, pad=1), 192, 1)
+        return n.concat(f"{p}_cat", [b1, b7, bd, bp])
+
+    def block_d(p, x):
+        b3 = basic(f"{p}_b3x3_2", basic(f"{p}_b3x3_1", x, 192, 1), 320, 3, stride=2)
+        b7 = basic(f"{p}_b7x7x3_1", x, 192, 1)
+        b7 = basic(f"{p}_b7x7x3_2", b7, 192, (1, 7), pad=(0, 3))
+        b7 = basic(f"{p}_b7x7x3_3", b7, 192, (7, 1), pad=(3, 0))
+        b7 = basic(f"{p}_b7x7x3_4", b7, 192, 3, stride=2)
+        bp = n.pool(f"{p}_max", x, "maxpool2d", 3, stride=2)
+        return n.concat(f"{p}_cat", [b3, b7, bp])
+
+    def block_e(p, x):
+        b1 = basic(f"{p}_b1x1", x, 320, 1)
+        b3 = basic(f"{p}_b3x3_1", x, 384, 1)
+        b3 = n.concat(f"{p}_b3x3_cat", [basic(f"{p}_b3x3_2a", b3, 384, (1, 3), pad=(0, 1)),
+                                        basic(f"{p}_b3x3_2b", b3, 384, (3, 1), pad=(1, 0))])
+        bd = basic(f"{p}_b3x3dbl_2", basic(f"{p}_b3x3dbl_1", x, 448, 1), 384, 3, pad=1)
+        bd = n.concat(f"{p}_b3x3dbl_cat", [basic(f"{p}_b3x3dbl_3a", bd, 384, (1, 3), pad=(0, 1)),
+                                           basic(f"{p}_b3x3dbl_3b", bd, 384, (3, 1), pad=(1, 0))])
+        bp = basic(f"{p}_bpool", n.pool(f"{p}_avg", x, "avgpool2d", 3, stride=1, pad=1), 192, 1)
+        return n.concat(f"{p}_cat", [b1, b3, bd, bp])
+
+    x = basic("c1a", None, 32, 3, stride=2)
+    x = basic("c2a", x, 32, 3)
+    x = basic("c2b", x, 64, 3, pad=1)
+    x = n.pool("pool1", x, "maxpool2d", 3, stride=2)
+    x = basic("c3b", x, 80, 1)
+    x = basic("c4a", x, 192, 3)
+    x = n.pool("pool2", x, "maxpool2d", 3, stride=2)
+    x = block_a("m5b", x, 32)
+    x = block_a("m5c", x, 64)
+    x = block_a("m5d", x, 64)
+    x = block_b("m6a", x)
+    for p, c7 in (("m6b", 128), ("m6c", 160), ("m6d", 160), ("m6e", 192)):
+        x = block_c(p, x, c7)
+    x = block_d("m7a", x)
+    x = block_e("m7b", x)
+    x = block_e("m7c", x)
+    x = n.gap("pool", x)
+    x = n.dense("fc", x, classes, init="torch_linear")
+    return n.build(x)
+
+
 BUILDERS = {
     "vgg16": vgg16,
     "mobilenet_v3_large": mobilenet_v3_large,
     "densenet161": densenet161,
     "efficientnet_v2_l": efficientnet_v2_l,
+    "resnet50": resnet50,
+    "resnet152": resnet152,
+    "inception_v3": inception_v3,
 }
 NORTH_STAR = ("vgg16", "mobilenet_v3_large", "densenet161", "efficientnet_v2_l")
+EIGHT_MODEL_CNNS = NORTH_STAR + ("resnet50", "resnet152", "inception_v3")
 PAIR = ("vgg16", "mobilenet_v3_large")
 
 

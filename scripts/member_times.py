@@ -4,22 +4,31 @@ sys.path.insert(0, '.')
 import numpy as np
 from paper_2410_21120_b200 import zoo, runtime as rt
 from paper_2410_21120_b200.device import DeviceDag
-ap = argparse.ArgumentParser(); ap.add_argument("--batch", type=int, default=1); a = ap.parse_args()
-models = [zoo.build(n) for n in zoo.NORTH_STAR]
+ap = argparse.ArgumentParser()
+ap.add_argument("--batch", type=int, default=1)
+ap.add_argument("--set", choices=("north", "eight"), default="north")
+a = ap.parse_args()
+names = zoo.NORTH_STAR if a.set == "north" else zoo.EIGHT_MODEL_CNNS
+models = [zoo.build(n) for n in names]
+
+
 def timeit(dag, batch, K=30):
     inst = dag.acquire(batch)
-    inst.upload_inputs([np.random.default_rng(0).standard_normal((b, 3, 224, 224)).astype(np.float32) for b in batch])
+    inst.upload_inputs([np.random.default_rng(0).standard_normal((b,) + tuple(g.input_spec.dims)).astype(np.float32)
+                        for b, (g, _) in zip(batch, dag.members)])
     for _ in range(3): inst.launch_graph()
     inst.sync(); e0, e1 = rt.Event(), rt.Event(); e0.record(inst.stream)
     for _ in range(K): inst.launch_graph()
     e1.record(inst.stream); return e0.elapsed_ms(e1) / K, inst.kernel_nodes
-for (g, w), name in zip(models, zoo.NORTH_STAR):
+
+
+for (g, w), name in zip(models, names):
     d = DeviceDag([(g, w)])
     ms, nodes = timeit(d, (a.batch,))
     print(f"{name:22s} alone: {ms:7.3f} ms  nodes {nodes:5d}  {ms / nodes * 1e3:6.2f} us/node", flush=True)
 d = DeviceDag(models)
-ms, nodes = timeit(d, tuple([a.batch] * 4))
+ms, nodes = timeit(d, tuple([a.batch] * len(models)))
 print(f"{'fused (concurrent)':22s}      {ms:7.3f} ms  nodes {nodes:5d}")
 d = DeviceDag(models, mode="sequential")
-ms, nodes = timeit(d, tuple([a.batch] * 4))
+ms, nodes = timeit(d, tuple([a.batch] * len(models)))
 print(f"{'fused (sequential)':22s}      {ms:7.3f} ms  nodes {nodes:5d}")

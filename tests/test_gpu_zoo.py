@@ -45,6 +45,33 @@ def test_four_model_fused_dag_parity(models):
     assert max(report.values()) < TOL, report
 
 
+def _check(g, w, x, got):
+    ref = run_fast(g, w, x)
+    err = np.abs(got - ref).max(axis=1) / np.abs(ref).max(axis=1)
+    srt = np.sort(ref, axis=1)
+    margin = (srt[:, -1] - srt[:, -2]) / np.abs(ref).max(axis=1)
+    decided = margin > 2 * err
+    assert np.all(ref.argmax(1)[decided] == got.argmax(1)[decided]), g.model_id
+    return float(err.max())
+
+
+@pytest.mark.slow
+def test_seven_cnn_fused_dag_mixed_batches():
+    """The CNN part of the 8-model config: seven members,
+    different per-member batch sizes in ONE fused launch."""
+    models = [zoo.build(n) for n in zoo.EIGHT_MODEL_CNNS]
+    dag = fuse.fuse_models(models)
+    rng = np.random.default_rng(78)
+    batches = dict(zip(zoo.EIGHT_MODEL_CNNS, (1, 2, 4, 3, 1, 2, 2)))
+    xs = {g.model_id: rng.standard_normal((batches[g.model_id],) + tuple(g.input_spec.dims)).astype(np.float32)
+          for g, _ in models}
+    outs = fuse.execute_fused(dag, {g.model_id: [Tensor(g.input_spec, v) for v in xs[g.model_id]]
+                                    for g, _ in models})
+    report = {g.model_id: _check(g, w, xs[g.model_id], np.stack([t.values for t in outs[g.model_id]]))
+              for g, w in models}
+    assert max(report.values()) < TOL, report
+
+
 def test_batch_one_matches_batched(models):
     """A member's logits do not depend on the batch it was computed in."""
     g, w = models[1]

@@ -21,7 +21,14 @@ TV = {
     "mobilenet_v3_large": lambda: tv.models.mobilenet_v3_large(),
     "densenet161": lambda: tv.models.densenet161(),
     "efficientnet_v2_l": lambda: tv.models.efficientnet_v2_l(),
+    "resnet50": lambda: tv.models.resnet50(),
+    "resnet152": lambda: tv.models.resnet152(),
+    "inception_v3": lambda: tv.models.inception_v3(aux_logits=False, init_weights=False),
 }
+
+
+def _input(g, seed, n):
+    return np.random.default_rng(seed).standard_normal((n,) + tuple(g.input_spec.dims)).astype(np.float32)
 
 
 def _load_into_torchvision(name, g, w):
@@ -55,26 +62,31 @@ def _load_into_torchvision(name, g, w):
 
 
 @pytest.mark.slow
-@pytest.mark.parametrize("name", zoo.NORTH_STAR)
+@pytest.mark.parametrize("name", zoo.EIGHT_MODEL_CNNS)
 def test_builder_and_oracle_match_torchvision(name):
     torch.set_num_threads(8)
     g, w = zoo.build(name)
     model = _load_into_torchvision(name, g, w)
-    xs = np.random.default_rng(11).standard_normal((2, 3, 224, 224)).astype(np.float32)
+    xs = _input(g, 11, 2)
     with torch.no_grad():
-        ref = model(torch.from_numpy(xs)).numpy()
+        t32 = model(torch.from_numpy(xs)).numpy()
+        t64 = model.double()(torch.from_numpy(xs).double()).numpy()
     got = run_fast(g, w, xs)
-    err = np.abs(got - ref).max(axis=1) / np.abs(ref).max(axis=1)
-    # fp32 reassociation noise (BLAS vs oneDNN) grows with depth: EfficientNetV2-L's
-    # ~300 layers land near 7e-5; the shallower nets stay near 1e-5
-    assert err.max() < (1e-4 if name == "efficientnet_v2_l" else 2e-5), err
+
+    def rel(a):
+        return (np.abs(a - t64).max(axis=1) / np.abs(t64).max(axis=1)).max()
+
+    # Reference = torchvision in fp64.  The oracle (fp32) must be as close to it as
+    # torchvision's own fp32 forward is (deep residual nets reach ~3e-4 of pure
+    # fp32 noise, ResNet-152); a semantic mismatch shows up at >= 1e-2.
+    assert rel(got) <= max(2e-5, 2.0 * rel(t32)), (rel(got), rel(t32))
 
 
 @pytest.mark.slow
-@pytest.mark.parametrize("name", zoo.NORTH_STAR)
+@pytest.mark.parametrize("name", zoo.EIGHT_MODEL_CNNS)
 def test_calibrated_logits_are_input_sensitive(name):
     g, w = zoo.build(name)
-    xs = np.random.default_rng(12).standard_normal((4, 3, 224, 224)).astype(np.float32)
+    xs = _input(g, 12, 4)
     out = run_fast(g, w, xs)
     spread = np.abs(out - out.mean(axis=0)).max() / np.abs(out).max()
     assert spread > 0.05, spread
