@@ -34,7 +34,7 @@
 extern "C" {
 #endif
 
-#define DFX_ABI_VERSION 2
+#define DFX_ABI_VERSION 3
 
 typedef enum dfx_status {
   DFX_OK = 0,
@@ -48,7 +48,8 @@ typedef enum dfx_status {
 
 typedef enum dfx_act {
   DFX_ACT_NONE = 0, DFX_ACT_RELU = 1, DFX_ACT_HARDSWISH = 2,
-  DFX_ACT_HARDSIGMOID = 3, DFX_ACT_SILU = 4, DFX_ACT_SIGMOID = 5
+  DFX_ACT_HARDSIGMOID = 3, DFX_ACT_SILU = 4, DFX_ACT_SIGMOID = 5,
+  DFX_ACT_GELU = 6     /* exact: 0.5 x (1 + erf(x / sqrt 2)) */
 } dfx_act;
 
 typedef enum dfx_binop {
@@ -66,8 +67,11 @@ typedef enum dfx_op {
   DFX_OP_EW = 6,       /* affine/act/add/scale/copy on NHWC views          */
   DFX_OP_IN = 7,       /* fp32 CHW samples -> bf16 NHWC                    */
   DFX_OP_OUT = 8,      /* bf16 NHWC -> fp32 samples in logical CHW order   */
-  DFX_OP_SE = 9        /* squeeze-excitation gate: GAP -> FC -> act -> FC -> gate,
+  DFX_OP_SE = 9,       /* squeeze-excitation gate: GAP -> FC -> act -> FC -> gate,
                           one 8-CTA cluster per image sharing data over DSMEM */
+  DFX_OP_LN = 10,      /* layer norm over channels of token rows (+ token select) */
+  DFX_OP_TOKENS = 11,  /* patch grid -> [class token; patches] + pos_embedding */
+  DFX_OP_ATTN = 12     /* multi-head softmax attention over packed q|k|v rows */
 } dfx_op;
 
 typedef enum dfx_dtype {
@@ -176,9 +180,14 @@ typedef struct dfx_ew_params {
   dfx_epilogue epi;
 } dfx_ew_params;
 
+/* block <= 1: out[n, h, w, c] = src[n][c][h][w].
+ * block = b > 1 (space-to-depth, feeds a patchify conv with kernel = stride = b
+ * as a 1x1 GEMM): out has h = H/b, w = W/b, c = b*b*C and
+ * out[n, y, x, (r*b + s)*C + c] = src[n][c][y*b + r][x*b + s]. */
 typedef struct dfx_in_params {
-  const float* src;                    /* n samples, each c*h*w fp32 in CHW order */
+  const float* src;                    /* n samples, each C*H*W fp32 in CHW order */
   dfx_view out;
+  int32_t block, _pad;
 } dfx_in_params;
 
 typedef struct dfx_out_params {
@@ -198,6 +207,40 @@ typedef struct dfx_se_params {
   const float* b2;                     /* may be NULL */
   int32_t cr, act1, act2, _pad;
 } dfx_se_params;
+
+/* Token tensors (ViT) are views with h = 1, w = L tokens, c = channels.
+ * out[n, 0, t, c] = norm ? (x - mean_t) * rsqrt(var_t + eps) * gamma[c] + beta[c]
+ *                        : x                     with x = in[n, 0, t, c],
+ * for t < out.w <= in.w (out.w = 1 after "layernorm -> select_token 0");
+ * mean/var over the c channels of row t (biased variance). */
+typedef struct dfx_ln_params {
+  dfx_view in;
+  dfx_view out;
+  const float* gamma;
+  const float* beta;
+  float eps;
+  int32_t norm, _pad[2];
+} dfx_ln_params;
+
+/* out[n, 0, 0, c] = cls[c] + pos[0][c];
+ * out[n, 0, 1 + h*W + w, c] = in[n, h, w, c] + pos[1 + h*W + w][c]. */
+typedef struct dfx_tokens_params {
+  dfx_view in;                         /* patch grid (n, H, W, c) */
+  dfx_view out;                        /* tokens (n, 1, 1 + H*W, c) */
+  const float* cls;                    /* [c] */
+  const float* pos;                    /* [1 + H*W][c] */
+} dfx_tokens_params;
+
+/* qkv (n, 1, L, 3C) packed q | k | v (column blocks); per head h (columns
+ * h*d .. h*d + d - 1 of each block, d = C / heads, d == 64):
+ * out[n, 0, :, h*d : h*d + d] = softmax(q_h k_h^T * scale) v_h. */
+typedef struct dfx_attn_params {
+  dfx_view qkv;
+  dfx_view out;                        /* (n, 1, L, C) */
+  int32_t heads;
+  float scale;
+  int32_t _pad[2];
+} dfx_attn_params;
 
 /* ---- library / device ------------------------------------------------- */
 const char* dfx_last_error(void);

@@ -24,6 +24,17 @@ fp32 reciprocal for means, no implicit broadcasting):
   silu              x / (1 + exp(-x))
   sigmoid           1 / (1 + exp(-x))
   channel_scale     x * s[:, None, None]
+ViT extension kinds (torchvision VisionTransformer semantics, fp32 with
+fp64 reductions — there is no reference code to follow):
+  gelu              0.5 x (1 + erf(x / sqrt 2))
+  dense rank-2      row-wise dense over the last axis
+  tokens            [class_token; x.reshape(C, H*W).T] + pos_embedding
+  layernorm         (x - mean) / sqrt(var + eps) * gamma + beta, biased var
+                    over the last axis
+  attention         q|k|v = split(x, 3, axis=-1); per head h (columns
+                    h*d:(h+1)*d, d = C/heads): softmax(q k^T / sqrt d) v,
+                    heads concatenated in order
+  select_token      x[index]
 
 Fast engine (``run_fast``): the same functions over a batch (N, ...) with
 conv/dense as BLAS matmuls (im2col), for real-size models; equal to the
@@ -59,7 +70,50 @@ def act(kind: str, x: np.ndarray) -> np.ndarray:
     if kind == "sigmoid":
         with np.errstate(over="ignore"):
             return (F32(1.0) / (F32(1.0) + np.exp(-x))).astype(F32)
+    if kind == "gelu":
+        from scipy.special import erf
+        x64 = x.astype(np.float64)
+        return (0.5 * x64 * (1.0 + erf(x64 / np.sqrt(2.0)))).astype(F32)
     raise KeyError(kind)
+
+
+# ----------------------------------------------------------------------------
+# token (ViT) kinds, batch-agnostic over leading axes
+
+def tokens(ws, node, x):
+    """x (..., C, H, W) -> (..., 1 + H*W, C)."""
+    cls = _w(ws, node, "class_token")
+    pos = _w(ws, node, "pos_embedding")
+    c = x.shape[-3]
+    t = np.swapaxes(x.reshape(x.shape[:-3] + (c, -1)), -1, -2)
+    cls_b = np.broadcast_to(cls, x.shape[:-3] + (1, c))
+    return (np.concatenate([cls_b, t], axis=-2) + pos).astype(F32)
+
+
+def layernorm(ws, node, x):
+    eps = float(node.attrs.get("epsilon", 1e-5))
+    x64 = x.astype(np.float64)
+    mu = x64.mean(axis=-1, keepdims=True)
+    var = ((x64 - mu) ** 2).mean(axis=-1, keepdims=True)
+    y = (x64 - mu) / np.sqrt(var + eps)
+    return (y * _w(ws, node, "gamma") + _w(ws, node, "beta")).astype(F32)
+
+
+def attention(node, x):
+    """x (..., L, 3C) -> (..., L, C)."""
+    heads = int(node.attrs["heads"])
+    c = x.shape[-1] // 3
+    d = c // heads
+    x64 = x.astype(np.float64)
+    outs = []
+    for h in range(heads):
+        q = x64[..., h * d:(h + 1) * d]
+        k = x64[..., c + h * d:c + (h + 1) * d]
+        v = x64[..., 2 * c + h * d:2 * c + (h + 1) * d]
+        s = (q @ np.swapaxes(k, -1, -2)) / np.sqrt(d)
+        s = np.exp(s - s.max(axis=-1, keepdims=True))
+        outs.append((s / s.sum(axis=-1, keepdims=True)) @ v)
+    return np.concatenate(outs, axis=-1).astype(F32)
 
 
 def bn_coeffs(ws, node):
@@ -104,9 +158,9 @@ def _conv_faithful(node, x, ws):
 
 def _dense_faithful(node, x, ws):
     wt = _w(ws, node, "weight")
-    acc = np.zeros(wt.shape[0], dtype=F32)
+    acc = np.zeros(x.shape[:-1] + (wt.shape[0],), dtype=F32)
     for j in range(wt.shape[1]):
-        acc += wt[:, j] * x[j]
+        acc += wt[:, j] * x[..., j, None]
     if "bias" in node.weight_refs:
         acc = acc + _w(ws, node, "bias")
     return acc
@@ -175,6 +229,14 @@ def eval_node_faithful(node, ins, ws):
         return np.concatenate(ins, axis=0)
     if k == "channel_scale":
         return (ins[0] * ins[1][:, None, None]).astype(F32)
+    if k == "tokens":
+        return tokens(ws, node, ins[0])
+    if k == "layernorm":
+        return layernorm(ws, node, ins[0])
+    if k == "attention":
+        return attention(node, ins[0])
+    if k == "select_token":
+        return ins[0][int(node.attrs.get("index", 0))].copy()
     return act(k, ins[0])
 
 
@@ -280,6 +342,14 @@ def eval_node_fast(node, ins, ws):
         return np.concatenate(ins, axis=1)
     if k == "channel_scale":
         return (x * ins[1][:, :, None, None]).astype(F32)
+    if k == "tokens":
+        return tokens(ws, node, x)
+    if k == "layernorm":
+        return layernorm(ws, node, x)
+    if k == "attention":
+        return attention(node, x)
+    if k == "select_token":
+        return np.ascontiguousarray(x[:, int(node.attrs.get("index", 0))])
     return act(k, x)
 
 

@@ -22,6 +22,9 @@ template <typename T> __global__ void gap_kernel(const __grid_constant__ dfx_gap
 template <typename T> __global__ void in_kernel(const __grid_constant__ dfx_in_params P);
 template <typename T> __global__ void out_kernel(const __grid_constant__ dfx_out_params P);
 template <typename T, int CL> __global__ void se_kernel(const __grid_constant__ dfx_se_params P);
+template <typename T> __global__ void ln_kernel(const __grid_constant__ dfx_ln_params P);
+template <typename T> __global__ void tokens_kernel(const __grid_constant__ dfx_tokens_params P);
+template <typename T> __global__ void attn_kernel(const __grid_constant__ dfx_attn_params P);
 }  // namespace dfx
 
 // kernel instantiation for a storage dtype (DFX_F16 / DFX_BF16)
@@ -196,6 +199,42 @@ int config_for(int op, const void* params, size_t size, LaunchCfg* c) {
         return fail(DFX_E_UNSUPPORTED, "se: c=%d cr=%d needs %zu B of smem", p->in.c, p->cr, c->smem);
       return DFX_OK;
     }
+    case DFX_OP_LN: {
+      NEED(dfx_ln_params);
+      const auto* p = static_cast<const dfx_ln_params*>(params);
+      if (p->out.w > p->in.w || p->out.c != p->in.c || p->out.n != p->in.n || p->in.h != 1 ||
+          (p->norm && (!p->gamma || !p->beta)))
+        return fail(DFX_E_ARG, "ln: bad views/weights");
+      c->func = DFX_PICK(ln_kernel, p->in.dtype);
+      c->grid = dim3(unsigned(cdiv(int64_t(p->out.n) * p->out.w, 8)));
+      c->block = dim3(256);
+      return DFX_OK;
+    }
+    case DFX_OP_TOKENS: {
+      NEED(dfx_tokens_params);
+      const auto* p = static_cast<const dfx_tokens_params*>(params);
+      if (p->out.w != 1 + p->in.h * p->in.w || p->out.c != p->in.c || p->out.h != 1)
+        return fail(DFX_E_ARG, "tokens: out (%d, %d, %d) for grid (%d, %d, %d)", p->out.h, p->out.w,
+                    p->out.c, p->in.h, p->in.w, p->in.c);
+      c->func = DFX_PICK(tokens_kernel, p->out.dtype);
+      c->grid = dim3(elementwise_grid(int64_t(p->out.n) * p->out.w * cdiv(p->out.c, 8), 256));
+      return DFX_OK;
+    }
+    case DFX_OP_ATTN: {
+      NEED(dfx_attn_params);
+      const auto* p = static_cast<const dfx_attn_params*>(params);
+      const int L = p->qkv.w;
+      if (p->heads < 1 || p->out.c != p->heads * 64 || p->qkv.c != 3 * p->out.c ||
+          p->out.w != L || p->qkv.h != 1 || L > dfx::kAttnMaxL || L < 1 ||
+          ((p->qkv.pitch | p->qkv.coff | p->out.pitch | p->out.coff) & 7))
+        return fail(DFX_E_UNSUPPORTED, "attention: L=%d heads=%d c=%d (head dim 64, L <= %d)", L,
+                    p->heads, p->out.c, dfx::kAttnMaxL);
+      c->func = DFX_PICK(attn_kernel, p->qkv.dtype);
+      c->grid = dim3(unsigned(cdiv(L, 64)), unsigned(p->heads), unsigned(p->qkv.n));
+      c->block = dim3(128);
+      c->smem = size_t(dfx::attn_smem_bytes(L));
+      return DFX_OK;
+    }
   }
 #undef NEED
   return fail(DFX_E_ARG, "unknown op %d", op);
@@ -235,7 +274,10 @@ int dfx_sizeof(const char* name) {
            {"dfx_ew_params", sizeof(dfx_ew_params)},
            {"dfx_in_params", sizeof(dfx_in_params)},
            {"dfx_out_params", sizeof(dfx_out_params)},
-           {"dfx_se_params", sizeof(dfx_se_params)}};
+           {"dfx_se_params", sizeof(dfx_se_params)},
+           {"dfx_ln_params", sizeof(dfx_ln_params)},
+           {"dfx_tokens_params", sizeof(dfx_tokens_params)},
+           {"dfx_attn_params", sizeof(dfx_attn_params)}};
   for (auto& e : t)
     if (!strcmp(e.n, name)) return e.s;
   return -1;
@@ -260,6 +302,8 @@ int dfx_init(int device) {
       CK(cudaFuncSetAttribute(se_func(dt, cl), cudaFuncAttributeMaxDynamicSharedMemorySize,
                               dfx::kSeSmemBudget));
     CK(cudaFuncSetAttribute(se_func(dt, 16), cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    CK(cudaFuncSetAttribute(DFX_PICK(attn_kernel, dt), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            dfx::attn_smem_bytes(dfx::kAttnMaxL)));
   }
   return get_encode();
 }

@@ -233,6 +233,30 @@ __global__ void in_kernel(const __grid_constant__ dfx_in_params P) {
   const int hw = o.h * o.w;
   const int cgp = o.pitch / 8;                 // channel groups incl. padding
   const int64_t total = int64_t(o.n) * hw * cgp;
+  if (P.block > 1) {                           // space-to-depth (patchify conv input)
+    const int b = P.block, C = o.c / (b * b), W = o.w * b;
+    const int64_t HW = int64_t(hw) * b * b;
+    for (int64_t idx = grid_stride_start(); idx < total; idx += grid_stride_step()) {
+      const int64_t pix = idx / cgp;
+      const int c0 = int(idx - pix * cgp) * 8;
+      const int n = int(pix / hw);
+      const int s = int(pix - int64_t(n) * hw);
+      const int y = s / o.w, x = s - (s / o.w) * o.w;
+      float v[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int cc = c0 + i;
+        v[i] = 0.0f;
+        if (cc < o.c) {
+          const int rs = cc / C, c = cc - rs * C;
+          const int r = rs / b, sx = rs - r * b;
+          v[i] = __ldg(P.src + (int64_t(n) * C + c) * HW + int64_t(y * b + r) * W + x * b + sx);
+        }
+      }
+      st8<T>(o.base, pix * o.pitch + c0, v);
+    }
+    return;
+  }
   for (int64_t idx = grid_stride_start(); idx < total; idx += grid_stride_step()) {
     const int64_t pix = idx / cgp;
     const int c = int(idx - pix * cgp) * 8;

@@ -26,6 +26,7 @@ DFX_DEV float act_apply(int act, float v) {
     case DFX_ACT_HARDSIGMOID: return fminf(fmaxf(v + 3.0f, 0.0f), 6.0f) / 6.0f;
     case DFX_ACT_SILU: return v / (1.0f + __expf(-v));
     case DFX_ACT_SIGMOID: return 1.0f / (1.0f + __expf(-v));
+    case DFX_ACT_GELU: return 0.5f * v * (1.0f + erff(v * 0.70710678118654752f));
     default: return v;
   }
 }
@@ -52,6 +53,10 @@ DFX_DEV void act8(int act, float* v) {
     case DFX_ACT_SIGMOID:
 #pragma unroll
       for (int i = 0; i < 8; ++i) v[i] = 1.0f / (1.0f + __expf(-v[i]));
+      break;
+    case DFX_ACT_GELU:
+#pragma unroll
+      for (int i = 0; i < 8; ++i) v[i] = 0.5f * v[i] * (1.0f + erff(v[i] * 0.70710678118654752f));
       break;
     default:
       break;
@@ -388,6 +393,17 @@ __host__ __device__ inline uint32_t tmem_cols_for(int bn) {
   uint32_t c = 32;
   while (c < uint32_t(bn)) c <<= 1;
   return c;
+}
+
+// ---------------------------------------------------------------- attention geometry (dfx_vit.cu)
+constexpr int kAttnD = 64;          // head dim
+constexpr int kAttnQ = 64;          // query rows per CTA (4 warps x 16)
+constexpr int kAttnKB = 64;         // keys per online-softmax block
+constexpr int kAttnLd = kAttnD + 8; // smem row pitch (elements): conflict-free ldmatrix
+constexpr int kAttnMaxL = 512;
+
+__host__ __device__ constexpr int attn_smem_bytes(int L) {
+  return (kAttnQ + 2 * ((L + kAttnKB - 1) / kAttnKB) * kAttnKB) * kAttnLd * 2;
 }
 
 }  // namespace dfx

@@ -20,6 +20,7 @@ batch signature so concurrent ``execute_fused`` callers never share one.
 from __future__ import annotations
 
 import ctypes as C
+import math
 import os
 import threading
 import time
@@ -29,7 +30,8 @@ import numpy as np
 
 from . import runtime as rt
 from .graph_ir import LiveInterval
-from .lower import COPY, DWCONV, EW, GAP, GEMM, POOL, SE, MemberProgram, gemm_tiling, lower_member
+from .lower import (ATTN, COPY, DWCONV, EW, GAP, GEMM, LN, POOL, SE, TOKENS, MemberProgram,
+                    gemm_tiling, lower_member)
 from .planner import first_fit
 
 ALIGN = 256
@@ -52,6 +54,12 @@ def program_for(g, w, precision: str = "fp16") -> MemberProgram:
     with _cache_lock:
         _program_cache[key] = (g, w, prog)
     return prog
+
+
+def _fold_rows(v: "rt.View") -> "rt.View":
+    """(n, 1, L, c) token view -> (1, 1, n*L, c): the same bytes, one GEMM M axis."""
+    assert v.h == 1
+    return rt.View(v.base, 1, 1, v.n * v.w, v.c, v.pitch, v.coff, v.dtype)
 
 
 def _align(x, a=ALIGN):
@@ -265,7 +273,10 @@ def plan_member(prog: MemberProgram, n: int, sm_count: int = 148) -> MemberPlan:
         if L.kind != GEMM:
             continue
         out = prog.values[L.dst]
-        t = gemm_tiling(L.geom, n, out.h, out.w, sm_count)
+        if L.geom.get("tokens"):        # token rows of all images are one contiguous M
+            t = gemm_tiling(L.geom, 1, 1, n * out.w, sm_count)
+        else:
+            t = gemm_tiling(L.geom, n, out.h, out.w, sm_count)
         tilings[L.index] = t
         if t["splits"] > 1:
             ws = max(ws, t["splits"] * n * out.h * out.w * t["nt"] * t["bn"] * 4)
@@ -352,7 +363,8 @@ class ExecInstance:
             if n == 0:
                 continue
             deps = [prev_tail] if (self.dag.mode == "sequential" and prev_tail is not None) else []
-            pin = rt.InParams(self.dev_in + self.in_off[m], self._view(m, prog, "<input>", n))
+            pin = rt.InParams(self.dev_in + self.in_off[m], self._view(m, prog, "<input>", n),
+                              prog.input_block)
             last = g.add(rt.OP_IN, pin, deps)
             self.nodes.append((rt.OP_IN, pin, dict(member=m, kind="in", flops=0,
                                                    bytes=self.in_sizes[m] * 3 // 2)))
@@ -409,6 +421,12 @@ class ExecInstance:
         elif L.kind == SE:
             g = L.geom
             info.update(flops=4 * n * g["c"] * g["cr"], bytes=in_b + out_b + 2 * 2 * g["c"] * g["cr"])
+        elif L.kind == ATTN:
+            g = L.geom
+            info.update(flops=4 * n * g["seq"] * g["seq"] * g["c"], bytes=in_b + out_b)
+        elif L.kind == LN:
+            out = prog.values[L.dst]            # rows actually normalised
+            info.update(bytes=2 * n * out.w * out.c * 2)
         else:
             info.update(bytes=in_b + out_b + other_b)
         return info
@@ -454,11 +472,13 @@ class ExecInstance:
         if L.kind == GEMM:
             geo, t = L.geom, self.plans[m].tilings[L.index]
             out = self._view(m, prog, L.dst, n)
+            if geo.get("tokens"):            # fold (n, 1, L) token rows into one M axis
+                src, out = _fold_rows(src), _fold_rows(out)
             d = rt.GemmDesc()
             d.tmap_a = rt.tmap_act(src, geo["cb"], t["tq"], t["tp"], t["tn"], geo["sw"], geo["sh"])
             d.tmap_b = rt.tmap_weights(arena.addr(m, L.blobs["weight"]), geo["cout"], geo["k"],
                                        geo["cb"], t["bn"], self.dtype)
-            d.n, d.p, d.q = n, out.h, out.w
+            d.n, d.p, d.q = out.n, out.h, out.w
             d.tn, d.tp, d.tq = t["tn"], t["tp"], t["tq"]
             d.mt_n, d.mt_p, d.mt_q, d.nt = t["mt_n"], t["mt_p"], t["mt_q"], t["nt"]
             d.r, d.s = geo["kh"], geo["kw"]
@@ -468,6 +488,8 @@ class ExecInstance:
             d.bn, d.cout, d.tile_begin, d.tiles = t["bn"], geo["cout"], 0, t["tiles"]
             d.out = out
             epi = self._epi(m, prog, L, n)
+            if geo.get("tokens") and epi.binop:
+                epi.other = _fold_rows(epi.other)
             d.epi = epi
             d.ws = (self.ws + self.ws_off[m]) if t["splits"] > 1 else None
             fixup = t["splits"] > 1 and SPLITK_MODE == "fixup"
@@ -483,7 +505,7 @@ class ExecInstance:
             yield rt.OP_GEMM, gl
             if t["splits"] > 1 and not fixup:
                 yield rt.OP_SPLITK, rt.SplitKParams(self.ws + self.ws_off[m], t["splits"],
-                                                    n * out.h * out.w, geo["cout"],
+                                                    out.n * out.h * out.w, geo["cout"],
                                                     t["nt"] * t["bn"], out, epi)
         elif L.kind == DWCONV:
             geo = L.geom
@@ -504,6 +526,17 @@ class ExecInstance:
             cv = self._view(m, prog, L.geom["concat"], n)
             out = rt.View(cv.base, n, src.h, src.w, src.c, cv.pitch, L.geom["coff"], self.dtype)
             yield rt.OP_EW, rt.EwParams(src, out, rt.Epilogue())
+        elif L.kind == LN:
+            addr = (lambda r: arena.addr(m, L.blobs[r]) if r in L.blobs else None)
+            yield rt.OP_LN, rt.LnParams(src, self._view(m, prog, L.dst, n), addr("gamma"),
+                                        addr("beta"), L.geom["eps"], L.geom["norm"])
+        elif L.kind == TOKENS:
+            yield rt.OP_TOKENS, rt.TokensParams(src, self._view(m, prog, L.dst, n),
+                                                arena.addr(m, L.blobs["class_token"]),
+                                                arena.addr(m, L.blobs["pos_embedding"]))
+        elif L.kind == ATTN:
+            yield rt.OP_ATTN, rt.AttnParams(src, self._view(m, prog, L.dst, n), L.geom["heads"],
+                                            1.0 / math.sqrt(L.geom["c"] // L.geom["heads"]))
         elif L.kind == SE:
             geo = L.geom
             addr = (lambda r: arena.addr(m, L.blobs[r]) if r in L.blobs else None)

@@ -15,10 +15,21 @@ let the north-star CNNs be written down without approximation:
     silu            -                                           1
     sigmoid         -                                           1
     channel_scale   -   (C,H,W) x (C,) -> (C,H,W)               2
+    gelu            -   exact (erf) GELU                        1
+    tokens          weights class_token (C,), pos_embedding     1
+                    (1+H*W, C):  (C,H,W) -> (1+H*W, C), row 0 the class
+                    token, row 1+h*W+w the pixel (h, w); + pos_embedding
+    layernorm       epsilon (default 1e-5); weights gamma,      1
+                    beta (C,): normalise over the last axis
+    attention       heads:  (L, 3C) packed q|k|v -> (L, C),     1
+                    per head softmax(q k^T / sqrt(C/heads)) v
+    select_token    index (default 0):  (L, C) -> (C,)          1
+    dense           + a rank-2 input (L, fan_in) -> (L, units) (row-wise)
 
-Tensors are single-sample, rank 1 or 3 (C,H,W); byte sizes count 32-bit
-elements exactly like the reference (graph_ir.py:82-84), so the liveness
-plan below reproduces ``peak_activation_bytes`` (graph_ir.py:486-512).
+Tensors are single-sample, rank 1, 2 (L, C: token sequences) or 3 (C,H,W);
+byte sizes count 32-bit elements exactly like the reference
+(graph_ir.py:82-84), so the liveness plan below reproduces
+``peak_activation_bytes`` (graph_ir.py:486-512).
 """
 
 from __future__ import annotations
@@ -38,9 +49,10 @@ REFERENCE_KINDS = (
 )
 EXTENSION_KINDS = (
     "avgpool2d", "hardswish", "hardsigmoid", "silu", "sigmoid", "channel_scale",
+    "gelu", "tokens", "layernorm", "attention", "select_token",
 )
 KINDS = REFERENCE_KINDS + EXTENSION_KINDS
-ACTIVATION_KINDS = ("relu", "hardswish", "hardsigmoid", "silu", "sigmoid")
+ACTIVATION_KINDS = ("relu", "hardswish", "hardsigmoid", "silu", "sigmoid", "gelu")
 VARIADIC_KINDS = ("residual_add", "concat")       # >= 2 inputs
 BINARY_KINDS = ("channel_scale",)                  # exactly 2 inputs
 SINGLE_INPUT_KINDS = tuple(k for k in KINDS if k not in VARIADIC_KINDS + BINARY_KINDS)
@@ -253,12 +265,41 @@ def _need_chw(node: OpNode, dims) -> None:
 
 def _shape_dense(node, ins):
     (d,) = ins
-    if len(d) != 1:
-        raise ShapeMismatch(node.node_id, f"dense expects a rank-1 input, got {d}")
+    if len(d) not in (1, 2):
+        raise ShapeMismatch(node.node_id, f"dense expects a rank-1 (or token rank-2) input, got {d}")
     fan_in = int(node.attrs["fan_in"])
-    if d[0] != fan_in:
-        raise ShapeMismatch(node.node_id, f"fan_in {fan_in} but input has {d[0]} features")
-    return (int(node.attrs["units"]),)
+    if d[-1] != fan_in:
+        raise ShapeMismatch(node.node_id, f"fan_in {fan_in} but input has {d[-1]} features")
+    return tuple(d[:-1]) + (int(node.attrs["units"]),)
+
+
+def _shape_tokens(node, ins):
+    (d,) = ins
+    _need_chw(node, d)
+    return (1 + d[1] * d[2], d[0])
+
+
+def _shape_layernorm(node, ins):
+    (d,) = ins
+    if len(d) not in (1, 2):
+        raise ShapeMismatch(node.node_id, f"layernorm expects (C,) or (L, C), got {d}")
+    return d
+
+
+def _shape_attention(node, ins):
+    (d,) = ins
+    heads = int(node.attrs["heads"])
+    if len(d) != 2 or d[1] % 3 or (d[1] // 3) % heads:
+        raise ShapeMismatch(node.node_id, f"attention expects (L, 3C) with C % heads == 0, got {d}")
+    return (d[0], d[1] // 3)
+
+
+def _shape_select_token(node, ins):
+    (d,) = ins
+    idx = int(node.attrs.get("index", 0))
+    if len(d) != 2 or not 0 <= idx < d[0]:
+        raise ShapeMismatch(node.node_id, f"select_token {idx} of {d}")
+    return (d[1],)
 
 
 def _shape_conv(node, ins):
@@ -333,6 +374,8 @@ _SHAPE: dict[str, Callable] = {
     "avgpool2d": _shape_pool, "batchnorm_inference": _shape_same,
     "residual_add": _shape_add, "global_avg_pool": _shape_gap, "flatten": _shape_flatten,
     "concat": _shape_concat, "channel_scale": _shape_channel_scale,
+    "tokens": _shape_tokens, "layernorm": _shape_layernorm, "attention": _shape_attention,
+    "select_token": _shape_select_token,
     **{k: _shape_same for k in ACTIVATION_KINDS},
 }
 
@@ -388,6 +431,12 @@ def expected_weight_shapes(node: OpNode, input_dims) -> dict[str, tuple[tuple[in
     if node.kind == "batchnorm_inference":
         per = ((input_dims[0][0],), True)
         return {"gamma": per, "beta": per, "mean": per, "var": per}
+    if node.kind == "layernorm":
+        per = ((input_dims[0][-1],), True)
+        return {"gamma": per, "beta": per}
+    if node.kind == "tokens":
+        c, h, w = input_dims[0]
+        return {"class_token": ((c,), True), "pos_embedding": ((1 + h * w, c), True)}
     return {}
 
 
@@ -477,7 +526,10 @@ def node_flops(node: OpNode, input_dims, output_dims) -> int:
         out *= int(d)
     a = node.attrs
     if node.kind == "dense":
-        return 2 * int(a["fan_in"]) * int(a["units"])
+        return 2 * int(a["fan_in"]) * out          # = 2 * fan_in * units for rank-1
+    if node.kind == "attention":                   # q k^T and p v
+        seq = int(output_dims[0])
+        return 4 * seq * out
     if node.kind == "conv2d":
         kh, kw, *_ = conv_geometry(a)
         cin = input_dims[0][0] // int(a.get("groups", 1))
@@ -498,11 +550,11 @@ def node_flops(node: OpNode, input_dims, output_dims) -> int:
 
 
 def gemm_flops(g, shapes=None) -> int:
-    """Sum of conv2d + dense FLOPs of one graph (the tensor-core work)."""
+    """Sum of conv2d + dense + attention FLOPs of one graph (the tensor-core work)."""
     shapes = shapes or infer_shapes(g)
     total = 0
     for nid, node in g.nodes.items():
-        if node.kind in ("conv2d", "dense"):
+        if node.kind in ("conv2d", "dense", "attention"):
             total += node_flops(node, node_input_dims(g, nid, shapes), shapes[nid].dims)
     return total
 

@@ -37,6 +37,7 @@ from .graph_ir import (ACTIVATION_KINDS, conv_geometry, infer_shapes, pool_geome
                        topo_order)
 
 GEMM, DWCONV, POOL, GAP, EW, COPY, SE = "gemm", "dwconv", "pool", "gap", "ew", "copy", "se"
+LN, TOKENS, ATTN = "ln", "tokens", "attn"      # token (ViT) launches, dfx_vit.cu
 SE_MAX_C, SE_MAX_CR = 4096, 512          # limits of dfx_fused.cu se_kernel
 
 
@@ -138,6 +139,7 @@ class MemberProgram:
     input_value: str = "<input>"
     gemm_flops_per_sample: int = 0
     precision: str = "fp16"
+    input_block: int = 1                # > 1: input stored space-to-depth (patchify conv)
 
     def weight_bytes(self) -> int:
         return sum(b.nbytes for b in self.blobs.values())
@@ -168,11 +170,27 @@ class _Lowerer:
         self.acc_owner: dict[str, str] = {}
         self.pending_weights: list = []
         self.pending_se: list = []
+        self.pending_vec: list = []             # (launch, node, fp32 weight roles)
         self.precision = "fp16"
         self.keep_f32 = False
+        self.input_block = self._patchify_block()
         self.debug_f32: dict[str, np.ndarray] = {}
 
     # -------------------------------------------------------------- helpers
+    def _patchify_block(self) -> int:
+        """k if the entry node is a patchify conv (kernel = stride = k > 1, no padding,
+        k | H, W): the input is then stored space-to-depth (dfx_in_params.block) and
+        the conv runs as a 1x1 GEMM over k*k*C channels (strides > 8 do not fit a
+        TMA element stride; C = 3 would also waste 13/16 of every channel block)."""
+        node = self.g.nodes[self.g.entry]
+        d = self.g.input_spec.dims
+        if node.kind != "conv2d" or len(d) != 3 or int(node.attrs.get("groups", 1)) != 1:
+            return 1
+        kh, kw, sh, sw, ph, pw = conv_geometry(node.attrs)
+        if kh == kw == sh == sw and kh > 1 and ph == pw == 0 and d[1] % kh == 0 and d[2] % kh == 0:
+            return kh
+        return 1
+
     def dims(self, nid):
         return self.shapes[nid].dims
 
@@ -200,6 +218,12 @@ class _Lowerer:
         return s, t
 
     # -------------------------------------------------------------- chains
+    def materialized(self, nid) -> bool:
+        """Is ``nid``'s value stored by some launch (not a folded middle of a chain)?"""
+        if nid not in self.absorbed:
+            return True
+        return any(L.dst == nid for L in self.launches)
+
     def absorb(self, anchor_id: str, tail: str, epi: Epi, allow_affine: bool, allow_bin: bool):
         """Greedily fold single-consumer successors into the epilogue."""
         nodes = [anchor_id] if anchor_id != tail else [tail]
@@ -223,13 +247,13 @@ class _Lowerer:
                     and len(node.inputs) == 2:
                 other = node.inputs[1] if node.inputs[0] == tail else node.inputs[0]
                 if other == tail or self.pos[other] >= self.pos[anchor_id] \
-                        or other in self.absorbed:
+                        or not self.materialized(other):
                     break
                 epi.binop, epi.other = 1, other
             elif k == "channel_scale" and allow_bin and epi.binop == 0 and epi.act2 is None \
                     and node.inputs[0] == tail:
                 other = node.inputs[1]
-                if self.pos[other] >= self.pos[anchor_id] or other in self.absorbed:
+                if self.pos[other] >= self.pos[anchor_id] or not self.materialized(other):
                     break
                 epi.binop, epi.other = 2, other
             else:
@@ -261,6 +285,36 @@ class _Lowerer:
             return
         if k in ("flatten", "concat"):
             return          # views; handled in placement
+        if k == "layernorm":
+            sel = self.single_user(nid)
+            geom = dict(norm=1, eps=float(node.attrs.get("epsilon", 1e-5)))
+            if sel is not None and self.g.nodes[sel].kind == "select_token" \
+                    and int(self.g.nodes[sel].attrs.get("index", 0)) == 0:
+                self.absorbed[sel] = nid            # normalise only the selected row
+                L = Launch(LN, [nid, sel], self.src_of(nid), sel, geom=geom)
+            else:
+                L = Launch(LN, [nid], self.src_of(nid), nid, geom=geom)
+            self.pending_vec.append((L, node, ("gamma", "beta")))
+            self.launches.append(L)
+            return
+        if k == "select_token":
+            if int(node.attrs.get("index", 0)) != 0:
+                raise UnsupportedOnDevice(nid, "select_token index != 0")
+            self.launches.append(Launch(LN, [nid], self.src_of(nid), nid, geom=dict(norm=0, eps=0.0)))
+            return
+        if k == "tokens":
+            L = Launch(TOKENS, [nid], self.src_of(nid), nid)
+            self.pending_vec.append((L, node, ("class_token", "pos_embedding")))
+            self.launches.append(L)
+            return
+        if k == "attention":
+            heads = int(node.attrs["heads"])
+            c = self.dims(nid)[1]
+            if c % heads or c // heads != 64:
+                raise UnsupportedOnDevice(nid, f"attention head dim {c // max(heads, 1)} (64 only)")
+            self.launches.append(Launch(ATTN, [nid], self.src_of(nid), nid,
+                                        geom=dict(heads=heads, seq=self.dims(nid)[0], c=c)))
+            return
         # elementwise anchors
         epi = Epi()
         src = self.src_of(nid)
@@ -303,7 +357,7 @@ class _Lowerer:
             wt = self.warr(node, "weight")
             src = self.src_of(nid)
             geom = dict(cout=units, cin=fan_in, kh=1, kw=1, sh=1, sw=1, ph=0, pw=0,
-                        dense=True)
+                        dense=True, tokens=len(idims) == 2)
             wt4 = wt.reshape(units, fan_in, 1, 1)
             kind = GEMM
         else:
@@ -312,6 +366,13 @@ class _Lowerer:
             cin = idims[0]
             wt4 = self.warr(node, "weight")
             src = self.src_of(nid)
+            if nid == self.g.entry and self.input_block > 1:
+                # patchify conv over the space-to-depth input: 1x1, K order (r, s, c)
+                b = self.input_block
+                wt4 = np.ascontiguousarray(wt4.transpose(0, 2, 3, 1)).reshape(cout, b * b * cin, 1, 1)
+                cin, kh, kw, sh, sw = b * b * cin, 1, 1, 1, 1
+            elif max(sh, sw) > 8:
+                raise UnsupportedOnDevice(nid, f"conv stride {sh}x{sw} > 8 (TMA element stride)")
             geom = dict(cout=cout, cin=cin, kh=kh, kw=kw, sh=sh, sw=sw, ph=ph, pw=pw,
                         dense=False)
             if groups == 1:
@@ -348,6 +409,8 @@ class _Lowerer:
             return self.values[name]
         node = self.g.nodes.get(name)
         if node is not None and node.kind == "flatten":
+            if len(self.in_dims(name)) == 2:
+                raise UnsupportedOnDevice(name, "flatten of a token tensor")
             src = self.resolve(self.src_of(name))
             v = Value(src.buf, src.coff, src.h, src.w, src.c, flat=src.flat or src.h * src.w > 1)
             self.values[name] = v
@@ -358,9 +421,12 @@ class _Lowerer:
         g = self.g
         ind = g.input_spec.dims
         h, w = (ind[1], ind[2]) if len(ind) == 3 else (1, 1)
-        ib = self.new_buffer(h, w, ind[0], "<input>")
+        c, b = ind[0], self.input_block
+        if b > 1:
+            h, w, c = h // b, w // b, c * b * b
+        ib = self.new_buffer(h, w, c, "<input>")
         self.buffers[ib].is_input = True
-        self.values["<input>"] = Value(ib, 0, h, w, ind[0])
+        self.values["<input>"] = Value(ib, 0, h, w, c)
 
         produced = {L.dst for L in self.launches}
         # concat groups, outermost first (reverse topo order): parts written in place
@@ -399,6 +465,8 @@ class _Lowerer:
             elif len(d) == 3:
                 self.values[L.dst] = Value(self.new_buffer(d[1], d[2], d[0], L.dst), 0,
                                            d[1], d[2], d[0])
+            elif len(d) == 2:                    # token rows (L, C) -> view h = 1, w = L
+                self.values[L.dst] = Value(self.new_buffer(1, d[0], d[1], L.dst), 0, 1, d[0], d[1])
             else:
                 self.values[L.dst] = Value(self.new_buffer(1, 1, d[0], L.dst), 0, 1, 1, d[0])
         for nid in self.order:              # remaining views (e.g. a flatten exit)
@@ -407,6 +475,8 @@ class _Lowerer:
 
     # -------------------------------------------------------------- build
     def run(self) -> MemberProgram:
+        if len(self.g.input_spec.dims) == 2 or len(self.dims(self.g.exit)) == 2:
+            raise UnsupportedOnDevice(self.g.exit, "token tensor as the model input or output")
         for nid in self.order:
             if nid in self.absorbed:
                 continue
@@ -496,6 +566,14 @@ class _Lowerer:
         return L
 
     def pack_weights(self):
+        for L, node, roles in self.pending_vec:
+            for role in roles:
+                v = self.warr(node, role).reshape(-1)
+                arr = np.zeros(round_up(len(v), 8), dtype=np.float32)
+                arr[:len(v)] = v
+                key = f"{node.node_id}.{role}"
+                self.blobs[key] = arr
+                L.blobs[role] = key
         for L in self.pending_se:
             for role, fc in (("1", L.geom["fc1"]), ("2", L.geom["fc2"])):
                 node = self.g.nodes[fc]
@@ -577,6 +655,7 @@ def lower_member(g, w, keep_f32: bool = False, precision: str = "fp16") -> Membe
     prog = low.run()
     prog.debug_f32 = low.debug_f32
     prog.precision = precision
+    prog.input_block = low.input_block
     from .graph_ir import gemm_flops
     prog.gemm_flops_per_sample = gemm_flops(g)
     return prog

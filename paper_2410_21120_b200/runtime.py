@@ -19,12 +19,13 @@ from .errors import DeviceError
 PKG = Path(__file__).resolve().parent
 LIB_PATH = PKG / "libdfx.so"
 
-OP_GEMM, OP_SPLITK, OP_DWCONV, OP_POOL, OP_GAP, OP_EW, OP_IN, OP_OUT, OP_SE = range(1, 10)
-ACT = {None: 0, "relu": 1, "hardswish": 2, "hardsigmoid": 3, "silu": 4, "sigmoid": 5}
+(OP_GEMM, OP_SPLITK, OP_DWCONV, OP_POOL, OP_GAP, OP_EW, OP_IN, OP_OUT, OP_SE, OP_LN, OP_TOKENS,
+ OP_ATTN) = range(1, 13)
+ACT = {None: 0, "relu": 1, "hardswish": 2, "hardsigmoid": 3, "silu": 4, "sigmoid": 5, "gelu": 6}
 BIN_NONE, BIN_ADD, BIN_SCALE = 0, 1, 2
 DT_BF16, DT_F16 = 0, 1
 DTYPES = {"bf16": DT_BF16, "fp16": DT_F16}
-ABI_VERSION = 2
+ABI_VERSION = 3
 
 i32, i64, u64, vp = C.c_int32, C.c_int64, C.c_uint64, C.c_void_p
 fptr = C.POINTER(C.c_float)
@@ -83,7 +84,7 @@ class EwParams(C.Structure):
 
 
 class InParams(C.Structure):
-    _fields_ = [("src", vp), ("out", View)]
+    _fields_ = [("src", vp), ("out", View), ("block", i32), ("_pad", i32)]
 
 
 class OutParams(C.Structure):
@@ -95,16 +96,31 @@ class SeParams(C.Structure):
                 ("cr", i32), ("act1", i32), ("act2", i32), ("_pad", i32)]
 
 
+class LnParams(C.Structure):
+    _fields_ = [("inp", View), ("out", View), ("gamma", vp), ("beta", vp), ("eps", C.c_float),
+                ("norm", i32), ("_pad", i32 * 2)]
+
+
+class TokensParams(C.Structure):
+    _fields_ = [("inp", View), ("out", View), ("cls", vp), ("pos", vp)]
+
+
+class AttnParams(C.Structure):
+    _fields_ = [("qkv", View), ("out", View), ("heads", i32), ("scale", C.c_float), ("_pad", i32 * 2)]
+
+
 STRUCTS = {
     "dfx_view": View, "dfx_epilogue": Epilogue, "dfx_gemm_desc": GemmDesc,
     "dfx_gemm_launch": GemmLaunch, "dfx_splitk_params": SplitKParams,
     "dfx_dwconv_params": DwconvParams, "dfx_pool_params": PoolParams,
     "dfx_gap_params": GapParams, "dfx_ew_params": EwParams, "dfx_in_params": InParams,
-    "dfx_out_params": OutParams, "dfx_se_params": SeParams,
+    "dfx_out_params": OutParams, "dfx_se_params": SeParams, "dfx_ln_params": LnParams,
+    "dfx_tokens_params": TokensParams, "dfx_attn_params": AttnParams,
 }
 OP_PARAMS = {OP_GEMM: GemmLaunch, OP_SPLITK: SplitKParams, OP_DWCONV: DwconvParams,
              OP_POOL: PoolParams, OP_GAP: GapParams, OP_EW: EwParams, OP_IN: InParams,
-             OP_OUT: OutParams, OP_SE: SeParams}
+             OP_OUT: OutParams, OP_SE: SeParams, OP_LN: LnParams, OP_TOKENS: TokensParams,
+             OP_ATTN: AttnParams}
 
 # every symbol include/dfx.h declares (tests check the .so exports all of them)
 EXPORTS = (

@@ -77,7 +77,7 @@ class Net:
         return float(self.calib.get(f"{nid}:lsuv", 1.0))
 
     # ---- layers
-    def conv(self, nid, src, cout, k, stride=1, pad=None, groups=1, bias=False):
+    def conv(self, nid, src, cout, k, stride=1, pad=None, groups=1, bias=False, std=None):
         cin, h, w = self._in_dims(src)
         kh, kw = (k, k) if isinstance(k, int) else k
         if pad is None:
@@ -86,7 +86,9 @@ class Net:
         sh, sw = (stride, stride) if isinstance(stride, int) else stride
         fan_in = (cin // groups) * kh * kw
         s = self._scale(nid)
-        if self.init == "lsuv":          # N(0, 1/fan_in), rescaled by calibration
+        if std is not None:              # explicit (ViT conv_proj)
+            pass
+        elif self.init == "lsuv":        # N(0, 1/fan_in), rescaled by calibration
             std = s / np.sqrt(fan_in)
         elif self.init == "kaiming_fan_in":
             std = np.sqrt(2.0 / fan_in)
@@ -112,14 +114,21 @@ class Net:
         oh, ow = (h + 2 * ph - kh) // sh + 1, (w + 2 * pw - kw) // sw + 1
         return self._add(nid, "conv2d", src, attrs, refs, out_dims=(cout, oh, ow))
 
-    def dense(self, nid, src, units, bias=True, init=None):
+    def dense(self, nid, src, units, bias=True, init=None, bias_std=0.0):
         """init: "lsuv" | "se" (1x1-conv kaiming fan_out) | "torch_linear"
-        (U(+-1/sqrt(fan_in)) weight and bias) | "uniform_fanout" | "normal001"."""
-        (fan_in,) = self._in_dims(src)
+        (U(+-1/sqrt(fan_in)) weight and bias) | "uniform_fanout" | "normal001" |
+        "xavier_uniform" | "normal002".  A rank-2 (L, fan_in) input is row-wise."""
+        idims = self._in_dims(src)
+        fan_in = idims[-1]
         s = self._scale(nid)
         init = init or self.init
-        b = np.zeros(units, F32)
-        if init == "lsuv":
+        b = (self.rng.standard_normal(units) * bias_std).astype(F32) if bias_std else np.zeros(units, F32)
+        if init == "xavier_uniform":
+            r = np.sqrt(6.0 / (fan_in + units))
+            wt = self.rng.uniform(-r, r, units * fan_in).astype(F32)
+        elif init == "normal002":
+            wt = self.rng.standard_normal(units * fan_in, dtype=F32) * F32(0.02)
+        elif init == "lsuv":
             wt = self.rng.standard_normal(units * fan_in, dtype=F32) * F32(s / np.sqrt(fan_in))
             b = self.rng.standard_normal(units, dtype=F32) * F32(0.01 * s)
         elif init == "se":
@@ -139,7 +148,33 @@ class Net:
         if bias:
             refs["bias"] = self._put(f"{nid}.bias", (units,), b)
         return self._add(nid, "dense", src, {"units": units, "fan_in": fan_in}, refs,
-                         out_dims=(units,))
+                         out_dims=tuple(idims[:-1]) + (units,))
+
+    def layernorm(self, nid, src, eps=1e-6):
+        """gamma ~ U(0.5, 1.5), beta ~ N(0, 0.1) (synthetic, like bn)."""
+        c = self._in_dims(src)[-1]
+        gamma = self.rng.uniform(0.5, 1.5, c).astype(F32)
+        beta = (self.rng.standard_normal(c) * 0.1).astype(F32)
+        refs = {"gamma": self._put(f"{nid}.gamma", (c,), gamma),
+                "beta": self._put(f"{nid}.beta", (c,), beta)}
+        return self._add(nid, "layernorm", src, {"epsilon": eps}, refs, out_dims=self._in_dims(src))
+
+    def tokens(self, nid, src):
+        """class token N(0, 0.02) (torchvision: zeros), pos_embedding N(0, 0.02)."""
+        c, h, w = self._in_dims(src)
+        cls = self.rng.standard_normal(c) * 0.02
+        pos = self.rng.standard_normal((1 + h * w) * c) * 0.02
+        refs = {"class_token": self._put(f"{nid}.class_token", (c,), cls),
+                "pos_embedding": self._put(f"{nid}.pos_embedding", (1 + h * w, c), pos)}
+        return self._add(nid, "tokens", src, {}, refs, out_dims=(1 + h * w, c))
+
+    def attention(self, nid, src, heads):
+        seq, c3 = self._in_dims(src)
+        return self._add(nid, "attention", src, {"heads": heads}, out_dims=(seq, c3 // 3))
+
+    def select_token(self, nid, src, index=0):
+        return self._add(nid, "select_token", src, {"index": index},
+                         out_dims=(self._in_dims(src)[-1],))
 
     def bn(self, nid, src, eps=1e-5, gamma_scale=1.0):
         """gamma ~ U(0.5, 1.5) * gamma_scale (gamma_scale < 1 on the last BN of a
@@ -465,7 +500,41 @@ def inception_v3(model_id="inception_v3", seed=1607, calib=None, res=299, classe
     return n.build(x)
 
 
+# ----------------------------------------------------------------------------- ViT-B/16
+
+def vit_b_16(model_id="vit_b_16", seed=1608, calib=None, res=224, classes=1000,
+             patch=16, hidden=768, layers=12, heads=12, mlp=3072):
+    """torchvision vit_b_16 (eval): conv_proj 16x16/16 -> [class token; patches] +
+    pos_embedding -> 12 pre-LN encoder blocks (LN 1e-6, MHA with packed in_proj,
+    out_proj, residual; LN, Linear-GELU-Linear, residual) -> LN -> token 0 -> head.
+    Inits follow torchvision (trunc-normal conv_proj ~ N(0, 1/fan_in), xavier
+    in_proj / MLP, N(0, 1e-6) MLP biases) except the zero-initialised pieces,
+    which are synthetic here so every path carries signal: class token and LN
+    affine (see Net.tokens / Net.layernorm) and the head, N(0, 0.02)."""
+    n = Net(model_id, (3, res, res), seed, calib)
+    x = n.conv("conv_proj", None, hidden, patch, stride=patch, pad=0, bias=True,
+               std=np.sqrt(1.0 / (3 * patch * patch)))
+    x = n.tokens("tokens", x)
+    for i in range(layers):
+        p = f"enc{i:02d}"
+        y = n.layernorm(f"{p}_ln1", x)
+        y = n.dense(f"{p}_qkv", y, 3 * hidden, init="xavier_uniform")
+        y = n.attention(f"{p}_attn", y, heads)
+        y = n.dense(f"{p}_out", y, hidden, init="torch_linear")
+        x = n.add(f"{p}_add1", x, y)
+        y = n.layernorm(f"{p}_ln2", x)
+        y = n.dense(f"{p}_fc1", y, mlp, init="xavier_uniform", bias_std=1e-6)
+        y = n.act(f"{p}_gelu", y, "gelu")
+        y = n.dense(f"{p}_fc2", y, hidden, init="xavier_uniform", bias_std=1e-6)
+        x = n.add(f"{p}_add2", x, y)
+    x = n.layernorm("ln", x)
+    x = n.select_token("cls", x, 0)
+    x = n.dense("head", x, classes, init="normal002")
+    return n.build(x)
+
+
 BUILDERS = {
+    "vit_b_16": vit_b_16,
     "vgg16": vgg16,
     "mobilenet_v3_large": mobilenet_v3_large,
     "densenet161": densenet161,
@@ -476,6 +545,7 @@ BUILDERS = {
 }
 NORTH_STAR = ("vgg16", "mobilenet_v3_large", "densenet161", "efficientnet_v2_l")
 EIGHT_MODEL_CNNS = NORTH_STAR + ("resnet50", "resnet152", "inception_v3")
+EIGHT_MODEL = EIGHT_MODEL_CNNS + ("vit_b_16",)
 PAIR = ("vgg16", "mobilenet_v3_large")
 
 

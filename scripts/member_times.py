@@ -8,7 +8,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--batch", type=int, default=1)
 ap.add_argument("--set", choices=("north", "eight"), default="north")
 a = ap.parse_args()
-names = zoo.NORTH_STAR if a.set == "north" else zoo.EIGHT_MODEL_CNNS
+names = zoo.NORTH_STAR if a.set == "north" else zoo.EIGHT_MODEL
 models = [zoo.build(n) for n in names]
 
 

@@ -29,6 +29,9 @@ def _act(kind, v):
         return v / (1 + np.exp(-v))
     if kind == "sigmoid":
         return 1 / (1 + np.exp(-v))
+    if kind == "gelu":
+        from scipy.special import erf
+        return (0.5 * v * (1 + erf(v / np.sqrt(2)))).astype(np.float32)
     raise KeyError(kind)
 
 
@@ -72,6 +75,11 @@ class Emulator:
         p = self.p
         xs = np.asarray(xs, np.float32).reshape((self.n,) + tuple(p.input_dims))
         iv = self.view("<input>")
+        b = getattr(p, "input_block", 1)
+        if b > 1:                               # space-to-depth, channel order (r, s, c)
+            n, c, h, w = xs.shape
+            xs = xs.reshape(n, c, h // b, b, w // b, b).transpose(0, 2, 4, 3, 5, 1) \
+                .reshape(n, h // b, w // b, b * b * c).transpose(0, 3, 1, 2)
         if xs.ndim == 4:
             self.store(iv, xs.transpose(0, 2, 3, 1))
         else:
@@ -153,6 +161,39 @@ class Emulator:
             o = o + self.p.blobs[L.blobs["b2"]][:g["c"]]
         o = _act(g["act2"], o.astype(np.float32))
         self.store(self.view(L.dst), o[:, None, None, :])
+
+    def do_ln(self, L):
+        x = self.view(L.src).astype(np.float64)             # (n, 1, L, c)
+        dst = self.view(L.dst)
+        rows = dst.shape[2] if dst.ndim == 4 else 1
+        x = x[:, :, :rows, :]
+        if L.geom["norm"]:
+            mu = x.mean(axis=-1, keepdims=True)
+            var = ((x - mu) ** 2).mean(axis=-1, keepdims=True)
+            g = self.p.blobs[L.blobs["gamma"]][:x.shape[-1]]
+            b = self.p.blobs[L.blobs["beta"]][:x.shape[-1]]
+            x = (x - mu) / np.sqrt(var + L.geom["eps"]) * g + b
+        self.store(dst, x.reshape(dst.shape).astype(np.float32))
+
+    def do_tokens(self, L):
+        x = self.view(L.src)                                 # (n, h, w, c)
+        n, h, w, c = x.shape
+        cls = self.p.blobs[L.blobs["class_token"]][:c]
+        pos = self.p.blobs[L.blobs["pos_embedding"]][:(1 + h * w) * c].reshape(1 + h * w, c)
+        t = np.concatenate([np.broadcast_to(cls, (n, 1, c)), x.reshape(n, h * w, c)], axis=1) + pos
+        self.store(self.view(L.dst), t[:, None].astype(np.float32))
+
+    def do_attn(self, L):
+        x = self.view(L.src)[:, 0].astype(np.float64)       # (n, L, 3c)
+        heads, c = L.geom["heads"], L.geom["c"]
+        d = c // heads
+        outs = []
+        for hd in range(heads):
+            q, k, v = (x[..., j * c + hd * d:j * c + (hd + 1) * d] for j in range(3))
+            s = q @ np.swapaxes(k, 1, 2) / np.sqrt(d)
+            s = np.exp(s - s.max(axis=-1, keepdims=True))
+            outs.append((s / s.sum(axis=-1, keepdims=True)) @ v)
+        self.store(self.view(L.dst), np.concatenate(outs, axis=-1)[:, None].astype(np.float32))
 
     def do_ew(self, L):
         self.store(self.view(L.dst), self.epilogue(L, self.view(L.src)))

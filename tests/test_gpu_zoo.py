@@ -56,13 +56,13 @@ def _check(g, w, x, got):
 
 
 @pytest.mark.slow
-def test_seven_cnn_fused_dag_mixed_batches():
-    """The CNN part of the 8-model config: seven members,
-    different per-member batch sizes in ONE fused launch."""
-    models = [zoo.build(n) for n in zoo.EIGHT_MODEL_CNNS]
+def test_eight_model_fused_dag_mixed_batches():
+    """The 8-model config: seven CNNs + ViT-B/16 with
+    per-member batches {1, 2, 4, 8, 1, 2, 4, 8} in ONE fused graph launch."""
+    models = [zoo.build(n) for n in zoo.EIGHT_MODEL]
     dag = fuse.fuse_models(models)
     rng = np.random.default_rng(78)
-    batches = dict(zip(zoo.EIGHT_MODEL_CNNS, (1, 2, 4, 3, 1, 2, 2)))
+    batches = dict(zip(zoo.EIGHT_MODEL, (1, 2, 4, 8, 1, 2, 4, 8)))
     xs = {g.model_id: rng.standard_normal((batches[g.model_id],) + tuple(g.input_spec.dims)).astype(np.float32)
           for g, _ in models}
     outs = fuse.execute_fused(dag, {g.model_id: [Tensor(g.input_spec, v) for v in xs[g.model_id]]

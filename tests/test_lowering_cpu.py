@@ -64,3 +64,37 @@ def test_launch_counts_show_fusion(corpus):
         nodes += sum(1 for n in g.nodes.values() if n.kind not in ("flatten",))
         launches += len(prog.launches)
     assert launches < nodes
+
+
+def _tiny_vit(res=32, patch=8, **kw):
+    from paper_2410_21120_b200 import zoo
+    return zoo.vit_b_16(model_id=f"vit_tiny_{res}_{patch}", res=res, patch=patch, hidden=128,
+                        layers=2, heads=2, mlp=256, classes=10, **kw)
+
+
+@pytest.mark.parametrize("res,patch", [(32, 8), (64, 8), (16, 16)])     # L = 17, 65, 2
+def test_token_kinds_lowering(res, patch):
+    """ViT kinds (tokens, layernorm(+select), attention, GELU, row-wise dense with
+    residual epilogue): exact in fp32, north-star tolerance in fp16/bf16."""
+    g, w = _tiny_vit(res, patch)
+    xs = np.random.default_rng(res).standard_normal((3, 3, res, res)).astype(np.float32)
+    ref = run_fast(g, w, xs)
+    got = Emulator(lower_member(g, w, keep_f32=True), 3, round_bf16=False).run(xs)
+    assert _rel(got, ref) < 1e-5
+    for pr in ("fp16", "bf16"):
+        got = Emulator(lower_member(g, w, precision=pr), 3).run(xs)
+        assert _rel(got, ref) <= TOL, pr
+
+
+def test_vit_launch_structure():
+    """ViT-B/16: 4 GEMMs + 2 LN + 1 attention per block, residuals and GELU folded
+    into GEMM epilogues, final LN computes only the class-token row."""
+    from paper_2410_21120_b200 import zoo
+    g, w = zoo.build("vit_b_16")
+    prog = lower_member(g, w)
+    kinds = [L.kind for L in prog.launches]
+    assert kinds.count("gemm") == 1 + 12 * 4 + 1
+    assert kinds.count("ln") == 12 * 2 + 1 and kinds.count("attn") == 12
+    assert "ew" not in kinds and kinds.count("tokens") == 1
+    last_ln = [L for L in prog.launches if L.kind == "ln"][-1]
+    assert last_ln.dst == "cls" and prog.values["cls"].w == 1

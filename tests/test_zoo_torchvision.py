@@ -1,4 +1,4 @@
-"""Zoo builders + oracle extension kinds vs torchvision CPU fp32 (same weights).
+"""Zoo builders + oracle extension kinds vs torchvision (same weights), incl. ViT-B/16.
 
 Pins the parts of the oracle that have no reference code (depthwise/grouped
 conv, padded pools, avgpool, hardswish/hardsigmoid/SiLU/sigmoid, channel
@@ -24,7 +24,33 @@ TV = {
     "resnet50": lambda: tv.models.resnet50(),
     "resnet152": lambda: tv.models.resnet152(),
     "inception_v3": lambda: tv.models.inception_v3(aux_logits=False, init_weights=False),
+    "vit_b_16": lambda: tv.models.vit_b_16(),
 }
+
+
+def _load_vit(g, w):
+    """ViT-B/16: parameters by name (MHA's packed in_proj is not a Linear module)."""
+    model = TV["vit_b_16"]().eval()
+
+    def a(name):
+        return torch.from_numpy(w.array(name).copy())
+
+    sd = {"conv_proj.weight": a("conv_proj.weight"), "conv_proj.bias": a("conv_proj.bias"),
+          "class_token": a("tokens.class_token").reshape(1, 1, -1),
+          "encoder.pos_embedding": a("tokens.pos_embedding")[None],
+          "encoder.ln.weight": a("ln.gamma"), "encoder.ln.bias": a("ln.beta"),
+          "heads.head.weight": a("head.weight"), "heads.head.bias": a("head.bias")}
+    layers = sum(1 for n in g.nodes if n.endswith("_attn"))
+    for i in range(layers):
+        p, q = f"enc{i:02d}", f"encoder.layers.encoder_layer_{i}"
+        for ours, theirs in (("ln1", "ln_1"), ("ln2", "ln_2")):
+            sd[f"{q}.{theirs}.weight"], sd[f"{q}.{theirs}.bias"] = a(f"{p}_{ours}.gamma"), a(f"{p}_{ours}.beta")
+        for ours, theirs in (("out", "self_attention.out_proj"), ("fc1", "mlp.0"), ("fc2", "mlp.3")):
+            sd[f"{q}.{theirs}.weight"], sd[f"{q}.{theirs}.bias"] = a(f"{p}_{ours}.weight"), a(f"{p}_{ours}.bias")
+        sd[f"{q}.self_attention.in_proj_weight"] = a(f"{p}_qkv.weight")
+        sd[f"{q}.self_attention.in_proj_bias"] = a(f"{p}_qkv.bias")
+    model.load_state_dict(sd, strict=True)
+    return model
 
 
 def _input(g, seed, n):
@@ -32,6 +58,8 @@ def _input(g, seed, n):
 
 
 def _load_into_torchvision(name, g, w):
+    if name == "vit_b_16":
+        return _load_vit(g, w)
     model = TV[name]().eval()
     mods = [m for m in model.modules()
             if isinstance(m, (torch.nn.Conv2d, torch.nn.Linear, torch.nn.BatchNorm2d))]
@@ -62,7 +90,7 @@ def _load_into_torchvision(name, g, w):
 
 
 @pytest.mark.slow
-@pytest.mark.parametrize("name", zoo.EIGHT_MODEL_CNNS)
+@pytest.mark.parametrize("name", zoo.EIGHT_MODEL)
 def test_builder_and_oracle_match_torchvision(name):
     torch.set_num_threads(8)
     g, w = zoo.build(name)
@@ -83,7 +111,7 @@ def test_builder_and_oracle_match_torchvision(name):
 
 
 @pytest.mark.slow
-@pytest.mark.parametrize("name", zoo.EIGHT_MODEL_CNNS)
+@pytest.mark.parametrize("name", zoo.EIGHT_MODEL)
 def test_calibrated_logits_are_input_sensitive(name):
     g, w = zoo.build(name)
     xs = _input(g, 12, 4)
