@@ -216,6 +216,112 @@ def config_dict(args):
             "l2": "weights 587 MB > 126 MB L2; 256 MB L2-flush write between timed steps (untimed)"}
 
 
+# ----------------------------------------------------------------------------- secondary configs
+
+def time_device_steps(rt, inst, flush, steps, warmup=3):
+    """Device-timed steps of one instance's graph (L2 flushed between steps)."""
+    for _ in range(warmup):
+        inst.launch_graph()
+    inst.sync()
+    ms = []
+    for _ in range(steps):
+        rt.memset(flush, 0, 256 << 20, inst.stream)
+        e0, e1 = rt.Event(), rt.Event()
+        e0.record(inst.stream)
+        inst.launch_graph()
+        e1.record(inst.stream)
+        ms.append(e0.elapsed_ms(e1))
+    inst.sync()
+    return float(np.median(ms)), float(np.mean(ms))
+
+
+def gemm_class(inst, tc_peak):
+    """Tensor-core view of one instance: GEMM launches replayed alone (profile_nodes)."""
+    prof = inst.profile_nodes(reps=4, kinds={"gemm"})
+    ms = sum(r["ms"] for r in prof)
+    fl = sum(r["flops"] for r in prof)
+    best = max(prof, key=lambda r: r["flops"] / r["ms"])
+    return {"gemm_launches": len(prof), "gemm_ms": round(ms, 4),
+            "gemm_tflops": round(fl / (ms * 1e-3) / 1e12, 1),
+            "frac_of_bf16_peak": round(fl / (ms * 1e-3) / 1e12 / tc_peak, 4),
+            "best_launch": {"node": best["node"], "tflops": round(best["flops"] / (best["ms"] * 1e-3) / 1e12, 1)}}
+
+
+def secondary_configs(args, rt, members, programs, arena, flush, P, local_rank):
+    """configs[2] (batch 32 on one GPU), configs[3] (swap-in stress) and configs[4]
+    (8-model mixed batch) -- measured on the same box after the headline run."""
+    from paper_2410_21120_b200.device import DeviceDag, PerTensorArena, WeightArena, program_for
+    tc_peak = float(P.get("bf16_tflops", 1590.0))
+    out = {}
+    # configs[2]: the same fused DAG at batch 32 per member (1 GPU; N>1 shards it over replicas)
+    dag = DeviceDag(members, local_rank, args.mode, arena=arena, programs=programs, precision=args.precision)
+    b = 32
+    inst = dag.acquire(tuple([b] * len(members)))
+    inst.upload_inputs(make_inputs([(sg, w) for sg, w in members], b, seed=99))
+    med, mean = time_device_steps(rt, inst, flush, steps=20)
+    flops = sum(p.gemm_flops_per_sample for p in programs) * b
+    out["batch32"] = {"config": "configs[2]: 4-model fused DAG, batch 32 per member, 1 GPU",
+                      "ms_per_step": med, "images_per_s": len(members) * b / (med * 1e-3),
+                      "step_tflops": round(flops / (med * 1e-3) / 1e12, 1),
+                      "step_frac_of_bf16_peak": round(flops / (med * 1e-3) / 1e12 / tc_peak, 4),
+                      **gemm_class(inst, tc_peak)}
+    dag.free_instances()
+    # configs[3]: swap-in stress -- repeated load/unload of the fused arena vs per-model loads
+    stress = WeightArena(programs, local_rank)
+    fused_ms, fused_copy = [], []
+    for _ in range(20):
+        stress.upload()
+        fused_ms.append(stress.upload_ms)
+        fused_copy.append(stress.memcpy_ms)
+        stress.unload()
+    total = stress.total
+    stress.free()
+    unf = []
+    for _ in range(3):
+        pt = PerTensorArena(programs, local_rank)
+        unf.append(pt.upload_ms)
+        pt.free()
+    out["swap_stress"] = {"config": "configs[3]: 20 load/unload cycles of the fused arena vs 3 per-tensor loads",
+                          "arena_mb": total / 1e6,
+                          "fused_load_ms_median": float(np.median(fused_ms)),
+                          "fused_h2d_gbs_median": total / (float(np.median(fused_copy)) * 1e-3) / 1e9,
+                          "unfused_load_ms_median": float(np.median(unf)),
+                          "speedup": float(np.median(unf) / np.median(fused_ms))}
+    # configs[4]: 8-model fused DAG with mixed per-member batches
+    from paper_2410_21120_b200 import zoo
+    names = list(zoo.EIGHT_MODEL)
+    batches = (1, 2, 4, 8, 1, 2, 4, 8)
+    m8 = build_models(names)
+    p8 = [program_for(g, w, args.precision) for g, w in m8]
+    free0, _ = rt.mem_info()
+    dag8 = DeviceDag(m8, local_rank, args.mode, programs=p8, precision=args.precision)
+    inst8 = dag8.acquire(batches)
+    inst8.upload_inputs([np.random.default_rng(7 + i).standard_normal((bb,) + tuple(g.input_spec.dims))
+                         .astype(np.float32) for i, (bb, (g, _)) in enumerate(zip(batches, m8))])
+    med8, _ = time_device_steps(rt, inst8, flush, steps=20)
+    free1, _ = rt.mem_info()
+    out["eight_model"] = {"config": "configs[4]: 8-model fused DAG, per-member batches "
+                                    + ",".join(f"{n}:{bb}" for n, bb in zip(names, batches)),
+                          "ms_per_step": med8, "images_per_s": sum(batches) / (med8 * 1e-3),
+                          "arena_mb": dag8.arena.total / 1e6, "swap_in_ms": dag8.swap_in_ms,
+                          "peak_hbm_gb": (free0 - free1) / 1e9, "graph_nodes": inst8.kernel_nodes}
+    dag8.free_instances()
+    dag8.arena.free()
+    return out
+
+
+def ncu_traffic():
+    """dram bytes per GEMM launch from the committed ncu capture of this workload
+    (profiles/*traffic*.json, written by scripts/summarize_profiles.py), else None."""
+    for f in sorted((ROOT / "profiles").glob("*traffic*.json"), reverse=True):
+        try:
+            d = json.loads(f.read_text())
+            return d.get("dram_bytes_per_gemm_launch"), f.name
+        except Exception:  # noqa: BLE001
+            continue
+    return None, None
+
+
 # ----------------------------------------------------------------------------- our arm
 
 def run_ours(args, world, rank, local_rank):
@@ -390,6 +496,13 @@ def run_ours(args, world, rank, local_rank):
         "dominant_class": dom,
     }
 
+    traffic, traffic_src = ncu_traffic()
+    roofline["traffic"] = traffic
+    roofline["traffic_source"] = traffic_src
+    roofline["algorithmic_bytes_per_gemm_launch"] = g["bytes"] / max(g["launches"], 1)
+    extra = None
+    if not args.skip_extra and world == 1:
+        extra = secondary_configs(args, rt, members, programs, arena, flush, P, local_rank)
     h2d_gbs = measure_pinned_h2d(rt)
     cpu_ips, cpu_imgs, cpu_s = cpu_port_time(models, xs)
     cores = os.cpu_count() or 1
@@ -436,6 +549,7 @@ def run_ours(args, world, rank, local_rank):
                                    f"oracle/executor_ref.run_fast (numpy fp32, BLAS on {cores} threads)"},
         "parity_rel_err": parity,
         "clocks": clk,
+        "other_configs": extra,
     }
     print(json.dumps(line), flush=True)
     if dist is not None:
@@ -465,6 +579,8 @@ def main():
     ap.add_argument("--models", nargs="+",
                     default=["vgg16", "mobilenet_v3_large", "densenet161", "efficientnet_v2_l"])
     ap.add_argument("--skip-unfused", action="store_true")
+    ap.add_argument("--skip-extra", action="store_true",
+                    help="skip configs[2..4] (batch 32, swap stress, 8-model) after the headline")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     world = int(os.environ.get("WORLD_SIZE", "1"))

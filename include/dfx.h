@@ -197,15 +197,17 @@ typedef struct dfx_out_params {
 
 /* gate[n, c] = act2(b2[c] + sum_j w2[c][j] * act1(b1[j] + sum_k w1[j][k] * mean_hw x[n, :, :, k]))
  * (global_avg_pool -> dense -> act -> dense -> act of the reference IR).
+ * apply = 0: out = gate (n, 1, 1, c);  apply = 1: out = x * gate (n, h, w, c), i.e. the
+ * following channel_scale is fused (each cluster CTA scales its channel slice).
  * w1 [cr][c], w2 [c][cr]: 16-bit, dtype of the views, row-major. */
 typedef struct dfx_se_params {
   dfx_view in;                         /* x (n, h, w, c) */
-  dfx_view out;                        /* gate (n, 1, 1, c) */
+  dfx_view out;                        /* gate (n, 1, 1, c), or x * gate (n, h, w, c) */
   const void* w1;
   const float* b1;                     /* may be NULL */
   const void* w2;
   const float* b2;                     /* may be NULL */
-  int32_t cr, act1, act2, _pad;
+  int32_t cr, act1, act2, apply;
 } dfx_se_params;
 
 /* Token tensors (ViT) are views with h = 1, w = L tokens, c = channels.

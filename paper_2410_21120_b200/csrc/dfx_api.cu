@@ -191,6 +191,9 @@ int config_for(int op, const void* params, size_t size, LaunchCfg* c) {
         return fail(DFX_E_UNSUPPORTED, "se: c=%d cr=%d beyond the cluster kernel's limits",
                     p->in.c, p->cr);
       // one cluster per image: 8 CTAs, or 16 when the weight slices would not fit in smem
+      if (p->apply && (p->out.n != p->in.n || p->out.h != p->in.h || p->out.w != p->in.w ||
+                       p->out.c != p->in.c))
+        return fail(DFX_E_ARG, "se apply: out view must have the input's shape");
       const int cl = dfx::se_smem_bytes(p->in.c, p->cr, 8) <= dfx::kSeSmemBudget ? 8 : 16;
       c->func = se_func(p->in.dtype, cl);
       c->grid = dim3(unsigned(cl), unsigned(p->in.n));

@@ -19,7 +19,9 @@
 //      + bias, act1;
 //   4. computes the gate for its channels (8 lanes per channel, 16-B weight
 //      reads, shuffle reduction), + bias, act2, 16-bit store;
-//   5. cluster.sync so no CTA's smem disappears while a peer still reads it.
+//   5. optionally (apply = 1) the following channel_scale: each CTA multiplies its
+//      channel slice of x by the gate -- no separate elementwise launch;
+//   6. cluster.sync so no CTA's smem disappears while a peer still reads it.
 // Deterministic: fixed summation orders, no atomics.  Timeline probes
 // (-DDFX_TIMELINE): dfx_debug_timeline_se.
 #include <cooperative_groups.h>
@@ -143,7 +145,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kSeThreads)
     pooled[k] = s * (1.0f / float(hw));
   }
   if (threadIdx.x == 0) DFX_TL(2);
-  mbar_wait(&wbar, 0);                                       // weight slices landed
+  if (threadIdx.x == 0) mbar_wait(&wbar, 0);                 // weight slices landed (one poller)
   __syncthreads();
   if (threadIdx.x == 0) DFX_TL(3);
 
@@ -212,7 +214,50 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kSeThreads)
     const int c = c_lo + k;
     float a[8] = {s0 + s1 + (P.b2 ? P.b2[c] : 0.f), 0, 0, 0, 0, 0, 0, 0};
     act8(P.act2, a);
-    st1<T>(out.base, int64_t(n) * out.pitch + out.coff + c, a[0]);
+    if (P.apply)
+      pooled[k] = a[0];                                      // gate of this CTA's channel k
+    else
+      st1<T>(out.base, int64_t(n) * out.pitch + out.coff + c, a[0]);
+  }
+  if (P.apply) {
+    // ---- 5. fused channel_scale: out[n, :, :, slice] = x * gate (x re-read from L2)
+    __syncthreads();
+    const int64_t pb = int64_t(n) * hw;
+    if (((in.coff | out.coff | c_lo | nch) & 7) == 0) {
+      // 4 independent 16-B loads in flight per thread before any store (the
+      // per-iteration load -> store chain otherwise serialises on L2 latency)
+      const int G8 = nch / 8, total = hw * G8;
+      for (int i0 = threadIdx.x; i0 < total; i0 += 4 * kSeThreads) {
+        uint4 raw[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int i = i0 + u * kSeThreads;
+          if (i < total) {
+            const int s = i / G8, g8 = (i - s * G8) * 8;
+            raw[u] = __ldcg(reinterpret_cast<const uint4*>(reinterpret_cast<const T*>(in.base) +
+                                                           view_pixel_index(in, pb + s, c_lo + g8)));
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int i = i0 + u * kSeThreads;
+          if (i < total) {
+            const int s = i / G8, g8 = (i - s * G8) * 8;
+            float x[8];
+            unpack8<T>(raw[u], x);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) x[j] *= pooled[g8 + j];
+            st8<T>(out.base, view_pixel_index(out, pb + s, c_lo + g8), x);
+          }
+        }
+      }
+    } else {
+      for (int i = threadIdx.x; i < hw * nch; i += kSeThreads) {
+        const int s = i / nch, k = i - s * nch;
+        st1<T>(out.base, view_pixel_index(out, pb + s, c_lo + k),
+               ld1<T>(in.base, view_pixel_index(in, pb + s, c_lo + k)) * pooled[k]);
+      }
+    }
   }
   if (threadIdx.x == 0) DFX_TL(7);
   cluster.sync();        // keep this CTA's smem alive until every peer finished reading it

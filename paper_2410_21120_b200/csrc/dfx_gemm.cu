@@ -40,6 +40,13 @@ __device__ unsigned long long dfx_timeline[64];
       dfx_timeline[i] = _t;                                      \
     }                                                            \
   } while (0)
+// block-0 clock64 probes (cycles) into slots 42..63
+#define DFX_TC(i)                                                          \
+  do {                                                                     \
+    if (blockIdx.x == 0 && (i) < 64) dfx_timeline[i] = clock64();         \
+  } while (0)
+#else
+#define DFX_TC(i) do { } while (0)
 #endif
 
 #include "dfx_common.cuh"
@@ -227,7 +234,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       mbar_wait(&hdr->full[slot], par);
       if (it == 0) DFX_TL(3);                      // first stage landed
       if (it > 0 && it < 9) DFX_TL(12 + it);       // later stages landed (13..20)
+      if (it < 7) DFX_TC(42 + 3 * it);
       tc_fence_after();
+      if (it < 7) DFX_TC(43 + 3 * it);
       const uint32_t a_base = smem_u32(slots + slot * slot_bytes);
       const uint32_t b_base = a_base + kStageABytes;
       const int nk = min(kpack, ksteps - st * kpack);
@@ -235,10 +244,15 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         for (int kk = 0; kk < kk_n; ++kk) {
           const uint64_t ad = umma_smem_desc(a_base + j * sub_a + kk * 32, row_bytes);
           const uint64_t bd = umma_smem_desc(b_base + j * sub_b + kk * 32, row_bytes);
+#ifndef DFX_EXP_NOMMA
           umma_f16(tmem_base, ad, bd, idesc, accumulate);
+#else
+          (void)ad; (void)bd; (void)idesc;
+#endif
           accumulate = 1;
         }
       }
+      if (it < 7) DFX_TC(44 + 3 * it);
       if (it < 8) DFX_TL(21 + it);                 // stage's MMAs issued (21..28)
       umma_commit(&hdr->empty[slot]);
     }
@@ -269,11 +283,14 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   const int ldw = D.nt * bn;
 
   griddep_wait();                              // residual / output buffers of predecessors
-  mbar_wait(&hdr->accum, 0);
+  // ONE thread polls the accumulator barrier; the rest park in bar.sync.  (All 128
+  // threads spinning on try_wait measurably slowed the producer's TMA issue and
+  // the mbarrier transaction updates of the stages still in flight.)
+  if (threadIdx.x == 32) mbar_wait(&hdr->accum, 0);
+  __syncthreads();                             // accumulator complete, epilogue vectors visible
   if (threadIdx.x == 0) DFX_TL(5);             // accumulator complete
   tc_fence_after();
   griddep_launch();                            // successor may start its prologue now
-  __syncthreads();                             // staged epilogue vectors visible
 
   const int row = threadIdx.x;                 // tile row == TMEM lane
   const int qi = row % tq;

@@ -140,6 +140,14 @@ class WeightArena:
         self.member_base = [self.dev + off for off, _ in self.segments]
         return self.upload_ms
 
+    def unload(self) -> None:
+        """Free the device copy, keep the pinned host staging (swap-out; the next
+        upload() is again one cudaMalloc + one H2D)."""
+        if self.dev:
+            rt.free(self.dev)
+        self.dev = 0
+        self.member_base = []
+
     def allocate(self) -> None:
         """Device allocation only (a replica that receives the arena by broadcast)."""
         self.dev = rt.malloc(self.total)
@@ -185,7 +193,8 @@ class WeightArena:
         return twin
 
     def free(self):
-        rt.free(self.dev)
+        if self.dev:
+            rt.free(self.dev)
         for p in self.extra_allocs:
             rt.free(p)
         rt.host_free(self.host)
@@ -542,7 +551,7 @@ class ExecInstance:
             addr = (lambda r: arena.addr(m, L.blobs[r]) if r in L.blobs else None)
             yield rt.OP_SE, rt.SeParams(src, self._view(m, prog, L.dst, n), addr("w1"), addr("b1"),
                                         addr("w2"), addr("b2"), geo["cr"], rt.ACT[geo["act1"]],
-                                        rt.ACT[geo["act2"]])
+                                        rt.ACT[geo["act2"]], geo.get("apply", 0))
         else:
             raise AssertionError(L.kind)
 

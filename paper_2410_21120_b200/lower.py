@@ -28,6 +28,7 @@ oracle within the north-star tolerance.
 from __future__ import annotations
 
 import math
+import os
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -39,6 +40,10 @@ from .graph_ir import (ACTIVATION_KINDS, conv_geometry, infer_shapes, pool_geome
 GEMM, DWCONV, POOL, GAP, EW, COPY, SE = "gemm", "dwconv", "pool", "gap", "ew", "copy", "se"
 LN, TOKENS, ATTN = "ln", "tokens", "attn"      # token (ViT) launches, dfx_vit.cu
 SE_MAX_C, SE_MAX_CR = 4096, 512          # limits of dfx_fused.cu se_kernel
+# fold the gate's channel_scale into the SE launch (DFX_SE_FUSE=1).  Off by default: the
+# in-cluster scaling on 8-16 CTAs measured slower (EfficientNetV2-L alone 2.73 vs 2.66 ms)
+# than the separate full-GPU elementwise launch it replaces, which PDL mostly hides.
+SE_FUSE_SCALE = os.environ.get("DFX_SE_FUSE", "0") == "1"
 
 
 def round_up(x: int, a: int) -> int:
@@ -558,10 +563,19 @@ class _Lowerer:
         cr = int(self.g.nodes[fcs[0]].attrs["units"])
         if int(self.g.nodes[fcs[1]].attrs["units"]) != c or c > SE_MAX_C or cr > SE_MAX_CR:
             return None
+        # the gate's only consumer scales the pooled tensor itself: fuse it (apply = 1)
+        apply = 0
+        sc = self.single_user(cur)
+        x = self.src_of(gap_id)
+        if SE_FUSE_SCALE and sc is not None and self.g.nodes[sc].kind == "channel_scale" \
+                and self.g.nodes[sc].inputs == (x, cur):
+            chain.append(sc)
+            cur, apply = sc, 1
         for n in chain[1:]:
             self.absorbed[n] = gap_id
-        L = Launch(SE, chain, self.src_of(gap_id), cur,
-                   geom=dict(c=c, cr=cr, act1=acts[0], act2=acts[1], fc1=fcs[0], fc2=fcs[1]))
+        L = Launch(SE, chain, x, cur,
+                   geom=dict(c=c, cr=cr, act1=acts[0], act2=acts[1], fc1=fcs[0], fc2=fcs[1],
+                             apply=apply))
         self.pending_se.append(L)
         return L
 

@@ -93,7 +93,7 @@ class OutParams(C.Structure):
 
 class SeParams(C.Structure):
     _fields_ = [("inp", View), ("out", View), ("w1", vp), ("b1", vp), ("w2", vp), ("b2", vp),
-                ("cr", i32), ("act1", i32), ("act2", i32), ("_pad", i32)]
+                ("cr", i32), ("act1", i32), ("act2", i32), ("apply", i32)]
 
 
 class LnParams(C.Structure):

@@ -339,8 +339,17 @@ EFFV2L_CFG = (  # block, expand, kernel, stride, in, out, layers
 )
 
 
-def efficientnet_v2_l(model_id="efficientnet_v2_l", seed=1604, calib=None, res=224, classes=1000):
+# Residual-branch gain of EfficientNetV2's MBConv / FusedMBConv blocks (gamma of the
+# projection BN of every block with a skip connection), as for ResNet: at random init
+# the 56 residual blocks otherwise compound into logits so input-chaotic that fp16
+# storage noise reads as a 2-3% logit error on some inputs.
+EFFNET_BRANCH_GAIN = 0.2
+
+
+def efficientnet_v2_l(model_id="efficientnet_v2_l", seed=1604, calib=None, res=224, classes=1000,
+                      branch_gain=None):
     n = Net(model_id, (3, res, res), seed, calib)
+    gain = EFFNET_BRANCH_GAIN if branch_gain is None else branch_gain
     eps = 1e-3
     x = n.conv("stem_conv", None, 32, 3, stride=2, pad=1)
     x = n.act("stem_act", n.bn("stem_bn", x, eps), "silu")
@@ -355,7 +364,8 @@ def efficientnet_v2_l(model_id="efficientnet_v2_l", seed=1604, calib=None, res=2
                 else:
                     x = n.conv(f"{p}_exp", x, make_divisible(cin * e), k, stride=s)
                     x = n.act(f"{p}_exp_act", n.bn(f"{p}_exp_bn", x, eps), "silu")
-                    x = n.bn(f"{p}_proj_bn", n.conv(f"{p}_proj", x, cout, 1, pad=0), eps)
+                    x = n.bn(f"{p}_proj_bn", n.conv(f"{p}_proj", x, cout, 1, pad=0), eps,
+                             gamma_scale=gain if (s == 1 and cin == cout) else 1.0)
             else:
                 exp = make_divisible(cin * e)
                 x = n.act(f"{p}_exp_act", n.bn(f"{p}_exp_bn", n.conv(f"{p}_exp", x, exp, 1, pad=0), eps), "silu")
@@ -366,7 +376,8 @@ def efficientnet_v2_l(model_id="efficientnet_v2_l", seed=1604, calib=None, res=2
                 t = n.act(f"{p}_se_act", n.dense(f"{p}_se_fc1", t, sq, init="se"), "silu")
                 t = n.act(f"{p}_se_gate", n.dense(f"{p}_se_fc2", t, exp, init="se"), "sigmoid")
                 x = n.scale(f"{p}_se_scale", x, t)
-                x = n.bn(f"{p}_proj_bn", n.conv(f"{p}_proj", x, cout, 1, pad=0), eps)
+                x = n.bn(f"{p}_proj_bn", n.conv(f"{p}_proj", x, cout, 1, pad=0), eps,
+                         gamma_scale=gain if (s == 1 and cin == cout) else 1.0)
             if s == 1 and cin == cout:
                 x = n.add(f"{p}_add", x, inp)
     x = n.conv("head_conv", x, 1280, 1, pad=0)

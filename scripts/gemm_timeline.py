@@ -59,6 +59,9 @@ for case in a.cases.split(","):
     tl += f"\n   A loads issued: {(buf[29] - base) / 1e3:.2f}"
     tl += "\n   B prefetch issued: " + " ".join(f"{(buf[30 + i] - base) / 1e3:.2f}"
                                               for i in range(0, min(stages, 8)))
+    tl += "\n   MMA loop cycles (landed->fenced->issued, from stage-0 landing): " + "  ".join(
+        f"{buf[42 + 3 * i] - buf[42]}/{buf[43 + 3 * i] - buf[42]}/{buf[44 + 3 * i] - buf[42]}"
+        for i in range(0, min(stages, 7)))
     tl += f"\n   SM clock over the CTA: {(buf[41] - buf[40]) / max(buf[6] - buf[0], 1) * 1e3:.0f} MHz"
     print(f"cin={cin} cout={cout} hw={hw} n={n} tiling={gemm[2]['tiling']['tiles']}t/"
           f"{gemm[2]['tiling']['splits']}s/{gemm[2]['tiling']['stages']}st  graph {ms * 1e3 / a.chain:.1f} us/node"

@@ -160,7 +160,10 @@ class Emulator:
         if "b2" in L.blobs:
             o = o + self.p.blobs[L.blobs["b2"]][:g["c"]]
         o = _act(g["act2"], o.astype(np.float32))
-        self.store(self.view(L.dst), o[:, None, None, :])
+        if g.get("apply"):                                     # fused channel_scale
+            self.store(self.view(L.dst), x * o[:, None, None, :])
+        else:
+            self.store(self.view(L.dst), o[:, None, None, :])
 
     def do_ln(self, L):
         x = self.view(L.src).astype(np.float64)             # (n, 1, L, c)
