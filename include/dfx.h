@@ -126,7 +126,7 @@ typedef struct __attribute__((aligned(64))) dfx_gemm_desc {
   int32_t cout;
   int32_t tile_begin;              /* first blockIdx.x of this problem */
   int32_t tiles;                   /* mt_n*mt_p*mt_q*nt*splits */
-  int32_t _pad0;
+  int32_t m2;                      /* 1: the CTA covers M tiles 2i and 2i+1, sharing each B stage */
   dfx_view out;                    /* bf16 output view (n, p, q, cout) */
   dfx_epilogue epi;
   float* ws;                       /* split-K workspace [splits][n*p*q][nt*bn] */
@@ -147,7 +147,9 @@ typedef struct __attribute__((aligned(64))) dfx_gemm_launch {
   int32_t bn_max;                  /* sizes smem / TMEM */
   int32_t dtype;                   /* dfx_dtype of every problem */
   int32_t nslots;                  /* smem pipeline depth, 2..8 */
-  int32_t _pad[9];
+  int32_t flags;                   /* bit 0: read desc0 from `descs` (debug) */
+  int32_t m2;                      /* any problem has m2 = 1 (sizes smem / TMEM) */
+  int32_t _pad[7];
   dfx_gemm_desc desc0;             /* the problem when ndesc == 1 */
 } dfx_gemm_launch;
 

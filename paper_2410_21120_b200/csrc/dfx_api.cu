@@ -13,7 +13,7 @@
 #include "dfx_common.cuh"
 
 namespace dfx {
-template <typename T> __global__ void gemm_kernel(const __grid_constant__ dfx_gemm_launch L);
+template <typename T, int M2> __global__ void gemm_kernel(const __grid_constant__ dfx_gemm_launch L);
 template <typename T> __global__ void splitk_kernel(const __grid_constant__ dfx_splitk_params P);
 template <typename T> __global__ void ew_kernel(const __grid_constant__ dfx_ew_params P);
 template <typename T> __global__ void dwconv_kernel(const __grid_constant__ dfx_dwconv_params P);
@@ -33,6 +33,14 @@ template <typename T> __global__ void attn_kernel(const __grid_constant__ dfx_at
                    : reinterpret_cast<const void*>(&dfx::K<__nv_bfloat16>))
 
 namespace {
+
+const void* gemm_func(int dt, int m2) {
+  if (m2)
+    return dt == DFX_F16 ? reinterpret_cast<const void*>(&dfx::gemm_kernel<__half, 1>)
+                         : reinterpret_cast<const void*>(&dfx::gemm_kernel<__nv_bfloat16, 1>);
+  return dt == DFX_F16 ? reinterpret_cast<const void*>(&dfx::gemm_kernel<__half, 0>)
+                       : reinterpret_cast<const void*>(&dfx::gemm_kernel<__nv_bfloat16, 0>);
+}
 
 const void* se_func(int dt, int cl) {
   if (cl == 16)
@@ -123,12 +131,13 @@ int config_for(int op, const void* params, size_t size, LaunchCfg* c) {
       const auto* p = static_cast<const dfx_gemm_launch*>(params);
       if (p->bn_max < 16 || p->bn_max > 256 || p->total_tiles < 1)
         return fail(DFX_E_ARG, "gemm: bad bn_max %d / tiles %d", p->bn_max, p->total_tiles);
-      c->func = DFX_PICK(gemm_kernel, p->dtype);
+      c->func = gemm_func(p->dtype, p->m2);
       c->grid = dim3(p->total_tiles);
       c->block = dim3(128);
       if (p->nslots < 2 || p->nslots > dfx::kMaxSlots)
         return fail(DFX_E_ARG, "gemm: nslots %d", p->nslots);
-      c->smem = dfx::gemm_smem_bytes(p->bn_max, p->nslots) + 1024;
+      if (p->m2 && p->bn_max > 256) return fail(DFX_E_ARG, "gemm: m2 with bn %d", p->bn_max);
+      c->smem = dfx::gemm_smem_bytes(p->bn_max, p->nslots, p->m2 ? 1 : 0) + 1024;
       if (c->smem > size_t(kGemmSmemLimit))
         return fail(DFX_E_ARG, "gemm: %zu B of shared memory (bn %d x %d slots)", c->smem,
                     p->bn_max, p->nslots);
@@ -299,8 +308,9 @@ int dfx_init(int device) {
                 prop.major, prop.minor);
   g_sm_count = prop.multiProcessorCount;
   for (int dt : {int(DFX_BF16), int(DFX_F16)}) {
-    CK(cudaFuncSetAttribute(DFX_PICK(gemm_kernel, dt), cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            kGemmSmemLimit));
+    for (int m2 : {0, 1})
+      CK(cudaFuncSetAttribute(gemm_func(dt, m2), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              kGemmSmemLimit));
     for (int cl : {8, 16})
       CK(cudaFuncSetAttribute(se_func(dt, cl), cudaFuncAttributeMaxDynamicSharedMemorySize,
                               dfx::kSeSmemBudget));

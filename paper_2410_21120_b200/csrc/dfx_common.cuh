@@ -373,9 +373,12 @@ constexpr int kHeaderBytes = 1024;           // barriers + staged descriptor
 constexpr int kEpiBytes = 2048;              // alpha[256] + beta[256] fp32, staged
 constexpr int kSlotsOffset = kHeaderBytes + kEpiBytes;   // 1024-B aligned
 
-__host__ __device__ inline int gemm_slot_bytes(int bn_max) { return kStageABytes + bn_max * 128; }
-__host__ __device__ inline int gemm_smem_bytes(int bn_max, int nslots) {
-  return kSlotsOffset + nslots * gemm_slot_bytes(bn_max);
+// one pipeline slot: A of 1 (or 2, m2) M tiles of 128 rows x 64 K, then B of bn rows x 64 K
+__host__ __device__ inline int gemm_slot_bytes(int bn_max, int m2 = 0) {
+  return kStageABytes * (1 + m2) + bn_max * 128;
+}
+__host__ __device__ inline int gemm_smem_bytes(int bn_max, int nslots, int m2 = 0) {
+  return kSlotsOffset + nslots * gemm_slot_bytes(bn_max, m2);
 }
 // ---- squeeze-excitation cluster kernel geometry (dfx_fused.cu)
 constexpr int kSeThreads = 256;

@@ -79,7 +79,9 @@ struct GemmHeader {
 };
 static_assert(sizeof(GemmHeader) <= kHeaderBytes, "gemm smem header overflow");
 
-template <typename T>
+// M2 (compile-time): 256-row CTAs, see `m2` below.  A separate instantiation so the
+// latency-critical 128-row path carries none of the second tile's bookkeeping.
+template <typename T, int M2>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     gemm_kernel(const __grid_constant__ dfx_gemm_launch L) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -90,7 +92,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   float* s_alpha = reinterpret_cast<float*>(smem + kHeaderBytes);
   float* s_beta = s_alpha + 256;
   uint8_t* slots = smem + kSlotsOffset;
-  const int slot_bytes = gemm_slot_bytes(L.bn_max);
+  constexpr int m2l = M2;                          // slot / TMEM sizing
+  const int slot_bytes = gemm_slot_bytes(L.bn_max, m2l);
+  const int a_bytes = kStageABytes * (1 + m2l);    // A part of a slot (B follows)
   const int nslots = L.nslots;
   if (threadIdx.x == 0) DFX_TL(0);                 // CTA start
 #ifdef DFX_TIMELINE
@@ -102,7 +106,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   const int bid = blockIdx.x;
 
   const dfx_gemm_desc* gd;                         // tensor maps are read through this
-  if (L.ndesc == 1 && L._pad[0] == 0) {
+  if (L.ndesc == 1 && (L.flags & 1) == 0) {
     gd = &L.desc0;                                 // kernel-parameter space
   } else {
     int pi = 0;
@@ -115,7 +119,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   if (threadIdx.x < sizeof(dfx_gemm_desc) / 16)
     reinterpret_cast<uint4*>(&hdr->desc)[threadIdx.x] =
         reinterpret_cast<const uint4*>(gd)[threadIdx.x];
-  const uint32_t tmem_cols = tmem_cols_for(L.bn_max);
+  const uint32_t tmem_cols = tmem_cols_for(L.bn_max * (1 + m2l));
   if (threadIdx.x == 0) {
     DFX_TL(7);                                     // descriptor copied
     for (int i = 0; i < nslots; ++i) {
@@ -146,14 +150,24 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   const int tn = D.tn, tp = D.tp, tq = D.tq;
   int t = bid - D.tile_begin;
   const int mt_total = D.mt_n * mt_p * mt_q;
-  const int mi = t % mt_total;
-  t /= mt_total;
+  // m2: this CTA owns M tiles 2g and 2g+1 (two TMEM accumulators, columns [0, bn)
+  // and [bn, 2bn)); both are multiplied by the same B stage, so the weight bytes
+  // per MAC halve -- the lever when the chip-wide TMA/L2 fill rate caps the MMA.
+  constexpr int m2 = M2;
+  const int mgroups = m2 ? (mt_total + 1) / 2 : mt_total;
+  const int mi = (t % mgroups) << m2;
+  t /= mgroups;
   const int split = t % splits;
   const int ntile = t / splits;
-  const int mq = mi % mt_q;
-  const int mp = (mi / mt_q) % mt_p;
-  const int mn = mi / (mt_q * mt_p);
-  const int n0 = mn * tn, p0 = mp * tp, q0 = mq * tq;
+  const int nhalf = (m2 && mi + 1 < mt_total) ? 2 : 1;   // M tiles in this CTA
+  int n0h[1 + M2], p0h[1 + M2], q0h[1 + M2];
+#pragma unroll
+  for (int h = 0; h < 1 + M2; ++h) {
+    const int m = mi + h;
+    n0h[h] = (m / (mt_q * mt_p)) * tn;
+    p0h[h] = ((m / mt_q) % mt_p) * tp;
+    q0h[h] = (m % mt_q) * tq;
+  }
   const int bn = D.bn, cb = D.cb, kpack = D.kpack, ksteps = D.ksteps;
   const int st_begin = split * D.stages_per_split;
   const int st_end = min(D.stages, st_begin + D.stages_per_split);
@@ -166,8 +180,13 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   if (warp == 0 && lane == 0) {
     // ================= TMA producer
     const int cblocks = D.cblocks, S = D.s;
-    const int qbase = q0 * D.stride_w - D.pad_w, pbase = p0 * D.stride_h - D.pad_h;
-    const uint32_t box_a_bytes = uint32_t(cb) * 2u * tq * tp * tn;
+    int qb[1 + M2], pb[1 + M2];
+#pragma unroll
+    for (int h = 0; h < 1 + M2; ++h) {
+      qb[h] = q0h[h] * D.stride_w - D.pad_w;
+      pb[h] = p0h[h] * D.stride_h - D.pad_h;
+    }
+    const uint32_t box_a_bytes = uint32_t(cb) * 2u * tq * tp * tn * nhalf;
     const void* tma = gd->tmap_a;
     const void* tmb = gd->tmap_b;
     // Weights are static: the first nslots stages' B tiles are requested before
@@ -175,7 +194,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     const int npre = min(nslots, st_end - st_begin);
     for (int it = 0; it < npre; ++it) {
       const int st = st_begin + it;
-      uint8_t* b_dst = slots + it * slot_bytes + kStageABytes;
+      uint8_t* b_dst = slots + it * slot_bytes + a_bytes;
       const int k0 = st * kpack;
       const int nk = min(kpack, ksteps - k0);
       mbar_arrive_expect_tx(&hdr->full[it], nk * (box_a_bytes + uint32_t(sub_b)));
@@ -197,7 +216,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         const int cblk = kstep - rs * cblocks;
         const int r = rs / S;
         const int s = rs - r * S;
-        tma_load_4d(a_dst + j * sub_a, tma, &hdr->full[it], cblk * cb, qbase + s, pbase + r, n0);
+#pragma unroll
+        for (int h = 0; h < 1 + M2; ++h)
+          if (h < nhalf)
+            tma_load_4d(a_dst + h * kStageABytes + j * sub_a, tma, &hdr->full[it], cblk * cb, qb[h] + s,
+                        pb[h] + r, n0h[h]);
       }
     }
     DFX_TL(29);                                    // all prefetched stages' A loads issued
@@ -207,7 +230,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       const uint32_t par = (it / nslots) & 1;
       mbar_wait(&hdr->empty[slot], par ^ 1);
       uint8_t* a_dst = slots + slot * slot_bytes;
-      uint8_t* b_dst = a_dst + kStageABytes;
+      uint8_t* b_dst = a_dst + a_bytes;
       const int k0 = st * kpack;
       const int nk = min(kpack, ksteps - k0);
       mbar_arrive_expect_tx(&hdr->full[slot], nk * (box_a_bytes + uint32_t(sub_b)));
@@ -217,7 +240,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         const int cblk = kstep - rs * cblocks;
         const int r = rs / S;
         const int s = rs - r * S;
-        tma_load_4d(a_dst + j * sub_a, tma, &hdr->full[slot], cblk * cb, qbase + s, pbase + r, n0);
+#pragma unroll
+        for (int h = 0; h < 1 + M2; ++h)
+          if (h < nhalf)
+            tma_load_4d(a_dst + h * kStageABytes + j * sub_a, tma, &hdr->full[slot], cblk * cb, qb[h] + s,
+                        pb[h] + r, n0h[h]);
         tma_load_2d(b_dst + j * sub_b, tmb, &hdr->full[slot], kstep * cb, co_base);
       }
     }
@@ -238,17 +265,21 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       tc_fence_after();
       if (it < 7) DFX_TC(43 + 3 * it);
       const uint32_t a_base = smem_u32(slots + slot * slot_bytes);
-      const uint32_t b_base = a_base + kStageABytes;
+      const uint32_t b_base = a_base + a_bytes;
       const int nk = min(kpack, ksteps - st * kpack);
       for (int j = 0; j < nk; ++j) {
         for (int kk = 0; kk < kk_n; ++kk) {
-          const uint64_t ad = umma_smem_desc(a_base + j * sub_a + kk * 32, row_bytes);
           const uint64_t bd = umma_smem_desc(b_base + j * sub_b + kk * 32, row_bytes);
+#pragma unroll
+          for (int h = 0; h < 1 + M2; ++h) {
+            if (h >= nhalf) break;
+            const uint64_t ad = umma_smem_desc(a_base + h * kStageABytes + j * sub_a + kk * 32, row_bytes);
 #ifndef DFX_EXP_NOMMA
-          umma_f16(tmem_base, ad, bd, idesc, accumulate);
+            umma_f16(tmem_base + uint32_t(h * bn), ad, bd, idesc, accumulate);
 #else
-          (void)ad; (void)bd; (void)idesc;
+            (void)ad; (void)bd; (void)idesc;
 #endif
+          }
           accumulate = 1;
         }
       }
@@ -296,18 +327,21 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   const int qi = row % tq;
   const int pi_ = (row / tq) % tp;
   const int ni = row / (tq * tp);
-  const int on = n0 + ni, op = p0 + pi_, oq = q0 + qi;
-  const bool valid = row < tn * tp * tq && on < N && op < P && oq < Q;
-  const int64_t pix = (int64_t(on) * P + op) * Q + oq;
   const uint32_t lane_addr = tmem_base + (uint32_t(warp * 32) << 16);
   const int ncols = min(bn, ((cout - co_base) + 15) & ~15);
   const bool views_vec = vec8_ok(o, 0) && (e.binop == DFX_BIN_NONE || vec8_ok(e.other, 0));
 
   const int64_t plane = int64_t(N) * P * Q * ldw;      // one split's partials
   if (threadIdx.x == 0) DFX_TL(11);                    // epilogue starts
+#pragma unroll
+  for (int h = 0; h < 1 + M2; ++h) {                   // M tiles of this CTA (m2: two)
+  if (h >= nhalf) break;
+  const int on = n0h[h] + ni, op = p0h[h] + pi_, oq = q0h[h] + qi;
+  const bool valid = row < tn * tp * tq && on < N && op < P && oq < Q;
+  const int64_t pix = (int64_t(on) * P + op) * Q + oq;
   for (int c0 = 0; c0 < ncols; c0 += 16) {
     float v[16];
-    tmem_ld16(lane_addr + uint32_t(c0), v);
+    tmem_ld16(lane_addr + uint32_t(h * bn + c0), v);
     if (c0 == 0 && threadIdx.x == 0) DFX_TL(12);       // first TMEM load back
     if (!valid) continue;
     const int co = co_base + c0;
@@ -330,6 +364,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       epilogue_store_tail<T>(e, o, tail, pix, on, co, min(16, cout - co));
     }
   }
+  }
 
   if (splits > 1 && D.counters != nullptr) {
     // ---- in-kernel split-K fixup (DFX_SPLITK=fixup): the last CTA to arrive for
@@ -348,7 +383,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         const int r = item / c8n;
         const int co = co_base + (item - r * c8n) * 8;
         const int rq = r % tq, rp = (r / tq) % tp, rn = r / (tq * tp);
-        const int an = n0 + rn, ap = p0 + rp, aq = q0 + rq;
+        const int an = n0h[0] + rn, ap = p0h[0] + rp, aq = q0h[0] + rq;
         if (r >= tn * tp * tq || an >= N || ap >= P || aq >= Q || co >= cout) continue;
         const int64_t rpix = (int64_t(an) * P + ap) * Q + aq;
         const float4* src = reinterpret_cast<const float4*>(ws + rpix * ldw + co);
@@ -418,8 +453,10 @@ __global__ void splitk_kernel(const __grid_constant__ dfx_splitk_params P) {
   }
 }
 
-template __global__ void gemm_kernel<__nv_bfloat16>(const __grid_constant__ dfx_gemm_launch);
-template __global__ void gemm_kernel<__half>(const __grid_constant__ dfx_gemm_launch);
+template __global__ void gemm_kernel<__nv_bfloat16, 0>(const __grid_constant__ dfx_gemm_launch);
+template __global__ void gemm_kernel<__half, 0>(const __grid_constant__ dfx_gemm_launch);
+template __global__ void gemm_kernel<__nv_bfloat16, 1>(const __grid_constant__ dfx_gemm_launch);
+template __global__ void gemm_kernel<__half, 1>(const __grid_constant__ dfx_gemm_launch);
 template __global__ void splitk_kernel<__nv_bfloat16>(const __grid_constant__ dfx_splitk_params);
 template __global__ void splitk_kernel<__half>(const __grid_constant__ dfx_splitk_params);
 

@@ -70,12 +70,12 @@ GEMM_SMEM_LIMIT = 227 * 1024 - 1024          # minus the kernel's 1 KB alignment
 GEMM_SMEM_FIXED = 1024 + 2048                # barriers/descriptor + epilogue vectors
 
 
-def gemm_slots(bn: int, tiles: int, sm_count: int = 148) -> int:
+def gemm_slots(bn: int, tiles: int, sm_count: int = 148, m2: int = 0) -> int:
     """Pipeline depth of a GEMM launch: as deep as shared memory allows (<= 8)
     when the grid fits in one wave -- every extra slot is another weight tile
     requested before griddepcontrol.wait -- else 4, leaving room for two CTAs
-    per SM on narrow tiles."""
-    slot = 128 * 64 * 2 + bn * 128
+    per SM on narrow tiles.  m2 slots hold two A tiles (dfx_common.cuh gemm_slot_bytes)."""
+    slot = 128 * 64 * 2 * (1 + m2) + bn * 128
     fit = (GEMM_SMEM_LIMIT - GEMM_SMEM_FIXED) // slot
     return max(2, min(8 if tiles <= sm_count else 4, fit))
 
@@ -495,6 +495,7 @@ class ExecInstance:
             d.cb, d.cblocks, d.ksteps, d.kpack = geo["cb"], geo["cblocks"], geo["ksteps"], t["kpack"]
             d.stages, d.splits, d.stages_per_split = t["stages"], t["splits"], t["sps"]
             d.bn, d.cout, d.tile_begin, d.tiles = t["bn"], geo["cout"], 0, t["tiles"]
+            d.m2 = t.get("m2", 0)
             d.out = out
             epi = self._epi(m, prog, L, n)
             if geo.get("tokens") and epi.binop:
@@ -509,7 +510,9 @@ class ExecInstance:
             host_descs.append(d)
             self.gemm_count += 1
             gl = rt.GemmLaunch(self.descs + slot * C.sizeof(rt.GemmDesc), 1, t["tiles"], t["bn"],
-                               self.dtype, gemm_slots(t["bn"], t["tiles"], self.dag.sm_count))
+                               self.dtype, gemm_slots(t["bn"], t["tiles"], self.dag.sm_count,
+                                                      t.get("m2", 0)))
+            gl.m2 = t.get("m2", 0)
             gl.desc0 = d                    # single problem: descriptor in kernel-param space
             yield rt.OP_GEMM, gl
             if t["splits"] > 1 and not fixup:

@@ -709,6 +709,9 @@ def choose_bn(cout: int) -> tuple[int, int]:
     return bn, -(-cout // bn)
 
 
+GEMM_M2 = os.environ.get("DFX_GEMM_M2", "1") != "0"     # A/B switch for 256-row CTAs
+
+
 def gemm_tiling(geom: dict, n: int, p: int, q: int, sm_count: int = 148) -> dict:
     tn, tp, tq = choose_m_tile(n, p, q, geom["sh"], geom["sw"])
     mt = (math.ceil(n / tn), math.ceil(p / tp), math.ceil(q / tq))
@@ -726,6 +729,14 @@ def gemm_tiling(geom: dict, n: int, p: int, q: int, sm_count: int = 148) -> dict
         splits = min(math.ceil(sm_count / base), stages // 4)      # >= 4 stages per split
     sps = math.ceil(stages / max(splits, 1))
     splits = math.ceil(stages / sps)
+    # m2: 256-row CTAs (two M tiles sharing each weight stage) once the grid still
+    # fills the GPU -- halves B bytes per MAC for the fill-rate-bound large layers
+    # (a 256-row CTA takes ~1.6x a 128-row one: only when the wave count drops enough)
+    waves1 = math.ceil(m_tiles * nt / sm_count)
+    waves2 = math.ceil(math.ceil(m_tiles / 2) * nt / sm_count)
+    m2 = int(GEMM_M2 and splits == 1 and bn >= 128 and m_tiles >= 2
+             and math.ceil(m_tiles / 2) * nt >= sm_count and waves2 * 1.6 < waves1)
+    tiles = (math.ceil(m_tiles / 2) if m2 else m_tiles) * nt * splits
     return dict(tn=tn, tp=tp, tq=tq, mt_n=mt[0], mt_p=mt[1], mt_q=mt[2], bn=bn, nt=nt,
-                kpack=kpack, stages=stages, splits=splits, sps=sps,
-                tiles=base * splits)
+                kpack=kpack, stages=stages, splits=splits, sps=sps, m2=m2,
+                tiles=tiles)

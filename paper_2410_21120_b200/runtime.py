@@ -49,13 +49,14 @@ class GemmDesc(C.Structure):
                 ("r", i32), ("s", i32), ("stride_h", i32), ("stride_w", i32),
                 ("pad_h", i32), ("pad_w", i32), ("cb", i32), ("cblocks", i32), ("ksteps", i32),
                 ("kpack", i32), ("stages", i32), ("splits", i32), ("stages_per_split", i32),
-                ("bn", i32), ("cout", i32), ("tile_begin", i32), ("tiles", i32), ("_pad0", i32),
+                ("bn", i32), ("cout", i32), ("tile_begin", i32), ("tiles", i32), ("m2", i32),
                 ("out", View), ("epi", Epilogue), ("ws", vp), ("counters", vp), ("_pad1", i64 * 2)]
 
 
 class GemmLaunch(C.Structure):
     _fields_ = [("descs", vp), ("ndesc", i32), ("total_tiles", i32), ("bn_max", i32),
-                ("dtype", i32), ("nslots", i32), ("_pad", i32 * 9), ("desc0", GemmDesc)]
+                ("dtype", i32), ("nslots", i32), ("flags", i32), ("m2", i32), ("_pad", i32 * 7),
+                ("desc0", GemmDesc)]
 
 
 class SplitKParams(C.Structure):

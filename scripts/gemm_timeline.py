@@ -34,7 +34,7 @@ for case in a.cases.split(","):
     inst.upload_inputs([rng.standard_normal((n, cin, hw, hw)).astype(np.float32)])
     gemm = [(op, p, info) for op, p, info in inst.nodes if op == rt.OP_GEMM][0]
     if a.global_desc:
-        gemm[1]._pad[0] = 1          # debug: read descriptor + tensor maps from global memory
+        gemm[1].flags = 1          # debug: read descriptor + tensor maps from global memory
     graph = rt.Graph()
     last = None
     for _ in range(a.chain):

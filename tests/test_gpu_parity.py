@@ -64,6 +64,23 @@ def test_conv_layer(cin, h, w, cout, k, s, p, n):
     assert rel(got, ref) < TOL
 
 
+# large-M layers that take the 256-row CTA path (two M tiles per CTA sharing each
+# weight stage, lower.gemm_tiling m2), including an odd M-tile count (last CTA
+# holds one tile) and a stride-2 input
+M2_CASES = [(64, 28, 28, 256, 3, 1, 1, 21), (64, 28, 28, 128, 3, 1, 1, 64),
+            (128, 14, 14, 256, 1, 1, 0, 148), (32, 56, 56, 256, 3, 2, 1, 21)]
+
+
+@pytest.mark.parametrize("cin,h,w,cout,k,s,p,n", M2_CASES)
+def test_conv_layer_m2_tiles(cin, h, w, cout, k, s, p, n):
+    from paper_2410_21120_b200.lower import choose_cb, gemm_tiling
+    cb = choose_cb(cin)
+    oh = (h + 2 * p - k) // s + 1
+    t = gemm_tiling(dict(cout=cout, cb=cb, ksteps=k * k * (-(-cin // cb)), sh=s, sw=s), n, oh, oh)
+    assert t["m2"] == 1
+    test_conv_layer(cin, h, w, cout, k, s, p, n)
+
+
 @pytest.mark.parametrize("units,fan_in,n", [(10, 7, 1), (4096, 25088 // 49, 2), (1000, 1280, 3), (240, 960, 1)])
 def test_dense_layer(units, fan_in, n):
     rng = np.random.default_rng(units)
