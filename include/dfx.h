@@ -147,7 +147,10 @@ typedef struct __attribute__((aligned(64))) dfx_gemm_launch {
   int32_t bn_max;                  /* sizes smem / TMEM */
   int32_t dtype;                   /* dfx_dtype of every problem */
   int32_t nslots;                  /* smem pipeline depth, 2..8 */
-  int32_t flags;                   /* bit 0: read desc0 from `descs` (debug) */
+  int32_t flags;                   /* bit 0: read desc0 from `descs` (debug);
+                                      bit 1: persistent kernel (<= 2 CTAs/SM walk the
+                                      tile list, double-buffered TMEM; one problem,
+                                      no split-K, no m2) */
   int32_t m2;                      /* any problem has m2 = 1 (sizes smem / TMEM) */
   int32_t _pad[7];
   dfx_gemm_desc desc0;             /* the problem when ndesc == 1 */
@@ -182,14 +185,16 @@ typedef struct dfx_ew_params {
   dfx_epilogue epi;
 } dfx_ew_params;
 
-/* block <= 1: out[n, h, w, c] = src[n][c][h][w].
- * block = b > 1 (space-to-depth, feeds a patchify conv with kernel = stride = b
- * as a 1x1 GEMM): out has h = H/b, w = W/b, c = b*b*C and
- * out[n, y, x, (r*b + s)*C + c] = src[n][c][y*b + r][x*b + s]. */
+/* kh == 0: out[n, h, w, c] = src[n][c][h][w]  (out.c == c, out.h == h, out.w == w).
+ * kh > 0 (im2col of the entry conv -- a stem with few input channels, or a
+ * patchify conv -- which then runs as a 1x1 GEMM over kh*kw*c channels):
+ * out[n, y, x, (r*kw + s)*c + ci] = src[n][ci][y*sh - ph + r][x*sw - pw + s]
+ * (0 outside the image); out.h, out.w are the conv's output size. */
 typedef struct dfx_in_params {
-  const float* src;                    /* n samples, each C*H*W fp32 in CHW order */
+  const float* src;                    /* n samples, each c*h*w fp32 in CHW order */
   dfx_view out;
-  int32_t block, _pad;
+  int32_t kh, kw, sh, sw, ph, pw;      /* entry conv geometry (kh = 0: plain copy) */
+  int32_t c, h, w, _pad;               /* source sample dims */
 } dfx_in_params;
 
 typedef struct dfx_out_params {

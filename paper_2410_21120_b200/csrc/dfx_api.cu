@@ -3,6 +3,7 @@
 // Memory, streams, TMA descriptor encoding, kernel dispatch, and the CUDA
 // graph that executes a whole fused DAG.  Host-side only; kernels live in
 // dfx_gemm.cu and dfx_bw.cu.
+#include <algorithm>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
@@ -14,12 +15,14 @@
 
 namespace dfx {
 template <typename T, int M2> __global__ void gemm_kernel(const __grid_constant__ dfx_gemm_launch L);
+template <typename T> __global__ void gemm_persist_kernel(const __grid_constant__ dfx_gemm_launch L);
 template <typename T> __global__ void splitk_kernel(const __grid_constant__ dfx_splitk_params P);
 template <typename T> __global__ void ew_kernel(const __grid_constant__ dfx_ew_params P);
 template <typename T> __global__ void dwconv_kernel(const __grid_constant__ dfx_dwconv_params P);
 template <typename T> __global__ void pool_kernel(const __grid_constant__ dfx_pool_params P);
 template <typename T> __global__ void gap_kernel(const __grid_constant__ dfx_gap_params P);
 template <typename T> __global__ void in_kernel(const __grid_constant__ dfx_in_params P);
+template <typename T> __global__ void in_im2col_kernel(const __grid_constant__ dfx_in_params P);
 template <typename T> __global__ void out_kernel(const __grid_constant__ dfx_out_params P);
 template <typename T, int CL> __global__ void se_kernel(const __grid_constant__ dfx_se_params P);
 template <typename T> __global__ void ln_kernel(const __grid_constant__ dfx_ln_params P);
@@ -53,6 +56,7 @@ const void* se_func(int dt, int cl) {
 thread_local std::string g_err;
 int g_sm_count = 148;
 constexpr int kGemmSmemLimit = 227 * 1024;     // opt-in dynamic smem per CTA on sm_100
+constexpr int kIm2colSmemLimit = kGemmSmemLimit - int(sizeof(int)) * dfx::kIm2colMaxK;  // - static table
 
 int fail(int code, const char* fmt, ...) {
   char buf[512];
@@ -134,6 +138,15 @@ int config_for(int op, const void* params, size_t size, LaunchCfg* c) {
       c->func = gemm_func(p->dtype, p->m2);
       c->grid = dim3(p->total_tiles);
       c->block = dim3(128);
+      if (p->flags & 2) {               // persistent: <= 2 CTAs per SM walk the tile list
+        if (p->m2 || p->ndesc != 1 || p->desc0.splits != 1 || p->bn_max > 256)
+          return fail(DFX_E_ARG, "gemm: persistent launch needs one problem, no m2 / split-K");
+        c->func = DFX_PICK(gemm_persist_kernel, p->dtype);
+        const size_t smem = dfx::gemm_smem_bytes(p->bn_max, p->nslots, 0) + 1024;
+        const int per_sm = (p->bn_max <= 128 && 2 * smem <= size_t(228 * 1024)) ? 2 : 1;
+        c->grid = dim3(unsigned(std::min<int64_t>(p->total_tiles, int64_t(per_sm) * g_sm_count)));
+        c->block = dim3(192);
+      }
       if (p->nslots < 2 || p->nslots > dfx::kMaxSlots)
         return fail(DFX_E_ARG, "gemm: nslots %d", p->nslots);
       if (p->m2 && p->bn_max > 256) return fail(DFX_E_ARG, "gemm: m2 with bn %d", p->bn_max);
@@ -182,6 +195,17 @@ int config_for(int op, const void* params, size_t size, LaunchCfg* c) {
       NEED(dfx_in_params);
       const auto* p = static_cast<const dfx_in_params*>(params);
       if (p->out.pitch % 8 || p->out.coff) return fail(DFX_E_ARG, "in: pitch/coff");
+      if (p->kh > 0) {
+        if (p->out.c > dfx::kIm2colMaxK || p->out.c != p->kh * p->kw * p->c)
+          return fail(DFX_E_UNSUPPORTED, "in: im2col of %d channels", p->out.c);
+        c->func = DFX_PICK(in_im2col_kernel, p->out.dtype);
+        c->grid = dim3(unsigned(cdiv(p->out.w, dfx::kIm2colTile)), unsigned(p->out.h), unsigned(p->out.n));
+        c->block = dim3(256);
+        c->smem = size_t(dfx::im2col_smem_bytes(p->c, p->kh, p->kw, p->sw, p->out.w));
+        if (c->smem > size_t(kIm2colSmemLimit))
+          return fail(DFX_E_UNSUPPORTED, "in: im2col window of %zu B", c->smem);
+        return DFX_OK;
+      }
       c->func = DFX_PICK(in_kernel, p->out.dtype);
       c->grid = dim3(elementwise_grid(int64_t(p->out.n) * p->out.h * p->out.w * (p->out.pitch / 8), 256));
       return DFX_OK;
@@ -311,6 +335,10 @@ int dfx_init(int device) {
     for (int m2 : {0, 1})
       CK(cudaFuncSetAttribute(gemm_func(dt, m2), cudaFuncAttributeMaxDynamicSharedMemorySize,
                               kGemmSmemLimit));
+    CK(cudaFuncSetAttribute(DFX_PICK(gemm_persist_kernel, dt), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            kGemmSmemLimit));
+    CK(cudaFuncSetAttribute(DFX_PICK(in_im2col_kernel, dt), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            kIm2colSmemLimit));
     for (int cl : {8, 16})
       CK(cudaFuncSetAttribute(se_func(dt, cl), cudaFuncAttributeMaxDynamicSharedMemorySize,
                               dfx::kSeSmemBudget));

@@ -233,9 +233,9 @@ __global__ void in_kernel(const __grid_constant__ dfx_in_params P) {
   const int hw = o.h * o.w;
   const int cgp = o.pitch / 8;                 // channel groups incl. padding
   const int64_t total = int64_t(o.n) * hw * cgp;
-  if (P.block > 1) {                           // space-to-depth (patchify conv input)
-    const int b = P.block, C = o.c / (b * b), W = o.w * b;
-    const int64_t HW = int64_t(hw) * b * b;
+  if (P.kh > 0) {                              // im2col of the entry conv
+    const int C = P.c, H = P.h, W = P.w;
+    const int64_t HW = int64_t(H) * W;
     for (int64_t idx = grid_stride_start(); idx < total; idx += grid_stride_step()) {
       const int64_t pix = idx / cgp;
       const int c0 = int(idx - pix * cgp) * 8;
@@ -249,8 +249,10 @@ __global__ void in_kernel(const __grid_constant__ dfx_in_params P) {
         v[i] = 0.0f;
         if (cc < o.c) {
           const int rs = cc / C, c = cc - rs * C;
-          const int r = rs / b, sx = rs - r * b;
-          v[i] = __ldg(P.src + (int64_t(n) * C + c) * HW + int64_t(y * b + r) * W + x * b + sx);
+          const int r = rs / P.kw, sx = rs - r * P.kw;
+          const int iy = y * P.sh - P.ph + r, ix = x * P.sw - P.pw + sx;
+          if (iy >= 0 && iy < H && ix >= 0 && ix < W)
+            v[i] = __ldg(P.src + (int64_t(n) * C + c) * HW + int64_t(iy) * W + ix);
         }
       }
       st8<T>(o.base, pix * o.pitch + c0, v);
@@ -267,6 +269,53 @@ __global__ void in_kernel(const __grid_constant__ dfx_in_params P) {
 #pragma unroll
     for (int i = 0; i < 8; ++i) v[i] = (c + i < o.c) ? __ldg(src + int64_t(c + i) * hw) : 0.0f;
     st8<T>(o.base, pix * o.pitch + c, v);
+  }
+}
+
+// im2col of the entry conv (dfx_in_params.kh > 0), one CTA per (row segment of up to
+// kIm2colTile output pixels, output row, image): the source window the segment
+// needs (C x kh x ((TW-1)*sw + kw) fp32, zero outside the image) is staged in
+// shared memory with coalesced loads, then the segment's NHWC bytes -- contiguous,
+// TW * pitch halves -- are written with coalesced 16-B stores.
+template <typename T>
+__global__ void __launch_bounds__(256) in_im2col_kernel(const __grid_constant__ dfx_in_params P) {
+  extern __shared__ float win[];
+  __shared__ int off[kIm2colMaxK];                  // channel cc -> (c*kh + r)*ww + s
+  griddep_wait();
+  griddep_launch();
+  const dfx_view& o = P.out;
+  const int C = P.c, H = P.h, W = P.w, kh = P.kh, kw = P.kw;
+  const int x0 = blockIdx.x * kIm2colTile, y = blockIdx.y, n = blockIdx.z;
+  const int tw = min(kIm2colTile, o.w - x0);
+  const int ww = (tw - 1) * P.sw + kw;              // window width
+  const int iy0 = y * P.sh - P.ph, ix0 = x0 * P.sw - P.pw;
+  const float* src = P.src + int64_t(n) * C * H * W;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  for (int rc = warp; rc < C * kh; rc += blockDim.x / 32) {   // one window row per warp
+    const int r = rc % kh, c = rc / kh;
+    const int iy = iy0 + r;
+    const bool row_ok = iy >= 0 && iy < H;
+    const float* srow = src + (int64_t(c) * H + (row_ok ? iy : 0)) * W;
+    for (int col = lane; col < ww; col += 32) {
+      const int ix = ix0 + col;
+      win[rc * ww + col] = (row_ok && ix >= 0 && ix < W) ? __ldg(srow + ix) : 0.f;
+    }
+  }
+  for (int cc = threadIdx.x; cc < o.c; cc += blockDim.x) {
+    const int rs = cc / C, c = cc - rs * C;
+    const int r = rs / kw, s = rs - r * kw;
+    off[cc] = (c * kh + r) * ww + s;
+  }
+  __syncthreads();
+  const int groups = o.pitch / 8;
+  T* out = reinterpret_cast<T*>(o.base) + ((int64_t(n) * o.h + y) * o.w + x0) * o.pitch;
+  for (int i = threadIdx.x; i < tw * groups; i += blockDim.x) {
+    const int px = i / groups, c0 = (i - px * groups) * 8;
+    const int base = px * P.sw;
+    float v[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) v[j] = (c0 + j < o.c) ? win[off[c0 + j] + base] : 0.f;
+    *reinterpret_cast<uint4*>(out + int64_t(px) * o.pitch + c0) = pack8<T>(v);
   }
 }
 
@@ -296,6 +345,7 @@ DFX_INSTANTIATE(dwconv_kernel, dfx_dwconv_params)
 DFX_INSTANTIATE(pool_kernel, dfx_pool_params)
 DFX_INSTANTIATE(gap_kernel, dfx_gap_params)
 DFX_INSTANTIATE(in_kernel, dfx_in_params)
+DFX_INSTANTIATE(in_im2col_kernel, dfx_in_params)
 DFX_INSTANTIATE(out_kernel, dfx_out_params)
 #undef DFX_INSTANTIATE
 

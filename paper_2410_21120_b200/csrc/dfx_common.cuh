@@ -380,6 +380,13 @@ __host__ __device__ inline int gemm_slot_bytes(int bn_max, int m2 = 0) {
 __host__ __device__ inline int gemm_smem_bytes(int bn_max, int nslots, int m2 = 0) {
   return kSlotsOffset + nslots * gemm_slot_bytes(bn_max, m2);
 }
+// ---- entry-conv im2col (dfx_bw.cu in_im2col_kernel): output pixels per CTA
+constexpr int kIm2colTile = 256;           // a whole output row (<= 256 px) per CTA
+constexpr int kIm2colMaxK = 2048;          // kh*kw*c of an im2col'ed entry conv
+__host__ __device__ inline int im2col_smem_bytes(int c, int kh, int kw, int sw, int ow) {
+  const int tw = ow < kIm2colTile ? ow : kIm2colTile;
+  return c * kh * ((tw - 1) * sw + kw) * 4;
+}
 // ---- squeeze-excitation cluster kernel geometry (dfx_fused.cu)
 constexpr int kSeThreads = 256;
 constexpr int kSeMaxC = 4096;      // pooled channels held per CTA

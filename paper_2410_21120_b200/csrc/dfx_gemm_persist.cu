@@ -1,0 +1,207 @@
+// dfx_gemm_persist.cu — persistent variant of the tcgen05 implicit-GEMM conv
+// (dfx_gemm.cu) for multi-wave layers (batch >= 8: tens to thousands of
+// 128 x bn output tiles).
+//
+// The one-tile-per-CTA kernel pays per tile: the prologue (descriptor staging,
+// barrier init, TMEM alloc), the pipeline fill, and an epilogue that the
+// tensor core sits idle through.  Here a grid of <= 2 CTAs per SM walks the
+// tile list (M fastest, so concurrently running CTAs share each weight tile in
+// L2) and overlaps everything:
+//   warp 0  lane 0: TMA producer -- one smem slot ring across ALL of the CTA's
+//                   tiles, so the next tile's first stages load while the
+//                   current tile's MMAs and the previous tile's epilogue run;
+//   warp 1  lane 0: MMA issuer -- two TMEM accumulators (2 x bn columns); tile
+//                   i+1 accumulates into the buffer the epilogue of tile i-1
+//                   has released (acc_empty) while tile i is drained;
+//   warps 2..5    : epilogue -- warp w drains TMEM lanes 32*(w%4)..+31 (the
+//                   lane quadrant a warp may access), fused epilogue, 16-B
+//                   stores, then releases the accumulator buffer.
+// Split-K never applies (multi-wave layers have enough tiles), so every tile
+// finishes in its own epilogue.  Same descriptor (dfx_gemm_desc) and numerics
+// as gemm_kernel: K order, fp32 accumulation, epilogue slots.
+#include "dfx_common.cuh"
+
+namespace dfx {
+
+constexpr int kPersistThreads = 192;
+
+struct PersistHeader {
+  uint64_t full[kMaxSlots];
+  uint64_t empty[kMaxSlots];
+  uint64_t acc_full[2];
+  uint64_t acc_empty[2];
+  uint32_t tmem_base;
+  uint32_t _pad[7];
+  dfx_gemm_desc desc;
+};
+static_assert(sizeof(PersistHeader) <= kHeaderBytes + kEpiBytes, "persistent gemm header overflow");
+
+template <typename T>
+__global__ void __launch_bounds__(kPersistThreads, 1)
+    gemm_persist_kernel(const __grid_constant__ dfx_gemm_launch L) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  PersistHeader* hdr = reinterpret_cast<PersistHeader*>(smem);
+  uint8_t* slots = smem + kSlotsOffset;
+  const int slot_bytes = gemm_slot_bytes(L.bn_max, 0);
+  const int nslots = L.nslots;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const dfx_gemm_desc* gd = &L.desc0;
+
+  if (threadIdx.x < sizeof(dfx_gemm_desc) / 16)
+    reinterpret_cast<uint4*>(&hdr->desc)[threadIdx.x] = reinterpret_cast<const uint4*>(gd)[threadIdx.x];
+  const uint32_t tmem_cols = tmem_cols_for(2 * L.bn_max);
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < nslots; ++i) {
+      mbar_init(&hdr->full[i], 1);
+      mbar_init(&hdr->empty[i], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&hdr->acc_full[b], 1);
+      mbar_init(&hdr->acc_empty[b], 128);
+    }
+    fence_barrier_init();
+    tma_prefetch_desc(gd->tmap_a);
+    tma_prefetch_desc(gd->tmap_b);
+  }
+  if (warp == 1) tmem_alloc(&hdr->tmem_base, tmem_cols);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = hdr->tmem_base;
+  const dfx_gemm_desc& D = hdr->desc;
+
+  const int mt_q = D.mt_q, mt_p = D.mt_p;
+  const int tn = D.tn, tp = D.tp, tq = D.tq;
+  const int mt_total = D.mt_n * mt_p * mt_q;
+  const int total = D.tiles;
+  const int bn = D.bn, cb = D.cb, kpack = D.kpack, ksteps = D.ksteps, stages = D.stages;
+  const int sub_a = 128 * cb * 2, sub_b = bn * cb * 2;
+  const int grid = gridDim.x;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ================= TMA producer: one slot ring across all tiles of this CTA
+      const int cblocks = D.cblocks, S = D.s;
+      const uint32_t box_a_bytes = uint32_t(cb) * 2u * tq * tp * tn;
+      const void* tma = gd->tmap_a;
+      const void* tmb = gd->tmap_b;
+      int it = 0;
+      bool waited = false;
+      for (int tile = blockIdx.x; tile < total; tile += grid) {
+        const int mi = tile % mt_total, ntile = tile / mt_total;
+        const int n0 = (mi / (mt_q * mt_p)) * tn, p0 = ((mi / mt_q) % mt_p) * tp, q0 = (mi % mt_q) * tq;
+        const int qbase = q0 * D.stride_w - D.pad_w, pbase = p0 * D.stride_h - D.pad_h;
+        const int co_base = ntile * bn;
+        for (int st = 0; st < stages; ++st, ++it) {
+          const int slot = it % nslots;
+          const uint32_t par = (it / nslots) & 1;
+          if (it >= nslots) mbar_wait(&hdr->empty[slot], par ^ 1);
+          uint8_t* a_dst = slots + slot * slot_bytes;
+          uint8_t* b_dst = a_dst + kStageABytes;
+          const int k0 = st * kpack;
+          const int nk = min(kpack, ksteps - k0);
+          mbar_arrive_expect_tx(&hdr->full[slot], nk * (box_a_bytes + uint32_t(sub_b)));
+          for (int j = 0; j < nk; ++j)                  // weights: static, before the dependency
+            tma_load_2d(b_dst + j * sub_b, tmb, &hdr->full[slot], (k0 + j) * cb, co_base);
+          if (!waited) {
+            griddep_wait();
+            waited = true;
+          }
+          for (int j = 0; j < nk; ++j) {
+            const int kstep = k0 + j;
+            const int rs = kstep / cblocks;
+            const int cblk = kstep - rs * cblocks;
+            const int r = rs / S, s = rs - (rs / S) * S;
+            tma_load_4d(a_dst + j * sub_a, tma, &hdr->full[slot], cblk * cb, qbase + s, pbase + r, n0);
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ================= MMA issuer: double-buffered TMEM accumulators
+      const uint32_t idesc = umma_idesc_f16(uint32_t(bn), Elt<T>::kDtype);
+      const uint32_t row_bytes = uint32_t(cb) * 2u;
+      const int kk_n = cb / 16;
+      int it = 0, lt = 0;
+      for (int tile = blockIdx.x; tile < total; tile += grid, ++lt) {
+        const int b = lt & 1;
+        if (lt >= 2) mbar_wait(&hdr->acc_empty[b], ((lt >> 1) - 1) & 1);
+        tc_fence_after();
+        const uint32_t acc = tmem_base + uint32_t(b * bn);
+        uint32_t accumulate = 0;
+        for (int st = 0; st < stages; ++st, ++it) {
+          const int slot = it % nslots;
+          mbar_wait(&hdr->full[slot], (it / nslots) & 1);
+          tc_fence_after();
+          const uint32_t a_base = smem_u32(slots + slot * slot_bytes);
+          const uint32_t b_base = a_base + kStageABytes;
+          const int nk = min(kpack, ksteps - st * kpack);
+          for (int j = 0; j < nk; ++j)
+            for (int kk = 0; kk < kk_n; ++kk) {
+              umma_f16(acc, umma_smem_desc(a_base + j * sub_a + kk * 32, row_bytes),
+                       umma_smem_desc(b_base + j * sub_b + kk * 32, row_bytes), idesc, accumulate);
+              accumulate = 1;
+            }
+          umma_commit(&hdr->empty[slot]);
+        }
+        umma_commit(&hdr->acc_full[b]);
+      }
+    }
+  } else {
+    // ================= epilogue warps 2..5: TMEM lane quadrant (warp % 4)
+    griddep_wait();                                   // residual operands / output of predecessors
+    const int quad = warp & 3;
+    const int row = quad * 32 + lane;                 // tile row == TMEM lane
+    const int qi = row % tq, pi_ = (row / tq) % tp, ni = row / (tq * tp);
+    const dfx_view o = D.out;
+    const dfx_epilogue e = D.epi;
+    const int P = D.p, Q = D.q, N = D.n, cout = D.cout;
+    const bool views_vec = vec8_ok(o, 0) && (e.binop == DFX_BIN_NONE || vec8_ok(e.other, 0));
+    const uint32_t lane_addr = tmem_base + (uint32_t(quad * 32) << 16);
+    int lt = 0;
+    for (int tile = blockIdx.x; tile < total; tile += grid, ++lt) {
+      const int b = lt & 1;
+      const int mi = tile % mt_total, ntile = tile / mt_total;
+      const int n0 = (mi / (mt_q * mt_p)) * tn, p0 = ((mi / mt_q) % mt_p) * tp, q0 = (mi % mt_q) * tq;
+      const int co_base = ntile * bn;
+      const int on = n0 + ni, op = p0 + pi_, oq = q0 + qi;
+      const bool valid = row < tn * tp * tq && on < N && op < P && oq < Q;
+      const int64_t pix = (int64_t(on) * P + op) * Q + oq;
+      const int ncols = min(bn, ((cout - co_base) + 15) & ~15);
+      if (tile + grid >= total) griddep_launch();     // this CTA's last tile
+      mbar_wait(&hdr->acc_full[b], (lt >> 1) & 1);
+      tc_fence_after();
+      for (int c0 = 0; c0 < ncols; c0 += 16) {
+        float v[16];
+        tmem_ld16(lane_addr + uint32_t(b * bn + c0), v);
+        if (!valid) continue;
+        const int co = co_base + c0;
+        if (views_vec && co + 16 <= cout) {
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            epilogue8<T>(e, v + 8 * h, pix, on, co + 8 * h);
+            st8<T>(o.base, view_pixel_index(o, pix, co + 8 * h), v + 8 * h);
+          }
+        } else {
+          float tail[16];
+#pragma unroll
+          for (int i = 0; i < 16; ++i) tail[i] = v[i];
+          epilogue_store_tail<T>(e, o, tail, pix, on, co, min(16, cout - co));
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(&hdr->acc_empty[b]);                // buffer b may be overwritten
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc(tmem_base, tmem_cols);
+}
+
+template __global__ void gemm_persist_kernel<__nv_bfloat16>(const __grid_constant__ dfx_gemm_launch);
+template __global__ void gemm_persist_kernel<__half>(const __grid_constant__ dfx_gemm_launch);
+
+}  // namespace dfx

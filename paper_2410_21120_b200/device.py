@@ -70,6 +70,9 @@ GEMM_SMEM_LIMIT = 227 * 1024 - 1024          # minus the kernel's 1 KB alignment
 GEMM_SMEM_FIXED = 1024 + 2048                # barriers/descriptor + epilogue vectors
 
 
+GEMM_PERSIST = os.environ.get("DFX_GEMM_PERSIST", "1") != "0"    # A/B switch
+
+
 def gemm_slots(bn: int, tiles: int, sm_count: int = 148, m2: int = 0) -> int:
     """Pipeline depth of a GEMM launch: as deep as shared memory allows (<= 8)
     when the grid fits in one wave -- every extra slot is another weight tile
@@ -372,8 +375,10 @@ class ExecInstance:
             if n == 0:
                 continue
             deps = [prev_tail] if (self.dag.mode == "sequential" and prev_tail is not None) else []
+            ic = prog.input_im2col or (0, 0, 0, 0, 0, 0)
+            ind = tuple(prog.input_dims) if len(prog.input_dims) == 3 else (prog.input_dims[0], 1, 1)
             pin = rt.InParams(self.dev_in + self.in_off[m], self._view(m, prog, "<input>", n),
-                              prog.input_block)
+                              *ic, *ind)
             last = g.add(rt.OP_IN, pin, deps)
             self.nodes.append((rt.OP_IN, pin, dict(member=m, kind="in", flops=0,
                                                    bytes=self.in_sizes[m] * 3 // 2)))
@@ -513,6 +518,8 @@ class ExecInstance:
                                self.dtype, gemm_slots(t["bn"], t["tiles"], self.dag.sm_count,
                                                       t.get("m2", 0)))
             gl.m2 = t.get("m2", 0)
+            if GEMM_PERSIST and not gl.m2 and t["splits"] == 1 and t["tiles"] > 2 * self.dag.sm_count:
+                gl.flags |= 2                # persistent kernel for multi-wave layers
             gl.desc0 = d                    # single problem: descriptor in kernel-param space
             yield rt.OP_GEMM, gl
             if t["splits"] > 1 and not fixup:

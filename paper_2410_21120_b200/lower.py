@@ -144,7 +144,7 @@ class MemberProgram:
     input_value: str = "<input>"
     gemm_flops_per_sample: int = 0
     precision: str = "fp16"
-    input_block: int = 1                # > 1: input stored space-to-depth (patchify conv)
+    input_im2col: tuple | None = None   # (kh, kw, sh, sw, ph, pw): input stored im2col'ed
 
     def weight_bytes(self) -> int:
         return sum(b.nbytes for b in self.blobs.values())
@@ -178,23 +178,28 @@ class _Lowerer:
         self.pending_vec: list = []             # (launch, node, fp32 weight roles)
         self.precision = "fp16"
         self.keep_f32 = False
-        self.input_block = self._patchify_block()
+        self.input_im2col = self._entry_im2col()
         self.debug_f32: dict[str, np.ndarray] = {}
 
     # -------------------------------------------------------------- helpers
-    def _patchify_block(self) -> int:
-        """k if the entry node is a patchify conv (kernel = stride = k > 1, no padding,
-        k | H, W): the input is then stored space-to-depth (dfx_in_params.block) and
-        the conv runs as a 1x1 GEMM over k*k*C channels (strides > 8 do not fit a
-        TMA element stride; C = 3 would also waste 13/16 of every channel block)."""
+    def _entry_im2col(self):
+        """(kh, kw, sh, sw, ph, pw) when the entry conv should read an im2col'ed input
+        written by the input kernel (dfx_in_params.kh > 0) and run as a 1x1 GEMM over
+        kh*kw*C channels: stems with C < 16 input channels (C = 3 would otherwise pad
+        every tap's channel block 3 -> 16, 5.3x the MMA work) and patchify convs
+        (stride 16 does not fit a TMA element stride)."""
         node = self.g.nodes[self.g.entry]
         d = self.g.input_spec.dims
         if node.kind != "conv2d" or len(d) != 3 or int(node.attrs.get("groups", 1)) != 1:
-            return 1
+            return None
         kh, kw, sh, sw, ph, pw = conv_geometry(node.attrs)
-        if kh == kw == sh == sw and kh > 1 and ph == pw == 0 and d[1] % kh == 0 and d[2] % kh == 0:
-            return kh
-        return 1
+        if kh * kw == 1 or (d[0] >= 16 and max(sh, sw) <= 8):
+            return None
+        ow = (d[2] + 2 * pw - kw) // sw + 1
+        window = d[0] * kh * ((min(ow, 256) - 1) * sw + kw) * 4     # dfx_bw.cu in_im2col_kernel smem
+        if kh * kw * d[0] > 2048 or window > 219 * 1024:
+            return None
+        return (kh, kw, sh, sw, ph, pw)
 
     def dims(self, nid):
         return self.shapes[nid].dims
@@ -371,11 +376,10 @@ class _Lowerer:
             cin = idims[0]
             wt4 = self.warr(node, "weight")
             src = self.src_of(nid)
-            if nid == self.g.entry and self.input_block > 1:
-                # patchify conv over the space-to-depth input: 1x1, K order (r, s, c)
-                b = self.input_block
-                wt4 = np.ascontiguousarray(wt4.transpose(0, 2, 3, 1)).reshape(cout, b * b * cin, 1, 1)
-                cin, kh, kw, sh, sw = b * b * cin, 1, 1, 1, 1
+            if nid == self.g.entry and self.input_im2col is not None:
+                # 1x1 conv over the im2col'ed input, K order (r, s, c)
+                wt4 = np.ascontiguousarray(wt4.transpose(0, 2, 3, 1)).reshape(cout, kh * kw * cin, 1, 1)
+                cin, kh, kw, sh, sw, ph, pw = kh * kw * cin, 1, 1, 1, 1, 0, 0
             elif max(sh, sw) > 8:
                 raise UnsupportedOnDevice(nid, f"conv stride {sh}x{sw} > 8 (TMA element stride)")
             geom = dict(cout=cout, cin=cin, kh=kh, kw=kw, sh=sh, sw=sw, ph=ph, pw=pw,
@@ -426,9 +430,10 @@ class _Lowerer:
         g = self.g
         ind = g.input_spec.dims
         h, w = (ind[1], ind[2]) if len(ind) == 3 else (1, 1)
-        c, b = ind[0], self.input_block
-        if b > 1:
-            h, w, c = h // b, w // b, c * b * b
+        c = ind[0]
+        if self.input_im2col is not None:
+            kh, kw, sh, sw, ph, pw = self.input_im2col
+            h, w, c = (h + 2 * ph - kh) // sh + 1, (w + 2 * pw - kw) // sw + 1, c * kh * kw
         ib = self.new_buffer(h, w, c, "<input>")
         self.buffers[ib].is_input = True
         self.values["<input>"] = Value(ib, 0, h, w, c)
@@ -669,7 +674,7 @@ def lower_member(g, w, keep_f32: bool = False, precision: str = "fp16") -> Membe
     prog = low.run()
     prog.debug_f32 = low.debug_f32
     prog.precision = precision
-    prog.input_block = low.input_block
+    prog.input_im2col = low.input_im2col
     from .graph_ir import gemm_flops
     prog.gemm_flops_per_sample = gemm_flops(g)
     return prog

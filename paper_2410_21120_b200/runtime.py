@@ -85,7 +85,8 @@ class EwParams(C.Structure):
 
 
 class InParams(C.Structure):
-    _fields_ = [("src", vp), ("out", View), ("block", i32), ("_pad", i32)]
+    _fields_ = [("src", vp), ("out", View), ("kh", i32), ("kw", i32), ("sh", i32), ("sw", i32),
+                ("ph", i32), ("pw", i32), ("c", i32), ("h", i32), ("w", i32), ("_pad", i32)]
 
 
 class OutParams(C.Structure):

@@ -75,11 +75,14 @@ class Emulator:
         p = self.p
         xs = np.asarray(xs, np.float32).reshape((self.n,) + tuple(p.input_dims))
         iv = self.view("<input>")
-        b = getattr(p, "input_block", 1)
-        if b > 1:                               # space-to-depth, channel order (r, s, c)
+        ic = getattr(p, "input_im2col", None)
+        if ic is not None:                      # im2col of the entry conv, channel order (r, s, c)
+            kh, kw, sh, sw, ph, pw = ic
             n, c, h, w = xs.shape
-            xs = xs.reshape(n, c, h // b, b, w // b, b).transpose(0, 2, 4, 3, 5, 1) \
-                .reshape(n, h // b, w // b, b * b * c).transpose(0, 3, 1, 2)
+            xp = np.pad(xs, ((0, 0), (0, 0), (ph, ph), (pw, pw)))
+            oh, ow = (h + 2 * ph - kh) // sh + 1, (w + 2 * pw - kw) // sw + 1
+            cols = [xp[:, :, r:r + oh * sh:sh, s:s + ow * sw:sw] for r in range(kh) for s in range(kw)]
+            xs = np.concatenate(cols, axis=1)   # (n, kh*kw*c, oh, ow), (r, s) major, c minor
         if xs.ndim == 4:
             self.store(iv, xs.transpose(0, 2, 3, 1))
         else:

@@ -81,6 +81,23 @@ def test_conv_layer_m2_tiles(cin, h, w, cout, k, s, p, n):
     test_conv_layer(cin, h, w, cout, k, s, p, n)
 
 
+# multi-wave layers that take the persistent kernel (dfx_gemm_persist.cu: <= 2 CTAs
+# per SM walk the tile list, double-buffered TMEM accumulators): bn 64 / 128 / 256,
+# ragged output width and channel tail
+PERSIST_CASES = [(16, 112, 112, 64, 3, 1, 1, 4), (32, 56, 56, 128, 3, 1, 1, 13),
+                 (24, 56, 56, 256, 1, 1, 0, 12), (40, 60, 57, 200, 3, 1, 1, 11)]
+
+
+@pytest.mark.parametrize("cin,h,w,cout,k,s,p,n", PERSIST_CASES)
+def test_conv_layer_persistent(cin, h, w, cout, k, s, p, n):
+    from paper_2410_21120_b200.lower import choose_cb, gemm_tiling
+    cb = choose_cb(cin)
+    t = gemm_tiling(dict(cout=cout, cb=cb, ksteps=k * k * (-(-cin // cb)), sh=s, sw=s), n,
+                    (h + 2 * p - k) // s + 1, (w + 2 * p - k) // s + 1)
+    assert not t["m2"] and t["splits"] == 1 and t["tiles"] > 2 * 148
+    test_conv_layer(cin, h, w, cout, k, s, p, n)
+
+
 @pytest.mark.parametrize("units,fan_in,n", [(10, 7, 1), (4096, 25088 // 49, 2), (1000, 1280, 3), (240, 960, 1)])
 def test_dense_layer(units, fan_in, n):
     rng = np.random.default_rng(units)
