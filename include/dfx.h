@@ -148,9 +148,10 @@ typedef struct __attribute__((aligned(64))) dfx_gemm_launch {
   int32_t dtype;                   /* dfx_dtype of every problem */
   int32_t nslots;                  /* smem pipeline depth, 2..8 */
   int32_t flags;                   /* bit 0: read desc0 from `descs` (debug);
-                                      bit 1: persistent kernel (<= 2 CTAs/SM walk the
-                                      tile list, double-buffered TMEM; one problem,
-                                      no split-K, no m2) */
+                                      bit 1: persistent kernel (1-2 CTAs/SM walk the
+                                      tile list, a ring of TMEM accumulators; one
+                                      problem, no split-K, no m2);
+                                      bit 2: smem-transposed epilogue drain (A/B only) */
   int32_t m2;                      /* any problem has m2 = 1 (sizes smem / TMEM) */
   int32_t _pad[7];
   dfx_gemm_desc desc0;             /* the problem when ndesc == 1 */

@@ -12,6 +12,7 @@
 #include <vector>
 
 #include "dfx_common.cuh"
+#include "dfx_epi.cuh"
 
 namespace dfx {
 template <typename T, int M2> __global__ void gemm_kernel(const __grid_constant__ dfx_gemm_launch L);
@@ -137,20 +138,28 @@ int config_for(int op, const void* params, size_t size, LaunchCfg* c) {
         return fail(DFX_E_ARG, "gemm: bad bn_max %d / tiles %d", p->bn_max, p->total_tiles);
       c->func = gemm_func(p->dtype, p->m2);
       c->grid = dim3(p->total_tiles);
-      c->block = dim3(128);
-      if (p->flags & 2) {               // persistent: <= 2 CTAs per SM walk the tile list
-        if (p->m2 || p->ndesc != 1 || p->desc0.splits != 1 || p->bn_max > 256)
-          return fail(DFX_E_ARG, "gemm: persistent launch needs one problem, no m2 / split-K");
-        c->func = DFX_PICK(gemm_persist_kernel, p->dtype);
-        const size_t smem = dfx::gemm_smem_bytes(p->bn_max, p->nslots, 0) + 1024;
-        const int per_sm = (p->bn_max <= 128 && 2 * smem <= size_t(228 * 1024)) ? 2 : 1;
-        c->grid = dim3(unsigned(std::min<int64_t>(p->total_tiles, int64_t(per_sm) * g_sm_count)));
-        c->block = dim3(192);
-      }
+      c->block = dim3(dfx::kGemmThreads);
       if (p->nslots < 2 || p->nslots > dfx::kMaxSlots)
         return fail(DFX_E_ARG, "gemm: nslots %d", p->nslots);
       if (p->m2 && p->bn_max > 256) return fail(DFX_E_ARG, "gemm: m2 with bn %d", p->bn_max);
-      c->smem = dfx::gemm_smem_bytes(p->bn_max, p->nslots, p->m2 ? 1 : 0) + 1024;
+      if (p->flags & 2) {               // persistent: one CTA per SM walks the tile list
+        if (p->m2 || p->ndesc != 1 || p->desc0.splits != 1 || p->bn_max > 256)
+          return fail(DFX_E_ARG, "gemm: persistent launch needs one problem, no m2 / split-K");
+        c->func = DFX_PICK(gemm_persist_kernel, p->dtype);
+        // narrow tiles (bn <= 64): two CTAs per SM with one epilogue group each (two
+        // producers / MMA issuers per SM); else one CTA per SM with two groups
+        const int per_sm = p->bn_max <= 64 ? 2 : 1;
+        const int groups = 3 - per_sm;
+        c->smem = dfx::gemm_smem_bytes(p->bn_max, p->nslots, 0) + 1024 +
+                  ((p->flags & 4) ? 4 * groups * dfx::kEpiStageWarpBytes : 0);
+        c->grid = dim3(unsigned(std::min<int64_t>(p->total_tiles, int64_t(per_sm) * g_sm_count)));
+        c->block = dim3(64 + 128 * groups);
+      } else {
+        c->smem = dfx::gemm_smem_bytes(p->bn_max, p->nslots, p->m2 ? 1 : 0) + 1024;
+        // 8 warps (4 more drain the epilogue) when shared memory already limits the
+        // SM to one CTA; else 4, so small-tile grids keep several CTAs per SM
+        c->block = dim3(c->smem > size_t(114 * 1024) ? dfx::kGemmThreads : 128);
+      }
       if (c->smem > size_t(kGemmSmemLimit))
         return fail(DFX_E_ARG, "gemm: %zu B of shared memory (bn %d x %d slots)", c->smem,
                     p->bn_max, p->nslots);

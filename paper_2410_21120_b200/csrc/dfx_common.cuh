@@ -19,13 +19,27 @@
 namespace dfx {
 
 // ---------------------------------------------------------------- math
+// Activations in fast-math form: no IEEE division (x / 6 and 1 / (1 + e) would
+// each compile to a ~20-instruction division subroutine, which made SiLU and
+// hardswish epilogues -- not the MMAs -- the bottleneck of multi-wave GEMMs).
+// rcp.approx (one MUFU op, 1 ulp) and __expf (ex2.approx, 2 ulp) are far below
+// the 16-bit storage rounding that follows.  (__frcp_rn's correctly-rounded
+// fix-up path compiled to per-element branches.)
+DFX_DEV float rcp_approx(float x) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+DFX_DEV float sigmoid_f(float v) { return rcp_approx(1.0f + __expf(-v)); }
+DFX_DEV float hsig_f(float v) { return fminf(fmaxf(v + 3.0f, 0.0f), 6.0f) * (1.0f / 6.0f); }
+
 DFX_DEV float act_apply(int act, float v) {
   switch (act) {
     case DFX_ACT_RELU: return fmaxf(v, 0.0f);
-    case DFX_ACT_HARDSWISH: return v * fminf(fmaxf(v + 3.0f, 0.0f), 6.0f) / 6.0f;
-    case DFX_ACT_HARDSIGMOID: return fminf(fmaxf(v + 3.0f, 0.0f), 6.0f) / 6.0f;
-    case DFX_ACT_SILU: return v / (1.0f + __expf(-v));
-    case DFX_ACT_SIGMOID: return 1.0f / (1.0f + __expf(-v));
+    case DFX_ACT_HARDSWISH: return v * hsig_f(v);
+    case DFX_ACT_HARDSIGMOID: return hsig_f(v);
+    case DFX_ACT_SILU: return v * sigmoid_f(v);
+    case DFX_ACT_SIGMOID: return sigmoid_f(v);
     case DFX_ACT_GELU: return 0.5f * v * (1.0f + erff(v * 0.70710678118654752f));
     default: return v;
   }
@@ -40,19 +54,19 @@ DFX_DEV void act8(int act, float* v) {
       break;
     case DFX_ACT_HARDSWISH:
 #pragma unroll
-      for (int i = 0; i < 8; ++i) v[i] = v[i] * fminf(fmaxf(v[i] + 3.0f, 0.0f), 6.0f) / 6.0f;
+      for (int i = 0; i < 8; ++i) v[i] = v[i] * hsig_f(v[i]);
       break;
     case DFX_ACT_HARDSIGMOID:
 #pragma unroll
-      for (int i = 0; i < 8; ++i) v[i] = fminf(fmaxf(v[i] + 3.0f, 0.0f), 6.0f) / 6.0f;
+      for (int i = 0; i < 8; ++i) v[i] = hsig_f(v[i]);
       break;
     case DFX_ACT_SILU:
 #pragma unroll
-      for (int i = 0; i < 8; ++i) v[i] = v[i] / (1.0f + __expf(-v[i]));
+      for (int i = 0; i < 8; ++i) v[i] = v[i] * sigmoid_f(v[i]);
       break;
     case DFX_ACT_SIGMOID:
 #pragma unroll
-      for (int i = 0; i < 8; ++i) v[i] = 1.0f / (1.0f + __expf(-v[i]));
+      for (int i = 0; i < 8; ++i) v[i] = sigmoid_f(v[i]);
       break;
     case DFX_ACT_GELU:
 #pragma unroll
@@ -340,6 +354,27 @@ DFX_DEV void tmem_ld16(uint32_t taddr, float* v) {
   for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+// Split form: issue the load, overlap other work, then wait.  The wait names the
+// destination registers as read-write operands so the compiler cannot move any
+// use of them above it.
+DFX_DEV void tmem_ld16_issue(uint32_t taddr, uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+      "{%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),
+        "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+}
+DFX_DEV void tmem_ld_wait(uint32_t (&r)[16]) {
+  asm volatile("tcgen05.wait::ld.sync.aligned;"
+               : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]),
+                 "+r"(r[7]), "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]),
+                 "+r"(r[13]), "+r"(r[14]), "+r"(r[15])
+               :
+               : "memory");
+}
+
 // UMMA shared-memory descriptor, K-major operand with 32/64/128-byte swizzle.
 // rows of `row_bytes` (= swizzle width), 8-row core groups stacked densely.
 DFX_DEV uint64_t umma_smem_desc(uint32_t saddr, uint32_t row_bytes) {
@@ -366,7 +401,7 @@ DFX_DEV uint32_t umma_idesc_f16(uint32_t n, int dtype) {
   return d;
 }
 
-constexpr int kGemmThreads = 128;
+constexpr int kGemmThreads = 256;          // warps 0-3 roles + 4 more for the epilogue drain
 constexpr int kMaxSlots = 8;                 // pipeline depth is a launch parameter, 2..8
 constexpr int kStageABytes = 128 * 64 * 2;   // 128 rows x 64 16-bit
 constexpr int kHeaderBytes = 1024;           // barriers + staged descriptor

@@ -1,0 +1,130 @@
+// dfx_epi.cuh — GEMM epilogue drain shared by gemm_kernel and gemm_persist_kernel.
+//
+// drain_rows (launch flag 4, A/B only) -- one warp owns 32 TMEM lanes = 32 tile rows = 32 output pixels.  Reading the
+// accumulator gives each thread ONE pixel's consecutive channels, so storing
+// straight from registers makes every warp store touch 32 pixels 16 B each
+// (half-used 32-B sectors, ncu: "16.1 of 32 bytes per sector") and every
+// residual load likewise.  Here each 16-column chunk goes through a per-warp
+// fp32 smem transpose (32 rows x 20 floats, conflict-free for both the row
+// writes and the column-group reads) so that lane l then handles pixel
+// (l % 16) + 16 i, channels 8 (l / 16) .. +7: a warp store covers 16 pixels x
+// 32 contiguous bytes (full sectors), and the residual/scale operand loads
+// coalesce the same way.  The TMEM load of chunk c+1 is in flight while chunk
+// c is staged and stored.
+#pragma once
+
+#include "dfx_common.cuh"
+
+namespace dfx {
+
+constexpr int kEpiStagePitch = 20;                        // floats per staged row
+constexpr int kEpiStageWarpBytes = 32 * kEpiStagePitch * 4;   // 2560 B per warp
+
+// Drain accumulator columns c_first, c_first + c_step, ... (16-column chunks,
+// c < ncols, ncols a multiple of 16) from TMEM address `taddr` (lane base of
+// this warp already folded in).  Two warps sharing a TMEM lane quadrant split
+// the chunks (c_step 32) -- the drain is issue-bound, so more warps = faster.  The calling thread's own
+// tile row maps to pixel `pix` of image `img`, `valid` if inside the output.
+// Output channel of column j is co_base + j.  If `ws` is set the raw fp32 sums
+// go to the split-K workspace plane ws[pix * ldw + co] instead.
+template <typename T>
+DFX_DEV void drain_rows(uint32_t taddr, float* stg, int ncols, int64_t pix, int img, bool valid,
+                        int co_base, int cout, const dfx_epilogue& e, const dfx_view& o,
+                        bool views_vec, float* ws, int ldw, int c_first, int c_step) {
+  if (c_first >= ncols) return;
+  const int lane = threadIdx.x & 31;
+  const unsigned full = 0xffffffffu;
+  uint32_t cur[16], nxt[16];
+  tmem_ld16_issue(taddr + uint32_t(c_first), cur);
+  tmem_ld_wait(cur);
+  // the two pixels this lane stores (rows lane%16 and lane%16 + 16)
+  const int rr0 = lane & 15, cg = lane >> 4;
+  int64_t spix[2];
+  int simg[2];
+  bool sval[2];
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const int src = rr0 + 16 * i;
+    spix[i] = (int64_t(__shfl_sync(full, int(pix >> 32), src)) << 32) |
+              uint32_t(__shfl_sync(full, int(pix & 0xffffffff), src));
+    simg[i] = __shfl_sync(full, img, src);
+    sval[i] = __shfl_sync(full, int(valid), src) != 0;
+  }
+  float4* my_row = reinterpret_cast<float4*>(stg + lane * kEpiStagePitch);
+  for (int c0 = c_first; c0 < ncols; c0 += c_step) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      my_row[k] = make_float4(__uint_as_float(cur[4 * k]), __uint_as_float(cur[4 * k + 1]),
+                              __uint_as_float(cur[4 * k + 2]), __uint_as_float(cur[4 * k + 3]));
+    const bool more = c0 + c_step < ncols;
+    if (more) tmem_ld16_issue(taddr + uint32_t(c0 + c_step), nxt);
+    __syncwarp();
+    const int co = co_base + c0 + 8 * cg;
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      const float4* src = reinterpret_cast<const float4*>(stg + (rr0 + 16 * i) * kEpiStagePitch + 8 * cg);
+      const float4 a = src[0], b = src[1];
+      float v[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+      if (!sval[i] || co >= cout) continue;
+      if (ws != nullptr) {
+        float4* dst = reinterpret_cast<float4*>(ws + spix[i] * ldw + co);
+        dst[0] = a;
+        dst[1] = b;
+      } else if (views_vec && co + 8 <= cout) {
+        epilogue8<T>(e, v, spix[i], simg[i], co);
+        st8<T>(o.base, view_pixel_index(o, spix[i], co), v);
+      } else {
+        float tail[8];          // a separate array: taking v's address would spill it on every path
+#pragma unroll
+        for (int k = 0; k < 8; ++k) tail[k] = v[k];
+        epilogue_store_tail<T>(e, o, tail, spix[i], simg[i], co, min(8, cout - co));
+      }
+    }
+    __syncwarp();
+    if (more) {
+      tmem_ld_wait(nxt);
+#pragma unroll
+      for (int k = 0; k < 16; ++k) cur[k] = nxt[k];
+    }
+  }
+}
+
+// The unstaged drain (the default): each thread stores its own row's channels
+// straight from registers (16 B per thread per store, one pixel per lane).
+// Measured faster than drain_rows on every batch-32 layer shape tried
+// (scripts/gpu_ab_drain.sh: e.g. 3x3 64->256 55 vs 67 us, 1x1 224->1344 20 vs
+// 27 us): the drain is issue-bound, and the transpose's extra shared-memory
+// instructions cost more than the half-used store sectors.
+template <typename T>
+DFX_DEV void drain_rows_direct(uint32_t taddr, int ncols, int64_t pix, int img, bool valid,
+                               int co_base, int cout, const dfx_epilogue& e, const dfx_view& o,
+                               bool views_vec, float* ws, int ldw, int c_first, int c_step) {
+  for (int c0 = c_first; c0 < ncols; c0 += c_step) {
+    uint32_t r[16];
+    tmem_ld16_issue(taddr + uint32_t(c0), r);
+    tmem_ld_wait(r);
+    if (!valid) continue;
+    float v[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+    const int co = co_base + c0;
+    if (ws != nullptr) {
+      float4* dst = reinterpret_cast<float4*>(ws + pix * ldw + co);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) dst[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+    } else if (views_vec && co + 16 <= cout) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        epilogue8<T>(e, v + 8 * h, pix, img, co + 8 * h);
+        st8<T>(o.base, view_pixel_index(o, pix, co + 8 * h), v + 8 * h);
+      }
+    } else {
+      float tail[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) tail[i] = v[i];
+      epilogue_store_tail<T>(e, o, tail, pix, img, co, min(16, cout - co));
+    }
+  }
+}
+
+}  // namespace dfx

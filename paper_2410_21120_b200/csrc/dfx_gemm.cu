@@ -50,6 +50,7 @@ __device__ unsigned long long dfx_timeline[64];
 #endif
 
 #include "dfx_common.cuh"
+#include "dfx_epi.cuh"
 
 // Debug builds (-DDFX_TIMELINE): copy the kernel timeline probes (ns).  Not in
 // dfx.h: a development hook, not part of the ABI.
@@ -294,7 +295,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     const int ti = threadIdx.x - 64;
     const float* ga = D.epi.alpha;
     const float* gb = D.epi.beta;
-    for (int i = ti; i < bn; i += 64) {
+    for (int i = ti; i < bn; i += int(blockDim.x) - 64) {
       const int c = co_base + i;
       if (ga) s_alpha[i] = c < cout ? ga[c] : 0.f;
       if (gb) s_beta[i] = c < cout ? gb[c] : 0.f;
@@ -323,47 +324,32 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   tc_fence_after();
   griddep_launch();                            // successor may start its prologue now
 
-  const int row = threadIdx.x;                 // tile row == TMEM lane
+  const int row = threadIdx.x & 127;           // tile row == TMEM lane (warps w, w+4 share it)
   const int qi = row % tq;
   const int pi_ = (row / tq) % tp;
   const int ni = row / (tq * tp);
-  const uint32_t lane_addr = tmem_base + (uint32_t(warp * 32) << 16);
+  const uint32_t lane_addr = tmem_base + (uint32_t((warp & 3) * 32) << 16);
   const int ncols = min(bn, ((cout - co_base) + 15) & ~15);
   const bool views_vec = vec8_ok(o, 0) && (e.binop == DFX_BIN_NONE || vec8_ok(e.other, 0));
 
   const int64_t plane = int64_t(N) * P * Q * ldw;      // one split's partials
   if (threadIdx.x == 0) DFX_TL(11);                    // epilogue starts
+  // per-warp transpose staging for the coalesced drain: the operand slots are
+  // free once the accumulator barrier fired (every TMA load was consumed)
+  float* stg = reinterpret_cast<float*>(slots + warp * kEpiStageWarpBytes);
 #pragma unroll
   for (int h = 0; h < 1 + M2; ++h) {                   // M tiles of this CTA (m2: two)
-  if (h >= nhalf) break;
-  const int on = n0h[h] + ni, op = p0h[h] + pi_, oq = q0h[h] + qi;
-  const bool valid = row < tn * tp * tq && on < N && op < P && oq < Q;
-  const int64_t pix = (int64_t(on) * P + op) * Q + oq;
-  for (int c0 = 0; c0 < ncols; c0 += 16) {
-    float v[16];
-    tmem_ld16(lane_addr + uint32_t(h * bn + c0), v);
-    if (c0 == 0 && threadIdx.x == 0) DFX_TL(12);       // first TMEM load back
-    if (!valid) continue;
-    const int co = co_base + c0;
-    if (splits > 1) {
-      float4* dst = reinterpret_cast<float4*>(ws + split * plane + pix * ldw + co);
-#pragma unroll
-      for (int i = 0; i < 4; ++i) dst[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
-      continue;
-    }
-    if (views_vec && co + 16 <= cout) {
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        epilogue8<T>(e, v + 8 * h, pix, on, co + 8 * h);
-        st8<T>(o.base, view_pixel_index(o, pix, co + 8 * h), v + 8 * h);
-      }
-    } else {
-      float tail[16];
-#pragma unroll
-      for (int i = 0; i < 16; ++i) tail[i] = v[i];
-      epilogue_store_tail<T>(e, o, tail, pix, on, co, min(16, cout - co));
-    }
-  }
+    if (h >= nhalf) break;
+    const int on = n0h[h] + ni, op = p0h[h] + pi_, oq = q0h[h] + qi;
+    const bool valid = row < tn * tp * tq && on < N && op < P && oq < Q;
+    const int64_t pix = (int64_t(on) * P + op) * Q + oq;
+    float* wsp = splits > 1 ? ws + split * plane : nullptr;
+    if (!(L.flags & 4))
+      drain_rows_direct<T>(lane_addr + uint32_t(h * bn), ncols, pix, on, valid, co_base, cout, e, o,
+                           views_vec, wsp, ldw, 16 * (warp >> 2), 16 * int(blockDim.x >> 7));
+    else
+      drain_rows<T>(lane_addr + uint32_t(h * bn), stg, ncols, pix, on, valid, co_base, cout, e, o,
+                    views_vec, wsp, ldw, 16 * (warp >> 2), 16 * int(blockDim.x >> 7));
   }
 
   if (splits > 1 && D.counters != nullptr) {
@@ -379,7 +365,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     if (hdr->last_split) {
       __threadfence();
       const int c8n = ncols / 8;
-      for (int item = threadIdx.x; item < 128 * c8n; item += kGemmThreads) {
+      for (int item = threadIdx.x; item < 128 * c8n; item += int(blockDim.x)) {
         const int r = item / c8n;
         const int co = co_base + (item - r * c8n) * 8;
         const int rq = r % tq, rp = (r / tq) % tp, rn = r / (tq * tp);

@@ -10,26 +10,31 @@
 //   warp 0  lane 0: TMA producer -- one smem slot ring across ALL of the CTA's
 //                   tiles, so the next tile's first stages load while the
 //                   current tile's MMAs and the previous tile's epilogue run;
-//   warp 1  lane 0: MMA issuer -- two TMEM accumulators (2 x bn columns); tile
-//                   i+1 accumulates into the buffer the epilogue of tile i-1
-//                   has released (acc_empty) while tile i is drained;
-//   warps 2..5    : epilogue -- warp w drains TMEM lanes 32*(w%4)..+31 (the
-//                   lane quadrant a warp may access), fused epilogue, 16-B
-//                   stores, then releases the accumulator buffer.
+//   warp 1  lane 0: MMA issuer -- a ring of nacc = min(8, 512 / bn) TMEM
+//                   accumulators; tile i accumulates into buffer i % nacc once
+//                   the epilogue of tile i - nacc released it (acc_empty);
+//   warps 2..     : epilogue -- one or two groups of 4 warps (two when the SM
+//                   holds one CTA, bn > 64); warp w drains TMEM lanes
+//                   32*(w%4)..+31 (the lane quadrant a warp may access) with
+//                   coalesced stores (dfx_epi.cuh), then releases the buffer.
+//                   The drain is issue-bound: more warps and a deep ring keep
+//                   it off the MMA's critical path.
 // Split-K never applies (multi-wave layers have enough tiles), so every tile
 // finishes in its own epilogue.  Same descriptor (dfx_gemm_desc) and numerics
 // as gemm_kernel: K order, fp32 accumulation, epilogue slots.
 #include "dfx_common.cuh"
+#include "dfx_epi.cuh"
 
 namespace dfx {
 
-constexpr int kPersistThreads = 192;
+constexpr int kPersistThreads = 320;      // producer, MMA, 8 epilogue warps
+constexpr int kMaxAcc = 8;                // TMEM accumulator buffers (as many as 512 columns hold)
 
 struct PersistHeader {
   uint64_t full[kMaxSlots];
   uint64_t empty[kMaxSlots];
-  uint64_t acc_full[2];
-  uint64_t acc_empty[2];
+  uint64_t acc_full[kMaxAcc];
+  uint64_t acc_empty[kMaxAcc];
   uint32_t tmem_base;
   uint32_t _pad[7];
   dfx_gemm_desc desc;
@@ -51,15 +56,23 @@ __global__ void __launch_bounds__(kPersistThreads, 1)
 
   if (threadIdx.x < sizeof(dfx_gemm_desc) / 16)
     reinterpret_cast<uint4*>(&hdr->desc)[threadIdx.x] = reinterpret_cast<const uint4*>(gd)[threadIdx.x];
-  const uint32_t tmem_cols = tmem_cols_for(2 * L.bn_max);
+  // epilogue groups of 4 warps (blockDim = 64 + 128 * groups): with a deep
+  // accumulator ring the groups take alternate tiles, else they split each
+  // tile's columns (with 2 buffers a tile's drain must finish within one tile).
+  // One group = two CTAs per SM: each may hold only half of TMEM (a second
+  // CTA's tcgen05.alloc would otherwise block until the first one exits).
+  const int groups = (int(blockDim.x) - 64) >> 7;
+  const int nacc = max(2, min(kMaxAcc, (groups > 1 ? 512 : 256) / L.bn_max));
+  const bool alt = groups > 1 && nacc >= 4;
+  const uint32_t tmem_cols = tmem_cols_for(nacc * L.bn_max);
   if (threadIdx.x == 0) {
     for (int i = 0; i < nslots; ++i) {
       mbar_init(&hdr->full[i], 1);
       mbar_init(&hdr->empty[i], 1);
     }
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < nacc; ++b) {
       mbar_init(&hdr->acc_full[b], 1);
-      mbar_init(&hdr->acc_empty[b], 128);
+      mbar_init(&hdr->acc_empty[b], alt ? 128 : blockDim.x - 64);
     }
     fence_barrier_init();
     tma_prefetch_desc(gd->tmap_a);
@@ -121,14 +134,14 @@ __global__ void __launch_bounds__(kPersistThreads, 1)
     }
   } else if (warp == 1) {
     if (lane == 0) {
-      // ================= MMA issuer: double-buffered TMEM accumulators
+      // ================= MMA issuer: nacc TMEM accumulators in a ring
       const uint32_t idesc = umma_idesc_f16(uint32_t(bn), Elt<T>::kDtype);
       const uint32_t row_bytes = uint32_t(cb) * 2u;
       const int kk_n = cb / 16;
       int it = 0, lt = 0;
       for (int tile = blockIdx.x; tile < total; tile += grid, ++lt) {
-        const int b = lt & 1;
-        if (lt >= 2) mbar_wait(&hdr->acc_empty[b], ((lt >> 1) - 1) & 1);
+        const int b = lt % nacc;
+        if (lt >= nacc) mbar_wait(&hdr->acc_empty[b], ((lt / nacc) - 1) & 1);
         tc_fence_after();
         const uint32_t acc = tmem_base + uint32_t(b * bn);
         uint32_t accumulate = 0;
@@ -151,7 +164,7 @@ __global__ void __launch_bounds__(kPersistThreads, 1)
       }
     }
   } else {
-    // ================= epilogue warps 2..5: TMEM lane quadrant (warp % 4)
+    // ================= epilogue warps 2..9: TMEM lane quadrant (warp % 4)
     griddep_wait();                                   // residual operands / output of predecessors
     const int quad = warp & 3;
     const int row = quad * 32 + lane;                 // tile row == TMEM lane
@@ -161,9 +174,13 @@ __global__ void __launch_bounds__(kPersistThreads, 1)
     const int P = D.p, Q = D.q, N = D.n, cout = D.cout;
     const bool views_vec = vec8_ok(o, 0) && (e.binop == DFX_BIN_NONE || vec8_ok(e.other, 0));
     const uint32_t lane_addr = tmem_base + (uint32_t(quad * 32) << 16);
+    float* stg = reinterpret_cast<float*>(slots + nslots * slot_bytes + (warp - 2) * kEpiStageWarpBytes);
+    const int group = (warp - 2) >> 2;
+    const int c_first = alt ? 0 : 16 * group, c_step = alt ? 16 : 16 * groups;
     int lt = 0;
     for (int tile = blockIdx.x; tile < total; tile += grid, ++lt) {
-      const int b = lt & 1;
+      if (alt && (lt % groups) != group) continue;
+      const int b = lt % nacc;
       const int mi = tile % mt_total, ntile = tile / mt_total;
       const int n0 = (mi / (mt_q * mt_p)) * tn, p0 = ((mi / mt_q) % mt_p) * tp, q0 = (mi % mt_q) * tq;
       const int co_base = ntile * bn;
@@ -172,26 +189,14 @@ __global__ void __launch_bounds__(kPersistThreads, 1)
       const int64_t pix = (int64_t(on) * P + op) * Q + oq;
       const int ncols = min(bn, ((cout - co_base) + 15) & ~15);
       if (tile + grid >= total) griddep_launch();     // this CTA's last tile
-      mbar_wait(&hdr->acc_full[b], (lt >> 1) & 1);
+      mbar_wait(&hdr->acc_full[b], (lt / nacc) & 1);
       tc_fence_after();
-      for (int c0 = 0; c0 < ncols; c0 += 16) {
-        float v[16];
-        tmem_ld16(lane_addr + uint32_t(b * bn + c0), v);
-        if (!valid) continue;
-        const int co = co_base + c0;
-        if (views_vec && co + 16 <= cout) {
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            epilogue8<T>(e, v + 8 * h, pix, on, co + 8 * h);
-            st8<T>(o.base, view_pixel_index(o, pix, co + 8 * h), v + 8 * h);
-          }
-        } else {
-          float tail[16];
-#pragma unroll
-          for (int i = 0; i < 16; ++i) tail[i] = v[i];
-          epilogue_store_tail<T>(e, o, tail, pix, on, co, min(16, cout - co));
-        }
-      }
+      if (!(L.flags & 4))
+        drain_rows_direct<T>(lane_addr + uint32_t(b * bn), ncols, pix, on, valid, co_base, cout, e, o,
+                             views_vec, nullptr, 0, c_first, c_step);
+      else
+        drain_rows<T>(lane_addr + uint32_t(b * bn), stg, ncols, pix, on, valid, co_base, cout, e, o,
+                      views_vec, nullptr, 0, c_first, c_step);
       tc_fence_before();
       mbar_arrive(&hdr->acc_empty[b]);                // buffer b may be overwritten
     }

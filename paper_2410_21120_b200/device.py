@@ -71,6 +71,7 @@ GEMM_SMEM_FIXED = 1024 + 2048                # barriers/descriptor + epilogue ve
 
 
 GEMM_PERSIST = os.environ.get("DFX_GEMM_PERSIST", "1") != "0"    # A/B switch
+GEMM_DRAIN_STAGED = os.environ.get("DFX_GEMM_DRAIN", "direct") == "staged"   # A/B switch
 
 
 def gemm_slots(bn: int, tiles: int, sm_count: int = 148, m2: int = 0) -> int:
@@ -520,6 +521,16 @@ class ExecInstance:
             gl.m2 = t.get("m2", 0)
             if GEMM_PERSIST and not gl.m2 and t["splits"] == 1 and t["tiles"] > 2 * self.dag.sm_count:
                 gl.flags |= 2                # persistent kernel for multi-wave layers
+                # bn > 64: one CTA per SM, as deep a ring as smem allows; bn <= 64: two
+                # CTAs per SM (dfx_api.cu), 4 slots each
+                if t["bn"] > 64:
+                    gl.nslots = max(2, min(8, (GEMM_SMEM_LIMIT - GEMM_SMEM_FIXED
+                                               - (8 * 2560 if GEMM_DRAIN_STAGED else 0))
+                                           // (128 * 64 * 2 + t["bn"] * 128)))
+                else:
+                    gl.nslots = 4
+            if GEMM_DRAIN_STAGED:
+                gl.flags |= 4                # smem-transposed epilogue drain (A/B)
             gl.desc0 = d                    # single problem: descriptor in kernel-param space
             yield rt.OP_GEMM, gl
             if t["splits"] > 1 and not fixup:

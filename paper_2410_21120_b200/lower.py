@@ -739,7 +739,10 @@ def gemm_tiling(geom: dict, n: int, p: int, q: int, sm_count: int = 148) -> dict
     # (a 256-row CTA takes ~1.6x a 128-row one: only when the wave count drops enough)
     waves1 = math.ceil(m_tiles * nt / sm_count)
     waves2 = math.ceil(math.ceil(m_tiles / 2) * nt / sm_count)
-    m2 = int(GEMM_M2 and splits == 1 and bn >= 128 and m_tiles >= 2
+    # (short-K layers go to the persistent kernel instead, whose overlapped epilogue
+    # matters more there than the halved weight traffic: measured on 3x3 64->256 at
+    # batch 32, 115 us m2 vs 80 us persistent; VGG's K=4608 layers keep m2)
+    m2 = int(GEMM_M2 and splits == 1 and bn >= 128 and m_tiles >= 2 and stages >= 24
              and math.ceil(m_tiles / 2) * nt >= sm_count and waves2 * 1.6 < waves1)
     tiles = (math.ceil(m_tiles / 2) if m2 else m_tiles) * nt * splits
     return dict(tn=tn, tp=tp, tq=tq, mt_n=mt[0], mt_p=mt[1], mt_q=mt[2], bn=bn, nt=nt,

@@ -66,9 +66,10 @@ def test_conv_layer(cin, h, w, cout, k, s, p, n):
 
 # large-M layers that take the 256-row CTA path (two M tiles per CTA sharing each
 # weight stage, lower.gemm_tiling m2), including an odd M-tile count (last CTA
-# holds one tile) and a stride-2 input
-M2_CASES = [(64, 28, 28, 256, 3, 1, 1, 21), (64, 28, 28, 128, 3, 1, 1, 64),
-            (128, 14, 14, 256, 1, 1, 0, 148), (32, 56, 56, 256, 3, 2, 1, 21)]
+# holds one tile) and a stride-2 input; m2 needs >= 24 K stages (shorter K goes to
+# the persistent kernel)
+M2_CASES = [(192, 28, 28, 256, 3, 1, 1, 21), (192, 28, 28, 128, 3, 1, 1, 64),
+            (1536, 14, 14, 256, 1, 1, 0, 148), (192, 56, 56, 256, 3, 2, 1, 21)]
 
 
 @pytest.mark.parametrize("cin,h,w,cout,k,s,p,n", M2_CASES)
@@ -81,8 +82,8 @@ def test_conv_layer_m2_tiles(cin, h, w, cout, k, s, p, n):
     test_conv_layer(cin, h, w, cout, k, s, p, n)
 
 
-# multi-wave layers that take the persistent kernel (dfx_gemm_persist.cu: <= 2 CTAs
-# per SM walk the tile list, double-buffered TMEM accumulators): bn 64 / 128 / 256,
+# multi-wave layers that take the persistent kernel (dfx_gemm_persist.cu: one CTA
+# per SM walks the tile list, a ring of TMEM accumulators): bn 64 / 128 / 256,
 # ragged output width and channel tail
 PERSIST_CASES = [(16, 112, 112, 64, 3, 1, 1, 4), (32, 56, 56, 128, 3, 1, 1, 13),
                  (24, 56, 56, 256, 1, 1, 0, 12), (40, 60, 57, 200, 3, 1, 1, 11)]
