@@ -6,6 +6,7 @@
 #include <algorithm>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -20,6 +21,8 @@ template <typename T> __global__ void gemm_persist_kernel(const __grid_constant_
 template <typename T> __global__ void splitk_kernel(const __grid_constant__ dfx_splitk_params P);
 template <typename T> __global__ void ew_kernel(const __grid_constant__ dfx_ew_params P);
 template <typename T> __global__ void dwconv_kernel(const __grid_constant__ dfx_dwconv_params P);
+template <typename T, int K, int S, int QV>
+__global__ void dwconv_tile_kernel(const __grid_constant__ dfx_dwconv_params P);
 template <typename T> __global__ void pool_kernel(const __grid_constant__ dfx_pool_params P);
 template <typename T> __global__ void gap_kernel(const __grid_constant__ dfx_gap_params P);
 template <typename T> __global__ void in_kernel(const __grid_constant__ dfx_in_params P);
@@ -52,6 +55,24 @@ const void* se_func(int dt, int cl) {
                          : reinterpret_cast<const void*>(&dfx::se_kernel<__nv_bfloat16, 16>);
   return dt == DFX_F16 ? reinterpret_cast<const void*>(&dfx::se_kernel<__half, 8>)
                        : reinterpret_cast<const void*>(&dfx::se_kernel<__nv_bfloat16, 8>);
+}
+
+template <typename T>
+const void* dwconv_tile_func_t(int k, int s, int qv) {
+#define DFX_DW_CASE(K, S)                                                                 \
+  if (k == K && s == S)                                                                   \
+    return qv == 4 ? reinterpret_cast<const void*>(&dfx::dwconv_tile_kernel<T, K, S, 4>)  \
+         : qv == 2 ? reinterpret_cast<const void*>(&dfx::dwconv_tile_kernel<T, K, S, 2>)  \
+                   : reinterpret_cast<const void*>(&dfx::dwconv_tile_kernel<T, K, S, 1>);
+  DFX_DW_CASE(3, 1)
+  DFX_DW_CASE(3, 2)
+  DFX_DW_CASE(5, 1)
+  DFX_DW_CASE(5, 2)
+#undef DFX_DW_CASE
+  return nullptr;
+}
+const void* dwconv_tile_func(int dt, int k, int s, int qv) {
+  return dt == DFX_F16 ? dwconv_tile_func_t<__half>(k, s, qv) : dwconv_tile_func_t<__nv_bfloat16>(k, s, qv);
 }
 
 thread_local std::string g_err;
@@ -175,6 +196,20 @@ int config_for(int op, const void* params, size_t size, LaunchCfg* c) {
     case DFX_OP_DWCONV: {
       NEED(dfx_dwconv_params);
       const auto* p = static_cast<const dfx_dwconv_params*>(params);
+      const int k = p->kh, st = p->stride_h;
+      const bool tiled = p->kh == p->kw && (k == 3 || k == 5) && p->stride_w == st &&
+                         (st == 1 || st == 2) && (p->in.c & 7) == 0 &&
+                         ((p->in.coff | p->out.coff | p->in.pitch) & 7) == 0 &&
+                         int64_t(p->out.n) * p->out.h * p->out.w * p->in.c < (int64_t(1) << 34);
+      if (tiled) {
+        // outputs per thread: as many as keep >= 2 waves of 256-thread blocks
+        const int64_t rows = int64_t(p->out.n) * p->out.h * (p->in.c / 8);
+        int qv = 4;
+        while (qv > 1 && rows * cdiv(p->out.w, qv) < int64_t(2) * g_sm_count * 256) qv >>= 1;
+        c->func = dwconv_tile_func(p->in.dtype, k, st, qv);
+        c->grid = dim3(elementwise_grid(rows * cdiv(p->out.w, qv), 256));
+        return DFX_OK;
+      }
       c->func = DFX_PICK(dwconv_kernel, p->in.dtype);
       c->grid = dim3(elementwise_grid(int64_t(p->out.n) * p->out.h * p->out.w * cdiv(p->in.c, 8), 256));
       return DFX_OK;
@@ -233,13 +268,16 @@ int config_for(int op, const void* params, size_t size, LaunchCfg* c) {
         return fail(DFX_E_UNSUPPORTED, "se: c=%d cr=%d beyond the cluster kernel's limits",
                     p->in.c, p->cr);
       // one cluster per image: 8 CTAs, or 16 when the weight slices would not fit in smem
-      if (p->apply && (p->out.n != p->in.n || p->out.h != p->in.h || p->out.w != p->in.w ||
+      if ((p->apply & 1) && (p->out.n != p->in.n || p->out.h != p->in.h || p->out.w != p->in.w ||
                        p->out.c != p->in.c))
         return fail(DFX_E_ARG, "se apply: out view must have the input's shape");
-      const int cl = dfx::se_smem_bytes(p->in.c, p->cr, 8) <= dfx::kSeSmemBudget ? 8 : 16;
+      // 16 CTAs per image (measured faster than 8 at batch 1 and 32: smaller slices,
+      // more pooling parallelism); DFX_SE_CL=8 for A/B
+      static const int cl_env = getenv("DFX_SE_CL") ? atoi(getenv("DFX_SE_CL")) : 16;
+      int cl = (cl_env == 8 && dfx::se_smem_bytes(p->in.c, p->cr, 8) <= dfx::kSeSmemBudget) ? 8 : 16;
       c->func = se_func(p->in.dtype, cl);
       c->grid = dim3(unsigned(cl), unsigned(p->in.n));
-      c->smem = size_t(dfx::se_smem_bytes(p->in.c, p->cr, cl));
+      c->smem = (p->apply & 2) ? 0 : size_t(dfx::se_smem_bytes(p->in.c, p->cr, cl));
       if (c->smem > size_t(dfx::kSeSmemBudget))
         return fail(DFX_E_UNSUPPORTED, "se: c=%d cr=%d needs %zu B of smem", p->in.c, p->cr, c->smem);
       return DFX_OK;

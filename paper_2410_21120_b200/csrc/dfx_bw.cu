@@ -47,7 +47,97 @@ __global__ void ew_kernel(const __grid_constant__ dfx_ew_params P) {
   }
 }
 
-// ------------------------------------------------------------------ depthwise conv
+// ------------------------------------------------------------------ depthwise conv (tiled)
+// Square K x K depthwise conv with stride S (the 3x3 / 5x5, stride 1 / 2 layers
+// of MobileNetV3 and EfficientNetV2).  One thread = 8 channels (16 B) x QV
+// consecutive output pixels of one row: each input row's (QV-1)*S + K columns
+// are loaded once and reused by the QV outputs (a 3x3/s1 tap costs 1.5 loads
+// per output at QV = 4 instead of 9), the taps of a kernel row are held in
+// registers, and all index math is 32-bit (the generic kernel below spends
+// most of its issue slots on 64-bit divisions).  Same fold order as the
+// generic kernel: for every output, (ki, kj) ascending.
+template <typename T, int K, int S, int QV>
+__global__ void __launch_bounds__(256) dwconv_tile_kernel(const __grid_constant__ dfx_dwconv_params P) {
+  griddep_wait();
+  griddep_launch();
+  const dfx_view& in = P.in;
+  const dfx_view& out = P.out;
+  constexpr int NCOL = (QV - 1) * S + K;
+  const int C = in.c, cg = C >> 3;
+  const int OW = out.w, OH = out.h, IW = in.w, IH = in.h;
+  const int qb = (OW + QV - 1) / QV;
+  const unsigned total = unsigned(out.n) * unsigned(OH) * unsigned(qb) * unsigned(cg);
+  const T* ib = reinterpret_cast<const T*>(in.base);
+  for (unsigned item = blockIdx.x * blockDim.x + threadIdx.x; item < total;
+       item += gridDim.x * blockDim.x) {
+    const unsigned cgi = item % unsigned(cg);
+    unsigned t = item / unsigned(cg);
+    const int qbi = int(t % unsigned(qb));
+    t /= unsigned(qb);
+    const int p = int(t % unsigned(OH));
+    const int n = int(t / unsigned(OH));
+    const int c = int(cgi) * 8;
+    const int q0 = qbi * QV;
+    const int h0 = p * S - P.pad_h, w0 = q0 * S - P.pad_w;
+    float acc[QV][8];
+#pragma unroll
+    for (int v = 0; v < QV; ++v)
+#pragma unroll
+      for (int i = 0; i < 8; ++i) acc[v][i] = 0.0f;
+#pragma unroll
+    for (int ki = 0; ki < K; ++ki) {
+      const int h = h0 + ki;
+      if (h < 0 || h >= IH) continue;
+      float wv[K][8];
+#pragma unroll
+      for (int kj = 0; kj < K; ++kj) {
+        const float4* wt = reinterpret_cast<const float4*>(P.weight + (ki * K + kj) * C + c);
+        const float4 lo = __ldg(wt), hi = __ldg(wt + 1);
+        wv[kj][0] = lo.x; wv[kj][1] = lo.y; wv[kj][2] = lo.z; wv[kj][3] = lo.w;
+        wv[kj][4] = hi.x; wv[kj][5] = hi.y; wv[kj][6] = hi.z; wv[kj][7] = hi.w;
+      }
+      const T* row = ib + (int64_t(n) * IH + h) * IW * in.pitch + in.coff + c;
+#pragma unroll
+      for (int j = 0; j < NCOL; ++j) {
+        const int w = w0 + j;
+        if (w < 0 || w >= IW) continue;
+        float x[8];
+        unpack8<T>(*reinterpret_cast<const uint4*>(row + int64_t(w) * in.pitch), x);
+#pragma unroll
+        for (int v = 0; v < QV; ++v) {
+          const int kj = j - v * S;
+          if (kj < 0 || kj >= K) continue;
+#pragma unroll
+          for (int i = 0; i < 8; ++i) acc[v][i] = fmaf(wv[kj][i], x[i], acc[v][i]);
+        }
+      }
+    }
+#pragma unroll
+    for (int v = 0; v < QV; ++v) {
+      const int q = q0 + v;
+      if (q >= OW) break;
+      const int64_t pix = (int64_t(n) * OH + p) * OW + q;
+      epilogue8<T>(P.epi, acc[v], pix, n, c);
+      st8<T>(out.base, view_pixel_index(out, pix, c), acc[v]);
+    }
+  }
+}
+
+#define DFX_DW_INST(T, K, S)                                                                         \
+  template __global__ void dwconv_tile_kernel<T, K, S, 1>(const __grid_constant__ dfx_dwconv_params); \
+  template __global__ void dwconv_tile_kernel<T, K, S, 2>(const __grid_constant__ dfx_dwconv_params); \
+  template __global__ void dwconv_tile_kernel<T, K, S, 4>(const __grid_constant__ dfx_dwconv_params);
+DFX_DW_INST(__half, 3, 1)
+DFX_DW_INST(__half, 3, 2)
+DFX_DW_INST(__half, 5, 1)
+DFX_DW_INST(__half, 5, 2)
+DFX_DW_INST(__nv_bfloat16, 3, 1)
+DFX_DW_INST(__nv_bfloat16, 3, 2)
+DFX_DW_INST(__nv_bfloat16, 5, 1)
+DFX_DW_INST(__nv_bfloat16, 5, 2)
+#undef DFX_DW_INST
+
+// ------------------------------------------------------------------ depthwise conv (generic)
 // One thread = 8 channels of one output pixel; fp32 taps [kh*kw][c].
 template <typename T>
 __global__ void dwconv_kernel(const __grid_constant__ dfx_dwconv_params P) {

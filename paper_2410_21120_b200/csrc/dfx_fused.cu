@@ -79,7 +79,11 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kSeThreads)
   const int nch = c_hi - c_lo;
   const T* w1g = reinterpret_cast<const T*>(P.w1);    // fc1^T  [C][Cr]
   const T* w2g = reinterpret_cast<const T*>(P.w2);    // fc2    [C][Cr]
-  const bool staged = (C & 7) == 0 && (Cr & 7) == 0;  // 16-B aligned slices
+  // 16-B aligned slices are staged in smem unless apply bit 1 says otherwise (large
+  // batches: clusters of smem-heavy CTAs then cannot be co-scheduled, while the
+  // weights are L2-resident and shared by every image's cluster anyway)
+  const bool staged = (C & 7) == 0 && (Cr & 7) == 0 && !(P.apply & 2);
+  const bool apply = P.apply & 1;
   const int sb = ((cs * Cr * 2) + 15) & ~15;
   const T* w1 = staged ? reinterpret_cast<const T*>(wsm) : w1g + int64_t(c_lo) * Cr;
   const T* w2 = staged ? reinterpret_cast<const T*>(wsm + sb) : w2g + int64_t(c_lo) * Cr;
@@ -199,7 +203,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kSeThreads)
   for (int k = threadIdx.x; k < nch; k += kSeThreads) {
     const T* row = w2 + int64_t(k) * Cr;
     float s0 = 0.f, s1 = 0.f;
-    if (staged) {
+    if ((Cr & 7) == 0) {
       for (int j = 0; j < Cr; j += 8) {
         float wv[8];
         ld8<T>(row, j, wv);
@@ -214,12 +218,12 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kSeThreads)
     const int c = c_lo + k;
     float a[8] = {s0 + s1 + (P.b2 ? P.b2[c] : 0.f), 0, 0, 0, 0, 0, 0, 0};
     act8(P.act2, a);
-    if (P.apply)
+    if (apply)
       pooled[k] = a[0];                                      // gate of this CTA's channel k
     else
       st1<T>(out.base, int64_t(n) * out.pitch + out.coff + c, a[0]);
   }
-  if (P.apply) {
+  if (apply) {
     // ---- 5. fused channel_scale: out[n, :, :, slice] = x * gate (x re-read from L2)
     __syncthreads();
     const int64_t pb = int64_t(n) * hw;

@@ -71,6 +71,9 @@ GEMM_SMEM_FIXED = 1024 + 2048                # barriers/descriptor + epilogue ve
 
 
 GEMM_PERSIST = os.environ.get("DFX_GEMM_PERSIST", "1") != "0"    # A/B switch
+# from this batch on the SE gate reads its FC weights from L2 instead of staging
+# them in smem per CTA (dfx_fused.cu; apply bit 1)
+SE_UNSTAGED_BATCH = int(os.environ.get("DFX_SE_UNSTAGED_BATCH", "8"))
 GEMM_DRAIN_STAGED = os.environ.get("DFX_GEMM_DRAIN", "direct") == "staged"   # A/B switch
 
 
@@ -572,7 +575,8 @@ class ExecInstance:
             addr = (lambda r: arena.addr(m, L.blobs[r]) if r in L.blobs else None)
             yield rt.OP_SE, rt.SeParams(src, self._view(m, prog, L.dst, n), addr("w1"), addr("b1"),
                                         addr("w2"), addr("b2"), geo["cr"], rt.ACT[geo["act1"]],
-                                        rt.ACT[geo["act2"]], geo.get("apply", 0))
+                                        rt.ACT[geo["act2"]],
+                                        geo.get("apply", 0) | (2 if n >= SE_UNSTAGED_BATCH else 0))
         else:
             raise AssertionError(L.kind)
 

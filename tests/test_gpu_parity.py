@@ -64,6 +64,35 @@ def test_conv_layer(cin, h, w, cout, k, s, p, n):
     assert rel(got, ref) < TOL
 
 
+# depthwise conv: the tiled kernel (square 3x3 / 5x5, stride 1 / 2, C % 8 == 0;
+# 1, 2 or 4 outputs per thread by grid size, ragged last pixel group) and the
+# generic kernel (C = 12)
+DW_CASES = [
+    # c, h, w, k, stride, n
+    (16, 9, 11, 3, 1, 2), (32, 56, 56, 3, 1, 8), (24, 17, 23, 3, 2, 3), (72, 28, 28, 5, 2, 16),
+    (40, 14, 13, 5, 1, 4), (96, 112, 112, 3, 2, 2), (12, 10, 10, 3, 1, 2),
+]
+
+
+@pytest.mark.parametrize("c,h,w,k,s,n", DW_CASES)
+def test_depthwise_layer(c, h, w, k, s, n):
+    rng = np.random.default_rng(c * 100 + h + k)
+    st = graph_ir.WeightStore()
+    st.put("w", graph_ir.TensorSpec((c, 1, k, k)), rng.standard_normal(c * k * k) / k)
+    st.put("b", graph_ir.TensorSpec((c,)), rng.standard_normal(c) * 0.1)
+    p = k // 2
+    oh, ow = (h + 2 * p - k) // s + 1, (w + 2 * p - k) // s + 1
+    nodes = [graph_ir.OpNode("d", "conv2d", {"out_channels": c, "kernel": k, "stride": s, "padding": p,
+                                             "groups": c}, {"weight": "w", "bias": "b"}),
+             graph_ir.OpNode("a", "silu", {}, {}, ("d",))]
+    g = graph_ir.ModelGraph("dw", nodes, "d", "a", graph_ir.TensorSpec((c, h, w)),
+                            graph_ir.TensorSpec((c, oh, ow)))
+    xs = rng.standard_normal((n, c, h, w)).astype(np.float32)
+    got = [t.values for t in run_batch(g, st, [Tensor(g.input_spec, x) for x in xs])]
+    ref = run_fast(g, st, xs)
+    assert rel(got, ref) < TOL
+
+
 # large-M layers that take the 256-row CTA path (two M tiles per CTA sharing each
 # weight stage, lower.gemm_tiling m2), including an odd M-tile count (last CTA
 # holds one tile) and a stride-2 input; m2 needs >= 24 K stages (shorter K goes to
