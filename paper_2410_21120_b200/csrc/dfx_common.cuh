@@ -19,18 +19,23 @@
 namespace dfx {
 
 // ---------------------------------------------------------------- math
-// Activations in fast-math form: no IEEE division (x / 6 and 1 / (1 + e) would
-// each compile to a ~20-instruction division subroutine, which made SiLU and
-// hardswish epilogues -- not the MMAs -- the bottleneck of multi-wave GEMMs).
-// rcp.approx (one MUFU op, 1 ulp) and __expf (ex2.approx, 2 ulp) are far below
-// the 16-bit storage rounding that follows.  (__frcp_rn's correctly-rounded
-// fix-up path compiled to per-element branches.)
-DFX_DEV float rcp_approx(float x) {
+// Activations in fast-math form, each a handful of instructions: the GEMM
+// epilogue drain is issue-bound, so instructions per output element set the
+// speed of every multi-wave layer.  sigmoid(v) = 0.5 + 0.5 tanh(v / 2) and
+// silu(v) = v sigmoid(v) use ONE MUFU.TANH (tanh.approx, ~2^-11 relative --
+// the fp16 storage rounding that follows is of the same order, and the parity
+// bar is 2e-2); no IEEE division anywhere (x / 6 and 1 / (1 + e) each
+// compiled to a division subroutine).
+DFX_DEV float tanh_approx(float x) {
   float r;
-  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  asm("tanh.approx.f32 %0, %1;" : "=f"(r) : "f"(x));
   return r;
 }
-DFX_DEV float sigmoid_f(float v) { return rcp_approx(1.0f + __expf(-v)); }
+DFX_DEV float sigmoid_f(float v) { return fmaf(0.5f, tanh_approx(0.5f * v), 0.5f); }
+DFX_DEV float silu_f(float v) {
+  const float h = 0.5f * v;
+  return fmaf(h, tanh_approx(h), h);
+}
 DFX_DEV float hsig_f(float v) { return fminf(fmaxf(v + 3.0f, 0.0f), 6.0f) * (1.0f / 6.0f); }
 
 DFX_DEV float act_apply(int act, float v) {
@@ -38,7 +43,7 @@ DFX_DEV float act_apply(int act, float v) {
     case DFX_ACT_RELU: return fmaxf(v, 0.0f);
     case DFX_ACT_HARDSWISH: return v * hsig_f(v);
     case DFX_ACT_HARDSIGMOID: return hsig_f(v);
-    case DFX_ACT_SILU: return v * sigmoid_f(v);
+    case DFX_ACT_SILU: return silu_f(v);
     case DFX_ACT_SIGMOID: return sigmoid_f(v);
     case DFX_ACT_GELU: return 0.5f * v * (1.0f + erff(v * 0.70710678118654752f));
     default: return v;
@@ -62,7 +67,7 @@ DFX_DEV void act8(int act, float* v) {
       break;
     case DFX_ACT_SILU:
 #pragma unroll
-      for (int i = 0; i < 8; ++i) v[i] = v[i] * sigmoid_f(v[i]);
+      for (int i = 0; i < 8; ++i) v[i] = silu_f(v[i]);
       break;
     case DFX_ACT_SIGMOID:
 #pragma unroll
@@ -98,9 +103,10 @@ template <> struct Elt<__half> {
   static DFX_DEV float sat(float v) { return fminf(fmaxf(v, -65504.0f), 65504.0f); }
   static DFX_DEV float to_f(__half v) { return __half2float(v); }
   static DFX_DEV __half from_f(float v) { return __float2half_rn(sat(v)); }
-  static DFX_DEV uint32_t pack2(float a, float b) {
-    __half2 h = __floats2half2_rn(sat(a), sat(b));
-    return *reinterpret_cast<uint32_t*>(&h);
+  static DFX_DEV uint32_t pack2(float a, float b) {   // one F2FP.SATFINITE: a low, b high
+    uint32_t r;
+    asm("cvt.rn.satfinite.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(b), "f"(a));
+    return r;
   }
   static DFX_DEV float2 unpack2(uint32_t u) { return __half22float2(*reinterpret_cast<__half2*>(&u)); }
 };
@@ -162,13 +168,21 @@ DFX_DEV float epilogue(const dfx_epilogue& e, float x, int64_t pix, int n, int c
 // Vector form over 8 consecutive channels c..c+7 (caller guarantees alignment).
 template <typename T>
 DFX_DEV void epilogue8(const dfx_epilogue& e, float* v, int64_t pix, int n, int c) {
-  if (e.alpha) {
+  if (e.alpha && e.beta) {                    // folded BN: one FFMA per element
+    const float4 a0 = *reinterpret_cast<const float4*>(e.alpha + c);
+    const float4 a1 = *reinterpret_cast<const float4*>(e.alpha + c + 4);
+    const float4 b0 = *reinterpret_cast<const float4*>(e.beta + c);
+    const float4 b1 = *reinterpret_cast<const float4*>(e.beta + c + 4);
+    v[0] = fmaf(v[0], a0.x, b0.x); v[1] = fmaf(v[1], a0.y, b0.y);
+    v[2] = fmaf(v[2], a0.z, b0.z); v[3] = fmaf(v[3], a0.w, b0.w);
+    v[4] = fmaf(v[4], a1.x, b1.x); v[5] = fmaf(v[5], a1.y, b1.y);
+    v[6] = fmaf(v[6], a1.z, b1.z); v[7] = fmaf(v[7], a1.w, b1.w);
+  } else if (e.alpha) {
     const float4 a0 = *reinterpret_cast<const float4*>(e.alpha + c);
     const float4 a1 = *reinterpret_cast<const float4*>(e.alpha + c + 4);
     v[0] *= a0.x; v[1] *= a0.y; v[2] *= a0.z; v[3] *= a0.w;
     v[4] *= a1.x; v[5] *= a1.y; v[6] *= a1.z; v[7] *= a1.w;
-  }
-  if (e.beta) {
+  } else if (e.beta) {
     const float4 b0 = *reinterpret_cast<const float4*>(e.beta + c);
     const float4 b1 = *reinterpret_cast<const float4*>(e.beta + c + 4);
     v[0] += b0.x; v[1] += b0.y; v[2] += b0.z; v[3] += b0.w;
