@@ -151,7 +151,11 @@ typedef struct __attribute__((aligned(64))) dfx_gemm_launch {
                                       bit 1: persistent kernel (1-2 CTAs/SM walk the
                                       tile list, a ring of TMEM accumulators; one
                                       problem, no split-K, no m2);
-                                      bit 2: smem-transposed epilogue drain (A/B only) */
+                                      bit 2: smem-transposed epilogue drain (A/B only);
+                                      bit 3: cluster split-K -- the desc0.splits (2..8)
+                                      CTAs of an output tile form a cluster and reduce
+                                      their partials over DSMEM (no workspace, no
+                                      splitk launch) */
   int32_t m2;                      /* any problem has m2 = 1 (sizes smem / TMEM) */
   int32_t _pad[7];
   dfx_gemm_desc desc0;             /* the problem when ndesc == 1 */

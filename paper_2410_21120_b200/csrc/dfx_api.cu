@@ -143,6 +143,7 @@ struct LaunchCfg {
   const void* func;
   dim3 grid, block;
   size_t smem;
+  unsigned cluster = 1;          // thread-block cluster size along x (1 = none)
 };
 
 int config_for(int op, const void* params, size_t size, LaunchCfg* c) {
@@ -177,6 +178,14 @@ int config_for(int op, const void* params, size_t size, LaunchCfg* c) {
         c->block = dim3(64 + 128 * groups);
       } else {
         c->smem = dfx::gemm_smem_bytes(p->bn_max, p->nslots, p->m2 ? 1 : 0) + 1024;
+        if (p->flags & 8) {             // cluster split-K: one cluster per output tile
+          const int sp = p->desc0.splits;
+          if (p->m2 || p->ndesc != 1 || sp < 2 || sp > 8 || p->total_tiles % sp)
+            return fail(DFX_E_ARG, "gemm: cluster split-K needs one problem, no m2, 2..8 splits");
+          if (size_t(128) * (p->bn_max + 4) * 4 > size_t(p->nslots) * dfx::gemm_slot_bytes(p->bn_max, 0))
+            return fail(DFX_E_ARG, "gemm: cluster split-K partial tile exceeds the %d slots", p->nslots);
+          c->cluster = unsigned(sp);
+        }
         // 8 warps (4 more drain the epilogue) when shared memory already limits the
         // SM to one CTA; else 4, so small-tile grids keep several CTAs per SM
         c->block = dim3(c->smem > size_t(114 * 1024) ? dfx::kGemmThreads : 128);
@@ -549,6 +558,22 @@ int dfx_launch(int op, const void* params, size_t params_size, void* stream) {
   int rc = config_for(op, params, params_size, &c);
   if (rc) return rc;
   void* args[1] = {const_cast<void*>(params)};
+  if (c.cluster > 1) {
+    cudaLaunchConfig_t lc = {};
+    lc.gridDim = c.grid;
+    lc.blockDim = c.block;
+    lc.dynamicSmemBytes = c.smem;
+    lc.stream = S(stream);
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = c.cluster;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    lc.attrs = at;
+    lc.numAttrs = 1;
+    CK(cudaLaunchKernelExC(&lc, c.func, args));
+    return DFX_OK;
+  }
   CK(cudaLaunchKernel(c.func, c.grid, c.block, args, c.smem, S(stream)));
   return DFX_OK;
 }
@@ -598,6 +623,13 @@ int dfx_graph_add(void* graph, int op, const void* params, size_t params_size, c
     }
   } else {
     CK(cudaGraphAddKernelNode(&node, g->g, dn.data(), dn.size(), &kp));
+  }
+  if (c.cluster > 1) {
+    cudaLaunchAttributeValue v = {};
+    v.clusterDim.x = c.cluster;
+    v.clusterDim.y = 1;
+    v.clusterDim.z = 1;
+    CK(cudaGraphKernelNodeSetAttribute(node, cudaLaunchAttributeClusterDimension, &v));
   }
   g->nodes.push_back(node);
   if (node_id) *node_id = int(g->nodes.size()) - 1;

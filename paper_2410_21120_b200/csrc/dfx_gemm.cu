@@ -156,10 +156,21 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   // per MAC halve -- the lever when the chip-wide TMA/L2 fill rate caps the MMA.
   constexpr int m2 = M2;
   const int mgroups = m2 ? (mt_total + 1) / 2 : mt_total;
-  const int mi = (t % mgroups) << m2;
-  t /= mgroups;
-  const int split = t % splits;
-  const int ntile = t / splits;
+  // cluster split-K (flag 8): the `splits` CTAs of one output tile are consecutive
+  // blocks = one thread-block cluster, split index = cluster rank
+  const bool csplit = !M2 && (L.flags & 8) && splits > 1;
+  int split, mi, ntile;
+  if (csplit) {
+    split = t % splits;
+    t /= splits;
+    mi = t % mgroups;
+    ntile = t / mgroups;
+  } else {
+    mi = (t % mgroups) << m2;
+    t /= mgroups;
+    split = t % splits;
+    ntile = t / splits;
+  }
   const int nhalf = (m2 && mi + 1 < mt_total) ? 2 : 1;   // M tiles in this CTA
   int n0h[1 + M2], p0h[1 + M2], q0h[1 + M2];
 #pragma unroll
@@ -334,6 +345,61 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 
   const int64_t plane = int64_t(N) * P * Q * ldw;      // one split's partials
   if (threadIdx.x == 0) DFX_TL(11);                    // epilogue starts
+  if (csplit) {
+    // ---- cluster split-K: every rank parks its fp32 partial tile in its own smem
+    // (the operand slots are free once the accumulator barrier fired), then rank r
+    // reduces rows [r*R/S, (r+1)*R/S) over all ranks IN RANK ORDER through DSMEM
+    // (deterministic, same order as splitk_kernel) and runs the epilogue on them.
+    // No fp32 workspace round trip through L2 and no second launch.
+    float* red = reinterpret_cast<float*>(slots);
+    const int rp = bn + 4;                               // row pitch (floats), conflict-free
+    const int c_step = 16 * int(blockDim.x >> 7);
+    for (int c0 = 16 * (warp >> 2); c0 < ncols; c0 += c_step) {
+      uint32_t r[16];
+      tmem_ld16_issue(lane_addr + uint32_t(c0), r);
+      tmem_ld_wait(r);
+      float4* dst = reinterpret_cast<float4*>(red + row * rp + c0);
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        dst[k] = make_float4(__uint_as_float(r[4 * k]), __uint_as_float(r[4 * k + 1]),
+                             __uint_as_float(r[4 * k + 2]), __uint_as_float(r[4 * k + 3]));
+    }
+    cluster_sync_all();
+    const int R = tn * tp * tq;
+    const int rows_per = (R + splits - 1) / splits;
+    const int r0 = split * rows_per, r1 = min(R, r0 + rows_per);
+    const int c8n = ncols / 8;
+    for (int item = threadIdx.x; item < (r1 - r0) * c8n; item += int(blockDim.x)) {
+      const int rr = r0 + item / c8n;
+      const int cc = (item - (rr - r0) * c8n) * 8;
+      const int co = co_base + cc;
+      const int on = n0h[0] + rr / (tq * tp), op = p0h[0] + (rr / tq) % tp, oq = q0h[0] + rr % tq;
+      if (on >= N || op >= P || oq >= Q || co >= cout) continue;
+      const float* src = red + rr * rp + cc;
+      float v[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+      for (int sr = 0; sr < splits; ++sr) {
+        const float4 a = dsmem_ld4(src, uint32_t(sr)), b = dsmem_ld4(src + 4, uint32_t(sr));
+        v[0] += a.x; v[1] += a.y; v[2] += a.z; v[3] += a.w;
+        v[4] += b.x; v[5] += b.y; v[6] += b.z; v[7] += b.w;
+      }
+      const int64_t pix = (int64_t(on) * P + op) * Q + oq;
+      if (views_vec && co + 8 <= cout) {
+        epilogue8<T>(e, v, pix, on, co);
+        st8<T>(o.base, view_pixel_index(o, pix, co), v);
+      } else {
+        float tail[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) tail[k] = v[k];
+        epilogue_store_tail<T>(e, o, tail, pix, on, co, min(8, cout - co));
+      }
+    }
+    cluster_sync_all();                                  // peers done reading this smem
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 2) tmem_dealloc(tmem_base, tmem_cols);
+    return;
+  }
+
   // per-warp transpose staging for the coalesced drain: the operand slots are
   // free once the accumulator barrier fired (every TMA load was consumed)
   float* stg = reinterpret_cast<float*>(slots + warp * kEpiStageWarpBytes);

@@ -38,7 +38,7 @@ ALIGN = 256
 # split-K reduction: "kernel" = a separate deterministic reduction node (default,
 # measured faster at batch 1: its launch overlaps via PDL and it is spread over
 # the whole GPU); "fixup" = the last-arriving CTA of each tile reduces in-kernel
-SPLITK_MODE = os.environ.get("DFX_SPLITK", "kernel")
+from .lower import SPLITK_MODE
 _program_cache: dict[tuple[int, int], tuple] = {}
 _cache_lock = threading.Lock()
 
@@ -294,7 +294,7 @@ def plan_member(prog: MemberProgram, n: int, sm_count: int = 148) -> MemberPlan:
         else:
             t = gemm_tiling(L.geom, n, out.h, out.w, sm_count)
         tilings[L.index] = t
-        if t["splits"] > 1:
+        if t["splits"] > 1 and not t["csplit"]:      # cluster split-K needs no workspace
             ws = max(ws, t["splits"] * n * out.h * out.w * t["nt"] * t["bn"] * 4)
     return MemberPlan(offsets, _align(arena), _align(ws), tilings)
 
@@ -510,7 +510,8 @@ class ExecInstance:
             if geo.get("tokens") and epi.binop:
                 epi.other = _fold_rows(epi.other)
             d.epi = epi
-            d.ws = (self.ws + self.ws_off[m]) if t["splits"] > 1 else None
+            csplit = bool(t["csplit"])
+            d.ws = (self.ws + self.ws_off[m]) if t["splits"] > 1 and not csplit else None
             fixup = t["splits"] > 1 and SPLITK_MODE == "fixup"
             if fixup:                  # per-output-tile arrival counters (in-kernel fixup)
                 d.counters = self.counters + 4 * self._ctr_used
@@ -522,6 +523,10 @@ class ExecInstance:
                                self.dtype, gemm_slots(t["bn"], t["tiles"], self.dag.sm_count,
                                                       t.get("m2", 0)))
             gl.m2 = t.get("m2", 0)
+            if csplit:
+                gl.flags |= 8                # cluster split-K (DSMEM reduction, no splitk node)
+                need = 128 * (t["bn"] + 4) * 4          # the fp32 partial tile parks in the slots
+                gl.nslots = max(gl.nslots, -(-need // (128 * 64 * 2 + t["bn"] * 128)))
             if GEMM_PERSIST and not gl.m2 and t["splits"] == 1 and t["tiles"] > 2 * self.dag.sm_count:
                 gl.flags |= 2                # persistent kernel for multi-wave layers
                 # bn > 64: one CTA per SM, as deep a ring as smem allows; bn <= 64: two
@@ -536,7 +541,7 @@ class ExecInstance:
                 gl.flags |= 4                # smem-transposed epilogue drain (A/B)
             gl.desc0 = d                    # single problem: descriptor in kernel-param space
             yield rt.OP_GEMM, gl
-            if t["splits"] > 1 and not fixup:
+            if t["splits"] > 1 and not fixup and not csplit:
                 yield rt.OP_SPLITK, rt.SplitKParams(self.ws + self.ws_off[m], t["splits"],
                                                     out.n * out.h * out.w, geo["cout"],
                                                     t["nt"] * t["bn"], out, epi)

@@ -655,10 +655,13 @@ class _Lowerer:
                         L.blobs[role] = key
 
 
+CB_WASTE = float(os.environ.get("DFX_CB_WASTE", "0.125"))     # A/B knob
+
+
 def choose_cb(cin: int) -> int:
-    """Channel block for the K loop: the widest of 64/32/16 wasting <= 12.5%."""
+    """Channel block for the K loop: the widest of 64/32/16 wasting <= CB_WASTE."""
     for cb in (64, 32):
-        if -(-cin // cb) * cb <= cin * 1.125:
+        if -(-cin // cb) * cb <= cin * (1 + CB_WASTE):
             return cb
     return 16
 
@@ -715,6 +718,14 @@ def choose_bn(cout: int) -> tuple[int, int]:
 
 
 GEMM_M2 = os.environ.get("DFX_GEMM_M2", "1") != "0"     # A/B switch for 256-row CTAs
+# split-K reduction: "kernel" (default) = fp32 workspace + a splitk_kernel launch;
+# "cluster" = the splits of a tile form a thread-block cluster and reduce over DSMEM
+# inside the GEMM (dfx_gemm.cu, <= 8 splits; removes 245 of 928 launches at batch 1
+# but measured no faster: 2.651 vs 2.635 ms fused, 4.539 vs 4.617 ms sequential --
+# the splitk launch overlaps the GEMM tail under PDL, cluster co-scheduling does not);
+# "fixup" = last-arriving CTA reduces (A/B)
+SPLITK_MODE = os.environ.get("DFX_SPLITK", "kernel")
+SPLITK_CLUSTER_MAX = 8
 
 
 def gemm_tiling(geom: dict, n: int, p: int, q: int, sm_count: int = 148) -> dict:
@@ -745,6 +756,9 @@ def gemm_tiling(geom: dict, n: int, p: int, q: int, sm_count: int = 148) -> dict
     m2 = int(GEMM_M2 and splits == 1 and bn >= 128 and m_tiles >= 2 and stages >= 24
              and math.ceil(m_tiles / 2) * nt >= sm_count and waves2 * 1.6 < waves1)
     tiles = (math.ceil(m_tiles / 2) if m2 else m_tiles) * nt * splits
-    return dict(tn=tn, tp=tp, tq=tq, mt_n=mt[0], mt_p=mt[1], mt_q=mt[2], bn=bn, nt=nt,
+    # cluster split-K when the splits fit one portable cluster; wider splits keep the
+    # workspace + splitk_kernel reduction
+    csplit = int(SPLITK_MODE == "cluster" and 1 < splits <= SPLITK_CLUSTER_MAX)
+    return dict(tn=tn, tp=tp, tq=tq, mt_n=mt[0], mt_p=mt[1], mt_q=mt[2], bn=bn, nt=nt, csplit=csplit,
                 kpack=kpack, stages=stages, splits=splits, sps=sps, m2=m2,
                 tiles=tiles)

@@ -283,3 +283,18 @@ def test_concurrent_execute_fused(corpus):
     for out in results:
         for mid in ref:
             assert np.array_equal(out[mid].values, ref[mid].values)
+
+
+# cluster split-K (DFX_SPLITK=cluster, dfx_gemm.cu): the splits of an output tile
+# reduce over DSMEM in rank order; small-M layers with 2..8 splits
+@pytest.mark.parametrize("cin,h,w,cout,k,s,p,n", [(192, 7, 7, 256, 3, 1, 1, 1), (1344, 14, 14, 224, 1, 1, 0, 1),
+                                                  (1536, 7, 7, 384, 1, 1, 0, 2), (1024, 7, 7, 130, 1, 1, 0, 3)])
+def test_conv_layer_cluster_splitk(cin, h, w, cout, k, s, p, n, monkeypatch):
+    from paper_2410_21120_b200 import device, lower
+    monkeypatch.setattr(lower, "SPLITK_MODE", "cluster")
+    monkeypatch.setattr(device, "SPLITK_MODE", "cluster")
+    cb = lower.choose_cb(cin)
+    oh = (h + 2 * p - k) // s + 1
+    t = lower.gemm_tiling(dict(cout=cout, cb=cb, ksteps=k * k * (-(-cin // cb)), sh=s, sw=s), n, oh, oh)
+    assert t["csplit"] == 1 and 2 <= t["splits"] <= 8
+    test_conv_layer(cin, h, w, cout, k, s, p, n)
