@@ -204,7 +204,9 @@ class WeightArena:
             rt.free(self.dev)
         for p in self.extra_allocs:
             rt.free(p)
-        rt.host_free(self.host)
+        if getattr(self, "host_pinned", True):       # pack_io may stage in pageable memory
+            rt.host_free(self.host)
+        self._host_keep = None
         self.dev = self.host = 0
 
 
