@@ -316,6 +316,12 @@ int dfx_launch(int op, const void* params, size_t params_size, void* stream);
 int dfx_graph_create(void** graph);
 int dfx_graph_add(void* graph, int op, const void* params, size_t params_size,
                   const int* deps, int ndeps, int* node_id);
+/* Scheduling priority of one node (cudaLaunchAttributePriority; lower = more
+ * urgent, within cudaDeviceGetStreamPriorityRange).  The executor raises the
+ * members with the longest dependent chains so the fused DAG's critical path
+ * is not delayed by the other branches' CTAs.  *range_out (optional) receives
+ * {least, greatest}. */
+int dfx_graph_set_priority(void* graph, int node_id, int priority, int* range_out);
 int dfx_graph_instantiate(void* graph);
 int dfx_graph_launch(void* graph, void* stream);
 int dfx_graph_node_count(void* graph, int* count);

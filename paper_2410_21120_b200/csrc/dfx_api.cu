@@ -336,6 +336,7 @@ struct Graph {
   cudaGraph_t g = nullptr;
   cudaGraphExec_t exec = nullptr;
   std::vector<cudaGraphNode_t> nodes;
+  bool use_priority = false;      // some node carries a priority attribute
   // programmatic dependent launch between nodes; DFX_PDL=0 in the environment
   // turns it off (A/B measurements)
   bool pdl = [] {
@@ -636,11 +637,30 @@ int dfx_graph_add(void* graph, int op, const void* params, size_t params_size, c
   return DFX_OK;
 }
 
+int dfx_graph_set_priority(void* graph, int node_id, int priority, int* range_out) {
+  auto* g = static_cast<Graph*>(graph);
+  if (!g || g->exec) return fail(DFX_E_STATE, "graph_set_priority after instantiate");
+  int least = 0, greatest = 0;
+  CK(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+  if (range_out) {
+    range_out[0] = least;
+    range_out[1] = greatest;
+  }
+  if (node_id < 0 || node_id >= int(g->nodes.size()))
+    return fail(DFX_E_ARG, "graph_set_priority: node %d out of range", node_id);
+  cudaLaunchAttributeValue v = {};
+  v.priority = std::min(least, std::max(greatest, priority));
+  CK(cudaGraphKernelNodeSetAttribute(g->nodes[node_id], cudaLaunchAttributePriority, &v));
+  g->use_priority = true;
+  return DFX_OK;
+}
+
 int dfx_graph_instantiate(void* graph) {
   auto* g = static_cast<Graph*>(graph);
   if (!g) return fail(DFX_E_ARG, "null graph");
   if (g->exec) return DFX_OK;
-  CK(cudaGraphInstantiate(&g->exec, g->g, 0));
+  CK(cudaGraphInstantiate(&g->exec, g->g,
+                          g->use_priority ? cudaGraphInstantiateFlagUseNodePriority : 0));
   return DFX_OK;
 }
 

@@ -74,6 +74,11 @@ GEMM_PERSIST = os.environ.get("DFX_GEMM_PERSIST", "1") != "0"    # A/B switch
 # from this batch on the SE gate reads its FC weights from L2 instead of staging
 # them in smem per CTA (dfx_fused.cu; apply bit 1)
 SE_UNSTAGED_BATCH = int(os.environ.get("DFX_SE_UNSTAGED_BATCH", "8"))
+# node priorities by member chain length (DFX_PRIORITY=0: off, A/B) for latency-bound
+# (small-batch) instances: 4-model batch 1 2.63 -> 2.48 ms, 8-model mixed 3.37 ->
+# 2.91 ms; at batch 32 the chain length is no proxy for work (12.3 -> 13.3 ms), so off
+NODE_PRIORITY = os.environ.get("DFX_PRIORITY", "1") != "0"
+PRIORITY_MAX_BATCH = 8
 GEMM_DRAIN_STAGED = os.environ.get("DFX_GEMM_DRAIN", "direct") == "staged"   # A/B switch
 
 
@@ -377,6 +382,7 @@ class ExecInstance:
         prev_tail = None
         self._keep = []                                # keep param structs alive
         self.nodes = []                                # (op, params, algorithmic info)
+        self._node_member = []                         # member index of every graph node
         for m, (prog, n) in enumerate(zip(progs, self.batch)):
             if n == 0:
                 continue
@@ -386,11 +392,13 @@ class ExecInstance:
             pin = rt.InParams(self.dev_in + self.in_off[m], self._view(m, prog, "<input>", n),
                               *ic, *ind)
             last = g.add(rt.OP_IN, pin, deps)
+            self._node_member.append(m)
             self.nodes.append((rt.OP_IN, pin, dict(member=m, kind="in", flops=0,
                                                    bytes=self.in_sizes[m] * 3 // 2)))
             for L in prog.launches:
                 for op, params in self._params(m, prog, L, n, host_descs):
                     last = g.add(op, params, [last])
+                    self._node_member.append(m)
                     info = self._algo(prog, L, n, op)
                     info["node"] = L.nodes[0]
                     if op == rt.OP_GEMM:
@@ -399,9 +407,12 @@ class ExecInstance:
                     self.nodes.append((op, params, info))
             pout = rt.OutParams(self._view(m, prog, prog.exit_value, n), self.dev_out + self.out_off[m])
             last = g.add(rt.OP_OUT, pout, [last])
+            self._node_member.append(m)
             self.nodes.append((rt.OP_OUT, pout, dict(member=m, kind="out", flops=0,
                                                      bytes=self.out_sizes[m] * 3 // 2)))
             prev_tail = last
+        if NODE_PRIORITY and self.dag.mode == "concurrent" and max(self.batch) <= PRIORITY_MAX_BATCH:
+            self._prioritise(g)
         self._keep = [p for _, p, _ in self.nodes]
         if host_descs:
             arr = (rt.GemmDesc * len(host_descs))(*host_descs)
@@ -410,6 +421,21 @@ class ExecInstance:
         g.instantiate()
         self.kernel_nodes = len(g.kinds)
         return g
+
+    def _prioritise(self, g) -> None:
+        """Concurrent members are independent branches of one graph; the query
+        ends when the LONGEST dependent chain ends.  Members get node priorities
+        by chain length (graph nodes, a latency proxy at small batch): the longest
+        chain most urgent, so other branches' CTAs fill in around it instead of
+        delaying it."""
+        chain: dict[int, int] = {}
+        for m in self._node_member:
+            chain[m] = chain.get(m, 0) + 1
+        order = sorted(chain, key=lambda m: (-chain[m], m))
+        least, greatest = g.set_priority(0, 0)
+        prio = {m: min(least, greatest + r) for r, m in enumerate(order)}
+        for nid, m in enumerate(self._node_member):
+            g.set_priority(nid, prio[m])
 
     @staticmethod
     def _algo(prog: MemberProgram, L, n: int, op: int) -> dict:

@@ -132,7 +132,7 @@ EXPORTS = (
     "dfx_memcpy_d2d", "dfx_arena_upload", "dfx_stream_create", "dfx_stream_destroy",
     "dfx_stream_sync", "dfx_event_create", "dfx_event_destroy", "dfx_event_record",
     "dfx_event_elapsed", "dfx_tmap_act", "dfx_tmap_weights", "dfx_launch", "dfx_graph_create",
-    "dfx_graph_add", "dfx_graph_instantiate", "dfx_graph_launch", "dfx_graph_node_count",
+    "dfx_graph_add", "dfx_graph_set_priority", "dfx_graph_instantiate", "dfx_graph_launch", "dfx_graph_node_count",
     "dfx_graph_destroy", "dfx_execute",
 )
 
@@ -283,6 +283,12 @@ class Graph:
              C.c_size_t(C.sizeof(params)), arr, C.c_int(len(deps)), C.byref(nid))
         self.kinds.append(op)
         return nid.value
+
+    def set_priority(self, node_id: int, priority: int) -> tuple[int, int]:
+        """Node scheduling priority (lower = more urgent); returns (least, greatest)."""
+        rng = (C.c_int * 2)()
+        call("dfx_graph_set_priority", vp(self.ptr), C.c_int(node_id), C.c_int(priority), rng)
+        return rng[0], rng[1]
 
     def instantiate(self):
         call("dfx_graph_instantiate", vp(self.ptr))
