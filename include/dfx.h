@@ -133,7 +133,16 @@ typedef struct __attribute__((aligned(64))) dfx_gemm_desc {
   uint32_t* counters;              /* split-K arrival counters, one per output tile, zeroed
                                       once; the last-arriving CTA of a tile reduces all splits
                                       in split order (deterministic) and resets its counter */
-  int64_t _pad1[2];                
+  /* A-operand prologue transform (1x1 convs, r = s = 1, no padding): every A tile
+   * is rewritten in shared memory before the MMA reads it, fusing the producer
+   * elementwise node into the GEMM:
+   *   pre_mode 1: a = act(a * pre_scale[c] + pre_shift[c])   (fp32 vectors, >= cblocks*cb
+   *               entries; DenseNet's pre-activation BN + ReLU)
+   *   pre_mode 2: a = a * gate[n][c], gate 16-bit at pre_scale + n*pre_pitch + c
+   *               (the squeeze-excitation channel scale before a projection conv) */
+  const void* pre_scale;
+  const float* pre_shift;
+  int32_t pre_mode, pre_act, pre_cin, pre_pitch;
 } dfx_gemm_desc;
 
 /* Kernel parameter of one GEMM launch.  A single problem travels inline

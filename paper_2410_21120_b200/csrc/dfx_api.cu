@@ -164,13 +164,16 @@ int config_for(int op, const void* params, size_t size, LaunchCfg* c) {
       if (p->nslots < 2 || p->nslots > dfx::kMaxSlots)
         return fail(DFX_E_ARG, "gemm: nslots %d", p->nslots);
       if (p->m2 && p->bn_max > 256) return fail(DFX_E_ARG, "gemm: m2 with bn %d", p->bn_max);
+      if (p->desc0.pre_mode && (p->m2 || p->ndesc != 1 || p->desc0.r != 1 || p->desc0.s != 1 ||
+                                p->desc0.pad_h || p->desc0.pad_w))
+        return fail(DFX_E_ARG, "gemm: A prologue transform needs one 1x1 unpadded problem, no m2");
       if (p->flags & 2) {               // persistent: one CTA per SM walks the tile list
         if (p->m2 || p->ndesc != 1 || p->desc0.splits != 1 || p->bn_max > 256)
           return fail(DFX_E_ARG, "gemm: persistent launch needs one problem, no m2 / split-K");
         c->func = DFX_PICK(gemm_persist_kernel, p->dtype);
         // narrow tiles (bn <= 64): two CTAs per SM with one epilogue group each (two
         // producers / MMA issuers per SM); else one CTA per SM with two groups
-        const int per_sm = p->bn_max <= 64 ? 2 : 1;
+        const int per_sm = (p->bn_max <= 64 && !p->desc0.pre_mode) ? 2 : 1;   // pre_mode: 2 groups
         const int groups = 3 - per_sm;
         c->smem = dfx::gemm_smem_bytes(p->bn_max, p->nslots, 0) + 1024 +
                   ((p->flags & 4) ? 4 * groups * dfx::kEpiStageWarpBytes : 0);
@@ -188,7 +191,7 @@ int config_for(int op, const void* params, size_t size, LaunchCfg* c) {
         }
         // 8 warps (4 more drain the epilogue) when shared memory already limits the
         // SM to one CTA; else 4, so small-tile grids keep several CTAs per SM
-        c->block = dim3(c->smem > size_t(114 * 1024) ? dfx::kGemmThreads : 128);
+        c->block = dim3((c->smem > size_t(114 * 1024) || p->desc0.pre_mode) ? dfx::kGemmThreads : 128);
       }
       if (c->smem > size_t(kGemmSmemLimit))
         return fail(DFX_E_ARG, "gemm: %zu B of shared memory (bn %d x %d slots)", c->smem,

@@ -128,3 +128,78 @@ DFX_DEV void drain_rows_direct(uint32_t taddr, int ncols, int64_t pix, int img, 
 }
 
 }  // namespace dfx
+
+namespace dfx {
+
+// ---------------------------------------------------------------- A-operand prologue transform
+// Rewrites one pipeline stage's A sub-tiles (nk k-steps of cb channels x 128 rows,
+// 16-bit, TMA-swizzled: 16-B chunk bits [4:6] XOR address bits [7:9] for 128-B rows,
+// [4:5]/[7:8] for 64-B rows, [4]/[7] for 32-B rows) in place, before the MMA reads
+// them (dfx_gemm_desc pre_mode; 1x1 convs, so k-step == channel block).  Chunks of
+// channels >= pre_cin (the zero fill of the last block) are left untouched.
+template <typename T>
+DFX_DEV void pre_transform_stage(uint8_t* a_base, int nk, int cb, int kstep0, const dfx_gemm_desc& D,
+                                 int n0, int rows_per_img, int tid, int nthr) {
+  // With nthr a multiple of 64, every chunk a thread visits (tid + k * nthr) holds
+  // the SAME 8 logical channels of its k-step (the swizzle phase repeats every 8
+  // rows): the per-channel vectors are loaded once per k-step, not per chunk.
+  const int sub_a = 128 * cb * 2;
+  const int cps = sub_a >> 4;                         // 16-B chunks per sub-tile
+  const uint32_t m = cb == 64 ? 7u : (cb == 32 ? 3u : 1u);
+  const int rshift = cb == 64 ? 7 : (cb == 32 ? 6 : 5);   // log2(row bytes)
+  const int mode = D.pre_mode, act = D.pre_act, cin = D.pre_cin;
+  const float* sc = static_cast<const float*>(D.pre_scale);
+  const float* sh = D.pre_shift;
+  const uint32_t a_t = uint32_t(tid) << 4;
+  const uint32_t la_t = a_t ^ (((a_t >> 7) & m) << 4);
+  const int lchunk = int((la_t & ((1u << rshift) - 1)) >> 4);
+  const int row_step = (nthr << 4) >> rshift;          // rows advanced per k
+  for (int j = 0; j < nk; ++j) {
+    const int c = (kstep0 + j) * cb + lchunk * 8;
+    if (c >= cin) continue;
+    uint8_t* sub = a_base + j * sub_a;
+    if (mode == 1) {
+      const float4 a0 = *reinterpret_cast<const float4*>(sc + c), a1 = *reinterpret_cast<const float4*>(sc + c + 4);
+      float4 b0 = make_float4(0.f, 0.f, 0.f, 0.f), b1 = b0;
+      if (sh) {
+        b0 = *reinterpret_cast<const float4*>(sh + c);
+        b1 = *reinterpret_cast<const float4*>(sh + c + 4);
+      }
+      for (int i = tid; i < cps; i += nthr) {
+        uint4* p = reinterpret_cast<uint4*>(sub + (i << 4));
+        float x[8];
+        unpack8<T>(*p, x);
+        x[0] = fmaf(x[0], a0.x, b0.x); x[1] = fmaf(x[1], a0.y, b0.y);
+        x[2] = fmaf(x[2], a0.z, b0.z); x[3] = fmaf(x[3], a0.w, b0.w);
+        x[4] = fmaf(x[4], a1.x, b1.x); x[5] = fmaf(x[5], a1.y, b1.y);
+        x[6] = fmaf(x[6], a1.z, b1.z); x[7] = fmaf(x[7], a1.w, b1.w);
+        act8(act, x);
+        *p = pack8<T>(x);
+      }
+    } else {
+      int row = int(la_t >> rshift), cur_n = -1;
+      float g[8];
+      for (int i = tid; i < cps; i += nthr, row += row_step) {
+        const int n = n0 + row / rows_per_img;
+        if (n != cur_n) {
+          ld8<T>(D.pre_scale, int64_t(n) * D.pre_pitch + c, g);
+          cur_n = n;
+        }
+        uint4* p = reinterpret_cast<uint4*>(sub + (i << 4));
+        float x[8];
+        unpack8<T>(*p, x);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) x[k] *= g[k];
+        *p = pack8<T>(x);
+      }
+    }
+  }
+}
+
+// generic-proxy smem writes -> visible to the tensor core's async proxy
+DFX_DEV void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+DFX_DEV void named_bar_sync(int id, int nthreads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+}  // namespace dfx

@@ -73,6 +73,7 @@ struct GemmHeader {
   uint64_t full[kMaxSlots];
   uint64_t empty[kMaxSlots];
   uint64_t accum;
+  uint64_t ready[kMaxSlots];   // pre_mode: A stage transformed in smem, MMA may read it
   uint32_t tmem_base;
   uint32_t last_split;    // split-K: this CTA arrived last for its output tile
   uint32_t _pad[12];
@@ -126,6 +127,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     for (int i = 0; i < nslots; ++i) {
       mbar_init(&hdr->full[i], 1);
       mbar_init(&hdr->empty[i], 1);
+      mbar_init(&hdr->ready[i], 1);
     }
     mbar_init(&hdr->accum, 1);
     fence_barrier_init();
@@ -267,10 +269,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     const int kk_n = cb / 16;
     uint32_t accumulate = 0;
     int it = 0;
+    uint64_t* const gate_bar = D.pre_mode ? hdr->ready : hdr->full;   // pre_mode: wait for the transform
     for (int st = st_begin; st < st_end; ++st, ++it) {
       const int slot = it % nslots;
       const uint32_t par = (it / nslots) & 1;
-      mbar_wait(&hdr->full[slot], par);
+      mbar_wait(&gate_bar[slot], par);
       if (it == 0) DFX_TL(3);                      // first stage landed
       if (it > 0 && it < 9) DFX_TL(12 + it);       // later stages landed (13..20)
       if (it < 7) DFX_TC(42 + 3 * it);
@@ -301,15 +304,32 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     }
     umma_commit(&hdr->accum);
     DFX_TL(4);                                     // last MMA issued
-  } else if (warp >= 2 && splits == 1) {
-    // ================= stage this N tile's epilogue vectors (static data) in smem
-    const int ti = threadIdx.x - 64;
-    const float* ga = D.epi.alpha;
-    const float* gb = D.epi.beta;
-    for (int i = ti; i < bn; i += int(blockDim.x) - 64) {
-      const int c = co_base + i;
-      if (ga) s_alpha[i] = c < cout ? ga[c] : 0.f;
-      if (gb) s_beta[i] = c < cout ? gb[c] : 0.f;
+  } else if (warp >= 2) {
+    const int ti = threadIdx.x - 64, nthr = int(blockDim.x) - 64;
+    if (splits == 1) {
+      // ================= stage this N tile's epilogue vectors (static data) in smem
+      const float* ga = D.epi.alpha;
+      const float* gb = D.epi.beta;
+      for (int i = ti; i < bn; i += nthr) {
+        const int c = co_base + i;
+        if (ga) s_alpha[i] = c < cout ? ga[c] : 0.f;
+        if (gb) s_beta[i] = c < cout ? gb[c] : 0.f;
+      }
+    }
+    if (D.pre_mode) {
+      // ================= A prologue transform: rewrite each landed A stage in smem
+      griddep_wait();                                  // the gate vector is a predecessor's output
+      int it = 0;
+      for (int st = st_begin; st < st_end; ++st, ++it) {
+        const int slot = it % nslots;
+        if (ti == 0) mbar_wait(&hdr->full[slot], (it / nslots) & 1);
+        named_bar_sync(1, nthr);
+        pre_transform_stage<T>(slots + slot * slot_bytes, min(kpack, ksteps - st * kpack), cb, st * kpack, D,
+                               n0h[0], tp * tq, ti, nthr);
+        fence_proxy_async_smem();
+        named_bar_sync(1, nthr);
+        if (ti == 0) mbar_arrive(&hdr->ready[slot]);
+      }
     }
   }
   __syncwarp();

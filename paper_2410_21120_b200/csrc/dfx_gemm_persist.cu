@@ -35,6 +35,7 @@ struct PersistHeader {
   uint64_t empty[kMaxSlots];
   uint64_t acc_full[kMaxAcc];
   uint64_t acc_empty[kMaxAcc];
+  uint64_t ready[kMaxSlots];     // pre_mode: A stage transformed in smem
   uint32_t tmem_base;
   uint32_t _pad[7];
   dfx_gemm_desc desc;
@@ -63,16 +64,19 @@ __global__ void __launch_bounds__(kPersistThreads, 1)
   // CTA's tcgen05.alloc would otherwise block until the first one exits).
   const int groups = (int(blockDim.x) - 64) >> 7;
   const int nacc = max(2, min(kMaxAcc, (groups > 1 ? 512 : 256) / L.bn_max));
-  const bool alt = groups > 1 && nacc >= 4;
+  // pre_mode (A prologue transform): group 1 transforms A stages, group 0 drains
+  const bool pre = L.desc0.pre_mode != 0;
+  const bool alt = groups > 1 && nacc >= 4 && !pre;
   const uint32_t tmem_cols = tmem_cols_for(nacc * L.bn_max);
   if (threadIdx.x == 0) {
     for (int i = 0; i < nslots; ++i) {
       mbar_init(&hdr->full[i], 1);
       mbar_init(&hdr->empty[i], 1);
+      mbar_init(&hdr->ready[i], 1);
     }
     for (int b = 0; b < nacc; ++b) {
       mbar_init(&hdr->acc_full[b], 1);
-      mbar_init(&hdr->acc_empty[b], alt ? 128 : blockDim.x - 64);
+      mbar_init(&hdr->acc_empty[b], (alt || pre) ? 128 : blockDim.x - 64);
     }
     fence_barrier_init();
     tma_prefetch_desc(gd->tmap_a);
@@ -147,7 +151,7 @@ __global__ void __launch_bounds__(kPersistThreads, 1)
         uint32_t accumulate = 0;
         for (int st = 0; st < stages; ++st, ++it) {
           const int slot = it % nslots;
-          mbar_wait(&hdr->full[slot], (it / nslots) & 1);
+          mbar_wait(pre ? &hdr->ready[slot] : &hdr->full[slot], (it / nslots) & 1);
           tc_fence_after();
           const uint32_t a_base = smem_u32(slots + slot * slot_bytes);
           const uint32_t b_base = a_base + kStageABytes;
@@ -176,7 +180,26 @@ __global__ void __launch_bounds__(kPersistThreads, 1)
     const uint32_t lane_addr = tmem_base + (uint32_t(quad * 32) << 16);
     float* stg = reinterpret_cast<float*>(slots + nslots * slot_bytes + (warp - 2) * kEpiStageWarpBytes);
     const int group = (warp - 2) >> 2;
-    const int c_first = alt ? 0 : 16 * group, c_step = alt ? 16 : 16 * groups;
+    const int c_first = (alt || pre) ? 0 : 16 * group, c_step = (alt || pre) ? 16 : 16 * groups;
+    if (pre && group == 1) {
+      // ================= A prologue transform over every stage of every tile of this CTA
+      const int ti = threadIdx.x - 64 - 128;
+      int it = 0;
+      for (int tile = blockIdx.x; tile < total; tile += grid) {
+        const int mi = tile % mt_total;
+        const int n0 = (mi / (mt_q * mt_p)) * tn;
+        for (int st = 0; st < stages; ++st, ++it) {
+          const int slot = it % nslots;
+          if (ti == 0) mbar_wait(&hdr->full[slot], (it / nslots) & 1);
+          named_bar_sync(1, 128);
+          pre_transform_stage<T>(slots + slot * slot_bytes, min(kpack, ksteps - st * kpack), cb, st * kpack, D,
+                                 n0, tp * tq, ti, 128);
+          fence_proxy_async_smem();
+          named_bar_sync(1, 128);
+          if (ti == 0) mbar_arrive(&hdr->ready[slot]);
+        }
+      }
+    } else {
     int lt = 0;
     for (int tile = blockIdx.x; tile < total; tile += grid, ++lt) {
       if (alt && (lt % groups) != group) continue;
@@ -199,6 +222,7 @@ __global__ void __launch_bounds__(kPersistThreads, 1)
                       views_vec, nullptr, 0, c_first, c_step);
       tc_fence_before();
       mbar_arrive(&hdr->acc_empty[b]);                // buffer b may be overwritten
+    }
     }
   }
   tc_fence_before();

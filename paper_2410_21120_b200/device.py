@@ -538,6 +538,16 @@ class ExecInstance:
             if geo.get("tokens") and epi.binop:
                 epi.other = _fold_rows(epi.other)
             d.epi = epi
+            if L.pre is not None:            # A prologue transform (lower.fold_pre_transforms)
+                if L.pre.binop == 2:
+                    gv = self._view(m, prog, L.pre.other, n)
+                    d.pre_mode, d.pre_scale, d.pre_pitch = 2, gv.base + 2 * gv.coff, gv.pitch
+                else:
+                    d.pre_mode = 1
+                    d.pre_scale = arena.addr(m, L.blobs["pre_alpha"])
+                    d.pre_shift = arena.addr(m, L.blobs["pre_beta"]) if "pre_beta" in L.blobs else None
+                d.pre_act = rt.ACT[L.pre.act1]
+                d.pre_cin = geo["cin"]
             csplit = bool(t["csplit"])
             d.ws = (self.ws + self.ws_off[m]) if t["splits"] > 1 and not csplit else None
             fixup = t["splits"] > 1 and SPLITK_MODE == "fixup"

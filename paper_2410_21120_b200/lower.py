@@ -129,6 +129,8 @@ class Launch:
     geom: dict = field(default_factory=dict)
     blobs: dict = field(default_factory=dict)     # role -> blob key
     index: int = -1
+    pre: Epi | None = None              # GEMM A prologue transform (a folded EW producer)
+    pre_nodes: list = field(default_factory=list)
 
 
 @dataclass
@@ -491,6 +493,8 @@ class _Lowerer:
             if nid in self.absorbed:
                 continue
             self.lower_node(nid)
+        if FOLD_PRE:
+            self.fold_pre_transforms()
         self.place()
         for s, cid, off in self.copies:
             self.launches.append(Launch(COPY, [cid], s, f"{cid}@{off}",
@@ -504,6 +508,49 @@ class _Lowerer:
         return MemberProgram(self.g.model_id, tuple(self.g.input_spec.dims),
                              tuple(self.g.output_spec.dims), self.launches, self.values,
                              self.buffers, self.blobs, self.g.exit)
+
+    def fold_pre_transforms(self):
+        """Fold an elementwise producer into the A operand of the 1x1 conv that is its
+        only consumer: DenseNet's pre-activation BN + ReLU on the concat buffer (mode
+        1) and the squeeze-excitation channel scale before a projection conv (mode
+        2).  The GEMM rewrites each A tile in shared memory before the MMA
+        (dfx_epi.cuh pre_transform_stage): one launch and one full activation
+        write + read fewer.  1x1 / unpadded only: a transform of padding zeros
+        would not stay zero."""
+        g = self.g
+        uses: dict[str, int] = {}
+        for L in self.launches:
+            uses[L.src] = uses.get(L.src, 0) + 1
+            if L.epi.other is not None:
+                uses[L.epi.other] = uses.get(L.epi.other, 0) + 1
+        for nid in self.order:
+            if g.nodes[nid].kind in ("concat", "flatten"):
+                for s in g.nodes[nid].inputs:
+                    uses[s] = uses.get(s, 0) + 2          # views / copies: never fold
+        uses[g.exit] = uses.get(g.exit, 0) + 2
+        producer = {L.dst: L for L in self.launches}
+        drop = set()
+        for L in self.launches:
+            geo = L.geom
+            if L.kind != GEMM or geo.get("dense") or geo.get("tokens") or geo["kh"] != 1 or \
+                    geo["kw"] != 1 or geo["ph"] or geo["pw"]:
+                continue
+            E = producer.get(L.src)
+            if E is None or E.kind != EW or uses.get(E.dst, 0) != 1 or E.dst.endswith("#acc"):
+                continue
+            if E.src in g.nodes and g.nodes[E.src].kind == "flatten":
+                continue
+            e = E.epi
+            if e.binop == 0 and e.act2 is None and (e.alpha is not None or e.beta is not None or e.act1):
+                pre = Epi(alpha=e.alpha, beta=e.beta, act1=e.act1)
+            elif e.binop == 2 and e.alpha is None and e.beta is None and e.act1 is None and e.act2 is None:
+                pre = Epi(binop=2, other=e.other)
+            else:
+                continue
+            L.pre, L.pre_nodes, L.src = pre, list(E.nodes), E.src
+            geo["pre"] = 1
+            drop.add(id(E))
+        self.launches = [L for L in self.launches if id(L) not in drop]
 
     def value_of(self, name):
         return self.resolve(name)
@@ -527,6 +574,8 @@ class _Lowerer:
             touch_read(self.value_of(L.src), i)
             if L.epi.other is not None:
                 touch_read(self.value_of(L.epi.other), i)
+            if L.pre is not None and L.pre.other is not None:
+                touch_read(self.value_of(L.pre.other), i)
             if L.kind == COPY:
                 touch_write(self.value_of(L.geom["concat"]), i)
             else:
@@ -635,6 +684,18 @@ class _Lowerer:
                 self.blobs[L.blobs["weight"]] = packed
                 if self.keep_f32:
                     self.debug_f32[L.blobs["weight"]] = t.reshape(cout, -1)
+                if L.pre is not None and L.pre.binop == 0:
+                    # the transform reads whole 8-channel chunks up to cblocks * cb;
+                    # an identity scale where only a shift / an activation is folded
+                    for role, v in (("pre_alpha", L.pre.alpha if L.pre.alpha is not None
+                                     else np.ones(cin, np.float32)), ("pre_beta", L.pre.beta)):
+                        if v is None:
+                            continue
+                        arr = np.zeros(cblocks * cb, dtype=np.float32)
+                        arr[:len(v)] = v
+                        key = f"{L.nodes[0]}.{role}"
+                        self.blobs[key] = arr
+                        L.blobs[role] = key
             for role in ("alpha", "beta"):
                 v = getattr(L.epi, role)
                 if v is not None:
@@ -725,6 +786,11 @@ GEMM_M2 = os.environ.get("DFX_GEMM_M2", "1") != "0"     # A/B switch for 256-row
 # the splitk launch overlaps the GEMM tail under PDL, cluster co-scheduling does not);
 # "fixup" = last-arriving CTA reduces (A/B)
 SPLITK_MODE = os.environ.get("DFX_SPLITK", "kernel")
+# fold elementwise producers into the A operand of 1x1 convs (DFX_FOLD_PRE=1: on, A/B).
+# Off by default: the in-smem rewrite serialises each pipeline stage behind 4-6
+# transform warps and measured slower than the separate bandwidth-bound pass
+# (4-model batch 1 2.72 vs 2.52 ms, batch 32 17.1 vs 12.5 ms, 150 launches fewer)
+FOLD_PRE = os.environ.get("DFX_FOLD_PRE", "0") == "1"
 SPLITK_CLUSTER_MAX = 8
 
 
@@ -754,6 +820,7 @@ def gemm_tiling(geom: dict, n: int, p: int, q: int, sm_count: int = 148) -> dict
     # matters more there than the halved weight traffic: measured on 3x3 64->256 at
     # batch 32, 115 us m2 vs 80 us persistent; VGG's K=4608 layers keep m2)
     m2 = int(GEMM_M2 and splits == 1 and bn >= 128 and m_tiles >= 2 and stages >= 24
+             and not geom.get("pre")
              and math.ceil(m_tiles / 2) * nt >= sm_count and waves2 * 1.6 < waves1)
     tiles = (math.ceil(m_tiles / 2) if m2 else m_tiles) * nt * splits
     # cluster split-K when the splits fit one portable cluster; wider splits keep the

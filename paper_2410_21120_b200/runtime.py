@@ -27,7 +27,7 @@ DT_BF16, DT_F16 = 0, 1
 DTYPES = {"bf16": DT_BF16, "fp16": DT_F16}
 ABI_VERSION = 3
 
-i32, i64, u64, vp = C.c_int32, C.c_int64, C.c_uint64, C.c_void_p
+i32, i64, u64, vp, u8 = C.c_int32, C.c_int64, C.c_uint64, C.c_void_p, C.c_uint8
 fptr = C.POINTER(C.c_float)
 
 
@@ -50,7 +50,9 @@ class GemmDesc(C.Structure):
                 ("pad_h", i32), ("pad_w", i32), ("cb", i32), ("cblocks", i32), ("ksteps", i32),
                 ("kpack", i32), ("stages", i32), ("splits", i32), ("stages_per_split", i32),
                 ("bn", i32), ("cout", i32), ("tile_begin", i32), ("tiles", i32), ("m2", i32),
-                ("out", View), ("epi", Epilogue), ("ws", vp), ("counters", vp), ("_pad1", i64 * 2)]
+                ("out", View), ("epi", Epilogue), ("ws", vp), ("counters", vp),
+                ("pre_scale", vp), ("pre_shift", vp), ("pre_mode", i32), ("pre_act", i32),
+                ("pre_cin", i32), ("pre_pitch", i32), ("_pad2", u8 * 48)]
 
 
 class GemmLaunch(C.Structure):

@@ -102,6 +102,17 @@ class Emulator:
         w = packed.reshape(g["cout"], g["kh"], g["kw"], g["cblocks"] * g["cb"])[..., :g["cin"]]
         if self.round:
             x = self.q(x)
+        if L.pre is not None:                   # A prologue transform, rounded like the smem rewrite
+            pe = L.pre
+            if pe.binop == 2:
+                x = x * self.view(pe.other)[:, 0:1, 0:1, :]
+            else:
+                if pe.alpha is not None:
+                    x = x * pe.alpha
+                if pe.beta is not None:
+                    x = x + pe.beta
+                x = _act(pe.act1, x)
+            x = self.q(x) if self.round else x.astype(np.float32)
         n, h, wd, c = x.shape
         xp = np.pad(x, ((0, 0), (g["ph"], g["ph"]), (g["pw"], g["pw"]), (0, 0)))
         out = self.view(L.dst)

@@ -298,3 +298,20 @@ def test_conv_layer_cluster_splitk(cin, h, w, cout, k, s, p, n, monkeypatch):
     t = lower.gemm_tiling(dict(cout=cout, cb=cb, ksteps=k * k * (-(-cin // cb)), sh=s, sw=s), n, oh, oh)
     assert t["csplit"] == 1 and 2 <= t["splits"] <= 8
     test_conv_layer(cin, h, w, cout, k, s, p, n)
+
+
+# A-operand prologue transform (DFX_FOLD_PRE=1, lower.fold_pre_transforms): DenseNet's
+# pre-activation BN + ReLU (mode 1) and the SE channel scale (mode 2) folded into the
+# 1x1 conv that consumes them; freshly built models so the program cache misses
+@pytest.mark.parametrize("name,mode", [("densenet161", 0), ("mobilenet_v3_large", 2)])
+def test_fold_pre_transform(name, mode, monkeypatch):
+    from paper_2410_21120_b200 import lower, zoo
+    monkeypatch.setattr(lower, "FOLD_PRE", True)
+    g, w = zoo.build(name)
+    prog = lower.lower_member(g, w)
+    assert {L.pre.binop for L in prog.launches if L.pre is not None} == {mode}
+    rng = np.random.default_rng(5)
+    xs = rng.standard_normal((2,) + tuple(g.input_spec.dims)).astype(np.float32)
+    got = [t.values for t in run_batch(g, w, [Tensor(g.input_spec, x) for x in xs])]
+    ref = run_fast(g, w, xs)
+    assert rel(got, ref) < TOL
