@@ -75,10 +75,11 @@ GEMM_PERSIST = os.environ.get("DFX_GEMM_PERSIST", "1") != "0"    # A/B switch
 # them in smem per CTA (dfx_fused.cu; apply bit 1)
 SE_UNSTAGED_BATCH = int(os.environ.get("DFX_SE_UNSTAGED_BATCH", "8"))
 # node priorities by member chain length (DFX_PRIORITY=0: off, A/B) for latency-bound
-# (small-batch) instances: 4-model batch 1 2.63 -> 2.48 ms, 8-model mixed 3.37 ->
-# 2.91 ms; at batch 32 the chain length is no proxy for work (12.3 -> 13.3 ms), so off
+# (every member batch <= 2) instances: 4-model batch 1 2.63 -> 2.48 ms, 8-model batch 1
+# 3.37 -> 2.91 ms; with larger or mixed batches chain length is no proxy for work
+# (4-model batch 32 12.3 -> 13.3 ms, 8-model batches 1..8 6.6 -> 7.3 ms), so off
 NODE_PRIORITY = os.environ.get("DFX_PRIORITY", "1") != "0"
-PRIORITY_MAX_BATCH = 8
+PRIORITY_MAX_BATCH = 2
 GEMM_DRAIN_STAGED = os.environ.get("DFX_GEMM_DRAIN", "direct") == "staged"   # A/B switch
 
 
