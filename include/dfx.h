@@ -71,7 +71,9 @@ typedef enum dfx_op {
                           one 8-CTA cluster per image sharing data over DSMEM */
   DFX_OP_LN = 10,      /* layer norm over channels of token rows (+ token select) */
   DFX_OP_TOKENS = 11,  /* patch grid -> [class token; patches] + pos_embedding */
-  DFX_OP_ATTN = 12     /* multi-head softmax attention over packed q|k|v rows */
+  DFX_OP_ATTN = 12,    /* multi-head softmax attention over packed q|k|v rows */
+  DFX_OP_DWSE = 13     /* depthwise conv + BN/act -> squeeze-excitation gate -> channel
+                          scale, one cluster per image (an MBConv block's middle) */
 } dfx_op;
 
 typedef enum dfx_dtype {
@@ -232,6 +234,23 @@ typedef struct dfx_se_params {
   const float* b2;                     /* may be NULL */
   int32_t cr, act1, act2, apply;
 } dfx_se_params;
+
+/* Depthwise conv (+ epi: folded BN, act) -> SE gate (as dfx_se_params) -> scale, in
+ * ONE launch: a 16-CTA cluster per image, CTA r owns a channel slice; the slice's
+ * depthwise output stays in shared memory (16-bit, rounded as a stored tensor would
+ * be), is pooled there, and is scaled by the gate on the way out.
+ * out[n,p,q,c] = dw[n,p,q,c] * gate[n,c]. */
+typedef struct dfx_dwse_params {
+  dfx_view in, out;                    /* out.c == in.c; out spatial = dw output */
+  const float* dw_weight;              /* [kh*kw][c] fp32 taps */
+  int32_t kh, kw, stride_h, stride_w, pad_h, pad_w;
+  dfx_epilogue dw_epi;                 /* affine + act1 only */
+  const void* w1;                      /* fc1^T [c][cr], 16-bit */
+  const float* b1;
+  const void* w2;                      /* fc2 [c][cr], 16-bit */
+  const float* b2;
+  int32_t cr, act1, act2, staged;      /* staged: FC slices in smem (small batch) */
+} dfx_dwse_params;
 
 /* Token tensors (ViT) are views with h = 1, w = L tokens, c = channels.
  * out[n, 0, t, c] = norm ? (x - mean_t) * rsqrt(var_t + eps) * gamma[c] + beta[c]

@@ -29,6 +29,7 @@ template <typename T> __global__ void in_kernel(const __grid_constant__ dfx_in_p
 template <typename T> __global__ void in_im2col_kernel(const __grid_constant__ dfx_in_params P);
 template <typename T> __global__ void out_kernel(const __grid_constant__ dfx_out_params P);
 template <typename T, int CL> __global__ void se_kernel(const __grid_constant__ dfx_se_params P);
+template <typename T> __global__ void dwse_kernel(const __grid_constant__ dfx_dwse_params P);
 template <typename T> __global__ void ln_kernel(const __grid_constant__ dfx_ln_params P);
 template <typename T> __global__ void tokens_kernel(const __grid_constant__ dfx_tokens_params P);
 template <typename T> __global__ void attn_kernel(const __grid_constant__ dfx_attn_params P);
@@ -294,6 +295,21 @@ int config_for(int op, const void* params, size_t size, LaunchCfg* c) {
         return fail(DFX_E_UNSUPPORTED, "se: c=%d cr=%d needs %zu B of smem", p->in.c, p->cr, c->smem);
       return DFX_OK;
     }
+    case DFX_OP_DWSE: {
+      NEED(dfx_dwse_params);
+      const auto* p = static_cast<const dfx_dwse_params*>(params);
+      if (p->in.c > 4096 || (p->in.c & 7) || p->cr > 512 || p->cr < 1 || p->out.c != p->in.c ||
+          p->out.n != p->in.n || ((p->in.coff | p->out.coff | p->in.pitch | p->out.pitch) & 7) ||
+          p->dw_epi.binop != DFX_BIN_NONE)
+        return fail(DFX_E_UNSUPPORTED, "dwse: c=%d cr=%d / views beyond the fused kernel's limits",
+                    p->in.c, p->cr);
+      c->func = DFX_PICK(dwse_kernel, p->in.dtype);
+      c->grid = dim3(16u, unsigned(p->in.n));
+      c->smem = size_t(dfx::dwse_smem_bytes(p->in.c, p->cr, p->out.h * p->out.w, p->staged));
+      if (c->smem > size_t(dfx::kSeSmemBudget))
+        return fail(DFX_E_UNSUPPORTED, "dwse: %zu B of smem", c->smem);
+      return DFX_OK;
+    }
     case DFX_OP_LN: {
       NEED(dfx_ln_params);
       const auto* p = static_cast<const dfx_ln_params*>(params);
@@ -373,7 +389,8 @@ int dfx_sizeof(const char* name) {
            {"dfx_se_params", sizeof(dfx_se_params)},
            {"dfx_ln_params", sizeof(dfx_ln_params)},
            {"dfx_tokens_params", sizeof(dfx_tokens_params)},
-           {"dfx_attn_params", sizeof(dfx_attn_params)}};
+           {"dfx_attn_params", sizeof(dfx_attn_params)},
+           {"dfx_dwse_params", sizeof(dfx_dwse_params)}};
   for (auto& e : t)
     if (!strcmp(e.n, name)) return e.s;
   return -1;
@@ -403,6 +420,9 @@ int dfx_init(int device) {
       CK(cudaFuncSetAttribute(se_func(dt, cl), cudaFuncAttributeMaxDynamicSharedMemorySize,
                               dfx::kSeSmemBudget));
     CK(cudaFuncSetAttribute(se_func(dt, 16), cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    CK(cudaFuncSetAttribute(DFX_PICK(dwse_kernel, dt), cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    CK(cudaFuncSetAttribute(DFX_PICK(dwse_kernel, dt), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            dfx::kSeSmemBudget));
     CK(cudaFuncSetAttribute(DFX_PICK(attn_kernel, dt), cudaFuncAttributeMaxDynamicSharedMemorySize,
                             dfx::attn_smem_bytes(dfx::kAttnMaxL)));
   }

@@ -468,6 +468,11 @@ constexpr int kSeSmemBudget = 190 * 1024;
 __host__ __device__ inline int se_chan_slice(int C, int cl) { return ((C + cl * 8 - 1) / (cl * 8)) * 8; }
 __host__ __device__ inline int se_hid_slice(int Cr, int cl) { return (Cr + cl - 1) / cl; }
 // dynamic smem of one CTA: its channel rows of fc1^T and of fc2 (16-bit, [rows][Cr])
+// dynamic smem of a dwse_kernel CTA: (staged) FC slices + its 16-bit dw tile [HWo][slice]
+__host__ __device__ inline int dwse_smem_bytes(int C, int Cr, int hwo, int staged) {
+  const int cs = ((C + 16 * 8 - 1) / (16 * 8)) * 8;
+  return (staged ? 2 * (((cs * Cr * 2) + 15) & ~15) : 0) + ((hwo * cs * 2 + 15) & ~15);
+}
 __host__ __device__ inline int se_smem_bytes(int C, int Cr, int cl) {
   return 2 * (((se_chan_slice(C, cl) * Cr * 2) + 15) & ~15);
 }

@@ -268,6 +268,165 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kSeThreads)
   if (threadIdx.x == 0) DFX_TL(8);
 }
 
+// ---------------------------------------------------------------- dwse_kernel
+// An MBConv block's middle -- depthwise conv (+ folded BN + act) -> squeeze-
+// excitation gate -> channel scale -- as ONE launch (the three were dwconv,
+// se and ew launches, ~14 us of dependent chain per block at batch 1).  One
+// 16-CTA cluster per image; CTA r owns channel slice [c_lo, c_hi):
+//   0. FC weight slices bulk-copied to smem before griddepcontrol.wait (small
+//      batch, P.staged), as in se_kernel;
+//   1. depthwise conv of its slice over all output pixels, epilogue, rounded to
+//      the 16-bit storage type into an smem tile [HWo][slice] -- the tensor the
+//      unfused path would have stored;
+//   2. pools the tile per channel (fixed order), fc1 partial sums over its
+//      channels, cluster.sync, rank-order DSMEM reduction, act1 (se_kernel 2-3);
+//   3. its channels' gate (+b2, act2), rounded like a stored gate;
+//   4. out = tile * gate, 16-B stores; cluster.sync so peers' smem stays alive.
+constexpr int kDwseCL = 16;
+
+template <typename T>
+__global__ void __cluster_dims__(kDwseCL, 1, 1) __launch_bounds__(kSeThreads)
+    dwse_kernel(const __grid_constant__ dfx_dwse_params P) {
+  constexpr int CL = kDwseCL;
+  __shared__ float pooled[kSeMaxSlice];
+  __shared__ float partial[kSeMaxCr];
+  __shared__ float hidden[kSeMaxCr];
+  __shared__ float red[kSeThreads];
+  __shared__ __align__(8) uint64_t wbar;
+  extern __shared__ __align__(16) uint8_t wsm[];
+  cg::cluster_group cluster = cg::this_cluster();
+  const int rank = int(cluster.block_rank());
+  const int n = blockIdx.y;
+  const dfx_view& in = P.in;
+  const dfx_view& out = P.out;
+  const int C = in.c, Cr = P.cr;
+  const int OW = out.w, HWo = out.h * out.w;
+  const int cs = se_chan_slice(C, CL);
+  const int c_lo = min(C, rank * cs), c_hi = min(C, c_lo + cs);
+  const int nch = c_hi - c_lo;                       // multiple of 8 (C % 8 == 0)
+  const int G = nch >> 3;
+  const T* w1g = reinterpret_cast<const T*>(P.w1);
+  const T* w2g = reinterpret_cast<const T*>(P.w2);
+  const bool staged = P.staged && (Cr & 7) == 0;
+  const int sb = ((cs * Cr * 2) + 15) & ~15;
+  const T* w1 = staged ? reinterpret_cast<const T*>(wsm) : w1g + int64_t(c_lo) * Cr;
+  const T* w2 = staged ? reinterpret_cast<const T*>(wsm + sb) : w2g + int64_t(c_lo) * Cr;
+  T* tile = reinterpret_cast<T*>(wsm + (staged ? 2 * sb : 0));     // [HWo][nch]
+
+  if (threadIdx.x == 0) {
+    mbar_init(&wbar, 1);
+    fence_barrier_init();
+    const uint32_t bytes = uint32_t(nch) * Cr * 2;
+    if (staged && bytes) {
+      mbar_arrive_expect_tx(&wbar, 2 * bytes);
+      bulk_load(wsm, w1g + int64_t(c_lo) * Cr, bytes, &wbar);
+      bulk_load(wsm + sb, w2g + int64_t(c_lo) * Cr, bytes, &wbar);
+    } else {
+      mbar_arrive(&wbar);
+    }
+  }
+  griddep_wait();
+  griddep_launch();
+
+  // ---- 1. depthwise conv of this slice -> smem tile (16-bit, as a stored tensor)
+  const int kh = P.kh, kw = P.kw;
+  for (int item = threadIdx.x; item < HWo * G; item += kSeThreads) {
+    const int p = item / G, g = item - p * G;
+    const int c = c_lo + g * 8;
+    const int oh = p / OW, ow = p - oh * OW;
+    const int h0 = oh * P.stride_h - P.pad_h, w0 = ow * P.stride_w - P.pad_w;
+    float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    for (int ki = 0; ki < kh; ++ki) {
+      const int h = h0 + ki;
+      if (h < 0 || h >= in.h) continue;
+      for (int kj = 0; kj < kw; ++kj) {
+        const int w = w0 + kj;
+        if (w < 0 || w >= in.w) continue;
+        float x[8];
+        ld8<T>(in.base, view_index(in, n, h, w, c), x);
+        const float4* wt = reinterpret_cast<const float4*>(P.dw_weight + (ki * kw + kj) * C + c);
+        const float4 lo = __ldg(wt), hi = __ldg(wt + 1);
+        acc[0] = fmaf(lo.x, x[0], acc[0]); acc[1] = fmaf(lo.y, x[1], acc[1]);
+        acc[2] = fmaf(lo.z, x[2], acc[2]); acc[3] = fmaf(lo.w, x[3], acc[3]);
+        acc[4] = fmaf(hi.x, x[4], acc[4]); acc[5] = fmaf(hi.y, x[5], acc[5]);
+        acc[6] = fmaf(hi.z, x[6], acc[6]); acc[7] = fmaf(hi.w, x[7], acc[7]);
+      }
+    }
+    epilogue8<T>(P.dw_epi, acc, 0, n, c);
+    *reinterpret_cast<uint4*>(tile + p * nch + g * 8) = pack8<T>(acc);
+  }
+  __syncthreads();
+
+  // ---- 2. pool the tile per channel (pixel order, two interleaved partial sums)
+  for (int k = threadIdx.x; k < nch; k += kSeThreads) {
+    float s0 = 0.f, s1 = 0.f;
+    int p = 0;
+    for (; p + 1 < HWo; p += 2) {
+      s0 += Elt<T>::to_f(tile[p * nch + k]);
+      s1 += Elt<T>::to_f(tile[(p + 1) * nch + k]);
+    }
+    if (p < HWo) s0 += Elt<T>::to_f(tile[p * nch + k]);
+    pooled[k] = (s0 + s1) * (1.0f / float(HWo));
+  }
+  if (threadIdx.x == 0) mbar_wait(&wbar, 0);
+  __syncthreads();
+  // fc1 partial sums over this CTA's channels (one hidden unit per thread pass)
+  for (int j = threadIdx.x; j < Cr; j += kSeThreads) {
+    float s0 = 0.f, s1 = 0.f;
+    int k = 0;
+    for (; k + 1 < nch; k += 2) {
+      s0 = fmaf(Elt<T>::to_f(w1[int64_t(k) * Cr + j]), pooled[k], s0);
+      s1 = fmaf(Elt<T>::to_f(w1[int64_t(k + 1) * Cr + j]), pooled[k + 1], s1);
+    }
+    if (k < nch) s0 = fmaf(Elt<T>::to_f(w1[int64_t(k) * Cr + j]), pooled[k], s0);
+    partial[j] = s0 + s1;
+  }
+  cluster.sync();
+  for (int j = threadIdx.x; j < Cr; j += kSeThreads) {
+    float s = 0.f;
+#pragma unroll
+    for (int r = 0; r < CL; ++r) s += cluster.map_shared_rank(partial, r)[j];
+    float a[8] = {s + (P.b1 ? P.b1[j] : 0.f), 0, 0, 0, 0, 0, 0, 0};
+    act8(P.act1, a);
+    hidden[j] = a[0];
+  }
+  __syncthreads();
+  // ---- 3. gate of this CTA's channels, rounded like a stored 16-bit gate
+  for (int k = threadIdx.x; k < nch; k += kSeThreads) {
+    const T* row = w2 + int64_t(k) * Cr;
+    float s0 = 0.f, s1 = 0.f;
+    if ((Cr & 7) == 0) {
+      for (int j = 0; j < Cr; j += 8) {
+        float wv[8];
+        ld8<T>(row, j, wv);
+        s0 = fmaf(wv[0], hidden[j], s0); s1 = fmaf(wv[1], hidden[j + 1], s1);
+        s0 = fmaf(wv[2], hidden[j + 2], s0); s1 = fmaf(wv[3], hidden[j + 3], s1);
+        s0 = fmaf(wv[4], hidden[j + 4], s0); s1 = fmaf(wv[5], hidden[j + 5], s1);
+        s0 = fmaf(wv[6], hidden[j + 6], s0); s1 = fmaf(wv[7], hidden[j + 7], s1);
+      }
+    } else {
+      for (int j = 0; j < Cr; ++j) s0 = fmaf(Elt<T>::to_f(row[j]), hidden[j], s0);
+    }
+    float a[8] = {s0 + s1 + (P.b2 ? P.b2[c_lo + k] : 0.f), 0, 0, 0, 0, 0, 0, 0};
+    act8(P.act2, a);
+    red[k] = Elt<T>::to_f(Elt<T>::from_f(a[0]));
+  }
+  __syncthreads();
+  // ---- 4. out = tile * gate
+  for (int item = threadIdx.x; item < HWo * G; item += kSeThreads) {
+    const int p = item / G, g = item - p * G;
+    float x[8];
+    unpack8<T>(*reinterpret_cast<const uint4*>(tile + p * nch + g * 8), x);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) x[k] *= red[g * 8 + k];
+    st8<T>(out.base, view_pixel_index(out, int64_t(n) * HWo + p, c_lo + g * 8), x);
+  }
+  cluster.sync();        // peers finished reading this CTA's partial[]
+}
+
+template __global__ void dwse_kernel<__nv_bfloat16>(const __grid_constant__ dfx_dwse_params);
+template __global__ void dwse_kernel<__half>(const __grid_constant__ dfx_dwse_params);
+
 #define DFX_SE_INST(T, CL) template __global__ void se_kernel<T, CL>(const __grid_constant__ dfx_se_params);
 DFX_SE_INST(__nv_bfloat16, 8)
 DFX_SE_INST(__half, 8)

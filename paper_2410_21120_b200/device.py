@@ -30,7 +30,7 @@ import numpy as np
 
 from . import runtime as rt
 from .graph_ir import LiveInterval
-from .lower import (ATTN, COPY, DWCONV, EW, GAP, GEMM, LN, POOL, SE, TOKENS, MemberProgram,
+from .lower import (ATTN, COPY, DWCONV, DWSE, EW, GAP, GEMM, LN, POOL, SE, TOKENS, MemberProgram,
                     gemm_tiling, lower_member)
 from .planner import first_fit
 
@@ -468,6 +468,11 @@ class ExecInstance:
         elif L.kind == SE:
             g = L.geom
             info.update(flops=4 * n * g["c"] * g["cr"], bytes=in_b + out_b + 2 * 2 * g["c"] * g["cr"])
+        elif L.kind == DWSE:
+            g = L.geom
+            out = prog.values[L.dst]
+            info.update(flops=2 * n * out.h * out.w * out.c * g["kh"] * g["kw"] + 4 * n * g["c"] * g["cr"],
+                        bytes=in_b + out_b + out.c * g["kh"] * g["kw"] * 4 + 2 * 2 * g["c"] * g["cr"])
         elif L.kind == ATTN:
             g = L.geom
             info.update(flops=4 * n * g["seq"] * g["seq"] * g["c"], bytes=in_b + out_b)
@@ -621,6 +626,15 @@ class ExecInstance:
                                         addr("w2"), addr("b2"), geo["cr"], rt.ACT[geo["act1"]],
                                         rt.ACT[geo["act2"]],
                                         geo.get("apply", 0) | (2 if n >= SE_UNSTAGED_BATCH else 0))
+        elif L.kind == DWSE:
+            geo = L.geom
+            addr = (lambda r: arena.addr(m, L.blobs[r]) if r in L.blobs else None)
+            dep = self._epi(m, prog, L, n)
+            yield rt.OP_DWSE, rt.DwseParams(src, self._view(m, prog, L.dst, n), addr("weight"),
+                                            geo["kh"], geo["kw"], geo["sh"], geo["sw"], geo["ph"], geo["pw"],
+                                            dep, addr("w1"), addr("b1"), addr("w2"), addr("b2"), geo["cr"],
+                                            rt.ACT[geo["act1"]], rt.ACT[geo["act2"]],
+                                            int(n < SE_UNSTAGED_BATCH))
         else:
             raise AssertionError(L.kind)
 

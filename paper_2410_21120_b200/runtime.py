@@ -20,7 +20,7 @@ PKG = Path(__file__).resolve().parent
 LIB_PATH = PKG / "libdfx.so"
 
 (OP_GEMM, OP_SPLITK, OP_DWCONV, OP_POOL, OP_GAP, OP_EW, OP_IN, OP_OUT, OP_SE, OP_LN, OP_TOKENS,
- OP_ATTN) = range(1, 13)
+ OP_ATTN, OP_DWSE) = range(1, 14)
 ACT = {None: 0, "relu": 1, "hardswish": 2, "hardsigmoid": 3, "silu": 4, "sigmoid": 5, "gelu": 6}
 BIN_NONE, BIN_ADD, BIN_SCALE = 0, 1, 2
 DT_BF16, DT_F16 = 0, 1
@@ -100,6 +100,13 @@ class SeParams(C.Structure):
                 ("cr", i32), ("act1", i32), ("act2", i32), ("apply", i32)]
 
 
+class DwseParams(C.Structure):
+    _fields_ = [("inp", View), ("out", View), ("dw_weight", vp), ("kh", i32), ("kw", i32),
+                ("stride_h", i32), ("stride_w", i32), ("pad_h", i32), ("pad_w", i32),
+                ("dw_epi", Epilogue), ("w1", vp), ("b1", vp), ("w2", vp), ("b2", vp),
+                ("cr", i32), ("act1", i32), ("act2", i32), ("staged", i32)]
+
+
 class LnParams(C.Structure):
     _fields_ = [("inp", View), ("out", View), ("gamma", vp), ("beta", vp), ("eps", C.c_float),
                 ("norm", i32), ("_pad", i32 * 2)]
@@ -119,12 +126,12 @@ STRUCTS = {
     "dfx_dwconv_params": DwconvParams, "dfx_pool_params": PoolParams,
     "dfx_gap_params": GapParams, "dfx_ew_params": EwParams, "dfx_in_params": InParams,
     "dfx_out_params": OutParams, "dfx_se_params": SeParams, "dfx_ln_params": LnParams,
-    "dfx_tokens_params": TokensParams, "dfx_attn_params": AttnParams,
+    "dfx_tokens_params": TokensParams, "dfx_attn_params": AttnParams, "dfx_dwse_params": DwseParams,
 }
 OP_PARAMS = {OP_GEMM: GemmLaunch, OP_SPLITK: SplitKParams, OP_DWCONV: DwconvParams,
              OP_POOL: PoolParams, OP_GAP: GapParams, OP_EW: EwParams, OP_IN: InParams,
              OP_OUT: OutParams, OP_SE: SeParams, OP_LN: LnParams, OP_TOKENS: TokensParams,
-             OP_ATTN: AttnParams}
+             OP_ATTN: AttnParams, OP_DWSE: DwseParams}
 
 # every symbol include/dfx.h declares (tests check the .so exports all of them)
 EXPORTS = (

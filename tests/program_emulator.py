@@ -137,6 +137,38 @@ class Emulator:
                 acc += xp[:, r:r + P * g["sh"]:g["sh"], s:s + Q * g["sw"]:g["sw"], :] * taps[r, s]
         self.store(out, self.epilogue(L, acc))
 
+    def do_dwse(self, L):
+        """depthwise conv + epilogue -> 16-bit tile -> SE gate (rounded) -> tile * gate."""
+        g = L.geom
+        x = self.view(L.src)
+        taps = self.p.blobs[L.blobs["weight"]].reshape(g["kh"], g["kw"], -1)
+        xp = np.pad(x, ((0, 0), (g["ph"], g["ph"]), (g["pw"], g["pw"]), (0, 0)))
+        P, Q = self.view(L.dst).shape[1:3]
+        acc = np.zeros((x.shape[0], P, Q, x.shape[3]), np.float32)
+        for r in range(g["kh"]):
+            for s in range(g["kw"]):
+                acc += xp[:, r:r + P * g["sh"]:g["sh"], s:s + Q * g["sw"]:g["sw"], :] * taps[r, s]
+        e = L.epi
+        if e.alpha is not None:
+            acc = acc * e.alpha
+        if e.beta is not None:
+            acc = acc + e.beta
+        t = _act(e.act1, acc)
+        t = self.q(t) if self.round else t
+        pooled = t.mean(axis=(1, 2))
+        w1 = storage_bits_to_f32(self.p.blobs[L.blobs["w1"]], self.p.precision).reshape(g["c"], g["cr"])
+        w2 = storage_bits_to_f32(self.p.blobs[L.blobs["w2"]], self.p.precision).reshape(g["c"], g["cr"])
+        h = pooled @ w1
+        if "b1" in L.blobs:
+            h = h + self.p.blobs[L.blobs["b1"]][:h.shape[1]]
+        h = _act(g["act1"], h)
+        gate = h @ w2.T
+        if "b2" in L.blobs:
+            gate = gate + self.p.blobs[L.blobs["b2"]][:gate.shape[1]]
+        gate = _act(g["act2"], gate)
+        gate = self.q(gate) if self.round else gate
+        self.store(self.view(L.dst), t * gate[:, None, None, :])
+
     def do_pool(self, L):
         g = L.geom
         x = self.view(L.src)

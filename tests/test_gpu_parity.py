@@ -315,3 +315,20 @@ def test_fold_pre_transform(name, mode, monkeypatch):
     got = [t.values for t in run_batch(g, w, [Tensor(g.input_spec, x) for x in xs])]
     ref = run_fast(g, w, xs)
     assert rel(got, ref) < TOL
+
+
+# dw -> SE -> scale as one cluster launch (DFX_FUSE_DWSE=1, dfx_fused.cu dwse_kernel):
+# MobileNetV3-L (3x3 / 5x5, stride 1 / 2, hardsigmoid gates) and EfficientNetV2-L's
+# MBConv blocks at a small and a multi-image batch
+@pytest.mark.parametrize("name,n", [("mobilenet_v3_large", 3), ("efficientnet_v2_l", 2)])
+def test_fused_dw_se(name, n, monkeypatch):
+    from paper_2410_21120_b200 import lower, zoo
+    monkeypatch.setattr(lower, "FUSE_DWSE", True)
+    g, w = zoo.build(name)
+    prog = lower.lower_member(g, w)
+    assert sum(L.kind == lower.DWSE for L in prog.launches) in (8, 61)
+    rng = np.random.default_rng(11)
+    xs = rng.standard_normal((n,) + tuple(g.input_spec.dims)).astype(np.float32)
+    got = [t.values for t in run_batch(g, w, [Tensor(g.input_spec, x) for x in xs])]
+    ref = run_fast(g, w, xs)
+    assert rel(got, ref) < TOL
