@@ -219,47 +219,62 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     DFX_TL(1);                                     // weight prefetch issued
     griddep_wait();
     DFX_TL(2);                                     // dependency resolved
-    for (int it = 0; it < npre; ++it) {
-      const int st = st_begin + it;
+    // k-step cursor (channel block, s, r) advanced incrementally: the producer is
+    // ONE thread, and integer divisions per k-step (~20-40 instructions each) made
+    // its issue loop slower than the MMAs it feeds
+    int cblk, sc, rc;
+    {
+      const int k = st_begin * kpack, rs = k / cblocks;
+      cblk = k - rs * cblocks;
+      rc = rs / S;
+      sc = rs - rc * S;
+    }
+    int k0 = st_begin * kpack;
+    for (int it = 0; it < npre; ++it, k0 += kpack) {
       uint8_t* a_dst = slots + it * slot_bytes;
-      const int k0 = st * kpack;
       const int nk = min(kpack, ksteps - k0);
       for (int j = 0; j < nk; ++j) {
-        const int kstep = k0 + j;
-        const int rs = kstep / cblocks;
-        const int cblk = kstep - rs * cblocks;
-        const int r = rs / S;
-        const int s = rs - r * S;
 #pragma unroll
         for (int h = 0; h < 1 + M2; ++h)
           if (h < nhalf)
-            tma_load_4d(a_dst + h * kStageABytes + j * sub_a, tma, &hdr->full[it], cblk * cb, qb[h] + s,
-                        pb[h] + r, n0h[h]);
+            tma_load_4d(a_dst + h * kStageABytes + j * sub_a, tma, &hdr->full[it], cblk * cb, qb[h] + sc,
+                        pb[h] + rc, n0h[h]);
+        if (++cblk == cblocks) {
+          cblk = 0;
+          if (++sc == S) {
+            sc = 0;
+            ++rc;
+          }
+        }
       }
     }
     DFX_TL(29);                                    // all prefetched stages' A loads issued
-    int it = npre;
-    for (int st = st_begin + npre; st < st_end; ++st, ++it) {
-      const int slot = it % nslots;
-      const uint32_t par = (it / nslots) & 1;
+    int slot = npre == nslots ? 0 : npre;
+    uint32_t par = npre == nslots ? 1u : 0u;
+    for (int st = st_begin + npre; st < st_end; ++st, k0 += kpack) {
       mbar_wait(&hdr->empty[slot], par ^ 1);
       uint8_t* a_dst = slots + slot * slot_bytes;
       uint8_t* b_dst = a_dst + a_bytes;
-      const int k0 = st * kpack;
       const int nk = min(kpack, ksteps - k0);
       mbar_arrive_expect_tx(&hdr->full[slot], nk * (box_a_bytes + uint32_t(sub_b)));
       for (int j = 0; j < nk; ++j) {
-        const int kstep = k0 + j;
-        const int rs = kstep / cblocks;
-        const int cblk = kstep - rs * cblocks;
-        const int r = rs / S;
-        const int s = rs - r * S;
 #pragma unroll
         for (int h = 0; h < 1 + M2; ++h)
           if (h < nhalf)
-            tma_load_4d(a_dst + h * kStageABytes + j * sub_a, tma, &hdr->full[slot], cblk * cb, qb[h] + s,
-                        pb[h] + r, n0h[h]);
-        tma_load_2d(b_dst + j * sub_b, tmb, &hdr->full[slot], kstep * cb, co_base);
+            tma_load_4d(a_dst + h * kStageABytes + j * sub_a, tma, &hdr->full[slot], cblk * cb, qb[h] + sc,
+                        pb[h] + rc, n0h[h]);
+        tma_load_2d(b_dst + j * sub_b, tmb, &hdr->full[slot], (k0 + j) * cb, co_base);
+        if (++cblk == cblocks) {
+          cblk = 0;
+          if (++sc == S) {
+            sc = 0;
+            ++rc;
+          }
+        }
+      }
+      if (++slot == nslots) {
+        slot = 0;
+        par ^= 1u;
       }
     }
   } else if (warp == 1 && lane == 0) {
@@ -270,9 +285,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     uint32_t accumulate = 0;
     int it = 0;
     uint64_t* const gate_bar = D.pre_mode ? hdr->ready : hdr->full;   // pre_mode: wait for the transform
+    int slot = 0;
+    uint32_t par = 0;
     for (int st = st_begin; st < st_end; ++st, ++it) {
-      const int slot = it % nslots;
-      const uint32_t par = (it / nslots) & 1;
       mbar_wait(&gate_bar[slot], par);
       if (it == 0) DFX_TL(3);                      // first stage landed
       if (it > 0 && it < 9) DFX_TL(12 + it);       // later stages landed (13..20)
@@ -301,6 +316,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       if (it < 7) DFX_TC(44 + 3 * it);
       if (it < 8) DFX_TL(21 + it);                 // stage's MMAs issued (21..28)
       umma_commit(&hdr->empty[slot]);
+      if (++slot == nslots) {
+        slot = 0;
+        par ^= 1u;
+      }
     }
     umma_commit(&hdr->accum);
     DFX_TL(4);                                     // last MMA issued

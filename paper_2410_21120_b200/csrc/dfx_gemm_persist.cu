@@ -104,20 +104,22 @@ __global__ void __launch_bounds__(kPersistThreads, 1)
       const uint32_t box_a_bytes = uint32_t(cb) * 2u * tq * tp * tn;
       const void* tma = gd->tmap_a;
       const void* tmb = gd->tmap_b;
-      int it = 0;
+      // slot / phase and the k-step cursor (channel block, s, r) advance
+      // incrementally: this ONE thread feeds the MMA, and per-k-step integer
+      // divisions made its issue loop the bottleneck of short-K layers
+      int slot = 0, filled = 0;
+      uint32_t par = 0;
       bool waited = false;
       for (int tile = blockIdx.x; tile < total; tile += grid) {
         const int mi = tile % mt_total, ntile = tile / mt_total;
         const int n0 = (mi / (mt_q * mt_p)) * tn, p0 = ((mi / mt_q) % mt_p) * tp, q0 = (mi % mt_q) * tq;
         const int qbase = q0 * D.stride_w - D.pad_w, pbase = p0 * D.stride_h - D.pad_h;
         const int co_base = ntile * bn;
-        for (int st = 0; st < stages; ++st, ++it) {
-          const int slot = it % nslots;
-          const uint32_t par = (it / nslots) & 1;
-          if (it >= nslots) mbar_wait(&hdr->empty[slot], par ^ 1);
+        int cblk = 0, sc = 0, rc = 0;
+        for (int st = 0, k0 = 0; st < stages; ++st, k0 += kpack) {
+          if (filled >= nslots) mbar_wait(&hdr->empty[slot], par ^ 1);
           uint8_t* a_dst = slots + slot * slot_bytes;
           uint8_t* b_dst = a_dst + kStageABytes;
-          const int k0 = st * kpack;
           const int nk = min(kpack, ksteps - k0);
           mbar_arrive_expect_tx(&hdr->full[slot], nk * (box_a_bytes + uint32_t(sub_b)));
           for (int j = 0; j < nk; ++j)                  // weights: static, before the dependency
@@ -127,11 +129,19 @@ __global__ void __launch_bounds__(kPersistThreads, 1)
             waited = true;
           }
           for (int j = 0; j < nk; ++j) {
-            const int kstep = k0 + j;
-            const int rs = kstep / cblocks;
-            const int cblk = kstep - rs * cblocks;
-            const int r = rs / S, s = rs - (rs / S) * S;
-            tma_load_4d(a_dst + j * sub_a, tma, &hdr->full[slot], cblk * cb, qbase + s, pbase + r, n0);
+            tma_load_4d(a_dst + j * sub_a, tma, &hdr->full[slot], cblk * cb, qbase + sc, pbase + rc, n0);
+            if (++cblk == cblocks) {
+              cblk = 0;
+              if (++sc == S) {
+                sc = 0;
+                ++rc;
+              }
+            }
+          }
+          ++filled;
+          if (++slot == nslots) {
+            slot = 0;
+            par ^= 1u;
           }
         }
       }
@@ -142,16 +152,16 @@ __global__ void __launch_bounds__(kPersistThreads, 1)
       const uint32_t idesc = umma_idesc_f16(uint32_t(bn), Elt<T>::kDtype);
       const uint32_t row_bytes = uint32_t(cb) * 2u;
       const int kk_n = cb / 16;
-      int it = 0, lt = 0;
+      int lt = 0, slot = 0, b = 0;
+      uint32_t par = 0, apar = 0;
+      uint64_t* const gate = pre ? hdr->ready : hdr->full;
       for (int tile = blockIdx.x; tile < total; tile += grid, ++lt) {
-        const int b = lt % nacc;
-        if (lt >= nacc) mbar_wait(&hdr->acc_empty[b], ((lt / nacc) - 1) & 1);
+        if (lt >= nacc) mbar_wait(&hdr->acc_empty[b], apar ^ 1);
         tc_fence_after();
         const uint32_t acc = tmem_base + uint32_t(b * bn);
         uint32_t accumulate = 0;
-        for (int st = 0; st < stages; ++st, ++it) {
-          const int slot = it % nslots;
-          mbar_wait(pre ? &hdr->ready[slot] : &hdr->full[slot], (it / nslots) & 1);
+        for (int st = 0; st < stages; ++st) {
+          mbar_wait(&gate[slot], par);
           tc_fence_after();
           const uint32_t a_base = smem_u32(slots + slot * slot_bytes);
           const uint32_t b_base = a_base + kStageABytes;
@@ -163,8 +173,16 @@ __global__ void __launch_bounds__(kPersistThreads, 1)
               accumulate = 1;
             }
           umma_commit(&hdr->empty[slot]);
+          if (++slot == nslots) {
+            slot = 0;
+            par ^= 1u;
+          }
         }
         umma_commit(&hdr->acc_full[b]);
+        if (++b == nacc) {
+          b = 0;
+          apar ^= 1u;
+        }
       }
     }
   } else {
