@@ -828,6 +828,7 @@ def choose_bn(cout: int) -> tuple[int, int]:
 
 
 GEMM_M2 = os.environ.get("DFX_GEMM_M2", "1") != "0"     # A/B switch for 256-row CTAs
+SPLIT_MIN_STAGES = int(os.environ.get("DFX_SPLIT_MIN_STAGES", "4"))   # K stages per split, at least
 # split-K reduction: "kernel" (default) = fp32 workspace + a splitk_kernel launch;
 # "cluster" = the splits of a tile form a thread-block cluster and reduce over DSMEM
 # inside the GEMM (dfx_gemm.cu, <= 8 splits; removes 245 of 928 launches at batch 1
@@ -869,8 +870,8 @@ def gemm_tiling(geom: dict, n: int, p: int, q: int, sm_count: int = 148) -> dict
     stages = math.ceil(geom["ksteps"] / kpack)
     base = m_tiles * nt
     splits = 1
-    if base < sm_count and stages >= 8:
-        splits = min(math.ceil(sm_count / base), stages // 4)      # >= 4 stages per split
+    if base < sm_count and stages >= 2 * SPLIT_MIN_STAGES:
+        splits = min(math.ceil(sm_count / base), stages // SPLIT_MIN_STAGES)
     sps = math.ceil(stages / max(splits, 1))
     splits = math.ceil(stages / sps)
     # m2: 256-row CTAs (two M tiles sharing each weight stage) once the grid still
