@@ -11,5 +11,7 @@ python scripts/summarize_profiles.py traffic gpurun_out/gemm_traffic_b1.csv gpur
 ncu --set full --clock-control none --import-source on -k regex:gemm_kernel -s 40 -c 1 -o gpurun_out/gemm_effnet_b1 python scripts/prof_step.py --batch 1 --models efficientnet_v2_l > /dev/null 2>&1
 ncu --set full --clock-control none --import-source on -k regex:gemm -c 1 -o gpurun_out/gemm_persist_expand_b32 python scripts/gemm_micro.py --cases 224:1344:14:32:1 --act silu > /dev/null 2>&1
 ls gpurun_out
-echo "== b1 SE unstaged"; DFX_SE_UNSTAGED_BATCH=1 timeout 300 python scripts/member_times.py --batch 1 | tail -2
-echo "== b1 default"; timeout 300 python scripts/member_times.py --batch 1 | tail -2
+
+
+ncu --set full --clock-control none --import-source on -k regex:gemm -s 6 -c 1 -o gpurun_out/gemm_vgg_conv_b32 python scripts/prof_step.py --batch 32 --models vgg16 > /dev/null 2>&1
+ncu --set full --clock-control none --import-source on -k regex:dwconv -c 1 -o gpurun_out/dw_s5_b32 python scripts/dw_micro.py --cases 1344:14:32:3:1 > /dev/null 2>&1
