@@ -426,12 +426,12 @@ class ExecInstance:
     def _prioritise(self, g) -> None:
         """Concurrent members are independent branches of one graph; the query
         ends when the LONGEST dependent chain ends.  Members get node priorities
-        by chain length (graph nodes, a latency proxy at small batch): the longest
-        chain most urgent, so other branches' CTAs fill in around it instead of
-        delaying it."""
-        chain: dict[int, int] = {}
-        for m in self._node_member:
-            chain[m] = chain.get(m, 0) + 1
+        by estimated chain latency (_node_cost_us summed over the member's nodes):
+        the longest chain most urgent, so other branches' CTAs fill in around it
+        instead of delaying it."""
+        chain: dict[int, float] = {}
+        for m, (op, _, info) in zip(self._node_member, self.nodes):
+            chain[m] = chain.get(m, 0.0) + _node_cost_us(info)
         order = sorted(chain, key=lambda m: (-chain[m], m))
         least, greatest = g.set_priority(0, 0)
         prio = {m: min(least, greatest + r) for r, m in enumerate(order)}
@@ -685,6 +685,18 @@ class ExecInstance:
         rt.host_free(self.host_in)
         rt.host_free(self.host_out)
         rt.stream_destroy(self.stream)
+
+
+# measured batch-1 latency floor of one dependent node per kind, us (layer tables
+# of the B200 bench: GEMM ~6.5, SE cluster ~7, depthwise ~4.5, split-K ~3, rest ~2.5)
+_NODE_BASE_US = {"gemm": 6.5, "se": 7.0, "dwconv": 4.5, "splitk": 3.0, "dwse": 9.0}
+
+
+def _node_cost_us(info: dict) -> float:
+    """Latency estimate of one graph node for the priority ranking: a per-kind
+    floor plus its bytes at 3 TB/s and its FLOPs at 300 TFLOP/s."""
+    return (_NODE_BASE_US.get(info.get("kind"), 2.5) + info.get("bytes", 0) / 3e6
+            + info.get("flops", 0) / 3e8)
 
 
 class DeviceDag:

@@ -41,10 +41,11 @@ GEMM, DWCONV, POOL, GAP, EW, COPY, SE = "gemm", "dwconv", "pool", "gap", "ew", "
 DWSE = "dwse"            # depthwise conv -> SE gate -> channel scale, one launch
 LN, TOKENS, ATTN = "ln", "tokens", "attn"      # token (ViT) launches, dfx_vit.cu
 SE_MAX_C, SE_MAX_CR = 4096, 512          # limits of dfx_fused.cu se_kernel
-# fold the gate's channel_scale into the SE launch (DFX_SE_FUSE=1).  Off by default: the
-# in-cluster scaling on 8-16 CTAs measured slower (EfficientNetV2-L alone 2.73 vs 2.66 ms)
-# than the separate full-GPU elementwise launch it replaces, which PDL mostly hides.
-SE_FUSE_SCALE = os.environ.get("DFX_SE_FUSE", "0") == "1"
+# fold the gate's channel_scale into the SE launch (DFX_SE_FUSE=0: off, A/B).  With 8-CTA
+# clusters this measured slower (EfficientNetV2-L alone 2.73 vs 2.66 ms); with 16-CTA
+# clusters and the faster epilogue math it wins: EfficientNetV2-L batch 1 2.22 -> 2.16 ms,
+# 4-model batch 32 11.77 -> 11.58 ms (61 launches fewer)
+SE_FUSE_SCALE = os.environ.get("DFX_SE_FUSE", "1") == "1"
 
 
 def round_up(x: int, a: int) -> int:

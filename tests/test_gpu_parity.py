@@ -307,6 +307,7 @@ def test_conv_layer_cluster_splitk(cin, h, w, cout, k, s, p, n, monkeypatch):
 def test_fold_pre_transform(name, mode, monkeypatch):
     from paper_2410_21120_b200 import lower, zoo
     monkeypatch.setattr(lower, "FOLD_PRE", True)
+    monkeypatch.setattr(lower, "SE_FUSE_SCALE", False)     # keep the scale as its own node
     g, w = zoo.build(name)
     prog = lower.lower_member(g, w)
     assert {L.pre.binop for L in prog.launches if L.pre is not None} == {mode}
@@ -324,6 +325,7 @@ def test_fold_pre_transform(name, mode, monkeypatch):
 def test_fused_dw_se(name, n, monkeypatch):
     from paper_2410_21120_b200 import lower, zoo
     monkeypatch.setattr(lower, "FUSE_DWSE", True)
+    monkeypatch.setattr(lower, "SE_FUSE_SCALE", False)
     g, w = zoo.build(name)
     prog = lower.lower_member(g, w)
     assert sum(L.kind == lower.DWSE for L in prog.launches) in (8, 61)
