@@ -95,10 +95,37 @@ DFX_DEV void drain_rows(uint32_t taddr, float* stg, int ncols, int64_t pix, int 
 // (scripts/gpu_ab_drain.sh: e.g. 3x3 64->256 55 vs 67 us, 1x1 224->1344 20 vs
 // 27 us): the drain is issue-bound, and the transpose's extra shared-memory
 // instructions cost more than the half-used store sectors.
-template <typename T>
-DFX_DEV void drain_rows_direct(uint32_t taddr, int ncols, int64_t pix, int img, bool valid,
-                               int co_base, int cout, const dfx_epilogue& e, const dfx_view& o,
-                               bool views_vec, float* ws, int ldw, int c_first, int c_step) {
+//
+// Issue-bound means instructions per element set the speed: the first
+// activation is a template parameter (the runtime switch compiled to jump
+// tables and register shuffles: ncu counted ~184 instructions per 16-column
+// chunk on VGG16's first conv), the epilogue fields are copied to registers
+// once, and only the ragged channel tail takes the generic path.
+template <int ACT>
+DFX_DEV void act8_t(float* v) {
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    if constexpr (ACT == DFX_ACT_RELU) v[i] = fmaxf(v[i], 0.0f);
+    else if constexpr (ACT == DFX_ACT_HARDSWISH) v[i] = v[i] * hsig_f(v[i]);
+    else if constexpr (ACT == DFX_ACT_HARDSIGMOID) v[i] = hsig_f(v[i]);
+    else if constexpr (ACT == DFX_ACT_SILU) v[i] = silu_f(v[i]);
+    else if constexpr (ACT == DFX_ACT_SIGMOID) v[i] = sigmoid_f(v[i]);
+    else if constexpr (ACT == DFX_ACT_GELU) v[i] = 0.5f * v[i] * (1.0f + erff(v[i] * 0.70710678118654752f));
+  }
+}
+
+template <typename T, int ACT1>
+DFX_DEV void drain_rows_direct_t(uint32_t taddr, int ncols, int64_t pix, int img, bool valid, int co_base,
+                                 int cout, const dfx_epilogue& e, const dfx_view& o, bool views_vec, float* ws,
+                                 int ldw, int c_first, int c_step) {
+  const float* const alpha = e.alpha;
+  const float* const beta = e.beta;
+  const int binop = e.binop, act2 = e.act2;
+  void* const obase = o.base;
+  const int64_t orow = pix * o.pitch + o.coff;                  // view_pixel_index(o, pix, 0)
+  const void* const xbase = e.other.base;
+  const int64_t xrow = binop == DFX_BIN_ADD ? pix * e.other.pitch + e.other.coff
+                                            : int64_t(img) * e.other.pitch + e.other.coff;
   for (int c0 = c_first; c0 < ncols; c0 += c_step) {
     uint32_t r[16];
     tmem_ld16_issue(taddr + uint32_t(c0), r);
@@ -113,11 +140,45 @@ DFX_DEV void drain_rows_direct(uint32_t taddr, int ncols, int64_t pix, int img, 
 #pragma unroll
       for (int i = 0; i < 4; ++i) dst[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
     } else if (views_vec && co + 16 <= cout) {
+      if (alpha != nullptr) {
+        const float4* a = reinterpret_cast<const float4*>(alpha + co);
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        epilogue8<T>(e, v + 8 * h, pix, img, co + 8 * h);
-        st8<T>(o.base, view_pixel_index(o, pix, co + 8 * h), v + 8 * h);
+        for (int q = 0; q < 4; ++q) {
+          const float4 aq = a[q];
+          v[4 * q] *= aq.x; v[4 * q + 1] *= aq.y; v[4 * q + 2] *= aq.z; v[4 * q + 3] *= aq.w;
+        }
       }
+      if (beta != nullptr) {
+        const float4* b = reinterpret_cast<const float4*>(beta + co);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const float4 bq = b[q];
+          v[4 * q] += bq.x; v[4 * q + 1] += bq.y; v[4 * q + 2] += bq.z; v[4 * q + 3] += bq.w;
+        }
+      }
+      act8_t<ACT1>(v);
+      act8_t<ACT1>(v + 8);
+      if (binop != DFX_BIN_NONE) {
+        float x[16];
+        ld8<T>(xbase, xrow + co, x);
+        ld8<T>(xbase, xrow + co + 8, x + 8);
+        if (binop == DFX_BIN_ADD) {
+#pragma unroll
+          for (int i = 0; i < 16; ++i) v[i] += x[i];
+        } else {
+#pragma unroll
+          for (int i = 0; i < 16; ++i) v[i] *= x[i];
+        }
+      }
+      if (act2 == DFX_ACT_RELU) {
+#pragma unroll
+        for (int i = 0; i < 16; ++i) v[i] = fmaxf(v[i], 0.0f);
+      } else if (act2 != DFX_ACT_NONE) {
+        act8(act2, v);
+        act8(act2, v + 8);
+      }
+      st8<T>(obase, orow + co, v);
+      st8<T>(obase, orow + co + 8, v + 8);
     } else {
       float tail[16];
 #pragma unroll
@@ -125,6 +186,25 @@ DFX_DEV void drain_rows_direct(uint32_t taddr, int ncols, int64_t pix, int img, 
       epilogue_store_tail<T>(e, o, tail, pix, img, co, min(16, cout - co));
     }
   }
+}
+
+template <typename T>
+DFX_DEV void drain_rows_direct(uint32_t taddr, int ncols, int64_t pix, int img, bool valid,
+                               int co_base, int cout, const dfx_epilogue& e, const dfx_view& o,
+                               bool views_vec, float* ws, int ldw, int c_first, int c_step) {
+#define DFX_DRAIN(A)                                                                                  \
+  drain_rows_direct_t<T, A>(taddr, ncols, pix, img, valid, co_base, cout, e, o, views_vec, ws, ldw, \
+                            c_first, c_step)
+  switch (e.act1) {
+    case DFX_ACT_RELU: DFX_DRAIN(DFX_ACT_RELU); break;
+    case DFX_ACT_HARDSWISH: DFX_DRAIN(DFX_ACT_HARDSWISH); break;
+    case DFX_ACT_HARDSIGMOID: DFX_DRAIN(DFX_ACT_HARDSIGMOID); break;
+    case DFX_ACT_SILU: DFX_DRAIN(DFX_ACT_SILU); break;
+    case DFX_ACT_SIGMOID: DFX_DRAIN(DFX_ACT_SIGMOID); break;
+    case DFX_ACT_GELU: DFX_DRAIN(DFX_ACT_GELU); break;
+    default: DFX_DRAIN(DFX_ACT_NONE); break;
+  }
+#undef DFX_DRAIN
 }
 
 }  // namespace dfx
