@@ -263,6 +263,12 @@ DFX_DEV void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
+// try_wait suspends the thread until the phase completes or this many ns pass
+// (the hardware wakes it on completion): waiting warps stop spinning through
+// try_wait loops that steal issue slots from the drain warps on the same SMSP
+// (ncu: 1.7 M loop iterations in one VGG16 batch-32 conv).
+constexpr uint32_t kMbarSuspendNs = 100000;
+
 // Blocks until the phase with the given parity completed.  A pipeline bug would
 // otherwise hang the GPU; after ~2^26 polls the kernel traps instead.
 DFX_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
@@ -272,14 +278,14 @@ DFX_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
     asm volatile(
         "{\n"
         ".reg .pred P1;\n"
-        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2, %3;\n"
         "selp.u32 %0, 1, 0, P1;\n"
         "}\n"
         : "=r"(done)
-        : "r"(addr), "r"(parity)
+        : "r"(addr), "r"(parity), "r"(kMbarSuspendNs)
         : "memory");
     if (done) return;
-    if (tries > (1u << 26)) __trap();
+    if (tries > (1u << 24)) __trap();
   }
 }
 
