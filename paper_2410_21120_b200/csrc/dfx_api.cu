@@ -28,7 +28,7 @@ template <typename T> __global__ void gap_kernel(const __grid_constant__ dfx_gap
 template <typename T> __global__ void in_kernel(const __grid_constant__ dfx_in_params P);
 template <typename T> __global__ void in_im2col_kernel(const __grid_constant__ dfx_in_params P);
 template <typename T> __global__ void out_kernel(const __grid_constant__ dfx_out_params P);
-template <typename T, int CL> __global__ void se_kernel(const __grid_constant__ dfx_se_params P);
+template <typename T, int CL, int IPI> __global__ void se_kernel(const __grid_constant__ dfx_se_params P);
 template <typename T> __global__ void dwse_kernel(const __grid_constant__ dfx_dwse_params P);
 template <typename T> __global__ void ln_kernel(const __grid_constant__ dfx_ln_params P);
 template <typename T> __global__ void tokens_kernel(const __grid_constant__ dfx_tokens_params P);
@@ -50,12 +50,15 @@ const void* gemm_func(int dt, int m2) {
                        : reinterpret_cast<const void*>(&dfx::gemm_kernel<__nv_bfloat16, 0>);
 }
 
-const void* se_func(int dt, int cl) {
+const void* se_func(int dt, int cl, int ipi = 1) {
+  if (ipi == 4)
+    return dt == DFX_F16 ? reinterpret_cast<const void*>(&dfx::se_kernel<__half, 16, 4>)
+                         : reinterpret_cast<const void*>(&dfx::se_kernel<__nv_bfloat16, 16, 4>);
   if (cl == 16)
-    return dt == DFX_F16 ? reinterpret_cast<const void*>(&dfx::se_kernel<__half, 16>)
-                         : reinterpret_cast<const void*>(&dfx::se_kernel<__nv_bfloat16, 16>);
-  return dt == DFX_F16 ? reinterpret_cast<const void*>(&dfx::se_kernel<__half, 8>)
-                       : reinterpret_cast<const void*>(&dfx::se_kernel<__nv_bfloat16, 8>);
+    return dt == DFX_F16 ? reinterpret_cast<const void*>(&dfx::se_kernel<__half, 16, 1>)
+                         : reinterpret_cast<const void*>(&dfx::se_kernel<__nv_bfloat16, 16, 1>);
+  return dt == DFX_F16 ? reinterpret_cast<const void*>(&dfx::se_kernel<__half, 8, 1>)
+                       : reinterpret_cast<const void*>(&dfx::se_kernel<__nv_bfloat16, 8, 1>);
 }
 
 template <typename T>
@@ -288,8 +291,13 @@ int config_for(int op, const void* params, size_t size, LaunchCfg* c) {
       // more pooling parallelism); DFX_SE_CL=8 for A/B
       static const int cl_env = getenv("DFX_SE_CL") ? atoi(getenv("DFX_SE_CL")) : 16;
       int cl = (cl_env == 8 && dfx::se_smem_bytes(p->in.c, p->cr, 8) <= dfx::kSeSmemBudget) ? 8 : 16;
-      c->func = se_func(p->in.dtype, cl);
-      c->grid = dim3(unsigned(cl), unsigned(p->in.n));
+      // DFX_SE_IPI=4: 4 images per cluster from batch 8 (each FC weight read serves 4
+      // images).  Off by default: the lost pooling/scaling parallelism costs more than
+      // the weight traffic saves (EfficientNetV2-L batch 32 6.73 vs 6.07 ms)
+      static const int ipi_env = getenv("DFX_SE_IPI") ? atoi(getenv("DFX_SE_IPI")) : 1;
+      const int ipi = (ipi_env == 4 && cl == 16 && p->in.n >= 8) ? 4 : 1;
+      c->func = se_func(p->in.dtype, cl, ipi);
+      c->grid = dim3(unsigned(cl), unsigned((p->in.n + ipi - 1) / ipi));
       c->smem = (p->apply & 2) ? 0 : size_t(dfx::se_smem_bytes(p->in.c, p->cr, cl));
       if (c->smem > size_t(dfx::kSeSmemBudget))
         return fail(DFX_E_UNSUPPORTED, "se: c=%d cr=%d needs %zu B of smem", p->in.c, p->cr, c->smem);
@@ -420,6 +428,9 @@ int dfx_init(int device) {
       CK(cudaFuncSetAttribute(se_func(dt, cl), cudaFuncAttributeMaxDynamicSharedMemorySize,
                               dfx::kSeSmemBudget));
     CK(cudaFuncSetAttribute(se_func(dt, 16), cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    CK(cudaFuncSetAttribute(se_func(dt, 16, 4), cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    CK(cudaFuncSetAttribute(se_func(dt, 16, 4), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            dfx::kSeSmemBudget));
     CK(cudaFuncSetAttribute(DFX_PICK(dwse_kernel, dt), cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     CK(cudaFuncSetAttribute(DFX_PICK(dwse_kernel, dt), cudaFuncAttributeMaxDynamicSharedMemorySize,
                             dfx::kSeSmemBudget));

@@ -59,19 +59,23 @@ namespace dfx {
 
 constexpr int kSeMaxSlice = 512;   // channels per CTA (C <= 4096 -> <= 512 at CL = 8)
 
-template <typename T, int CL>
+// IPI images per cluster (large batches): every weight element a CTA reads serves
+// IPI images (the FC slices were re-read from L2 once per image: 2.4 MB per image
+// for EfficientNetV2-L's last stage), one cluster.sync covers all of them.
+template <typename T, int CL, int IPI>
 __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kSeThreads)
     se_kernel(const __grid_constant__ dfx_se_params P) {
-  __shared__ float pooled[kSeMaxSlice];      // this CTA's channels only
-  __shared__ float partial[kSeMaxCr];        // fc1 partial sums over this CTA's channels
-  __shared__ float hidden[kSeMaxCr];         // full hidden vector (rank-order reduction)
+  __shared__ float pooled[IPI][kSeMaxSlice];     // this CTA's channels only (later: gates)
+  __shared__ float partial[IPI][kSeMaxCr];       // fc1 partial sums over this CTA's channels
+  __shared__ float hidden[IPI][kSeMaxCr];        // full hidden vectors (rank-order reduction)
   __shared__ float red[kSeThreads * 8 + 8];  // pooling reduction scratch
   __shared__ __align__(8) uint64_t wbar;
   extern __shared__ __align__(16) uint8_t wsm[];
   cg::cluster_group cluster = cg::this_cluster();
   const int rank = int(cluster.block_rank());
-  const int n = blockIdx.y;
+  const int n0 = blockIdx.y * IPI;
   const dfx_view& in = P.in;
+  const int nimg = min(IPI, in.n - n0);
   const int C = in.c, Cr = P.cr;
   const int hw = in.h * in.w;
   const int cs = se_chan_slice(C, CL);
@@ -110,6 +114,8 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kSeThreads)
   const int G = (nch + 7) / 8;                        // channel groups of this CTA
   const int stripes = G ? kSeThreads / G : 1;
   const int g = threadIdx.x % max(G, 1), y = threadIdx.x / max(G, 1);
+  for (int im = 0; im < nimg; ++im) {
+  const int n = n0 + im;
   float acc[8];
 #pragma unroll
   for (int i = 0; i < 8; ++i) acc[i] = 0.f;
@@ -146,7 +152,9 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kSeThreads)
     const int gg = k / 8, ii = k % 8;
     float s = 0.f;
     for (int yy = 0; yy < stripes; ++yy) s += red[(yy * G + gg) * 8 + ii];
-    pooled[k] = s * (1.0f / float(hw));
+    pooled[im][k] = s * (1.0f / float(hw));
+  }
+  __syncthreads();                                    // red[] reused by the next image
   }
   if (threadIdx.x == 0) DFX_TL(2);
   if (threadIdx.x == 0) mbar_wait(&wbar, 0);                 // weight slices landed (one poller)
@@ -162,20 +170,25 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kSeThreads)
     for (int t = threadIdx.x; t < Cr * KQ; t += kSeThreads) {
       const int j = t % Cr, q = t / Cr;
       const int k0 = q * kq_len, k1 = min(nch, k0 + kq_len);
-      float s0 = 0.f, s1 = 0.f;
-      int k = k0;
-      for (; k + 1 < k1; k += 2) {
-        s0 = fmaf(Elt<T>::to_f(w1[int64_t(k) * Cr + j]), pooled[k], s0);
-        s1 = fmaf(Elt<T>::to_f(w1[int64_t(k + 1) * Cr + j]), pooled[k + 1], s1);
+      float sa[IPI];
+#pragma unroll
+      for (int i = 0; i < IPI; ++i) sa[i] = 0.f;
+      for (int k = k0; k < k1; ++k) {
+        const float wv = Elt<T>::to_f(w1[int64_t(k) * Cr + j]);     // one load, IPI images
+#pragma unroll
+        for (int i = 0; i < IPI; ++i) sa[i] = fmaf(wv, pooled[i][k], sa[i]);
       }
-      if (k < k1) s0 = fmaf(Elt<T>::to_f(w1[int64_t(k) * Cr + j]), pooled[k], s0);
-      red[t] = s0 + s1;
+#pragma unroll
+      for (int i = 0; i < IPI; ++i) red[t * IPI + i] = sa[i];
     }
     __syncthreads();
     for (int j = threadIdx.x; j < Cr; j += kSeThreads) {
-      float s = 0.f;
-      for (int q = 0; q < KQ; ++q) s += red[q * Cr + j];
-      partial[j] = s;
+#pragma unroll
+      for (int i = 0; i < IPI; ++i) {
+        float s = 0.f;
+        for (int q = 0; q < KQ; ++q) s += red[(q * Cr + j) * IPI + i];
+        partial[i][j] = s;
+      }
     }
   }
   if (threadIdx.x == 0) DFX_TL(4);
@@ -183,16 +196,17 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kSeThreads)
   if (threadIdx.x == 0) DFX_TL(5);
 
   // ---- 3. hidden = act1(b1 + sum over ranks of the partials), rank order
-  for (int j = threadIdx.x; j < Cr; j += kSeThreads) {
+  for (int t = threadIdx.x; t < Cr * IPI; t += kSeThreads) {
+    const int i = t / Cr, j = t - i * Cr;
     float v[CL];
 #pragma unroll
-    for (int r = 0; r < CL; ++r) v[r] = cluster.map_shared_rank(partial, r)[j];
+    for (int r = 0; r < CL; ++r) v[r] = cluster.map_shared_rank(&partial[i][0], r)[j];
     float s = 0.f;
 #pragma unroll
     for (int r = 0; r < CL; ++r) s += v[r];
     float a[8] = {s + (P.b1 ? P.b1[j] : 0.f), 0, 0, 0, 0, 0, 0, 0};
     act8(P.act1, a);
-    hidden[j] = a[0];
+    hidden[i][j] = a[0];
   }
   __syncthreads();
   if (threadIdx.x == 0) DFX_TL(6);
@@ -202,31 +216,46 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kSeThreads)
   const dfx_view& out = P.out;
   for (int k = threadIdx.x; k < nch; k += kSeThreads) {
     const T* row = w2 + int64_t(k) * Cr;
-    float s0 = 0.f, s1 = 0.f;
+    float sa[IPI], sb[IPI];
+#pragma unroll
+    for (int i = 0; i < IPI; ++i) sa[i] = sb[i] = 0.f;
     if ((Cr & 7) == 0) {
       for (int j = 0; j < Cr; j += 8) {
         float wv[8];
-        ld8<T>(row, j, wv);
-        s0 = fmaf(wv[0], hidden[j], s0); s1 = fmaf(wv[1], hidden[j + 1], s1);
-        s0 = fmaf(wv[2], hidden[j + 2], s0); s1 = fmaf(wv[3], hidden[j + 3], s1);
-        s0 = fmaf(wv[4], hidden[j + 4], s0); s1 = fmaf(wv[5], hidden[j + 5], s1);
-        s0 = fmaf(wv[6], hidden[j + 6], s0); s1 = fmaf(wv[7], hidden[j + 7], s1);
+        ld8<T>(row, j, wv);                                  // one load, IPI images
+#pragma unroll
+        for (int i = 0; i < IPI; ++i) {
+          const float* h = hidden[i] + j;
+          sa[i] = fmaf(wv[0], h[0], sa[i]); sb[i] = fmaf(wv[1], h[1], sb[i]);
+          sa[i] = fmaf(wv[2], h[2], sa[i]); sb[i] = fmaf(wv[3], h[3], sb[i]);
+          sa[i] = fmaf(wv[4], h[4], sa[i]); sb[i] = fmaf(wv[5], h[5], sb[i]);
+          sa[i] = fmaf(wv[6], h[6], sa[i]); sb[i] = fmaf(wv[7], h[7], sb[i]);
+        }
       }
     } else {
-      for (int j = 0; j < Cr; ++j) s0 = fmaf(Elt<T>::to_f(row[j]), hidden[j], s0);
+      for (int j = 0; j < Cr; ++j) {
+        const float wv = Elt<T>::to_f(row[j]);
+#pragma unroll
+        for (int i = 0; i < IPI; ++i) sa[i] = fmaf(wv, hidden[i][j], sa[i]);
+      }
     }
     const int c = c_lo + k;
-    float a[8] = {s0 + s1 + (P.b2 ? P.b2[c] : 0.f), 0, 0, 0, 0, 0, 0, 0};
-    act8(P.act2, a);
-    if (apply)
-      pooled[k] = a[0];                                      // gate of this CTA's channel k
-    else
-      st1<T>(out.base, int64_t(n) * out.pitch + out.coff + c, a[0]);
+#pragma unroll
+    for (int i = 0; i < IPI; ++i) {
+      if (i >= nimg) break;
+      float a[8] = {sa[i] + sb[i] + (P.b2 ? P.b2[c] : 0.f), 0, 0, 0, 0, 0, 0, 0};
+      act8(P.act2, a);
+      if (apply)
+        pooled[i][k] = a[0];                                 // gate of this CTA's channel k
+      else
+        st1<T>(out.base, int64_t(n0 + i) * out.pitch + out.coff + c, a[0]);
+    }
   }
-  if (apply) {
+  if (apply) __syncthreads();
+  for (int im = 0; apply && im < nimg; ++im) {
     // ---- 5. fused channel_scale: out[n, :, :, slice] = x * gate (x re-read from L2)
-    __syncthreads();
-    const int64_t pb = int64_t(n) * hw;
+    const float* gate = pooled[im];
+    const int64_t pb = int64_t(n0 + im) * hw;
     if (((in.coff | out.coff | c_lo | nch) & 7) == 0) {
       // 4 independent 16-B loads in flight per thread before any store (the
       // per-iteration load -> store chain otherwise serialises on L2 latency)
@@ -250,7 +279,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kSeThreads)
             float x[8];
             unpack8<T>(raw[u], x);
 #pragma unroll
-            for (int j = 0; j < 8; ++j) x[j] *= pooled[g8 + j];
+            for (int j = 0; j < 8; ++j) x[j] *= gate[g8 + j];
             st8<T>(out.base, view_pixel_index(out, pb + s, c_lo + g8), x);
           }
         }
@@ -259,7 +288,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kSeThreads)
       for (int i = threadIdx.x; i < hw * nch; i += kSeThreads) {
         const int s = i / nch, k = i - s * nch;
         st1<T>(out.base, view_pixel_index(out, pb + s, c_lo + k),
-               ld1<T>(in.base, view_pixel_index(in, pb + s, c_lo + k)) * pooled[k]);
+               ld1<T>(in.base, view_pixel_index(in, pb + s, c_lo + k)) * gate[k]);
       }
     }
   }
@@ -427,11 +456,14 @@ __global__ void __cluster_dims__(kDwseCL, 1, 1) __launch_bounds__(kSeThreads)
 template __global__ void dwse_kernel<__nv_bfloat16>(const __grid_constant__ dfx_dwse_params);
 template __global__ void dwse_kernel<__half>(const __grid_constant__ dfx_dwse_params);
 
-#define DFX_SE_INST(T, CL) template __global__ void se_kernel<T, CL>(const __grid_constant__ dfx_se_params);
-DFX_SE_INST(__nv_bfloat16, 8)
-DFX_SE_INST(__half, 8)
-DFX_SE_INST(__nv_bfloat16, 16)
-DFX_SE_INST(__half, 16)
+#define DFX_SE_INST(T, CL, IPI) \
+  template __global__ void se_kernel<T, CL, IPI>(const __grid_constant__ dfx_se_params);
+DFX_SE_INST(__nv_bfloat16, 8, 1)
+DFX_SE_INST(__half, 8, 1)
+DFX_SE_INST(__nv_bfloat16, 16, 1)
+DFX_SE_INST(__half, 16, 1)
+DFX_SE_INST(__nv_bfloat16, 16, 4)
+DFX_SE_INST(__half, 16, 4)
 #undef DFX_SE_INST
 
 }  // namespace dfx

@@ -334,3 +334,18 @@ def test_fused_dw_se(name, n, monkeypatch):
     got = [t.values for t in run_batch(g, w, [Tensor(g.input_spec, x) for x in xs])]
     ref = run_fast(g, w, xs)
     assert rel(got, ref) < TOL
+
+
+# squeeze-excitation with 4 images per cluster (batch >= 8, dfx_fused.cu se_kernel IPI = 4),
+# including a last cluster with a partial image group (batch 10)
+def test_se_multi_image_batch():
+    import os
+    from paper_2410_21120_b200 import zoo
+    if os.environ.get("DFX_SE_IPI", "1") != "4":
+        pytest.skip("4-image SE clusters are an A/B option (run with DFX_SE_IPI=4)")
+    g, w = zoo.build("mobilenet_v3_large")
+    rng = np.random.default_rng(17)
+    xs = rng.standard_normal((10,) + tuple(g.input_spec.dims)).astype(np.float32)
+    got = [t.values for t in run_batch(g, w, [Tensor(g.input_spec, x) for x in xs])]
+    ref = run_fast(g, w, xs)
+    assert rel(got, ref) < TOL
