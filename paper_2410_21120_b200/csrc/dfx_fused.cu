@@ -58,6 +58,7 @@ namespace cg = cooperative_groups;
 namespace dfx {
 
 constexpr int kSeMaxSlice = 512;   // channels per CTA (C <= 4096 -> <= 512 at CL = 8)
+__device__ __forceinline__ int out_coff_of(const dfx_se_params& P) { return P.out.coff; }
 
 // IPI images per cluster (large batches): every weight element a CTA reads serves
 // IPI images (the FC slices were re-read from L2 once per image: 2.4 MB per image
@@ -110,6 +111,16 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kSeThreads)
   griddep_launch();
   if (threadIdx.x == 0) DFX_TL(1);
 
+  // fused scale (apply): when the host sized dynamic smem for it, the CTA's slice
+  // of x is kept in smem while pooling, so the scale pass reads smem instead of
+  // a second L2 round trip (dfx_api.cu DFX_OP_SE)
+  uint32_t dsm;
+  asm("mov.u32 %0, %%dynamic_smem_size;" : "=r"(dsm));
+  const int wbytes = staged ? 2 * sb : 0;
+  T* xt = reinterpret_cast<T*>(wsm + wbytes);
+  const bool cache_x = apply && IPI == 1 && ((in.coff | out_coff_of(P) | c_lo | nch) & 7) == 0 &&
+                       uint32_t(wbytes + hw * nch * 2) <= dsm;
+
   // ---- 1. pool: thread = (channel group g, pixel stripe y); all loads in flight first
   const int G = (nch + 7) / 8;                        // channel groups of this CTA
   const int stripes = G ? kSeThreads / G : 1;
@@ -124,21 +135,31 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kSeThreads)
     const int nl = min(8, c_hi - c);
     const int64_t base = view_pixel_index(in, int64_t(n) * hw, c);
     if (nl == 8 && ((in.coff + c) & 7) == 0) {
+      const T* ib = reinterpret_cast<const T*>(in.base) + base;
       int s = y;
       for (; s + 3 * stripes < hw; s += 4 * stripes) {      // 4 independent 16-B loads
+        uint4 r[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) r[u] = *reinterpret_cast<const uint4*>(ib + int64_t(s + u * stripes) * in.pitch);
         float x0[8], x1[8], x2[8], x3[8];
-        ld8<T>(in.base, base + int64_t(s) * in.pitch, x0);
-        ld8<T>(in.base, base + int64_t(s + stripes) * in.pitch, x1);
-        ld8<T>(in.base, base + int64_t(s + 2 * stripes) * in.pitch, x2);
-        ld8<T>(in.base, base + int64_t(s + 3 * stripes) * in.pitch, x3);
+        unpack8<T>(r[0], x0);
+        unpack8<T>(r[1], x1);
+        unpack8<T>(r[2], x2);
+        unpack8<T>(r[3], x3);
 #pragma unroll
         for (int i = 0; i < 8; ++i) acc[i] += (x0[i] + x1[i]) + (x2[i] + x3[i]);
+        if (cache_x) {
+#pragma unroll
+          for (int u = 0; u < 4; ++u) *reinterpret_cast<uint4*>(xt + (s + u * stripes) * nch + g * 8) = r[u];
+        }
       }
       for (; s < hw; s += stripes) {
+        const uint4 r = *reinterpret_cast<const uint4*>(ib + int64_t(s) * in.pitch);
         float x[8];
-        ld8<T>(in.base, base + int64_t(s) * in.pitch, x);
+        unpack8<T>(r, x);
 #pragma unroll
         for (int i = 0; i < 8; ++i) acc[i] += x[i];
+        if (cache_x) *reinterpret_cast<uint4*>(xt + s * nch + g * 8) = r;
       }
     } else {
       for (int s = y; s < hw; s += stripes)
@@ -256,7 +277,17 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kSeThreads)
     // ---- 5. fused channel_scale: out[n, :, :, slice] = x * gate (x re-read from L2)
     const float* gate = pooled[im];
     const int64_t pb = int64_t(n0 + im) * hw;
-    if (((in.coff | out.coff | c_lo | nch) & 7) == 0) {
+    if (cache_x) {
+      const int G8 = nch / 8, total = hw * G8;
+      for (int i = threadIdx.x; i < total; i += kSeThreads) {
+        const int s = i / G8, g8 = (i - s * G8) * 8;
+        float x[8];
+        unpack8<T>(*reinterpret_cast<const uint4*>(xt + s * nch + g8), x);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) x[j] *= gate[g8 + j];
+        st8<T>(out.base, view_pixel_index(out, pb + s, c_lo + g8), x);
+      }
+    } else if (((in.coff | out.coff | c_lo | nch) & 7) == 0) {
       // 4 independent 16-B loads in flight per thread before any store (the
       // per-iteration load -> store chain otherwise serialises on L2 latency)
       const int G8 = nch / 8, total = hw * G8;

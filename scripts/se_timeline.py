@@ -12,10 +12,10 @@ from paper_2410_21120_b200 import graph_ir, runtime as rt
 from paper_2410_21120_b200.device import DeviceDag
 
 ap = argparse.ArgumentParser()
-ap.add_argument("--cases", default="1344:48:14:1,2304:56:7:1,3840:160:7:1,960:240:7:1")
+ap.add_argument("--cases", default="1344:56:14:1,2304:96:7:1,3840:160:7:1,960:240:7:1,1344:56:14:32")
 a = ap.parse_args()
-names = {0: "start", 1: "griddep", 2: "pooled", 3: "sync1", 9: "gathered", 4: "weights",
-         5: "fc1", 6: "sync2", 7: "fc2", 8: "sync3"}
+names = {0: "start", 1: "griddep", 2: "pooled", 3: "weights", 4: "fc1", 5: "cluster.sync",
+         6: "hidden", 7: "gate+scale", 8: "final sync"}
 O, S = graph_ir.OpNode, graph_ir.TensorSpec
 for case in a.cases.split(","):
     c, cr, hw, n = map(int, case.split(":"))
