@@ -20,6 +20,7 @@ template <typename T, int M2> __global__ void gemm_kernel(const __grid_constant_
 template <typename T> __global__ void gemm_persist_kernel(const __grid_constant__ dfx_gemm_launch L);
 template <typename T> __global__ void splitk_kernel(const __grid_constant__ dfx_splitk_params P);
 template <typename T> __global__ void ew_kernel(const __grid_constant__ dfx_ew_params P);
+template <typename T, int ACT1> __global__ void ew_vec_kernel(const __grid_constant__ dfx_ew_params P);
 template <typename T> __global__ void dwconv_kernel(const __grid_constant__ dfx_dwconv_params P);
 template <typename T, int K, int S, int QV>
 __global__ void dwconv_tile_kernel(const __grid_constant__ dfx_dwconv_params P);
@@ -74,6 +75,21 @@ const void* dwconv_tile_func_t(int k, int s, int qv) {
   DFX_DW_CASE(5, 2)
 #undef DFX_DW_CASE
   return nullptr;
+}
+template <typename T>
+const void* ew_vec_func_t(int act) {
+  switch (act) {
+    case DFX_ACT_RELU: return reinterpret_cast<const void*>(&dfx::ew_vec_kernel<T, DFX_ACT_RELU>);
+    case DFX_ACT_HARDSWISH: return reinterpret_cast<const void*>(&dfx::ew_vec_kernel<T, DFX_ACT_HARDSWISH>);
+    case DFX_ACT_HARDSIGMOID: return reinterpret_cast<const void*>(&dfx::ew_vec_kernel<T, DFX_ACT_HARDSIGMOID>);
+    case DFX_ACT_SILU: return reinterpret_cast<const void*>(&dfx::ew_vec_kernel<T, DFX_ACT_SILU>);
+    case DFX_ACT_SIGMOID: return reinterpret_cast<const void*>(&dfx::ew_vec_kernel<T, DFX_ACT_SIGMOID>);
+    case DFX_ACT_GELU: return reinterpret_cast<const void*>(&dfx::ew_vec_kernel<T, DFX_ACT_GELU>);
+    default: return reinterpret_cast<const void*>(&dfx::ew_vec_kernel<T, DFX_ACT_NONE>);
+  }
+}
+const void* ew_vec_func(int dt, int act) {
+  return dt == DFX_F16 ? ew_vec_func_t<__half>(act) : ew_vec_func_t<__nv_bfloat16>(act);
 }
 const void* dwconv_tile_func(int dt, int k, int s, int qv) {
   return dt == DFX_F16 ? dwconv_tile_func_t<__half>(k, s, qv) : dwconv_tile_func_t<__nv_bfloat16>(k, s, qv);
@@ -247,8 +263,17 @@ int config_for(int op, const void* params, size_t size, LaunchCfg* c) {
     case DFX_OP_EW: {
       NEED(dfx_ew_params);
       const auto* p = static_cast<const dfx_ew_params*>(params);
+      const int64_t items = int64_t(p->in.n) * p->in.h * p->in.w * cdiv(p->in.c, 8);
+      const bool vec = (p->in.c & 7) == 0 && items < (int64_t(1) << 31) &&
+                       ((p->in.coff | p->out.coff | p->in.pitch | p->out.pitch |
+                         (p->epi.binop ? (p->epi.other.coff | p->epi.other.pitch) : 0)) & 7) == 0;
+      if (vec) {
+        c->func = ew_vec_func(p->in.dtype, p->epi.act1);
+        c->grid = dim3(elementwise_grid(cdiv(items, 2), 256));
+        return DFX_OK;
+      }
       c->func = DFX_PICK(ew_kernel, p->in.dtype);
-      c->grid = dim3(elementwise_grid(int64_t(p->in.n) * p->in.h * p->in.w * cdiv(p->in.c, 8), 256));
+      c->grid = dim3(elementwise_grid(items, 256));
       return DFX_OK;
     }
     case DFX_OP_IN: {

@@ -10,6 +10,7 @@
 // offset allows it and falls back to scalar lanes for ragged toy shapes.
 // Templated on the storage type T (__half or __nv_bfloat16).
 #include "dfx_common.cuh"
+#include "dfx_epi.cuh"
 
 namespace dfx {
 
@@ -46,6 +47,86 @@ __global__ void ew_kernel(const __grid_constant__ dfx_ew_params P) {
     }
   }
 }
+
+// Vector form (every view 8-channel aligned, c % 8 == 0): 32-bit indexing, the
+// first activation a template parameter, two 16-B items in flight per thread.
+// The generic kernel above spent its issue slots on 64-bit divisions and the
+// activation switch (DenseNet's pre-activation BN + ReLU copies, 82 launches).
+template <typename T, int ACT1>
+__global__ void __launch_bounds__(256) ew_vec_kernel(const __grid_constant__ dfx_ew_params P) {
+  griddep_wait();
+  griddep_launch();
+  const dfx_view& in = P.in;
+  const dfx_view& out = P.out;
+  const dfx_epilogue& e = P.epi;
+  const unsigned cg = unsigned(in.c) >> 3;
+  const unsigned hw = unsigned(in.h * in.w);
+  const unsigned total = unsigned(in.n) * hw * cg;
+  const unsigned stride = gridDim.x * blockDim.x;
+  const float* alpha = e.alpha;
+  const float* beta = e.beta;
+  const int binop = e.binop, act2 = e.act2;
+  for (unsigned i0 = blockIdx.x * blockDim.x + threadIdx.x; i0 < total; i0 += 2 * stride) {
+    float v[2][8];
+    unsigned pix[2], c[2];
+    bool ok[2];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {                     // both loads issued before any math
+      const unsigned idx = i0 + u * stride;
+      ok[u] = idx < total;
+      pix[u] = ok[u] ? idx / cg : 0u;
+      c[u] = (ok[u] ? idx - pix[u] * cg : 0u) * 8u;
+      if (ok[u]) ld8<T>(in.base, view_pixel_index(in, pix[u], int(c[u])), v[u]);
+    }
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      if (!ok[u]) continue;
+      float* x = v[u];
+      const int cc = int(c[u]);
+      if (alpha) {
+        const float4 a0 = *reinterpret_cast<const float4*>(alpha + cc), a1 = *reinterpret_cast<const float4*>(alpha + cc + 4);
+        x[0] *= a0.x; x[1] *= a0.y; x[2] *= a0.z; x[3] *= a0.w; x[4] *= a1.x; x[5] *= a1.y; x[6] *= a1.z; x[7] *= a1.w;
+      }
+      if (beta) {
+        const float4 b0 = *reinterpret_cast<const float4*>(beta + cc), b1 = *reinterpret_cast<const float4*>(beta + cc + 4);
+        x[0] += b0.x; x[1] += b0.y; x[2] += b0.z; x[3] += b0.w; x[4] += b1.x; x[5] += b1.y; x[6] += b1.z; x[7] += b1.w;
+      }
+      act8_t<ACT1>(x);
+      if (binop != DFX_BIN_NONE) {
+        const int n = int(pix[u] / hw);
+        float o[8];
+        ld8<T>(e.other.base, binop == DFX_BIN_ADD ? view_pixel_index(e.other, pix[u], cc)
+                                                  : int64_t(n) * e.other.pitch + e.other.coff + cc, o);
+        if (binop == DFX_BIN_ADD) {
+#pragma unroll
+          for (int i = 0; i < 8; ++i) x[i] += o[i];
+        } else {
+#pragma unroll
+          for (int i = 0; i < 8; ++i) x[i] *= o[i];
+        }
+      }
+      if (act2 == DFX_ACT_RELU) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) x[i] = fmaxf(x[i], 0.0f);
+      } else if (act2 != DFX_ACT_NONE) {
+        act8(act2, x);
+      }
+      st8<T>(out.base, view_pixel_index(out, pix[u], cc), x);
+    }
+  }
+}
+
+#define DFX_EW_INST(T)                                                                            \
+  template __global__ void ew_vec_kernel<T, DFX_ACT_NONE>(const __grid_constant__ dfx_ew_params);  \
+  template __global__ void ew_vec_kernel<T, DFX_ACT_RELU>(const __grid_constant__ dfx_ew_params);  \
+  template __global__ void ew_vec_kernel<T, DFX_ACT_HARDSWISH>(const __grid_constant__ dfx_ew_params); \
+  template __global__ void ew_vec_kernel<T, DFX_ACT_HARDSIGMOID>(const __grid_constant__ dfx_ew_params); \
+  template __global__ void ew_vec_kernel<T, DFX_ACT_SILU>(const __grid_constant__ dfx_ew_params);  \
+  template __global__ void ew_vec_kernel<T, DFX_ACT_SIGMOID>(const __grid_constant__ dfx_ew_params); \
+  template __global__ void ew_vec_kernel<T, DFX_ACT_GELU>(const __grid_constant__ dfx_ew_params);
+DFX_EW_INST(__half)
+DFX_EW_INST(__nv_bfloat16)
+#undef DFX_EW_INST
 
 // ------------------------------------------------------------------ depthwise conv (tiled)
 // Square K x K depthwise conv with stride S (the 3x3 / 5x5, stride 1 / 2 layers
