@@ -134,7 +134,23 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kSeThreads)
     const int c = c_lo + g * 8;
     const int nl = min(8, c_hi - c);
     const int64_t base = view_pixel_index(in, int64_t(n) * hw, c);
-    if (nl == 8 && ((in.coff + c) & 7) == 0) {
+    if (cache_x && nl == 8) {
+      // every 16-B chunk of this thread's pixels as one async copy into the x tile:
+      // all in flight at once (one L2 round trip instead of one per 4 loads), then
+      // pooled from smem; the scale pass reuses the tile
+      const T* ib = reinterpret_cast<const T*>(in.base) + base;
+      for (int s = y; s < hw; s += stripes)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(xt + s * nch + g * 8)),
+                     "l"(ib + int64_t(s) * in.pitch)
+                     : "memory");
+      asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
+      for (int s = y; s < hw; s += stripes) {
+        float x[8];
+        unpack8<T>(*reinterpret_cast<const uint4*>(xt + s * nch + g * 8), x);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) acc[i] += x[i];
+      }
+    } else if (nl == 8 && ((in.coff + c) & 7) == 0) {
       const T* ib = reinterpret_cast<const T*>(in.base) + base;
       int s = y;
       for (; s + 3 * stripes < hw; s += 4 * stripes) {      // 4 independent 16-B loads
