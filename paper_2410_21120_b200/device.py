@@ -283,7 +283,9 @@ class MemberPlan:
     tilings: dict[int, dict]    # launch index -> gemm tiling
 
 
-def plan_member(prog: MemberProgram, n: int, sm_count: int = 148) -> MemberPlan:
+def plan_member(prog: MemberProgram, n: int, sm_count: int = 148, cluster_ok: bool = False) -> MemberPlan:
+    """Activation plan + GEMM tilings of one member at batch n.  ``cluster_ok``: the
+    DAG is small enough for cluster split-K (lower.SPLITK_MODE "auto")."""
     ivs = [LiveInterval(str(b.bid).zfill(6), b.bytes_for(n), b.first, b.last)
            for b in prog.buffers]
     places = first_fit(ivs, align=ALIGN)
@@ -298,9 +300,9 @@ def plan_member(prog: MemberProgram, n: int, sm_count: int = 148) -> MemberPlan:
             continue
         out = prog.values[L.dst]
         if L.geom.get("tokens"):        # token rows of all images are one contiguous M
-            t = gemm_tiling(L.geom, 1, 1, n * out.w, sm_count)
+            t = gemm_tiling(L.geom, 1, 1, n * out.w, sm_count, cluster_ok=cluster_ok and n <= 2)
         else:
-            t = gemm_tiling(L.geom, n, out.h, out.w, sm_count)
+            t = gemm_tiling(L.geom, n, out.h, out.w, sm_count, cluster_ok=cluster_ok)
         tilings[L.index] = t
         if t["splits"] > 1 and not t["csplit"]:      # cluster split-K needs no workspace
             ws = max(ws, t["splits"] * n * out.h * out.w * t["nt"] * t["bn"] * 4)
@@ -318,7 +320,10 @@ class ExecInstance:
         progs, arena = dag.programs, dag.arena
         rt.init_device(dag.device)
         self.stream = rt.stream_create()
-        self.plans = [plan_member(p, n, dag.sm_count) if n > 0 else MemberPlan([], 0, 0, {})
+        # cluster split-K only in small concurrent DAGs: its clusters need free GPC
+        # slices, which many concurrent branches rarely leave
+        cluster_ok = sum(1 for n in batch if n > 0) <= 4
+        self.plans = [plan_member(p, n, dag.sm_count, cluster_ok) if n > 0 else MemberPlan([], 0, 0, {})
                       for p, n in zip(progs, batch)]
         seq = dag.mode == "sequential"
         # activation arena: disjoint member segments (concurrent) or overlaid (sequential)

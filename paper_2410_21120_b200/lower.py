@@ -835,9 +835,10 @@ SPLIT_MIN_STAGES = int(os.environ.get("DFX_SPLIT_MIN_STAGES", "4"))   # K stages
 # inside the GEMM (dfx_gemm.cu, <= 8 splits; removes 245 of 928 launches at batch 1
 # but measured no faster: 2.651 vs 2.635 ms fused, 4.539 vs 4.617 ms sequential --
 # the splitk launch overlaps the GEMM tail under PDL, cluster co-scheduling does not);
-# "fixup" = last-arriving CTA reduces (A/B); "auto" = cluster at batch <= 2 (4-model
-# batch 1 2.40 -> 2.37 ms, but the 8-model batch-1 DAG 2.80 -> 3.14 ms), kernel above
-SPLITK_MODE = os.environ.get("DFX_SPLITK", "kernel")
+# "fixup" = last-arriving CTA reduces (A/B, 2.28 -> 3.11 ms); "auto" (default) = cluster
+# at batch <= 2 in DAGs of <= 4 members (4-model batch 1 2.27 -> 2.23 ms; with 8
+# concurrent members the clusters wait for free GPC slices: 2.71 -> 3.12 ms), kernel else
+SPLITK_MODE = os.environ.get("DFX_SPLITK", "auto")
 # fuse depthwise conv -> SE -> channel scale into one dwse launch (DFX_FUSE_DWSE=1: on, A/B).
 # Off by default: one 16-CTA cluster per image starves the depthwise phase of SMs
 # (EfficientNetV2-L alone, batch 1: 2.85 vs 2.29 ms; batch 32: 7.54 vs 6.95 ms)
@@ -859,7 +860,7 @@ FOLD_PRE = os.environ.get("DFX_FOLD_PRE", "0") == "1"
 SPLITK_CLUSTER_MAX = 8
 
 
-def gemm_tiling(geom: dict, n: int, p: int, q: int, sm_count: int = 148) -> dict:
+def gemm_tiling(geom: dict, n: int, p: int, q: int, sm_count: int = 148, cluster_ok: bool = False) -> dict:
     tn, tp, tq = choose_m_tile(n, p, q, geom["sh"], geom["sw"])
     mt = (math.ceil(n / tn), math.ceil(p / tp), math.ceil(q / tq))
     bn, nt = choose_bn(geom["cout"])
@@ -890,7 +891,7 @@ def gemm_tiling(geom: dict, n: int, p: int, q: int, sm_count: int = 148) -> dict
     tiles = (math.ceil(m_tiles / 2) if m2 else m_tiles) * nt * splits
     # cluster split-K when the splits fit one portable cluster; wider splits keep the
     # workspace + splitk_kernel reduction
-    csplit = int((SPLITK_MODE == "cluster" or (SPLITK_MODE == "auto" and n <= 2))
+    csplit = int((SPLITK_MODE == "cluster" or (SPLITK_MODE == "auto" and n <= 2 and cluster_ok))
                  and 1 < splits <= SPLITK_CLUSTER_MAX)
     return dict(tn=tn, tp=tp, tq=tq, mt_n=mt[0], mt_p=mt[1], mt_q=mt[2], bn=bn, nt=nt, csplit=csplit,
                 kpack=kpack, stages=stages, splits=splits, sps=sps, m2=m2,
