@@ -145,6 +145,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   __syncthreads();
   tc_fence_after();
   if (threadIdx.x == 0) DFX_TL(10);                // prologue barrier passed
+  if (L.flags & 16) griddep_launch();              // A/B: release the successor's prologue early
   const uint32_t tmem_base = hdr->tmem_base;
   const dfx_gemm_desc& D = hdr->desc;
 
@@ -372,7 +373,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   __syncthreads();                             // accumulator complete, epilogue vectors visible
   if (threadIdx.x == 0) DFX_TL(5);             // accumulator complete
   tc_fence_after();
-  griddep_launch();                            // successor may start its prologue now
+  if (!(L.flags & 16)) griddep_launch();       // successor may start its prologue now
 
   const int row = threadIdx.x & 127;           // tile row == TMEM lane (warps w, w+4 share it)
   const int qi = row % tq;

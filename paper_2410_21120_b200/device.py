@@ -80,6 +80,7 @@ SE_UNSTAGED_BATCH = int(os.environ.get("DFX_SE_UNSTAGED_BATCH", "8"))
 # (4-model batch 32 12.3 -> 13.3 ms, 8-model batches 1..8 6.6 -> 7.3 ms), so off
 NODE_PRIORITY = os.environ.get("DFX_PRIORITY", "1") != "0"
 PRIORITY_MAX_BATCH = 2
+GEMM_EARLY_PDL = os.environ.get("DFX_GEMM_EARLY_PDL", "0") == "1"            # A/B switch
 GEMM_DRAIN_STAGED = os.environ.get("DFX_GEMM_DRAIN", "direct") == "staged"   # A/B switch
 
 
@@ -588,6 +589,8 @@ class ExecInstance:
                     gl.nslots = 4
             if GEMM_DRAIN_STAGED:
                 gl.flags |= 4                # smem-transposed epilogue drain (A/B)
+            if GEMM_EARLY_PDL:
+                gl.flags |= 16               # launch_dependents right after the prologue (A/B)
             gl.desc0 = d                    # single problem: descriptor in kernel-param space
             yield rt.OP_GEMM, gl
             if t["splits"] > 1 and not fixup and not csplit:
