@@ -326,7 +326,8 @@ int config_for(int op, const void* params, size_t size, LaunchCfg* c) {
       c->smem = (p->apply & 2) ? 0 : size_t(dfx::se_smem_bytes(p->in.c, p->cr, cl));
       // room for the CTA's x slice (latency-bound small batches): the scale reads smem
       // (batch 1: EfficientNetV2-L 2.10 -> 2.08 ms; at batch 32 it costs occupancy)
-      if ((p->apply & 1) && ipi == 1 && p->in.n < 8) {
+      static const int xt_batch = getenv("DFX_SE_XTILE_BATCH") ? atoi(getenv("DFX_SE_XTILE_BATCH")) : 8;
+      if ((p->apply & 1) && ipi == 1 && p->in.n < xt_batch) {
         const size_t xt = size_t(p->in.h) * p->in.w * dfx::se_chan_slice(p->in.c, cl) * 2;
         if (c->smem + xt <= size_t(dfx::kSeSmemBudget)) c->smem += xt;
       }
