@@ -218,28 +218,49 @@ __global__ void __launch_bounds__(kPersistThreads, 1)
         }
       }
     } else {
-    int lt = 0;
+    // tile coordinates advance as a mixed-radix counter (q, p, n, N tile) by `grid`
+    // per step, the accumulator ring index and phase likewise: the per-tile integer
+    // divisions were a quarter of the drain's instructions on narrow (bn = 64) layers
+    const int mt_n = D.mt_n;
+    int cq, cp, cn, cnt;
+    int dq, dp, dn, dnt;
+    {
+      int t = blockIdx.x;
+      cq = t % mt_q; t /= mt_q; cp = t % mt_p; t /= mt_p; cn = t % mt_n; cnt = t / mt_n;
+      t = grid;
+      dq = t % mt_q; t /= mt_q; dp = t % mt_p; t /= mt_p; dn = t % mt_n; dnt = t / mt_n;
+    }
+    int lt = 0, b = 0;
+    uint32_t aph = 0;
     for (int tile = blockIdx.x; tile < total; tile += grid, ++lt) {
-      if (alt && (lt % groups) != group) continue;
-      const int b = lt % nacc;
-      const int mi = tile % mt_total, ntile = tile / mt_total;
-      const int n0 = (mi / (mt_q * mt_p)) * tn, p0 = ((mi / mt_q) % mt_p) * tp, q0 = (mi % mt_q) * tq;
-      const int co_base = ntile * bn;
+      const int n0 = cn * tn, p0 = cp * tp, q0 = cq * tq;
+      const int co_base = cnt * bn;
+      const int bcur = b;
+      const uint32_t phcur = aph;
+      {                                               // advance to this CTA's next tile
+        int c = 0;
+        cq += dq; if (cq >= mt_q) { cq -= mt_q; c = 1; }
+        cp += dp + c; c = 0; if (cp >= mt_p) { cp -= mt_p; c = 1; }
+        cn += dn + c; c = 0; if (cn >= mt_n) { cn -= mt_n; c = 1; }
+        cnt += dnt + c;
+        if (++b == nacc) { b = 0; aph ^= 1u; }
+      }
+      if (alt && (lt & 1) != group) continue;
       const int on = n0 + ni, op = p0 + pi_, oq = q0 + qi;
       const bool valid = row < tn * tp * tq && on < N && op < P && oq < Q;
       const int64_t pix = (int64_t(on) * P + op) * Q + oq;
       const int ncols = min(bn, ((cout - co_base) + 15) & ~15);
       if (tile + grid >= total) griddep_launch();     // this CTA's last tile
-      mbar_wait(&hdr->acc_full[b], (lt / nacc) & 1);
+      mbar_wait(&hdr->acc_full[bcur], phcur);
       tc_fence_after();
       if (!(L.flags & 4))
-        drain_rows_direct<T>(lane_addr + uint32_t(b * bn), ncols, pix, on, valid, co_base, cout, e, o,
+        drain_rows_direct<T>(lane_addr + uint32_t(bcur * bn), ncols, pix, on, valid, co_base, cout, e, o,
                              views_vec, nullptr, 0, c_first, c_step);
       else
-        drain_rows<T>(lane_addr + uint32_t(b * bn), stg, ncols, pix, on, valid, co_base, cout, e, o,
+        drain_rows<T>(lane_addr + uint32_t(bcur * bn), stg, ncols, pix, on, valid, co_base, cout, e, o,
                       views_vec, nullptr, 0, c_first, c_step);
       tc_fence_before();
-      mbar_arrive(&hdr->acc_empty[b]);                // buffer b may be overwritten
+      mbar_arrive(&hdr->acc_empty[bcur]);             // buffer may be overwritten
     }
     }
   }
