@@ -126,6 +126,45 @@ DFX_DEV void drain_rows_direct_t(uint32_t taddr, int ncols, int64_t pix, int img
   const void* const xbase = e.other.base;
   const int64_t xrow = binop == DFX_BIN_ADD ? pix * e.other.pitch + e.other.coff
                                             : int64_t(img) * e.other.pitch + e.other.coff;
+  if (ws == nullptr && views_vec && co_base + ncols <= cout && binop == DFX_BIN_NONE &&
+      act2 == DFX_ACT_NONE && (alpha == nullptr || beta != nullptr)) {
+    // the common conv epilogue (bias / folded-BN shift, one activation, 16-B stores)
+    // as a branch-free loop: per-chunk checks and reconvergence points were a
+    // third of its instructions
+    for (int c0 = c_first; c0 < ncols; c0 += c_step) {
+      uint32_t r[16];
+      tmem_ld16_issue(taddr + uint32_t(c0), r);
+      tmem_ld_wait(r);
+      float v[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+      const int co = co_base + c0;
+      if (alpha != nullptr) {                       // folded BN: one FFMA per element
+        const float4* aq = reinterpret_cast<const float4*>(alpha + co);
+        const float4* bq = reinterpret_cast<const float4*>(beta + co);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const float4 a4 = aq[q], b4 = bq[q];
+          v[4 * q] = fmaf(v[4 * q], a4.x, b4.x); v[4 * q + 1] = fmaf(v[4 * q + 1], a4.y, b4.y);
+          v[4 * q + 2] = fmaf(v[4 * q + 2], a4.z, b4.z); v[4 * q + 3] = fmaf(v[4 * q + 3], a4.w, b4.w);
+        }
+      } else if (beta != nullptr) {
+        const float4* bq = reinterpret_cast<const float4*>(beta + co);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const float4 b4 = bq[q];
+          v[4 * q] += b4.x; v[4 * q + 1] += b4.y; v[4 * q + 2] += b4.z; v[4 * q + 3] += b4.w;
+        }
+      }
+      act8_t<ACT1>(v);
+      act8_t<ACT1>(v + 8);
+      if (valid) {
+        st8<T>(obase, orow + co, v);
+        st8<T>(obase, orow + co + 8, v + 8);
+      }
+    }
+    return;
+  }
   for (int c0 = c_first; c0 < ncols; c0 += c_step) {
     uint32_t r[16];
     tmem_ld16_issue(taddr + uint32_t(c0), r);
