@@ -126,8 +126,10 @@ DFX_DEV void drain_rows_direct_t(uint32_t taddr, int ncols, int64_t pix, int img
   const void* const xbase = e.other.base;
   const int64_t xrow = binop == DFX_BIN_ADD ? pix * e.other.pitch + e.other.coff
                                             : int64_t(img) * e.other.pitch + e.other.coff;
-  if (ws == nullptr && views_vec && co_base + ncols <= cout && binop == DFX_BIN_NONE &&
+  if (ws == nullptr && views_vec && co_base + ncols <= cout &&
+      (binop == DFX_BIN_NONE || binop == DFX_BIN_ADD) &&
       act2 == DFX_ACT_NONE && (alpha == nullptr || beta != nullptr)) {
+    const bool res = binop == DFX_BIN_ADD;
     // the common conv epilogue (bias / folded-BN shift, one activation, 16-B stores)
     // as a branch-free loop: per-chunk checks and reconvergence points were a
     // third of its instructions
@@ -159,6 +161,13 @@ DFX_DEV void drain_rows_direct_t(uint32_t taddr, int ncols, int64_t pix, int img
       act8_t<ACT1>(v);
       act8_t<ACT1>(v + 8);
       if (valid) {
+        if (res) {                                  // residual add (ResNet / MBConv projections)
+          float x[16];
+          ld8<T>(xbase, xrow + co, x);
+          ld8<T>(xbase, xrow + co + 8, x + 8);
+#pragma unroll
+          for (int i = 0; i < 16; ++i) v[i] += x[i];
+        }
         st8<T>(obase, orow + co, v);
         st8<T>(obase, orow + co + 8, v + 8);
       }
