@@ -22,7 +22,7 @@ template <typename T> __global__ void splitk_kernel(const __grid_constant__ dfx_
 template <typename T> __global__ void ew_kernel(const __grid_constant__ dfx_ew_params P);
 template <typename T, int ACT1> __global__ void ew_vec_kernel(const __grid_constant__ dfx_ew_params P);
 template <typename T> __global__ void dwconv_kernel(const __grid_constant__ dfx_dwconv_params P);
-template <typename T, int K, int S, int QV>
+template <typename T, int K, int S, int QV, int ACT>
 __global__ void dwconv_tile_kernel(const __grid_constant__ dfx_dwconv_params P);
 template <typename T> __global__ void pool_kernel(const __grid_constant__ dfx_pool_params P);
 template <typename T> __global__ void gap_kernel(const __grid_constant__ dfx_gap_params P);
@@ -62,19 +62,31 @@ const void* se_func(int dt, int cl, int ipi = 1) {
                        : reinterpret_cast<const void*>(&dfx::se_kernel<__nv_bfloat16, 8, 1>);
 }
 
-template <typename T>
-const void* dwconv_tile_func_t(int k, int s, int qv) {
-#define DFX_DW_CASE(K, S)                                                                 \
-  if (k == K && s == S)                                                                   \
-    return qv == 4 ? reinterpret_cast<const void*>(&dfx::dwconv_tile_kernel<T, K, S, 4>)  \
-         : qv == 2 ? reinterpret_cast<const void*>(&dfx::dwconv_tile_kernel<T, K, S, 2>)  \
-                   : reinterpret_cast<const void*>(&dfx::dwconv_tile_kernel<T, K, S, 1>);
+template <typename T, int A>
+const void* dwconv_tile_func_a(int k, int s, int qv) {
+#define DFX_DW_CASE(K, S)                                                                    \
+  if (k == K && s == S)                                                                      \
+    return qv == 4 ? reinterpret_cast<const void*>(&dfx::dwconv_tile_kernel<T, K, S, 4, A>)  \
+         : qv == 2 ? reinterpret_cast<const void*>(&dfx::dwconv_tile_kernel<T, K, S, 2, A>)  \
+                   : reinterpret_cast<const void*>(&dfx::dwconv_tile_kernel<T, K, S, 1, A>);
   DFX_DW_CASE(3, 1)
   DFX_DW_CASE(3, 2)
   DFX_DW_CASE(5, 1)
   DFX_DW_CASE(5, 2)
 #undef DFX_DW_CASE
   return nullptr;
+}
+// the epilogue's first activation is a template parameter (the switch per 8 outputs
+// was a large share of the kernel's instructions); other activations take NONE's
+// instantiation, whose epilogue falls back to the generic switch
+template <typename T>
+const void* dwconv_tile_func_t(int k, int s, int qv, int act) {
+  switch (act) {
+    case DFX_ACT_RELU: return dwconv_tile_func_a<T, DFX_ACT_RELU>(k, s, qv);
+    case DFX_ACT_HARDSWISH: return dwconv_tile_func_a<T, DFX_ACT_HARDSWISH>(k, s, qv);
+    case DFX_ACT_SILU: return dwconv_tile_func_a<T, DFX_ACT_SILU>(k, s, qv);
+    default: return dwconv_tile_func_a<T, DFX_ACT_NONE>(k, s, qv);
+  }
 }
 template <typename T>
 const void* ew_vec_func_t(int act) {
@@ -91,8 +103,9 @@ const void* ew_vec_func_t(int act) {
 const void* ew_vec_func(int dt, int act) {
   return dt == DFX_F16 ? ew_vec_func_t<__half>(act) : ew_vec_func_t<__nv_bfloat16>(act);
 }
-const void* dwconv_tile_func(int dt, int k, int s, int qv) {
-  return dt == DFX_F16 ? dwconv_tile_func_t<__half>(k, s, qv) : dwconv_tile_func_t<__nv_bfloat16>(k, s, qv);
+const void* dwconv_tile_func(int dt, int k, int s, int qv, int act) {
+  return dt == DFX_F16 ? dwconv_tile_func_t<__half>(k, s, qv, act)
+                       : dwconv_tile_func_t<__nv_bfloat16>(k, s, qv, act);
 }
 
 thread_local std::string g_err;
@@ -238,7 +251,7 @@ int config_for(int op, const void* params, size_t size, LaunchCfg* c) {
         const int64_t rows = int64_t(p->out.n) * p->out.h * (p->in.c / 8);
         int qv = 4;
         while (qv > 1 && rows * cdiv(p->out.w, qv) < int64_t(2) * g_sm_count * 256) qv >>= 1;
-        c->func = dwconv_tile_func(p->in.dtype, k, st, qv);
+        c->func = dwconv_tile_func(p->in.dtype, k, st, qv, p->epi.act1);
         c->grid = dim3(elementwise_grid(rows * cdiv(p->out.w, qv), 256));
         return DFX_OK;
       }

@@ -137,7 +137,7 @@ DFX_EW_INST(__nv_bfloat16)
 // registers, and all index math is 32-bit (the generic kernel below spends
 // most of its issue slots on 64-bit divisions).  Same fold order as the
 // generic kernel: for every output, (ki, kj) ascending.
-template <typename T, int K, int S, int QV>
+template <typename T, int K, int S, int QV, int ACT>
 __global__ void __launch_bounds__(256) dwconv_tile_kernel(const __grid_constant__ dfx_dwconv_params P) {
   griddep_wait();
   griddep_launch();
@@ -198,16 +198,37 @@ __global__ void __launch_bounds__(256) dwconv_tile_kernel(const __grid_constant_
       const int q = q0 + v;
       if (q >= OW) break;
       const int64_t pix = (int64_t(n) * OH + p) * OW + q;
-      epilogue8<T>(P.epi, acc[v], pix, n, c);
+      if (P.epi.binop == DFX_BIN_NONE && P.epi.act2 == DFX_ACT_NONE && P.epi.act1 == ACT) {
+        // folded BN + the (template) activation: no per-element switch
+        float* x = acc[v];
+        const float* al = P.epi.alpha;
+        const float* be = P.epi.beta;
+        if (al) {
+          const float4 a0 = *reinterpret_cast<const float4*>(al + c), a1 = *reinterpret_cast<const float4*>(al + c + 4);
+          x[0] *= a0.x; x[1] *= a0.y; x[2] *= a0.z; x[3] *= a0.w; x[4] *= a1.x; x[5] *= a1.y; x[6] *= a1.z; x[7] *= a1.w;
+        }
+        if (be) {
+          const float4 b0 = *reinterpret_cast<const float4*>(be + c), b1 = *reinterpret_cast<const float4*>(be + c + 4);
+          x[0] += b0.x; x[1] += b0.y; x[2] += b0.z; x[3] += b0.w; x[4] += b1.x; x[5] += b1.y; x[6] += b1.z; x[7] += b1.w;
+        }
+        act8_t<ACT>(x);
+      } else {
+        epilogue8<T>(P.epi, acc[v], pix, n, c);
+      }
       st8<T>(out.base, view_pixel_index(out, pix, c), acc[v]);
     }
   }
 }
 
-#define DFX_DW_INST(T, K, S)                                                                         \
-  template __global__ void dwconv_tile_kernel<T, K, S, 1>(const __grid_constant__ dfx_dwconv_params); \
-  template __global__ void dwconv_tile_kernel<T, K, S, 2>(const __grid_constant__ dfx_dwconv_params); \
-  template __global__ void dwconv_tile_kernel<T, K, S, 4>(const __grid_constant__ dfx_dwconv_params);
+#define DFX_DW_INST_A(T, K, S, A)                                                                    \
+  template __global__ void dwconv_tile_kernel<T, K, S, 1, A>(const __grid_constant__ dfx_dwconv_params); \
+  template __global__ void dwconv_tile_kernel<T, K, S, 2, A>(const __grid_constant__ dfx_dwconv_params); \
+  template __global__ void dwconv_tile_kernel<T, K, S, 4, A>(const __grid_constant__ dfx_dwconv_params);
+#define DFX_DW_INST(T, K, S)                   \
+  DFX_DW_INST_A(T, K, S, DFX_ACT_NONE)         \
+  DFX_DW_INST_A(T, K, S, DFX_ACT_RELU)         \
+  DFX_DW_INST_A(T, K, S, DFX_ACT_HARDSWISH)    \
+  DFX_DW_INST_A(T, K, S, DFX_ACT_SILU)
 DFX_DW_INST(__half, 3, 1)
 DFX_DW_INST(__half, 3, 2)
 DFX_DW_INST(__half, 5, 1)
@@ -216,6 +237,7 @@ DFX_DW_INST(__nv_bfloat16, 3, 1)
 DFX_DW_INST(__nv_bfloat16, 3, 2)
 DFX_DW_INST(__nv_bfloat16, 5, 1)
 DFX_DW_INST(__nv_bfloat16, 5, 2)
+#undef DFX_DW_INST_A
 #undef DFX_DW_INST
 
 // ------------------------------------------------------------------ depthwise conv (generic)
