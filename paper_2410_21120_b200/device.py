@@ -80,6 +80,8 @@ SE_UNSTAGED_BATCH = int(os.environ.get("DFX_SE_UNSTAGED_BATCH", "8"))
 # (4-model batch 32 12.3 -> 13.3 ms, 8-model batches 1..8 6.6 -> 7.3 ms), so off
 NODE_PRIORITY = os.environ.get("DFX_PRIORITY", "1") != "0"
 PRIORITY_MAX_BATCH = 2
+# persistent GEMM for grids above this many waves (A/B knob)
+PERSIST_MIN_WAVES = float(os.environ.get("DFX_PERSIST_MIN_WAVES", "2"))
 GEMM_EARLY_PDL = os.environ.get("DFX_GEMM_EARLY_PDL", "0") == "1"            # A/B switch
 GEMM_DRAIN_STAGED = os.environ.get("DFX_GEMM_DRAIN", "direct") == "staged"   # A/B switch
 
@@ -577,7 +579,8 @@ class ExecInstance:
                 gl.flags |= 8                # cluster split-K (DSMEM reduction, no splitk node)
                 need = 128 * (t["bn"] + 4) * 4          # the fp32 partial tile parks in the slots
                 gl.nslots = max(gl.nslots, -(-need // (128 * 64 * 2 + t["bn"] * 128)))
-            if GEMM_PERSIST and not gl.m2 and t["splits"] == 1 and t["tiles"] > 2 * self.dag.sm_count:
+            if GEMM_PERSIST and not gl.m2 and t["splits"] == 1 and \
+                    t["tiles"] > PERSIST_MIN_WAVES * self.dag.sm_count:
                 gl.flags |= 2                # persistent kernel for multi-wave layers
                 # bn > 64: one CTA per SM, as deep a ring as smem allows; bn <= 64: two
                 # CTAs per SM (dfx_api.cu), 4 slots each
