@@ -81,3 +81,24 @@ def test_batch_one_matches_batched(models):
     single = fuse.execute_fused(dag, {g.model_id: Tensor(g.input_spec, x[2])})[g.model_id]
     err = np.abs(batched[2].values - single.values).max() / np.abs(single.values).max()
     assert err < 1e-2
+
+
+# bf16 storage through the real architectures' kernels (SiLU / hardswish drains,
+# templated depthwise, SE with the fused scale, persistent GEMM at batch 8)
+@pytest.mark.parametrize("name,n", [("mobilenet_v3_large", 2), ("efficientnet_v2_l", 8)])
+def test_zoo_bf16_storage(name, n):
+    import numpy as np
+    from oracle.executor_ref import run_fast
+    from paper_2410_21120_b200 import fuse, zoo
+    from paper_2410_21120_b200.executor import Tensor
+    g, w = zoo.build(name)
+    dag = fuse.fuse_models([(g, w)])
+    fuse.load_fused(dag, precision="bf16")
+    rng = np.random.default_rng(23)
+    xs = rng.standard_normal((n,) + tuple(g.input_spec.dims)).astype(np.float32)
+    out = fuse.execute_fused(dag, {g.model_id: [Tensor(g.input_spec, x) for x in xs]})[g.model_id]
+    ref = run_fast(g, w, xs)
+    for t, r in zip(out, ref):
+        r = np.asarray(r, np.float64).reshape(-1)
+        assert np.abs(t.values - r).max() <= 6e-2 * np.abs(r).max()
+    fuse.unload(dag)
