@@ -303,22 +303,24 @@ __global__ void dwconv_kernel(const __grid_constant__ dfx_dwconv_params P) {
 }
 
 // ------------------------------------------------------------------ pooling
-template <typename T>
-__global__ void pool_kernel(const __grid_constant__ dfx_pool_params P) {
-  griddep_wait();
-  griddep_launch();
+// Index type I: 32-bit when the item count allows (64-bit divisions per item were
+// most of the instructions of the bandwidth-bound pools), else 64-bit.
+template <typename T, typename I>
+__device__ __forceinline__ void pool_body(const dfx_pool_params& P) {
   const dfx_view& in = P.in;
   const dfx_view& out = P.out;
   const int C = in.c;
   const int cg = (C + 7) / 8;
-  const int64_t total = int64_t(out.n) * out.h * out.w * cg;
+  const I total = I(out.n) * I(out.h) * I(out.w) * I(cg);
   const bool vec = ((in.coff | out.coff) & 7) == 0;
-  for (int64_t idx = grid_stride_start(); idx < total; idx += grid_stride_step()) {
-    const int64_t pix = idx / cg;
-    const int c = int(idx - pix * cg) * 8;
-    const int q = int(pix % out.w);
-    const int p = int((pix / out.w) % out.h);
-    const int n = int(pix / (int64_t(out.w) * out.h));
+  for (I idx = I(blockIdx.x) * blockDim.x + threadIdx.x; idx < total; idx += I(gridDim.x) * blockDim.x) {
+    const I pixi = idx / I(cg);
+    const int c = int(idx - pixi * I(cg)) * 8;
+    const int q = int(pixi % I(out.w));
+    const I pr = pixi / I(out.w);
+    const int p = int(pr % I(out.h));
+    const int n = int(pr / I(out.h));
+    const int64_t pix = int64_t(pixi);
     const int h0 = p * P.stride_h - P.pad_h;
     const int w0 = q * P.stride_w - P.pad_w;
     const int nl = min(8, C - c);
@@ -359,6 +361,17 @@ __global__ void pool_kernel(const __grid_constant__ dfx_pool_params P) {
       for (int i = 0; i < nl; ++i) st1<T>(out.base, view_pixel_index(out, pix, c + i), acc[i]);
     }
   }
+}
+
+template <typename T>
+__global__ void pool_kernel(const __grid_constant__ dfx_pool_params P) {
+  griddep_wait();
+  griddep_launch();
+  const int64_t total = int64_t(P.out.n) * P.out.h * P.out.w * ((P.in.c + 7) / 8);
+  if (total < (int64_t(1) << 31))
+    pool_body<T, uint32_t>(P);
+  else
+    pool_body<T, int64_t>(P);
 }
 
 // ------------------------------------------------------------------ global average pool
