@@ -829,6 +829,7 @@ def choose_bn(cout: int) -> tuple[int, int]:
 
 
 GEMM_M2 = os.environ.get("DFX_GEMM_M2", "1") != "0"     # A/B switch for 256-row CTAs
+BN_FLOOR_MANY_M = int(os.environ.get("DFX_BN_FLOOR_MANY_M", "64"))   # A/B knob
 SPLIT_MIN_STAGES = int(os.environ.get("DFX_SPLIT_MIN_STAGES", "4"))   # K stages per split, at least
 # split-K reduction: "kernel" (default) = fp32 workspace + a splitk_kernel launch;
 # "cluster" = the splits of a tile form a thread-block cluster and reduce over DSMEM
@@ -866,8 +867,11 @@ def gemm_tiling(geom: dict, n: int, p: int, q: int, sm_count: int = 148, cluster
     bn, nt = choose_bn(geom["cout"])
     m_tiles = mt[0] * mt[1] * mt[2]
     # small-M layers: narrower N tiles first (more CTAs, no extra kernel), split-K second
-    while m_tiles * nt < sm_count and bn > 64:
-        bn = max(64, round_up(bn // 2, 16))
+    # (with many M tiles -- batched layers -- N stays >= BN_FLOOR_MANY_M: an N = 64 MMA
+    # costs what an N = 128 one does, so split-K keeps the tensor pipe denser)
+    bn_floor = BN_FLOOR_MANY_M if m_tiles >= 8 else 64
+    while m_tiles * nt < sm_count and bn > bn_floor:
+        bn = max(bn_floor, round_up(bn // 2, 16))
         nt = -(-geom["cout"] // bn)
     kpack = 64 // geom["cb"]
     stages = math.ceil(geom["ksteps"] / kpack)
