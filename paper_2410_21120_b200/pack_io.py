@@ -82,7 +82,8 @@ def save_packed(dag: fuse.FusedDag, path, precision: str = "fp16") -> dict:
     graphs = [fuse._as_graph(sg) for sg in dag.subgraphs]
     programs = [program_for(g, sg.weight_binding, precision) for g, sg in zip(graphs, dag.subgraphs)]
     layout, segments, total = arena_layout(programs)
-    header = dict(version=VERSION, precision=precision, dag_id=dag.dag_id, total=total, members=[
+    header = dict(version=VERSION, precision=precision, dag_id=dag.dag_id, total=total,
+                  mem_estimate_mib=dag.total_mem_estimate_mib, members=[
         dict(model_id=sg.model_id, graph=model_io.graph_to_dict(g),
              weights={n: list(sg.weight_binding.spec(n).dims) for n in sg.weight_binding.names()},
              segment=list(seg), blobs={k: int(off) for k, off in lay.items()})
@@ -201,7 +202,11 @@ def load_packed(path, device: int = 0, mode: str = "concurrent", pinned: bool = 
     arena.upload_ms = None
     arena.upload()
     t4 = time.perf_counter()
-    dag = fuse.fuse_models(members, dag_id=header["dag_id"], validate=False)
+    if "mem_estimate_mib" in header:        # the packed DAG's estimate: no profile_graph pass
+        dag = fuse.FusedDag(header["dag_id"], fuse.build_preamble(len(members), True, None),
+                            tuple(fuse._subgraph(g, w) for g, w in members), header["mem_estimate_mib"], 1)
+    else:
+        dag = fuse.fuse_models(members, dag_id=header["dag_id"], validate=False)
     img = DeviceDag([(sg, sg.weight_binding) for sg in dag.subgraphs], device, mode, arena=arena,
                     programs=programs, precision=header["precision"])
     fuse.attach_image(dag, img)

@@ -26,6 +26,7 @@ def test_load_packed_matches_fiwt_path(tmp_path, pinned):
     path = tmp_path / "dag.dfxpack"
     pack_io.save_packed(dag, path)
     packed = pack_io.load_packed(path, pinned=pinned)
+    assert packed.total_mem_estimate_mib == dag.total_mem_estimate_mib and packed.model_ids() == dag.model_ids()
     arena = fuse.device_image(packed).arena
     assert arena.read_ms > 0 and arena.memcpy_ms > 0 and arena.total == pack_io.read_header(path)[0]["total"]
     rng = np.random.default_rng(3)
