@@ -359,6 +359,14 @@ int dfx_graph_destroy(void* graph);
  * inputs, one graph launch, D2H of the packed fp32 outputs, stream sync. */
 int dfx_execute(void* graph, const void* host_in, void* dev_in, size_t in_bytes,
                 void* host_out, const void* dev_out, size_t out_bytes, void* stream);
+/* The same query with the inputs gathered from `nsrc` separate host arrays
+ * (one per member or sample, packed in list order): chunks are copied into the
+ * pinned staging buffer `host_in` on a pool of host threads
+ * (DFX_STAGE_THREADS, default half the cores) while the calling thread issues
+ * the H2D of every completed prefix, so the DMA overlaps the host copy. */
+int dfx_execute_gather(void* graph, const void* const* srcs, const size_t* sizes, int nsrc,
+                       void* host_in, void* dev_in, void* host_out, const void* dev_out,
+                       size_t out_bytes, void* stream);
 
 #ifdef __cplusplus
 }

@@ -84,6 +84,8 @@ PRIORITY_MAX_BATCH = 2
 PERSIST_MIN_WAVES = float(os.environ.get("DFX_PERSIST_MIN_WAVES", "2"))
 GEMM_EARLY_PDL = os.environ.get("DFX_GEMM_EARLY_PDL", "0") == "1"            # A/B switch
 GEMM_DRAIN_STAGED = os.environ.get("DFX_GEMM_DRAIN", "direct") == "staged"   # A/B switch
+# e2e queries gather their inputs on a host thread pool, overlapping the H2D (A/B switch)
+E2E_GATHER = os.environ.get("DFX_E2E_GATHER", "1") != "0"
 
 
 def gemm_slots(bn: int, tiles: int, sm_count: int = 148, m2: int = 0) -> int:
@@ -677,10 +679,28 @@ class ExecInstance:
         return outs
 
     def run(self, xs: list[np.ndarray]) -> list[np.ndarray]:
-        """End to end: stage -> H2D -> graph -> D2H -> sync (dfx_execute)."""
-        self.stage_inputs(xs)
-        self.graph.execute(self.host_in, self.dev_in, self.in_bytes, self.host_out, self.dev_out,
-                           self.out_bytes, self.stream)
+        """End to end: gather -> H2D -> graph -> D2H -> sync (dfx_execute_gather: the
+        host copies into the pinned staging run on a thread pool and overlap the
+        H2D).  DFX_E2E_GATHER=0: one-thread staging + dfx_execute."""
+        if not E2E_GATHER:
+            self.stage_inputs(xs)
+            self.graph.execute(self.host_in, self.dev_in, self.in_bytes, self.host_out, self.dev_out,
+                               self.out_bytes, self.stream)
+            return self.read_outputs()
+        keep = []
+        for m, x in enumerate(xs):
+            parts = x if isinstance(x, (list, tuple)) else [x]
+            total = 0
+            for t in parts:
+                a = np.ascontiguousarray(t, dtype=np.float32)
+                keep.append(a)
+                total += a.nbytes
+            if total != self.in_sizes[m]:
+                raise ValueError(f"member {m}: {total} input bytes, expected {self.in_sizes[m]}")
+        srcs = (C.c_void_p * len(keep))(*[a.ctypes.data for a in keep])
+        sizes = (C.c_size_t * len(keep))(*[a.nbytes for a in keep])
+        self.graph.execute_gather(srcs, sizes, self.host_in, self.dev_in, self.host_out, self.dev_out,
+                                  self.out_bytes, self.stream)
         return self.read_outputs()
 
     def upload_inputs(self, xs):

@@ -142,7 +142,7 @@ EXPORTS = (
     "dfx_stream_sync", "dfx_event_create", "dfx_event_destroy", "dfx_event_record",
     "dfx_event_elapsed", "dfx_tmap_act", "dfx_tmap_weights", "dfx_launch", "dfx_graph_create",
     "dfx_graph_add", "dfx_graph_set_priority", "dfx_graph_instantiate", "dfx_graph_launch", "dfx_graph_node_count",
-    "dfx_graph_destroy", "dfx_execute",
+    "dfx_graph_destroy", "dfx_execute", "dfx_execute_gather",
 )
 
 _lock = threading.Lock()
@@ -308,6 +308,11 @@ class Graph:
     def execute(self, host_in, dev_in, in_bytes, host_out, dev_out, out_bytes, stream):
         call("dfx_execute", vp(self.ptr), vp(host_in), vp(dev_in), C.c_size_t(in_bytes),
              vp(host_out), vp(dev_out), C.c_size_t(out_bytes), vp(stream))
+
+    def execute_gather(self, srcs, sizes, host_in, dev_in, host_out, dev_out, out_bytes, stream):
+        """srcs / sizes: ctypes arrays of host pointers and byte counts."""
+        call("dfx_execute_gather", vp(self.ptr), srcs, sizes, C.c_int(len(srcs)), vp(host_in),
+             vp(dev_in), vp(host_out), vp(dev_out), C.c_size_t(out_bytes), vp(stream))
 
     def destroy(self):
         if self.ptr:

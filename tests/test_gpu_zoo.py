@@ -102,3 +102,23 @@ def test_zoo_bf16_storage(name, n):
         r = np.asarray(r, np.float64).reshape(-1)
         assert np.abs(t.values - r).max() <= 6e-2 * np.abs(r).max()
     fuse.unload(dag)
+
+
+def test_gather_staging_matches_single_thread_staging(models, monkeypatch):
+    """dfx_execute_gather (inputs copied into the pinned staging on the host pool,
+    chunked H2D) gives bit-identical logits to one-thread staging + dfx_execute;
+    non-contiguous inputs are accepted, wrong sizes raise before device work."""
+    from paper_2410_21120_b200 import device
+    g, w = models[1]
+    dag = fuse.fuse_models([models[1]])
+    x = np.random.default_rng(6).standard_normal((5, 3, 224, 224)).astype(np.float32)
+    xf = [np.asfortranarray(v) for v in x]                   # non-contiguous per-sample inputs
+    monkeypatch.setattr(device, "E2E_GATHER", False)
+    ref = fuse.execute_fused(dag, {g.model_id: [Tensor(g.input_spec, v) for v in x]})[g.model_id]
+    monkeypatch.setattr(device, "E2E_GATHER", True)
+    for _ in range(3):                                       # pool reuse across queries
+        got = fuse.execute_fused(dag, {g.model_id: [Tensor(g.input_spec, v) for v in xf]})[g.model_id]
+        for a, b in zip(ref, got):
+            assert np.array_equal(a.values, b.values)
+    with pytest.raises(ValueError):
+        fuse.load_fused(dag).execute([[x[0][:, :100]]])
