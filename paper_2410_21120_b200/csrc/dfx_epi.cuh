@@ -331,3 +331,98 @@ DFX_DEV void named_bar_sync(int id, int nthreads) {
 }
 
 }  // namespace dfx
+
+namespace dfx {
+
+// ---- depthwise epilogue of a GEMM CTA (dfx_gemm_desc.dw_k > 0)
+//
+// The CTA's drain left its bn channels of the WHOLE GEMM output map in shared
+// memory (xs[((n * P + h) * Q + w) * xp + c], 16-bit, exactly the values the
+// unfused GEMM would have stored).  Depthwise convolution is channel-separable,
+// so these channels' depthwise outputs need nothing from other CTAs: no halo
+// exchange and no HBM round trip of the expanded map.  Arithmetic order is
+// dwconv_tile_kernel's (taps (ki, kj) ascending, fmaf, then * alpha + beta and
+// the activation), so fused and unfused results are bit-identical.
+template <typename T, int K, int S, int ACT>
+DFX_DEV void dw_smem_t(const dfx_gemm_desc& D, const T* xs, int xp, int N, int P, int Q, int co_base,
+                       int nch, const dfx_view& o, const float* sw, int bn, int tid, int nthr) {
+  const int OH = o.h, OW = o.w, cg = nch >> 3, C = D.cout;
+  const int total = N * OH * OW * cg;
+  // taps [K*K][bn] then alpha[bn], beta[bn] (staged in smem; identity when absent)
+  const float* const al = sw + K * K * bn;
+  const float* const be = al + bn;
+  const bool has_al = D.dw_alpha != nullptr, has_be = D.dw_beta != nullptr;
+  (void)C;
+  for (int item = tid; item < total; item += nthr) {
+    const int cgi = item % cg;
+    int t = item / cg;
+    const int q = t % OW;
+    t /= OW;
+    const int p = t % OH;
+    const int n = t / OH;
+    const int c = cgi * 8, ca = co_base + c;
+    const int h0 = p * S - D.dw_pad, w0 = q * S - D.dw_pad;
+    float acc[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) acc[i] = 0.0f;
+#pragma unroll
+    for (int ki = 0; ki < K; ++ki) {
+      const int h = h0 + ki;
+      if (h < 0 || h >= P) continue;
+      const T* row = xs + (n * P + h) * Q * xp + c;
+#pragma unroll
+      for (int kj = 0; kj < K; ++kj) {
+        const int w = w0 + kj;
+        if (w < 0 || w >= Q) continue;
+        const float4* wt = reinterpret_cast<const float4*>(sw + (ki * K + kj) * bn + c);
+        const float4 lo = wt[0], hi = wt[1];
+        const float wv[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
+        float x[8];
+        unpack8<T>(*reinterpret_cast<const uint4*>(row + w * xp), x);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) acc[i] = fmaf(wv[i], x[i], acc[i]);
+      }
+    }
+    if (has_al) {
+      const float4 a0 = *reinterpret_cast<const float4*>(al + c), a1 = *reinterpret_cast<const float4*>(al + c + 4);
+      acc[0] *= a0.x; acc[1] *= a0.y; acc[2] *= a0.z; acc[3] *= a0.w;
+      acc[4] *= a1.x; acc[5] *= a1.y; acc[6] *= a1.z; acc[7] *= a1.w;
+    }
+    if (has_be) {
+      const float4 b0 = *reinterpret_cast<const float4*>(be + c), b1 = *reinterpret_cast<const float4*>(be + c + 4);
+      acc[0] += b0.x; acc[1] += b0.y; acc[2] += b0.z; acc[3] += b0.w;
+      acc[4] += b1.x; acc[5] += b1.y; acc[6] += b1.z; acc[7] += b1.w;
+    }
+    act8_t<ACT>(acc);
+    const int64_t pix = (int64_t(n) * OH + p) * OW + q;
+    st8<T>(o.base, view_pixel_index(o, pix, ca), acc);
+  }
+}
+
+template <typename T, int K, int S>
+DFX_DEV void dw_smem_k(const dfx_gemm_desc& D, const T* xs, int xp, int N, int P, int Q, int co_base,
+                       int nch, const dfx_view& o, const float* sw, int bn, int tid, int nthr) {
+  switch (D.dw_act) {
+    case DFX_ACT_RELU: dw_smem_t<T, K, S, DFX_ACT_RELU>(D, xs, xp, N, P, Q, co_base, nch, o, sw, bn, tid, nthr); break;
+    case DFX_ACT_HARDSWISH:
+      dw_smem_t<T, K, S, DFX_ACT_HARDSWISH>(D, xs, xp, N, P, Q, co_base, nch, o, sw, bn, tid, nthr);
+      break;
+    case DFX_ACT_SILU: dw_smem_t<T, K, S, DFX_ACT_SILU>(D, xs, xp, N, P, Q, co_base, nch, o, sw, bn, tid, nthr); break;
+    default: dw_smem_t<T, K, S, DFX_ACT_NONE>(D, xs, xp, N, P, Q, co_base, nch, o, sw, bn, tid, nthr); break;
+  }
+}
+
+// dispatch on the (host-validated) square kernel size / stride: 3 or 5, 1 or 2
+template <typename T>
+DFX_DEV void dw_smem(const dfx_gemm_desc& D, const T* xs, int xp, int N, int P, int Q, int co_base, int nch,
+                     const dfx_view& o, const float* sw, int bn, int tid, int nthr) {
+  if (D.dw_k == 3) {
+    if (D.dw_s == 1) dw_smem_k<T, 3, 1>(D, xs, xp, N, P, Q, co_base, nch, o, sw, bn, tid, nthr);
+    else dw_smem_k<T, 3, 2>(D, xs, xp, N, P, Q, co_base, nch, o, sw, bn, tid, nthr);
+  } else {
+    if (D.dw_s == 1) dw_smem_k<T, 5, 1>(D, xs, xp, N, P, Q, co_base, nch, o, sw, bn, tid, nthr);
+    else dw_smem_k<T, 5, 2>(D, xs, xp, N, P, Q, co_base, nch, o, sw, bn, tid, nthr);
+  }
+}
+
+}  // namespace dfx

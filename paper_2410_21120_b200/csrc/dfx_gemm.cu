@@ -335,6 +335,20 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         if (ga) s_alpha[i] = c < cout ? ga[c] : 0.f;
         if (gb) s_beta[i] = c < cout ? gb[c] : 0.f;
       }
+      if (D.dw_k > 0) {
+        // depthwise epilogue: this CTA's taps [k*k][bn] and BN vectors, after the ring
+        float* s_dw = reinterpret_cast<float*>(slots + nslots * slot_bytes);
+        const int kk = D.dw_k * D.dw_k;
+        for (int i = ti; i < kk * bn; i += nthr) {
+          const int tap = i / bn, c = co_base + (i - tap * bn);
+          s_dw[i] = c < cout ? D.dw_w[tap * cout + c] : 0.f;
+        }
+        for (int i = ti; i < bn; i += nthr) {
+          const int c = co_base + i;
+          s_dw[kk * bn + i] = (D.dw_alpha && c < cout) ? D.dw_alpha[c] : 1.f;
+          s_dw[kk * bn + bn + i] = (D.dw_beta && c < cout) ? D.dw_beta[c] : 0.f;
+        }
+      }
     }
     if (D.pre_mode) {
       // ================= A prologue transform: rewrite each landed A stage in smem
@@ -437,6 +451,37 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     tc_fence_before();
     __syncthreads();
     if (warp == 2) tmem_dealloc(tmem_base, tmem_cols);
+    return;
+  }
+
+  if (D.dw_k > 0) {
+    // ---- depthwise epilogue: this CTA covers every M tile (host-checked), so the
+    // drain parks its channels of the whole output map in the (now free) operand
+    // slots -- the same epilogue and 16-bit rounding as a global store, through a
+    // view whose base is shared memory -- and the consumer depthwise conv runs on
+    // it (dfx_epi.cuh dw_smem).  The expanded map never goes to HBM.
+    T* xs = reinterpret_cast<T*>(slots);
+    const int xp = bn + 8;                             // row pitch: 16 B pad against bank conflicts
+    dfx_view sv = o;
+    sv.base = xs;
+    sv.n = N; sv.h = P; sv.w = Q; sv.c = bn;
+    sv.pitch = xp;
+    sv.coff = -co_base;                                // absolute channel -> slot column
+#pragma unroll
+    for (int h = 0; h < 1 + M2; ++h) {
+      if (h >= nhalf) break;
+      const int on = n0h[h] + ni, op = p0h[h] + pi_, oq = q0h[h] + qi;
+      const bool valid = row < tn * tp * tq && on < N && op < P && oq < Q;
+      const int64_t pix = (int64_t(on) * P + op) * Q + oq;
+      drain_rows_direct<T>(lane_addr + uint32_t(h * bn), ncols, pix, on, valid, co_base, cout, e, sv, true,
+                           nullptr, ldw, 16 * (warp >> 2), 16 * int(blockDim.x >> 7));
+    }
+    tc_fence_before();
+    __syncthreads();                                   // map complete; TMEM reads done
+    if (warp == 2) tmem_dealloc(tmem_base, tmem_cols);
+    dw_smem<T>(D, xs, xp, N, P, Q, co_base, min(ncols, cout - co_base), o,
+               reinterpret_cast<const float*>(slots + nslots * slot_bytes), bn, int(threadIdx.x),
+               int(blockDim.x));
     return;
   }
 

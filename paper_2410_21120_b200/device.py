@@ -286,6 +286,55 @@ class MemberPlan:
     arena_bytes: int
     ws_bytes: int
     tilings: dict[int, dict]    # launch index -> gemm tiling
+    skip: frozenset = frozenset()   # launch indices absorbed by a GEMM's depthwise epilogue
+
+
+# GEMM -> depthwise conv in one launch when one CTA holds the whole GEMM output map
+# (batch-1 MBConv expand convs at 14x14 / 7x7; dfx_gemm.cu dw_k > 0).  DFX_GEMM_DW=0: off
+GEMM_DW = os.environ.get("DFX_GEMM_DW", "1") != "0"
+GEMM_DW_BN = int(os.environ.get("DFX_GEMM_DW_BN", "32"))
+GEMM_DW_BN_M2 = int(os.environ.get("DFX_GEMM_DW_BN_M2", "16"))     # two M tiles per CTA
+# "nosplit": only where the GEMM alone would not split K (the fused launch never does);
+# "single": only where one 128-row M tile holds the map (no m2)
+GEMM_DW_MODE = os.environ.get("DFX_GEMM_DW_MODE", "all")
+_DW_ACTS = (None, "relu", "hardswish", "silu")
+
+
+def gemm_dw_pairs(prog: MemberProgram) -> dict[int, int]:
+    """GEMM launch index -> index of the depthwise launch right after it that is
+    the ONLY reader of its output (structure only; the batch decides in plan_member).
+    The depthwise must be a shape dwconv_tile_kernel takes (square 3x3 / 5x5,
+    stride 1 / 2) with BN + one of its templated activations."""
+    readers: dict[str, int] = {}
+    for L in prog.launches:
+        for v in (L.src, L.epi.other):
+            if v is not None:
+                readers[v] = readers.get(v, 0) + 1
+    bufs: dict[int, int] = {}
+    for v in prog.values.values():
+        bufs[v.buf] = bufs.get(v.buf, 0) + 1
+    out = {}
+    ls = prog.launches
+    for i in range(len(ls) - 1):
+        L, D = ls[i], ls[i + 1]
+        if L.kind != GEMM or D.kind != DWCONV or D.src != L.dst or readers.get(L.dst) != 1:
+            continue
+        if L.dst == prog.exit_value or bufs.get(prog.values[L.dst].buf) != 1:
+            continue
+        if L.geom.get("tokens") or L.pre is not None or L.epi.binop or L.epi.act2 is not None:
+            continue
+        g = D.geom
+        if not (g["kh"] == g["kw"] and g["kh"] in (3, 5) and g["sh"] == g["sw"] and g["sh"] in (1, 2)
+                and g["ph"] == g["pw"]):
+            continue
+        if D.epi.binop or D.epi.act2 is not None or D.epi.act1 not in _DW_ACTS:
+            continue
+        vi, vo = prog.values[L.dst], prog.values[D.dst]
+        if L.geom["cout"] % 8 or vi.c != L.geom["cout"] or vo.coff % 8 or \
+                prog.buffers[vo.buf].pitch % 8:
+            continue
+        out[L.index] = D.index
+    return out
 
 
 def plan_member(prog: MemberProgram, n: int, sm_count: int = 148, cluster_ok: bool = False) -> MemberPlan:
@@ -300,6 +349,8 @@ def plan_member(prog: MemberProgram, n: int, sm_count: int = 148, cluster_ok: bo
     arena = max((pl.offset + pl.size for pl in places), default=0)
     ws = 0
     tilings = {}
+    skip: set[int] = set()
+    dw_pairs = gemm_dw_pairs(prog) if GEMM_DW else {}
     for L in prog.launches:
         if L.kind != GEMM:
             continue
@@ -308,10 +359,22 @@ def plan_member(prog: MemberProgram, n: int, sm_count: int = 148, cluster_ok: bo
             t = gemm_tiling(L.geom, 1, 1, n * out.w, sm_count, cluster_ok=cluster_ok and n <= 2)
         else:
             t = gemm_tiling(L.geom, n, out.h, out.w, sm_count, cluster_ok=cluster_ok)
+        if L.index in dw_pairs and n * out.h * out.w <= 256 and \
+                (GEMM_DW_MODE == "all" or t["splits"] == 1):
+            # one CTA (m2: two M tiles) holds the whole output map of its channels
+            mt = t["mt_n"] * t["mt_p"] * t["mt_q"]
+            bn = min(GEMM_DW_BN_M2 if mt == 2 else GEMM_DW_BN, t["bn"])
+            nt = -(-L.geom["cout"] // bn)
+            xs = n * out.h * out.w * (bn + 8) * 2           # the map in smem (dfx_gemm.cu)
+            nsl = gemm_slots(bn, nt, sm_count, int(mt == 2))
+            if mt <= (1 if GEMM_DW_MODE == "single" else 2) and xs <= nsl * (128 * 64 * 2 * (1 + int(mt == 2)) + bn * 128):
+                t = dict(t, bn=bn, nt=nt, splits=1, sps=t["stages"], csplit=0, m2=int(mt == 2),
+                         tiles=nt, dw=dw_pairs[L.index])
+                skip.add(dw_pairs[L.index])
         tilings[L.index] = t
         if t["splits"] > 1 and not t["csplit"]:      # cluster split-K needs no workspace
             ws = max(ws, t["splits"] * n * out.h * out.w * t["nt"] * t["bn"] * 4)
-    return MemberPlan(offsets, _align(arena), _align(ws), tilings)
+    return MemberPlan(offsets, _align(arena), _align(ws), tilings, frozenset(skip))
 
 
 # ------------------------------------------------------------------------------ instances
@@ -407,6 +470,8 @@ class ExecInstance:
             self.nodes.append((rt.OP_IN, pin, dict(member=m, kind="in", flops=0,
                                                    bytes=self.in_sizes[m] * 3 // 2)))
             for L in prog.launches:
+                if L.index in self.plans[m].skip:      # absorbed by the GEMM before it
+                    continue
                 for op, params in self._params(m, prog, L, n, host_descs):
                     last = g.add(op, params, [last])
                     self._node_member.append(m)
@@ -550,6 +615,15 @@ class ExecInstance:
             d.bn, d.cout, d.tile_begin, d.tiles = t["bn"], geo["cout"], 0, t["tiles"]
             d.m2 = t.get("m2", 0)
             d.out = out
+            if t.get("dw") is not None:      # depthwise epilogue: `out` is the dw output
+                D = next(x for x in prog.launches if x.index == t["dw"])
+                dg = D.geom
+                d.out = self._view(m, prog, D.dst, n)
+                d.dw_w = arena.addr(m, D.blobs["weight"])
+                d.dw_alpha = arena.addr(m, D.blobs["alpha"]) if "alpha" in D.blobs else None
+                d.dw_beta = arena.addr(m, D.blobs["beta"]) if "beta" in D.blobs else None
+                d.dw_k, d.dw_s, d.dw_pad = dg["kh"], dg["sh"], dg["ph"]
+                d.dw_act = rt.ACT[D.epi.act1]
             epi = self._epi(m, prog, L, n)
             if geo.get("tokens") and epi.binop:
                 epi.other = _fold_rows(epi.other)

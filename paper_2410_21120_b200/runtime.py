@@ -52,7 +52,9 @@ class GemmDesc(C.Structure):
                 ("bn", i32), ("cout", i32), ("tile_begin", i32), ("tiles", i32), ("m2", i32),
                 ("out", View), ("epi", Epilogue), ("ws", vp), ("counters", vp),
                 ("pre_scale", vp), ("pre_shift", vp), ("pre_mode", i32), ("pre_act", i32),
-                ("pre_cin", i32), ("pre_pitch", i32), ("_pad2", u8 * 48)]
+                ("pre_cin", i32), ("pre_pitch", i32), ("dw_w", vp), ("dw_alpha", vp),
+                ("dw_beta", vp), ("dw_k", i32), ("dw_s", i32), ("dw_pad", i32), ("dw_act", i32),
+                ("_pad2", u8 * 8)]
 
 
 class GemmLaunch(C.Structure):

@@ -122,3 +122,32 @@ def test_gather_staging_matches_single_thread_staging(models, monkeypatch):
             assert np.array_equal(a.values, b.values)
     with pytest.raises(ValueError):
         fuse.load_fused(dag).execute([[x[0][:, :100]]])
+
+
+@pytest.mark.parametrize("name,n", [("efficientnet_v2_l", 1), ("efficientnet_v2_l", 2),
+                                    ("mobilenet_v3_large", 1)])
+def test_gemm_depthwise_epilogue_bit_identical(name, n, monkeypatch):
+    """Expand conv + depthwise conv in ONE GEMM launch (the depthwise runs on the
+    CTA's shared-memory copy of the expanded map, dfx_gemm.cu dw_k > 0) matches the
+    two-launch path and the oracle, and is really taken.  Not bitwise: the fused
+    launch never splits K, the two-launch path does on long-K expand convs, so the
+    fp32 sums round to 16 bit from a different order."""
+    from paper_2410_21120_b200 import device
+    g, w = zoo.build(name)
+    x = np.random.default_rng(9).standard_normal((n, 3, 224, 224)).astype(np.float32)
+    outs, skipped = [], []
+    for on in (False, True):
+        monkeypatch.setattr(device, "GEMM_DW", on)
+        dag = fuse.fuse_models([(g, w)])
+        img = fuse.load_fused(dag)
+        inst = img.acquire((n,))
+        skipped.append(len(inst.plans[0].skip))
+        img.release(inst)
+        outs.append(fuse.execute_fused(dag, {g.model_id: [Tensor(g.input_spec, v) for v in x]})[g.model_id])
+        img.free_instances()
+    assert skipped[0] == 0 and skipped[1] > 0, skipped
+    for a, b in zip(*outs):
+        assert np.abs(a.values - b.values).max() / np.abs(a.values).max() < 5e-3
+    ref = run_fast(g, w, x)
+    got = np.stack([t.values for t in outs[1]])
+    assert (np.abs(got - ref).max(axis=1) / np.abs(ref).max(axis=1)).max() < TOL
