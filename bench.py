@@ -595,7 +595,7 @@ def run_ours(args, world, rank, local_rank):
                     "h2d_frac_of_pinned_peak": (arena.total / (arena.memcpy_ms * 1e-3) / 1e9 / h2d_gbs
                                                 if getattr(arena, "memcpy_ms", None) else None),
                     "nccl_broadcast_ms": bcast_ms,
-                    "note": "median of 3 load cycles (one cudaMalloc + one H2D each)",
+                    "note": "median of 3 load cycles (one allocation from the retained arena pool + one H2D each; first_load_ms maps the pool pages)",
                     "first_load_ms": first_load_ms,
                     "unfused_ms": unfused["swap_in_ms"] if unfused else None,
                     "unfused_malloc_ms": unfused["malloc_ms"] if unfused else None,

@@ -313,6 +313,14 @@ int dfx_mem_info(size_t* free_bytes, size_t* total_bytes);
 int dfx_malloc(void** dptr, size_t bytes);
 int dfx_free(void* dptr);
 int dfx_memset(void* dptr, int value, size_t bytes, void* stream);
+/* Weight arenas: allocation from a per-device stream-ordered pool that keeps
+ * freed pages mapped (unbounded release threshold), so swap-out / swap-in
+ * cycles do not remap physical memory (the cudaMalloc phase of simulate_load,
+ * costmodel.py:297-300).  dfx_pool_trim returns mapped-but-free pages to the
+ * driver down to keep_bytes. */
+int dfx_pool_malloc(void** dptr, size_t bytes, void* stream);
+int dfx_pool_free(void* dptr, void* stream);
+int dfx_pool_trim(size_t keep_bytes);
 int dfx_host_alloc(void** hptr, size_t bytes);          /* pinned */
 int dfx_host_free(void* hptr);
 int dfx_host_register(void* hptr, size_t bytes);

@@ -526,6 +526,56 @@ int dfx_free(void* dptr) {
   CK(cudaFree(dptr));
   return DFX_OK;
 }
+
+// Weight-arena pool: one stream-ordered memory pool per device whose release
+// threshold is unbounded, so a swapped-out arena's pages stay mapped and the next
+// arena (the same DAG again, or another one) is carved from them without a new
+// physical mapping.  A fresh cudaMalloc of a re-freed 587 MB arena measured
+// 0.5-54 ms depending on the box; a pool allocation of mapped memory is a few us.
+static int arena_pool(cudaMemPool_t* out) {
+  static std::mutex mu;
+  static cudaMemPool_t pools[64] = {};
+  int dev = 0;
+  CK(cudaGetDevice(&dev));
+  if (dev < 0 || dev >= 64) return fail(DFX_E_ARG, "device %d", dev);
+  std::lock_guard<std::mutex> g(mu);
+  if (!pools[dev]) {
+    cudaMemPoolProps props = {};
+    props.allocType = cudaMemAllocationTypePinned;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = dev;
+    CK(cudaMemPoolCreate(&pools[dev], &props));
+    uint64_t keep = ~uint64_t(0);
+    CK(cudaMemPoolSetAttribute(pools[dev], cudaMemPoolAttrReleaseThreshold, &keep));
+  }
+  *out = pools[dev];
+  return DFX_OK;
+}
+
+int dfx_pool_malloc(void** dptr, size_t bytes, void* stream) {
+  if (!dptr) return fail(DFX_E_ARG, "null out pointer");
+  cudaMemPool_t pool;
+  int rc = arena_pool(&pool);
+  if (rc) return rc;
+  CK(cudaMallocFromPoolAsync(dptr, bytes, pool, S(stream)));
+  CK(cudaStreamSynchronize(S(stream)));
+  return DFX_OK;
+}
+
+int dfx_pool_free(void* dptr, void* stream) {
+  if (!dptr) return DFX_OK;
+  CK(cudaFreeAsync(dptr, S(stream)));
+  CK(cudaStreamSynchronize(S(stream)));
+  return DFX_OK;
+}
+
+int dfx_pool_trim(size_t keep_bytes) {
+  cudaMemPool_t pool;
+  int rc = arena_pool(&pool);
+  if (rc) return rc;
+  CK(cudaMemPoolTrimTo(pool, keep_bytes));
+  return DFX_OK;
+}
 int dfx_memset(void* dptr, int value, size_t bytes, void* stream) {
   CK(cudaMemsetAsync(dptr, value, bytes, S(stream)));
   return DFX_OK;

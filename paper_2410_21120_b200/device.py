@@ -124,6 +124,31 @@ def fill_arena(buf: np.ndarray, programs: list[MemberProgram], layout) -> None:
             buf[off:off + raw.size] = raw
 
 
+# weight arenas come from a retained stream-ordered pool (dfx_pool_malloc): a
+# swapped-out arena's pages stay mapped for the next swap-in (DFX_ARENA_POOL=0:
+# plain cudaMalloc / cudaFree, A/B)
+ARENA_POOL = os.environ.get("DFX_ARENA_POOL", "1") != "0"
+
+
+_pooled: set[int] = set()             # arena pointers that came from the pool
+
+
+def _arena_malloc(nbytes: int, stream=None) -> int:
+    if not ARENA_POOL:
+        return rt.malloc(nbytes)
+    p = rt.pool_malloc(nbytes, stream)
+    _pooled.add(p)
+    return p
+
+
+def _arena_free(ptr: int) -> None:
+    if ptr in _pooled:
+        _pooled.discard(ptr)
+        rt.pool_free(ptr)
+    else:
+        rt.free(ptr)
+
+
 class WeightArena:
     """Packed weights of all members: host pinned staging + device copy."""
 
@@ -146,7 +171,7 @@ class WeightArena:
         as separate cudaMalloc / cudaMemcpyAsync rows, costmodel.py:297-300):
         ``malloc_ms`` by wall clock, ``memcpy_ms`` by CUDA events."""
         t0 = time.perf_counter()
-        self.dev = rt.malloc(self.total)
+        self.dev = _arena_malloc(self.total, stream)
         self.malloc_ms = (time.perf_counter() - t0) * 1e3
         e0, e1 = rt.Event(), rt.Event()
         e0.record(stream)
@@ -162,13 +187,13 @@ class WeightArena:
         """Free the device copy, keep the pinned host staging (swap-out; the next
         upload() is again one cudaMalloc + one H2D)."""
         if self.dev:
-            rt.free(self.dev)
+            _arena_free(self.dev)
         self.dev = 0
         self.member_base = []
 
     def allocate(self) -> None:
         """Device allocation only (a replica that receives the arena by broadcast)."""
-        self.dev = rt.malloc(self.total)
+        self.dev = _arena_malloc(self.total)
         self.member_base = [self.dev + off for off, _ in self.segments]
 
     def addr(self, member: int, key: str) -> int:
@@ -212,7 +237,7 @@ class WeightArena:
 
     def free(self):
         if self.dev:
-            rt.free(self.dev)
+            _arena_free(self.dev)
         for p in self.extra_allocs:
             rt.free(p)
         if getattr(self, "host_pinned", True):       # pack_io may stage in pageable memory

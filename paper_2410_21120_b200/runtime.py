@@ -138,7 +138,7 @@ OP_PARAMS = {OP_GEMM: GemmLaunch, OP_SPLITK: SplitKParams, OP_DWCONV: DwconvPara
 # every symbol include/dfx.h declares (tests check the .so exports all of them)
 EXPORTS = (
     "dfx_last_error", "dfx_abi_version", "dfx_sizeof", "dfx_init", "dfx_device_info", "dfx_mem_info",
-    "dfx_malloc", "dfx_free", "dfx_memset", "dfx_host_alloc", "dfx_host_free",
+    "dfx_malloc", "dfx_free", "dfx_memset", "dfx_pool_malloc", "dfx_pool_free", "dfx_pool_trim", "dfx_host_alloc", "dfx_host_free",
     "dfx_host_register", "dfx_host_unregister", "dfx_memcpy_h2d", "dfx_memcpy_d2h",
     "dfx_memcpy_d2d", "dfx_arena_upload", "dfx_stream_create", "dfx_stream_destroy",
     "dfx_stream_sync", "dfx_event_create", "dfx_event_destroy", "dfx_event_record",
@@ -206,6 +206,22 @@ def malloc(nbytes: int) -> int:
 def free(ptr: int) -> None:
     if ptr:
         call("dfx_free", vp(ptr))
+
+
+def pool_malloc(nbytes: int, stream=None) -> int:
+    """Weight-arena allocation from the device's retained pool (dfx_pool_malloc)."""
+    p = vp()
+    call("dfx_pool_malloc", C.byref(p), C.c_size_t(nbytes), vp(stream))
+    return p.value
+
+
+def pool_free(ptr: int, stream=None) -> None:
+    if ptr:
+        call("dfx_pool_free", vp(ptr), vp(stream))
+
+
+def pool_trim(keep_bytes: int = 0) -> None:
+    call("dfx_pool_trim", C.c_size_t(keep_bytes))
 
 
 def host_alloc(nbytes: int) -> int:
