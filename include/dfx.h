@@ -145,12 +145,14 @@ typedef struct __attribute__((aligned(64))) dfx_gemm_desc {
   const void* pre_scale;
   const float* pre_shift;
   int32_t pre_mode, pre_act, pre_cin, pre_pitch;
-  /* Depthwise epilogue (dw_k > 0; gemm launch flag 32): the CTA holds the whole
+  /* Depthwise epilogue (dw_k > 0): the CTA holds the whole
    * GEMM output map (n, p, q) for its bn channels, so the consumer depthwise
    * conv (square dw_k x dw_k, stride dw_s, padding dw_pad; fp32 taps
    * [dw_k*dw_k][cout]) runs on it in shared memory: the GEMM output (after
    * `epi`, rounded to 16 bit exactly as when stored) never reaches HBM, and
-   * `out` is the depthwise OUTPUT view, written as act(acc * dw_alpha + dw_beta). */
+   * `out` is the depthwise OUTPUT view, written as act(acc * dw_alpha + dw_beta).
+   * Two M tiles split along p (mt_p == 2, m2 == 0) run as a 2-CTA cluster: each
+   * CTA drains its own rows and reads the peer's rows over DSMEM. */
   const float* dw_w;
   const float* dw_alpha;
   const float* dw_beta;

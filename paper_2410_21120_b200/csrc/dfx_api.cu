@@ -231,10 +231,13 @@ int config_for(int op, const void* params, size_t size, LaunchCfg* c) {
         c->block = dim3((c->smem > size_t(114 * 1024) || p->desc0.pre_mode) ? dfx::kGemmThreads : 128);
         const dfx_gemm_desc& d0 = p->desc0;
         if (d0.dw_k > 0) {              // depthwise epilogue: one CTA holds the whole map
+          const int mtt = d0.mt_n * d0.mt_p * d0.mt_q;
+          const bool pair = !p->m2 && mtt == 2;         // one M tile per CTA of a 2-CTA cluster
           if (p->ndesc != 1 || (p->flags & 8) || d0.splits != 1 || (d0.dw_k != 3 && d0.dw_k != 5) ||
-              (d0.dw_s != 1 && d0.dw_s != 2) || d0.mt_n * d0.mt_p * d0.mt_q > 1 + (p->m2 ? 1 : 0) ||
-              (d0.cout & 7))
-            return fail(DFX_E_ARG, "gemm: depthwise epilogue needs one problem whose M tiles fit one CTA");
+              (d0.dw_s != 1 && d0.dw_s != 2) || mtt > 2 || (pair && d0.mt_p != 2) || (d0.cout & 7))
+            return fail(DFX_E_ARG, "gemm: depthwise epilogue needs one problem whose M tiles fit one CTA "
+                                   "(or a 2-CTA cluster split along p)");
+          if (pair) c->cluster = 2;
           if (size_t(d0.n) * d0.p * d0.q * (p->bn_max + 8) * 2 >
               size_t(p->nslots) * dfx::gemm_slot_bytes(p->bn_max, p->m2 ? 1 : 0))
             return fail(DFX_E_ARG, "gemm: depthwise epilogue map exceeds the %d slots", p->nslots);

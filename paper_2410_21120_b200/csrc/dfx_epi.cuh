@@ -343,17 +343,29 @@ namespace dfx {
 // exchange and no HBM round trip of the expanded map.  Arithmetic order is
 // dwconv_tile_kernel's (taps (ki, kj) ascending, fmaf, then * alpha + beta and
 // the activation), so fused and unfused results are bit-identical.
+// Cluster variant (D.mt_p == 2, one M tile per CTA of a 2-CTA cluster): each CTA
+// drained its own rows; rows p >= D.tp live in rank 1's shared memory and are read
+// over DSMEM, and the output items are split between the two ranks.
 template <typename T, int K, int S, int ACT>
 DFX_DEV void dw_smem_t(const dfx_gemm_desc& D, const T* xs, int xp, int N, int P, int Q, int co_base,
                        int nch, const dfx_view& o, const float* sw, int bn, int tid, int nthr) {
   const int OH = o.h, OW = o.w, cg = nch >> 3, C = D.cout;
-  const int total = N * OH * OW * cg;
+  int total = N * OH * OW * cg;
+  const bool pair = D.mt_p == 2 && D.m2 == 0;         // 2-CTA cluster, split along p
+  const int rank = pair ? int(cluster_ctarank()) : 0;
+  int item0 = 0;
+  if (pair) {
+    const int half = (total + 1) / 2;
+    item0 = rank * half;
+    total = min(total, item0 + half);
+  }
+  const int tp_rows = D.tp;
   // taps [K*K][bn] then alpha[bn], beta[bn] (staged in smem; identity when absent)
   const float* const al = sw + K * K * bn;
   const float* const be = al + bn;
   const bool has_al = D.dw_alpha != nullptr, has_be = D.dw_beta != nullptr;
   (void)C;
-  for (int item = tid; item < total; item += nthr) {
+  for (int item = item0 + tid; item < total; item += nthr) {
     const int cgi = item % cg;
     int t = item / cg;
     const int q = t % OW;
@@ -378,7 +390,12 @@ DFX_DEV void dw_smem_t(const dfx_gemm_desc& D, const T* xs, int xp, int N, int P
         const float4 lo = wt[0], hi = wt[1];
         const float wv[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
         float x[8];
-        unpack8<T>(*reinterpret_cast<const uint4*>(row + w * xp), x);
+        if (pair) {
+          const float4 r4 = dsmem_ld4(row + w * xp, uint32_t(h >= tp_rows));
+          unpack8<T>(*reinterpret_cast<const uint4*>(&r4), x);
+        } else {
+          unpack8<T>(*reinterpret_cast<const uint4*>(row + w * xp), x);
+        }
 #pragma unroll
         for (int i = 0; i < 8; ++i) acc[i] = fmaf(wv[i], x[i], acc[i]);
       }

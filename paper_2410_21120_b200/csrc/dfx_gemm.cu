@@ -477,11 +477,14 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                            nullptr, ldw, 16 * (warp >> 2), 16 * int(blockDim.x >> 7));
     }
     tc_fence_before();
-    __syncthreads();                                   // map complete; TMEM reads done
+    const bool pair = !M2 && mt_total == 2;            // 2-CTA cluster: the peer holds the other rows
+    if (pair) cluster_sync_all();
+    else __syncthreads();                              // map complete; TMEM reads done
     if (warp == 2) tmem_dealloc(tmem_base, tmem_cols);
     dw_smem<T>(D, xs, xp, N, P, Q, co_base, min(ncols, cout - co_base), o,
                reinterpret_cast<const float*>(slots + nslots * slot_bytes), bn, int(threadIdx.x),
                int(blockDim.x));
+    if (pair) cluster_sync_all();                      // the peer finished reading this map
     return;
   }
 

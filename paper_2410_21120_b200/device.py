@@ -319,6 +319,10 @@ class MemberPlan:
 GEMM_DW = os.environ.get("DFX_GEMM_DW", "1") != "0"
 GEMM_DW_BN = int(os.environ.get("DFX_GEMM_DW_BN", "32"))
 GEMM_DW_BN_M2 = int(os.environ.get("DFX_GEMM_DW_BN_M2", "16"))     # two M tiles per CTA
+# two M tiles (14x14 maps): a 2-CTA cluster, one tile each, halo rows over DSMEM
+# ("cluster"), or both tiles in one m2 CTA ("m2")
+GEMM_DW_PAIR = os.environ.get("DFX_GEMM_DW_PAIR", "cluster")
+GEMM_DW_BN_PAIR = int(os.environ.get("DFX_GEMM_DW_BN_PAIR", "32"))
 # "nosplit": only where the GEMM alone would not split K (the fused launch never does);
 # "single": only where one 128-row M tile holds the map (no m2)
 GEMM_DW_MODE = os.environ.get("DFX_GEMM_DW_MODE", "all")
@@ -388,13 +392,15 @@ def plan_member(prog: MemberProgram, n: int, sm_count: int = 148, cluster_ok: bo
                 (GEMM_DW_MODE == "all" or t["splits"] == 1):
             # one CTA (m2: two M tiles) holds the whole output map of its channels
             mt = t["mt_n"] * t["mt_p"] * t["mt_q"]
-            bn = min(GEMM_DW_BN_M2 if mt == 2 else GEMM_DW_BN, t["bn"])
+            pair = mt == 2 and GEMM_DW_PAIR == "cluster" and t["mt_p"] == 2
+            m2 = int(mt == 2 and not pair)
+            bn = min(GEMM_DW_BN_M2 if m2 else GEMM_DW_BN_PAIR if pair else GEMM_DW_BN, t["bn"])
             nt = -(-L.geom["cout"] // bn)
             xs = n * out.h * out.w * (bn + 8) * 2           # the map in smem (dfx_gemm.cu)
-            nsl = gemm_slots(bn, nt, sm_count, int(mt == 2))
-            if mt <= (1 if GEMM_DW_MODE == "single" else 2) and xs <= nsl * (128 * 64 * 2 * (1 + int(mt == 2)) + bn * 128):
-                t = dict(t, bn=bn, nt=nt, splits=1, sps=t["stages"], csplit=0, m2=int(mt == 2),
-                         tiles=nt, dw=dw_pairs[L.index])
+            nsl = gemm_slots(bn, nt * (2 if pair else 1), sm_count, m2)
+            if mt <= (1 if GEMM_DW_MODE == "single" else 2) and xs <= nsl * (128 * 64 * 2 * (1 + m2) + bn * 128):
+                t = dict(t, bn=bn, nt=nt, splits=1, sps=t["stages"], csplit=0, m2=m2,
+                         tiles=nt * (2 if pair else 1), dw=dw_pairs[L.index])
                 skip.add(dw_pairs[L.index])
         tilings[L.index] = t
         if t["splits"] > 1 and not t["csplit"]:      # cluster split-K needs no workspace
