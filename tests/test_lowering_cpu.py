@@ -98,3 +98,29 @@ def test_vit_launch_structure():
     assert "ew" not in kinds and kinds.count("tokens") == 1
     last_ln = [L for L in prog.launches if L.kind == "ln"][-1]
     assert last_ln.dst == "cls" and prog.values["cls"].w == 1
+
+
+def test_gemm_depthwise_epilogue_plan():
+    """Host side of the depthwise epilogue (device.gemm_dw_pairs / plan_member):
+    every EfficientNetV2-L MBConv expand conv pairs with its depthwise conv; at
+    batch 1 the 14x14 / 7x7 ones (not the 28x28 one) absorb it, 14x14 as 2-CTA
+    clusters (one M tile per CTA, no m2), never with split-K; at batch 8 none do."""
+    from paper_2410_21120_b200 import device, zoo
+    g, w = zoo.build("efficientnet_v2_l")
+    prog = lower_member(g, w)
+    pairs = device.gemm_dw_pairs(prog)
+    assert len(pairs) == 61
+    by_index = {L.index: L for L in prog.launches}
+    for gi, di in pairs.items():
+        assert by_index[gi].kind == "gemm" and by_index[di].kind == "dwconv"
+        assert by_index[di].src == by_index[gi].dst
+    p1 = device.plan_member(prog, 1, 148, True)
+    assert len(p1.skip) == 60 and p1.skip <= set(pairs.values())
+    fused = [t for t in p1.tilings.values() if t.get("dw") is not None]
+    assert len(fused) == 60
+    for t in fused:
+        assert t["splits"] == 1 and not t["csplit"] and t["m2"] == 0
+        mt = t["mt_n"] * t["mt_p"] * t["mt_q"]
+        assert mt in (1, 2) and t["tiles"] == t["nt"] * mt
+    assert {t["mt_p"] for t in fused} == {1, 2}
+    assert not device.plan_member(prog, 8, 148, True).skip
