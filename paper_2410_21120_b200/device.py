@@ -80,6 +80,7 @@ SE_UNSTAGED_BATCH = int(os.environ.get("DFX_SE_UNSTAGED_BATCH", "8"))
 # (4-model batch 32 12.3 -> 13.3 ms, 8-model batches 1..8 6.6 -> 7.3 ms), so off
 NODE_PRIORITY = os.environ.get("DFX_PRIORITY", "1") != "0"
 PRIORITY_MAX_BATCH = 2
+SLACK_SPLIT_MAX = int(os.environ.get("DFX_SLACK_SPLIT_MAX", "0"))
 # persistent GEMM for grids above this many waves (A/B knob)
 PERSIST_MIN_WAVES = float(os.environ.get("DFX_PERSIST_MIN_WAVES", "2"))
 GEMM_EARLY_PDL = os.environ.get("DFX_GEMM_EARLY_PDL", "0") == "1"            # A/B switch
@@ -366,7 +367,8 @@ def gemm_dw_pairs(prog: MemberProgram) -> dict[int, int]:
     return out
 
 
-def plan_member(prog: MemberProgram, n: int, sm_count: int = 148, cluster_ok: bool = False) -> MemberPlan:
+def plan_member(prog: MemberProgram, n: int, sm_count: int = 148, cluster_ok: bool = False,
+                max_splits: int = 0) -> MemberPlan:
     """Activation plan + GEMM tilings of one member at batch n.  ``cluster_ok``: the
     DAG is small enough for cluster split-K (lower.SPLITK_MODE "auto")."""
     ivs = [LiveInterval(str(b.bid).zfill(6), b.bytes_for(n), b.first, b.last)
@@ -385,9 +387,10 @@ def plan_member(prog: MemberProgram, n: int, sm_count: int = 148, cluster_ok: bo
             continue
         out = prog.values[L.dst]
         if L.geom.get("tokens"):        # token rows of all images are one contiguous M
-            t = gemm_tiling(L.geom, 1, 1, n * out.w, sm_count, cluster_ok=cluster_ok and n <= 2)
+            t = gemm_tiling(L.geom, 1, 1, n * out.w, sm_count, cluster_ok=cluster_ok and n <= 2,
+                            max_splits=max_splits)
         else:
-            t = gemm_tiling(L.geom, n, out.h, out.w, sm_count, cluster_ok=cluster_ok)
+            t = gemm_tiling(L.geom, n, out.h, out.w, sm_count, cluster_ok=cluster_ok, max_splits=max_splits)
         if L.index in dw_pairs and n * out.h * out.w <= 256 and \
                 (GEMM_DW_MODE == "all" or t["splits"] == 1):
             # one CTA (m2: two M tiles) holds the whole output map of its channels
@@ -422,8 +425,16 @@ class ExecInstance:
         # cluster split-K only in small concurrent DAGs: its clusters need free GPC
         # slices, which many concurrent branches rarely leave
         cluster_ok = sum(1 for n in batch if n > 0) <= 4
-        self.plans = [plan_member(p, n, dag.sm_count, cluster_ok) if n > 0 else MemberPlan([], 0, 0, {})
-                      for p, n in zip(progs, batch)]
+        # A/B (DFX_SLACK_SPLIT_MAX=k): at small batch, members off the critical chain
+        # split K at most k ways, leaving SMs to the longest chain
+        caps = [0] * len(progs)
+        if SLACK_SPLIT_MAX and dag.mode == "concurrent" and max(batch) <= PRIORITY_MAX_BATCH:
+            est = [sum(_NODE_BASE_US.get(L.kind, 2.5) for L in p.launches) if n > 0 else 0
+                   for p, n in zip(progs, batch)]
+            crit = est.index(max(est))
+            caps = [0 if i == crit else SLACK_SPLIT_MAX for i in range(len(progs))]
+        self.plans = [plan_member(p, n, dag.sm_count, cluster_ok, caps[i]) if n > 0 else MemberPlan([], 0, 0, {})
+                      for i, (p, n) in enumerate(zip(progs, batch))]
         seq = dag.mode == "sequential"
         # activation arena: disjoint member segments (concurrent) or overlaid (sequential)
         self.seg_off, at = [], 0

@@ -861,7 +861,8 @@ FOLD_PRE = os.environ.get("DFX_FOLD_PRE", "0") == "1"
 SPLITK_CLUSTER_MAX = 8
 
 
-def gemm_tiling(geom: dict, n: int, p: int, q: int, sm_count: int = 148, cluster_ok: bool = False) -> dict:
+def gemm_tiling(geom: dict, n: int, p: int, q: int, sm_count: int = 148, cluster_ok: bool = False,
+                max_splits: int = 0) -> dict:
     tn, tp, tq = choose_m_tile(n, p, q, geom["sh"], geom["sw"])
     mt = (math.ceil(n / tn), math.ceil(p / tp), math.ceil(q / tq))
     bn, nt = choose_bn(geom["cout"])
@@ -879,6 +880,8 @@ def gemm_tiling(geom: dict, n: int, p: int, q: int, sm_count: int = 148, cluster
     splits = 1
     if base < sm_count and stages >= 2 * SPLIT_MIN_STAGES:
         splits = min(math.ceil(sm_count / base), stages // SPLIT_MIN_STAGES)
+    if max_splits:
+        splits = min(splits, max_splits)
     sps = math.ceil(stages / max(splits, 1))
     splits = math.ceil(stages / sps)
     # m2: 256-row CTAs (two M tiles sharing each weight stage) once the grid still
