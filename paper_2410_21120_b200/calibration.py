@@ -221,7 +221,20 @@ def _has(lib: str) -> bool:
 
 def measure(models, workdir, precision: str = "fp16", device: int = 0) -> tuple[CostTable, dict]:
     """Run the calibration episode for ``models`` [(graph, weights)] on the GPU and
-    return (CostTable, report).  ``workdir`` receives the graph / packed files."""
+    return (CostTable, report).  ``workdir`` receives the graph / packed files.
+    The episode books cudaMalloc explicitly and reads per-model overheads from
+    cudaMemGetInfo deltas, so arenas use plain cudaMalloc here (the retained
+    arena pool would hide both)."""
+    from . import device as _dev
+    saved = _dev.ARENA_POOL
+    _dev.ARENA_POOL = False
+    try:
+        return _measure(models, workdir, precision, device)
+    finally:
+        _dev.ARENA_POOL = saved
+
+
+def _measure(models, workdir, precision: str = "fp16", device: int = 0) -> tuple[CostTable, dict]:
     from . import fuse, model_io, pack_io, runtime as rt
     from .device import DeviceDag, PerTensorArena, WeightArena, program_for
     from .lower import lower_member
