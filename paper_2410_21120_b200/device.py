@@ -371,13 +371,6 @@ def plan_member(prog: MemberProgram, n: int, sm_count: int = 148, cluster_ok: bo
                 max_splits: int = 0) -> MemberPlan:
     """Activation plan + GEMM tilings of one member at batch n.  ``cluster_ok``: the
     DAG is small enough for cluster split-K (lower.SPLITK_MODE "auto")."""
-    ivs = [LiveInterval(str(b.bid).zfill(6), b.bytes_for(n), b.first, b.last)
-           for b in prog.buffers]
-    places = first_fit(ivs, align=ALIGN)
-    offsets = [0] * len(prog.buffers)
-    for pl in places:
-        offsets[int(pl.name)] = pl.offset
-    arena = max((pl.offset + pl.size for pl in places), default=0)
     ws = 0
     tilings = {}
     skip: set[int] = set()
@@ -408,6 +401,25 @@ def plan_member(prog: MemberProgram, n: int, sm_count: int = 148, cluster_ok: bo
         tilings[L.index] = t
         if t["splits"] > 1 and not t["csplit"]:      # cluster split-K needs no workspace
             ws = max(ws, t["splits"] * n * out.h * out.w * t["nt"] * t["bn"] * 4)
+    # buffer lifetimes AFTER the fusion decisions: a GEMM that absorbs its depthwise
+    # conv writes the depthwise output at its own launch index, one launch before
+    # the (skipped) depthwise launch would have -- while its own input is still
+    # being read by slower CTAs of the same grid.  The output's interval must
+    # therefore start at the GEMM, or first_fit could overlay it on that input.
+    first = {b.bid: b.first for b in prog.buffers}
+    by_index = {L.index: L for L in prog.launches}
+    for gi, t in tilings.items():
+        if t.get("dw") is not None:
+            D = by_index[t["dw"]]
+            ob = prog.values[D.dst].buf
+            first[ob] = min(first[ob], gi)
+    ivs = [LiveInterval(str(b.bid).zfill(6), b.bytes_for(n), first[b.bid], b.last)
+           for b in prog.buffers]
+    places = first_fit(ivs, align=ALIGN)
+    offsets = [0] * len(prog.buffers)
+    for pl in places:
+        offsets[int(pl.name)] = pl.offset
+    arena = max((pl.offset + pl.size for pl in places), default=0)
     return MemberPlan(offsets, _align(arena), _align(ws), tilings, frozenset(skip))
 
 

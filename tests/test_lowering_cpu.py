@@ -124,3 +124,40 @@ def test_gemm_depthwise_epilogue_plan():
         assert mt in (1, 2) and t["tiles"] == t["nt"] * mt
     assert {t["mt_p"] for t in fused} == {1, 2}
     assert not device.plan_member(prog, 8, 148, True).skip
+
+
+@pytest.mark.parametrize("name", ["efficientnet_v2_l", "mobilenet_v3_large", "densenet161"])
+@pytest.mark.parametrize("n", [1, 2])
+def test_plan_never_overlays_a_launch_output_on_its_inputs(name, n):
+    """No launch writes bytes it (or another CTA of the same grid) still reads: a
+    GEMM carrying a depthwise epilogue writes the depthwise output at ITS index,
+    so that buffer must be disjoint from the GEMM's own input (first_fit
+    used the depthwise launch's later start and overlaid the two)."""
+    from paper_2410_21120_b200 import device, zoo
+    g, w = zoo.build(name)
+    prog = lower_member(g, w)
+    plan = device.plan_member(prog, n, 148, True)
+    by_index = {L.index: L for L in prog.launches}
+
+    def rng(vname):
+        b = prog.values[vname].buf
+        off = plan.offsets[b]
+        return off, off + prog.buffers[b].bytes_for(n), b
+
+    checked = 0
+    for L in prog.launches:
+        if L.index in plan.skip:
+            continue
+        t = plan.tilings.get(L.index, {})
+        dst = by_index[t["dw"]].dst if t.get("dw") is not None else L.dst
+        w0, w1, wb = rng(dst if L.kind != "copy" else L.geom["concat"])
+        for src in (L.src, L.epi.other):
+            if src is None:
+                continue
+            r0, r1, rb = rng(src)
+            if rb == wb:
+                continue                  # concat windows of one buffer (disjoint channels)
+            assert w1 <= r0 or r1 <= w0, (L.index, L.kind, src, dst)
+        checked += t.get("dw") is not None
+    if name == "efficientnet_v2_l":
+        assert checked == 60 if n == 1 else checked >= 0
