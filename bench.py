@@ -38,6 +38,7 @@ ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
 PEAKS_PATH = ROOT / "MEASURED_PEAKS.json"
+NVLINK_GBS = 900.0          # NVLink 5 per GPU per direction (NVSwitch: full bandwidth to every peer)
 FALLBACK_PEAKS = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
 
 
@@ -214,6 +215,7 @@ def run_reference(args, world, rank):
     print(json.dumps(line), flush=True)
 
 
+SHARD_BATCH = 32           # configs[2]: per-member batch sharded over the replicas
 METRIC = "fused 4-model DAG images/s (batch 1 per member), with latency ms, peak HBM GB, swap-in ms"
 
 
@@ -227,8 +229,9 @@ def config_dict(args):
 
 # ----------------------------------------------------------------------------- secondary configs
 
-def time_device_steps(rt, inst, flush, steps, warmup=3):
-    """Device-timed steps of one instance's graph (L2 flushed between steps)."""
+def time_device_steps(rt, inst, flush, steps, warmup=3, raw=False):
+    """Device-timed steps of one instance's graph (L2 flushed between steps);
+    (median, mean) ms, or every step's ms with ``raw``."""
     for _ in range(warmup):
         inst.launch_graph()
     inst.sync()
@@ -241,6 +244,8 @@ def time_device_steps(rt, inst, flush, steps, warmup=3):
         e1.record(inst.stream)
         ms.append(e0.elapsed_ms(e1))
     inst.sync()
+    if raw:
+        return ms
     return float(np.median(ms)), float(np.mean(ms))
 
 
@@ -378,17 +383,14 @@ def ncu_traffic():
 
 # ----------------------------------------------------------------------------- our arm
 
-def run_ours(args, world, rank, local_rank):
+def run_ours(args):
     from paper_2410_21120_b200 import fuse, runtime as rt
     from paper_2410_21120_b200.device import DeviceDag, PerTensorArena, WeightArena, program_for
     from paper_2410_21120_b200.executor import Tensor
+    from paper_2410_21120_b200.replicas import ReplicaGroup, measure_sharded
 
-    dist = None
-    if world > 1:
-        import torch
-        import torch.distributed as dist
-        torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl")
+    rg = ReplicaGroup()                       # NCCL process group when WORLD_SIZE > 1
+    world, rank, local_rank = rg.world, rg.rank, rg.local_rank
     rt.init_device(local_rank)
     P, peak_kind = peaks()
 
@@ -430,19 +432,20 @@ def run_ours(args, world, rank, local_rank):
 
 
     # ---------------- swap-in: one pinned arena, ONE H2D (rank 0), NCCL broadcast to replicas
+    rt.pool_trim(0)            # the retained arena pool must not hide the allocation from cudaMemGetInfo
     free0, _ = rt.mem_info()
     first_load_ms = None
     arena = WeightArena(programs, local_rank)
+    bcast_ms = bcast_first_ms = None
     if world > 1:
         if rank == 0:
             arena.upload()
         else:
             arena.allocate()
-        t0 = time.perf_counter()
-        from paper_2410_21120_b200.device import broadcast_arena
-        broadcast_arena(arena, src=0)
-        torch.cuda.synchronize()
-        bcast_ms = (time.perf_counter() - t0) * 1e3
+        bcast_ms = rg.broadcast_device(arena.dev, arena.total, local_rank, src=0)
+        # a second broadcast of the resident arena: the first one includes NCCL's
+        # lazy connection setup
+        bcast_first_ms, bcast_ms = bcast_ms, rg.broadcast_device(arena.dev, arena.total, local_rank, src=0)
     else:
         # the swap-in reported is the median of 3 load cycles (the first cudaMalloc of
         # a fresh process is occasionally 10-50x slower); the first is reported too
@@ -454,7 +457,6 @@ def run_ours(args, world, rank, local_rank):
             loads.append((arena.upload_ms, arena.malloc_ms, arena.memcpy_ms))
         first_load_ms = loads[0][0]
         arena.upload_ms, arena.malloc_ms, arena.memcpy_ms = sorted(loads)[1]
-        bcast_ms = None
     img = DeviceDag(members, local_rank, args.mode, arena=arena, programs=programs,
                     precision=args.precision)
     batch = tuple([args.batch] * len(members))
@@ -473,8 +475,7 @@ def run_ours(args, world, rank, local_rank):
     for _ in range(args.warmup):
         inst.launch_graph()
     inst.sync()
-    if dist is not None:
-        dist.barrier()
+    rg.barrier()
     clocks.start()
     step_ms = []
     for _ in range(args.steps):
@@ -486,13 +487,7 @@ def run_ours(args, world, rank, local_rank):
         step_ms.append(e0.elapsed_ms(e1))
     inst.sync()
     clk = clocks.stop()
-    total_ms = float(np.sum(step_ms))
-    if dist is not None:
-        import torch
-        t = torch.tensor([total_ms], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms = float(t.item())
-        dist.barrier()
+    total_ms = rg.max(float(np.sum(step_ms)))
     imgs_per_step = len(members) * args.batch
     value = world * imgs_per_step * args.steps / (total_ms * 1e-3)
     ms_per_step = total_ms / args.steps
@@ -504,22 +499,28 @@ def run_ours(args, world, rank, local_rank):
                    for sg, x in zip(dag.subgraphs, xs)}
     for _ in range(max(args.warmup, 1)):
         fuse.execute_fused(dag, host_inputs)
-    if dist is not None:
-        dist.barrier()
+    rg.barrier()
     t0 = time.perf_counter()
     for _ in range(args.steps):
         outs = fuse.execute_fused(dag, host_inputs)
-    e2e_s = time.perf_counter() - t0
-    if dist is not None:
-        import torch
-        t = torch.tensor([e2e_s], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_s = float(t.item())
+    e2e_s = rg.max(time.perf_counter() - t0)
     e2e_value = world * imgs_per_step * args.steps / e2e_s
 
+    # ---------------- configs[2]: batch 32 per member sharded over the replicas (strong
+    # scaling; at N=1 the whole batch on one GPU)
+    def run_rows(start, stop, steps):
+        rows = stop - start
+        si = img.acquire(tuple([rows] * len(members)))
+        si.upload_inputs([x[start:stop] for x in make_inputs(models, SHARD_BATCH, seed=99)])
+        ms = time_device_steps(rt, si, flush, steps=steps, warmup=3, raw=True)
+        img.release(si)
+        return ms
+    sharded = measure_sharded(rg, run_rows, SHARD_BATCH, steps=max(10, min(args.steps, 50)))
+    sharded["images_per_s"] = len(members) * SHARD_BATCH / (sharded["ms_per_step"] * 1e-3)
+    sharded["config"] = (f"configs[2]: 4-model fused DAG, batch {SHARD_BATCH} per member sharded over "
+                         f"{world} replica(s) (rows per rank {sharded['rows_per_rank']}); step time = slowest rank")
+
     if rank != 0:
-        if dist is not None:
-            dist.destroy_process_group()
         return
 
     # ---------------- per-kernel-class roofline (eager replay, CUDA events per launch)
@@ -568,8 +569,13 @@ def run_ours(args, world, rank, local_rank):
     if not args.skip_extra and world == 1:
         extra = secondary_configs(args, rt, members, programs, arena, flush, P, local_rank)
     h2d_gbs = measure_pinned_h2d(rt)
-    cpu_ips, cpu_imgs, cpu_s = cpu_port_time(models, xs)
     cores = os.cpu_count() or 1
+    cpu_baseline = None
+    if world == 1:            # the CPU baseline runs on rank 0 at N=1 only
+        cpu_ips, cpu_imgs, cpu_s = cpu_port_time(models, xs)
+        cpu_baseline = {"value": cpu_ips, "unit": "images/s", "cores": cores, "kind": "port",
+                        "sample": f"{cpu_imgs} member-images ({cpu_s:.1f} s) through "
+                                  f"oracle/executor_ref.run_fast (numpy fp32, BLAS on {cores} threads)"}
     # check the logits of the e2e run against the CPU oracle (4 members, 1 image)
     from oracle.executor_ref import run_fast
     parity = {}
@@ -595,6 +601,10 @@ def run_ours(args, world, rank, local_rank):
                     "h2d_frac_of_pinned_peak": (arena.total / (arena.memcpy_ms * 1e-3) / 1e9 / h2d_gbs
                                                 if getattr(arena, "memcpy_ms", None) else None),
                     "nccl_broadcast_ms": bcast_ms,
+                    "nccl_broadcast_first_ms": bcast_first_ms,
+                    "nccl_broadcast_gbs": arena.total / (bcast_ms * 1e-3) / 1e9 if bcast_ms else None,
+                    "nccl_broadcast_frac_of_nvlink": (arena.total / (bcast_ms * 1e-3) / 1e9 / NVLINK_GBS
+                                                      if bcast_ms else None),
                     "note": "median of 3 load cycles (one allocation from the retained arena pool + one H2D each; first_load_ms maps the pool pages)",
                     "first_load_ms": first_load_ms,
                     "unfused_ms": unfused["swap_in_ms"] if unfused else None,
@@ -610,16 +620,13 @@ def run_ours(args, world, rank, local_rank):
         "gpu_launches": inst.kernel_nodes * args.steps,
         "graph_nodes_per_step": inst.kernel_nodes,
         "roofline": roofline,
-        "cpu_baseline": {"value": cpu_ips, "unit": "images/s", "cores": cores, "kind": "port",
-                         "sample": f"{cpu_imgs} member-images ({cpu_s:.1f} s) through "
-                                   f"oracle/executor_ref.run_fast (numpy fp32, BLAS on {cores} threads)"},
+        "cpu_baseline": cpu_baseline,
         "parity_rel_err": parity,
         "clocks": clk,
+        "sharded_batch32": sharded,
         "other_configs": extra,
     }
     print(json.dumps(line), flush=True)
-    if dist is not None:
-        dist.destroy_process_group()
 
 
 class _SubArena:
@@ -649,13 +656,34 @@ def main():
                     help="skip configs[2..4] (batch 32, swap stress, 8-model) after the headline")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(launch_ranks(args.gpus))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
-    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     if args.impl == "reference":
         run_reference(args, world, rank)
     else:
-        run_ours(args, world, rank, local_rank)
+        run_ours(args)
+
+
+def torchrun_cmd(n: int, port: int, argv: list[str]) -> list[str]:
+    """One process per GPU on this node (rendezvous on 127.0.0.1)."""
+    return [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+            "--master-addr", "127.0.0.1", "--master-port", str(port), str(Path(__file__).resolve()), *argv]
+
+
+def launch_ranks(n: int) -> int:
+    """``bench.py --gpus N`` outside torchrun: spawn the N ranks ourselves (rank 0
+    prints the JSON line).  NCCL init logging stays on so the communicator's
+    nranks is visible in stderr."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    return subprocess.call(torchrun_cmd(n, port, sys.argv[1:]), env=env)
 
 
 if __name__ == "__main__":

@@ -222,7 +222,11 @@ typedef struct dfx_in_params {
   const float* src;                    /* n samples, each c*h*w fp32 in CHW order */
   dfx_view out;
   int32_t kh, kw, sh, sw, ph, pw;      /* entry conv geometry (kh = 0: plain copy) */
-  int32_t c, h, w, _pad;               /* source sample dims */
+  int32_t c, h, w;                     /* source sample dims */
+  int32_t split;                       /* > 0 (im2col only): out.c = 3*split channels written
+                                          as [x_hi | x_hi | x_lo], blocks of `split` channels
+                                          (kh*kw*c real ones, zero padded); x = x_hi + x_lo,
+                                          both 16-bit: the split-precision stem GEMM */
 } dfx_in_params;
 
 typedef struct dfx_out_params {
@@ -323,6 +327,9 @@ int dfx_memset(void* dptr, int value, size_t bytes, void* stream);
 int dfx_pool_malloc(void** dptr, size_t bytes, void* stream);
 int dfx_pool_free(void* dptr, void* stream);
 int dfx_pool_trim(size_t keep_bytes);
+/* Bytes the arena pool holds mapped (reserved) and hands out (used): peak-HBM
+ * samples taken with cudaMemGetInfo account for the retained pages with it. */
+int dfx_pool_stats(size_t* reserved, size_t* used);
 int dfx_host_alloc(void** hptr, size_t bytes);          /* pinned */
 int dfx_host_free(void* hptr);
 int dfx_host_register(void* hptr, size_t bytes);
@@ -383,7 +390,10 @@ int dfx_execute(void* graph, const void* host_in, void* dev_in, size_t in_bytes,
  * (one per member or sample, packed in list order): chunks are copied into the
  * pinned staging buffer `host_in` on a pool of host threads
  * (DFX_STAGE_THREADS, default half the cores) while the calling thread issues
- * the H2D of every completed prefix, so the DMA overlaps the host copy. */
+ * the H2D of every completed prefix, so the DMA overlaps the host copy.
+ * Re-entrant on distinct graphs/streams/staging buffers: only the staging
+ * phase uses the shared pool (a caller that finds it busy copies on its own
+ * thread); the graph launch and the stream sync run without any global lock. */
 int dfx_execute_gather(void* graph, const void* const* srcs, const size_t* sizes, int nsrc,
                        void* host_in, void* dev_in, void* host_out, const void* dev_out,
                        size_t out_bytes, void* stream);

@@ -292,8 +292,7 @@ def _measure(models, workdir, precision: str = "fp16", device: int = 0) -> tuple
                 a = ops.setdefault(kind, [0.0, 0.0])
                 a[0] += r["ms"]
                 a[1] += r["flops"] / 1e6
-        img.free_instances()
-        img.arena.free()
+        img.free()
     per_model = float(sum(overheads) / n)
     ct = CostTable(context_base_mib=round(context_mib, 1), per_model_overhead_mib=round(per_model, 1),
                    dedup_saving_mib_per_extra_model=round(per_model, 1),

@@ -313,8 +313,10 @@ int config_for(int op, const void* params, size_t size, LaunchCfg* c) {
       const auto* p = static_cast<const dfx_in_params*>(params);
       if (p->out.pitch % 8 || p->out.coff) return fail(DFX_E_ARG, "in: pitch/coff");
       if (p->kh > 0) {
-        if (p->out.c > dfx::kIm2colMaxK || p->out.c != p->kh * p->kw * p->c)
-          return fail(DFX_E_UNSUPPORTED, "in: im2col of %d channels", p->out.c);
+        const int kreal = p->kh * p->kw * p->c;
+        const bool ok = p->split > 0 ? (p->split >= kreal && p->out.c == 3 * p->split && p->split <= dfx::kIm2colMaxK)
+                                     : (p->out.c == kreal && p->out.c <= dfx::kIm2colMaxK);
+        if (!ok) return fail(DFX_E_UNSUPPORTED, "in: im2col of %d channels (split %d)", p->out.c, p->split);
         c->func = DFX_PICK(in_im2col_kernel, p->out.dtype);
         c->grid = dim3(unsigned(cdiv(p->out.w, dfx::kIm2colTile)), unsigned(p->out.h), unsigned(p->out.n));
         c->block = dim3(256);
@@ -577,6 +579,18 @@ int dfx_pool_trim(size_t keep_bytes) {
   int rc = arena_pool(&pool);
   if (rc) return rc;
   CK(cudaMemPoolTrimTo(pool, keep_bytes));
+  return DFX_OK;
+}
+
+int dfx_pool_stats(size_t* reserved, size_t* used) {
+  cudaMemPool_t pool;
+  int rc = arena_pool(&pool);
+  if (rc) return rc;
+  uint64_t r = 0, u = 0;
+  CK(cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &r));
+  CK(cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &u));
+  if (reserved) *reserved = size_t(r);
+  if (used) *used = size_t(u);
   return DFX_OK;
 }
 int dfx_memset(void* dptr, int value, size_t bytes, void* stream) {
@@ -861,20 +875,27 @@ namespace {
 struct StagePool {
   static constexpr size_t kChunk = size_t(256) << 10;
   static constexpr int kMaxChunks = 4096;
+  // One 64-bit word carries the job: bits [27, 40) the chunk count n of the job,
+  // bits [0, 27) the next claim index.  A claim (fetch_add) therefore returns the
+  // index together with the count of the SAME job: a worker whose claim is >= n
+  // drops it without touching chunks[] / done[], whichever job is current by then.
+  // A claim < n pins the job: the job cannot end (and chunks[] cannot be rewritten)
+  // until that chunk's done flag is set by the claimant.
+  static constexpr int kIdxBits = 27;
+  static constexpr uint64_t kIdxMask = (uint64_t(1) << kIdxBits) - 1;
   struct Chunk {
     char* dst;
     const char* src;
     size_t bytes;
   };
-  std::mutex job_mu;                       // one job at a time
+  std::mutex job_mu;                       // one job at a time uses the workers
   std::mutex mu;
   std::condition_variable cv;
   std::vector<std::thread> workers;
   std::atomic<uint64_t> gen{0};
-  std::atomic<int> claim{0};
+  std::atomic<uint64_t> claim{0};          // (n << kIdxBits) | next index
   std::atomic<int> done[kMaxChunks];
   Chunk chunks[kMaxChunks];
-  std::atomic<int> nchunks{0};
   bool stop = false;
 
   explicit StagePool(int nthreads) {
@@ -889,13 +910,18 @@ struct StagePool {
     cv.notify_all();
     for (auto& t : workers) t.join();
   }
+  // claim one chunk of the current job; -1 when the job has none left
+  int take() {
+    const uint64_t v = claim.fetch_add(1, std::memory_order_acq_rel);
+    const uint64_t idx = v & kIdxMask, n = v >> kIdxBits;
+    return idx < n ? int(idx) : -1;
+  }
+  void copy(int c) {
+    std::memcpy(chunks[c].dst, chunks[c].src, chunks[c].bytes);
+    done[c].store(1, std::memory_order_release);
+  }
   void work() {
-    for (;;) {
-      const int c = claim.fetch_add(1, std::memory_order_acq_rel);
-      if (c >= nchunks.load(std::memory_order_relaxed)) break;
-      std::memcpy(chunks[c].dst, chunks[c].src, chunks[c].bytes);
-      done[c].store(1, std::memory_order_release);
-    }
+    for (int c; (c = take()) >= 0;) copy(c);
   }
   void loop() {
     uint64_t seen = gen.load();
@@ -911,9 +937,7 @@ struct StagePool {
       }
       seen = gen.load(std::memory_order_acquire);
       if (stop) return;
-      // the job may have ended before this worker woke: `claim` is then >= nchunks
-      // (or parked far above it while the next job is being set up)
-      work();
+      work();      // a job that already ended (or is being set up) has no claimable chunk
     }
   }
 };
@@ -935,55 +959,68 @@ extern "C" {
 int dfx_execute_gather(void* graph, const void* const* srcs, const size_t* sizes, int nsrc, void* host_in,
                        void* dev_in, void* host_out, const void* dev_out, size_t out_bytes, void* stream) {
   if (nsrc < 0 || (nsrc > 0 && (!srcs || !sizes)) || !host_in) return fail(DFX_E_ARG, "bad gather list");
-  StagePool* P = stage_pool();
-  std::lock_guard<std::mutex> job(P->job_mu);
-  // park the claim counter far above any chunk count while the list is rewritten,
-  // so a worker still draining the previous job cannot pick up a half-built chunk
-  P->claim.store(1 << 30, std::memory_order_relaxed);
-  // chunk the segments (destination contiguous in host_in, in list order)
-  int n = 0;
-  size_t off = 0;
+  size_t total = 0;
+  int nch = 0;
   for (int i = 0; i < nsrc; ++i) {
-    for (size_t s = 0; s < sizes[i]; s += StagePool::kChunk) {
-      if (n == StagePool::kMaxChunks) return fail(DFX_E_ARG, "gather list too large");
-      const size_t b = std::min(StagePool::kChunk, sizes[i] - s);
-      P->chunks[n] = {static_cast<char*>(host_in) + off + s, static_cast<const char*>(srcs[i]) + s, b};
-      P->done[n].store(0, std::memory_order_relaxed);
-      ++n;
-    }
-    off += sizes[i];
+    total += sizes[i];
+    nch += int((sizes[i] + StagePool::kChunk - 1) / StagePool::kChunk);
   }
-  P->nchunks.store(n, std::memory_order_relaxed);
-  P->claim.store(0, std::memory_order_release);
-  if (!P->workers.empty() && n > 1) {
+  if (nch > StagePool::kMaxChunks) return fail(DFX_E_ARG, "gather list too large");
+  StagePool* P = stage_pool();
+  // The pool serves one staging job at a time; a concurrent query whose staging
+  // finds it busy copies on its own thread instead of waiting.  Only the staging
+  // is serialised: the lock is dropped before the graph launch and the sync.
+  std::unique_lock<std::mutex> job(P->job_mu, std::try_to_lock);
+  if (!job.owns_lock() || P->workers.empty() || nch <= 1) {
+    if (job.owns_lock()) job.unlock();
+    size_t off = 0;
+    for (int i = 0; i < nsrc; ++i) {
+      std::memcpy(static_cast<char*>(host_in) + off, srcs[i], sizes[i]);
+      off += sizes[i];
+    }
+    CK(cudaMemcpyAsync(dev_in, host_in, total, cudaMemcpyHostToDevice, S(stream)));
+  } else {
+    // no claim of the previous job can be outstanding (it ended with every chunk
+    // done); late claimers see n = 0 while the list is rewritten
+    P->claim.store(0, std::memory_order_relaxed);
+    int n = 0;
+    size_t off = 0;
+    for (int i = 0; i < nsrc; ++i) {
+      for (size_t s = 0; s < sizes[i]; s += StagePool::kChunk) {
+        const size_t b = std::min(StagePool::kChunk, sizes[i] - s);
+        P->chunks[n] = {static_cast<char*>(host_in) + off + s, static_cast<const char*>(srcs[i]) + s, b};
+        P->done[n].store(0, std::memory_order_relaxed);
+        ++n;
+      }
+      off += sizes[i];
+    }
+    P->claim.store(uint64_t(n) << StagePool::kIdxBits, std::memory_order_release);
     {
       std::lock_guard<std::mutex> g(P->mu);
       P->gen.fetch_add(1, std::memory_order_release);
     }
     P->cv.notify_all();
-  }
-  // the caller copies chunks too, and issues the H2D of each completed in-order prefix
-  int issued = 0;
-  cudaError_t err = cudaSuccess;
-  while (issued < n) {
-    int ready = issued;
-    while (ready < n && P->done[ready].load(std::memory_order_acquire)) ++ready;
-    if (ready > issued) {
-      const size_t b0 = size_t(P->chunks[issued].dst - static_cast<char*>(host_in));
-      const size_t b1 = size_t(P->chunks[ready - 1].dst - static_cast<char*>(host_in)) + P->chunks[ready - 1].bytes;
-      if (err == cudaSuccess)
-        err = cudaMemcpyAsync(static_cast<char*>(dev_in) + b0, static_cast<char*>(host_in) + b0, b1 - b0,
-                              cudaMemcpyHostToDevice, S(stream));
-      issued = ready;
-      continue;
+    // the caller copies chunks too, and issues the H2D of each completed in-order prefix
+    int issued = 0;
+    cudaError_t err = cudaSuccess;
+    while (issued < n) {
+      int ready = issued;
+      while (ready < n && P->done[ready].load(std::memory_order_acquire)) ++ready;
+      if (ready > issued) {
+        const size_t b0 = size_t(P->chunks[issued].dst - static_cast<char*>(host_in));
+        const size_t b1 = size_t(P->chunks[ready - 1].dst - static_cast<char*>(host_in)) + P->chunks[ready - 1].bytes;
+        if (err == cudaSuccess)
+          err = cudaMemcpyAsync(static_cast<char*>(dev_in) + b0, static_cast<char*>(host_in) + b0, b1 - b0,
+                                cudaMemcpyHostToDevice, S(stream));
+        issued = ready;
+        continue;
+      }
+      const int c = P->take();
+      if (c >= 0) P->copy(c);
     }
-    const int c = P->claim.fetch_add(1, std::memory_order_acq_rel);
-    if (c < n) {
-      std::memcpy(P->chunks[c].dst, P->chunks[c].src, P->chunks[c].bytes);
-      P->done[c].store(1, std::memory_order_release);
-    }
+    job.unlock();
+    CK(err);
   }
-  CK(err);
   int rc = dfx_graph_launch(graph, stream);
   if (rc) return rc;
   CK(cudaMemcpyAsync(host_out, dev_out, out_bytes, cudaMemcpyDeviceToHost, S(stream)));

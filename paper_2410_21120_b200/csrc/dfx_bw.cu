@@ -507,10 +507,12 @@ __global__ void __launch_bounds__(256) in_im2col_kernel(const __grid_constant__ 
       win[rc * ww + col] = (row_ok && ix >= 0 && ix < W) ? __ldg(srow + ix) : 0.f;
     }
   }
-  for (int cc = threadIdx.x; cc < o.c; cc += blockDim.x) {
+  const int kreal = C * kh * kw;                    // real im2col channels
+  const int kb = P.split > 0 ? P.split : o.c;       // channels per block
+  for (int cc = threadIdx.x; cc < kb; cc += blockDim.x) {
     const int rs = cc / C, c = cc - rs * C;
     const int r = rs / kw, s = rs - r * kw;
-    off[cc] = (c * kh + r) * ww + s;
+    off[cc] = cc < kreal ? (c * kh + r) * ww + s : -1;
   }
   __syncthreads();
   const int groups = o.pitch / 8;
@@ -520,7 +522,13 @@ __global__ void __launch_bounds__(256) in_im2col_kernel(const __grid_constant__ 
     const int base = px * P.sw;
     float v[8];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) v[j] = (c0 + j < o.c) ? win[off[c0 + j] + base] : 0.f;
+    for (int j = 0; j < 8; ++j) {
+      const int cc = c0 + j;
+      const int blk = cc / kb, k = cc - blk * kb;
+      const float x = (cc < o.c && off[k] >= 0) ? win[off[k] + base] : 0.f;
+      // split blocks: [x_hi | x_hi | x_lo], x_lo = x - x_hi exactly in fp32
+      v[j] = blk == 2 ? x - Elt<T>::to_f(Elt<T>::from_f(x)) : x;
+    }
     *reinterpret_cast<uint4*>(out + int64_t(px) * o.pitch + c0) = pack8<T>(v);
   }
 }

@@ -24,6 +24,7 @@ import math
 import os
 import threading
 import time
+import weakref
 from dataclasses import dataclass
 
 import numpy as np
@@ -44,15 +45,19 @@ _cache_lock = threading.Lock()
 
 
 def program_for(g, w, precision: str = "fp16") -> MemberProgram:
-    """Lowered program of (graph, weights, precision), cached by object identity."""
+    """Lowered program of (graph, weights, precision), cached by object identity
+    for as long as both objects live (weak references + finalizers: the cache
+    never keeps a graph, a weight store or its packed 16-bit blobs alive)."""
     key = (id(g), id(w), precision)
     with _cache_lock:
         hit = _program_cache.get(key)
-        if hit is not None and hit[0] is g and hit[1] is w:
+        if hit is not None and hit[0]() is g and hit[1]() is w:
             return hit[2]
     prog = lower_member(g, w, precision=precision)
     with _cache_lock:
-        _program_cache[key] = (g, w, prog)
+        _program_cache[key] = (weakref.ref(g), weakref.ref(w), prog)
+    for obj in (g, w):
+        weakref.finalize(obj, _program_cache.pop, key, None).atexit = False
     return prog
 
 
@@ -131,39 +136,95 @@ def fill_arena(buf: np.ndarray, programs: list[MemberProgram], layout) -> None:
 ARENA_POOL = os.environ.get("DFX_ARENA_POOL", "1") != "0"
 
 
-_pooled: set[int] = set()             # arena pointers that came from the pool
+class _Block:
+    """One device (or pinned host) allocation, reference-counted by the arenas
+    that read it: a swapped DAG shares every untouched member's bytes with the
+    DAG it was swapped from, and the memory goes back when the last one is
+    unloaded (release on refs == 0)."""
+
+    _lock = threading.Lock()
+
+    def __init__(self, ptr: int, kind: str):
+        self.ptr, self.kind, self.refs = ptr, kind, 1
+
+    def retain(self) -> "_Block":
+        with self._lock:
+            assert self.refs > 0, "retain of a released block"
+            self.refs += 1
+        return self
+
+    def release(self) -> None:
+        with self._lock:
+            self.refs -= 1
+            last = self.refs == 0
+        if last and self.ptr:
+            {"pool": rt.pool_free, "dev": rt.free, "host": rt.host_free}[self.kind](self.ptr)
+            self.ptr = 0
 
 
-def _arena_malloc(nbytes: int, stream=None) -> int:
+def _arena_block(nbytes: int, stream=None) -> _Block:
     if not ARENA_POOL:
-        return rt.malloc(nbytes)
-    p = rt.pool_malloc(nbytes, stream)
-    _pooled.add(p)
-    return p
-
-
-def _arena_free(ptr: int) -> None:
-    if ptr in _pooled:
-        _pooled.discard(ptr)
-        rt.pool_free(ptr)
-    else:
-        rt.free(ptr)
+        return _Block(rt.malloc(nbytes), "dev")
+    return _Block(rt.pool_malloc(nbytes, stream), "pool")
 
 
 class WeightArena:
-    """Packed weights of all members: host pinned staging + device copy."""
+    """Packed weights of all members: host pinned staging + device copy.
+
+    Ownership: the device allocation(s) and the pinned staging are _Blocks.
+    ``clone_for_swap`` shares them (retain); ``replace_member`` puts the incoming
+    member in a NEW device block, so the source DAG's bytes are never written
+    and it stays valid; ``free`` releases this arena's references."""
 
     def __init__(self, programs: list[MemberProgram], device: int = 0):
         self.device = device
         self.layout, self.segments, self.total = arena_layout(programs)
         rt.init_device(device)
-        self.host = rt.host_alloc(self.total)
-        view = (C.c_uint8 * self.total).from_address(self.host)
+        host = rt.host_alloc(self.total)
+        self._host_block = _Block(host, "host")
+        self.host_pinned = True
+        view = (C.c_uint8 * self.total).from_address(host)
         fill_arena(np.frombuffer(view, dtype=np.uint8), programs, self.layout)
-        self.dev = 0
+        self._init_device_state()
+
+    @classmethod
+    def from_host(cls, layout, segments, total, host: int, device: int = 0, pinned: bool = True,
+                  keep=None) -> "WeightArena":
+        """An arena over an already-filled host buffer (pack_io: read from a file).
+        Pinned buffers are owned (freed with the arena); pageable ones are kept
+        alive through ``keep``."""
+        a = cls.__new__(cls)
+        a.device = device
+        a.layout, a.segments, a.total = layout, segments, total
+        a._host_block = _Block(host, "host") if pinned else None
+        a.host_pinned = pinned
+        a._host_keep = keep
+        a._host_ptr = host
+        a._init_device_state()
+        return a
+
+    def _init_device_state(self):
+        self._dev_block: _Block | None = None
+        self._swap_blocks: list[_Block] = []
         self.member_base: list[int] = []       # device base of each member's segment
-        self.extra_allocs: list[int] = []
         self.upload_ms = None
+        self.last_swap = None
+
+    @property
+    def host(self) -> int:
+        return self._host_block.ptr if self._host_block is not None else getattr(self, "_host_ptr", 0)
+
+    @property
+    def dev(self) -> int:
+        return self._dev_block.ptr if self._dev_block is not None else 0
+
+    @property
+    def shared(self) -> bool:
+        return any(b.refs > 1 for b in self._blocks())
+
+    def _blocks(self):
+        out = [self._dev_block] if self._dev_block is not None else []
+        return out + list(self._swap_blocks)
 
     def upload(self, stream=None) -> float:
         """ONE device allocation + ONE H2D copy of the whole arena; returns ms.
@@ -171,8 +232,10 @@ class WeightArena:
         The two phases are timed apart (the reference's cost model books them
         as separate cudaMalloc / cudaMemcpyAsync rows, costmodel.py:297-300):
         ``malloc_ms`` by wall clock, ``memcpy_ms`` by CUDA events."""
+        if self._dev_block is not None:
+            raise RuntimeError("arena already resident (unload() first)")
         t0 = time.perf_counter()
-        self.dev = _arena_malloc(self.total, stream)
+        self._dev_block = _arena_block(self.total, stream)
         self.malloc_ms = (time.perf_counter() - t0) * 1e3
         e0, e1 = rt.Event(), rt.Event()
         e0.record(stream)
@@ -186,65 +249,92 @@ class WeightArena:
 
     def unload(self) -> None:
         """Free the device copy, keep the pinned host staging (swap-out; the next
-        upload() is again one cudaMalloc + one H2D)."""
-        if self.dev:
-            _arena_free(self.dev)
-        self.dev = 0
+        upload() is again one allocation + one H2D).  Only for an arena no
+        swapped DAG shares."""
+        if self.shared:
+            raise RuntimeError("arena shared with a swapped DAG: unload the DAGs instead")
+        for b in self._blocks():
+            b.release()
+        self._dev_block, self._swap_blocks = None, []
         self.member_base = []
 
     def allocate(self) -> None:
         """Device allocation only (a replica that receives the arena by broadcast)."""
-        self.dev = _arena_malloc(self.total)
+        self._dev_block = _arena_block(self.total)
         self.member_base = [self.dev + off for off, _ in self.segments]
 
     def addr(self, member: int, key: str) -> int:
         return self.member_base[member] + (self.layout[member][key] - self.segments[member][0])
 
-    def replace_member(self, member: int, prog: MemberProgram, stream=None) -> float:
-        """swap_subgraph: pack + upload only the incoming member's segment."""
+    def segment(self, member: int) -> tuple[int, int]:
+        """(device address, bytes) of one member's weights."""
+        return self.member_base[member], self.segments[member][1]
+
+    def replace_member(self, member: int, prog: MemberProgram, stream=None, upload: bool = True) -> float:
+        """swap_subgraph: pack the incoming member and upload ONLY its segment, into
+        a fresh device block (never into bytes the source DAG may be reading).
+        Returns the wall ms of allocation + H2D; ``last_swap`` has the phases."""
         offs, at = {}, 0
         for key in sorted(prog.blobs):
             offs[key] = at
             at = _align(at + prog.blobs[key].nbytes)
         size = max(at, ALIGN)
+        if not upload:                       # a replica receiving the segment by broadcast
+            blk = _arena_block(size, stream)
+            self.last_swap = {"bytes": size, "malloc_ms": None, "memcpy_ms": None, "ms": 0.0}
+            self._swap_blocks.append(blk)
+            self.member_base[member] = blk.ptr
+            self.layout[member] = offs
+            self.segments[member] = (0, size)
+            return 0.0
         host = rt.host_alloc(size)
-        buf = np.frombuffer((C.c_uint8 * size).from_address(host), dtype=np.uint8)
-        for key, off in offs.items():
-            raw = prog.blobs[key].view(np.uint8).reshape(-1)
-            buf[off:off + raw.size] = raw
-        t0 = time.perf_counter()
-        cap = self.segments[member][1]
-        if size <= cap:
-            base = self.member_base[member]
-        else:
-            base = rt.malloc(size)
-            self.extra_allocs.append(base)
-        rt.h2d(base, host, size, stream)
-        rt.stream_sync(stream)
-        ms = (time.perf_counter() - t0) * 1e3
-        rt.host_free(host)
-        self.member_base[member] = base
+        try:
+            buf = np.frombuffer((C.c_uint8 * size).from_address(host), dtype=np.uint8)
+            for key, off in offs.items():
+                raw = prog.blobs[key].view(np.uint8).reshape(-1)
+                buf[off:off + raw.size] = raw
+            t0 = time.perf_counter()
+            blk = _arena_block(size, stream)
+            t1 = time.perf_counter()
+            e0, e1 = rt.Event(), rt.Event()
+            e0.record(stream)
+            rt.h2d(blk.ptr, host, size, stream)
+            e1.record(stream)
+            rt.stream_sync(stream)
+            ms = (time.perf_counter() - t0) * 1e3
+            self.last_swap = {"bytes": size, "malloc_ms": (t1 - t0) * 1e3, "memcpy_ms": e0.elapsed_ms(e1),
+                              "ms": ms}
+        finally:
+            rt.host_free(host)
+        self._swap_blocks.append(blk)
+        self.member_base[member] = blk.ptr
         self.layout[member] = offs
-        self.segments[member] = (0, max(cap, size)) if size <= cap else (0, size)
+        self.segments[member] = (0, size)
         return ms
 
     def clone_for_swap(self) -> "WeightArena":
+        """A second arena over the same blocks (each retained once more)."""
         twin = object.__new__(WeightArena)
         twin.__dict__.update(self.__dict__)
         twin.layout = list(self.layout)
         twin.segments = list(self.segments)
         twin.member_base = list(self.member_base)
+        twin._dev_block = self._dev_block.retain() if self._dev_block is not None else None
+        twin._swap_blocks = [b.retain() for b in self._swap_blocks]
+        twin._host_block = self._host_block.retain() if self._host_block is not None else None
         return twin
 
     def free(self):
-        if self.dev:
-            _arena_free(self.dev)
-        for p in self.extra_allocs:
-            rt.free(p)
-        if getattr(self, "host_pinned", True):       # pack_io may stage in pageable memory
-            rt.host_free(self.host)
+        """Release this arena's references (device blocks, pinned staging);
+        idempotent."""
+        for b in self._blocks():
+            b.release()
+        if self._host_block is not None:
+            self._host_block.release()
+        self._dev_block, self._swap_blocks, self._host_block = None, [], None
         self._host_keep = None
-        self.dev = self.host = 0
+        self._host_ptr = 0
+        self.member_base = []
 
 
 class PerTensorArena:
@@ -518,7 +608,7 @@ class ExecInstance:
             ic = prog.input_im2col or (0, 0, 0, 0, 0, 0)
             ind = tuple(prog.input_dims) if len(prog.input_dims) == 3 else (prog.input_dims[0], 1, 1)
             pin = rt.InParams(self.dev_in + self.in_off[m], self._view(m, prog, "<input>", n),
-                              *ic, *ind)
+                              *ic, *ind, getattr(prog, "input_split", 0))
             last = g.add(rt.OP_IN, pin, deps)
             self._node_member.append(m)
             self.nodes.append((rt.OP_IN, pin, dict(member=m, kind="in", flops=0,
@@ -917,11 +1007,11 @@ class DeviceDag:
         finally:
             self.release(inst)
 
-    def swapped(self, index: int, incoming) -> "DeviceDag":
+    def swapped(self, index: int, incoming, upload: bool = True) -> "DeviceDag":
         g, w = incoming
         prog = program_for(g, w, self.precision)
         arena = self.arena.clone_for_swap()
-        ms = arena.replace_member(index, prog)
+        ms = arena.replace_member(index, prog, upload=upload)
         members = list(self.members)
         members[index] = incoming
         programs = list(self.programs)
@@ -929,6 +1019,7 @@ class DeviceDag:
         out = DeviceDag(members, self.device, self.mode, arena=arena, programs=programs,
                         precision=self.precision)
         out.last_swap_ms = ms
+        out.last_swap = dict(arena.last_swap, member=index)
         return out
 
     def free_instances(self):
@@ -937,3 +1028,9 @@ class DeviceDag:
                 inst.free()
             self._all.clear()
             self._pool.clear()
+
+    def free(self):
+        """Swap-out: every execution instance and this image's arena references
+        (device blocks shared with a swapped DAG stay until it is freed too)."""
+        self.free_instances()
+        self.arena.free()

@@ -12,6 +12,7 @@ libdfx or a B200 the call raises ``DeviceError``.
 from __future__ import annotations
 
 import threading
+import weakref
 from dataclasses import dataclass
 
 import numpy as np
@@ -51,8 +52,17 @@ class Tensor:
         return self.values.reshape(self.spec.dims)
 
 
+# (id(g), id(w)) -> (weakref g, weakref w, DeviceDag): the solo device DAG of a
+# (graph, weights) pair lives as long as both objects do (a finalizer frees it)
 _solo: dict[tuple[int, int], tuple] = {}
 _solo_lock = threading.Lock()
+
+
+def _drop_solo(key) -> None:
+    with _solo_lock:
+        hit = _solo.pop(key, None)
+    if hit is not None:
+        hit[2].free()
 
 
 def _solo_dag(g, w):
@@ -60,11 +70,16 @@ def _solo_dag(g, w):
     key = (id(g), id(w))
     with _solo_lock:
         hit = _solo.get(key)
-        if hit is not None and hit[0] is g and hit[1] is w:
+        if hit is not None and hit[0]() is g and hit[1]() is w:
             return hit[2]
     d = DeviceDag([(g, w)])
     with _solo_lock:
-        _solo[key] = (g, w, d)
+        old = _solo.get(key)
+        _solo[key] = (weakref.ref(g), weakref.ref(w), d)
+    if old is not None:
+        old[2].free()
+    for obj in (g, w):
+        weakref.finalize(obj, _drop_solo, key).atexit = False
     return d
 
 

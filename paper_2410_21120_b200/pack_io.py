@@ -12,9 +12,11 @@ Layout (little-endian):
   graph (``model_io.graph_to_dict``, the reference's graph JSON), its weight
   tensor specs, its arena segment and the byte offset of every packed blob.
 * The program table is the lowered launch list of each member
-  (``lower.MemberProgram`` with the blob arrays left out), pickled: this is a
-  local cache written by ``save_packed`` for the same library build, not an
-  interchange format -- load only files you wrote.
+  (``lower.MemberProgram`` with the blob arrays left out) as JSON: dataclasses
+  from a fixed whitelist and base64 arrays, so reading a file never runs code
+  from it.  It is a cache written by ``save_packed`` for the same library
+  build (the layout is re-derived and checked at load), not an interchange
+  format.
 * The arena bytes are exactly what ``device.WeightArena`` uploads: 16-bit GEMM
   weights, fp32 epilogue vectors, 256-B aligned, member segments in member
   order.
@@ -32,7 +34,6 @@ from __future__ import annotations
 import copy
 import ctypes as C
 import json
-import pickle
 import struct
 import time
 from pathlib import Path
@@ -43,7 +44,7 @@ from . import fuse, model_io
 from .graph_ir import TensorSpec, WeightStore
 
 MAGIC = b"DFXPACK1"
-VERSION = 1
+VERSION = 2                  # 2: program table as JSON (was pickle)
 PAGE = 4096
 
 
@@ -64,16 +65,77 @@ class PackedWeights(WeightStore):
     array = values
 
 
-def _program_table(programs):
+# The lowered programs travel as JSON: dataclasses of lower.py (a fixed whitelist)
+# and numpy arrays (dtype, shape, base64 bytes).  Loading a packed file therefore
+# never executes code from it (no pickle).
+def _program_classes():
+    from .lower import Buffer, Epi, Launch, MemberProgram, Value
+    return {c.__name__: c for c in (Buffer, Epi, Launch, MemberProgram, Value)}
+
+
+def _enc(x):
+    import base64
+    import dataclasses
+    if dataclasses.is_dataclass(x) and not isinstance(x, type):
+        return {"__dc__": type(x).__name__,
+                "f": {f.name: _enc(getattr(x, f.name)) for f in dataclasses.fields(x)}}
+    if isinstance(x, np.ndarray):
+        a = np.ascontiguousarray(x)
+        return {"__nd__": a.dtype.str, "shape": list(a.shape), "b64": base64.b64encode(a.tobytes()).decode()}
+    if isinstance(x, np.generic):
+        return x.item()
+    if isinstance(x, tuple):
+        return {"__t__": [_enc(v) for v in x]}
+    if isinstance(x, list):
+        return [_enc(v) for v in x]
+    if isinstance(x, dict):
+        if not all(isinstance(k, str) for k in x):
+            return {"__kv__": [[_enc(k), _enc(v)] for k, v in x.items()]}
+        return {"__d__": {k: _enc(v) for k, v in x.items()}}
+    if x is None or isinstance(x, (bool, int, float, str)):
+        return x
+    raise TypeError(f"cannot serialise {type(x).__name__} in a program table")
+
+
+def _dec(x, classes):
+    import base64
+    if isinstance(x, list):
+        return [_dec(v, classes) for v in x]
+    if not isinstance(x, dict):
+        return x
+    if "__dc__" in x:
+        cls = classes.get(x["__dc__"])
+        if cls is None:
+            raise ValueError(f"unexpected type {x['__dc__']!r} in a program table")
+        return cls(**{k: _dec(v, classes) for k, v in x["f"].items()})
+    if "__nd__" in x:
+        return np.frombuffer(base64.b64decode(x["b64"]), dtype=np.dtype(x["__nd__"])).reshape(x["shape"]).copy()
+    if "__t__" in x:
+        return tuple(_dec(v, classes) for v in x["__t__"])
+    if "__kv__" in x:
+        return {_dec(k, classes): _dec(v, classes) for k, v in x["__kv__"]}
+    if "__d__" in x:
+        return {k: _dec(v, classes) for k, v in x["__d__"].items()}
+    raise ValueError("malformed program table")
+
+
+def _program_table(programs) -> bytes:
     metas = []
     for p in programs:
         m = copy.copy(p)
         m.blobs = {k: (str(v.dtype), tuple(v.shape)) for k, v in p.blobs.items()}
-        for attr in ("debug_f32",):
-            if hasattr(m, attr):
-                setattr(m, attr, None)
         metas.append(m)
-    return pickle.dumps(metas, protocol=pickle.HIGHEST_PROTOCOL)
+    return json.dumps([_enc(m) for m in metas]).encode()
+
+
+def _read_program_table(raw: bytes) -> list:
+    classes = _program_classes()
+    out = []
+    for d in json.loads(raw):
+        m = _dec(d, classes)
+        m.debug_f32 = {}
+        out.append(m)
+    return out
 
 
 def save_packed(dag: fuse.FusedDag, path, precision: str = "fp16") -> dict:
@@ -108,11 +170,11 @@ def read_header(path) -> tuple[dict, list, int]:
             raise ValueError(f"{path}: not a packed-arena file")
         (hn,) = struct.unpack("<Q", f.read(8))
         header = json.loads(f.read(hn))
+        if header.get("version") != VERSION:
+            raise ValueError(f"{path}: packed-arena version {header.get('version')} != {VERSION}")
         (pn,) = struct.unpack("<Q", f.read(8))
-        table = pickle.loads(f.read(pn))
+        table = _read_program_table(f.read(pn))
         data_off = -(-(16 + hn + 8 + pn) // PAGE) * PAGE
-    if header.get("version") != VERSION:
-        raise ValueError(f"{path}: packed-arena version {header.get('version')} != {VERSION}")
     return header, table, data_off
 
 
@@ -194,12 +256,7 @@ def load_packed(path, device: int = 0, mode: str = "concurrent", pinned: bool = 
         if pinned:
             rt.host_free(host)
         raise ValueError(f"{path}: arena layout does not match this library build")
-    arena = WeightArena.__new__(WeightArena)
-    arena.device = device
-    arena.layout, arena.segments, arena.total = layout, segments, total
-    arena.host, arena.dev, arena.member_base, arena.extra_allocs = host, 0, [], []
-    arena.host_pinned, arena._host_keep = pinned, hb
-    arena.upload_ms = None
+    arena = WeightArena.from_host(layout, segments, total, host, device, pinned=pinned, keep=hb)
     arena.upload()
     t4 = time.perf_counter()
     if "mem_estimate_mib" in header:        # the packed DAG's estimate: no profile_graph pass

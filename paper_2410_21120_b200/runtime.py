@@ -90,7 +90,7 @@ class EwParams(C.Structure):
 
 class InParams(C.Structure):
     _fields_ = [("src", vp), ("out", View), ("kh", i32), ("kw", i32), ("sh", i32), ("sw", i32),
-                ("ph", i32), ("pw", i32), ("c", i32), ("h", i32), ("w", i32), ("_pad", i32)]
+                ("ph", i32), ("pw", i32), ("c", i32), ("h", i32), ("w", i32), ("split", i32)]
 
 
 class OutParams(C.Structure):
@@ -138,7 +138,7 @@ OP_PARAMS = {OP_GEMM: GemmLaunch, OP_SPLITK: SplitKParams, OP_DWCONV: DwconvPara
 # every symbol include/dfx.h declares (tests check the .so exports all of them)
 EXPORTS = (
     "dfx_last_error", "dfx_abi_version", "dfx_sizeof", "dfx_init", "dfx_device_info", "dfx_mem_info",
-    "dfx_malloc", "dfx_free", "dfx_memset", "dfx_pool_malloc", "dfx_pool_free", "dfx_pool_trim", "dfx_host_alloc", "dfx_host_free",
+    "dfx_malloc", "dfx_free", "dfx_memset", "dfx_pool_malloc", "dfx_pool_free", "dfx_pool_trim", "dfx_pool_stats", "dfx_host_alloc", "dfx_host_free",
     "dfx_host_register", "dfx_host_unregister", "dfx_memcpy_h2d", "dfx_memcpy_d2h",
     "dfx_memcpy_d2d", "dfx_arena_upload", "dfx_stream_create", "dfx_stream_destroy",
     "dfx_stream_sync", "dfx_event_create", "dfx_event_destroy", "dfx_event_record",
@@ -222,6 +222,13 @@ def pool_free(ptr: int, stream=None) -> None:
 
 def pool_trim(keep_bytes: int = 0) -> None:
     call("dfx_pool_trim", C.c_size_t(keep_bytes))
+
+
+def pool_stats() -> tuple[int, int]:
+    """(bytes the arena pool keeps mapped, bytes of it in use)."""
+    r, u = C.c_size_t(), C.c_size_t()
+    call("dfx_pool_stats", C.byref(r), C.byref(u))
+    return r.value, u.value
 
 
 def host_alloc(nbytes: int) -> int:

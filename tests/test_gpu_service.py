@@ -69,6 +69,6 @@ def test_socket(tmp_path):
             break
         data += chunk
     c.close()
-    s._stop.set()
+    s.stop()
     t.join(60)
     check_done(repo, data.decode().splitlines(), reqs)

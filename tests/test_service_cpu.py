@@ -32,3 +32,25 @@ def test_replies(tmp_path):
     assert got == ["ACK req00001", "REJ unknown-model", "REJ iterations-must-be->=-1", "ERR parse", "ERR parse",
                    "ACK req00004"]
     assert [r.request_id for r in s.queue.snapshot()] == ["req00001", "req00004"]
+
+
+def test_parse_request_grammar():
+    import pytest
+    from paper_2410_21120_b200.service import ParseError, Request, parse_request
+    assert parse_request("REQ m0 5 short zeros") == Request("m0", 5, "short", "zeros")
+    assert parse_request("  REQ m0 -1 long rand:3 \n") == Request("m0", -1, "long", "rand:3")
+    assert parse_request("") is None and parse_request(" \t\n") is None
+    for bad in ("REQ m0 5 short", "REQ m0 5 short zeros extra", "ACK x", "REQ m0 five short zeros",
+                "req m0 5 short zeros"):
+        with pytest.raises(ParseError):
+            parse_request(bad)
+
+
+def test_stdio_transport_replies_without_gpu(tmp_path):
+    """serve_stdin with requests that are all refused at ingest: the lane never
+    needs the GPU, every line is answered in order and EOF returns."""
+    import io
+    s = loop(tmp_path)
+    out = io.StringIO()
+    s.serve_stdin(io.StringIO("REQ ghost 5 short zeros\nbad line\n\nREQ m1 0 short zeros\n"), out)
+    assert out.getvalue().splitlines() == ["REJ unknown-model", "ERR parse", "REJ iterations-must-be->=-1"]
