@@ -34,7 +34,7 @@
 extern "C" {
 #endif
 
-#define DFX_ABI_VERSION 3
+#define DFX_ABI_VERSION 4
 
 typedef enum dfx_status {
   DFX_OK = 0,
@@ -78,7 +78,14 @@ typedef enum dfx_op {
 
 typedef enum dfx_dtype {
   DFX_BF16 = 0,        /* bfloat16 storage, kind::f16 MMA with BF16 operands */
-  DFX_F16 = 1          /* IEEE half storage (saturating stores), F16 operands */
+  DFX_F16 = 1,         /* IEEE half storage (saturating stores), F16 operands */
+  /* Split precision: every value stored as two 16-bit planes x = hi + lo
+   * (hi = rn(x), lo = rn(x - hi)); a view's pitch spans both planes of a pixel,
+   * the lo plane of channel c sits pitch/2 elements after the hi one.  GEMMs
+   * accumulate hi*hi + lo*hi + hi*lo on the tensor core (fp32); weights are
+   * packed [hi rows; lo rows].  The accurate mode (fp32-class logits). */
+  DFX_BF16X2 = 2,
+  DFX_F16X2 = 3
 } dfx_dtype;
 
 /* A 16-bit NHWC view: element (n, h, w, c) at base[((n*H + h)*W + w)*pitch + coff + c].

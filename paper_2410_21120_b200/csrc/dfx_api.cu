@@ -40,14 +40,22 @@ template <typename T> __global__ void tokens_kernel(const __grid_constant__ dfx_
 template <typename T> __global__ void attn_kernel(const __grid_constant__ dfx_attn_params P);
 }  // namespace dfx
 
-// kernel instantiation for a storage dtype (DFX_F16 / DFX_BF16)
-#define DFX_PICK(K, dt) \
+// kernel instantiation for a storage dtype (DFX_F16 / DFX_BF16 / DFX_F16X2 / DFX_BF16X2)
+#define DFX_PICK(K, dt)                                                              \
+  ((dt) == DFX_F16      ? reinterpret_cast<const void*>(&dfx::K<__half>)           \
+   : (dt) == DFX_BF16   ? reinterpret_cast<const void*>(&dfx::K<__nv_bfloat16>)    \
+   : (dt) == DFX_F16X2  ? reinterpret_cast<const void*>(&dfx::K<dfx::f16x2>)       \
+                        : reinterpret_cast<const void*>(&dfx::K<dfx::bf16x2>))
+// kernels without a split-precision instantiation (ViT, fused dw+SE): 16-bit only
+#define DFX_PICK16(K, dt) \
   ((dt) == DFX_F16 ? reinterpret_cast<const void*>(&dfx::K<__half>) \
                    : reinterpret_cast<const void*>(&dfx::K<__nv_bfloat16>))
 
 namespace {
 
 const void* gemm_func(int dt, int m2) {
+  if (dt == DFX_F16X2) return reinterpret_cast<const void*>(&dfx::gemm_kernel<dfx::f16x2, 0>);
+  if (dt == DFX_BF16X2) return reinterpret_cast<const void*>(&dfx::gemm_kernel<dfx::bf16x2, 0>);
   if (m2)
     return dt == DFX_F16 ? reinterpret_cast<const void*>(&dfx::gemm_kernel<__half, 1>)
                          : reinterpret_cast<const void*>(&dfx::gemm_kernel<__nv_bfloat16, 1>);
@@ -56,6 +64,8 @@ const void* gemm_func(int dt, int m2) {
 }
 
 const void* se_func(int dt, int cl, int ipi = 1) {
+  if (dt == DFX_F16X2) return reinterpret_cast<const void*>(&dfx::se_kernel<dfx::f16x2, 16, 1>);
+  if (dt == DFX_BF16X2) return reinterpret_cast<const void*>(&dfx::se_kernel<dfx::bf16x2, 16, 1>);
   if (ipi == 4)
     return dt == DFX_F16 ? reinterpret_cast<const void*>(&dfx::se_kernel<__half, 16, 4>)
                          : reinterpret_cast<const void*>(&dfx::se_kernel<__nv_bfloat16, 16, 4>);
@@ -105,11 +115,20 @@ const void* ew_vec_func_t(int act) {
   }
 }
 const void* ew_vec_func(int dt, int act) {
-  return dt == DFX_F16 ? ew_vec_func_t<__half>(act) : ew_vec_func_t<__nv_bfloat16>(act);
+  switch (dt) {
+    case DFX_F16: return ew_vec_func_t<__half>(act);
+    case DFX_F16X2: return ew_vec_func_t<dfx::f16x2>(act);
+    case DFX_BF16X2: return ew_vec_func_t<dfx::bf16x2>(act);
+    default: return ew_vec_func_t<__nv_bfloat16>(act);
+  }
 }
 const void* dwconv_tile_func(int dt, int k, int s, int qv, int act) {
-  return dt == DFX_F16 ? dwconv_tile_func_t<__half>(k, s, qv, act)
-                       : dwconv_tile_func_t<__nv_bfloat16>(k, s, qv, act);
+  switch (dt) {
+    case DFX_F16: return dwconv_tile_func_t<__half>(k, s, qv, act);
+    case DFX_F16X2: return dwconv_tile_func_t<dfx::f16x2>(k, s, qv, act);
+    case DFX_BF16X2: return dwconv_tile_func_t<dfx::bf16x2>(k, s, qv, act);
+    default: return dwconv_tile_func_t<__nv_bfloat16>(k, s, qv, act);
+  }
 }
 
 thread_local std::string g_err;
@@ -163,7 +182,8 @@ CUtensorMapSwizzle swizzle_for(int cb) {
 }
 
 CUtensorMapDataType tmap_dtype(int dt) {
-  return dt == DFX_F16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
+  return (dt == DFX_F16 || dt == DFX_F16X2) ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16
+                                            : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
 }
 
 int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
@@ -195,6 +215,10 @@ int config_for(int op, const void* params, size_t size, LaunchCfg* c) {
       const auto* p = static_cast<const dfx_gemm_launch*>(params);
       if (p->bn_max < 16 || p->bn_max > 256 || p->total_tiles < 1)
         return fail(DFX_E_ARG, "gemm: bad bn_max %d / tiles %d", p->bn_max, p->total_tiles);
+      const int planes = dfx::dtype_split(p->dtype) ? 2 : 1;
+      if (planes == 2 && (p->m2 || p->desc0.pre_mode || p->desc0.dw_k > 0 || (p->flags & 4)))
+        return fail(DFX_E_UNSUPPORTED, "gemm: split precision without m2 / A transform / dw epilogue / staged drain");
+      if (p->dtype < DFX_BF16 || p->dtype > DFX_F16X2) return fail(DFX_E_ARG, "gemm: dtype %d", p->dtype);
       c->func = gemm_func(p->dtype, p->m2);
       c->grid = dim3(p->total_tiles);
       c->block = dim3(dfx::kGemmThreads);
@@ -212,17 +236,17 @@ int config_for(int op, const void* params, size_t size, LaunchCfg* c) {
         // producers / MMA issuers per SM); else one CTA per SM with two groups
         const int per_sm = (p->bn_max <= 64 && !p->desc0.pre_mode) ? 2 : 1;   // pre_mode: 2 groups
         const int groups = 3 - per_sm;
-        c->smem = dfx::gemm_smem_bytes(p->bn_max, p->nslots, 0) + 1024 +
+        c->smem = dfx::gemm_smem_bytes(p->bn_max, p->nslots, 0, planes) + 1024 +
                   ((p->flags & 4) ? 4 * groups * dfx::kEpiStageWarpBytes : 0);
         c->grid = dim3(unsigned(std::min<int64_t>(p->total_tiles, int64_t(per_sm) * g_sm_count)));
         c->block = dim3(64 + 128 * groups);
       } else {
-        c->smem = dfx::gemm_smem_bytes(p->bn_max, p->nslots, p->m2 ? 1 : 0) + 1024;
+        c->smem = dfx::gemm_smem_bytes(p->bn_max, p->nslots, p->m2 ? 1 : 0, planes) + 1024;
         if (p->flags & 8) {             // cluster split-K: one cluster per output tile
           const int sp = p->desc0.splits;
           if (p->m2 || p->ndesc != 1 || sp < 2 || sp > 8 || p->total_tiles % sp)
             return fail(DFX_E_ARG, "gemm: cluster split-K needs one problem, no m2, 2..8 splits");
-          if (size_t(128) * (p->bn_max + 4) * 4 > size_t(p->nslots) * dfx::gemm_slot_bytes(p->bn_max, 0))
+          if (size_t(128) * (p->bn_max + 4) * 4 > size_t(p->nslots) * dfx::gemm_slot_bytes(p->bn_max, 0, planes))
             return fail(DFX_E_ARG, "gemm: cluster split-K partial tile exceeds the %d slots", p->nslots);
           c->cluster = unsigned(sp);
         }
@@ -314,6 +338,8 @@ int config_for(int op, const void* params, size_t size, LaunchCfg* c) {
       if (p->out.pitch % 8 || p->out.coff) return fail(DFX_E_ARG, "in: pitch/coff");
       if (p->kh > 0) {
         const int kreal = p->kh * p->kw * p->c;
+        if (p->split > 0 && dfx::dtype_split(p->out.dtype))
+          return fail(DFX_E_ARG, "in: split stem with split-precision storage");
         const bool ok = p->split > 0 ? (p->split >= kreal && p->out.c == 3 * p->split && p->split <= dfx::kIm2colMaxK)
                                      : (p->out.c == kreal && p->out.c <= dfx::kIm2colMaxK);
         if (!ok) return fail(DFX_E_UNSUPPORTED, "in: im2col of %d channels (split %d)", p->out.c, p->split);
@@ -326,7 +352,8 @@ int config_for(int op, const void* params, size_t size, LaunchCfg* c) {
         return DFX_OK;
       }
       c->func = DFX_PICK(in_kernel, p->out.dtype);
-      c->grid = dim3(elementwise_grid(int64_t(p->out.n) * p->out.h * p->out.w * (p->out.pitch / 8), 256));
+      const int plane_pitch = dfx::dtype_split(p->out.dtype) ? p->out.pitch / 2 : p->out.pitch;
+      c->grid = dim3(elementwise_grid(int64_t(p->out.n) * p->out.h * p->out.w * (plane_pitch / 8), 256));
       return DFX_OK;
     }
     case DFX_OP_OUT: {
@@ -354,14 +381,16 @@ int config_for(int op, const void* params, size_t size, LaunchCfg* c) {
       // images).  Off by default: the lost pooling/scaling parallelism costs more than
       // the weight traffic saves (EfficientNetV2-L batch 32 6.73 vs 6.07 ms)
       static const int ipi_env = getenv("DFX_SE_IPI") ? atoi(getenv("DFX_SE_IPI")) : 1;
-      const int ipi = (ipi_env == 4 && cl == 16 && p->in.n >= 8) ? 4 : 1;
+      const int ipi = (ipi_env == 4 && cl == 16 && p->in.n >= 8 && !dfx::dtype_split(p->in.dtype)) ? 4 : 1;
+      const bool split = dfx::dtype_split(p->in.dtype);       // FC weights from L2, no x tile
+      if (split) cl = 16;
       c->func = se_func(p->in.dtype, cl, ipi);
       c->grid = dim3(unsigned(cl), unsigned((p->in.n + ipi - 1) / ipi));
-      c->smem = (p->apply & 2) ? 0 : size_t(dfx::se_smem_bytes(p->in.c, p->cr, cl));
+      c->smem = ((p->apply & 2) || split) ? 0 : size_t(dfx::se_smem_bytes(p->in.c, p->cr, cl));
       // room for the CTA's x slice (latency-bound small batches): the scale reads smem
       // (batch 1: EfficientNetV2-L 2.10 -> 2.08 ms; at batch 32 it costs occupancy)
       static const int xt_batch = getenv("DFX_SE_XTILE_BATCH") ? atoi(getenv("DFX_SE_XTILE_BATCH")) : 8;
-      if ((p->apply & 1) && ipi == 1 && p->in.n < xt_batch) {
+      if (!split && (p->apply & 1) && ipi == 1 && p->in.n < xt_batch) {
         const size_t xt = size_t(p->in.h) * p->in.w * dfx::se_chan_slice(p->in.c, cl) * 2;
         if (c->smem + xt <= size_t(dfx::kSeSmemBudget)) c->smem += xt;
       }
@@ -377,7 +406,8 @@ int config_for(int op, const void* params, size_t size, LaunchCfg* c) {
           p->dw_epi.binop != DFX_BIN_NONE)
         return fail(DFX_E_UNSUPPORTED, "dwse: c=%d cr=%d / views beyond the fused kernel's limits",
                     p->in.c, p->cr);
-      c->func = DFX_PICK(dwse_kernel, p->in.dtype);
+      if (dfx::dtype_split(p->in.dtype)) return fail(DFX_E_UNSUPPORTED, "dwse: split precision");
+      c->func = DFX_PICK16(dwse_kernel, p->in.dtype);
       c->grid = dim3(16u, unsigned(p->in.n));
       c->smem = size_t(dfx::dwse_smem_bytes(p->in.c, p->cr, p->out.h * p->out.w, p->staged));
       if (c->smem > size_t(dfx::kSeSmemBudget))
@@ -390,7 +420,8 @@ int config_for(int op, const void* params, size_t size, LaunchCfg* c) {
       if (p->out.w > p->in.w || p->out.c != p->in.c || p->out.n != p->in.n || p->in.h != 1 ||
           (p->norm && (!p->gamma || !p->beta)))
         return fail(DFX_E_ARG, "ln: bad views/weights");
-      c->func = DFX_PICK(ln_kernel, p->in.dtype);
+      if (dfx::dtype_split(p->in.dtype)) return fail(DFX_E_UNSUPPORTED, "ln: split precision");
+      c->func = DFX_PICK16(ln_kernel, p->in.dtype);
       c->grid = dim3(unsigned(cdiv(int64_t(p->out.n) * p->out.w, 8)));
       c->block = dim3(256);
       return DFX_OK;
@@ -401,7 +432,8 @@ int config_for(int op, const void* params, size_t size, LaunchCfg* c) {
       if (p->out.w != 1 + p->in.h * p->in.w || p->out.c != p->in.c || p->out.h != 1)
         return fail(DFX_E_ARG, "tokens: out (%d, %d, %d) for grid (%d, %d, %d)", p->out.h, p->out.w,
                     p->out.c, p->in.h, p->in.w, p->in.c);
-      c->func = DFX_PICK(tokens_kernel, p->out.dtype);
+      if (dfx::dtype_split(p->out.dtype)) return fail(DFX_E_UNSUPPORTED, "tokens: split precision");
+      c->func = DFX_PICK16(tokens_kernel, p->out.dtype);
       c->grid = dim3(elementwise_grid(int64_t(p->out.n) * p->out.w * cdiv(p->out.c, 8), 256));
       return DFX_OK;
     }
@@ -414,7 +446,8 @@ int config_for(int op, const void* params, size_t size, LaunchCfg* c) {
           ((p->qkv.pitch | p->qkv.coff | p->out.pitch | p->out.coff) & 7))
         return fail(DFX_E_UNSUPPORTED, "attention: L=%d heads=%d c=%d (head dim 64, L <= %d)", L,
                     p->heads, p->out.c, dfx::kAttnMaxL);
-      c->func = DFX_PICK(attn_kernel, p->qkv.dtype);
+      if (dfx::dtype_split(p->qkv.dtype)) return fail(DFX_E_UNSUPPORTED, "attn: split precision");
+      c->func = DFX_PICK16(attn_kernel, p->qkv.dtype);
       c->grid = dim3(unsigned(cdiv(L, 64)), unsigned(p->heads), unsigned(p->qkv.n));
       c->block = dim3(128);
       c->smem = size_t(dfx::attn_smem_bytes(L));
@@ -497,11 +530,19 @@ int dfx_init(int device) {
     CK(cudaFuncSetAttribute(se_func(dt, 16, 4), cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     CK(cudaFuncSetAttribute(se_func(dt, 16, 4), cudaFuncAttributeMaxDynamicSharedMemorySize,
                             dfx::kSeSmemBudget));
-    CK(cudaFuncSetAttribute(DFX_PICK(dwse_kernel, dt), cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-    CK(cudaFuncSetAttribute(DFX_PICK(dwse_kernel, dt), cudaFuncAttributeMaxDynamicSharedMemorySize,
+    CK(cudaFuncSetAttribute(DFX_PICK16(dwse_kernel, dt), cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    CK(cudaFuncSetAttribute(DFX_PICK16(dwse_kernel, dt), cudaFuncAttributeMaxDynamicSharedMemorySize,
                             dfx::kSeSmemBudget));
-    CK(cudaFuncSetAttribute(DFX_PICK(attn_kernel, dt), cudaFuncAttributeMaxDynamicSharedMemorySize,
+    CK(cudaFuncSetAttribute(DFX_PICK16(attn_kernel, dt), cudaFuncAttributeMaxDynamicSharedMemorySize,
                             dfx::attn_smem_bytes(dfx::kAttnMaxL)));
+  }
+  for (int dt : {int(DFX_BF16X2), int(DFX_F16X2)}) {         // split precision
+    CK(cudaFuncSetAttribute(gemm_func(dt, 0), cudaFuncAttributeMaxDynamicSharedMemorySize, kGemmSmemLimit));
+    CK(cudaFuncSetAttribute(DFX_PICK(gemm_persist_kernel, dt), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            kGemmSmemLimit));
+    CK(cudaFuncSetAttribute(DFX_PICK(in_im2col_kernel, dt), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            kIm2colSmemLimit));
+    CK(cudaFuncSetAttribute(se_func(dt, 16), cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   }
   return get_encode();
 }
@@ -680,13 +721,16 @@ int dfx_tmap_act(void* out128, const dfx_view* v, int cb, int tq, int tp, int tn
     return fail(DFX_E_ARG, "tmap_act: box %dx%dx%d stride %d,%d", tq, tp, tn, stride_w, stride_h);
   void* base = static_cast<char*>(v->base) + int64_t(v->coff) * 2;
   if (reinterpret_cast<uintptr_t>(base) % 16) return fail(DFX_E_ARG, "tmap_act: base alignment");
-  cuuint64_t dims[4] = {cuuint64_t(v->c), cuuint64_t(v->w), cuuint64_t(v->h), cuuint64_t(v->n)};
-  cuuint64_t strides[3] = {cuuint64_t(v->pitch) * 2, cuuint64_t(v->pitch) * 2 * v->w,
-                           cuuint64_t(v->pitch) * 2 * v->w * v->h};
-  cuuint32_t box[4] = {cuuint32_t(cb), cuuint32_t(tq * stride_w), cuuint32_t(tp * stride_h),
-                       cuuint32_t(tn)};
-  cuuint32_t estr[4] = {1, cuuint32_t(stride_w), cuuint32_t(stride_h), 1};
-  CUresult r = g_encode(reinterpret_cast<CUtensorMap*>(out128), tmap_dtype(v->dtype), 4,
+  // split precision: a 5th dimension selects the plane (hi = 0, lo = 1, pitch/2 elements apart)
+  const bool split = dfx::dtype_split(v->dtype);
+  if (split && v->pitch % 16) return fail(DFX_E_ARG, "tmap_act: split pitch %d", v->pitch);
+  cuuint64_t dims[5] = {cuuint64_t(v->c), cuuint64_t(v->w), cuuint64_t(v->h), cuuint64_t(v->n), 2};
+  cuuint64_t strides[4] = {cuuint64_t(v->pitch) * 2, cuuint64_t(v->pitch) * 2 * v->w,
+                           cuuint64_t(v->pitch) * 2 * v->w * v->h, cuuint64_t(v->pitch)};
+  cuuint32_t box[5] = {cuuint32_t(cb), cuuint32_t(tq * stride_w), cuuint32_t(tp * stride_h),
+                       cuuint32_t(tn), 1};
+  cuuint32_t estr[5] = {1, cuuint32_t(stride_w), cuuint32_t(stride_h), 1, 1};
+  CUresult r = g_encode(reinterpret_cast<CUtensorMap*>(out128), tmap_dtype(v->dtype), split ? 5 : 4,
                         base, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                         swizzle_for(cb), CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);

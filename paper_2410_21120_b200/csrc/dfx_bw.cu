@@ -36,13 +36,13 @@ __global__ void ew_kernel(const __grid_constant__ dfx_ew_params P) {
     const int n = int(pix / hw);
     if (vec_ok_views && c + 8 <= in.c) {
       float v[8];
-      ld8<T>(in.base, view_pixel_index(in, pix, c), v);
+      ldv8<T>(in, view_pixel_index(in, pix, c), v);
       epilogue8<T>(P.epi, v, pix, n, c);
-      st8<T>(out.base, view_pixel_index(out, pix, c), v);
+      stv8<T>(out, view_pixel_index(out, pix, c), v);
     } else {
       for (int i = 0; i < 8 && c + i < in.c; ++i) {
-        const float x = ld1<T>(in.base, view_pixel_index(in, pix, c + i));
-        st1<T>(out.base, view_pixel_index(out, pix, c + i), epilogue<T>(P.epi, x, pix, n, c + i));
+        const float x = ldv1<T>(in, view_pixel_index(in, pix, c + i));
+        stv1<T>(out, view_pixel_index(out, pix, c + i), epilogue<T>(P.epi, x, pix, n, c + i));
       }
     }
   }
@@ -76,7 +76,7 @@ __global__ void __launch_bounds__(256) ew_vec_kernel(const __grid_constant__ dfx
       ok[u] = idx < total;
       pix[u] = ok[u] ? idx / cg : 0u;
       c[u] = (ok[u] ? idx - pix[u] * cg : 0u) * 8u;
-      if (ok[u]) ld8<T>(in.base, view_pixel_index(in, pix[u], int(c[u])), v[u]);
+      if (ok[u]) ldv8<T>(in, view_pixel_index(in, pix[u], int(c[u])), v[u]);
     }
 #pragma unroll
     for (int u = 0; u < 2; ++u) {
@@ -91,11 +91,11 @@ __global__ void __launch_bounds__(256) ew_vec_kernel(const __grid_constant__ dfx
         const float4 b0 = *reinterpret_cast<const float4*>(beta + cc), b1 = *reinterpret_cast<const float4*>(beta + cc + 4);
         x[0] += b0.x; x[1] += b0.y; x[2] += b0.z; x[3] += b0.w; x[4] += b1.x; x[5] += b1.y; x[6] += b1.z; x[7] += b1.w;
       }
-      act8_t<ACT1>(x);
+      act8_t<ACT1, kSplitT<T>>(x);
       if (binop != DFX_BIN_NONE) {
         const int n = int(pix[u] / hw);
         float o[8];
-        ld8<T>(e.other.base, binop == DFX_BIN_ADD ? view_pixel_index(e.other, pix[u], cc)
+        ldv8<T>(e.other, binop == DFX_BIN_ADD ? view_pixel_index(e.other, pix[u], cc)
                                                   : int64_t(n) * e.other.pitch + e.other.coff + cc, o);
         if (binop == DFX_BIN_ADD) {
 #pragma unroll
@@ -109,9 +109,9 @@ __global__ void __launch_bounds__(256) ew_vec_kernel(const __grid_constant__ dfx
 #pragma unroll
         for (int i = 0; i < 8; ++i) x[i] = fmaxf(x[i], 0.0f);
       } else if (act2 != DFX_ACT_NONE) {
-        act8(act2, x);
+        act8<kSplitT<T>>(act2, x);
       }
-      st8<T>(out.base, view_pixel_index(out, pix[u], cc), x);
+      stv8<T>(out, view_pixel_index(out, pix[u], cc), x);
     }
   }
 }
@@ -126,6 +126,8 @@ __global__ void __launch_bounds__(256) ew_vec_kernel(const __grid_constant__ dfx
   template __global__ void ew_vec_kernel<T, DFX_ACT_GELU>(const __grid_constant__ dfx_ew_params);
 DFX_EW_INST(__half)
 DFX_EW_INST(__nv_bfloat16)
+DFX_EW_INST(f16x2)
+DFX_EW_INST(bf16x2)
 #undef DFX_EW_INST
 
 // ------------------------------------------------------------------ depthwise conv (tiled)
@@ -183,7 +185,7 @@ __global__ void __launch_bounds__(256) dwconv_tile_kernel(const __grid_constant_
         const int w = w0 + j;
         if (w < 0 || w >= IW) continue;
         float x[8];
-        unpack8<T>(*reinterpret_cast<const uint4*>(row + int64_t(w) * in.pitch), x);
+        ld8<T>(row, int64_t(w) * in.pitch, lo_of<T>(in), x);
 #pragma unroll
         for (int v = 0; v < QV; ++v) {
           const int kj = j - v * S;
@@ -211,11 +213,11 @@ __global__ void __launch_bounds__(256) dwconv_tile_kernel(const __grid_constant_
           const float4 b0 = *reinterpret_cast<const float4*>(be + c), b1 = *reinterpret_cast<const float4*>(be + c + 4);
           x[0] += b0.x; x[1] += b0.y; x[2] += b0.z; x[3] += b0.w; x[4] += b1.x; x[5] += b1.y; x[6] += b1.z; x[7] += b1.w;
         }
-        act8_t<ACT>(x);
+        act8_t<ACT, kSplitT<T>>(x);
       } else {
         epilogue8<T>(P.epi, acc[v], pix, n, c);
       }
-      st8<T>(out.base, view_pixel_index(out, pix, c), acc[v]);
+      stv8<T>(out, view_pixel_index(out, pix, c), acc[v]);
     }
   }
 }
@@ -237,6 +239,14 @@ DFX_DW_INST(__nv_bfloat16, 3, 1)
 DFX_DW_INST(__nv_bfloat16, 3, 2)
 DFX_DW_INST(__nv_bfloat16, 5, 1)
 DFX_DW_INST(__nv_bfloat16, 5, 2)
+DFX_DW_INST(f16x2, 3, 1)
+DFX_DW_INST(f16x2, 3, 2)
+DFX_DW_INST(f16x2, 5, 1)
+DFX_DW_INST(f16x2, 5, 2)
+DFX_DW_INST(bf16x2, 3, 1)
+DFX_DW_INST(bf16x2, 3, 2)
+DFX_DW_INST(bf16x2, 5, 1)
+DFX_DW_INST(bf16x2, 5, 2)
 #undef DFX_DW_INST_A
 #undef DFX_DW_INST
 
@@ -271,7 +281,7 @@ __global__ void dwconv_kernel(const __grid_constant__ dfx_dwconv_params P) {
           const int w = w0 + kj;
           if (w < 0 || w >= in.w) continue;
           float x[8];
-          ld8<T>(in.base, view_index(in, n, h, w, c), x);
+          ldv8<T>(in, view_index(in, n, h, w, c), x);
           const float* wt = P.weight + int64_t(ki * P.kw + kj) * C + c;
           const float4 w_lo = __ldg(reinterpret_cast<const float4*>(wt));
           const float4 w_hi = __ldg(reinterpret_cast<const float4*>(wt + 4));
@@ -282,7 +292,7 @@ __global__ void dwconv_kernel(const __grid_constant__ dfx_dwconv_params P) {
         }
       }
       epilogue8<T>(P.epi, acc, pix, n, c);
-      st8<T>(out.base, view_pixel_index(out, pix, c), acc);
+      stv8<T>(out, view_pixel_index(out, pix, c), acc);
     } else {
       for (int i = 0; i < 8 && c + i < C; ++i) {
         float a = 0.0f;
@@ -293,10 +303,10 @@ __global__ void dwconv_kernel(const __grid_constant__ dfx_dwconv_params P) {
             const int w = w0 + kj;
             if (w < 0 || w >= in.w) continue;
             a = fmaf(P.weight[int64_t(ki * P.kw + kj) * C + c + i],
-                     ld1<T>(in.base, view_index(in, n, h, w, c + i)), a);
+                     ldv1<T>(in, view_index(in, n, h, w, c + i)), a);
           }
         }
-        st1<T>(out.base, view_pixel_index(out, pix, c + i), epilogue<T>(P.epi, a, pix, n, c + i));
+        stv1<T>(out, view_pixel_index(out, pix, c + i), epilogue<T>(P.epi, a, pix, n, c + i));
       }
     }
   }
@@ -337,9 +347,9 @@ __device__ __forceinline__ void pool_body(const dfx_pool_params& P) {
         ++count;
         float x[8];
         if (vec && nl == 8) {
-          ld8<T>(in.base, view_index(in, n, h, w, c), x);
+          ldv8<T>(in, view_index(in, n, h, w, c), x);
         } else {
-          for (int i = 0; i < 8; ++i) x[i] = i < nl ? ld1<T>(in.base, view_index(in, n, h, w, c + i)) : 0.f;
+          for (int i = 0; i < 8; ++i) x[i] = i < nl ? ldv1<T>(in, view_index(in, n, h, w, c + i)) : 0.f;
         }
         if (P.is_max) {
 #pragma unroll
@@ -356,9 +366,9 @@ __device__ __forceinline__ void pool_body(const dfx_pool_params& P) {
       for (int i = 0; i < 8; ++i) acc[i] *= inv;
     }
     if (vec && nl == 8) {
-      st8<T>(out.base, view_pixel_index(out, pix, c), acc);
+      stv8<T>(out, view_pixel_index(out, pix, c), acc);
     } else {
-      for (int i = 0; i < nl; ++i) st1<T>(out.base, view_pixel_index(out, pix, c + i), acc[i]);
+      for (int i = 0; i < nl; ++i) stv1<T>(out, view_pixel_index(out, pix, c + i), acc[i]);
     }
   }
 }
@@ -399,20 +409,20 @@ __global__ void gap_kernel(const __grid_constant__ dfx_gap_params P) {
       int s = ty;
       for (; s + 32 < hw; s += 64) {            // two independent 16-B loads in flight
         float x0[8], x1[8];
-        ld8<T>(in.base, base + int64_t(s) * in.pitch, x0);
-        ld8<T>(in.base, base + int64_t(s + 32) * in.pitch, x1);
+        ldv8<T>(in, base + int64_t(s) * in.pitch, x0);
+        ldv8<T>(in, base + int64_t(s + 32) * in.pitch, x1);
 #pragma unroll
         for (int i = 0; i < 8; ++i) acc[i] += x0[i] + x1[i];
       }
       for (; s < hw; s += 32) {
         float x[8];
-        ld8<T>(in.base, base + int64_t(s) * in.pitch, x);
+        ldv8<T>(in, base + int64_t(s) * in.pitch, x);
 #pragma unroll
         for (int i = 0; i < 8; ++i) acc[i] += x[i];
       }
     } else {
       for (int s = ty; s < hw; s += 32)
-        for (int i = 0; i < nl; ++i) acc[i] += ld1<T>(in.base, base + int64_t(s) * in.pitch + i);
+        for (int i = 0; i < nl; ++i) acc[i] += ldv1<T>(in, base + int64_t(s) * in.pitch + i);
     }
   }
 #pragma unroll
@@ -424,7 +434,7 @@ __global__ void gap_kernel(const __grid_constant__ dfx_gap_params P) {
       float sum = 0.f;
       for (int r = 0; r < 32; ++r) sum += part[r][threadIdx.x];
       const dfx_view& out = P.out;
-      st1<T>(out.base, int64_t(n) * out.pitch + out.coff + cc, sum * (1.0f / float(hw)));
+      stv1<T>(out, int64_t(n) * out.pitch + out.coff + cc, sum * (1.0f / float(hw)));
     }
   }
 }
@@ -437,7 +447,7 @@ __global__ void in_kernel(const __grid_constant__ dfx_in_params P) {
   griddep_launch();
   const dfx_view& o = P.out;
   const int hw = o.h * o.w;
-  const int cgp = o.pitch / 8;                 // channel groups incl. padding
+  const int cgp = (kSplitT<T> ? o.pitch / 2 : o.pitch) / 8;   // channel groups incl. padding (one plane)
   const int64_t total = int64_t(o.n) * hw * cgp;
   if (P.kh > 0) {                              // im2col of the entry conv
     const int C = P.c, H = P.h, W = P.w;
@@ -461,7 +471,7 @@ __global__ void in_kernel(const __grid_constant__ dfx_in_params P) {
             v[i] = __ldg(P.src + (int64_t(n) * C + c) * HW + int64_t(iy) * W + ix);
         }
       }
-      st8<T>(o.base, pix * o.pitch + c0, v);
+      stv8<T>(o, pix * o.pitch + c0, v);
     }
     return;
   }
@@ -474,7 +484,7 @@ __global__ void in_kernel(const __grid_constant__ dfx_in_params P) {
     float v[8];
 #pragma unroll
     for (int i = 0; i < 8; ++i) v[i] = (c + i < o.c) ? __ldg(src + int64_t(c + i) * hw) : 0.0f;
-    st8<T>(o.base, pix * o.pitch + c, v);
+    stv8<T>(o, pix * o.pitch + c, v);
   }
 }
 
@@ -515,7 +525,7 @@ __global__ void __launch_bounds__(256) in_im2col_kernel(const __grid_constant__ 
     off[cc] = cc < kreal ? (c * kh + r) * ww + s : -1;
   }
   __syncthreads();
-  const int groups = o.pitch / 8;
+  const int groups = (kSplitT<T> ? o.pitch / 2 : o.pitch) / 8;   // one plane's channel groups
   T* out = reinterpret_cast<T*>(o.base) + ((int64_t(n) * o.h + y) * o.w + x0) * o.pitch;
   for (int i = threadIdx.x; i < tw * groups; i += blockDim.x) {
     const int px = i / groups, c0 = (i - px * groups) * 8;
@@ -529,7 +539,7 @@ __global__ void __launch_bounds__(256) in_im2col_kernel(const __grid_constant__ 
       // split blocks: [x_hi | x_hi | x_lo], x_lo = x - x_hi exactly in fp32
       v[j] = blk == 2 ? x - Elt<T>::to_f(Elt<T>::from_f(x)) : x;
     }
-    *reinterpret_cast<uint4*>(out + int64_t(px) * o.pitch + c0) = pack8<T>(v);
+    st8<T>(out, int64_t(px) * o.pitch + c0, lo_of<T>(o), v);
   }
 }
 
@@ -547,13 +557,15 @@ __global__ void out_kernel(const __grid_constant__ dfx_out_params P) {
     const int64_t r = idx - int64_t(n) * per;
     const int c = int(r / hw);
     const int s = int(r - int64_t(c) * hw);
-    P.dst[idx] = ld1<T>(v.base, view_pixel_index(v, int64_t(n) * hw + s, c));
+    P.dst[idx] = ldv1<T>(v, view_pixel_index(v, int64_t(n) * hw + s, c));
   }
 }
 
 #define DFX_INSTANTIATE(K, P)                                               \
   template __global__ void K<__nv_bfloat16>(const __grid_constant__ P); \
-  template __global__ void K<__half>(const __grid_constant__ P);
+  template __global__ void K<__half>(const __grid_constant__ P);          \
+  template __global__ void K<f16x2>(const __grid_constant__ P);           \
+  template __global__ void K<bf16x2>(const __grid_constant__ P);
 DFX_INSTANTIATE(ew_kernel, dfx_ew_params)
 DFX_INSTANTIATE(dwconv_kernel, dfx_dwconv_params)
 DFX_INSTANTIATE(pool_kernel, dfx_pool_params)

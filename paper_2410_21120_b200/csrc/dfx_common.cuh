@@ -31,27 +31,40 @@ DFX_DEV float tanh_approx(float x) {
   asm("tanh.approx.f32 %0, %1;" : "=f"(r) : "f"(x));
   return r;
 }
-DFX_DEV float sigmoid_f(float v) { return fmaf(0.5f, tanh_approx(0.5f * v), 0.5f); }
-DFX_DEV float silu_f(float v) {
-  const float h = 0.5f * v;
-  return fmaf(h, tanh_approx(h), h);
+// P (precise): the split-precision storage types (two 16-bit planes, ~22-bit
+// significand) use IEEE-accurate forms instead -- tanh.approx's 2^-11 would
+// otherwise be the largest error left in the network.
+template <bool P = false> DFX_DEV float sigmoid_f(float v) {
+  if constexpr (P) return 1.0f / (1.0f + expf(-v));
+  else return fmaf(0.5f, tanh_approx(0.5f * v), 0.5f);
 }
-DFX_DEV float hsig_f(float v) { return fminf(fmaxf(v + 3.0f, 0.0f), 6.0f) * (1.0f / 6.0f); }
+template <bool P = false> DFX_DEV float silu_f(float v) {
+  if constexpr (P) return v / (1.0f + expf(-v));
+  else {
+    const float h = 0.5f * v;
+    return fmaf(h, tanh_approx(h), h);
+  }
+}
+template <bool P = false> DFX_DEV float hsig_f(float v) {
+  if constexpr (P) return fminf(fmaxf(v + 3.0f, 0.0f), 6.0f) / 6.0f;
+  else return fminf(fmaxf(v + 3.0f, 0.0f), 6.0f) * (1.0f / 6.0f);
+}
+DFX_DEV float gelu_f(float v) { return 0.5f * v * (1.0f + erff(v * 0.70710678118654752f)); }
 
-DFX_DEV float act_apply(int act, float v) {
+template <bool P = false> DFX_DEV float act_apply(int act, float v) {
   switch (act) {
     case DFX_ACT_RELU: return fmaxf(v, 0.0f);
-    case DFX_ACT_HARDSWISH: return v * hsig_f(v);
-    case DFX_ACT_HARDSIGMOID: return hsig_f(v);
-    case DFX_ACT_SILU: return silu_f(v);
-    case DFX_ACT_SIGMOID: return sigmoid_f(v);
-    case DFX_ACT_GELU: return 0.5f * v * (1.0f + erff(v * 0.70710678118654752f));
+    case DFX_ACT_HARDSWISH: return v * hsig_f<P>(v);
+    case DFX_ACT_HARDSIGMOID: return hsig_f<P>(v);
+    case DFX_ACT_SILU: return silu_f<P>(v);
+    case DFX_ACT_SIGMOID: return sigmoid_f<P>(v);
+    case DFX_ACT_GELU: return gelu_f(v);
     default: return v;
   }
 }
 
 // Activation over 8 values with the switch hoisted out of the element loop.
-DFX_DEV void act8(int act, float* v) {
+template <bool P = false> DFX_DEV void act8(int act, float* v) {
   switch (act) {
     case DFX_ACT_RELU:
 #pragma unroll
@@ -59,35 +72,48 @@ DFX_DEV void act8(int act, float* v) {
       break;
     case DFX_ACT_HARDSWISH:
 #pragma unroll
-      for (int i = 0; i < 8; ++i) v[i] = v[i] * hsig_f(v[i]);
+      for (int i = 0; i < 8; ++i) v[i] = v[i] * hsig_f<P>(v[i]);
       break;
     case DFX_ACT_HARDSIGMOID:
 #pragma unroll
-      for (int i = 0; i < 8; ++i) v[i] = hsig_f(v[i]);
+      for (int i = 0; i < 8; ++i) v[i] = hsig_f<P>(v[i]);
       break;
     case DFX_ACT_SILU:
 #pragma unroll
-      for (int i = 0; i < 8; ++i) v[i] = silu_f(v[i]);
+      for (int i = 0; i < 8; ++i) v[i] = silu_f<P>(v[i]);
       break;
     case DFX_ACT_SIGMOID:
 #pragma unroll
-      for (int i = 0; i < 8; ++i) v[i] = sigmoid_f(v[i]);
+      for (int i = 0; i < 8; ++i) v[i] = sigmoid_f<P>(v[i]);
       break;
     case DFX_ACT_GELU:
 #pragma unroll
-      for (int i = 0; i < 8; ++i) v[i] = 0.5f * v[i] * (1.0f + erff(v[i] * 0.70710678118654752f));
+      for (int i = 0; i < 8; ++i) v[i] = gelu_f(v[i]);
       break;
     default:
       break;
   }
 }
 
-// ---------------------------------------------------------------- 16-bit storage types
+// ---------------------------------------------------------------- storage types
 // Activations and GEMM operands are 16-bit: bf16 or IEEE half (saturating stores,
 // so an out-of-range value clamps to +-65504 instead of becoming inf).
+//
+// Split precision (f16x2 / bf16x2, dtypes DFX_F16X2 / DFX_BF16X2): every value is
+// stored as TWO 16-bit planes, x = hi + lo with hi = rn16(x), lo = rn16(x - hi),
+// i.e. a 22-bit (fp16) or 16-bit (bf16) significand.  A view's pitch then spans
+// both planes of a pixel: hi channel c at pix * pitch + coff + c, lo channel c
+// pitch / 2 elements later.  GEMMs multiply three plane products on the tensor
+// core (hi*hi + lo*hi + hi*lo, fp32 accumulation): the precision escape of
+// SURVEY.md §7 hard part 2 that carries the fp32 reference's top-1 decisions.
+// The 2-byte struct makes `T*` arithmetic address the hi plane.
+struct f16x2 { unsigned short bits; };
+struct bf16x2 { unsigned short bits; };
+
 template <typename T> struct Elt;
 template <> struct Elt<__nv_bfloat16> {
-  static constexpr int kDtype = DFX_BF16;
+  static constexpr int kDtype = DFX_BF16;       // MMA operand type
+  static constexpr bool kSplit = false;
   static DFX_DEV float to_f(__nv_bfloat16 v) { return __bfloat162float(v); }
   static DFX_DEV __nv_bfloat16 from_f(float v) { return __float2bfloat16_rn(v); }
   static DFX_DEV uint32_t pack2(float a, float b) {
@@ -100,6 +126,7 @@ template <> struct Elt<__nv_bfloat16> {
 };
 template <> struct Elt<__half> {
   static constexpr int kDtype = DFX_F16;
+  static constexpr bool kSplit = false;
   static DFX_DEV float sat(float v) { return fminf(fmaxf(v, -65504.0f), 65504.0f); }
   static DFX_DEV float to_f(__half v) { return __half2float(v); }
   static DFX_DEV __half from_f(float v) { return __float2half_rn(sat(v)); }
@@ -110,6 +137,18 @@ template <> struct Elt<__half> {
   }
   static DFX_DEV float2 unpack2(uint32_t u) { return __half22float2(*reinterpret_cast<__half2*>(&u)); }
 };
+// split types: the per-plane conversions are the 16-bit type's
+template <> struct Elt<f16x2> : Elt<__half> {
+  static constexpr bool kSplit = true;
+  static DFX_DEV float to_f(f16x2 v) { return __half2float(__ushort_as_half(v.bits)); }
+  static DFX_DEV f16x2 from_f(float v) { return f16x2{__half_as_ushort(Elt<__half>::from_f(v))}; }
+};
+template <> struct Elt<bf16x2> : Elt<__nv_bfloat16> {
+  static constexpr bool kSplit = true;
+  static DFX_DEV float to_f(bf16x2 v) { return __bfloat162float(__ushort_as_bfloat16(v.bits)); }
+  static DFX_DEV bf16x2 from_f(float v) { return bf16x2{__bfloat16_as_ushort(__float2bfloat16_rn(v))}; }
+};
+template <typename T> constexpr bool kSplitT = Elt<T>::kSplit;
 
 template <typename T> DFX_DEV void unpack8(const uint4& u, float* f) {
   float2 t;
@@ -128,18 +167,59 @@ template <typename T> DFX_DEV uint4 pack8(const float* f) {
   return u;
 }
 
-template <typename T> DFX_DEV float ld1(const void* base, int64_t idx) {
-  return Elt<T>::to_f(reinterpret_cast<const T*>(base)[idx]);
+// split form: hi = rn16(f), lo = rn16(f - hi)
+template <typename T> DFX_DEV void pack8_split(const float* f, uint4& hi, uint4& lo) {
+  hi = pack8<T>(f);
+  float h[8], r[8];
+  unpack8<T>(hi, h);
+#pragma unroll
+  for (int i = 0; i < 8; ++i) r[i] = f[i] - h[i];
+  lo = pack8<T>(r);
 }
-template <typename T> DFX_DEV void st1(void* base, int64_t idx, float v) {
-  reinterpret_cast<T*>(base)[idx] = Elt<T>::from_f(v);
+
+// Loads / stores of activations.  `lo` is the element offset of the lo plane
+// (lo_of(view)); ignored for single-plane types.
+template <typename T> DFX_DEV int64_t lo_of(const dfx_view& v) {
+  if constexpr (kSplitT<T>) return int64_t(v.pitch >> 1);
+  else return 0;
 }
-template <typename T> DFX_DEV void ld8(const void* base, int64_t idx, float* f) {
-  unpack8<T>(*reinterpret_cast<const uint4*>(reinterpret_cast<const T*>(base) + idx), f);
+template <typename T> DFX_DEV float ld1(const void* base, int64_t idx, int64_t lo) {
+  const T* p = reinterpret_cast<const T*>(base);
+  if constexpr (kSplitT<T>) return Elt<T>::to_f(p[idx]) + Elt<T>::to_f(p[idx + lo]);
+  else return Elt<T>::to_f(p[idx]);
 }
-template <typename T> DFX_DEV void st8(void* base, int64_t idx, const float* f) {
-  *reinterpret_cast<uint4*>(reinterpret_cast<T*>(base) + idx) = pack8<T>(f);
+template <typename T> DFX_DEV void st1(void* base, int64_t idx, int64_t lo, float v) {
+  T* p = reinterpret_cast<T*>(base);
+  const T h = Elt<T>::from_f(v);
+  p[idx] = h;
+  if constexpr (kSplitT<T>) p[idx + lo] = Elt<T>::from_f(v - Elt<T>::to_f(h));
 }
+template <typename T> DFX_DEV void ld8(const void* base, int64_t idx, int64_t lo, float* f) {
+  const T* p = reinterpret_cast<const T*>(base) + idx;
+  unpack8<T>(*reinterpret_cast<const uint4*>(p), f);
+  if constexpr (kSplitT<T>) {
+    float l[8];
+    unpack8<T>(*reinterpret_cast<const uint4*>(p + lo), l);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) f[i] += l[i];
+  }
+}
+template <typename T> DFX_DEV void st8(void* base, int64_t idx, int64_t lo, const float* f) {
+  T* p = reinterpret_cast<T*>(base) + idx;
+  if constexpr (kSplitT<T>) {
+    uint4 h, l;
+    pack8_split<T>(f, h, l);
+    *reinterpret_cast<uint4*>(p) = h;
+    *reinterpret_cast<uint4*>(p + lo) = l;
+  } else {
+    *reinterpret_cast<uint4*>(p) = pack8<T>(f);
+  }
+}
+// view forms
+template <typename T> DFX_DEV float ldv1(const dfx_view& v, int64_t idx) { return ld1<T>(v.base, idx, lo_of<T>(v)); }
+template <typename T> DFX_DEV void stv1(const dfx_view& v, int64_t idx, float x) { st1<T>(v.base, idx, lo_of<T>(v), x); }
+template <typename T> DFX_DEV void ldv8(const dfx_view& v, int64_t idx, float* f) { ld8<T>(v.base, idx, lo_of<T>(v), f); }
+template <typename T> DFX_DEV void stv8(const dfx_view& v, int64_t idx, const float* f) { st8<T>(v.base, idx, lo_of<T>(v), f); }
 
 DFX_DEV int64_t view_index(const dfx_view& v, int n, int h, int w, int c) {
   return ((int64_t(n) * v.h + h) * v.w + w) * v.pitch + v.coff + c;
@@ -156,13 +236,13 @@ DFX_DEV float epilogue(const dfx_epilogue& e, float x, int64_t pix, int n, int c
   float v = x;
   if (e.alpha) v = v * e.alpha[c];           // generic loads: alpha/beta may be staged in smem
   if (e.beta) v = v + e.beta[c];
-  v = act_apply(e.act1, v);
+  v = act_apply<kSplitT<T>>(e.act1, v);
   if (e.binop == DFX_BIN_ADD) {
-    v += ld1<T>(e.other.base, view_pixel_index(e.other, pix, c));
+    v += ldv1<T>(e.other, view_pixel_index(e.other, pix, c));
   } else if (e.binop == DFX_BIN_SCALE) {
-    v *= ld1<T>(e.other.base, int64_t(n) * e.other.pitch + e.other.coff + c);
+    v *= ldv1<T>(e.other, int64_t(n) * e.other.pitch + e.other.coff + c);
   }
-  return act_apply(e.act2, v);
+  return act_apply<kSplitT<T>>(e.act2, v);
 }
 
 // Vector form over 8 consecutive channels c..c+7 (caller guarantees alignment).
@@ -188,13 +268,13 @@ DFX_DEV void epilogue8(const dfx_epilogue& e, float* v, int64_t pix, int n, int 
     v[0] += b0.x; v[1] += b0.y; v[2] += b0.z; v[3] += b0.w;
     v[4] += b1.x; v[5] += b1.y; v[6] += b1.z; v[7] += b1.w;
   }
-  act8(e.act1, v);
+  act8<kSplitT<T>>(e.act1, v);
   if (e.binop != DFX_BIN_NONE) {
     const int64_t idx = e.binop == DFX_BIN_ADD
                             ? view_pixel_index(e.other, pix, c)
                             : int64_t(n) * e.other.pitch + e.other.coff + c;
     float o[8];
-    ld8<T>(e.other.base, idx, o);
+    ldv8<T>(e.other, idx, o);
     if (e.binop == DFX_BIN_ADD) {
 #pragma unroll
       for (int i = 0; i < 8; ++i) v[i] += o[i];
@@ -203,7 +283,7 @@ DFX_DEV void epilogue8(const dfx_epilogue& e, float* v, int64_t pix, int n, int 
       for (int i = 0; i < 8; ++i) v[i] *= o[i];
     }
   }
-  act8(e.act2, v);
+  act8<kSplitT<T>>(e.act2, v);
 }
 
 // Scalar epilogue + store of `count` (<= 16) consecutive channels starting at c.
@@ -215,7 +295,7 @@ __device__ __noinline__ void epilogue_store_tail(const dfx_epilogue& e, const df
                                                  const float* v, int64_t pix, int n, int c,
                                                  int count) {
   for (int i = 0; i < count; ++i)
-    st1<T>(o.base, view_pixel_index(o, pix, c + i), epilogue<T>(e, v[i], pix, n, c + i));
+    stv1<T>(o, view_pixel_index(o, pix, c + i), epilogue<T>(e, v[i], pix, n, c + i));
 }
 
 // True when 8-channel vector access at channel c is legal for view v.
@@ -295,6 +375,16 @@ DFX_DEV void tma_load_4d(void* dst, const void* tmap, uint64_t* bar, int c0, int
       "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
       " [%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(smem_u32(dst)),
       "l"(tmap), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+      : "memory");
+}
+
+// 5-D box: the split-precision activation map (c, w, h, n, plane)
+DFX_DEV void tma_load_5d(void* dst, const void* tmap, uint64_t* bar, int c0, int c1, int c2,
+                         int c3, int c4) {
+  asm volatile(
+      "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5, %6, %7}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(tmap), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4)
       : "memory");
 }
 
@@ -452,13 +542,15 @@ constexpr int kHeaderBytes = 1024;           // barriers + staged descriptor
 constexpr int kEpiBytes = 2048;              // alpha[256] + beta[256] fp32, staged
 constexpr int kSlotsOffset = kHeaderBytes + kEpiBytes;   // 1024-B aligned
 
-// one pipeline slot: A of 1 (or 2, m2) M tiles of 128 rows x 64 K, then B of bn rows x 64 K
-__host__ __device__ inline int gemm_slot_bytes(int bn_max, int m2 = 0) {
-  return kStageABytes * (1 + m2) + bn_max * 128;
+// one pipeline slot: A of 1 (or 2, m2) M tiles of 128 rows x 64 K, then B of bn rows x 64 K;
+// split precision (`planes` 2): A hi tiles, A lo tiles, B hi, B lo
+__host__ __device__ inline int gemm_slot_bytes(int bn_max, int m2 = 0, int planes = 1) {
+  return (kStageABytes * (1 + m2) + bn_max * 128) * planes;
 }
-__host__ __device__ inline int gemm_smem_bytes(int bn_max, int nslots, int m2 = 0) {
-  return kSlotsOffset + nslots * gemm_slot_bytes(bn_max, m2);
+__host__ __device__ inline int gemm_smem_bytes(int bn_max, int nslots, int m2 = 0, int planes = 1) {
+  return kSlotsOffset + nslots * gemm_slot_bytes(bn_max, m2, planes);
 }
+__host__ __device__ inline bool dtype_split(int dt) { return dt == DFX_F16X2 || dt == DFX_BF16X2; }
 // ---- entry-conv im2col (dfx_bw.cu in_im2col_kernel): output pixels per CTA
 constexpr int kIm2colTile = 256;           // a whole output row (<= 256 px) per CTA
 constexpr int kIm2colMaxK = 2048;          // kh*kw*c of an im2col'ed entry conv

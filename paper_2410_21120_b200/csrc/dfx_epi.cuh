@@ -72,7 +72,7 @@ DFX_DEV void drain_rows(uint32_t taddr, float* stg, int ncols, int64_t pix, int 
         dst[1] = b;
       } else if (views_vec && co + 8 <= cout) {
         epilogue8<T>(e, v, spix[i], simg[i], co);
-        st8<T>(o.base, view_pixel_index(o, spix[i], co), v);
+        stv8<T>(o, view_pixel_index(o, spix[i], co), v);
       } else {
         float tail[8];          // a separate array: taking v's address would spill it on every path
 #pragma unroll
@@ -101,16 +101,16 @@ DFX_DEV void drain_rows(uint32_t taddr, float* stg, int ncols, int64_t pix, int 
 // tables and register shuffles: ncu counted ~184 instructions per 16-column
 // chunk on VGG16's first conv), the epilogue fields are copied to registers
 // once, and only the ragged channel tail takes the generic path.
-template <int ACT>
+template <int ACT, bool P = false>
 DFX_DEV void act8_t(float* v) {
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
     if constexpr (ACT == DFX_ACT_RELU) v[i] = fmaxf(v[i], 0.0f);
-    else if constexpr (ACT == DFX_ACT_HARDSWISH) v[i] = v[i] * hsig_f(v[i]);
-    else if constexpr (ACT == DFX_ACT_HARDSIGMOID) v[i] = hsig_f(v[i]);
-    else if constexpr (ACT == DFX_ACT_SILU) v[i] = silu_f(v[i]);
-    else if constexpr (ACT == DFX_ACT_SIGMOID) v[i] = sigmoid_f(v[i]);
-    else if constexpr (ACT == DFX_ACT_GELU) v[i] = 0.5f * v[i] * (1.0f + erff(v[i] * 0.70710678118654752f));
+    else if constexpr (ACT == DFX_ACT_HARDSWISH) v[i] = v[i] * hsig_f<P>(v[i]);
+    else if constexpr (ACT == DFX_ACT_HARDSIGMOID) v[i] = hsig_f<P>(v[i]);
+    else if constexpr (ACT == DFX_ACT_SILU) v[i] = silu_f<P>(v[i]);
+    else if constexpr (ACT == DFX_ACT_SIGMOID) v[i] = sigmoid_f<P>(v[i]);
+    else if constexpr (ACT == DFX_ACT_GELU) v[i] = gelu_f(v[i]);
   }
 }
 
@@ -123,6 +123,8 @@ DFX_DEV void drain_rows_direct_t(uint32_t taddr, int ncols, int64_t pix, int img
   const int binop = e.binop, act2 = e.act2;
   void* const obase = o.base;
   const int64_t orow = pix * o.pitch + o.coff;                  // view_pixel_index(o, pix, 0)
+  const int64_t olo = lo_of<T>(o), xlo = lo_of<T>(e.other);    // split: lo-plane offsets
+  constexpr bool P = kSplitT<T>;
   const void* const xbase = e.other.base;
   const int64_t xrow = binop == DFX_BIN_ADD ? pix * e.other.pitch + e.other.coff
                                             : int64_t(img) * e.other.pitch + e.other.coff;
@@ -158,18 +160,18 @@ DFX_DEV void drain_rows_direct_t(uint32_t taddr, int ncols, int64_t pix, int img
           v[4 * q] += b4.x; v[4 * q + 1] += b4.y; v[4 * q + 2] += b4.z; v[4 * q + 3] += b4.w;
         }
       }
-      act8_t<ACT1>(v);
-      act8_t<ACT1>(v + 8);
+      act8_t<ACT1, P>(v);
+      act8_t<ACT1, P>(v + 8);
       if (valid) {
         if (res) {                                  // residual add (ResNet / MBConv projections)
           float x[16];
-          ld8<T>(xbase, xrow + co, x);
-          ld8<T>(xbase, xrow + co + 8, x + 8);
+          ld8<T>(xbase, xrow + co, xlo, x);
+          ld8<T>(xbase, xrow + co + 8, xlo, x + 8);
 #pragma unroll
           for (int i = 0; i < 16; ++i) v[i] += x[i];
         }
-        st8<T>(obase, orow + co, v);
-        st8<T>(obase, orow + co + 8, v + 8);
+        st8<T>(obase, orow + co, olo, v);
+        st8<T>(obase, orow + co + 8, olo, v + 8);
       }
     }
     return;
@@ -204,12 +206,12 @@ DFX_DEV void drain_rows_direct_t(uint32_t taddr, int ncols, int64_t pix, int img
           v[4 * q] += bq.x; v[4 * q + 1] += bq.y; v[4 * q + 2] += bq.z; v[4 * q + 3] += bq.w;
         }
       }
-      act8_t<ACT1>(v);
-      act8_t<ACT1>(v + 8);
+      act8_t<ACT1, P>(v);
+      act8_t<ACT1, P>(v + 8);
       if (binop != DFX_BIN_NONE) {
         float x[16];
-        ld8<T>(xbase, xrow + co, x);
-        ld8<T>(xbase, xrow + co + 8, x + 8);
+        ld8<T>(xbase, xrow + co, xlo, x);
+        ld8<T>(xbase, xrow + co + 8, xlo, x + 8);
         if (binop == DFX_BIN_ADD) {
 #pragma unroll
           for (int i = 0; i < 16; ++i) v[i] += x[i];
@@ -222,11 +224,11 @@ DFX_DEV void drain_rows_direct_t(uint32_t taddr, int ncols, int64_t pix, int img
 #pragma unroll
         for (int i = 0; i < 16; ++i) v[i] = fmaxf(v[i], 0.0f);
       } else if (act2 != DFX_ACT_NONE) {
-        act8(act2, v);
-        act8(act2, v + 8);
+        act8<P>(act2, v);
+        act8<P>(act2, v + 8);
       }
-      st8<T>(obase, orow + co, v);
-      st8<T>(obase, orow + co + 8, v + 8);
+      st8<T>(obase, orow + co, olo, v);
+      st8<T>(obase, orow + co + 8, olo, v + 8);
     } else {
       float tail[16];
 #pragma unroll
@@ -310,7 +312,7 @@ DFX_DEV void pre_transform_stage(uint8_t* a_base, int nk, int cb, int kstep0, co
       for (int i = tid; i < cps; i += nthr, row += row_step) {
         const int n = n0 + row / rows_per_img;
         if (n != cur_n) {
-          ld8<T>(D.pre_scale, int64_t(n) * D.pre_pitch + c, g);
+          ld8<T>(D.pre_scale, int64_t(n) * D.pre_pitch + c, 0, g);
           cur_n = n;
         }
         uint4* p = reinterpret_cast<uint4*>(sub + (i << 4));
@@ -412,7 +414,7 @@ DFX_DEV void dw_smem_t(const dfx_gemm_desc& D, const T* xs, int xp, int N, int P
     }
     act8_t<ACT>(acc);
     const int64_t pix = (int64_t(n) * OH + p) * OW + q;
-    st8<T>(o.base, view_pixel_index(o, pix, ca), acc);
+    stv8<T>(o, view_pixel_index(o, pix, ca), acc);
   }
 }
 

@@ -87,7 +87,9 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kSeThreads)
   // 16-B aligned slices are staged in smem unless apply bit 1 says otherwise (large
   // batches: clusters of smem-heavy CTAs then cannot be co-scheduled, while the
   // weights are L2-resident and shared by every image's cluster anyway)
-  const bool staged = (C & 7) == 0 && (Cr & 7) == 0 && !(P.apply & 2);
+  // split precision: FC weights [hi C x Cr][lo C x Cr], read from L2 (not staged)
+  const bool staged = !kSplitT<T> && (C & 7) == 0 && (Cr & 7) == 0 && !(P.apply & 2);
+  const int64_t wlo = kSplitT<T> ? int64_t(C) * Cr : 0;   // lo block offset (elements)
   const bool apply = P.apply & 1;
   const int sb = ((cs * Cr * 2) + 15) & ~15;
   const T* w1 = staged ? reinterpret_cast<const T*>(wsm) : w1g + int64_t(c_lo) * Cr;
@@ -118,7 +120,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kSeThreads)
   asm("mov.u32 %0, %%dynamic_smem_size;" : "=r"(dsm));
   const int wbytes = staged ? 2 * sb : 0;
   T* xt = reinterpret_cast<T*>(wsm + wbytes);
-  const bool cache_x = apply && IPI == 1 && ((in.coff | out_coff_of(P) | c_lo | nch) & 7) == 0 &&
+  const bool cache_x = !kSplitT<T> && apply && IPI == 1 && ((in.coff | out_coff_of(P) | c_lo | nch) & 7) == 0 &&
                        uint32_t(wbytes + hw * nch * 2) <= dsm;
 
   // ---- 1. pool: thread = (channel group g, pixel stripe y); all loads in flight first
@@ -147,6 +149,13 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kSeThreads)
       for (int s = y; s < hw; s += stripes) {
         float x[8];
         unpack8<T>(*reinterpret_cast<const uint4*>(xt + s * nch + g * 8), x);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) acc[i] += x[i];
+      }
+    } else if (kSplitT<T> && nl == 8 && ((in.coff + c) & 7) == 0) {
+      for (int s = y; s < hw; s += stripes) {
+        float x[8];
+        ldv8<T>(in, base + int64_t(s) * in.pitch, x);
 #pragma unroll
         for (int i = 0; i < 8; ++i) acc[i] += x[i];
       }
@@ -179,7 +188,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kSeThreads)
       }
     } else {
       for (int s = y; s < hw; s += stripes)
-        for (int i = 0; i < nl; ++i) acc[i] += ld1<T>(in.base, base + int64_t(s) * in.pitch + i);
+        for (int i = 0; i < nl; ++i) acc[i] += ldv1<T>(in, base + int64_t(s) * in.pitch + i);
     }
   }
 #pragma unroll
@@ -211,7 +220,8 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kSeThreads)
 #pragma unroll
       for (int i = 0; i < IPI; ++i) sa[i] = 0.f;
       for (int k = k0; k < k1; ++k) {
-        const float wv = Elt<T>::to_f(w1[int64_t(k) * Cr + j]);     // one load, IPI images
+        float wv = Elt<T>::to_f(w1[int64_t(k) * Cr + j]);           // one load, IPI images
+        if constexpr (kSplitT<T>) wv += Elt<T>::to_f(w1[int64_t(k) * Cr + j + wlo]);
 #pragma unroll
         for (int i = 0; i < IPI; ++i) sa[i] = fmaf(wv, pooled[i][k], sa[i]);
       }
@@ -242,7 +252,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kSeThreads)
 #pragma unroll
     for (int r = 0; r < CL; ++r) s += v[r];
     float a[8] = {s + (P.b1 ? P.b1[j] : 0.f), 0, 0, 0, 0, 0, 0, 0};
-    act8(P.act1, a);
+    act8<kSplitT<T>>(P.act1, a);
     hidden[i][j] = a[0];
   }
   // every DSMEM read of the peers' partial[] is done: arrive now, wait at exit (the
@@ -262,7 +272,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kSeThreads)
     if ((Cr & 7) == 0) {
       for (int j = 0; j < Cr; j += 8) {
         float wv[8];
-        ld8<T>(row, j, wv);                                  // one load, IPI images
+        ld8<T>(row, j, wlo, wv);                             // one load, IPI images
 #pragma unroll
         for (int i = 0; i < IPI; ++i) {
           const float* h = hidden[i] + j;
@@ -274,7 +284,8 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kSeThreads)
       }
     } else {
       for (int j = 0; j < Cr; ++j) {
-        const float wv = Elt<T>::to_f(row[j]);
+        float wv = Elt<T>::to_f(row[j]);
+        if constexpr (kSplitT<T>) wv += Elt<T>::to_f(row[j + wlo]);
 #pragma unroll
         for (int i = 0; i < IPI; ++i) sa[i] = fmaf(wv, hidden[i][j], sa[i]);
       }
@@ -284,11 +295,11 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kSeThreads)
     for (int i = 0; i < IPI; ++i) {
       if (i >= nimg) break;
       float a[8] = {sa[i] + sb[i] + (P.b2 ? P.b2[c] : 0.f), 0, 0, 0, 0, 0, 0, 0};
-      act8(P.act2, a);
+      act8<kSplitT<T>>(P.act2, a);
       if (apply)
         pooled[i][k] = a[0];                                 // gate of this CTA's channel k
       else
-        st1<T>(out.base, int64_t(n0 + i) * out.pitch + out.coff + c, a[0]);
+        stv1<T>(out, int64_t(n0 + i) * out.pitch + out.coff + c, a[0]);
     }
   }
   if (apply) __syncthreads();
@@ -304,7 +315,17 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kSeThreads)
         unpack8<T>(*reinterpret_cast<const uint4*>(xt + s * nch + g8), x);
 #pragma unroll
         for (int j = 0; j < 8; ++j) x[j] *= gate[g8 + j];
-        st8<T>(out.base, view_pixel_index(out, pb + s, c_lo + g8), x);
+        stv8<T>(out, view_pixel_index(out, pb + s, c_lo + g8), x);
+      }
+    } else if (kSplitT<T> && ((in.coff | out.coff | c_lo | nch) & 7) == 0) {
+      const int G8 = nch / 8, total = hw * G8;
+      for (int i = threadIdx.x; i < total; i += kSeThreads) {
+        const int s = i / G8, g8 = (i - s * G8) * 8;
+        float x[8];
+        ldv8<T>(in, view_pixel_index(in, pb + s, c_lo + g8), x);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) x[j] *= gate[g8 + j];
+        stv8<T>(out, view_pixel_index(out, pb + s, c_lo + g8), x);
       }
     } else if (((in.coff | out.coff | c_lo | nch) & 7) == 0) {
       // 4 independent 16-B loads in flight per thread before any store (the
@@ -330,15 +351,15 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kSeThreads)
             unpack8<T>(raw[u], x);
 #pragma unroll
             for (int j = 0; j < 8; ++j) x[j] *= gate[g8 + j];
-            st8<T>(out.base, view_pixel_index(out, pb + s, c_lo + g8), x);
+            stv8<T>(out, view_pixel_index(out, pb + s, c_lo + g8), x);
           }
         }
       }
     } else {
       for (int i = threadIdx.x; i < hw * nch; i += kSeThreads) {
         const int s = i / nch, k = i - s * nch;
-        st1<T>(out.base, view_pixel_index(out, pb + s, c_lo + k),
-               ld1<T>(in.base, view_pixel_index(in, pb + s, c_lo + k)) * gate[k]);
+        stv1<T>(out, view_pixel_index(out, pb + s, c_lo + k),
+               ldv1<T>(in, view_pixel_index(in, pb + s, c_lo + k)) * gate[k]);
       }
     }
   }
@@ -422,7 +443,7 @@ __global__ void __cluster_dims__(kDwseCL, 1, 1) __launch_bounds__(kSeThreads)
         const int w = w0 + kj;
         if (w < 0 || w >= in.w) continue;
         float x[8];
-        ld8<T>(in.base, view_index(in, n, h, w, c), x);
+        ldv8<T>(in, view_index(in, n, h, w, c), x);
         const float4* wt = reinterpret_cast<const float4*>(P.dw_weight + (ki * kw + kj) * C + c);
         const float4 lo = __ldg(wt), hi = __ldg(wt + 1);
         acc[0] = fmaf(lo.x, x[0], acc[0]); acc[1] = fmaf(lo.y, x[1], acc[1]);
@@ -477,7 +498,7 @@ __global__ void __cluster_dims__(kDwseCL, 1, 1) __launch_bounds__(kSeThreads)
     if ((Cr & 7) == 0) {
       for (int j = 0; j < Cr; j += 8) {
         float wv[8];
-        ld8<T>(row, j, wv);
+        ld8<T>(row, j, 0, wv);
         s0 = fmaf(wv[0], hidden[j], s0); s1 = fmaf(wv[1], hidden[j + 1], s1);
         s0 = fmaf(wv[2], hidden[j + 2], s0); s1 = fmaf(wv[3], hidden[j + 3], s1);
         s0 = fmaf(wv[4], hidden[j + 4], s0); s1 = fmaf(wv[5], hidden[j + 5], s1);
@@ -498,7 +519,7 @@ __global__ void __cluster_dims__(kDwseCL, 1, 1) __launch_bounds__(kSeThreads)
     unpack8<T>(*reinterpret_cast<const uint4*>(tile + p * nch + g * 8), x);
 #pragma unroll
     for (int k = 0; k < 8; ++k) x[k] *= red[g * 8 + k];
-    st8<T>(out.base, view_pixel_index(out, int64_t(n) * HWo + p, c_lo + g * 8), x);
+    stv8<T>(out, view_pixel_index(out, int64_t(n) * HWo + p, c_lo + g * 8), x);
   }
   cluster.sync();        // peers finished reading this CTA's partial[]
 }
@@ -514,6 +535,8 @@ DFX_SE_INST(__nv_bfloat16, 16, 1)
 DFX_SE_INST(__half, 16, 1)
 DFX_SE_INST(__nv_bfloat16, 16, 4)
 DFX_SE_INST(__half, 16, 4)
+DFX_SE_INST(f16x2, 16, 1)
+DFX_SE_INST(bf16x2, 16, 1)
 #undef DFX_SE_INST
 
 }  // namespace dfx

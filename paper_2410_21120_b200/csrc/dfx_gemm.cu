@@ -95,8 +95,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   float* s_beta = s_alpha + 256;
   uint8_t* slots = smem + kSlotsOffset;
   constexpr int m2l = M2;                          // slot / TMEM sizing
-  const int slot_bytes = gemm_slot_bytes(L.bn_max, m2l);
-  const int a_bytes = kStageABytes * (1 + m2l);    // A part of a slot (B follows)
+  constexpr int planes = kSplitT<T> ? 2 : 1;       // split precision: hi + lo operand tiles
+  const int slot_bytes = gemm_slot_bytes(L.bn_max, m2l, planes);
+  const int a_lo_off = kStageABytes * (1 + m2l);   // lo A tiles follow the hi ones
+  const int a_bytes = a_lo_off * planes;           // A part of a slot (B follows)
+  const int b_lo_off = L.bn_max * 128;             // lo B tile follows the hi one
   const int nslots = L.nslots;
   if (threadIdx.x == 0) DFX_TL(0);                 // CTA start
 #ifdef DFX_TIMELINE
@@ -202,6 +205,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       pb[h] = p0h[h] * D.stride_h - D.pad_h;
     }
     const uint32_t box_a_bytes = uint32_t(cb) * 2u * tq * tp * tn * nhalf;
+    const uint32_t tx_per_k = (box_a_bytes + uint32_t(sub_b)) * planes;
     const void* tma = gd->tmap_a;
     const void* tmb = gd->tmap_b;
     // Weights are static: the first nslots stages' B tiles are requested before
@@ -212,9 +216,12 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       uint8_t* b_dst = slots + it * slot_bytes + a_bytes;
       const int k0 = st * kpack;
       const int nk = min(kpack, ksteps - k0);
-      mbar_arrive_expect_tx(&hdr->full[it], nk * (box_a_bytes + uint32_t(sub_b)));
-      for (int j = 0; j < nk; ++j)
+      mbar_arrive_expect_tx(&hdr->full[it], nk * tx_per_k);
+      for (int j = 0; j < nk; ++j) {
         tma_load_2d(b_dst + j * sub_b, tmb, &hdr->full[it], (k0 + j) * cb, co_base);
+        if constexpr (planes == 2)       // W_lo rows follow the cout W_hi rows
+          tma_load_2d(b_dst + b_lo_off + j * sub_b, tmb, &hdr->full[it], (k0 + j) * cb, cout + co_base);
+      }
       if (it < 8) DFX_TL(30 + it);                 // B prefetch of stage `it` issued (30..37)
     }
     DFX_TL(1);                                     // weight prefetch issued
@@ -237,9 +244,17 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       for (int j = 0; j < nk; ++j) {
 #pragma unroll
         for (int h = 0; h < 1 + M2; ++h)
-          if (h < nhalf)
-            tma_load_4d(a_dst + h * kStageABytes + j * sub_a, tma, &hdr->full[it], cblk * cb, qb[h] + sc,
-                        pb[h] + rc, n0h[h]);
+          if (h < nhalf) {
+            if constexpr (planes == 2) {
+              tma_load_5d(a_dst + h * kStageABytes + j * sub_a, tma, &hdr->full[it], cblk * cb, qb[h] + sc,
+                          pb[h] + rc, n0h[h], 0);
+              tma_load_5d(a_dst + a_lo_off + h * kStageABytes + j * sub_a, tma, &hdr->full[it], cblk * cb,
+                          qb[h] + sc, pb[h] + rc, n0h[h], 1);
+            } else {
+              tma_load_4d(a_dst + h * kStageABytes + j * sub_a, tma, &hdr->full[it], cblk * cb, qb[h] + sc,
+                          pb[h] + rc, n0h[h]);
+            }
+          }
         if (++cblk == cblocks) {
           cblk = 0;
           if (++sc == S) {
@@ -257,14 +272,24 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       uint8_t* a_dst = slots + slot * slot_bytes;
       uint8_t* b_dst = a_dst + a_bytes;
       const int nk = min(kpack, ksteps - k0);
-      mbar_arrive_expect_tx(&hdr->full[slot], nk * (box_a_bytes + uint32_t(sub_b)));
+      mbar_arrive_expect_tx(&hdr->full[slot], nk * tx_per_k);
       for (int j = 0; j < nk; ++j) {
 #pragma unroll
         for (int h = 0; h < 1 + M2; ++h)
-          if (h < nhalf)
-            tma_load_4d(a_dst + h * kStageABytes + j * sub_a, tma, &hdr->full[slot], cblk * cb, qb[h] + sc,
-                        pb[h] + rc, n0h[h]);
+          if (h < nhalf) {
+            if constexpr (planes == 2) {
+              tma_load_5d(a_dst + h * kStageABytes + j * sub_a, tma, &hdr->full[slot], cblk * cb, qb[h] + sc,
+                          pb[h] + rc, n0h[h], 0);
+              tma_load_5d(a_dst + a_lo_off + h * kStageABytes + j * sub_a, tma, &hdr->full[slot], cblk * cb,
+                          qb[h] + sc, pb[h] + rc, n0h[h], 1);
+            } else {
+              tma_load_4d(a_dst + h * kStageABytes + j * sub_a, tma, &hdr->full[slot], cblk * cb, qb[h] + sc,
+                          pb[h] + rc, n0h[h]);
+            }
+          }
         tma_load_2d(b_dst + j * sub_b, tmb, &hdr->full[slot], (k0 + j) * cb, co_base);
+        if constexpr (planes == 2)
+          tma_load_2d(b_dst + b_lo_off + j * sub_b, tmb, &hdr->full[slot], (k0 + j) * cb, cout + co_base);
         if (++cblk == cblocks) {
           cblk = 0;
           if (++sc == S) {
@@ -307,6 +332,13 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             const uint64_t ad = umma_smem_desc(a_base + h * kStageABytes + j * sub_a + kk * 32, row_bytes);
 #ifndef DFX_EXP_NOMMA
             umma_f16(tmem_base + uint32_t(h * bn), ad, bd, idesc, accumulate);
+            if constexpr (planes == 2) {       // + lo(A) hi(B) + hi(A) lo(B)
+              const uint64_t adl =
+                  umma_smem_desc(a_base + a_lo_off + h * kStageABytes + j * sub_a + kk * 32, row_bytes);
+              const uint64_t bdl = umma_smem_desc(b_base + b_lo_off + j * sub_b + kk * 32, row_bytes);
+              umma_f16(tmem_base + uint32_t(h * bn), adl, bd, idesc, 1u);
+              umma_f16(tmem_base + uint32_t(h * bn), ad, bdl, idesc, 1u);
+            }
 #else
             (void)ad; (void)bd; (void)idesc;
 #endif
@@ -335,7 +367,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         if (ga) s_alpha[i] = c < cout ? ga[c] : 0.f;
         if (gb) s_beta[i] = c < cout ? gb[c] : 0.f;
       }
-      if (D.dw_k > 0) {
+      if (!kSplitT<T> && D.dw_k > 0) {
         // depthwise epilogue: this CTA's taps [k*k][bn] and BN vectors, after the ring
         float* s_dw = reinterpret_cast<float*>(slots + nslots * slot_bytes);
         const int kk = D.dw_k * D.dw_k;
@@ -350,7 +382,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         }
       }
     }
-    if (D.pre_mode) {
+    if constexpr (!kSplitT<T>) if (D.pre_mode) {
       // ================= A prologue transform: rewrite each landed A stage in smem
       griddep_wait();                                  // the gate vector is a predecessor's output
       int it = 0;
@@ -439,7 +471,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       const int64_t pix = (int64_t(on) * P + op) * Q + oq;
       if (views_vec && co + 8 <= cout) {
         epilogue8<T>(e, v, pix, on, co);
-        st8<T>(o.base, view_pixel_index(o, pix, co), v);
+        stv8<T>(o, view_pixel_index(o, pix, co), v);
       } else {
         float tail[8];
 #pragma unroll
@@ -454,7 +486,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     return;
   }
 
-  if (D.dw_k > 0) {
+  if constexpr (!kSplitT<T>) if (D.dw_k > 0) {
     // ---- depthwise epilogue: this CTA covers every M tile (host-checked), so the
     // drain parks its channels of the whole output map in the (now free) operand
     // slots -- the same epilogue and 16-bit rounding as a global store, through a
@@ -498,7 +530,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     const bool valid = row < tn * tp * tq && on < N && op < P && oq < Q;
     const int64_t pix = (int64_t(on) * P + op) * Q + oq;
     float* wsp = splits > 1 ? ws + split * plane : nullptr;
-    if (!(L.flags & 4))
+    if (kSplitT<T> || !(L.flags & 4))
       drain_rows_direct<T>(lane_addr + uint32_t(h * bn), ncols, pix, on, valid, co_base, cout, e, o,
                            views_vec, wsp, ldw, 16 * (warp >> 2), 16 * int(blockDim.x >> 7));
     else
@@ -537,7 +569,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         float v[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
         if (views_vec && co + 8 <= cout) {
           epilogue8<T>(e, v, rpix, an, co);
-          st8<T>(o.base, view_pixel_index(o, rpix, co), v);
+          stv8<T>(o, view_pixel_index(o, rpix, co), v);
         } else {
           epilogue_store_tail<T>(e, o, v, rpix, an, co, min(8, cout - co));
         }
@@ -586,7 +618,7 @@ __global__ void splitk_kernel(const __grid_constant__ dfx_splitk_params P) {
                      (P.epi.binop == DFX_BIN_NONE || vec8_ok(P.epi.other, c));
     if (vec) {
       epilogue8<T>(P.epi, v, pix, n, c);
-      st8<T>(P.out.base, view_pixel_index(P.out, pix, c), v);
+      stv8<T>(P.out, view_pixel_index(P.out, pix, c), v);
     } else {
       epilogue_store_tail<T>(P.epi, P.out, v, pix, n, c, min(8, P.cout - c));
     }
@@ -599,5 +631,9 @@ template __global__ void gemm_kernel<__nv_bfloat16, 1>(const __grid_constant__ d
 template __global__ void gemm_kernel<__half, 1>(const __grid_constant__ dfx_gemm_launch);
 template __global__ void splitk_kernel<__nv_bfloat16>(const __grid_constant__ dfx_splitk_params);
 template __global__ void splitk_kernel<__half>(const __grid_constant__ dfx_splitk_params);
+template __global__ void gemm_kernel<f16x2, 0>(const __grid_constant__ dfx_gemm_launch);
+template __global__ void gemm_kernel<bf16x2, 0>(const __grid_constant__ dfx_gemm_launch);
+template __global__ void splitk_kernel<f16x2>(const __grid_constant__ dfx_splitk_params);
+template __global__ void splitk_kernel<bf16x2>(const __grid_constant__ dfx_splitk_params);
 
 }  // namespace dfx

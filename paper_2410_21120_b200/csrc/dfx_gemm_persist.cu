@@ -50,7 +50,9 @@ __global__ void __launch_bounds__(kPersistThreads, 1)
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   PersistHeader* hdr = reinterpret_cast<PersistHeader*>(smem);
   uint8_t* slots = smem + kSlotsOffset;
-  const int slot_bytes = gemm_slot_bytes(L.bn_max, 0);
+  constexpr int planes = kSplitT<T> ? 2 : 1;       // split precision: hi + lo operand tiles
+  const int slot_bytes = gemm_slot_bytes(L.bn_max, 0, planes);
+  const int a_lo_off = kStageABytes, b_off = kStageABytes * planes, b_lo_off = L.bn_max * 128;
   const int nslots = L.nslots;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const dfx_gemm_desc* gd = &L.desc0;
@@ -65,7 +67,7 @@ __global__ void __launch_bounds__(kPersistThreads, 1)
   const int groups = (int(blockDim.x) - 64) >> 7;
   const int nacc = max(2, min(kMaxAcc, (groups > 1 ? 512 : 256) / L.bn_max));
   // pre_mode (A prologue transform): group 1 transforms A stages, group 0 drains
-  const bool pre = L.desc0.pre_mode != 0;
+  const bool pre = !kSplitT<T> && L.desc0.pre_mode != 0;
   const bool alt = groups > 1 && nacc >= 4 && !pre;
   const uint32_t tmem_cols = tmem_cols_for(nacc * L.bn_max);
   if (threadIdx.x == 0) {
@@ -102,6 +104,7 @@ __global__ void __launch_bounds__(kPersistThreads, 1)
       // ================= TMA producer: one slot ring across all tiles of this CTA
       const int cblocks = D.cblocks, S = D.s;
       const uint32_t box_a_bytes = uint32_t(cb) * 2u * tq * tp * tn;
+      const int cout = D.cout;
       const void* tma = gd->tmap_a;
       const void* tmb = gd->tmap_b;
       // slot / phase and the k-step cursor (channel block, s, r) advance
@@ -119,17 +122,26 @@ __global__ void __launch_bounds__(kPersistThreads, 1)
         for (int st = 0, k0 = 0; st < stages; ++st, k0 += kpack) {
           if (filled >= nslots) mbar_wait(&hdr->empty[slot], par ^ 1);
           uint8_t* a_dst = slots + slot * slot_bytes;
-          uint8_t* b_dst = a_dst + kStageABytes;
+          uint8_t* b_dst = a_dst + b_off;
           const int nk = min(kpack, ksteps - k0);
-          mbar_arrive_expect_tx(&hdr->full[slot], nk * (box_a_bytes + uint32_t(sub_b)));
-          for (int j = 0; j < nk; ++j)                  // weights: static, before the dependency
+          mbar_arrive_expect_tx(&hdr->full[slot], nk * (box_a_bytes + uint32_t(sub_b)) * planes);
+          for (int j = 0; j < nk; ++j) {                // weights: static, before the dependency
             tma_load_2d(b_dst + j * sub_b, tmb, &hdr->full[slot], (k0 + j) * cb, co_base);
+            if constexpr (planes == 2)
+              tma_load_2d(b_dst + b_lo_off + j * sub_b, tmb, &hdr->full[slot], (k0 + j) * cb, cout + co_base);
+          }
           if (!waited) {
             griddep_wait();
             waited = true;
           }
           for (int j = 0; j < nk; ++j) {
-            tma_load_4d(a_dst + j * sub_a, tma, &hdr->full[slot], cblk * cb, qbase + sc, pbase + rc, n0);
+            if constexpr (planes == 2) {
+              tma_load_5d(a_dst + j * sub_a, tma, &hdr->full[slot], cblk * cb, qbase + sc, pbase + rc, n0, 0);
+              tma_load_5d(a_dst + a_lo_off + j * sub_a, tma, &hdr->full[slot], cblk * cb, qbase + sc, pbase + rc,
+                          n0, 1);
+            } else {
+              tma_load_4d(a_dst + j * sub_a, tma, &hdr->full[slot], cblk * cb, qbase + sc, pbase + rc, n0);
+            }
             if (++cblk == cblocks) {
               cblk = 0;
               if (++sc == S) {
@@ -164,12 +176,17 @@ __global__ void __launch_bounds__(kPersistThreads, 1)
           mbar_wait(&gate[slot], par);
           tc_fence_after();
           const uint32_t a_base = smem_u32(slots + slot * slot_bytes);
-          const uint32_t b_base = a_base + kStageABytes;
+          const uint32_t b_base = a_base + b_off;
           const int nk = min(kpack, ksteps - st * kpack);
           for (int j = 0; j < nk; ++j)
             for (int kk = 0; kk < kk_n; ++kk) {
-              umma_f16(acc, umma_smem_desc(a_base + j * sub_a + kk * 32, row_bytes),
-                       umma_smem_desc(b_base + j * sub_b + kk * 32, row_bytes), idesc, accumulate);
+              const uint64_t ad = umma_smem_desc(a_base + j * sub_a + kk * 32, row_bytes);
+              const uint64_t bd = umma_smem_desc(b_base + j * sub_b + kk * 32, row_bytes);
+              umma_f16(acc, ad, bd, idesc, accumulate);
+              if constexpr (planes == 2) {         // + lo(A) hi(B) + hi(A) lo(B)
+                umma_f16(acc, umma_smem_desc(a_base + a_lo_off + j * sub_a + kk * 32, row_bytes), bd, idesc, 1u);
+                umma_f16(acc, ad, umma_smem_desc(b_base + b_lo_off + j * sub_b + kk * 32, row_bytes), idesc, 1u);
+              }
               accumulate = 1;
             }
           umma_commit(&hdr->empty[slot]);
@@ -201,6 +218,7 @@ __global__ void __launch_bounds__(kPersistThreads, 1)
     const int c_first = (alt || pre) ? 0 : 16 * group, c_step = (alt || pre) ? 16 : 16 * groups;
     if (pre && group == 1) {
       // ================= A prologue transform over every stage of every tile of this CTA
+      if constexpr (!kSplitT<T>) {
       const int ti = threadIdx.x - 64 - 128;
       int it = 0;
       for (int tile = blockIdx.x; tile < total; tile += grid) {
@@ -216,6 +234,7 @@ __global__ void __launch_bounds__(kPersistThreads, 1)
           named_bar_sync(1, 128);
           if (ti == 0) mbar_arrive(&hdr->ready[slot]);
         }
+      }
       }
     } else {
     // tile coordinates advance as a mixed-radix counter (q, p, n, N tile) by `grid`
@@ -253,7 +272,7 @@ __global__ void __launch_bounds__(kPersistThreads, 1)
       if (tile + grid >= total) griddep_launch();     // this CTA's last tile
       mbar_wait(&hdr->acc_full[bcur], phcur);
       tc_fence_after();
-      if (!(L.flags & 4))
+      if (kSplitT<T> || !(L.flags & 4))
         drain_rows_direct<T>(lane_addr + uint32_t(bcur * bn), ncols, pix, on, valid, co_base, cout, e, o,
                              views_vec, nullptr, 0, c_first, c_step);
       else
@@ -271,5 +290,7 @@ __global__ void __launch_bounds__(kPersistThreads, 1)
 
 template __global__ void gemm_persist_kernel<__nv_bfloat16>(const __grid_constant__ dfx_gemm_launch);
 template __global__ void gemm_persist_kernel<__half>(const __grid_constant__ dfx_gemm_launch);
+template __global__ void gemm_persist_kernel<f16x2>(const __grid_constant__ dfx_gemm_launch);
+template __global__ void gemm_persist_kernel<bf16x2>(const __grid_constant__ dfx_gemm_launch);
 
 }  // namespace dfx

@@ -47,7 +47,7 @@ __global__ void __launch_bounds__(256) ln_kernel(const __grid_constant__ dfx_ln_
     for (int k = 0; k < kLnMaxVec; ++k) {
       const int v = lane + 32 * k;
       if (v < nv) {
-        ld8<T>(in.base, ib + v * 8, x[k]);
+        ldv8<T>(in, ib + v * 8, x[k]);
 #pragma unroll
         for (int i = 0; i < 8; ++i) s += x[k][i];
       }
@@ -55,7 +55,7 @@ __global__ void __launch_bounds__(256) ln_kernel(const __grid_constant__ dfx_ln_
     if (!P.norm) {
 #pragma unroll
       for (int k = 0; k < kLnMaxVec; ++k)
-        if (lane + 32 * k < nv) st8<T>(out.base, ob + (lane + 32 * k) * 8, x[k]);
+        if (lane + 32 * k < nv) stv8<T>(out, ob + (lane + 32 * k) * 8, x[k]);
       return;
     }
 #pragma unroll
@@ -87,28 +87,28 @@ __global__ void __launch_bounds__(256) ln_kernel(const __grid_constant__ dfx_ln_
         float y[8];
 #pragma unroll
         for (int i = 0; i < 8; ++i) y[i] = fmaf((x[k][i] - mean) * rstd, g[i], b[i]);
-        st8<T>(out.base, ob + v * 8, y);
+        stv8<T>(out, ob + v * 8, y);
       }
     }
     return;
   }
   // generic path (ragged C): two passes over global memory
   float s = 0.f;
-  for (int c = lane; c < C; c += 32) s += ld1<T>(in.base, ib + c);
+  for (int c = lane; c < C; c += 32) s += ldv1<T>(in, ib + c);
 #pragma unroll
   for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
   const float mean = s / float(C);
   float q = 0.f;
   for (int c = lane; c < C; c += 32) {
-    const float d = ld1<T>(in.base, ib + c) - mean;
+    const float d = ldv1<T>(in, ib + c) - mean;
     q = fmaf(d, d, q);
   }
 #pragma unroll
   for (int o = 16; o; o >>= 1) q += __shfl_xor_sync(0xffffffffu, q, o);
   const float rstd = rsqrtf(q / float(C) + P.eps);
   for (int c = lane; c < C; c += 32) {
-    const float x = ld1<T>(in.base, ib + c);
-    st1<T>(out.base, ob + c, P.norm ? fmaf((x - mean) * rstd, P.gamma[c], P.beta[c]) : x);
+    const float x = ldv1<T>(in, ib + c);
+    stv1<T>(out, ob + c, P.norm ? fmaf((x - mean) * rstd, P.gamma[c], P.beta[c]) : x);
   }
 }
 
@@ -137,16 +137,16 @@ __global__ void tokens_kernel(const __grid_constant__ dfx_tokens_params P) {
 #pragma unroll
         for (int i = 0; i < 8; ++i) x[i] = P.cls[c + i];
       } else {
-        ld8<T>(in.base, view_pixel_index(in, int64_t(img) * hw + t - 1, c), x);
+        ldv8<T>(in, view_pixel_index(in, int64_t(img) * hw + t - 1, c), x);
       }
 #pragma unroll
       for (int i = 0; i < 8; ++i) x[i] += pos[c + i];
-      st8<T>(out.base, o, x);
+      stv8<T>(out, o, x);
     } else {
       for (int i = 0; i < 8 && c + i < C; ++i) {
         const float x = t == 0 ? P.cls[c + i]
-                               : ld1<T>(in.base, view_pixel_index(in, int64_t(img) * hw + t - 1, c + i));
-        st1<T>(out.base, o + i, x + pos[c + i]);
+                               : ldv1<T>(in, view_pixel_index(in, int64_t(img) * hw + t - 1, c + i));
+        stv1<T>(out, o + i, x + pos[c + i]);
       }
     }
   }

@@ -32,7 +32,7 @@ import numpy as np
 from . import runtime as rt
 from .graph_ir import LiveInterval
 from .lower import (ATTN, COPY, DWCONV, DWSE, EW, GAP, GEMM, LN, POOL, SE, TOKENS, MemberProgram,
-                    gemm_tiling, lower_member)
+                    gemm_tiling, lower_member, planes_of)
 from .planner import first_fit
 
 ALIGN = 256
@@ -94,12 +94,12 @@ GEMM_DRAIN_STAGED = os.environ.get("DFX_GEMM_DRAIN", "direct") == "staged"   # A
 E2E_GATHER = os.environ.get("DFX_E2E_GATHER", "1") != "0"
 
 
-def gemm_slots(bn: int, tiles: int, sm_count: int = 148, m2: int = 0) -> int:
+def gemm_slots(bn: int, tiles: int, sm_count: int = 148, m2: int = 0, planes: int = 1) -> int:
     """Pipeline depth of a GEMM launch: as deep as shared memory allows (<= 8)
     when the grid fits in one wave -- every extra slot is another weight tile
     requested before griddepcontrol.wait -- else 4, leaving room for two CTAs
     per SM on narrow tiles.  m2 slots hold two A tiles (dfx_common.cuh gemm_slot_bytes)."""
-    slot = 128 * 64 * 2 * (1 + m2) + bn * 128
+    slot = (128 * 64 * 2 * (1 + m2) + bn * 128) * planes
     fit = (GEMM_SMEM_LIMIT - GEMM_SMEM_FIXED) // slot
     return max(2, min(8 if tiles <= sm_count else 4, fit))
 
@@ -464,16 +464,18 @@ def plan_member(prog: MemberProgram, n: int, sm_count: int = 148, cluster_ok: bo
     ws = 0
     tilings = {}
     skip: set[int] = set()
-    dw_pairs = gemm_dw_pairs(prog) if GEMM_DW else {}
+    planes = planes_of(prog.precision)
+    dw_pairs = gemm_dw_pairs(prog) if GEMM_DW and planes == 1 else {}
     for L in prog.launches:
         if L.kind != GEMM:
             continue
         out = prog.values[L.dst]
         if L.geom.get("tokens"):        # token rows of all images are one contiguous M
             t = gemm_tiling(L.geom, 1, 1, n * out.w, sm_count, cluster_ok=cluster_ok and n <= 2,
-                            max_splits=max_splits)
+                            max_splits=max_splits, planes=planes)
         else:
-            t = gemm_tiling(L.geom, n, out.h, out.w, sm_count, cluster_ok=cluster_ok, max_splits=max_splits)
+            t = gemm_tiling(L.geom, n, out.h, out.w, sm_count, cluster_ok=cluster_ok, max_splits=max_splits,
+                            planes=planes)
         if L.index in dw_pairs and n * out.h * out.w <= 256 and \
                 (GEMM_DW_MODE == "all" or t["splits"] == 1):
             # one CTA (m2: two M tiles) holds the whole output map of its channels
@@ -579,7 +581,7 @@ class ExecInstance:
         v = prog.values[name]
         b = prog.buffers[v.buf]
         base = self.act + self.seg_off[m] + self.plans[m].offsets[v.buf]
-        return rt.View(base, n, v.h, v.w, v.c, b.pitch, v.coff, self.dtype)
+        return rt.View(base, n, v.h, v.w, v.c, b.phys_pitch, v.coff, self.dtype)
 
     def _epi(self, m, prog, L, n) -> rt.Epilogue:
         e = rt.Epilogue()
@@ -661,9 +663,10 @@ class ExecInstance:
     def _algo(prog: MemberProgram, L, n: int, op: int) -> dict:
         """Algorithmic FLOPs and HBM bytes of one launch (16-bit activations,
         unpadded weights): what a perfect kernel must move / compute."""
+        es = 2 * planes_of(prog.precision)      # bytes per stored element
         def vbytes(name):
             v = prog.values[name]
-            return n * v.h * v.w * v.c * 2
+            return n * v.h * v.w * v.c * es
         info = dict(member=prog.model_id, kind=L.kind, flops=0, bytes=0)
         out_b = vbytes(L.dst) if L.kind != COPY else vbytes(L.src)
         in_b = vbytes(L.src)
@@ -674,7 +677,7 @@ class ExecInstance:
             g = L.geom
             out = prog.values[L.dst]
             macs = n * out.h * out.w * g["cout"] * g["cin"] * g["kh"] * g["kw"]
-            wbytes = g["cout"] * g["cin"] * g["kh"] * g["kw"] * 2
+            wbytes = g["cout"] * g["cin"] * g["kh"] * g["kw"] * es
             if op == rt.OP_SPLITK:
                 info.update(kind="splitk", bytes=out_b + other_b)
             else:
@@ -747,8 +750,9 @@ class ExecInstance:
                 src, out = _fold_rows(src), _fold_rows(out)
             d = rt.GemmDesc()
             d.tmap_a = rt.tmap_act(src, geo["cb"], t["tq"], t["tp"], t["tn"], geo["sw"], geo["sh"])
-            d.tmap_b = rt.tmap_weights(arena.addr(m, L.blobs["weight"]), geo["cout"], geo["k"],
-                                       geo["cb"], t["bn"], self.dtype)
+            # split precision: [W_hi; W_lo] rows, the kernel loads lo rows at cout + co
+            d.tmap_b = rt.tmap_weights(arena.addr(m, L.blobs["weight"]), geo["cout"] * planes_of(prog.precision),
+                                       geo["k"], geo["cb"], t["bn"], self.dtype)
             d.n, d.p, d.q = out.n, out.h, out.w
             d.tn, d.tp, d.tq = t["tn"], t["tp"], t["tq"]
             d.mt_n, d.mt_p, d.mt_q, d.nt = t["mt_n"], t["mt_p"], t["mt_q"], t["nt"]
@@ -791,14 +795,16 @@ class ExecInstance:
             slot = len(host_descs)
             host_descs.append(d)
             self.gemm_count += 1
+            planes = planes_of(prog.precision)
+            slot_bytes = (128 * 64 * 2 + t["bn"] * 128) * planes     # dfx_common.cuh gemm_slot_bytes
             gl = rt.GemmLaunch(self.descs + slot * C.sizeof(rt.GemmDesc), 1, t["tiles"], t["bn"],
                                self.dtype, gemm_slots(t["bn"], t["tiles"], self.dag.sm_count,
-                                                      t.get("m2", 0)))
+                                                      t.get("m2", 0), planes))
             gl.m2 = t.get("m2", 0)
             if csplit:
                 gl.flags |= 8                # cluster split-K (DSMEM reduction, no splitk node)
                 need = 128 * (t["bn"] + 4) * 4          # the fp32 partial tile parks in the slots
-                gl.nslots = max(gl.nslots, -(-need // (128 * 64 * 2 + t["bn"] * 128)))
+                gl.nslots = max(gl.nslots, -(-need // slot_bytes))
             if GEMM_PERSIST and not gl.m2 and t["splits"] == 1 and \
                     t["tiles"] > PERSIST_MIN_WAVES * self.dag.sm_count:
                 gl.flags |= 2                # persistent kernel for multi-wave layers
@@ -807,9 +813,9 @@ class ExecInstance:
                 if t["bn"] > 64:
                     gl.nslots = max(2, min(8, (GEMM_SMEM_LIMIT - GEMM_SMEM_FIXED
                                                - (8 * 2560 if GEMM_DRAIN_STAGED else 0))
-                                           // (128 * 64 * 2 + t["bn"] * 128)))
+                                           // slot_bytes))
                 else:
-                    gl.nslots = 4
+                    gl.nslots = 4 if planes == 1 else 2
             if GEMM_DRAIN_STAGED:
                 gl.flags |= 4                # smem-transposed epilogue drain (A/B)
             if GEMM_EARLY_PDL:

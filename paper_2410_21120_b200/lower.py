@@ -63,7 +63,33 @@ def bf16_bits_to_f32(b: np.ndarray) -> np.ndarray:
     return (b.astype(np.uint32) << 16).view(np.float32)
 
 
-PRECISIONS = ("fp16", "bf16")
+PRECISIONS = ("fp16", "bf16", "fp16x2", "bf16x2")
+# Split precision (dfx.h DFX_F16X2 / DFX_BF16X2): every activation and GEMM / SE
+# weight stored as two 16-bit planes v = hi + lo; GEMMs accumulate
+# hi*hi + lo*hi + hi*lo.  The accurate mode: ~22 (fp16x2) / 16 (bf16x2)
+# significant bits instead of 11 / 8 (SURVEY.md §7 hard part 2's escape hatch).
+SPLIT_PRECISIONS = ("fp16x2", "bf16x2")
+
+
+def base_precision(precision: str) -> str:
+    """The 16-bit type of one plane: "fp16x2" -> "fp16"."""
+    return precision[:4]
+
+
+def planes_of(precision: str) -> int:
+    return 2 if precision in SPLIT_PRECISIONS else 1
+
+
+def pack_bits(a: np.ndarray, precision: str) -> np.ndarray:
+    """Stored bits of a weight matrix [rows][k]: 16-bit, or for split precision
+    [hi rows; lo rows] with hi = rn16(a), lo = rn16(a - hi)."""
+    if precision not in SPLIT_PRECISIONS:
+        return to_storage_bits(a, precision)
+    b = base_precision(precision)
+    a = np.asarray(a, np.float32)
+    hi = to_storage_bits(a, b)
+    lo = to_storage_bits(a - storage_bits_to_f32(hi, b), b)
+    return np.ascontiguousarray(np.concatenate([hi, lo], axis=0))
 
 
 def to_storage_bits(a: np.ndarray, precision: str) -> np.ndarray:
@@ -92,9 +118,15 @@ class Buffer:
     first: int = 10 ** 9    # launch index of first write
     last: int = -1          # launch index of last read
     is_input: bool = False
+    planes: int = 1         # 2: split precision, hi and lo planes of a pixel side by side
+
+    @property
+    def phys_pitch(self) -> int:
+        """Elements per pixel in memory (both planes for split precision)."""
+        return self.pitch * self.planes
 
     def bytes_for(self, n: int) -> int:
-        return n * self.h * self.w * self.pitch * 2
+        return n * self.h * self.w * self.phys_pitch * 2
 
 
 @dataclass
@@ -416,7 +448,7 @@ class _Lowerer:
 
     # -------------------------------------------------------------- placement
     def new_buffer(self, h, w, c, name):
-        b = Buffer(len(self.buffers), h, w, c, round_up(c, 8), name)
+        b = Buffer(len(self.buffers), h, w, c, round_up(c, 8), name, planes=planes_of(self.precision))
         self.buffers.append(b)
         return b.bid
 
@@ -508,9 +540,9 @@ class _Lowerer:
             if nid in self.absorbed:
                 continue
             self.lower_node(nid)
-        if FUSE_DWSE:
+        if FUSE_DWSE and self.precision not in SPLIT_PRECISIONS:
             self.fuse_dw_se()
-        if FOLD_PRE:
+        if FOLD_PRE and self.precision not in SPLIT_PRECISIONS:
             self.fold_pre_transforms()
         self.place()
         for s, cid, off in self.copies:
@@ -711,8 +743,8 @@ class _Lowerer:
                 wt = self.warr(node, "weight")            # (out, in)
                 # fc1 is stored transposed ([C][Cr]) so each cluster CTA's channel
                 # slice of both FCs is one contiguous block (dfx_fused.cu se_kernel)
-                self.blobs[key] = to_storage_bits(np.ascontiguousarray(wt.T) if role == "1" else wt,
-                                                  self.precision)
+                self.blobs[key] = pack_bits(np.ascontiguousarray(wt.T) if role == "1" else wt,
+                                            self.precision)
                 L.blobs["w" + role] = key
                 if "bias" in node.weight_refs:
                     b = self.warr(node, "bias")
@@ -740,7 +772,7 @@ class _Lowerer:
                 cout = geo["cout"]
                 t = np.zeros((cout, geo["kh"], geo["kw"], cblocks * cb), dtype=np.float32)
                 t[..., :cin] = wt4.transpose(0, 2, 3, 1)
-                packed = to_storage_bits(t.reshape(cout, -1), self.precision)
+                packed = pack_bits(t.reshape(cout, -1), self.precision)
                 geo.update(cb=cb, cblocks=cblocks, ksteps=geo["kh"] * geo["kw"] * cblocks,
                            k=packed.shape[1])
                 self.blobs[L.blobs["weight"]] = packed
@@ -806,7 +838,8 @@ def lower_member(g, w, keep_f32: bool = False, precision: str = "fp16") -> Membe
     low = _Lowerer(g, w)
     low.keep_f32 = keep_f32
     low.precision = precision
-    if low.input_im2col is not None and (STEM_SPLIT == "all" or STEM_SPLIT == precision):
+    if low.input_im2col is not None and (STEM_SPLIT == "all" or STEM_SPLIT == precision) and \
+            precision not in SPLIT_PRECISIONS:
         kh, kw = low.input_im2col[:2]
         low.input_split = round_up(kh * kw * g.input_spec.dims[0], 8)
     prog = low.run()
@@ -887,7 +920,7 @@ SPLITK_CLUSTER_MAX = 8
 
 
 def gemm_tiling(geom: dict, n: int, p: int, q: int, sm_count: int = 148, cluster_ok: bool = False,
-                max_splits: int = 0) -> dict:
+                max_splits: int = 0, planes: int = 1) -> dict:
     tn, tp, tq = choose_m_tile(n, p, q, geom["sh"], geom["sw"])
     mt = (math.ceil(n / tn), math.ceil(p / tp), math.ceil(q / tq))
     bn, nt = choose_bn(geom["cout"])
@@ -917,7 +950,7 @@ def gemm_tiling(geom: dict, n: int, p: int, q: int, sm_count: int = 148, cluster
     # (short-K layers go to the persistent kernel instead, whose overlapped epilogue
     # matters more there than the halved weight traffic: measured on 3x3 64->256 at
     # batch 32, 115 us m2 vs 80 us persistent; VGG's K=4608 layers keep m2)
-    m2 = int(GEMM_M2 and splits == 1 and bn >= 128 and m_tiles >= 2 and stages >= 24
+    m2 = int(GEMM_M2 and planes == 1 and splits == 1 and bn >= 128 and m_tiles >= 2 and stages >= 24
              and not geom.get("pre")
              and math.ceil(m_tiles / 2) * nt >= sm_count and waves2 * 1.6 < waves1)
     tiles = (math.ceil(m_tiles / 2) if m2 else m_tiles) * nt * splits

@@ -23,9 +23,9 @@ LIB_PATH = PKG / "libdfx.so"
  OP_ATTN, OP_DWSE) = range(1, 14)
 ACT = {None: 0, "relu": 1, "hardswish": 2, "hardsigmoid": 3, "silu": 4, "sigmoid": 5, "gelu": 6}
 BIN_NONE, BIN_ADD, BIN_SCALE = 0, 1, 2
-DT_BF16, DT_F16 = 0, 1
-DTYPES = {"bf16": DT_BF16, "fp16": DT_F16}
-ABI_VERSION = 3
+DT_BF16, DT_F16, DT_BF16X2, DT_F16X2 = 0, 1, 2, 3
+DTYPES = {"bf16": DT_BF16, "fp16": DT_F16, "bf16x2": DT_BF16X2, "fp16x2": DT_F16X2}
+ABI_VERSION = 4
 
 i32, i64, u64, vp, u8 = C.c_int32, C.c_int64, C.c_uint64, C.c_void_p, C.c_uint8
 fptr = C.POINTER(C.c_float)

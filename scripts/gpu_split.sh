@@ -1,3 +1,6 @@
 #!/bin/bash
-python -c "import __graft_entry__ as g; g.build()" 2>&1 | grep -i error
-for m in 4 3 2; do echo "== min stages $m"; DFX_SPLIT_MIN_STAGES=$m timeout 300 python scripts/member_times.py --batch 1; done
+# Split-precision bring-up: layer/zoo/corpus tests, then the north-star statistic.
+mkdir -p gpurun_out
+python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1 || { tail -20 gpurun_out/build.log; exit 1; }
+timeout 900 python -m pytest tests/test_gpu_split.py -x -q > gpurun_out/tests_split.txt 2>&1; tail -30 gpurun_out/tests_split.txt
+timeout 1200 python -m pytest tests/test_gpu_north_star.py -q -k split > gpurun_out/tests_ns_split.txt 2>&1; tail -30 gpurun_out/tests_ns_split.txt
