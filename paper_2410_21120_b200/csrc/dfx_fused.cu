@@ -105,8 +105,6 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kSeThreads)
       mbar_arrive_expect_tx(&wbar, 2 * bytes);
       bulk_load(wsm, w1g + int64_t(c_lo) * Cr, bytes, &wbar);
       bulk_load(wsm + sb, w2g + int64_t(c_lo) * Cr, bytes, &wbar);
-    } else {
-      mbar_arrive(&wbar);
     }
   }
   griddep_wait();
@@ -203,7 +201,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kSeThreads)
   __syncthreads();                                    // red[] reused by the next image
   }
   if (threadIdx.x == 0) DFX_TL(2);
-  if (threadIdx.x == 0) mbar_wait(&wbar, 0);                 // weight slices landed (one poller)
+  if (threadIdx.x == 0 && staged && nch * Cr > 0) mbar_wait(&wbar, 0);   // weight slices landed (one poller)
   __syncthreads();
   if (threadIdx.x == 0) DFX_TL(3);
 

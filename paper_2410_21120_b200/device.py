@@ -122,6 +122,50 @@ def arena_layout(programs: list[MemberProgram]):
     return layout, segments, max(at, ALIGN)
 
 
+# id(program) -> (weakref, offsets, bytes, pinned _Block): a member's packed weight
+# segment staged ONCE in pinned host memory, so a swap_subgraph that brings the
+# member in is one allocation + D2D of the untouched members + ONE H2D, with no
+# per-swap pinning or packing on the host
+_segments: dict[int, tuple] = {}
+_segments_lock = threading.Lock()
+
+
+def _release_segment(key):
+    with _segments_lock:
+        hit = _segments.pop(key, None)
+    if hit is not None:
+        hit[3].release()
+
+
+def stage_segment(prog: MemberProgram) -> tuple[dict, int, int]:
+    """(blob offsets, bytes, pinned host address) of a member's packed segment;
+    staged on first use and kept while the program lives."""
+    offs, size, blk = _stage_block(prog)
+    return offs, size, blk.ptr
+
+
+def _stage_block(prog: MemberProgram):
+    key = id(prog)
+    with _segments_lock:
+        hit = _segments.get(key)
+        if hit is not None and hit[0]() is prog:
+            return hit[1], hit[2], hit[3]
+    offs, at = {}, 0
+    for k in sorted(prog.blobs):
+        offs[k] = at
+        at = _align(at + prog.blobs[k].nbytes)
+    size = max(at, ALIGN)
+    blk = _Block(rt.host_alloc(size), "host")
+    buf = np.frombuffer((C.c_uint8 * size).from_address(blk.ptr), dtype=np.uint8)
+    for k, off in offs.items():
+        raw = prog.blobs[k].view(np.uint8).reshape(-1)
+        buf[off:off + raw.size] = raw
+    with _segments_lock:
+        _segments[key] = (weakref.ref(prog), offs, size, blk)
+    weakref.finalize(prog, _release_segment, key).atexit = False
+    return offs, size, blk
+
+
 def fill_arena(buf: np.ndarray, programs: list[MemberProgram], layout) -> None:
     """Copy every blob into its slot of a uint8 arena buffer."""
     for p, offs in zip(programs, layout):
@@ -180,6 +224,15 @@ class WeightArena:
         self.device = device
         self.layout, self.segments, self.total = arena_layout(programs)
         rt.init_device(device)
+        if len(programs) == 1:
+            # one member: its staged pinned segment (stage_segment) IS the arena's
+            # host copy -- no pinning or packing per load
+            offs, size, blk = _stage_block(programs[0])
+            assert size == self.total and offs == self.layout[0]
+            self._host_block = blk.retain()
+            self.host_pinned = True
+            self._init_device_state()
+            return
         host = rt.host_alloc(self.total)
         self._host_block = _Block(host, "host")
         self.host_pinned = True
@@ -248,11 +301,19 @@ class WeightArena:
         return self.upload_ms
 
     def unload(self) -> None:
-        """Free the device copy, keep the pinned host staging (swap-out; the next
-        upload() is again one allocation + one H2D).  Only for an arena no
-        swapped DAG shares."""
+        """Swap-out: free the device copy, keep a pinned host copy (the next upload()
+        is again one allocation + one H2D).  An arena made by a swap has no host
+        staging of its own layout yet: the device bytes are first read back into a
+        fresh pinned buffer (one D2H).  Only for an arena no other DAG shares."""
         if self.shared:
             raise RuntimeError("arena shared with a swapped DAG: unload the DAGs instead")
+        if self._dev_block is not None and getattr(self, "host_stale", False):
+            host = rt.host_alloc(self.total)
+            rt.d2h(host, self.dev, self.total, None)
+            rt.stream_sync(None)
+            if self._host_block is not None:
+                self._host_block.release()
+            self._host_block, self.host_pinned, self.host_stale = _Block(host, "host"), True, False
         for b in self._blocks():
             b.release()
         self._dev_block, self._swap_blocks = None, []
@@ -271,46 +332,58 @@ class WeightArena:
         return self.member_base[member], self.segments[member][1]
 
     def replace_member(self, member: int, prog: MemberProgram, stream=None, upload: bool = True) -> float:
-        """swap_subgraph: pack the incoming member and upload ONLY its segment, into
-        a fresh device block (never into bytes the source DAG may be reading).
-        Returns the wall ms of allocation + H2D; ``last_swap`` has the phases."""
-        offs, at = {}, 0
-        for key in sorted(prog.blobs):
-            offs[key] = at
-            at = _align(at + prog.blobs[key].nbytes)
-        size = max(at, ALIGN)
-        if not upload:                       # a replica receiving the segment by broadcast
-            blk = _arena_block(size, stream)
-            self.last_swap = {"bytes": size, "malloc_ms": None, "memcpy_ms": None, "ms": 0.0}
-            self._swap_blocks.append(blk)
-            self.member_base[member] = blk.ptr
-            self.layout[member] = offs
-            self.segments[member] = (0, size)
-            return 0.0
-        host = rt.host_alloc(size)
-        try:
-            buf = np.frombuffer((C.c_uint8 * size).from_address(host), dtype=np.uint8)
-            for key, off in offs.items():
-                raw = prog.blobs[key].view(np.uint8).reshape(-1)
-                buf[off:off + raw.size] = raw
-            t0 = time.perf_counter()
-            blk = _arena_block(size, stream)
-            t1 = time.perf_counter()
-            e0, e1 = rt.Event(), rt.Event()
-            e0.record(stream)
-            rt.h2d(blk.ptr, host, size, stream)
-            e1.record(stream)
-            rt.stream_sync(stream)
-            ms = (time.perf_counter() - t0) * 1e3
-            self.last_swap = {"bytes": size, "malloc_ms": (t1 - t0) * 1e3, "memcpy_ms": e0.elapsed_ms(e1),
-                              "ms": ms}
-        finally:
-            rt.host_free(host)
-        self._swap_blocks.append(blk)
-        self.member_base[member] = blk.ptr
-        self.layout[member] = offs
-        self.segments[member] = (0, size)
-        return ms
+        """swap_subgraph on a resident arena: a NEW contiguous device block for the
+        post-swap DAG -- the untouched members' segments copied device-to-device
+        from the source blocks (HBM speed), ONLY the incoming member uploaded from
+        the host.  The source DAG's bytes are never written (it stays valid, and
+        queries on it may run concurrently); when it is unloaded its block goes
+        back whole, so the outgoing member's bytes do not outlive it (no dead
+        segments accumulate over a swap sequence).  Returns the wall ms of
+        allocation + copies; ``last_swap`` has the phases.  ``upload=False`` (a
+        replica): the incoming segment is left for the broadcast."""
+        offs, size, host = stage_segment(prog) if upload else (None, 0, 0)
+        if not upload:
+            offs, at = {}, 0
+            for key in sorted(prog.blobs):
+                offs[key] = at
+                at = _align(at + prog.blobs[key].nbytes)
+            size = max(at, ALIGN)
+        # the new layout: members in order, each segment 256-B aligned
+        old_base, old_layout, old_segments = list(self.member_base), self.layout, self.segments
+        layout, segments, total = [], [], 0
+        for i in range(len(old_segments)):
+            if i == member:
+                rel, nbytes = offs, size
+            else:
+                o0, nbytes = old_segments[i]
+                rel = {k: v - o0 for k, v in old_layout[i].items()}
+            segments.append((total, nbytes))
+            layout.append({k: total + v for k, v in rel.items()})
+            total = _align(total + nbytes)
+        t0 = time.perf_counter()
+        blk = _arena_block(total, stream)
+        t1 = time.perf_counter()
+        e0, e1, e2 = rt.Event(), rt.Event(), rt.Event()
+        e0.record(stream)
+        for i, (off, nbytes) in enumerate(segments):
+            if i != member:
+                rt.d2d(blk.ptr + off, old_base[i], nbytes, stream)
+        e1.record(stream)
+        if upload:
+            rt.h2d(blk.ptr + segments[member][0], host, size, stream)
+        e2.record(stream)
+        rt.stream_sync(stream)
+        ms = (time.perf_counter() - t0) * 1e3
+        self.last_swap = {"bytes": size, "arena_bytes": total, "malloc_ms": (t1 - t0) * 1e3,
+                          "d2d_ms": e0.elapsed_ms(e1), "memcpy_ms": e1.elapsed_ms(e2) if upload else None,
+                          "ms": ms if upload else 0.0}
+        for b in self._blocks():                  # this arena now reads only the new block
+            b.release()
+        self._dev_block, self._swap_blocks = blk, []
+        self.layout, self.segments, self.total = layout, segments, total
+        self.member_base = [blk.ptr + off for off, _ in segments]
+        self.host_stale = True                    # the pinned staging has the old layout
+        return self.last_swap["ms"]
 
     def clone_for_swap(self) -> "WeightArena":
         """A second arena over the same blocks (each retained once more)."""
@@ -339,34 +412,61 @@ class WeightArena:
 
 class PerTensorArena:
     """The UNFUSED baseline loader (what per-model framework loading does):
-    one cudaMalloc + one cudaMemcpyAsync per weight tensor, from pageable host
-    memory, model by model.  Same interface as WeightArena so the same
-    kernels run on it; used only to measure the fused-vs-unfused claims."""
+    one cudaMalloc + one cudaMemcpyAsync per weight tensor, model by model.
+    Same interface as WeightArena so the same kernels run on it; used only to
+    measure the fused-vs-unfused claims.
 
-    def __init__(self, programs: list[MemberProgram], device: int = 0, stream=None):
+    ``pinned=False``: each tensor is copied from its own pageable host array (the
+    copy completes before cudaMemcpyAsync returns).  ``pinned=True``: the A/B that
+    separates consolidation from pinning -- every tensor is first staged (untimed,
+    like WeightArena's packed staging) in ONE pinned host buffer, then still gets
+    its own cudaMalloc and its own asynchronous cudaMemcpyAsync."""
+
+    def __init__(self, programs: list[MemberProgram], device: int = 0, stream=None, pinned: bool = False):
         rt.init_device(device)
         self.device = device
         self.ptrs: list[dict[str, int]] = []
         self.tensors = 0
         self.total = 0
         self.malloc_ms = self.memcpy_ms = 0.0
+        self.pinned = pinned
+        host = None
+        if pinned:
+            sizes = [_align(np.asarray(p.blobs[k]).nbytes) for p in programs for k in sorted(p.blobs)]
+            host = rt.host_alloc(max(sum(sizes), 16))
+            hb = np.frombuffer((C.c_uint8 * max(sum(sizes), 16)).from_address(host), dtype=np.uint8)
+            at = 0
+            for p in programs:
+                for key in sorted(p.blobs):
+                    raw = np.ascontiguousarray(p.blobs[key]).view(np.uint8).reshape(-1)
+                    hb[at:at + raw.size] = raw
+                    at += _align(raw.size)
         t0 = time.perf_counter()
+        at = 0
         for p in programs:
             table = {}
             for key in sorted(p.blobs):
                 blob = np.ascontiguousarray(p.blobs[key])
+                src = host + at if pinned else blob.ctypes.data
                 ta = time.perf_counter()
                 ptr = rt.malloc(blob.nbytes)
                 tb = time.perf_counter()
-                rt.call("dfx_memcpy_h2d", C.c_void_p(ptr), C.c_void_p(blob.ctypes.data),
+                rt.call("dfx_memcpy_h2d", C.c_void_p(ptr), C.c_void_p(src),
                         C.c_size_t(blob.nbytes), C.c_void_p(stream))
-                rt.stream_sync(stream)            # pageable source: copy completes before return
+                if not pinned:
+                    rt.stream_sync(stream)        # pageable source: copy completes before return
                 self.malloc_ms += (tb - ta) * 1e3
                 self.memcpy_ms += (time.perf_counter() - tb) * 1e3
                 table[key] = ptr
                 self.tensors += 1
                 self.total += blob.nbytes
+                at += _align(blob.nbytes)
             self.ptrs.append(table)
+        if pinned:
+            tc = time.perf_counter()
+            rt.stream_sync(stream)                # the queued copies drain
+            self.memcpy_ms += (time.perf_counter() - tc) * 1e3
+            rt.host_free(host)
         self.upload_ms = (time.perf_counter() - t0) * 1e3
 
     def addr(self, member: int, key: str) -> int:

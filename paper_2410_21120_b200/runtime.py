@@ -254,6 +254,10 @@ def d2h(dst: int, src: int, nbytes: int, stream=None) -> None:
     call("dfx_memcpy_d2h", vp(dst), vp(src), C.c_size_t(nbytes), vp(stream))
 
 
+def d2d(dst: int, src: int, nbytes: int, stream=None) -> None:
+    call("dfx_memcpy_d2d", vp(dst), vp(src), C.c_size_t(nbytes), vp(stream))
+
+
 def stream_create() -> int:
     s = vp()
     call("dfx_stream_create", C.byref(s))

@@ -6,8 +6,9 @@
   /root/reference/pkg/src/dagfuse/fuse.py:233-242; its concurrency contract is
   tests/test_fuse.py:180-205 there).
 * ``unload`` returns the instances AND the weight arena; a dropped DAG's image
-  is freed by its finalizer; the old and new DAG share the untouched members'
-  device bytes until both are gone.
+  is freed by its finalizer; a swap gives the new DAG its own re-packed arena
+  (untouched members copied device-to-device), so the old DAG's block -- with
+  the outgoing member's bytes -- returns whole when the old DAG is unloaded.
 """
 
 import gc
@@ -95,7 +96,7 @@ def test_unload_returns_arena_and_instances(corpus):
     fuse.execute_fused(new, _inputs([(sg, None) for sg in new.subgraphs], 14))
     fuse.unload(dag)
     _, used2 = rt.pool_stats()
-    assert used2 > used0                     # new still holds the shared segments
+    assert used2 > used0                     # new holds its re-packed arena
     del img
     fuse.unload(new)
     gc.collect()
@@ -119,3 +120,37 @@ def test_dropped_dag_is_freed(corpus):
     gc.collect()
     _, used2 = rt.pool_stats()
     assert used2 == used0
+
+
+def test_swap_repacks_arena_and_cycles(corpus):
+    """After a swap and the old DAG's unload, the device holds exactly the post-swap
+    arena (the outgoing member's bytes went back with the old block: no dead
+    segments pile up over a swap sequence, Table V); the swapped arena
+    still cycles through swap-out / swap-in (its host copy read back once)."""
+    models = corpus[80:84]
+    rt.pool_trim(0)
+    gc.collect()
+    _, used0 = rt.pool_stats()
+    dag = fuse.fuse_models(models)
+    fuse.execute_fused(dag, _inputs(models, 21))
+    cur = dag
+    for k, inc in enumerate(corpus[85:88]):           # three swaps, each old DAG unloaded
+        nxt = fuse.swap_subgraph(cur, cur.subgraphs[k].model_id, inc)
+        fuse.unload(cur)
+        cur = nxt
+    ins = _inputs([(sg, None) for sg in cur.subgraphs], 22)
+    out1 = fuse.execute_fused(cur, ins)
+    img = fuse.device_image(cur)
+    gc.collect()
+    _, used1 = rt.pool_stats()
+    assert img.arena.total <= used1 - used0 <= img.arena.total + (4 << 20)
+    img.free_instances()
+    img.arena.unload()                                 # swap-out (D2H of the repacked layout)
+    img.arena.upload()                                 # swap-in: one allocation + one H2D
+    out2 = fuse.execute_fused(cur, ins)
+    for mid in out1:
+        assert np.array_equal(out1[mid].values, out2[mid].values), mid
+    for (g, w) in [(sg, sg.weight_binding) for sg in cur.subgraphs]:
+        want = run_faithful(g, w, ins[g.model_id].values)
+        assert np.abs(out2[g.model_id].values - want).max() <= 2e-2 * np.abs(want).max()
+    fuse.unload(cur)
