@@ -90,6 +90,15 @@ SLACK_SPLIT_MAX = int(os.environ.get("DFX_SLACK_SPLIT_MAX", "0"))
 PERSIST_MIN_WAVES = float(os.environ.get("DFX_PERSIST_MIN_WAVES", "2"))
 GEMM_EARLY_PDL = os.environ.get("DFX_GEMM_EARLY_PDL", "0") == "1"            # A/B switch
 GEMM_DRAIN_STAGED = os.environ.get("DFX_GEMM_DRAIN", "direct") == "staged"   # A/B switch
+# grouped GEMM across members (north-star subsystem 4): pairs of concurrent members
+# whose GEMM sequences share layer shapes run those layers as ONE ndesc = 2 launch
+# (ExecInstance._pair_chains).  Measured: configs[4] (8 members) 6.09 ->
+# 5.99 ms; ResNet-50 + ResNet-152 alone slower (1.25 -> 1.28 ms at batch 1, 2.28 ->
+# 2.54 at batch 8: the coupled chains wait for each other).  "auto": DAGs of >= 6
+# concurrent members; "1" always; "0" never.
+GROUP_GEMM = {"1": True, "0": False}.get(os.environ.get("DFX_GROUP_GEMM", "auto"), "auto")
+GROUP_AUTO_MEMBERS = 6
+GROUP_MIN = int(os.environ.get("DFX_GROUP_MIN", "4"))          # matched layers for a pair to group
 # e2e queries gather their inputs on a host thread pool, overlapping the H2D (A/B switch)
 E2E_GATHER = os.environ.get("DFX_E2E_GATHER", "1") != "0"
 
@@ -664,7 +673,8 @@ class ExecInstance:
                     for pl in self.plans for t in pl.tilings.values() if t["splits"] > 1)
         self.counters = rt.malloc(max(4 * n_ctr, 16))
         self._ctr_used = 0
-        self.descs = rt.malloc(max(n_gemm, 1) * C.sizeof(rt.GemmDesc))
+        self.desc_capacity = 2 * max(n_gemm, 1)       # room for the grouped launches' copies
+        self.descs = rt.malloc(self.desc_capacity * C.sizeof(rt.GemmDesc))
         self.dev_in = rt.malloc(max(self.in_bytes, 16))
         self.dev_out = rt.malloc(max(self.out_bytes, 16))
         self.host_in = rt.host_alloc(max(self.in_bytes, 16))
@@ -698,51 +708,177 @@ class ExecInstance:
     def _build(self, progs, arena) -> rt.Graph:
         g = rt.Graph()
         host_descs = []
-        pending = []                                   # (member, launch, desc slot)
-        prev_tail = None
         self._keep = []                                # keep param structs alive
         self.nodes = []                                # (op, params, algorithmic info)
         self._node_member = []                         # member index of every graph node
+        # 1. every member's launches as a chain of (op, params, info) items
+        chains: list[list[tuple]] = []
         for m, (prog, n) in enumerate(zip(progs, self.batch)):
+            items = []
             if n == 0:
+                chains.append(items)
                 continue
-            deps = [prev_tail] if (self.dag.mode == "sequential" and prev_tail is not None) else []
             ic = prog.input_im2col or (0, 0, 0, 0, 0, 0)
             ind = tuple(prog.input_dims) if len(prog.input_dims) == 3 else (prog.input_dims[0], 1, 1)
             pin = rt.InParams(self.dev_in + self.in_off[m], self._view(m, prog, "<input>", n),
                               *ic, *ind, getattr(prog, "input_split", 0))
-            last = g.add(rt.OP_IN, pin, deps)
-            self._node_member.append(m)
-            self.nodes.append((rt.OP_IN, pin, dict(member=m, kind="in", flops=0,
-                                                   bytes=self.in_sizes[m] * 3 // 2)))
+            items.append((rt.OP_IN, pin, dict(member=m, kind="in", flops=0, bytes=self.in_sizes[m] * 3 // 2)))
             for L in prog.launches:
                 if L.index in self.plans[m].skip:      # absorbed by the GEMM before it
                     continue
                 for op, params in self._params(m, prog, L, n, host_descs):
-                    last = g.add(op, params, [last])
-                    self._node_member.append(m)
                     info = self._algo(prog, L, n, op)
                     info["node"] = L.nodes[0]
                     if op == rt.OP_GEMM:
                         info["tiling"] = self.plans[m].tilings[L.index]
                         info["geom"] = {k: L.geom[k] for k in ("cin", "cout", "kh", "kw", "cb")}
-                    self.nodes.append((op, params, info))
+                        info["gkey"] = self._group_key(prog, L, params)
+                    items.append((op, params, info))
             pout = rt.OutParams(self._view(m, prog, prog.exit_value, n), self.dev_out + self.out_off[m])
-            last = g.add(rt.OP_OUT, pout, [last])
-            self._node_member.append(m)
-            self.nodes.append((rt.OP_OUT, pout, dict(member=m, kind="out", flops=0,
-                                                     bytes=self.out_sizes[m] * 3 // 2)))
-            prev_tail = last
+            items.append((rt.OP_OUT, pout, dict(member=m, kind="out", flops=0, bytes=self.out_sizes[m] * 3 // 2)))
+            chains.append(items)
+        # 2. grouped GEMMs across members (north-star subsystem 4, DFX_GROUP_GEMM)
+        active = sum(1 for c in chains if c)
+        group = GROUP_GEMM if GROUP_GEMM != "auto" else active >= GROUP_AUTO_MEMBERS
+        pairs = self._pair_chains(chains) if group and self.dag.mode == "concurrent" else []
+        partner = {}                                   # (m, i) -> (m', i') matched item
+        for (a, b, matches) in pairs:
+            for ia, ib in matches:
+                partner[(a, ia)] = (b, ib)
+                partner[(b, ib)] = (a, ia)
+        self.grouped_launches = sum(len(mt) for _, _, mt in pairs)
+        # 3. graph nodes in dependency order: a matched pair becomes ONE launch once
+        # both chains reach it (monotone matching: no cross-chain cycle)
+        tail: dict[int, int] = {}                      # member -> last node id
+        pos = [0] * len(chains)
+        prev_tail = None
+        seq = self.dag.mode == "sequential"
+
+        def add(op, params, info, members):
+            deps = sorted({tail[mm] for mm in members if mm in tail})
+            nid = g.add(op, params, deps)
+            for mm in members:
+                tail[mm] = nid
+            self._node_member.append(members[0])
+            self.nodes.append((op, params, info))
+            return nid
+
+        order = [m for m in range(len(chains)) if chains[m]]
+        progressed = True
+        while progressed:
+            progressed = False
+            for m in order:
+                items = chains[m]
+                while pos[m] < len(items):
+                    i = pos[m]
+                    if seq and i == 0 and prev_tail is not None:
+                        tail[m] = prev_tail            # sequential mode: after the previous member
+                    op, params, info = items[i]
+                    mate = partner.get((m, i))
+                    if mate is not None:
+                        b, ib = mate
+                        if pos[b] != ib:                # wait for the partner chain to get there
+                            break
+                        gl = self._group_launch([items[i], chains[b][ib]], host_descs)
+                        gi = dict(kind="gemm", member=m, node=f"{info['node']}+{chains[b][ib][2]['node']}",
+                                  flops=info["flops"] + chains[b][ib][2]["flops"],
+                                  bytes=info["bytes"] + chains[b][ib][2]["bytes"],
+                                  weight_bytes=info.get("weight_bytes", 0) + chains[b][ib][2].get("weight_bytes", 0),
+                                  grouped=[info["node"], chains[b][ib][2]["node"]],
+                                  tiling=info["tiling"], geom=info["geom"])
+                        add(rt.OP_GEMM, gl, gi, [m, b])
+                        pos[b] += 1
+                    else:
+                        add(op, params, info, [m])
+                    pos[m] += 1
+                    progressed = True
+                if pos[m] == len(items) and seq:
+                    prev_tail = tail[m]
+        assert all(p == len(c) for p, c in zip(pos, chains)), "grouped GEMM matching left a chain blocked"
         if NODE_PRIORITY and self.dag.mode == "concurrent" and max(self.batch) <= PRIORITY_MAX_BATCH:
             self._prioritise(g)
         self._keep = [p for _, p, _ in self.nodes]
         if host_descs:
+            assert len(host_descs) <= self.desc_capacity
             arr = (rt.GemmDesc * len(host_descs))(*host_descs)
             rt.h2d(self.descs, C.addressof(arr), C.sizeof(arr), self.stream)
             rt.stream_sync(self.stream)
         g.instantiate()
         self.kernel_nodes = len(g.kinds)
         return g
+
+    # --- grouped GEMM across members
+    @staticmethod
+    def _group_key(prog, L, gl):
+        """Launches that may share ONE grouped gemm_kernel launch: the one-tile kernel
+        (no persistent walk, cluster split-K or depthwise epilogue), the same
+        weight geometry and input map, same storage type and M2 form."""
+        if gl.flags & (2 | 4 | 8 | 16) or gl.desc0.dw_k or gl.desc0.pre_mode or gl.m2:
+            return None
+        gm = L.geom
+        src = prog.values[L.src]
+        return (gm["cin"], gm["cout"], gm["kh"], gm["kw"], gm["sh"], gm["sw"], gm["ph"], gm["pw"], gm["cb"],
+                src.h, src.w, bool(gm.get("tokens")), gl.dtype)
+
+    def _pair_chains(self, chains):
+        """Members paired two by two (most matchable GEMMs first); within a pair the
+        GEMMs of equal group key are matched in order (longest common subsequence),
+        so every cross-member edge points forward in both chains."""
+        keyseq = [[(i, it[2].get("gkey")) for i, it in enumerate(c) if it[0] == rt.OP_GEMM and it[2].get("gkey")]
+                  for c in chains]
+
+        def lcs(x, y):
+            nx, ny = len(x), len(y)
+            dp = np.zeros((nx + 1, ny + 1), np.int32)
+            for i in range(nx - 1, -1, -1):
+                xi = x[i][1]
+                row, nxt = dp[i], dp[i + 1]
+                for j in range(ny - 1, -1, -1):
+                    row[j] = nxt[j + 1] + 1 if xi == y[j][1] else max(nxt[j], row[j + 1])
+            out, i, j = [], 0, 0
+            while i < nx and j < ny:
+                if x[i][1] == y[j][1]:
+                    out.append((x[i][0], y[j][0]))
+                    i += 1
+                    j += 1
+                elif dp[i + 1][j] >= dp[i][j + 1]:
+                    i += 1
+                else:
+                    j += 1
+            return out
+
+        cands = []
+        for a in range(len(chains)):
+            for b in range(a + 1, len(chains)):
+                if keyseq[a] and keyseq[b] and {k for _, k in keyseq[a]} & {k for _, k in keyseq[b]}:
+                    mt = lcs(keyseq[a], keyseq[b])
+                    if len(mt) >= GROUP_MIN:
+                        cands.append((len(mt), a, b, mt))
+        used, pairs = set(), []
+        for _, a, b, mt in sorted(cands, key=lambda t: (-t[0], t[1], t[2])):
+            if a not in used and b not in used:
+                used |= {a, b}
+                pairs.append((a, b, mt))
+        return pairs
+
+    def _group_launch(self, items, host_descs) -> rt.GemmLaunch:
+        """ONE gemm_kernel launch over the problems of several members (ndesc > 1):
+        descriptors copied contiguously into the device array, tiles numbered
+        problem after problem (dfx_gemm.cu picks its problem by tile_begin)."""
+        descs, at = [], 0
+        for _, gl, _ in items:
+            d = rt.GemmDesc()
+            C.memmove(C.addressof(d), C.addressof(gl.desc0), C.sizeof(d))
+            d.tile_begin = at
+            at += d.tiles
+            descs.append(d)
+        slot = len(host_descs)
+        host_descs.extend(descs)
+        bn = max(d.bn for d in descs)
+        planes = 2 if items[0][1].dtype in (rt.DT_F16X2, rt.DT_BF16X2) else 1
+        gl = rt.GemmLaunch(self.descs + slot * C.sizeof(rt.GemmDesc), len(descs), at, bn, items[0][1].dtype,
+                           gemm_slots(bn, at, self.dag.sm_count, 0, planes))
+        return gl
 
     def _prioritise(self, g) -> None:
         """Concurrent members are independent branches of one graph; the query

@@ -161,3 +161,26 @@ def test_plan_never_overlays_a_launch_output_on_its_inputs(name, n):
         checked += t.get("dw") is not None
     if name == "efficientnet_v2_l":
         assert checked == 60 if n == 1 else checked >= 0
+
+
+def test_group_pairing_is_monotone():
+    """Grouped-GEMM pairing (device.ExecInstance._pair_chains): members paired two by
+    two, matches strictly increasing in both chains (no cross-chain cycle), most
+    matches first, short overlaps below GROUP_MIN ignored."""
+    from paper_2410_21120_b200 import device, runtime as rt
+    G = rt.OP_GEMM
+
+    def chain(keys):
+        return [(rt.OP_IN, None, {})] + [(G, None, {"gkey": k}) for k in keys] + [(rt.OP_OUT, None, {})]
+    a = chain("abcdabcdxyz")
+    b = chain("abcdabcdabcdabcdxyz")       # a deeper model sharing a's shapes
+    c = chain("pqrs")
+    d = chain("pq")
+    pairs = device.ExecInstance._pair_chains(None, [a, b, c, d])
+    assert [(x, y) for x, y, _ in pairs] == [(0, 1)]          # c-d share only 2 < GROUP_MIN
+    _, _, mt = pairs[0]
+    assert len(mt) == 11
+    for (i0, j0), (i1, j1) in zip(mt, mt[1:]):
+        assert i1 > i0 and j1 > j0
+    for i, j in mt:
+        assert a[i][2]["gkey"] == b[j][2]["gkey"]
