@@ -354,10 +354,13 @@ def secondary_configs(args, rt, members, programs, arena, flush, P, local_rank):
     names = list(zoo.EIGHT_MODEL)
     batches = (1, 2, 4, 8, 1, 2, 4, 8)
     m8 = build_models(names)
-    p8 = [program_for(g, w, args.precision) for g, w in m8]
+    # ViT-B/16's layernorm / token / attention kernels are 16-bit only: the 8-model
+    # DAG runs in the split mode's 16-bit plane type (fp16x2 -> fp16)
+    prec8 = args.precision[:4]
+    p8 = [program_for(g, w, prec8) for g, w in m8]
     rt.pool_trim(0)            # retained arena-pool pages would hide the allocation from cudaMemGetInfo
     free0, _ = rt.mem_info()
-    dag8 = DeviceDag(m8, local_rank, args.mode, programs=p8, precision=args.precision)
+    dag8 = DeviceDag(m8, local_rank, args.mode, programs=p8, precision=prec8)
     inst8 = dag8.acquire(batches)
     inst8.upload_inputs([np.random.default_rng(7 + i).standard_normal((bb,) + tuple(g.input_spec.dims))
                          .astype(np.float32) for i, (bb, (g, _)) in enumerate(zip(batches, m8))])
@@ -365,6 +368,7 @@ def secondary_configs(args, rt, members, programs, arena, flush, P, local_rank):
     free1, _ = rt.mem_info()
     out["eight_model"] = {"config": "configs[4]: 8-model fused DAG, per-member batches "
                                     + ",".join(f"{n}:{bb}" for n, bb in zip(names, batches)),
+                          "precision": prec8,
                           "ms_per_step": med8, "images_per_s": sum(batches) / (med8 * 1e-3),
                           "arena_mb": dag8.arena.total / 1e6, "swap_in_ms": dag8.swap_in_ms,
                           "peak_hbm_gb": (free0 - free1) / 1e9, "graph_nodes": inst8.kernel_nodes}
@@ -373,12 +377,14 @@ def secondary_configs(args, rt, members, programs, arena, flush, P, local_rank):
     return out
 
 
-def accuracy_modes(args, models, flush, P, local_rank, modes=("fp16x2", "bf16x2", "bf16")):
+def accuracy_modes(args, models, flush, P, local_rank, modes=("fp16x2", "bf16x2", "fp16", "bf16")):
     """The same configs[1] / configs[2] workloads in the other storage precisions
     (the headline line is args.precision): the split modes fp16x2 / bf16x2 (two
     16-bit planes per value, three-product GEMMs) are the ones that meet the full
     north-star parity bar -- identical top-1 on >= 99.9 % of 1000 inputs, raw
-    (tests/test_gpu_north_star.py; statistic in profiles/r02/parity_*.json).
+    (tests/test_gpu_north_star.py; statistic in profiles/r02/parity_*.json); the
+    16-bit fp16 / bf16 modes are the fast ones (within 2e-2 / 1e-1, top-1 only
+    where the fp32 margin exceeds the error).
     Each: device-timed batch-1 and batch-32 steps, e2e through execute_fused with
     host tensors, and the logits of one image per member against the CPU oracle."""
     from oracle.executor_ref import run_fast
@@ -764,7 +770,10 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
     ap.add_argument("--batch", type=int, default=1)
-    ap.add_argument("--precision", default="fp16", choices=("fp16", "bf16", "fp16x2", "bf16x2"))
+    # default: the split fp16x2 storage -- the precision that meets the whole north-star
+    # parity bar (<= 2e-2 AND identical top-1 on >= 99.9 % of 1000 inputs, raw); the
+    # 16-bit modes are in the line's precision_modes block
+    ap.add_argument("--precision", default="fp16x2", choices=("fp16", "bf16", "fp16x2", "bf16x2"))
     ap.add_argument("--mode", default="concurrent", choices=("concurrent", "sequential"))
     ap.add_argument("--models", nargs="+",
                     default=["vgg16", "mobilenet_v3_large", "densenet161", "efficientnet_v2_l"])

@@ -216,8 +216,8 @@ int config_for(int op, const void* params, size_t size, LaunchCfg* c) {
       if (p->bn_max < 16 || p->bn_max > 256 || p->total_tiles < 1)
         return fail(DFX_E_ARG, "gemm: bad bn_max %d / tiles %d", p->bn_max, p->total_tiles);
       const int planes = dfx::dtype_split(p->dtype) ? 2 : 1;
-      if (planes == 2 && (p->m2 || p->desc0.pre_mode || p->desc0.dw_k > 0 || (p->flags & 4)))
-        return fail(DFX_E_UNSUPPORTED, "gemm: split precision without m2 / A transform / dw epilogue / staged drain");
+      if (planes == 2 && (p->m2 || p->desc0.pre_mode || (p->flags & 4)))
+        return fail(DFX_E_UNSUPPORTED, "gemm: split precision without m2 / A transform / staged drain");
       if (p->dtype < DFX_BF16 || p->dtype > DFX_F16X2) return fail(DFX_E_ARG, "gemm: dtype %d", p->dtype);
       c->func = gemm_func(p->dtype, p->m2);
       c->grid = dim3(p->total_tiles);
@@ -262,8 +262,8 @@ int config_for(int op, const void* params, size_t size, LaunchCfg* c) {
             return fail(DFX_E_ARG, "gemm: depthwise epilogue needs one problem whose M tiles fit one CTA "
                                    "(or a 2-CTA cluster split along p)");
           if (pair) c->cluster = 2;
-          if (size_t(d0.n) * d0.p * d0.q * (p->bn_max + 8) * 2 >
-              size_t(p->nslots) * dfx::gemm_slot_bytes(p->bn_max, p->m2 ? 1 : 0))
+          if (size_t(d0.n) * d0.p * d0.q * (p->bn_max + 8) * 2 * planes >
+              size_t(p->nslots) * dfx::gemm_slot_bytes(p->bn_max, p->m2 ? 1 : 0, planes))
             return fail(DFX_E_ARG, "gemm: depthwise epilogue map exceeds the %d slots", p->nslots);
           c->smem += size_t(d0.dw_k * d0.dw_k + 2) * p->bn_max * 4;   // taps + BN vectors
           c->block = dim3(dfx::kGemmThreads);
@@ -382,11 +382,11 @@ int config_for(int op, const void* params, size_t size, LaunchCfg* c) {
       // the weight traffic saves (EfficientNetV2-L batch 32 6.73 vs 6.07 ms)
       static const int ipi_env = getenv("DFX_SE_IPI") ? atoi(getenv("DFX_SE_IPI")) : 1;
       const int ipi = (ipi_env == 4 && cl == 16 && p->in.n >= 8 && !dfx::dtype_split(p->in.dtype)) ? 4 : 1;
-      const bool split = dfx::dtype_split(p->in.dtype);       // FC weights from L2, no x tile
+      const bool split = dfx::dtype_split(p->in.dtype);       // hi + lo FC slices, no x tile
       if (split) cl = 16;
       c->func = se_func(p->in.dtype, cl, ipi);
       c->grid = dim3(unsigned(cl), unsigned((p->in.n + ipi - 1) / ipi));
-      c->smem = ((p->apply & 2) || split) ? 0 : size_t(dfx::se_smem_bytes(p->in.c, p->cr, cl));
+      c->smem = (p->apply & 2) ? 0 : size_t(dfx::se_smem_bytes(p->in.c, p->cr, cl)) * (split ? 2 : 1);
       // room for the CTA's x slice (latency-bound small batches): the scale reads smem
       // (batch 1: EfficientNetV2-L 2.10 -> 2.08 ms; at batch 32 it costs occupancy)
       static const int xt_batch = getenv("DFX_SE_XTILE_BATCH") ? atoi(getenv("DFX_SE_XTILE_BATCH")) : 8;
@@ -543,6 +543,7 @@ int dfx_init(int device) {
     CK(cudaFuncSetAttribute(DFX_PICK(in_im2col_kernel, dt), cudaFuncAttributeMaxDynamicSharedMemorySize,
                             kIm2colSmemLimit));
     CK(cudaFuncSetAttribute(se_func(dt, 16), cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    CK(cudaFuncSetAttribute(se_func(dt, 16), cudaFuncAttributeMaxDynamicSharedMemorySize, dfx::kSeSmemBudget));
   }
   return get_encode();
 }

@@ -366,6 +366,9 @@ DFX_DEV void dw_smem_t(const dfx_gemm_desc& D, const T* xs, int xp, int N, int P
   const float* const al = sw + K * K * bn;
   const float* const be = al + bn;
   const bool has_al = D.dw_alpha != nullptr, has_be = D.dw_beta != nullptr;
+  // split precision: a pixel of the map holds [hi (xp) | lo (xp)]
+  constexpr bool kSp = kSplitT<T>;
+  const int pp = kSp ? 2 * xp : xp;
   (void)C;
   for (int item = item0 + tid; item < total; item += nthr) {
     const int cgi = item % cg;
@@ -383,7 +386,7 @@ DFX_DEV void dw_smem_t(const dfx_gemm_desc& D, const T* xs, int xp, int N, int P
     for (int ki = 0; ki < K; ++ki) {
       const int h = h0 + ki;
       if (h < 0 || h >= P) continue;
-      const T* row = xs + (n * P + h) * Q * xp + c;
+      const T* row = xs + (n * P + h) * Q * pp + c;
 #pragma unroll
       for (int kj = 0; kj < K; ++kj) {
         const int w = w0 + kj;
@@ -393,10 +396,23 @@ DFX_DEV void dw_smem_t(const dfx_gemm_desc& D, const T* xs, int xp, int N, int P
         const float wv[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
         float x[8];
         if (pair) {
-          const float4 r4 = dsmem_ld4(row + w * xp, uint32_t(h >= tp_rows));
+          const float4 r4 = dsmem_ld4(row + w * pp, uint32_t(h >= tp_rows));
           unpack8<T>(*reinterpret_cast<const uint4*>(&r4), x);
+          if constexpr (kSp) {
+            float l[8];
+            const float4 l4 = dsmem_ld4(row + w * pp + xp, uint32_t(h >= tp_rows));
+            unpack8<T>(*reinterpret_cast<const uint4*>(&l4), l);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) x[i] += l[i];
+          }
         } else {
-          unpack8<T>(*reinterpret_cast<const uint4*>(row + w * xp), x);
+          unpack8<T>(*reinterpret_cast<const uint4*>(row + w * pp), x);
+          if constexpr (kSp) {
+            float l[8];
+            unpack8<T>(*reinterpret_cast<const uint4*>(row + w * pp + xp), l);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) x[i] += l[i];
+          }
         }
 #pragma unroll
         for (int i = 0; i < 8; ++i) acc[i] = fmaf(wv[i], x[i], acc[i]);
@@ -412,7 +428,7 @@ DFX_DEV void dw_smem_t(const dfx_gemm_desc& D, const T* xs, int xp, int N, int P
       acc[0] += b0.x; acc[1] += b0.y; acc[2] += b0.z; acc[3] += b0.w;
       acc[4] += b1.x; acc[5] += b1.y; acc[6] += b1.z; acc[7] += b1.w;
     }
-    act8_t<ACT>(acc);
+    act8_t<ACT, kSp>(acc);
     const int64_t pix = (int64_t(n) * OH + p) * OW + q;
     stv8<T>(o, view_pixel_index(o, pix, ca), acc);
   }

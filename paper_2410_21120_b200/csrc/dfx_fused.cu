@@ -87,11 +87,12 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kSeThreads)
   // 16-B aligned slices are staged in smem unless apply bit 1 says otherwise (large
   // batches: clusters of smem-heavy CTAs then cannot be co-scheduled, while the
   // weights are L2-resident and shared by every image's cluster anyway)
-  // split precision: FC weights [hi C x Cr][lo C x Cr], read from L2 (not staged)
-  const bool staged = !kSplitT<T> && (C & 7) == 0 && (Cr & 7) == 0 && !(P.apply & 2);
-  const int64_t wlo = kSplitT<T> ? int64_t(C) * Cr : 0;   // lo block offset (elements)
+  const bool staged = (C & 7) == 0 && (Cr & 7) == 0 && !(P.apply & 2);
   const bool apply = P.apply & 1;
   const int sb = ((cs * Cr * 2) + 15) & ~15;
+  // split precision: FC weights [hi C x Cr][lo C x Cr]; staged, the lo slices follow
+  // the two hi slices in smem (w1_lo at +2 sb bytes, w2_lo at +3 sb)
+  const int64_t wlo = !kSplitT<T> ? 0 : staged ? int64_t(sb) : int64_t(C) * Cr;   // elements
   const T* w1 = staged ? reinterpret_cast<const T*>(wsm) : w1g + int64_t(c_lo) * Cr;
   const T* w2 = staged ? reinterpret_cast<const T*>(wsm + sb) : w2g + int64_t(c_lo) * Cr;
 
@@ -102,9 +103,13 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kSeThreads)
     fence_barrier_init();
     const uint32_t bytes = uint32_t(nch) * Cr * 2;
     if (staged && bytes) {
-      mbar_arrive_expect_tx(&wbar, 2 * bytes);
+      mbar_arrive_expect_tx(&wbar, (kSplitT<T> ? 4 : 2) * bytes);
       bulk_load(wsm, w1g + int64_t(c_lo) * Cr, bytes, &wbar);
       bulk_load(wsm + sb, w2g + int64_t(c_lo) * Cr, bytes, &wbar);
+      if constexpr (kSplitT<T>) {
+        bulk_load(wsm + 2 * sb, w1g + int64_t(C) * Cr + int64_t(c_lo) * Cr, bytes, &wbar);
+        bulk_load(wsm + 3 * sb, w2g + int64_t(C) * Cr + int64_t(c_lo) * Cr, bytes, &wbar);
+      }
     }
   }
   griddep_wait();
@@ -116,7 +121,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kSeThreads)
   // a second L2 round trip (dfx_api.cu DFX_OP_SE)
   uint32_t dsm;
   asm("mov.u32 %0, %%dynamic_smem_size;" : "=r"(dsm));
-  const int wbytes = staged ? 2 * sb : 0;
+  const int wbytes = staged ? (kSplitT<T> ? 4 : 2) * sb : 0;
   T* xt = reinterpret_cast<T*>(wsm + wbytes);
   const bool cache_x = !kSplitT<T> && apply && IPI == 1 && ((in.coff | out_coff_of(P) | c_lo | nch) & 7) == 0 &&
                        uint32_t(wbytes + hw * nch * 2) <= dsm;

@@ -367,7 +367,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         if (ga) s_alpha[i] = c < cout ? ga[c] : 0.f;
         if (gb) s_beta[i] = c < cout ? gb[c] : 0.f;
       }
-      if (!kSplitT<T> && D.dw_k > 0) {
+      if (D.dw_k > 0) {
         // depthwise epilogue: this CTA's taps [k*k][bn] and BN vectors, after the ring
         float* s_dw = reinterpret_cast<float*>(slots + nslots * slot_bytes);
         const int kk = D.dw_k * D.dw_k;
@@ -486,7 +486,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     return;
   }
 
-  if constexpr (!kSplitT<T>) if (D.dw_k > 0) {
+  if (D.dw_k > 0) {
     // ---- depthwise epilogue: this CTA covers every M tile (host-checked), so the
     // drain parks its channels of the whole output map in the (now free) operand
     // slots -- the same epilogue and 16-bit rounding as a global store, through a
@@ -497,7 +497,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     dfx_view sv = o;
     sv.base = xs;
     sv.n = N; sv.h = P; sv.w = Q; sv.c = bn;
-    sv.pitch = xp;
+    sv.pitch = xp * planes;                            // split: [hi | lo] per pixel
     sv.coff = -co_base;                                // absolute channel -> slot column
 #pragma unroll
     for (int h = 0; h < 1 + M2; ++h) {

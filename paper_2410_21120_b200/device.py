@@ -574,7 +574,7 @@ def plan_member(prog: MemberProgram, n: int, sm_count: int = 148, cluster_ok: bo
     tilings = {}
     skip: set[int] = set()
     planes = planes_of(prog.precision)
-    dw_pairs = gemm_dw_pairs(prog) if GEMM_DW and planes == 1 else {}
+    dw_pairs = gemm_dw_pairs(prog) if GEMM_DW else {}
     for L in prog.launches:
         if L.kind != GEMM:
             continue
@@ -593,9 +593,10 @@ def plan_member(prog: MemberProgram, n: int, sm_count: int = 148, cluster_ok: bo
             m2 = int(mt == 2 and not pair)
             bn = min(GEMM_DW_BN_M2 if m2 else GEMM_DW_BN_PAIR if pair else GEMM_DW_BN, t["bn"])
             nt = -(-L.geom["cout"] // bn)
-            xs = n * out.h * out.w * (bn + 8) * 2           # the map in smem (dfx_gemm.cu)
-            nsl = gemm_slots(bn, nt * (2 if pair else 1), sm_count, m2)
-            if mt <= (1 if GEMM_DW_MODE == "single" else 2) and xs <= nsl * (128 * 64 * 2 * (1 + m2) + bn * 128):
+            xs = n * out.h * out.w * (bn + 8) * 2 * planes  # the map in smem (dfx_gemm.cu)
+            nsl = gemm_slots(bn, nt * (2 if pair else 1), sm_count, m2, planes)
+            if mt <= (1 if GEMM_DW_MODE == "single" else 2) and not (m2 and planes > 1) and \
+                    xs <= nsl * (128 * 64 * 2 * (1 + m2) + bn * 128) * planes:
                 t = dict(t, bn=bn, nt=nt, splits=1, sps=t["stages"], csplit=0, m2=m2,
                          tiles=nt * (2 if pair else 1), dw=dw_pairs[L.index])
                 skip.add(dw_pairs[L.index])
@@ -1098,7 +1099,7 @@ class ExecInstance:
             yield rt.OP_SE, rt.SeParams(src, self._view(m, prog, L.dst, n), addr("w1"), addr("b1"),
                                         addr("w2"), addr("b2"), geo["cr"], rt.ACT[geo["act1"]],
                                         rt.ACT[geo["act2"]],
-                                        geo.get("apply", 0) | (2 if n >= SE_UNSTAGED_BATCH else 0))
+                                        geo.get("apply", 0) | (2 if self._se_unstaged(prog, geo, n) else 0))
         elif L.kind == DWSE:
             geo = L.geom
             addr = (lambda r: arena.addr(m, L.blobs[r]) if r in L.blobs else None)
@@ -1110,6 +1111,16 @@ class ExecInstance:
                                             int(n < SE_UNSTAGED_BATCH))
         else:
             raise AssertionError(L.kind)
+
+    @staticmethod
+    def _se_unstaged(prog, geo, n) -> bool:
+        """SE FC weights read from L2 instead of staged per CTA: large batches (the
+        clusters of smem-heavy CTAs could not be co-scheduled), or slices (hi + lo
+        for split precision) beyond the cluster kernel's smem budget
+        (dfx_common.cuh se_smem_bytes, kSeSmemBudget)."""
+        cs = -(-geo["c"] // 128) * 8
+        need = 2 * ((cs * geo["cr"] * 2 + 15) & ~15) * planes_of(prog.precision)
+        return n >= SE_UNSTAGED_BATCH or need > 190 * 1024
 
     # --- execution
     def stage_inputs(self, xs) -> None:

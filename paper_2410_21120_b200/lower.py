@@ -97,7 +97,12 @@ def to_storage_bits(a: np.ndarray, precision: str) -> np.ndarray:
     if precision == "bf16":
         return to_bf16_bits(a)
     if precision == "fp16":
-        return np.clip(np.asarray(a, np.float32), -65504, 65504).astype(np.float16).view(np.uint16)
+        c = np.clip(np.asarray(a, np.float32), -65504, 65504)
+        try:                       # torch's converter (F16C): ~15x numpy's on fp16 subnormals
+            import torch           # (the lo plane of split weights), same IEEE round-to-nearest-even
+            return torch.from_numpy(np.ascontiguousarray(c)).to(torch.float16).numpy().view(np.uint16)
+        except ImportError:
+            return c.astype(np.float16).view(np.uint16)
     raise ValueError(precision)
 
 
@@ -843,6 +848,10 @@ def lower_member(g, w, keep_f32: bool = False, precision: str = "fp16") -> Membe
         kh, kw = low.input_im2col[:2]
         low.input_split = round_up(kh * kw * g.input_spec.dims[0], 8)
     prog = low.run()
+    if precision in SPLIT_PRECISIONS:
+        for L in prog.launches:
+            if L.kind in (LN, TOKENS, ATTN):
+                raise UnsupportedOnDevice(L.nodes[0], f"{L.kind} has no split-precision kernel ({precision})")
     prog.debug_f32 = low.debug_f32
     prog.precision = precision
     prog.input_im2col = low.input_im2col

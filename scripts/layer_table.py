@@ -16,10 +16,11 @@ ap.add_argument("--batch", type=int, default=1)
 ap.add_argument("--top", type=int, default=40)
 ap.add_argument("--models", nargs="+", default=list(zoo.NORTH_STAR))
 ap.add_argument("--json", default=None)
+ap.add_argument("--precision", default="fp16")
 a = ap.parse_args()
 models = [zoo.build(n) for n in a.models]
 dag = fuse.fuse_models(models)
-img = fuse.load_fused(dag)
+img = fuse.load_fused(dag, precision=a.precision)
 inst = img.acquire(tuple([a.batch] * len(models)))
 inst.upload_inputs([np.random.default_rng(i).standard_normal((a.batch, 3, 224, 224)).astype(np.float32)
                     for i in range(len(models))])
