@@ -32,21 +32,23 @@ DFX_DEV float tanh_approx(float x) {
   return r;
 }
 // P (precise): the split-precision storage types (two 16-bit planes, ~22-bit
-// significand) use IEEE-accurate forms instead -- tanh.approx's 2^-11 would
-// otherwise be the largest error left in the network.
+// significand) use forms accurate to a few fp32 ulp -- tanh.approx's 2^-11 would
+// otherwise be the largest error left in the network.  __expf (ex2.approx) and
+// __fdividef are within 2 ulp over the activations' range: 1e-7 relative, below
+// the 2^-22 of the storage, at a fraction of the IEEE forms' instructions.
 template <bool P = false> DFX_DEV float sigmoid_f(float v) {
-  if constexpr (P) return 1.0f / (1.0f + expf(-v));
+  if constexpr (P) return __fdividef(1.0f, 1.0f + __expf(-v));
   else return fmaf(0.5f, tanh_approx(0.5f * v), 0.5f);
 }
 template <bool P = false> DFX_DEV float silu_f(float v) {
-  if constexpr (P) return v / (1.0f + expf(-v));
+  if constexpr (P) return __fdividef(v, 1.0f + __expf(-v));
   else {
     const float h = 0.5f * v;
     return fmaf(h, tanh_approx(h), h);
   }
 }
 template <bool P = false> DFX_DEV float hsig_f(float v) {
-  if constexpr (P) return fminf(fmaxf(v + 3.0f, 0.0f), 6.0f) / 6.0f;
+  if constexpr (P) return __fdividef(fminf(fmaxf(v + 3.0f, 0.0f), 6.0f), 6.0f);
   else return fminf(fmaxf(v + 3.0f, 0.0f), 6.0f) * (1.0f / 6.0f);
 }
 DFX_DEV float gelu_f(float v) { return 0.5f * v * (1.0f + erff(v * 0.70710678118654752f)); }

@@ -114,10 +114,27 @@ DFX_DEV void act8_t(float* v) {
   }
 }
 
+// lo_cols > 0 (split precision, gemm_kernel): the accumulator is two column halves,
+// [0, bn) and [lo_cols, lo_cols + bn), summed on the way out.
+template <typename T>
+DFX_DEV void tmem_ld16_acc(uint32_t taddr, int lo_cols, uint32_t (&r)[16]) {
+  tmem_ld16_issue(taddr, r);
+  if (kSplitT<T> && lo_cols > 0) {
+    uint32_t q[16];
+    tmem_ld16_issue(taddr + uint32_t(lo_cols), q);
+    tmem_ld_wait(q);
+    tmem_ld_wait(r);
+#pragma unroll
+    for (int k = 0; k < 16; ++k) r[k] = __float_as_uint(__uint_as_float(r[k]) + __uint_as_float(q[k]));
+  } else {
+    tmem_ld_wait(r);
+  }
+}
+
 template <typename T, int ACT1>
 DFX_DEV void drain_rows_direct_t(uint32_t taddr, int ncols, int64_t pix, int img, bool valid, int co_base,
                                  int cout, const dfx_epilogue& e, const dfx_view& o, bool views_vec, float* ws,
-                                 int ldw, int c_first, int c_step) {
+                                 int ldw, int c_first, int c_step, int lo_cols) {
   const float* const alpha = e.alpha;
   const float* const beta = e.beta;
   const int binop = e.binop, act2 = e.act2;
@@ -137,8 +154,7 @@ DFX_DEV void drain_rows_direct_t(uint32_t taddr, int ncols, int64_t pix, int img
     // third of its instructions
     for (int c0 = c_first; c0 < ncols; c0 += c_step) {
       uint32_t r[16];
-      tmem_ld16_issue(taddr + uint32_t(c0), r);
-      tmem_ld_wait(r);
+      tmem_ld16_acc<T>(taddr + uint32_t(c0), lo_cols, r);
       float v[16];
 #pragma unroll
       for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
@@ -178,8 +194,7 @@ DFX_DEV void drain_rows_direct_t(uint32_t taddr, int ncols, int64_t pix, int img
   }
   for (int c0 = c_first; c0 < ncols; c0 += c_step) {
     uint32_t r[16];
-    tmem_ld16_issue(taddr + uint32_t(c0), r);
-    tmem_ld_wait(r);
+    tmem_ld16_acc<T>(taddr + uint32_t(c0), lo_cols, r);
     if (!valid) continue;
     float v[16];
 #pragma unroll
@@ -241,10 +256,10 @@ DFX_DEV void drain_rows_direct_t(uint32_t taddr, int ncols, int64_t pix, int img
 template <typename T>
 DFX_DEV void drain_rows_direct(uint32_t taddr, int ncols, int64_t pix, int img, bool valid,
                                int co_base, int cout, const dfx_epilogue& e, const dfx_view& o,
-                               bool views_vec, float* ws, int ldw, int c_first, int c_step) {
+                               bool views_vec, float* ws, int ldw, int c_first, int c_step, int lo_cols = 0) {
 #define DFX_DRAIN(A)                                                                                  \
   drain_rows_direct_t<T, A>(taddr, ncols, pix, img, valid, co_base, cout, e, o, views_vec, ws, ldw, \
-                            c_first, c_step)
+                            c_first, c_step, lo_cols)
   switch (e.act1) {
     case DFX_ACT_RELU: DFX_DRAIN(DFX_ACT_RELU); break;
     case DFX_ACT_HARDSWISH: DFX_DRAIN(DFX_ACT_HARDSWISH); break;

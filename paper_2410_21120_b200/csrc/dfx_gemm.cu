@@ -99,7 +99,12 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   const int slot_bytes = gemm_slot_bytes(L.bn_max, m2l, planes);
   const int a_lo_off = kStageABytes * (1 + m2l);   // lo A tiles follow the hi ones
   const int a_bytes = a_lo_off * planes;           // A part of a slot (B follows)
-  const int b_lo_off = L.bn_max * 128;             // lo B tile follows the hi one
+  // split precision: each k-step's B sub-tile is [hi bn rows | lo bn rows], so ONE
+  // MMA with N = 2 bn computes A_hi*B_hi (TMEM columns [0, bn)) and A_hi*B_lo
+  // ([bn, 2 bn)) -- an MMA costs the same at N <= 128 (its SMEM A read bounds
+  // it) -- and A_lo*B_hi adds into [0, bn): two MMAs per K=16 step instead of
+  // three; the drain sums the two column halves
+  const int b_kstride = planes == 2 ? 2 : 1;      // sub-tile pitch in units of sub_b
   const int nslots = L.nslots;
   if (threadIdx.x == 0) DFX_TL(0);                 // CTA start
 #ifdef DFX_TIMELINE
@@ -124,7 +129,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   if (threadIdx.x < sizeof(dfx_gemm_desc) / 16)
     reinterpret_cast<uint4*>(&hdr->desc)[threadIdx.x] =
         reinterpret_cast<const uint4*>(gd)[threadIdx.x];
-  const uint32_t tmem_cols = tmem_cols_for(L.bn_max * (1 + m2l));
+  const uint32_t tmem_cols = tmem_cols_for(L.bn_max * (1 + m2l) * planes);
   if (threadIdx.x == 0) {
     DFX_TL(7);                                     // descriptor copied
     for (int i = 0; i < nslots; ++i) {
@@ -218,9 +223,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       const int nk = min(kpack, ksteps - k0);
       mbar_arrive_expect_tx(&hdr->full[it], nk * tx_per_k);
       for (int j = 0; j < nk; ++j) {
-        tma_load_2d(b_dst + j * sub_b, tmb, &hdr->full[it], (k0 + j) * cb, co_base);
+        tma_load_2d(b_dst + j * b_kstride * sub_b, tmb, &hdr->full[it], (k0 + j) * cb, co_base);
         if constexpr (planes == 2)       // W_lo rows follow the cout W_hi rows
-          tma_load_2d(b_dst + b_lo_off + j * sub_b, tmb, &hdr->full[it], (k0 + j) * cb, cout + co_base);
+          tma_load_2d(b_dst + (2 * j + 1) * sub_b, tmb, &hdr->full[it], (k0 + j) * cb, cout + co_base);
       }
       if (it < 8) DFX_TL(30 + it);                 // B prefetch of stage `it` issued (30..37)
     }
@@ -287,9 +292,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                           pb[h] + rc, n0h[h]);
             }
           }
-        tma_load_2d(b_dst + j * sub_b, tmb, &hdr->full[slot], (k0 + j) * cb, co_base);
+        tma_load_2d(b_dst + j * b_kstride * sub_b, tmb, &hdr->full[slot], (k0 + j) * cb, co_base);
         if constexpr (planes == 2)
-          tma_load_2d(b_dst + b_lo_off + j * sub_b, tmb, &hdr->full[slot], (k0 + j) * cb, cout + co_base);
+          tma_load_2d(b_dst + (2 * j + 1) * sub_b, tmb, &hdr->full[slot], (k0 + j) * cb, cout + co_base);
         if (++cblk == cblocks) {
           cblk = 0;
           if (++sc == S) {
@@ -306,6 +311,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   } else if (warp == 1 && lane == 0) {
     // ================= MMA issuer
     const uint32_t idesc = umma_idesc_f16(uint32_t(bn), Elt<T>::kDtype);
+    const bool wide = planes == 2 && 2 * bn <= 256;    // hi|lo B rows as one N = 2 bn MMA
+    const uint32_t idesc2 = umma_idesc_f16(uint32_t(wide ? 2 * bn : bn), Elt<T>::kDtype);
     const uint32_t row_bytes = uint32_t(cb) * 2u;
     const int kk_n = cb / 16;
     uint32_t accumulate = 0;
@@ -325,19 +332,27 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       const int nk = min(kpack, ksteps - st * kpack);
       for (int j = 0; j < nk; ++j) {
         for (int kk = 0; kk < kk_n; ++kk) {
-          const uint64_t bd = umma_smem_desc(b_base + j * sub_b + kk * 32, row_bytes);
+          const uint64_t bd = umma_smem_desc(b_base + j * b_kstride * sub_b + kk * 32, row_bytes);
 #pragma unroll
           for (int h = 0; h < 1 + M2; ++h) {
             if (h >= nhalf) break;
             const uint64_t ad = umma_smem_desc(a_base + h * kStageABytes + j * sub_a + kk * 32, row_bytes);
 #ifndef DFX_EXP_NOMMA
-            umma_f16(tmem_base + uint32_t(h * bn), ad, bd, idesc, accumulate);
-            if constexpr (planes == 2) {       // + lo(A) hi(B) + hi(A) lo(B)
+            if constexpr (planes == 2) {
+              // [0, bn) += A_hi B_hi, [bn, 2 bn) += A_hi B_lo (one MMA when 2 bn <= 256), then
+              // [0, bn) += A_lo B_hi
               const uint64_t adl =
                   umma_smem_desc(a_base + a_lo_off + h * kStageABytes + j * sub_a + kk * 32, row_bytes);
-              const uint64_t bdl = umma_smem_desc(b_base + b_lo_off + j * sub_b + kk * 32, row_bytes);
-              umma_f16(tmem_base + uint32_t(h * bn), adl, bd, idesc, 1u);
-              umma_f16(tmem_base + uint32_t(h * bn), ad, bdl, idesc, 1u);
+              if (wide) {
+                umma_f16(tmem_base, ad, bd, idesc2, accumulate);
+              } else {
+                const uint64_t bdl = umma_smem_desc(b_base + (2 * j + 1) * sub_b + kk * 32, row_bytes);
+                umma_f16(tmem_base, ad, bd, idesc, accumulate);
+                umma_f16(tmem_base + uint32_t(bn), ad, bdl, idesc, accumulate);
+              }
+              umma_f16(tmem_base, adl, bd, idesc, 1u);
+            } else {
+              umma_f16(tmem_base + uint32_t(h * bn), ad, bd, idesc, accumulate);
             }
 #else
             (void)ad; (void)bd; (void)idesc;
@@ -444,6 +459,13 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       uint32_t r[16];
       tmem_ld16_issue(lane_addr + uint32_t(c0), r);
       tmem_ld_wait(r);
+      if constexpr (planes == 2) {               // + the A_hi * B_lo column half
+        uint32_t q[16];
+        tmem_ld16_issue(lane_addr + uint32_t(bn + c0), q);
+        tmem_ld_wait(q);
+#pragma unroll
+        for (int k = 0; k < 16; ++k) r[k] = __float_as_uint(__uint_as_float(r[k]) + __uint_as_float(q[k]));
+      }
       float4* dst = reinterpret_cast<float4*>(red + row * rp + c0);
 #pragma unroll
       for (int k = 0; k < 4; ++k)
@@ -506,7 +528,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       const bool valid = row < tn * tp * tq && on < N && op < P && oq < Q;
       const int64_t pix = (int64_t(on) * P + op) * Q + oq;
       drain_rows_direct<T>(lane_addr + uint32_t(h * bn), ncols, pix, on, valid, co_base, cout, e, sv, true,
-                           nullptr, ldw, 16 * (warp >> 2), 16 * int(blockDim.x >> 7));
+                           nullptr, ldw, 16 * (warp >> 2), 16 * int(blockDim.x >> 7), planes == 2 ? bn : 0);
     }
     tc_fence_before();
     const bool pair = !M2 && mt_total == 2;            // 2-CTA cluster: the peer holds the other rows
@@ -532,7 +554,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     float* wsp = splits > 1 ? ws + split * plane : nullptr;
     if (kSplitT<T> || !(L.flags & 4))
       drain_rows_direct<T>(lane_addr + uint32_t(h * bn), ncols, pix, on, valid, co_base, cout, e, o,
-                           views_vec, wsp, ldw, 16 * (warp >> 2), 16 * int(blockDim.x >> 7));
+                           views_vec, wsp, ldw, 16 * (warp >> 2), 16 * int(blockDim.x >> 7), planes == 2 ? bn : 0);
     else
       drain_rows<T>(lane_addr + uint32_t(h * bn), stg, ncols, pix, on, valid, co_base, cout, e, o,
                     views_vec, wsp, ldw, 16 * (warp >> 2), 16 * int(blockDim.x >> 7));

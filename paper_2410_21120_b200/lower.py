@@ -898,6 +898,9 @@ def choose_bn(cout: int) -> tuple[int, int]:
 GEMM_M2 = os.environ.get("DFX_GEMM_M2", "1") != "0"     # A/B switch for 256-row CTAs
 BN_FLOOR_MANY_M = int(os.environ.get("DFX_BN_FLOOR_MANY_M", "64"))   # A/B knob
 SPLIT_MIN_STAGES = int(os.environ.get("DFX_SPLIT_MIN_STAGES", "4"))   # K stages per split, at least
+# split precision: a stage costs 2-3x the MMAs and twice the operand bytes, so fewer,
+# longer splits (measured at batch 1: 4-model fp16x2 3.34 ms at 4, 3.26 at 6, 3.39 at 8)
+SPLIT_MIN_STAGES_X2 = int(os.environ.get("DFX_SPLIT_MIN_STAGES_X2", "6"))
 # split-K reduction: "kernel" (default) = fp32 workspace + a splitk_kernel launch;
 # "cluster" = the splits of a tile form a thread-block cluster and reduce over DSMEM
 # inside the GEMM (dfx_gemm.cu, <= 8 splits; removes 245 of 928 launches at batch 1
@@ -945,8 +948,9 @@ def gemm_tiling(geom: dict, n: int, p: int, q: int, sm_count: int = 148, cluster
     stages = math.ceil(geom["ksteps"] / kpack)
     base = m_tiles * nt
     splits = 1
-    if base < sm_count and stages >= 2 * SPLIT_MIN_STAGES:
-        splits = min(math.ceil(sm_count / base), stages // SPLIT_MIN_STAGES)
+    min_st = SPLIT_MIN_STAGES_X2 if planes > 1 else SPLIT_MIN_STAGES
+    if base < sm_count and stages >= 2 * min_st:
+        splits = min(math.ceil(sm_count / base), stages // min_st)
     if max_splits:
         splits = min(splits, max_splits)
     sps = math.ceil(stages / max(splits, 1))
