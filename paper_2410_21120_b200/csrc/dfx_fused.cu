@@ -123,8 +123,11 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kSeThreads)
   asm("mov.u32 %0, %%dynamic_smem_size;" : "=r"(dsm));
   const int wbytes = staged ? (kSplitT<T> ? 4 : 2) * sb : 0;
   T* xt = reinterpret_cast<T*>(wsm + wbytes);
-  const bool cache_x = !kSplitT<T> && apply && IPI == 1 && ((in.coff | out_coff_of(P) | c_lo | nch) & 7) == 0 &&
-                       uint32_t(wbytes + hw * nch * 2) <= dsm;
+  constexpr int kPl = kSplitT<T> ? 2 : 1;            // split: the lo tile follows the hi one
+  const bool cache_x = apply && IPI == 1 && ((in.coff | out_coff_of(P) | c_lo | nch) & 7) == 0 &&
+                       uint32_t(wbytes + hw * nch * 2 * kPl) <= dsm;
+  T* const xtl = xt + hw * nch;                        // lo plane tile (split precision)
+  const int64_t xlo = lo_of<T>(in);
 
   // ---- 1. pool: thread = (channel group g, pixel stripe y); all loads in flight first
   const int G = (nch + 7) / 8;                        // channel groups of this CTA
@@ -144,14 +147,25 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kSeThreads)
       // all in flight at once (one L2 round trip instead of one per 4 loads), then
       // pooled from smem; the scale pass reuses the tile
       const T* ib = reinterpret_cast<const T*>(in.base) + base;
-      for (int s = y; s < hw; s += stripes)
+      for (int s = y; s < hw; s += stripes) {
         asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(xt + s * nch + g * 8)),
                      "l"(ib + int64_t(s) * in.pitch)
                      : "memory");
+        if constexpr (kPl == 2)
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(xtl + s * nch + g * 8)),
+                       "l"(ib + int64_t(s) * in.pitch + xlo)
+                       : "memory");
+      }
       asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
       for (int s = y; s < hw; s += stripes) {
         float x[8];
         unpack8<T>(*reinterpret_cast<const uint4*>(xt + s * nch + g * 8), x);
+        if constexpr (kPl == 2) {
+          float l[8];
+          unpack8<T>(*reinterpret_cast<const uint4*>(xtl + s * nch + g * 8), l);
+#pragma unroll
+          for (int i = 0; i < 8; ++i) x[i] += l[i];
+        }
 #pragma unroll
         for (int i = 0; i < 8; ++i) acc[i] += x[i];
       }
@@ -316,6 +330,12 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kSeThreads)
         const int s = i / G8, g8 = (i - s * G8) * 8;
         float x[8];
         unpack8<T>(*reinterpret_cast<const uint4*>(xt + s * nch + g8), x);
+        if constexpr (kPl == 2) {
+          float l[8];
+          unpack8<T>(*reinterpret_cast<const uint4*>(xtl + s * nch + g8), l);
+#pragma unroll
+          for (int j = 0; j < 8; ++j) x[j] += l[j];
+        }
 #pragma unroll
         for (int j = 0; j < 8; ++j) x[j] *= gate[g8 + j];
         stv8<T>(out, view_pixel_index(out, pb + s, c_lo + g8), x);

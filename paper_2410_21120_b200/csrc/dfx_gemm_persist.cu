@@ -52,7 +52,12 @@ __global__ void __launch_bounds__(kPersistThreads, 1)
   uint8_t* slots = smem + kSlotsOffset;
   constexpr int planes = kSplitT<T> ? 2 : 1;       // split precision: hi + lo operand tiles
   const int slot_bytes = gemm_slot_bytes(L.bn_max, 0, planes);
-  const int a_lo_off = kStageABytes, b_off = kStageABytes * planes, b_lo_off = L.bn_max * 128;
+  const int a_lo_off = kStageABytes, b_off = kStageABytes * planes;
+  // split precision: B sub-tile of k-step j = [hi bn rows | lo bn rows] (lo at (2j + 1)
+  // sub_b); "wide" (bn <= 128): A_hi * [B_hi; B_lo] as ONE N = 2 bn MMA into a
+  // 2 bn-column accumulator, + A_lo * B_hi into its first half (dfx_gemm.cu)
+  const bool wide = planes == 2 && L.bn_max <= 128;
+  const int accw = wide ? 2 : 1;                   // accumulator width in units of bn
   const int nslots = L.nslots;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const dfx_gemm_desc* gd = &L.desc0;
@@ -65,11 +70,11 @@ __global__ void __launch_bounds__(kPersistThreads, 1)
   // One group = two CTAs per SM: each may hold only half of TMEM (a second
   // CTA's tcgen05.alloc would otherwise block until the first one exits).
   const int groups = (int(blockDim.x) - 64) >> 7;
-  const int nacc = max(2, min(kMaxAcc, (groups > 1 ? 512 : 256) / L.bn_max));
+  const int nacc = max(2, min(kMaxAcc, (groups > 1 ? 512 : 256) / (L.bn_max * accw)));
   // pre_mode (A prologue transform): group 1 transforms A stages, group 0 drains
   const bool pre = !kSplitT<T> && L.desc0.pre_mode != 0;
   const bool alt = groups > 1 && nacc >= 4 && !pre;
-  const uint32_t tmem_cols = tmem_cols_for(nacc * L.bn_max);
+  const uint32_t tmem_cols = tmem_cols_for(nacc * L.bn_max * accw);
   if (threadIdx.x == 0) {
     for (int i = 0; i < nslots; ++i) {
       mbar_init(&hdr->full[i], 1);
@@ -126,9 +131,9 @@ __global__ void __launch_bounds__(kPersistThreads, 1)
           const int nk = min(kpack, ksteps - k0);
           mbar_arrive_expect_tx(&hdr->full[slot], nk * (box_a_bytes + uint32_t(sub_b)) * planes);
           for (int j = 0; j < nk; ++j) {                // weights: static, before the dependency
-            tma_load_2d(b_dst + j * sub_b, tmb, &hdr->full[slot], (k0 + j) * cb, co_base);
+            tma_load_2d(b_dst + j * planes * sub_b, tmb, &hdr->full[slot], (k0 + j) * cb, co_base);
             if constexpr (planes == 2)
-              tma_load_2d(b_dst + b_lo_off + j * sub_b, tmb, &hdr->full[slot], (k0 + j) * cb, cout + co_base);
+              tma_load_2d(b_dst + (2 * j + 1) * sub_b, tmb, &hdr->full[slot], (k0 + j) * cb, cout + co_base);
           }
           if (!waited) {
             griddep_wait();
@@ -162,6 +167,7 @@ __global__ void __launch_bounds__(kPersistThreads, 1)
     if (lane == 0) {
       // ================= MMA issuer: nacc TMEM accumulators in a ring
       const uint32_t idesc = umma_idesc_f16(uint32_t(bn), Elt<T>::kDtype);
+      const uint32_t idesc2 = umma_idesc_f16(uint32_t(accw * bn), Elt<T>::kDtype);
       const uint32_t row_bytes = uint32_t(cb) * 2u;
       const int kk_n = cb / 16;
       int lt = 0, slot = 0, b = 0;
@@ -170,7 +176,7 @@ __global__ void __launch_bounds__(kPersistThreads, 1)
       for (int tile = blockIdx.x; tile < total; tile += grid, ++lt) {
         if (lt >= nacc) mbar_wait(&hdr->acc_empty[b], apar ^ 1);
         tc_fence_after();
-        const uint32_t acc = tmem_base + uint32_t(b * bn);
+        const uint32_t acc = tmem_base + uint32_t(b * accw * bn);
         uint32_t accumulate = 0;
         for (int st = 0; st < stages; ++st) {
           mbar_wait(&gate[slot], par);
@@ -181,11 +187,17 @@ __global__ void __launch_bounds__(kPersistThreads, 1)
           for (int j = 0; j < nk; ++j)
             for (int kk = 0; kk < kk_n; ++kk) {
               const uint64_t ad = umma_smem_desc(a_base + j * sub_a + kk * 32, row_bytes);
-              const uint64_t bd = umma_smem_desc(b_base + j * sub_b + kk * 32, row_bytes);
-              umma_f16(acc, ad, bd, idesc, accumulate);
-              if constexpr (planes == 2) {         // + lo(A) hi(B) + hi(A) lo(B)
+              const uint64_t bd = umma_smem_desc(b_base + j * planes * sub_b + kk * 32, row_bytes);
+              if constexpr (planes == 2) {
+                if (wide) {                        // [0, bn) hi*hi, [bn, 2 bn) hi*lo
+                  umma_f16(acc, ad, bd, idesc2, accumulate);
+                } else {                           // + hi(A) lo(B) into the same columns
+                  umma_f16(acc, ad, bd, idesc, accumulate);
+                  umma_f16(acc, ad, umma_smem_desc(b_base + (2 * j + 1) * sub_b + kk * 32, row_bytes), idesc, 1u);
+                }
                 umma_f16(acc, umma_smem_desc(a_base + a_lo_off + j * sub_a + kk * 32, row_bytes), bd, idesc, 1u);
-                umma_f16(acc, ad, umma_smem_desc(b_base + b_lo_off + j * sub_b + kk * 32, row_bytes), idesc, 1u);
+              } else {
+                umma_f16(acc, ad, bd, idesc, accumulate);
               }
               accumulate = 1;
             }
@@ -273,8 +285,8 @@ __global__ void __launch_bounds__(kPersistThreads, 1)
       mbar_wait(&hdr->acc_full[bcur], phcur);
       tc_fence_after();
       if (kSplitT<T> || !(L.flags & 4))
-        drain_rows_direct<T>(lane_addr + uint32_t(bcur * bn), ncols, pix, on, valid, co_base, cout, e, o,
-                             views_vec, nullptr, 0, c_first, c_step);
+        drain_rows_direct<T>(lane_addr + uint32_t(bcur * accw * bn), ncols, pix, on, valid, co_base, cout, e, o,
+                             views_vec, nullptr, 0, c_first, c_step, wide ? bn : 0);
       else
         drain_rows<T>(lane_addr + uint32_t(bcur * bn), stg, ncols, pix, on, valid, co_base, cout, e, o,
                       views_vec, nullptr, 0, c_first, c_step);
