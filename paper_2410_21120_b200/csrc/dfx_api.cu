@@ -747,11 +747,15 @@ int dfx_tmap_weights(void* out128, const void* base, int rows, int k, int cb, in
   if (cb != 16 && cb != 32 && cb != 64) return fail(DFX_E_ARG, "tmap_weights: cb %d", cb);
   if (k % 8 || reinterpret_cast<uintptr_t>(base) % 16)
     return fail(DFX_E_ARG, "tmap_weights: k %d / alignment", k);
-  cuuint64_t dims[2] = {cuuint64_t(k), cuuint64_t(rows)};
-  cuuint64_t strides[1] = {cuuint64_t(k) * 2};
-  cuuint32_t box[2] = {cuuint32_t(cb), cuuint32_t(bn)};
-  cuuint32_t estr[2] = {1, 1};
-  CUresult r = g_encode(reinterpret_cast<CUtensorMap*>(out128), tmap_dtype(dtype), 2,
+  // split precision: `rows` = 2 cout ([hi rows; lo rows]) as a 3-D map (k, cout, plane):
+  // ONE box (cb, bn, 2) lands a k-step's hi and lo rows back to back in smem
+  const bool split = dfx::dtype_split(dtype);
+  if (split && rows % 2) return fail(DFX_E_ARG, "tmap_weights: split rows %d", rows);
+  cuuint64_t dims[3] = {cuuint64_t(k), cuuint64_t(split ? rows / 2 : rows), 2};
+  cuuint64_t strides[2] = {cuuint64_t(k) * 2, cuuint64_t(k) * 2 * cuuint64_t(rows / 2)};
+  cuuint32_t box[3] = {cuuint32_t(cb), cuuint32_t(bn), 2};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = g_encode(reinterpret_cast<CUtensorMap*>(out128), tmap_dtype(dtype), split ? 3 : 2,
                         const_cast<void*>(base), dims, strides, box, estr,
                         CU_TENSOR_MAP_INTERLEAVE_NONE, swizzle_for(cb),
                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);

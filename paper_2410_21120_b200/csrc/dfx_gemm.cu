@@ -223,9 +223,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       const int nk = min(kpack, ksteps - k0);
       mbar_arrive_expect_tx(&hdr->full[it], nk * tx_per_k);
       for (int j = 0; j < nk; ++j) {
-        tma_load_2d(b_dst + j * b_kstride * sub_b, tmb, &hdr->full[it], (k0 + j) * cb, co_base);
-        if constexpr (planes == 2)       // W_lo rows follow the cout W_hi rows
-          tma_load_2d(b_dst + (2 * j + 1) * sub_b, tmb, &hdr->full[it], (k0 + j) * cb, cout + co_base);
+        if constexpr (planes == 2)       // one 3-D box: the k-step's hi rows, then its lo rows
+          tma_load_3d(b_dst + 2 * j * sub_b, tmb, &hdr->full[it], (k0 + j) * cb, co_base, 0);
+        else
+          tma_load_2d(b_dst + j * sub_b, tmb, &hdr->full[it], (k0 + j) * cb, co_base);
       }
       if (it < 8) DFX_TL(30 + it);                 // B prefetch of stage `it` issued (30..37)
     }
@@ -292,9 +293,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                           pb[h] + rc, n0h[h]);
             }
           }
-        tma_load_2d(b_dst + j * b_kstride * sub_b, tmb, &hdr->full[slot], (k0 + j) * cb, co_base);
         if constexpr (planes == 2)
-          tma_load_2d(b_dst + (2 * j + 1) * sub_b, tmb, &hdr->full[slot], (k0 + j) * cb, cout + co_base);
+          tma_load_3d(b_dst + 2 * j * sub_b, tmb, &hdr->full[slot], (k0 + j) * cb, co_base, 0);
+        else
+          tma_load_2d(b_dst + j * sub_b, tmb, &hdr->full[slot], (k0 + j) * cb, co_base);
         if (++cblk == cblocks) {
           cblk = 0;
           if (++sc == S) {
@@ -350,7 +352,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                 umma_f16(tmem_base, ad, bd, idesc, accumulate);
                 umma_f16(tmem_base + uint32_t(bn), ad, bdl, idesc, accumulate);
               }
+#ifndef DFX_EXP_SPLIT_1MMA
               umma_f16(tmem_base, adl, bd, idesc, 1u);
+#else
+              (void)adl;
+#endif
             } else {
               umma_f16(tmem_base + uint32_t(h * bn), ad, bd, idesc, accumulate);
             }

@@ -131,9 +131,10 @@ __global__ void __launch_bounds__(kPersistThreads, 1)
           const int nk = min(kpack, ksteps - k0);
           mbar_arrive_expect_tx(&hdr->full[slot], nk * (box_a_bytes + uint32_t(sub_b)) * planes);
           for (int j = 0; j < nk; ++j) {                // weights: static, before the dependency
-            tma_load_2d(b_dst + j * planes * sub_b, tmb, &hdr->full[slot], (k0 + j) * cb, co_base);
-            if constexpr (planes == 2)
-              tma_load_2d(b_dst + (2 * j + 1) * sub_b, tmb, &hdr->full[slot], (k0 + j) * cb, cout + co_base);
+            if constexpr (planes == 2)          // hi rows then lo rows, one 3-D box
+              tma_load_3d(b_dst + 2 * j * sub_b, tmb, &hdr->full[slot], (k0 + j) * cb, co_base, 0);
+            else
+              tma_load_2d(b_dst + j * sub_b, tmb, &hdr->full[slot], (k0 + j) * cb, co_base);
           }
           if (!waited) {
             griddep_wait();
