@@ -34,7 +34,7 @@
 extern "C" {
 #endif
 
-#define DFX_ABI_VERSION 4
+#define DFX_ABI_VERSION 5
 
 typedef enum dfx_status {
   DFX_OK = 0,
@@ -164,7 +164,26 @@ typedef struct __attribute__((aligned(64))) dfx_gemm_desc {
   const float* dw_alpha;
   const float* dw_beta;
   int32_t dw_k, dw_s, dw_pad, dw_act;
+  /* Squeeze-excitation after the depthwise epilogue (dw_k > 0, se != NULL; device
+   * pointer): the CTAs keep their depthwise outputs in shared memory, pool their
+   * channels, add their fc1 partial sums into se->scratch, meet at ONE grid-wide
+   * barrier (se->sync), form the hidden vector, their channels' gates, and store
+   * x * gate to `out` (the SE's channel_scale output): the SE launch disappears. */
+  const struct dfx_se_fuse* se;
 } dfx_gemm_desc;
+
+/* Squeeze-excitation fused into a depthwise-epilogue GEMM (dfx_gemm_desc.se). */
+typedef struct dfx_se_fuse {
+  const void* w1;                      /* fc1^T [c][cr], 16-bit (split: [hi; lo] blocks) */
+  const float* b1;                     /* may be NULL */
+  const void* w2;                      /* fc2 [c][cr], 16-bit (split: [hi; lo]) */
+  const float* b2;                     /* may be NULL */
+  float* scratch;                      /* [N tiles][n][cr] fp32 fc1 partial sums */
+  uint32_t* sync;                      /* {arrivals, epoch}, zeroed once */
+  int32_t c, cr, act1, act2;
+  int32_t ctas;                        /* CTAs that meet at the barrier (the grid) */
+  int32_t _pad[3];
+} dfx_se_fuse;
 
 /* Kernel parameter of one GEMM launch.  A single problem travels inline
  * (desc0, ndesc == 1): descriptor and tensor maps then sit in kernel-parameter
@@ -187,7 +206,8 @@ typedef struct __attribute__((aligned(64))) dfx_gemm_launch {
                                       their partials over DSMEM (no workspace, no
                                       splitk launch) */
   int32_t m2;                      /* any problem has m2 = 1 (sizes smem / TMEM) */
-  int32_t _pad[7];
+  int32_t se_cr;                   /* desc0.se != NULL: its hidden width (sizes smem) */
+  int32_t _pad[6];
   dfx_gemm_desc desc0;             /* the problem when ndesc == 1 */
 } dfx_gemm_launch;
 

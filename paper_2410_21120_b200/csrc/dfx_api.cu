@@ -262,8 +262,18 @@ int config_for(int op, const void* params, size_t size, LaunchCfg* c) {
             return fail(DFX_E_ARG, "gemm: depthwise epilogue needs one problem whose M tiles fit one CTA "
                                    "(or a 2-CTA cluster split along p)");
           if (pair) c->cluster = 2;
-          if (size_t(d0.n) * d0.p * d0.q * (p->bn_max + 8) * 2 * planes >
-              size_t(p->nslots) * dfx::gemm_slot_bytes(p->bn_max, p->m2 ? 1 : 0, planes))
+          size_t need = (size_t(d0.n) * d0.p * d0.q * (p->bn_max + 8) * 2 * planes + 15) & ~size_t(15);
+          if (d0.se != nullptr) {       // fused SE: depthwise-output tile + reduction scratch
+            const int oh = d0.out.h, ow = d0.out.w, cr = p->se_cr;
+            const int nt = d0.nt;
+            if (p->m2 || d0.n > 2 || cr < 1 || cr > 512)
+              return fail(DFX_E_ARG, "gemm: fused SE needs batch <= 2, no m2, 1 <= cr <= 512");
+            need += ((size_t(d0.n) * oh * ow * p->bn_max * 2 * planes + 15) & ~size_t(15)) +
+                    size_t(dfx::kGemmThreads) * 16 * 4 +
+                    (4 * size_t(p->bn_max) + 2 * ((cr + 3) & ~3) + size_t(nt) * d0.n * cr + 4) * 4;
+            c->smem += size_t(2) * planes * p->bn_max * cr * 2;       // staged fc1^T / fc2 rows
+          }
+          if (need > size_t(p->nslots) * dfx::gemm_slot_bytes(p->bn_max, p->m2 ? 1 : 0, planes))
             return fail(DFX_E_ARG, "gemm: depthwise epilogue map exceeds the %d slots", p->nslots);
           c->smem += size_t(d0.dw_k * d0.dw_k + 2) * p->bn_max * 4;   // taps + BN vectors
           c->block = dim3(dfx::kGemmThreads);
@@ -497,7 +507,8 @@ int dfx_sizeof(const char* name) {
            {"dfx_ln_params", sizeof(dfx_ln_params)},
            {"dfx_tokens_params", sizeof(dfx_tokens_params)},
            {"dfx_attn_params", sizeof(dfx_attn_params)},
-           {"dfx_dwse_params", sizeof(dfx_dwse_params)}};
+           {"dfx_dwse_params", sizeof(dfx_dwse_params)},
+           {"dfx_se_fuse", sizeof(dfx_se_fuse)}};
   for (auto& e : t)
     if (!strcmp(e.n, name)) return e.s;
   return -1;

@@ -363,9 +363,15 @@ namespace dfx {
 // Cluster variant (D.mt_p == 2, one M tile per CTA of a 2-CTA cluster): each CTA
 // drained its own rows; rows p >= D.tp live in rank 1's shared memory and are read
 // over DSMEM, and the output items are split between the two ranks.
+template <typename T>
+DFX_DEV void se_finish(const dfx_gemm_desc& D, uint8_t* se_smem, const float (*csum)[8], int item0, int total,
+                       int N, int OH, int OW, int co_base, int nch, const dfx_view& o, int bn, int tid, int nthr,
+                       const uint16_t* wsm, uint64_t* gbar);
+
 template <typename T, int K, int S, int ACT>
 DFX_DEV void dw_smem_t(const dfx_gemm_desc& D, const T* xs, int xp, int N, int P, int Q, int co_base,
-                       int nch, const dfx_view& o, const float* sw, int bn, int tid, int nthr) {
+                       int nch, const dfx_view& o, const float* sw, int bn, int tid, int nthr,
+                       uint8_t* se_smem, uint64_t* gbar) {
   const int OH = o.h, OW = o.w, cg = nch >> 3, C = D.cout;
   int total = N * OH * OW * cg;
   const bool pair = D.mt_p == 2 && D.m2 == 0;         // 2-CTA cluster, split along p
@@ -385,6 +391,15 @@ DFX_DEV void dw_smem_t(const dfx_gemm_desc& D, const T* xs, int xp, int N, int P
   constexpr bool kSp = kSplitT<T>;
   const int pp = kSp ? 2 * xp : xp;
   (void)C;
+  // SE after the depthwise (D.se): outputs stay in shared memory (ot, stored-tensor
+  // rounding) and each thread sums its channel group's rounded values per image
+  float csum[2][8];
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int i = 0; i < 8; ++i) csum[a][i] = 0.0f;
+  T* const ot = reinterpret_cast<T*>(se_smem);
+  const int64_t ot_lo = int64_t(N) * OH * OW * nch;   // lo plane of the tile (split)
   for (int item = item0 + tid; item < total; item += nthr) {
     const int cgi = item % cg;
     int t = item / cg;
@@ -445,33 +460,244 @@ DFX_DEV void dw_smem_t(const dfx_gemm_desc& D, const T* xs, int xp, int N, int P
     }
     act8_t<ACT, kSp>(acc);
     const int64_t pix = (int64_t(n) * OH + p) * OW + q;
-    stv8<T>(o, view_pixel_index(o, pix, ca), acc);
+    if (se_smem == nullptr) {
+      stv8<T>(o, view_pixel_index(o, pix, ca), acc);
+    } else {
+      st8<T>(ot, pix * nch + c, ot_lo, acc);
+      float r[8];
+      ld8<T>(ot, pix * nch + c, ot_lo, r);           // the value a stored tensor would hold
+#pragma unroll
+      for (int i = 0; i < 8; ++i) csum[n & 1][i] += r[i];
+    }
   }
+  if (se_smem != nullptr)
+    se_finish<T>(D, se_smem, csum, item0, total, N, OH, OW, co_base, nch, o, bn, tid, nthr,
+                 reinterpret_cast<const uint16_t*>(sw + (K * K + 2) * bn), gbar);
+}
+
+DFX_DEV uint32_t ld_acquire_u32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+DFX_DEV float dsmem_ld1(const float* local, uint32_t rank) {
+  uint32_t remote;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(smem_u32(local)), "r"(rank));
+  float v;
+  asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(remote) : "memory");
+  return v;
+}
+
+// The squeeze-excitation of the fused MBConv middle (dfx_gemm_desc.se), after the
+// depthwise outputs of this CTA's bn channels sit in `ot` (stored-tensor rounding):
+//   1. channel sums: per-thread partials (fixed channel group per thread) reduced in
+//      thread order; a 2-CTA pair adds the peer's over DSMEM in rank order; x (1/HW);
+//   2. fc1 partial over this CTA's channels (c ascending) -> se->scratch[N tile];
+//   3. ONE grid-wide barrier (arrival counter + epoch; every CTA of the grid is
+//      resident: the host keeps the grid within its share of the SMs, and the
+//      successor launches only after every CTA called launch_dependents);
+//   4. hidden = act1(b1 + sum over N tiles in order), gates of this CTA's channels
+//      = act2(b2 + fc2 rows . hidden), out = x * gate (the se_kernel apply path).
+template <typename T>
+DFX_DEV void se_finish(const dfx_gemm_desc& D, uint8_t* se_smem, const float (*csum)[8], int item0, int total,
+                       int N, int OH, int OW, int co_base, int nch, const dfx_view& o, int bn, int tid, int nthr,
+                       const uint16_t* wsm, uint64_t* gbar) {
+  constexpr bool kSp = kSplitT<T>;
+  const dfx_se_fuse& F = *D.se;
+  const int Cr = F.cr, cg = nch >> 3;
+  const int hw = OH * OW;
+  const int64_t npix = int64_t(N) * hw;
+  T* const ot = reinterpret_cast<T*>(se_smem);
+  const int64_t ot_lo = npix * nch;
+  float* const red = reinterpret_cast<float*>(se_smem + ((npix * nch * 2 * (kSp ? 2 : 1) + 15) & ~15));
+  float* const mean = red + nthr * 16;                 // [2][nch]
+  float* const hidden = mean + 2 * bn;                 // [2][Cr]
+  float* const gate = hidden + 2 * ((Cr + 3) & ~3);    // [2][nch]
+  float* const part = gate + 2 * bn;                   // [N tiles][N][Cr]: the gathered fc1 partials (16-B aligned)
+  const bool pair = D.mt_p == 2 && D.m2 == 0;
+  const uint32_t rank = pair ? cluster_ctarank() : 0u;
+  if (tid == 0) DFX_TL(50);                            // depthwise done
+  // 1. channel sums.  Thread t always handled channel group (item0 + t) % cg: a
+  // butterfly over the lanes of equal group (xor cg, 2 cg, .. 16: fixed order) leaves
+  // lane l < cg with its warp's sums, then warps are added in warp order
+  const int lane = tid & 31, wid = tid >> 5, nwarps = nthr >> 5;
+  float v[16];
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int i = 0; i < 8; ++i) v[a * 8 + i] = csum[a][i];
+  for (int off = cg; off < 32; off <<= 1)
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[i] += __shfl_xor_sync(0xffffffffu, v[i], off);
+  if (lane < cg)
+#pragma unroll
+    for (int i = 0; i < 16; ++i) red[(wid * cg + lane) * 16 + i] = v[i];
+  __syncthreads();
+  const float inv = 1.0f / float(hw);
+  for (int k = tid; k < N * nch; k += nthr) {
+    const int n = k / nch, c = k - n * nch, g = c >> 3, i = c & 7;
+    const int l = ((g - item0) % cg + cg) % cg;        // the lane that held group g
+    float s = 0.0f;
+    for (int w = 0; w < nwarps; ++w) s += red[(w * cg + l) * 16 + (n & 1) * 8 + i];
+    if (pair) gate[k] = s;                             // this CTA's partial (gate[] reused later)
+    else mean[k] = s * inv;
+  }
+  if (pair) {
+    cluster_sync_all();
+    for (int k = tid; k < N * nch; k += nthr) mean[k] = (dsmem_ld1(gate + k, 0) + dsmem_ld1(gate + k, 1)) * inv;
+    cluster_sync_all();                                // peers done reading gate[]
+  } else {
+    __syncthreads();
+  }
+  if (tid == 0) DFX_TL(51);                            // channel means
+  // 2. fc1 partial over this CTA's channels (fc1^T rows staged in smem: wsm =
+  // [w1 hi, w2 hi(, w1 lo, w2 lo)] of [bn][Cr]) -> scratch (rank 0 of a pair only)
+  const int ntile = co_base / bn;
+  const T* w1 = reinterpret_cast<const T*>(wsm);
+  const T* w2 = w1 + bn * Cr;
+  const int wlo = kSp ? 2 * bn * Cr : 0;
+  if (tid == 0) mbar_wait(gbar + 1, 0);               // the staged fc1^T / fc2 rows landed
+  __syncthreads();
+  if (rank == 0) {
+    for (int k = tid; k < N * Cr; k += nthr) {
+      const int n = k / Cr, j = k - n * Cr;
+      float s = 0.0f;
+#pragma unroll 4
+      for (int c = 0; c < nch; ++c) {
+        const int wi = c * Cr + j;
+        float wv = Elt<T>::to_f(w1[wi]);
+        if constexpr (kSp) wv += Elt<T>::to_f(w1[wi + wlo]);
+        s = fmaf(wv, mean[n * nch + c], s);
+      }
+      F.scratch[(int64_t(ntile) * N + n) * Cr + j] = s;
+    }
+  }
+  // 3. grid barrier
+  __syncthreads();
+  if (tid == 0) DFX_TL(52);                            // fc1 partial written
+  if (tid == 0) {
+    __threadfence();
+    uint32_t* sync = F.sync;
+    const uint32_t e = ld_acquire_u32(sync + 1);
+    const uint32_t a = atomicAdd(sync, 1u) + 1u;
+    if (a == uint32_t(F.ctas)) {
+      atomicExch(sync, 0u);
+      __threadfence();
+      atomicAdd(sync + 1, 1u);
+    } else {
+      for (uint32_t tries = 0; ld_acquire_u32(sync + 1) == e; ++tries)
+        if (tries > (1u << 28)) __trap();               // never hang the GPU
+    }
+    __threadfence();
+  }
+  __syncthreads();
+  if (tid == 0) DFX_TL(53);                            // barrier passed
+  // 4. every N tile's partials in ONE bulk copy (global -> smem; the barrier's acquire
+  // plus a cross-proxy fence order it after the other CTAs' stores), hidden vector,
+  // gates of this CTA's channels, scale
+  const int ntiles = D.nt;
+  if (tid == 0) {
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+    const uint32_t bytes = (uint32_t(ntiles) * N * Cr * 4 + 15) & ~15u;
+    mbar_arrive_expect_tx(gbar, bytes);
+    bulk_load(part, F.scratch, bytes, gbar);
+    mbar_wait(gbar, 0);
+  }
+  __syncthreads();
+  if (tid == 0) DFX_TL(54);                            // partials gathered
+  {                                                    // nparts threads per hidden unit
+    const int units = N * Cr;
+    const int np = max(1, min(8, nthr / units));
+    const int tlen = (ntiles + np - 1) / np;
+    for (int k = tid; k < units * np; k += nthr) {
+      const int u = k / np, pt = k - u * np;
+      const int n = u / Cr, j = u - n * Cr;
+      const int t0 = pt * tlen, t1 = min(ntiles, t0 + tlen);
+      float s = 0.0f;
+      for (int t = t0; t < t1; ++t) s += part[(t * N + n) * Cr + j];
+      red[k] = s;
+    }
+    __syncthreads();
+    for (int u = tid; u < units; u += nthr) {
+      const int n = u / Cr, j = u - n * Cr;
+      float s = 0.0f;
+      for (int pt = 0; pt < np; ++pt) s += red[u * np + pt];
+      hidden[u] = act_apply<kSp>(F.act1, s + (F.b1 ? F.b1[j] : 0.0f));
+    }
+  }
+  __syncthreads();
+  if (tid == 0) DFX_TL(55);                            // hidden
+  // fc2 rows of this CTA's channels: nparts threads per (image, channel) over
+  // contiguous j ranges, partials combined in part order (deterministic)
+  const int items = N * nch;
+  const int nparts = max(1, min(8, nthr / items));
+  const int jlen = (Cr + nparts - 1) / nparts;
+  for (int k = tid; k < items * nparts; k += nthr) {
+    const int it = k / nparts, part = k - it * nparts;
+    const int n = it / nch, c = it - n * nch;
+    const int row = c * Cr;
+    const int j0 = part * jlen, j1 = min(Cr, j0 + jlen);
+    float s = 0.0f;
+#pragma unroll 4
+    for (int j = j0; j < j1; ++j) {
+      float wv = Elt<T>::to_f(w2[row + j]);
+      if constexpr (kSp) wv += Elt<T>::to_f(w2[row + j + wlo]);
+      s = fmaf(wv, hidden[n * Cr + j], s);
+    }
+    red[k] = s;                                        // red[] is free since step 1
+  }
+  __syncthreads();
+  for (int k = tid; k < items; k += nthr) {
+    const int n = k / nch, c = k - n * nch;
+    float s = 0.0f;
+    for (int part = 0; part < nparts; ++part) s += red[k * nparts + part];
+    gate[k] = act_apply<kSp>(F.act2, s + (F.b2 ? F.b2[co_base + c] : 0.0f));
+  }
+  __syncthreads();
+  if (tid == 0) DFX_TL(56);                            // gates
+  for (int item = item0 + tid; item < total; item += nthr) {
+    const int cgi = item % cg;
+    int t = item / cg;
+    const int q = t % OW;
+    t /= OW;
+    const int p = t % OH;
+    const int n = t / OH;
+    const int c = cgi * 8;
+    const int64_t pix = (int64_t(n) * OH + p) * OW + q;
+    float x[8];
+    ld8<T>(ot, pix * nch + c, ot_lo, x);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) x[i] *= gate[n * nch + c + i];
+    stv8<T>(o, view_pixel_index(o, pix, co_base + c), x);
+  }
+  if (tid == 0) DFX_TL(57);                            // scaled output stored
 }
 
 template <typename T, int K, int S>
 DFX_DEV void dw_smem_k(const dfx_gemm_desc& D, const T* xs, int xp, int N, int P, int Q, int co_base,
-                       int nch, const dfx_view& o, const float* sw, int bn, int tid, int nthr) {
+                       int nch, const dfx_view& o, const float* sw, int bn, int tid, int nthr, uint8_t* se_smem,
+                       uint64_t* gbar) {
   switch (D.dw_act) {
-    case DFX_ACT_RELU: dw_smem_t<T, K, S, DFX_ACT_RELU>(D, xs, xp, N, P, Q, co_base, nch, o, sw, bn, tid, nthr); break;
+    case DFX_ACT_RELU: dw_smem_t<T, K, S, DFX_ACT_RELU>(D, xs, xp, N, P, Q, co_base, nch, o, sw, bn, tid, nthr, se_smem, gbar); break;
     case DFX_ACT_HARDSWISH:
-      dw_smem_t<T, K, S, DFX_ACT_HARDSWISH>(D, xs, xp, N, P, Q, co_base, nch, o, sw, bn, tid, nthr);
+      dw_smem_t<T, K, S, DFX_ACT_HARDSWISH>(D, xs, xp, N, P, Q, co_base, nch, o, sw, bn, tid, nthr, se_smem, gbar);
       break;
-    case DFX_ACT_SILU: dw_smem_t<T, K, S, DFX_ACT_SILU>(D, xs, xp, N, P, Q, co_base, nch, o, sw, bn, tid, nthr); break;
-    default: dw_smem_t<T, K, S, DFX_ACT_NONE>(D, xs, xp, N, P, Q, co_base, nch, o, sw, bn, tid, nthr); break;
+    case DFX_ACT_SILU: dw_smem_t<T, K, S, DFX_ACT_SILU>(D, xs, xp, N, P, Q, co_base, nch, o, sw, bn, tid, nthr, se_smem, gbar); break;
+    default: dw_smem_t<T, K, S, DFX_ACT_NONE>(D, xs, xp, N, P, Q, co_base, nch, o, sw, bn, tid, nthr, se_smem, gbar); break;
   }
 }
 
 // dispatch on the (host-validated) square kernel size / stride: 3 or 5, 1 or 2
 template <typename T>
 DFX_DEV void dw_smem(const dfx_gemm_desc& D, const T* xs, int xp, int N, int P, int Q, int co_base, int nch,
-                     const dfx_view& o, const float* sw, int bn, int tid, int nthr) {
+                     const dfx_view& o, const float* sw, int bn, int tid, int nthr, uint8_t* se_smem = nullptr,
+                     uint64_t* gbar = nullptr) {
   if (D.dw_k == 3) {
-    if (D.dw_s == 1) dw_smem_k<T, 3, 1>(D, xs, xp, N, P, Q, co_base, nch, o, sw, bn, tid, nthr);
-    else dw_smem_k<T, 3, 2>(D, xs, xp, N, P, Q, co_base, nch, o, sw, bn, tid, nthr);
+    if (D.dw_s == 1) dw_smem_k<T, 3, 1>(D, xs, xp, N, P, Q, co_base, nch, o, sw, bn, tid, nthr, se_smem, gbar);
+    else dw_smem_k<T, 3, 2>(D, xs, xp, N, P, Q, co_base, nch, o, sw, bn, tid, nthr, se_smem, gbar);
   } else {
-    if (D.dw_s == 1) dw_smem_k<T, 5, 1>(D, xs, xp, N, P, Q, co_base, nch, o, sw, bn, tid, nthr);
-    else dw_smem_k<T, 5, 2>(D, xs, xp, N, P, Q, co_base, nch, o, sw, bn, tid, nthr);
+    if (D.dw_s == 1) dw_smem_k<T, 5, 1>(D, xs, xp, N, P, Q, co_base, nch, o, sw, bn, tid, nthr, se_smem, gbar);
+    else dw_smem_k<T, 5, 2>(D, xs, xp, N, P, Q, co_base, nch, o, sw, bn, tid, nthr, se_smem, gbar);
   }
 }
 

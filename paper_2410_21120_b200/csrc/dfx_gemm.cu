@@ -401,6 +401,23 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           s_dw[kk * bn + i] = (D.dw_alpha && c < cout) ? D.dw_alpha[c] : 1.f;
           s_dw[kk * bn + bn + i] = (D.dw_beta && c < cout) ? D.dw_beta[c] : 0.f;
         }
+        if (D.se != nullptr && ti == 0) {
+          // fused SE: this CTA's rows of fc1^T and fc2 ([bn][Cr] each; split: hi then lo)
+          // are static -- bulk copies issued now land while the main loop runs
+          // (dfx_epi.cuh se_finish waits on ready[1]); rows are contiguous and 16-B
+          // multiples (host-checked: cout % 8 == 0, cr even)
+          const dfx_se_fuse& F = *D.se;
+          const int Cr = F.cr;
+          const int64_t cc = int64_t(F.c) * Cr;
+          const uint32_t bytes = uint32_t(min(bn, F.c - co_base)) * Cr * 2;
+          uint8_t* dst = reinterpret_cast<uint8_t*>(s_dw + (kk + 2) * bn);
+          mbar_arrive_expect_tx(&hdr->ready[1], bytes * 2 * planes);
+          for (int mat = 0; mat < 2 * planes; ++mat) {
+            const uint16_t* src = reinterpret_cast<const uint16_t*>(mat & 1 ? F.w2 : F.w1) +
+                                  (mat >> 1) * cc + int64_t(co_base) * Cr;
+            bulk_load(dst + int64_t(mat) * bn * Cr * 2, src, bytes, &hdr->ready[1]);
+          }
+        }
       }
     }
     if constexpr (!kSplitT<T>) if (D.pre_mode) {
@@ -515,6 +532,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   }
 
   if (D.dw_k > 0) {
+    if (threadIdx.x == 0) DFX_TL(48);                  // depthwise-epilogue drain starts
     // ---- depthwise epilogue: this CTA covers every M tile (host-checked), so the
     // drain parks its channels of the whole output map in the (now free) operand
     // slots -- the same epilogue and 16-bit rounding as a global store, through a
@@ -541,9 +559,13 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     if (pair) cluster_sync_all();
     else __syncthreads();                              // map complete; TMEM reads done
     if (warp == 2) tmem_dealloc(tmem_base, tmem_cols);
+    // fused SE (D.se): the depthwise outputs + reduction scratch follow the map
+    uint8_t* se_smem = D.se != nullptr
+                           ? slots + ((size_t(N) * P * Q * xp * 2 * planes + 15) & ~size_t(15))
+                           : nullptr;
     dw_smem<T>(D, xs, xp, N, P, Q, co_base, min(ncols, cout - co_base), o,
                reinterpret_cast<const float*>(slots + nslots * slot_bytes), bn, int(threadIdx.x),
-               int(blockDim.x));
+               int(blockDim.x), se_smem, &hdr->ready[0]);   // ready[0]: partials gather, ready[1]: SE weights
     if (pair) cluster_sync_all();                      // the peer finished reading this map
     return;
   }

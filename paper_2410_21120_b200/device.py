@@ -526,6 +526,13 @@ GEMM_DW_BN_PAIR = int(os.environ.get("DFX_GEMM_DW_BN_PAIR", "32"))
 # "nosplit": only where the GEMM alone would not split K (the fused launch never does);
 # "single": only where one 128-row M tile holds the map (no m2)
 GEMM_DW_MODE = os.environ.get("DFX_GEMM_DW_MODE", "all")
+# the squeeze-excitation after a fused depthwise conv absorbed too (dfx_epi.cuh
+# se_finish: one grid-wide barrier instead of an SE launch).  Measured slower
+# (EfficientNetV2-L batch 1 node sum 1.95 -> 2.02 ms fp16; 4-model DAG 2.17 -> 2.49 ms):
+# the barrier waits out the CTA skew (~3.5 us) and the partial-sum gather + hidden
+# vector run serialised after it, where the separate SE launch overlaps its prologue
+# with the GEMM's tail under PDL.  Off by default (DFX_GEMM_DW_SE=1: on, A/B)
+GEMM_DW_SE = os.environ.get("DFX_GEMM_DW_SE", "0") == "1"
 _DW_ACTS = (None, "relu", "hardswish", "silu")
 
 
@@ -566,15 +573,56 @@ def gemm_dw_pairs(prog: MemberProgram) -> dict[int, int]:
     return out
 
 
+def dw_se_pairs(prog: MemberProgram, dw_pairs: dict[int, int]) -> dict[int, int]:
+    """GEMM launch index -> the SE launch its depthwise epilogue can absorb: the SE
+    (with its channel_scale fused, apply = 1) reads the depthwise output and nothing
+    else does (dfx_gemm_desc.se, dfx_epi.cuh se_finish)."""
+    readers: dict[str, int] = {}
+    for L in prog.launches:
+        for v in (L.src, L.epi.other):
+            if v is not None:
+                readers[v] = readers.get(v, 0) + 1
+    by_index = {L.index: L for L in prog.launches}
+    out = {}
+    for gi, di in dw_pairs.items():
+        D = by_index[di]
+        S = by_index.get(di + 1)
+        if S is None or S.kind != SE or S.src != D.dst or not S.geom.get("apply") or readers.get(D.dst) != 1:
+            continue
+        if D.dst == prog.exit_value or S.geom["cr"] > 512 or S.geom["c"] != D.geom["cout"]:
+            continue
+        vo = prog.values[S.dst]
+        if vo.coff % 8 or prog.buffers[vo.buf].pitch % 8:
+            continue
+        out[gi] = S.index
+    return out
+
+
+def _dw_smem_need(n, h, w, oh, ow, bn, planes, se_cr=0, nt=0) -> int:
+    """Operand-slot bytes a depthwise-epilogue GEMM CTA needs after its main loop: the
+    GEMM output map, and with a fused SE (hidden width se_cr, nt channel tiles) the
+    depthwise-output tile + reduction scratch + gathered fc1 partials (dfx_api.cu
+    DFX_OP_GEMM, dfx_epi.cuh se_finish)."""
+    need = (n * h * w * (bn + 8) * 2 * planes + 15) & ~15
+    if se_cr:
+        need += (((n * oh * ow * bn * 2 * planes + 15) & ~15) + 256 * 16 * 4 +
+                 (4 * bn + 2 * ((se_cr + 3) & ~3) + nt * n * se_cr + 4) * 4)
+    return need
+
+
 def plan_member(prog: MemberProgram, n: int, sm_count: int = 148, cluster_ok: bool = False,
-                max_splits: int = 0) -> MemberPlan:
+                max_splits: int = 0, se_cta_limit: int = 0) -> MemberPlan:
     """Activation plan + GEMM tilings of one member at batch n.  ``cluster_ok``: the
-    DAG is small enough for cluster split-K (lower.SPLITK_MODE "auto")."""
+    DAG is small enough for cluster split-K (lower.SPLITK_MODE "auto").
+    ``se_cta_limit`` > 0: depthwise-epilogue GEMMs may absorb the SE after them when
+    their grid has at most this many CTAs (a fused SE meets at a grid-wide barrier:
+    the concurrent members' fused grids must fit the GPU together)."""
     ws = 0
     tilings = {}
     skip: set[int] = set()
     planes = planes_of(prog.precision)
     dw_pairs = gemm_dw_pairs(prog) if GEMM_DW else {}
+    se_pairs = dw_se_pairs(prog, dw_pairs) if GEMM_DW_SE and se_cta_limit and n <= 2 else {}
     for L in prog.launches:
         if L.kind != GEMM:
             continue
@@ -600,6 +648,28 @@ def plan_member(prog: MemberProgram, n: int, sm_count: int = 148, cluster_ok: bo
                 t = dict(t, bn=bn, nt=nt, splits=1, sps=t["stages"], csplit=0, m2=m2,
                          tiles=nt * (2 if pair else 1), dw=dw_pairs[L.index])
                 skip.add(dw_pairs[L.index])
+                si = se_pairs.get(L.index)
+                if si is not None and not m2:
+                    # fused SE: the grid meets at one barrier -- widen the channel tile
+                    # until it fits its share of the SMs (and the tile fits smem)
+                    D = next(x for x in prog.launches if x.index == t["dw"])
+                    S = next(x for x in prog.launches if x.index == si)
+                    dv, cr = prog.values[D.dst], S.geom["cr"]
+                    for bn2 in sorted({bn, 64, 128}):
+                        if bn2 < bn:
+                            continue
+                        nt2 = -(-L.geom["cout"] // bn2)
+                        tiles2 = nt2 * (2 if pair else 1)
+                        slot = (128 * 64 * 2 + bn2 * 128) * planes
+                        extra = ((D.geom["kh"] ** 2 + 2) * bn2 * 4 +         # taps + BN vectors
+                                 2 * planes * bn2 * cr * 2)                  # staged fc1^T / fc2 rows
+                        nsl2 = min(gemm_slots(bn2, tiles2, sm_count, 0, planes),
+                                   (GEMM_SMEM_LIMIT - GEMM_SMEM_FIXED - extra) // slot)
+                        need = _dw_smem_need(n, out.h, out.w, dv.h, dv.w, bn2, planes, cr, nt2)
+                        if tiles2 <= se_cta_limit and nsl2 >= 2 and need <= nsl2 * slot:
+                            t = dict(t, bn=bn2, nt=nt2, tiles=tiles2, se=si, nslots=nsl2, se_cr=cr)
+                            skip.add(si)
+                            break
         tilings[L.index] = t
         if t["splits"] > 1 and not t["csplit"]:      # cluster split-K needs no workspace
             ws = max(ws, t["splits"] * n * out.h * out.w * t["nt"] * t["bn"] * 4)
@@ -611,10 +681,11 @@ def plan_member(prog: MemberProgram, n: int, sm_count: int = 148, cluster_ok: bo
     first = {b.bid: b.first for b in prog.buffers}
     by_index = {L.index: L for L in prog.launches}
     for gi, t in tilings.items():
-        if t.get("dw") is not None:
-            D = by_index[t["dw"]]
-            ob = prog.values[D.dst].buf
-            first[ob] = min(first[ob], gi)
+        for role in ("dw", "se"):              # absorbed launches write at the GEMM's index
+            if t.get(role) is not None:
+                D = by_index[t[role]]
+                ob = prog.values[D.dst].buf
+                first[ob] = min(first[ob], gi)
     ivs = [LiveInterval(str(b.bid).zfill(6), b.bytes_for(n), first[b.bid], b.last)
            for b in prog.buffers]
     places = first_fit(ivs, align=ALIGN)
@@ -647,7 +718,12 @@ class ExecInstance:
                    for p, n in zip(progs, batch)]
             crit = est.index(max(est))
             caps = [0 if i == crit else SLACK_SPLIT_MAX for i in range(len(progs))]
-        self.plans = [plan_member(p, n, dag.sm_count, cluster_ok, caps[i]) if n > 0 else MemberPlan([], 0, 0, {})
+        # fused SE grids meet at a grid-wide barrier: the members that may run one at the
+        # same time share the SMs (concurrent mode; sequential members never overlap)
+        se_members = sum(1 for p, n in zip(progs, batch) if 0 < n <= 2 and any(L.kind == SE for L in p.launches))
+        se_limit = (dag.sm_count if dag.mode == "sequential" else dag.sm_count // max(se_members, 1))
+        self.plans = [plan_member(p, n, dag.sm_count, cluster_ok, caps[i], se_limit) if n > 0
+                      else MemberPlan([], 0, 0, {})
                       for i, (p, n) in enumerate(zip(progs, batch))]
         seq = dag.mode == "sequential"
         # activation arena: disjoint member segments (concurrent) or overlaid (sequential)
@@ -676,11 +752,22 @@ class ExecInstance:
         self._ctr_used = 0
         self.desc_capacity = 2 * max(n_gemm, 1)       # room for the grouped launches' copies
         self.descs = rt.malloc(self.desc_capacity * C.sizeof(rt.GemmDesc))
+        # fused SE (dfx_se_fuse per absorbing GEMM): descriptors, fc1 partial scratch,
+        # barrier words (zeroed once; the barrier leaves them reusable)
+        self.se_count = sum(1 for pl in self.plans for t in pl.tilings.values() if t.get("se") is not None)
+        self.se_scratch_bytes = sum(_align(t["nt"] * n * 512 * 4) for pl, n in zip(self.plans, batch)
+                                    for t in pl.tilings.values() if t.get("se") is not None)
+        self.se_structs = rt.malloc(max(self.se_count, 1) * C.sizeof(rt.SeFuse))
+        self.se_sync = rt.malloc(max(self.se_count, 1) * 16)
+        self.se_scratch = rt.malloc(max(self.se_scratch_bytes, 16))
+        self._se_host: list = []
+        self._se_scratch_used = 0
         self.dev_in = rt.malloc(max(self.in_bytes, 16))
         self.dev_out = rt.malloc(max(self.out_bytes, 16))
         self.host_in = rt.host_alloc(max(self.in_bytes, 16))
         self.host_out = rt.host_alloc(max(self.out_bytes, 16))
         rt.memset(self.act, 0, self.act_bytes, self.stream)
+        rt.memset(self.se_sync, 0, max(self.se_count, 1) * 16, self.stream)
         rt.memset(self.counters, 0, max(4 * n_ctr, 16), self.stream)
         self.gemm_count = 0
         self.kernel_nodes = 0
@@ -799,6 +886,10 @@ class ExecInstance:
         if NODE_PRIORITY and self.dag.mode == "concurrent" and max(self.batch) <= PRIORITY_MAX_BATCH:
             self._prioritise(g)
         self._keep = [p for _, p, _ in self.nodes]
+        if self._se_host:
+            arr = (rt.SeFuse * len(self._se_host))(*self._se_host)
+            rt.h2d(self.se_structs, C.addressof(arr), C.sizeof(arr), self.stream)
+            rt.stream_sync(self.stream)
         if host_descs:
             assert len(host_descs) <= self.desc_capacity
             arr = (rt.GemmDesc * len(host_descs))(*host_descs)
@@ -1009,6 +1100,22 @@ class ExecInstance:
                 d.dw_beta = arena.addr(m, D.blobs["beta"]) if "beta" in D.blobs else None
                 d.dw_k, d.dw_s, d.dw_pad = dg["kh"], dg["sh"], dg["ph"]
                 d.dw_act = rt.ACT[D.epi.act1]
+                if t.get("se") is not None:  # the SE after it too: `out` is the SE's output
+                    S = next(x for x in prog.launches if x.index == t["se"])
+                    sg = S.geom
+                    d.out = self._view(m, prog, S.dst, n)
+                    addr = (lambda r: arena.addr(m, S.blobs[r]) if r in S.blobs else None)
+                    k = len(self._se_host)
+                    f = rt.SeFuse()
+                    f.w1, f.b1, f.w2, f.b2 = addr("w1"), addr("b1"), addr("w2"), addr("b2")
+                    f.scratch = self.se_scratch + self._se_scratch_used
+                    self._se_scratch_used += _align(t["nt"] * n * 512 * 4)
+                    f.sync = self.se_sync + 16 * k
+                    f.c, f.cr = sg["c"], sg["cr"]
+                    f.act1, f.act2 = rt.ACT[sg["act1"]], rt.ACT[sg["act2"]]
+                    f.ctas = t["tiles"]
+                    self._se_host.append(f)
+                    d.se = self.se_structs + k * C.sizeof(rt.SeFuse)
             epi = self._epi(m, prog, L, n)
             if geo.get("tokens") and epi.binop:
                 epi.other = _fold_rows(epi.other)
@@ -1035,9 +1142,10 @@ class ExecInstance:
             planes = planes_of(prog.precision)
             slot_bytes = (128 * 64 * 2 + t["bn"] * 128) * planes     # dfx_common.cuh gemm_slot_bytes
             gl = rt.GemmLaunch(self.descs + slot * C.sizeof(rt.GemmDesc), 1, t["tiles"], t["bn"],
-                               self.dtype, gemm_slots(t["bn"], t["tiles"], self.dag.sm_count,
-                                                      t.get("m2", 0), planes))
+                               self.dtype, t.get("nslots") or gemm_slots(t["bn"], t["tiles"], self.dag.sm_count,
+                                                                         t.get("m2", 0), planes))
             gl.m2 = t.get("m2", 0)
+            gl.se_cr = t.get("se_cr", 0)
             if csplit:
                 gl.flags |= 8                # cluster split-K (DSMEM reduction, no splitk node)
                 need = 128 * (t["bn"] + 4) * 4          # the fp32 partial tile parks in the slots
@@ -1192,7 +1300,8 @@ class ExecInstance:
 
     def free(self):
         self.graph.destroy()
-        for p in (self.act, self.ws, self.counters, self.descs, self.dev_in, self.dev_out):
+        for p in (self.act, self.ws, self.counters, self.descs, self.dev_in, self.dev_out,
+                  self.se_structs, self.se_sync, self.se_scratch):
             rt.free(p)
         rt.host_free(self.host_in)
         rt.host_free(self.host_out)

@@ -25,7 +25,7 @@ ACT = {None: 0, "relu": 1, "hardswish": 2, "hardsigmoid": 3, "silu": 4, "sigmoid
 BIN_NONE, BIN_ADD, BIN_SCALE = 0, 1, 2
 DT_BF16, DT_F16, DT_BF16X2, DT_F16X2 = 0, 1, 2, 3
 DTYPES = {"bf16": DT_BF16, "fp16": DT_F16, "bf16x2": DT_BF16X2, "fp16x2": DT_F16X2}
-ABI_VERSION = 4
+ABI_VERSION = 5
 
 i32, i64, u64, vp, u8 = C.c_int32, C.c_int64, C.c_uint64, C.c_void_p, C.c_uint8
 fptr = C.POINTER(C.c_float)
@@ -54,12 +54,17 @@ class GemmDesc(C.Structure):
                 ("pre_scale", vp), ("pre_shift", vp), ("pre_mode", i32), ("pre_act", i32),
                 ("pre_cin", i32), ("pre_pitch", i32), ("dw_w", vp), ("dw_alpha", vp),
                 ("dw_beta", vp), ("dw_k", i32), ("dw_s", i32), ("dw_pad", i32), ("dw_act", i32),
-                ("_pad2", u8 * 8)]
+                ("se", vp)]
+
+
+class SeFuse(C.Structure):
+    _fields_ = [("w1", vp), ("b1", vp), ("w2", vp), ("b2", vp), ("scratch", vp), ("sync", vp),
+                ("c", i32), ("cr", i32), ("act1", i32), ("act2", i32), ("ctas", i32), ("_pad", i32 * 3)]
 
 
 class GemmLaunch(C.Structure):
     _fields_ = [("descs", vp), ("ndesc", i32), ("total_tiles", i32), ("bn_max", i32),
-                ("dtype", i32), ("nslots", i32), ("flags", i32), ("m2", i32), ("_pad", i32 * 7),
+                ("dtype", i32), ("nslots", i32), ("flags", i32), ("m2", i32), ("se_cr", i32), ("_pad", i32 * 6),
                 ("desc0", GemmDesc)]
 
 
@@ -129,6 +134,7 @@ STRUCTS = {
     "dfx_gap_params": GapParams, "dfx_ew_params": EwParams, "dfx_in_params": InParams,
     "dfx_out_params": OutParams, "dfx_se_params": SeParams, "dfx_ln_params": LnParams,
     "dfx_tokens_params": TokensParams, "dfx_attn_params": AttnParams, "dfx_dwse_params": DwseParams,
+    "dfx_se_fuse": SeFuse,
 }
 OP_PARAMS = {OP_GEMM: GemmLaunch, OP_SPLITK: SplitKParams, OP_DWCONV: DwconvParams,
              OP_POOL: PoolParams, OP_GAP: GapParams, OP_EW: EwParams, OP_IN: InParams,
