@@ -145,14 +145,18 @@ DFX_DEV void drain_rows_direct_t(uint32_t taddr, int ncols, int64_t pix, int img
   const void* const xbase = e.other.base;
   const int64_t xrow = binop == DFX_BIN_ADD ? pix * e.other.pitch + e.other.coff
                                             : int64_t(img) * e.other.pitch + e.other.coff;
-  if (ws == nullptr && views_vec && co_base + ncols <= cout &&
+  // (cout - co_base) % 8 == 0: every chunk is 16 channels but possibly the tile's last,
+  // which then holds exactly 8 (cout = 8 mod 16: 24, 40, 72, 120 ... channels)
+  if (ws == nullptr && views_vec && ((cout - co_base) & 7) == 0 &&
       (binop == DFX_BIN_NONE || binop == DFX_BIN_ADD) &&
       act2 == DFX_ACT_NONE && (alpha == nullptr || beta != nullptr)) {
     const bool res = binop == DFX_BIN_ADD;
     // the common conv epilogue (bias / folded-BN shift, one activation, 16-B stores)
     // as a branch-free loop: per-chunk checks and reconvergence points were a
-    // third of its instructions
-    for (int c0 = c_first; c0 < ncols; c0 += c_step) {
+    // third of its instructions.  Full 16-channel chunks first; a final chunk with
+    // 8 valid channels (cout = 8 mod 16) after the loop
+    const int nfull = min(ncols, (cout - co_base) & ~15);
+    auto chunk = [&](int c0, bool half) {
       uint32_t r[16];
       tmem_ld16_acc<T>(taddr + uint32_t(c0), lo_cols, r);
       float v[16];
@@ -182,14 +186,17 @@ DFX_DEV void drain_rows_direct_t(uint32_t taddr, int ncols, int64_t pix, int img
         if (res) {                                  // residual add (ResNet / MBConv projections)
           float x[16];
           ld8<T>(xbase, xrow + co, xlo, x);
-          ld8<T>(xbase, xrow + co + 8, xlo, x + 8);
+          if (!half) ld8<T>(xbase, xrow + co + 8, xlo, x + 8);
 #pragma unroll
           for (int i = 0; i < 16; ++i) v[i] += x[i];
         }
         st8<T>(obase, orow + co, olo, v);
-        st8<T>(obase, orow + co + 8, olo, v + 8);
+        if (!half) st8<T>(obase, orow + co + 8, olo, v + 8);
       }
-    }
+    };
+    int c0 = c_first;
+    for (; c0 < nfull; c0 += c_step) chunk(c0, false);
+    if (c0 < ncols) chunk(c0, true);
     return;
   }
   for (int c0 = c_first; c0 < ncols; c0 += c_step) {
@@ -244,6 +251,11 @@ DFX_DEV void drain_rows_direct_t(uint32_t taddr, int ncols, int64_t pix, int img
       }
       st8<T>(obase, orow + co, olo, v);
       st8<T>(obase, orow + co + 8, olo, v + 8);
+    } else if (views_vec && co + 8 == cout) {
+      // the last 8 channels of a cout = 8 (mod 16) layer (MobileNetV3 / EfficientNetV2:
+      // 24, 40, 72, 120, 184, 200 ...): one vector epilogue, not the scalar tail
+      epilogue8<T>(e, v, pix, img, co);
+      st8<T>(obase, orow + co, olo, v);
     } else {
       float tail[16];
 #pragma unroll
