@@ -237,7 +237,8 @@ int config_for(int op, const void* params, size_t size, LaunchCfg* c) {
         const int per_sm = (p->bn_max <= 64 && !p->desc0.pre_mode) ? 2 : 1;   // pre_mode: 2 groups
         const int groups = 3 - per_sm;
         c->smem = dfx::gemm_smem_bytes(p->bn_max, p->nslots, 0, planes) + 1024 +
-                  ((p->flags & 4) ? 4 * groups * dfx::kEpiStageWarpBytes : 0);
+                  ((p->flags & 4) ? 8 * dfx::kEpiStageWarpBytes : 0) +
+                  (p->desc0.cout <= dfx::kPersistVecMax ? 2 * ((p->desc0.cout + 15) & ~15) * 4 : 0);
         c->grid = dim3(unsigned(std::min<int64_t>(p->total_tiles, int64_t(per_sm) * g_sm_count)));
         c->block = dim3(64 + 128 * groups);
       } else {

@@ -552,6 +552,7 @@ constexpr int kStageABytes = 128 * 64 * 2;   // 128 rows x 64 16-bit
 constexpr int kHeaderBytes = 1024;           // barriers + staged descriptor
 constexpr int kEpiBytes = 2048;              // alpha[256] + beta[256] fp32, staged
 constexpr int kSlotsOffset = kHeaderBytes + kEpiBytes;   // 1024-B aligned
+constexpr int kPersistVecMax = 1024;         // persistent GEMM: epilogue vectors staged up to this cout
 
 // one pipeline slot: A of 1 (or 2, m2) M tiles of 128 rows x 64 K, then B of bn rows x 64 K;
 // split precision (`planes` 2): A hi tiles, A lo tiles, B hi, B lo

@@ -217,12 +217,26 @@ __global__ void __launch_bounds__(kPersistThreads, 1)
     }
   } else {
     // ================= epilogue warps 2..9: TMEM lane quadrant (warp % 4)
+    // the folded-BN / bias vectors (static) staged in smem before the dependency: the
+    // drain's per-chunk vector loads were its long-scoreboard stalls from L1/L2
+    dfx_epilogue e = D.epi;
+    if (D.cout <= kPersistVecMax && (e.alpha || e.beta)) {
+      float* s_vec = reinterpret_cast<float*>(slots + nslots * slot_bytes +
+                                              ((L.flags & 4) ? 8 * kEpiStageWarpBytes : 0));
+      const int cp = (D.cout + 15) & ~15, ti = int(threadIdx.x) - 64, ne = int(blockDim.x) - 64;
+      for (int i = ti; i < cp; i += ne) {
+        if (e.alpha) s_vec[i] = i < D.cout ? e.alpha[i] : 0.f;
+        if (e.beta) s_vec[cp + i] = i < D.cout ? e.beta[i] : 0.f;
+      }
+      named_bar_sync(2, ne);
+      if (e.alpha) e.alpha = s_vec;
+      if (e.beta) e.beta = s_vec + cp;
+    }
     griddep_wait();                                   // residual operands / output of predecessors
     const int quad = warp & 3;
     const int row = quad * 32 + lane;                 // tile row == TMEM lane
     const int qi = row % tq, pi_ = (row / tq) % tp, ni = row / (tq * tp);
     const dfx_view o = D.out;
-    const dfx_epilogue e = D.epi;
     const int P = D.p, Q = D.q, N = D.n, cout = D.cout;
     const bool views_vec = vec8_ok(o, 0) && (e.binop == DFX_BIN_NONE || vec8_ok(e.other, 0));
     const uint32_t lane_addr = tmem_base + (uint32_t(quad * 32) << 16);

@@ -1156,7 +1156,8 @@ class ExecInstance:
                 # bn > 64: one CTA per SM, as deep a ring as smem allows; bn <= 64: two
                 # CTAs per SM (dfx_api.cu), 4 slots each
                 if t["bn"] > 64:
-                    gl.nslots = max(2, min(8, (GEMM_SMEM_LIMIT - GEMM_SMEM_FIXED
+                    vec = 2 * ((geo["cout"] + 15) // 16 * 16) * 4 if geo["cout"] <= 1024 else 0
+                    gl.nslots = max(2, min(8, (GEMM_SMEM_LIMIT - GEMM_SMEM_FIXED - vec
                                                - (8 * 2560 if GEMM_DRAIN_STAGED else 0))
                                            // slot_bytes))
                 else:
