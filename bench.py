@@ -349,6 +349,7 @@ def secondary_configs(args, rt, members, programs, arena, flush, P, local_rank):
     # swap-in from disk: the reference's FIWT files -> parse ->
     # lower + pack -> upload, vs one packed-arena file -> pinned read -> ONE H2D
     out["swap_from_disk"] = swap_from_disk(args, members)
+    out["member_swap"] = member_swaps(args)
     # configs[4]: 8-model fused DAG with mixed per-member batches
     from paper_2410_21120_b200 import zoo
     names = list(zoo.EIGHT_MODEL)
@@ -425,6 +426,40 @@ def accuracy_modes(args, models, flush, P, local_rank, modes=("fp16x2", "bf16x2"
                      "north_star_statistic": f"profiles/r02/parity_{{0,1,2}}_{prec}.json"}
         fuse.unload(dag)
     return out
+
+
+def member_swaps(args):
+    """swap_subgraph on the resident 4-model DAG (the measured replacement of the
+    reference's simulate_swap, costmodel.py:308-338): each member in turn replaced by
+    ResNet-50 and swapped back.  Per swap: the device work (one allocation from the
+    arena pool, D2D of the untouched members, ONE H2D of the incoming segment from
+    its pinned image) and the whole call (validation, profile of the incoming member,
+    DAG rebuild); incoming programs are lowered and pinned once beforehand."""
+    from paper_2410_21120_b200 import fuse, zoo
+    from paper_2410_21120_b200.device import program_for, stage_segment
+    models = build_models(args.models)
+    incoming = zoo.build("resnet50")
+    for g, w in models + [incoming]:
+        stage_segment(program_for(g, w, args.precision))
+    dag = fuse.fuse_models(models)
+    fuse.load_fused(dag, precision=args.precision)
+    rows = []
+    for (g, w) in models:
+        for out_id, inc in ((g.model_id, incoming), (incoming[0].model_id, (g, w))):
+            t0 = time.perf_counter()
+            new = fuse.swap_subgraph(dag, out_id, inc)
+            wall = (time.perf_counter() - t0) * 1e3
+            ls = fuse.device_image(new).last_swap
+            fuse.unload(dag)
+            dag = new
+            rows.append({"out": out_id, "in": inc[0].model_id, "segment_mb": ls["bytes"] / 1e6,
+                         "device_ms": ls["ms"], "malloc_ms": ls["malloc_ms"], "d2d_ms": ls["d2d_ms"],
+                         "h2d_ms": ls["memcpy_ms"], "call_ms": wall})
+    fuse.unload(dag)
+    return {"config": "each north-star member swapped out for ResNet-50 and back on the loaded DAG",
+            "precision": args.precision, "swaps": rows,
+            "device_ms_median": float(np.median([r["device_ms"] for r in rows])),
+            "call_ms_median": float(np.median([r["call_ms"] for r in rows]))}
 
 
 def swap_from_disk(args, members):
