@@ -45,19 +45,22 @@ _cache_lock = threading.Lock()
 
 
 def program_for(g, w, precision: str = "fp16") -> MemberProgram:
-    """Lowered program of (graph, weights, precision), cached by object identity
-    for as long as both objects live (weak references + finalizers: the cache
-    never keeps a graph, a weight store or its packed 16-bit blobs alive)."""
-    key = (id(g), id(w), precision)
+    """Lowered program of (graph, weights, precision), cached for as long as the
+    weight store lives (weak reference + finalizer: the cache never keeps a weight
+    store or its packed 16-bit blobs alive).  The key is the weight store's identity
+    plus the graph's identity-free fingerprint (model id, entry, exit, node count),
+    so a model's ModelGraph and the SubGraph fuse_models made of it -- the same
+    immutable structure over the same weights -- share one program (a swap brings
+    in a member whose program, and pinned segment, were prepared beforehand)."""
+    key = (id(w), g.model_id, g.entry, g.exit, len(g.nodes), precision)
     with _cache_lock:
         hit = _program_cache.get(key)
-        if hit is not None and hit[0]() is g and hit[1]() is w:
+        if hit is not None and hit[1]() is w:
             return hit[2]
     prog = lower_member(g, w, precision=precision)
     with _cache_lock:
-        _program_cache[key] = (weakref.ref(g), weakref.ref(w), prog)
-    for obj in (g, w):
-        weakref.finalize(obj, _program_cache.pop, key, None).atexit = False
+        _program_cache[key] = (None, weakref.ref(w), prog)
+    weakref.finalize(w, _program_cache.pop, key, None).atexit = False
     return prog
 
 
