@@ -266,7 +266,8 @@ typedef struct dfx_out_params {
  * apply = 0: out = gate (n, 1, 1, c);  apply = 1: out = x * gate (n, h, w, c), i.e. the
  * following channel_scale is fused (each cluster CTA scales its channel slice).
  * apply bit 1 (value 2): read the FC weights from global memory instead of staging
- * each CTA's slice in shared memory (large batches).
+ * each CTA's slice in shared memory (large batches); with bit 2 (value 4) as well,
+ * stage only the fc1 slices (split-precision slices of both FCs beyond the budget).
  * w1 [cr][c], w2 [c][cr]: 16-bit, dtype of the views, row-major. */
 typedef struct dfx_se_params {
   dfx_view in;                         /* x (n, h, w, c) */

@@ -397,7 +397,8 @@ int config_for(int op, const void* params, size_t size, LaunchCfg* c) {
       if (split) cl = 16;
       c->func = se_func(p->in.dtype, cl, ipi);
       c->grid = dim3(unsigned(cl), unsigned((p->in.n + ipi - 1) / ipi));
-      c->smem = (p->apply & 2) ? 0 : size_t(dfx::se_smem_bytes(p->in.c, p->cr, cl)) * (split ? 2 : 1);
+      c->smem = (p->apply & 2) ? ((p->apply & 4) ? size_t(dfx::se_smem_bytes(p->in.c, p->cr, cl)) / 2 * (split ? 2 : 1) : 0)
+                               : size_t(dfx::se_smem_bytes(p->in.c, p->cr, cl)) * (split ? 2 : 1);
       // room for the CTA's x slice (latency-bound small batches): the scale reads smem
       // (batch 1: EfficientNetV2-L 2.10 -> 2.08 ms; at batch 32 it costs occupancy)
       static const int xt_batch = getenv("DFX_SE_XTILE_BATCH") ? atoi(getenv("DFX_SE_XTILE_BATCH")) : 8;

@@ -87,13 +87,19 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kSeThreads)
   // 16-B aligned slices are staged in smem unless apply bit 1 says otherwise (large
   // batches: clusters of smem-heavy CTAs then cannot be co-scheduled, while the
   // weights are L2-resident and shared by every image's cluster anyway)
-  const bool staged = (C & 7) == 0 && (Cr & 7) == 0 && !(P.apply & 2);
+  const bool aligned = (C & 7) == 0 && (Cr & 7) == 0;
+  const bool staged = aligned && !(P.apply & 2);
+  // apply bit 2 (split precision, slices beyond the smem budget): stage the fc1
+  // slices only, fc2 rows read from L2 (fc1's per-k loads were the phase's cost)
+  const bool staged1 = staged || (aligned && (P.apply & 4));
   const bool apply = P.apply & 1;
   const int sb = ((cs * Cr * 2) + 15) & ~15;
   // split precision: FC weights [hi C x Cr][lo C x Cr]; staged, the lo slices follow
-  // the two hi slices in smem (w1_lo at +2 sb bytes, w2_lo at +3 sb)
-  const int64_t wlo = !kSplitT<T> ? 0 : staged ? int64_t(sb) : int64_t(C) * Cr;   // elements
-  const T* w1 = staged ? reinterpret_cast<const T*>(wsm) : w1g + int64_t(c_lo) * Cr;
+  // the two hi slices in smem (w1_lo at +2 sb bytes, w2_lo at +3 sb); fc1 only:
+  // [w1 hi][w1 lo]
+  const int64_t wlo = !kSplitT<T> ? 0 : staged ? int64_t(sb) : int64_t(C) * Cr;   // w2, elements
+  const int64_t wlo1 = !kSplitT<T> ? 0 : staged ? int64_t(sb) : staged1 ? int64_t(sb / 2) : int64_t(C) * Cr;
+  const T* w1 = staged1 ? reinterpret_cast<const T*>(wsm) : w1g + int64_t(c_lo) * Cr;
   const T* w2 = staged ? reinterpret_cast<const T*>(wsm + sb) : w2g + int64_t(c_lo) * Cr;
 
   // ---- 0. weight slices -> smem, before the dependency resolves
@@ -110,6 +116,11 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kSeThreads)
         bulk_load(wsm + 2 * sb, w1g + int64_t(C) * Cr + int64_t(c_lo) * Cr, bytes, &wbar);
         bulk_load(wsm + 3 * sb, w2g + int64_t(C) * Cr + int64_t(c_lo) * Cr, bytes, &wbar);
       }
+    } else if (staged1 && bytes) {
+      mbar_arrive_expect_tx(&wbar, (kSplitT<T> ? 2 : 1) * bytes);
+      bulk_load(wsm, w1g + int64_t(c_lo) * Cr, bytes, &wbar);
+      if constexpr (kSplitT<T>)
+        bulk_load(wsm + sb, w1g + int64_t(C) * Cr + int64_t(c_lo) * Cr, bytes, &wbar);
     }
   }
   griddep_wait();
@@ -121,7 +132,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kSeThreads)
   // a second L2 round trip (dfx_api.cu DFX_OP_SE)
   uint32_t dsm;
   asm("mov.u32 %0, %%dynamic_smem_size;" : "=r"(dsm));
-  const int wbytes = staged ? (kSplitT<T> ? 4 : 2) * sb : 0;
+  const int wbytes = staged ? (kSplitT<T> ? 4 : 2) * sb : staged1 ? (kSplitT<T> ? 2 : 1) * sb : 0;
   T* xt = reinterpret_cast<T*>(wsm + wbytes);
   constexpr int kPl = kSplitT<T> ? 2 : 1;            // split: the lo tile follows the hi one
   const bool cache_x = apply && IPI == 1 && ((in.coff | out_coff_of(P) | c_lo | nch) & 7) == 0 &&
@@ -220,7 +231,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kSeThreads)
   __syncthreads();                                    // red[] reused by the next image
   }
   if (threadIdx.x == 0) DFX_TL(2);
-  if (threadIdx.x == 0 && staged && nch * Cr > 0) mbar_wait(&wbar, 0);   // weight slices landed (one poller)
+  if (threadIdx.x == 0 && staged1 && nch * Cr > 0) mbar_wait(&wbar, 0);  // weight slices landed (one poller)
   __syncthreads();
   if (threadIdx.x == 0) DFX_TL(3);
 
@@ -238,7 +249,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kSeThreads)
       for (int i = 0; i < IPI; ++i) sa[i] = 0.f;
       for (int k = k0; k < k1; ++k) {
         float wv = Elt<T>::to_f(w1[int64_t(k) * Cr + j]);           // one load, IPI images
-        if constexpr (kSplitT<T>) wv += Elt<T>::to_f(w1[int64_t(k) * Cr + j + wlo]);
+        if constexpr (kSplitT<T>) wv += Elt<T>::to_f(w1[int64_t(k) * Cr + j + wlo1]);
 #pragma unroll
         for (int i = 0; i < IPI; ++i) sa[i] = fmaf(wv, pooled[i][k], sa[i]);
       }

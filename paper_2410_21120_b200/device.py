@@ -1211,7 +1211,7 @@ class ExecInstance:
             yield rt.OP_SE, rt.SeParams(src, self._view(m, prog, L.dst, n), addr("w1"), addr("b1"),
                                         addr("w2"), addr("b2"), geo["cr"], rt.ACT[geo["act1"]],
                                         rt.ACT[geo["act2"]],
-                                        geo.get("apply", 0) | (2 if self._se_unstaged(prog, geo, n) else 0))
+                                        geo.get("apply", 0) | self._se_unstaged(prog, geo, n))
         elif L.kind == DWSE:
             geo = L.geom
             addr = (lambda r: arena.addr(m, L.blobs[r]) if r in L.blobs else None)
@@ -1225,14 +1225,19 @@ class ExecInstance:
             raise AssertionError(L.kind)
 
     @staticmethod
-    def _se_unstaged(prog, geo, n) -> bool:
-        """SE FC weights read from L2 instead of staged per CTA: large batches (the
-        clusters of smem-heavy CTAs could not be co-scheduled), or slices (hi + lo
-        for split precision) beyond the cluster kernel's smem budget
-        (dfx_common.cuh se_smem_bytes, kSeSmemBudget)."""
+    def _se_unstaged(prog, geo, n) -> int:
+        """se_params.apply bits for the FC weights: 2 = read from L2 instead of staged
+        per CTA (large batches: the clusters of smem-heavy CTAs could not be
+        co-scheduled), 2|4 = stage only the fc1 slices (split precision, hi + lo
+        slices of both FCs beyond the cluster kernel's smem budget,
+        dfx_common.cuh se_smem_bytes / kSeSmemBudget)."""
+        if n >= SE_UNSTAGED_BATCH:
+            return 2
         cs = -(-geo["c"] // 128) * 8
-        need = 2 * ((cs * geo["cr"] * 2 + 15) & ~15) * planes_of(prog.precision)
-        return n >= SE_UNSTAGED_BATCH or need > 190 * 1024
+        one = ((cs * geo["cr"] * 2 + 15) & ~15) * planes_of(prog.precision)
+        if 2 * one <= 190 * 1024:
+            return 0
+        return 2 | 4 if one <= 190 * 1024 else 2
 
     # --- execution
     def stage_inputs(self, xs) -> None:

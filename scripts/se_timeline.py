@@ -13,6 +13,7 @@ from paper_2410_21120_b200.device import DeviceDag
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--cases", default="1344:56:14:1,2304:96:7:1,3840:160:7:1,960:240:7:1,1344:56:14:32")
+ap.add_argument("--precision", default="fp16")
 a = ap.parse_args()
 names = {0: "start", 1: "griddep", 2: "pooled", 3: "weights", 4: "fc1", 5: "cluster.sync",
          6: "hidden", 7: "gate+scale", 8: "final sync"}
@@ -29,7 +30,7 @@ for case in a.cases.split(","):
              O("e", "dense", {"units": c, "fan_in": cr}, {"weight": "f2"}, ("d",)),
              O("f", "sigmoid", inputs=("e",)), O("g", "channel_scale", inputs=("a", "f"))]
     g = graph_ir.ModelGraph("m", nodes, "a", "g", S((c, hw, hw)), S((c, hw, hw)))
-    d = DeviceDag([(g, st)])
+    d = DeviceDag([(g, st)], precision=a.precision)
     inst = d.acquire((n,))
     inst.upload_inputs([rng.standard_normal((n, c, hw, hw)).astype(np.float32)])
     se = [(op, p) for op, p, info in inst.nodes if op == rt.OP_SE][0]
@@ -46,5 +47,5 @@ for case in a.cases.split(","):
     buf = (C.c_ulonglong * 64)()
     rt.lib().dfx_debug_timeline_se(buf, 64)
     base = buf[0]
-    print(f"C={c} Cr={cr} hw={hw} n={n}: graph {ms * 1e3:.1f} us; CTA0: " +
+    print(f"{a.precision} C={c} Cr={cr} hw={hw} n={n}: graph {ms * 1e3:.1f} us; CTA0: " +
           ", ".join(f"{nm} +{(buf[i] - base) / 1e3:.2f}" for i, nm in names.items()), flush=True)
