@@ -343,6 +343,12 @@ int dfx_device_info(int device, int* sm_count, int* cc_major, int* cc_minor,
                     size_t* total_mem);
 int dfx_mem_info(size_t* free_bytes, size_t* total_bytes);
 
+/* NVTX ranges (header-only NVTX3: free unless a profiler is attached).  The library
+ * marks swap-in, graph instantiation and execution itself; the Python layer marks
+ * fuse_models / load_fused / swap_subgraph with these. */
+int dfx_nvtx_range_push(const char* msg);
+int dfx_nvtx_range_pop(void);
+
 /* ---- memory ------------------------------------------------------------ */
 int dfx_malloc(void** dptr, size_t bytes);
 int dfx_free(void* dptr);

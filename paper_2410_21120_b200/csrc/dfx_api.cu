@@ -16,6 +16,8 @@
 #include <thread>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>   // header-only NVTX3: ranges cost nothing without a tool attached
+
 #include "dfx_common.cuh"
 #include "dfx_epi.cuh"
 
@@ -50,6 +52,14 @@ template <typename T> __global__ void attn_kernel(const __grid_constant__ dfx_at
 #define DFX_PICK16(K, dt) \
   ((dt) == DFX_F16 ? reinterpret_cast<const void*>(&dfx::K<__half>) \
                    : reinterpret_cast<const void*>(&dfx::K<__nv_bfloat16>))
+
+namespace {
+// NVTX range for the lifetime of a scope (host side of the ABI entry points)
+struct NvtxRange {
+  explicit NvtxRange(const char* m) { nvtxRangePushA(m); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
+}  // namespace
 
 namespace {
 
@@ -682,7 +692,17 @@ int dfx_memcpy_d2d(void* dst, const void* src, size_t bytes, void* stream) {
   return DFX_OK;
 }
 
+int dfx_nvtx_range_push(const char* msg) {
+  nvtxRangePushA(msg ? msg : "dfx");
+  return DFX_OK;
+}
+int dfx_nvtx_range_pop(void) {
+  nvtxRangePop();
+  return DFX_OK;
+}
+
 int dfx_arena_upload(const void* pinned_host, size_t bytes, void** dev_arena, void* stream) {
+  NvtxRange r("dfx arena upload (swap-in)");
   int rc = dfx_malloc(dev_arena, bytes);
   if (rc) return rc;
   CK(cudaMemcpyAsync(*dev_arena, pinned_host, bytes, cudaMemcpyHostToDevice, S(stream)));
@@ -880,6 +900,7 @@ int dfx_graph_set_priority(void* graph, int node_id, int priority, int* range_ou
 }
 
 int dfx_graph_instantiate(void* graph) {
+  NvtxRange r("dfx graph instantiate");
   auto* g = static_cast<Graph*>(graph);
   if (!g) return fail(DFX_E_ARG, "null graph");
   if (g->exec) return DFX_OK;
@@ -889,6 +910,7 @@ int dfx_graph_instantiate(void* graph) {
 }
 
 int dfx_graph_launch(void* graph, void* stream) {
+  NvtxRange r("dfx fused DAG graph launch");
   auto* g = static_cast<Graph*>(graph);
   if (!g || !g->exec) return fail(DFX_E_STATE, "graph not instantiated");
   CK(cudaGraphLaunch(g->exec, S(stream)));
@@ -1020,6 +1042,7 @@ extern "C" {
 
 int dfx_execute_gather(void* graph, const void* const* srcs, const size_t* sizes, int nsrc, void* host_in,
                        void* dev_in, void* host_out, const void* dev_out, size_t out_bytes, void* stream) {
+  NvtxRange r("dfx execute_fused (gather, H2D, graph, D2H)");
   if (nsrc < 0 || (nsrc > 0 && (!srcs || !sizes)) || !host_in) return fail(DFX_E_ARG, "bad gather list");
   size_t total = 0;
   int nch = 0;

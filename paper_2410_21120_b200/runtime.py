@@ -150,7 +150,7 @@ EXPORTS = (
     "dfx_stream_sync", "dfx_event_create", "dfx_event_destroy", "dfx_event_record",
     "dfx_event_elapsed", "dfx_tmap_act", "dfx_tmap_weights", "dfx_launch", "dfx_graph_create",
     "dfx_graph_add", "dfx_graph_set_priority", "dfx_graph_instantiate", "dfx_graph_launch", "dfx_graph_node_count",
-    "dfx_graph_destroy", "dfx_execute", "dfx_execute_gather",
+    "dfx_graph_destroy", "dfx_execute", "dfx_execute_gather", "dfx_nvtx_range_push", "dfx_nvtx_range_pop",
 )
 
 _lock = threading.Lock()
@@ -367,3 +367,21 @@ def tmap_weights(base: int, rows: int, k: int, cb: int, bn: int, dtype: int):
     call("dfx_tmap_weights", buf, vp(base), C.c_int(rows), C.c_int(k), C.c_int(cb), C.c_int(bn),
          C.c_int(dtype))
     return buf
+
+
+class nvtx_range:
+    """``with rt.nvtx_range("fuse_models"):`` -- an NVTX range through libdfx (a no-op
+    unless a profiler is attached); silently absent when the library is not loaded."""
+
+    def __init__(self, msg: str):
+        self.msg = msg.encode()
+
+    def __enter__(self):
+        if _lib is not None:
+            _lib.dfx_nvtx_range_push(self.msg)
+        return self
+
+    def __exit__(self, *exc):
+        if _lib is not None:
+            _lib.dfx_nvtx_range_pop()
+        return False
