@@ -255,8 +255,8 @@ int config_for(int op, const void* params, size_t size, LaunchCfg* c) {
         c->smem = dfx::gemm_smem_bytes(p->bn_max, p->nslots, p->m2 ? 1 : 0, planes) + 1024;
         if (p->flags & 8) {             // cluster split-K: one cluster per output tile
           const int sp = p->desc0.splits;
-          if (p->m2 || p->ndesc != 1 || sp < 2 || sp > 8 || p->total_tiles % sp)
-            return fail(DFX_E_ARG, "gemm: cluster split-K needs one problem, no m2, 2..8 splits");
+          if (p->m2 || p->ndesc != 1 || sp < 2 || sp > 16 || p->total_tiles % sp)
+            return fail(DFX_E_ARG, "gemm: cluster split-K needs one problem, no m2, 2..16 splits");
           if (size_t(128) * (p->bn_max + 4) * 4 > size_t(p->nslots) * dfx::gemm_slot_bytes(p->bn_max, 0, planes))
             return fail(DFX_E_ARG, "gemm: cluster split-K partial tile exceeds the %d slots", p->nslots);
           c->cluster = unsigned(sp);
@@ -559,6 +559,8 @@ int dfx_init(int device) {
     CK(cudaFuncSetAttribute(DFX_PICK16(attn_kernel, dt), cudaFuncAttributeMaxDynamicSharedMemorySize,
                             dfx::attn_smem_bytes(dfx::kAttnMaxL)));
   }
+  for (int dt : {int(DFX_BF16X2), int(DFX_F16X2), int(DFX_BF16), int(DFX_F16)})   // 9..16-CTA split-K clusters
+    CK(cudaFuncSetAttribute(gemm_func(dt, 0), cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   for (int dt : {int(DFX_BF16X2), int(DFX_F16X2)}) {         // split precision
     CK(cudaFuncSetAttribute(gemm_func(dt, 0), cudaFuncAttributeMaxDynamicSharedMemorySize, kGemmSmemLimit));
     CK(cudaFuncSetAttribute(DFX_PICK(gemm_persist_kernel, dt), cudaFuncAttributeMaxDynamicSharedMemorySize,

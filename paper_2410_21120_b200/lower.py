@@ -928,7 +928,7 @@ def dwse_smem(c: int, cr: int, hwo: int) -> int:
 # transform warps and measured slower than the separate bandwidth-bound pass
 # (4-model batch 1 2.72 vs 2.52 ms, batch 32 17.1 vs 12.5 ms, 150 launches fewer)
 FOLD_PRE = os.environ.get("DFX_FOLD_PRE", "0") == "1"
-SPLITK_CLUSTER_MAX = 8
+SPLITK_CLUSTER_MAX = int(os.environ.get("DFX_SPLITK_CLUSTER_MAX", "16"))   # > 8: non-portable cluster sizes
 
 
 def gemm_tiling(geom: dict, n: int, p: int, q: int, sm_count: int = 148, cluster_ok: bool = False,
