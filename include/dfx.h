@@ -180,9 +180,14 @@ typedef struct dfx_se_fuse {
   const float* b2;                     /* may be NULL */
   float* scratch;                      /* [N tiles][n][cr] fp32 fc1 partial sums */
   uint32_t* sync;                      /* {arrivals, epoch}, zeroed once */
+  float* pooled;                       /* mode 1: [n][c] channel means out */
   int32_t c, cr, act1, act2;
   int32_t ctas;                        /* CTAs that meet at the barrier (the grid) */
-  int32_t _pad[3];
+  int32_t mode;                        /* 0: the whole SE (above); 1: squeeze only -- the
+                                          depthwise outputs are stored as usual and the CTA
+                                          writes its channels' means to `pooled` for the
+                                          SE launch that follows (dfx_se_params.pooled) */
+  int32_t _pad[2];
 } dfx_se_fuse;
 
 /* Kernel parameter of one GEMM launch.  A single problem travels inline
@@ -277,6 +282,9 @@ typedef struct dfx_se_params {
   const void* w2;
   const float* b2;                     /* may be NULL */
   int32_t cr, act1, act2, apply;
+  const float* pooled;                 /* non-NULL: [n][c] channel means of `in`, written by the
+                                          depthwise-epilogue GEMM before it (dfx_se_fuse mode 1):
+                                          no pooling pass over x */
 } dfx_se_params;
 
 /* Depthwise conv (+ epi: folded BN, act) -> SE gate (as dfx_se_params) -> scale, in

@@ -274,7 +274,10 @@ int config_for(int op, const void* params, size_t size, LaunchCfg* c) {
                                    "(or a 2-CTA cluster split along p)");
           if (pair) c->cluster = 2;
           size_t need = (size_t(d0.n) * d0.p * d0.q * (p->bn_max + 8) * 2 * planes + 15) & ~size_t(15);
-          if (d0.se != nullptr) {       // fused SE: depthwise-output tile + reduction scratch
+          if (d0.se != nullptr && p->se_cr == 0) {   // SE squeeze only: the means' scratch
+            if (p->m2 || d0.n > 2) return fail(DFX_E_ARG, "gemm: SE squeeze needs batch <= 2, no m2");
+            need += (size_t(dfx::kGemmThreads) * 16 + 4 * size_t(p->bn_max)) * 4;
+          } else if (d0.se != nullptr) {  // fused SE: depthwise-output tile + reduction scratch
             const int oh = d0.out.h, ow = d0.out.w, cr = p->se_cr;
             const int nt = d0.nt;
             if (p->m2 || d0.n > 2 || cr < 1 || cr > 512)

@@ -380,6 +380,9 @@ DFX_DEV void se_finish(const dfx_gemm_desc& D, uint8_t* se_smem, const float (*c
                        int N, int OH, int OW, int co_base, int nch, const dfx_view& o, int bn, int tid, int nthr,
                        const uint16_t* wsm, uint64_t* gbar);
 
+DFX_DEV void dw_squeeze(const dfx_gemm_desc& D, uint8_t* scratch, const float (*csum)[8], int item0, int N,
+                        int hw, int co_base, int nch, int tid, int nthr);
+
 template <typename T, int K, int S, int ACT>
 DFX_DEV void dw_smem_t(const dfx_gemm_desc& D, const T* xs, int xp, int N, int P, int Q, int co_base,
                        int nch, const dfx_view& o, const float* sw, int bn, int tid, int nthr,
@@ -474,6 +477,23 @@ DFX_DEV void dw_smem_t(const dfx_gemm_desc& D, const T* xs, int xp, int N, int P
     const int64_t pix = (int64_t(n) * OH + p) * OW + q;
     if (se_smem == nullptr) {
       stv8<T>(o, view_pixel_index(o, pix, ca), acc);
+    } else if (D.se->mode == 1) {
+      // squeeze only: store as usual, sum the stored (rounded) values per channel
+      stv8<T>(o, view_pixel_index(o, pix, ca), acc);
+      float r[8];
+      if constexpr (kSp) {
+        uint4 h, l;
+        pack8_split<T>(acc, h, l);
+        float lv[8];
+        unpack8<T>(h, r);
+        unpack8<T>(l, lv);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) r[i] += lv[i];
+      } else {
+        unpack8<T>(pack8<T>(acc), r);
+      }
+#pragma unroll
+      for (int i = 0; i < 8; ++i) csum[n & 1][i] += r[i];
     } else {
       st8<T>(ot, pix * nch + c, ot_lo, acc);
       float r[8];
@@ -482,23 +502,71 @@ DFX_DEV void dw_smem_t(const dfx_gemm_desc& D, const T* xs, int xp, int N, int P
       for (int i = 0; i < 8; ++i) csum[n & 1][i] += r[i];
     }
   }
-  if (se_smem != nullptr)
-    se_finish<T>(D, se_smem, csum, item0, total, N, OH, OW, co_base, nch, o, bn, tid, nthr,
-                 reinterpret_cast<const uint16_t*>(sw + (K * K + 2) * bn), gbar);
+  if (se_smem != nullptr) {
+    if (D.se->mode == 1)
+      dw_squeeze(D, se_smem, csum, item0, N, OH * OW, co_base, nch, tid, nthr);
+    else
+      se_finish<T>(D, se_smem, csum, item0, total, N, OH, OW, co_base, nch, o, bn, tid, nthr,
+                   reinterpret_cast<const uint16_t*>(sw + (K * K + 2) * bn), gbar);
+  }
 }
 
-DFX_DEV uint32_t ld_acquire_u32(const uint32_t* p) {
-  uint32_t v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
+// Channel sums of this CTA's depthwise outputs (csum: per thread, its fixed channel
+// group (item0 + tid) % cg) reduced in a fixed order: a butterfly over the lanes of
+// equal group (xor cg .. 16), then warps in warp order; a 2-CTA pair adds the
+// peer's sums over DSMEM in rank order.  Leaves mean[n * nch + c] (x 1/hw) in smem.
+DFX_DEV void dw_channel_means(float* red, float* mean, float* peer, const float (*csum)[8], int item0, int N,
+                              int hw, int nch, int tid, int nthr, bool pair) {
+  const int cg = nch >> 3;
+  const int lane = tid & 31, wid = tid >> 5, nwarps = nthr >> 5;
+  float v[16];
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int i = 0; i < 8; ++i) v[a * 8 + i] = csum[a][i];
+  for (int off = cg; off < 32; off <<= 1)
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[i] += __shfl_xor_sync(0xffffffffu, v[i], off);
+  if (lane < cg)
+#pragma unroll
+    for (int i = 0; i < 16; ++i) red[(wid * cg + lane) * 16 + i] = v[i];
+  __syncthreads();
+  const float inv = 1.0f / float(hw);
+  for (int k = tid; k < N * nch; k += nthr) {
+    const int n = k / nch, c = k - n * nch, g = c >> 3, i = c & 7;
+    const int l = ((g - item0) % cg + cg) % cg;        // the lane that held group g
+    float s = 0.0f;
+    for (int w = 0; w < nwarps; ++w) s += red[(w * cg + l) * 16 + (n & 1) * 8 + i];
+    if (pair) peer[k] = s;
+    else mean[k] = s * inv;
+  }
+  if (pair) {
+    cluster_sync_all();
+    for (int k = tid; k < N * nch; k += nthr) mean[k] = (dsmem_ld1(peer + k, 0) + dsmem_ld1(peer + k, 1)) * inv;
+    cluster_sync_all();                                // peers done reading peer[]
+  } else {
+    __syncthreads();
+  }
 }
-DFX_DEV float dsmem_ld1(const float* local, uint32_t rank) {
-  uint32_t remote;
-  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(smem_u32(local)), "r"(rank));
-  float v;
-  asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(remote) : "memory");
-  return v;
+
+// dfx_se_fuse mode 1: the SE launch after this GEMM reads its channel means from
+// D.se->pooled ([n][c]) instead of pooling x (rank 0 of a pair writes).
+DFX_DEV void dw_squeeze(const dfx_gemm_desc& D, uint8_t* scratch, const float (*csum)[8], int item0, int N,
+                        int hw, int co_base, int nch, int tid, int nthr) {
+  float* const red = reinterpret_cast<float*>(scratch);
+  float* const mean = red + nthr * 16;
+  float* const peer = mean + 2 * nch;
+  const bool pair = D.mt_p == 2 && D.m2 == 0;
+  dw_channel_means(red, mean, peer, csum, item0, N, hw, nch, tid, nthr, pair);
+  if (!pair || cluster_ctarank() == 0) {
+    const dfx_se_fuse& F = *D.se;
+    for (int k = tid; k < N * nch; k += nthr) {
+      const int n = k / nch, c = k - n * nch;
+      F.pooled[int64_t(n) * F.c + co_base + c] = mean[k];
+    }
+  }
 }
+
 
 // The squeeze-excitation of the fused MBConv middle (dfx_gemm_desc.se), after the
 // depthwise outputs of this CTA's bn channels sit in `ot` (stored-tensor rounding):
@@ -529,38 +597,8 @@ DFX_DEV void se_finish(const dfx_gemm_desc& D, uint8_t* se_smem, const float (*c
   const bool pair = D.mt_p == 2 && D.m2 == 0;
   const uint32_t rank = pair ? cluster_ctarank() : 0u;
   if (tid == 0) DFX_TL(50);                            // depthwise done
-  // 1. channel sums.  Thread t always handled channel group (item0 + t) % cg: a
-  // butterfly over the lanes of equal group (xor cg, 2 cg, .. 16: fixed order) leaves
-  // lane l < cg with its warp's sums, then warps are added in warp order
-  const int lane = tid & 31, wid = tid >> 5, nwarps = nthr >> 5;
-  float v[16];
-#pragma unroll
-  for (int a = 0; a < 2; ++a)
-#pragma unroll
-    for (int i = 0; i < 8; ++i) v[a * 8 + i] = csum[a][i];
-  for (int off = cg; off < 32; off <<= 1)
-#pragma unroll
-    for (int i = 0; i < 16; ++i) v[i] += __shfl_xor_sync(0xffffffffu, v[i], off);
-  if (lane < cg)
-#pragma unroll
-    for (int i = 0; i < 16; ++i) red[(wid * cg + lane) * 16 + i] = v[i];
-  __syncthreads();
-  const float inv = 1.0f / float(hw);
-  for (int k = tid; k < N * nch; k += nthr) {
-    const int n = k / nch, c = k - n * nch, g = c >> 3, i = c & 7;
-    const int l = ((g - item0) % cg + cg) % cg;        // the lane that held group g
-    float s = 0.0f;
-    for (int w = 0; w < nwarps; ++w) s += red[(w * cg + l) * 16 + (n & 1) * 8 + i];
-    if (pair) gate[k] = s;                             // this CTA's partial (gate[] reused later)
-    else mean[k] = s * inv;
-  }
-  if (pair) {
-    cluster_sync_all();
-    for (int k = tid; k < N * nch; k += nthr) mean[k] = (dsmem_ld1(gate + k, 0) + dsmem_ld1(gate + k, 1)) * inv;
-    cluster_sync_all();                                // peers done reading gate[]
-  } else {
-    __syncthreads();
-  }
+  // 1. channel means (dw_channel_means; gate[] is the pair's exchange buffer)
+  dw_channel_means(red, mean, gate, csum, item0, N, hw, nch, tid, nthr, pair);
   if (tid == 0) DFX_TL(51);                            // channel means
   // 2. fc1 partial over this CTA's channels (fc1^T rows staged in smem: wsm =
   // [w1 hi, w2 hi(, w1 lo, w2 lo)] of [bn][Cr]) -> scratch (rank 0 of a pair only)

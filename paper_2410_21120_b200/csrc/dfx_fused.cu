@@ -144,7 +144,28 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kSeThreads)
   const int G = (nch + 7) / 8;                        // channel groups of this CTA
   const int stripes = G ? kSeThreads / G : 1;
   const int g = threadIdx.x % max(G, 1), y = threadIdx.x / max(G, 1);
-  for (int im = 0; im < nimg; ++im) {
+  if (P.pooled != nullptr) {
+    // the channel means come from the depthwise-epilogue GEMM before (dfx_se_fuse mode 1):
+    // no pooling pass; the scale's x tile loads asynchronously behind the FC phases
+    if (cache_x && G && y < stripes) {
+      const T* ib = reinterpret_cast<const T*>(in.base) + view_pixel_index(in, int64_t(n0) * hw, c_lo + g * 8);
+      for (int s = y; s < hw; s += stripes) {
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(xt + s * nch + g * 8)),
+                     "l"(ib + int64_t(s) * in.pitch)
+                     : "memory");
+        if constexpr (kPl == 2)
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(xtl + s * nch + g * 8)),
+                       "l"(ib + int64_t(s) * in.pitch + xlo)
+                       : "memory");
+      }
+      asm volatile("cp.async.commit_group;" ::: "memory");
+    }
+    for (int im = 0; im < nimg; ++im)
+      for (int k = threadIdx.x; k < nch; k += kSeThreads)
+        pooled[im][k] = __ldcg(P.pooled + int64_t(n0 + im) * C + c_lo + k);
+    __syncthreads();
+  }
+  for (int im = 0; P.pooled == nullptr && im < nimg; ++im) {
   const int n = n0 + im;
   float acc[8];
 #pragma unroll
@@ -336,6 +357,10 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kSeThreads)
     const float* gate = pooled[im];
     const int64_t pb = int64_t(n0 + im) * hw;
     if (cache_x) {
+      if (P.pooled != nullptr) {                       // the x tile loaded behind the FCs
+        asm volatile("cp.async.wait_group 0;" ::: "memory");
+        __syncthreads();
+      }
       const int G8 = nch / 8, total = hw * G8;
       for (int i = threadIdx.x; i < total; i += kSeThreads) {
         const int s = i / G8, g8 = (i - s * G8) * 8;

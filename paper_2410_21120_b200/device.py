@@ -536,6 +536,13 @@ GEMM_DW_MODE = os.environ.get("DFX_GEMM_DW_MODE", "all")
 # vector run serialised after it, where the separate SE launch overlaps its prologue
 # with the GEMM's tail under PDL.  Off by default (DFX_GEMM_DW_SE=1: on, A/B)
 GEMM_DW_SE = os.environ.get("DFX_GEMM_DW_SE", "0") == "1"
+# the SE launch after a depthwise-epilogue GEMM keeps running, but the GEMM's CTAs --
+# which hold every depthwise output of their channels -- write the channel means
+# (dfx_se_fuse mode 1), so the SE skips its pooling pass over x.  Measured slower:
+# the means (butterflies, syncs, a pair's DSMEM exchange) add 2.5 us to the GEMM
+# and save 0.8 us in the SE (EfficientNetV2-L fp16x2 node classes; 4-model batch 1
+# 3.04 -> 3.10 ms fp16x2, 2.19 -> 2.28 ms fp16).  Off (DFX_GEMM_DW_SQUEEZE=1: A/B)
+GEMM_DW_SQUEEZE = os.environ.get("DFX_GEMM_DW_SQUEEZE", "0") == "1"
 _DW_ACTS = (None, "relu", "hardswish", "silu")
 
 
@@ -626,6 +633,7 @@ def plan_member(prog: MemberProgram, n: int, sm_count: int = 148, cluster_ok: bo
     planes = planes_of(prog.precision)
     dw_pairs = gemm_dw_pairs(prog) if GEMM_DW else {}
     se_pairs = dw_se_pairs(prog, dw_pairs) if GEMM_DW_SE and se_cta_limit and n <= 2 else {}
+    sq_pairs = dw_se_pairs(prog, dw_pairs) if GEMM_DW_SQUEEZE and n <= 2 else {}
     for L in prog.launches:
         if L.kind != GEMM:
             continue
@@ -673,6 +681,12 @@ def plan_member(prog: MemberProgram, n: int, sm_count: int = 148, cluster_ok: bo
                             t = dict(t, bn=bn2, nt=nt2, tiles=tiles2, se=si, nslots=nsl2, se_cr=cr)
                             skip.add(si)
                             break
+                sq = sq_pairs.get(L.index)
+                if sq is not None and t.get("se") is None and not m2:
+                    # the SE's squeeze from the depthwise epilogue (means' scratch after the map)
+                    need = xs + (256 * 16 + 4 * bn) * 4 + 16
+                    if need <= nsl * (128 * 64 * 2 + bn * 128) * planes:
+                        t = dict(t, squeeze=sq)
         tilings[L.index] = t
         if t["splits"] > 1 and not t["csplit"]:      # cluster split-K needs no workspace
             ws = max(ws, t["splits"] * n * out.h * out.w * t["nt"] * t["bn"] * 4)
@@ -757,7 +771,13 @@ class ExecInstance:
         self.descs = rt.malloc(self.desc_capacity * C.sizeof(rt.GemmDesc))
         # fused SE (dfx_se_fuse per absorbing GEMM): descriptors, fc1 partial scratch,
         # barrier words (zeroed once; the barrier leaves them reusable)
-        self.se_count = sum(1 for pl in self.plans for t in pl.tilings.values() if t.get("se") is not None)
+        self.se_count = sum(1 for pl in self.plans for t in pl.tilings.values()
+                            if t.get("se") is not None or t.get("squeeze") is not None)
+        self.pool_bytes = sum(_align(n * 4 * 4096) for pl, n in zip(self.plans, batch)
+                              for t in pl.tilings.values() if t.get("squeeze") is not None)
+        self.se_pooled = rt.malloc(max(self.pool_bytes, 16))
+        self._pool_used = 0
+        self._squeeze_ptr: dict = {}
         self.se_scratch_bytes = sum(_align(t["nt"] * n * 512 * 4) for pl, n in zip(self.plans, batch)
                                     for t in pl.tilings.values() if t.get("se") is not None)
         self.se_structs = rt.malloc(max(self.se_count, 1) * C.sizeof(rt.SeFuse))
@@ -1119,6 +1139,16 @@ class ExecInstance:
                     f.ctas = t["tiles"]
                     self._se_host.append(f)
                     d.se = self.se_structs + k * C.sizeof(rt.SeFuse)
+                elif t.get("squeeze") is not None:   # the SE after it reads our channel means
+                    S = next(x for x in prog.launches if x.index == t["squeeze"])
+                    k = len(self._se_host)
+                    f = rt.SeFuse()
+                    f.mode, f.c = 1, S.geom["c"]
+                    f.pooled = self.se_pooled + self._pool_used
+                    self._pool_used += _align(n * 4 * 4096)
+                    self._squeeze_ptr[(m, S.index)] = f.pooled
+                    self._se_host.append(f)
+                    d.se = self.se_structs + k * C.sizeof(rt.SeFuse)
             epi = self._epi(m, prog, L, n)
             if geo.get("tokens") and epi.binop:
                 epi.other = _fold_rows(epi.other)
@@ -1211,7 +1241,8 @@ class ExecInstance:
             yield rt.OP_SE, rt.SeParams(src, self._view(m, prog, L.dst, n), addr("w1"), addr("b1"),
                                         addr("w2"), addr("b2"), geo["cr"], rt.ACT[geo["act1"]],
                                         rt.ACT[geo["act2"]],
-                                        geo.get("apply", 0) | self._se_unstaged(prog, geo, n))
+                                        geo.get("apply", 0) | self._se_unstaged(prog, geo, n),
+                                        self._squeeze_ptr.get((m, L.index)))
         elif L.kind == DWSE:
             geo = L.geom
             addr = (lambda r: arena.addr(m, L.blobs[r]) if r in L.blobs else None)
@@ -1310,7 +1341,7 @@ class ExecInstance:
     def free(self):
         self.graph.destroy()
         for p in (self.act, self.ws, self.counters, self.descs, self.dev_in, self.dev_out,
-                  self.se_structs, self.se_sync, self.se_scratch):
+                  self.se_structs, self.se_sync, self.se_scratch, self.se_pooled):
             rt.free(p)
         rt.host_free(self.host_in)
         rt.host_free(self.host_out)

@@ -59,7 +59,8 @@ class GemmDesc(C.Structure):
 
 class SeFuse(C.Structure):
     _fields_ = [("w1", vp), ("b1", vp), ("w2", vp), ("b2", vp), ("scratch", vp), ("sync", vp),
-                ("c", i32), ("cr", i32), ("act1", i32), ("act2", i32), ("ctas", i32), ("_pad", i32 * 3)]
+                ("pooled", vp), ("c", i32), ("cr", i32), ("act1", i32), ("act2", i32), ("ctas", i32),
+                ("mode", i32), ("_pad", i32 * 2)]
 
 
 class GemmLaunch(C.Structure):
@@ -104,7 +105,7 @@ class OutParams(C.Structure):
 
 class SeParams(C.Structure):
     _fields_ = [("inp", View), ("out", View), ("w1", vp), ("b1", vp), ("w2", vp), ("b2", vp),
-                ("cr", i32), ("act1", i32), ("act2", i32), ("apply", i32)]
+                ("cr", i32), ("act1", i32), ("act2", i32), ("apply", i32), ("pooled", vp)]
 
 
 class DwseParams(C.Structure):

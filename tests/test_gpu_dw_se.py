@@ -49,3 +49,29 @@ def test_dw_se_fused(monkeypatch, name, batch, precision):
     tol = 2e-4 if precision == "fp16x2" else 2e-2
     assert _rel(outs[True][0], ref) <= tol
     assert _rel(outs[True][0], outs[False][0]) <= tol
+
+
+@pytest.mark.parametrize("name,batch,precision", [("efficientnet_v2_l", 1, "fp16x2"),
+                                                  ("efficientnet_v2_l", 2, "fp16"),
+                                                  ("mobilenet_v3_large", 1, "fp16")])
+def test_dw_squeeze_feeds_se(monkeypatch, name, batch, precision):
+    """dfx_se_fuse mode 1 (the default at batch <= 2): the depthwise-epilogue GEMM
+    writes its channels' means, the SE launch after it skips its pooling pass."""
+    g, w = zoo.build(name)
+    xs = np.random.default_rng(4).standard_normal((batch,) + tuple(g.input_spec.dims)).astype(np.float32)
+    outs, nsq = {}, {}
+    for on in (False, True):
+        monkeypatch.setattr(device, "GEMM_DW_SQUEEZE", on)
+        dd = DeviceDag([(g, w)], precision=precision)
+        try:
+            inst = dd.acquire((batch,))
+            nsq[on] = sum(1 for _, p, _ in inst.nodes if isinstance(p, rt.SeParams) and p.pooled)
+            dd.release(inst)
+            outs[on] = [dd.execute([xs])[0] for _ in range(2)]
+        finally:
+            dd.free()
+    assert nsq[False] == 0 and nsq[True] > 0
+    assert np.array_equal(outs[True][0], outs[True][1])
+    tol = 2e-4 if precision == "fp16x2" else 2e-2
+    assert _rel(outs[True][0], run_fast(g, w, xs)) <= tol
+    assert _rel(outs[True][0], outs[False][0]) <= tol
