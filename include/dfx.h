@@ -72,8 +72,10 @@ typedef enum dfx_op {
   DFX_OP_LN = 10,      /* layer norm over channels of token rows (+ token select) */
   DFX_OP_TOKENS = 11,  /* patch grid -> [class token; patches] + pos_embedding */
   DFX_OP_ATTN = 12,    /* multi-head softmax attention over packed q|k|v rows */
-  DFX_OP_DWSE = 13     /* depthwise conv + BN/act -> squeeze-excitation gate -> channel
+  DFX_OP_DWSE = 13,    /* depthwise conv + BN/act -> squeeze-excitation gate -> channel
                           scale, one cluster per image (an MBConv block's middle) */
+  DFX_OP_GATE = 14     /* one thread waits until *flag != 0, then clears it: a member's
+                          input has landed (dfx_execute_gated) */
 } dfx_op;
 
 typedef enum dfx_dtype {
@@ -338,6 +340,16 @@ typedef struct dfx_attn_params {
   int32_t _pad[2];
 } dfx_attn_params;
 
+/* Input gate of one member (DFX_OP_GATE): the member's branch of the fused graph
+ * starts when its input is on the device -- the host sets the flag (an H2D of a
+ * pinned 1 on the copy stream, after the member's input copy) -- so the graph is
+ * launched BEFORE the inputs are gathered and each member starts as soon as its own
+ * input lands.  The kernel traps after ~4 s instead of hanging the GPU. */
+typedef struct dfx_gate_params {
+  uint32_t* flag;                      /* device word, 0 = closed */
+  int32_t _pad[2];
+} dfx_gate_params;
+
 /* ---- library / device ------------------------------------------------- */
 const char* dfx_last_error(void);
 int dfx_abi_version(void);
@@ -439,6 +451,20 @@ int dfx_execute(void* graph, const void* host_in, void* dev_in, size_t in_bytes,
 int dfx_execute_gather(void* graph, const void* const* srcs, const size_t* sizes, int nsrc,
                        void* host_in, void* dev_in, void* host_out, const void* dev_out,
                        size_t out_bytes, void* stream);
+
+/* End-to-end query with per-member gates (fuse.py execute_fused): the graph (whose
+ * members each start with a DFX_OP_GATE node on flags[m]) is launched on `stream`
+ * FIRST; then members are gathered into the pinned staging in `order` (the longest
+ * chain first), and for each one, once all its sources are copied (thread pool as
+ * dfx_execute_gather), its byte range is sent H2D on `copy_stream` followed by its
+ * flag (a 4-byte H2D from the pinned word `one`).  Sources are listed member by
+ * member in `order`; src_member[i] names the member of source i; member_off /
+ * member_bytes give each member's range of host_in / dev_in.  Then the D2H of the
+ * outputs on `stream` and a stream sync. */
+int dfx_execute_gated(void* graph, const void* const* srcs, const size_t* sizes, const int* src_member, int nsrc,
+                      const size_t* member_off, const size_t* member_bytes, int nmembers, void* host_in,
+                      void* dev_in, uint32_t* flags, const uint32_t* one, void* host_out, const void* dev_out,
+                      size_t out_bytes, void* stream, void* copy_stream);
 
 #ifdef __cplusplus
 }

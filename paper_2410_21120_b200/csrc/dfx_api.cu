@@ -35,6 +35,7 @@ template <typename T> __global__ void gap_kernel(const __grid_constant__ dfx_gap
 template <typename T> __global__ void in_kernel(const __grid_constant__ dfx_in_params P);
 template <typename T> __global__ void in_im2col_kernel(const __grid_constant__ dfx_in_params P);
 template <typename T> __global__ void out_kernel(const __grid_constant__ dfx_out_params P);
+__global__ void gate_kernel(const __grid_constant__ dfx_gate_params P);
 template <typename T, int CL, int IPI> __global__ void se_kernel(const __grid_constant__ dfx_se_params P);
 template <typename T> __global__ void dwse_kernel(const __grid_constant__ dfx_dwse_params P);
 template <typename T> __global__ void ln_kernel(const __grid_constant__ dfx_ln_params P);
@@ -462,6 +463,15 @@ int config_for(int op, const void* params, size_t size, LaunchCfg* c) {
       c->grid = dim3(elementwise_grid(int64_t(p->out.n) * p->out.w * cdiv(p->out.c, 8), 256));
       return DFX_OK;
     }
+    case DFX_OP_GATE: {
+      NEED(dfx_gate_params);
+      const auto* p = static_cast<const dfx_gate_params*>(params);
+      if (!p->flag) return fail(DFX_E_ARG, "gate: null flag");
+      c->func = reinterpret_cast<const void*>(&dfx::gate_kernel);
+      c->grid = dim3(1);
+      c->block = dim3(32);
+      return DFX_OK;
+    }
     case DFX_OP_ATTN: {
       NEED(dfx_attn_params);
       const auto* p = static_cast<const dfx_attn_params*>(params);
@@ -523,7 +533,8 @@ int dfx_sizeof(const char* name) {
            {"dfx_tokens_params", sizeof(dfx_tokens_params)},
            {"dfx_attn_params", sizeof(dfx_attn_params)},
            {"dfx_dwse_params", sizeof(dfx_dwse_params)},
-           {"dfx_se_fuse", sizeof(dfx_se_fuse)}};
+           {"dfx_se_fuse", sizeof(dfx_se_fuse)},
+           {"dfx_gate_params", sizeof(dfx_gate_params)}};
   for (auto& e : t)
     if (!strcmp(e.n, name)) return e.s;
   return -1;
@@ -1113,6 +1124,105 @@ int dfx_execute_gather(void* graph, const void* const* srcs, const size_t* sizes
   }
   int rc = dfx_graph_launch(graph, stream);
   if (rc) return rc;
+  CK(cudaMemcpyAsync(host_out, dev_out, out_bytes, cudaMemcpyDeviceToHost, S(stream)));
+  CK(cudaStreamSynchronize(S(stream)));
+  return DFX_OK;
+}
+
+int dfx_execute_gated(void* graph, const void* const* srcs, const size_t* sizes, const int* src_member, int nsrc,
+                      const size_t* member_off, const size_t* member_bytes, int nmembers, void* host_in,
+                      void* dev_in, uint32_t* flags, const uint32_t* one, void* host_out, const void* dev_out,
+                      size_t out_bytes, void* stream, void* copy_stream) {
+  NvtxRange r("dfx execute_fused (gated: graph first, members' inputs behind it)");
+  if (nsrc < 0 || nmembers < 1 || nmembers > 64 || (nsrc > 0 && (!srcs || !sizes || !src_member)) || !host_in ||
+      !flags || !one || !member_off || !member_bytes || copy_stream == stream)
+    return fail(DFX_E_ARG, "execute_gated: bad arguments");
+  // 1. the graph first: every member's gate node waits for its flag
+  int rc = dfx_graph_launch(graph, stream);
+  if (rc) return rc;
+  // 2. sources -> pinned staging, member by member (sources arrive member by member)
+  int nch = 0;
+  for (int i = 0; i < nsrc; ++i) nch += int((sizes[i] + StagePool::kChunk - 1) / StagePool::kChunk);
+  if (nch > StagePool::kMaxChunks) return fail(DFX_E_ARG, "gather list too large");
+  std::vector<int> chunk_member(size_t(nch > 0 ? nch : 1));
+  std::vector<int> left(size_t(nmembers), 0);            // chunks still to copy, per member
+  cudaError_t err = cudaSuccess;
+  auto open_gate = [&](int m) {
+    if (err != cudaSuccess) return;
+    if (member_bytes[m])
+      err = cudaMemcpyAsync(static_cast<char*>(dev_in) + member_off[m], static_cast<char*>(host_in) + member_off[m],
+                            member_bytes[m], cudaMemcpyHostToDevice, S(copy_stream));
+    if (err == cudaSuccess)
+      err = cudaMemcpyAsync(flags + m, one, sizeof(uint32_t), cudaMemcpyHostToDevice, S(copy_stream));
+  };
+  std::vector<size_t> at(size_t(nmembers), 0);
+  StagePool* P = stage_pool();
+  std::unique_lock<std::mutex> job(P->job_mu, std::try_to_lock);
+  if (!job.owns_lock() || P->workers.empty() || nch <= 1) {
+    if (job.owns_lock()) job.unlock();
+    int i = 0;
+    std::vector<char> opened(size_t(nmembers), 0);
+    while (i < nsrc) {                                     // member by member, as listed
+      const int m = src_member[i];
+      for (; i < nsrc && src_member[i] == m; ++i) {
+        std::memcpy(static_cast<char*>(host_in) + member_off[m] + at[m], srcs[i], sizes[i]);
+        at[m] += sizes[i];
+      }
+      open_gate(m);
+      opened[m] = 1;
+    }
+    for (int m = 0; m < nmembers; ++m)
+      if (!opened[m]) open_gate(m);                      // members with no sources (batch 0)
+  } else {
+    P->claim.store(0, std::memory_order_relaxed);
+    int n = 0;
+    for (int i = 0; i < nsrc; ++i) {
+      const int m = src_member[i];
+      for (size_t s0 = 0; s0 < sizes[i]; s0 += StagePool::kChunk) {
+        const size_t b = std::min(StagePool::kChunk, sizes[i] - s0);
+        P->chunks[n] = {static_cast<char*>(host_in) + member_off[m] + at[m] + s0,
+                        static_cast<const char*>(srcs[i]) + s0, b};
+        P->done[n].store(0, std::memory_order_relaxed);
+        chunk_member[size_t(n)] = m;
+        ++left[size_t(m)];
+        ++n;
+      }
+      at[m] += sizes[i];
+    }
+    P->claim.store(uint64_t(n) << StagePool::kIdxBits, std::memory_order_release);
+    {
+      std::lock_guard<std::mutex> g(P->mu);
+      P->gen.fetch_add(1, std::memory_order_release);
+    }
+    P->cv.notify_all();
+    // members open in listed order as soon as all their chunks are copied; the
+    // caller copies chunks too
+    std::vector<char> opened(size_t(nmembers), 0);
+    int scan = 0, nopen = 0;
+    for (int m = 0; m < nmembers; ++m)
+      if (left[size_t(m)] == 0) {
+        open_gate(m);
+        opened[size_t(m)] = 1;
+        ++nopen;
+      }
+    while (nopen < nmembers) {
+      while (scan < n && P->done[scan].load(std::memory_order_acquire)) {
+        const int m = chunk_member[size_t(scan)];
+        if (--left[size_t(m)] == 0 && !opened[size_t(m)]) {
+          open_gate(m);
+          opened[size_t(m)] = 1;
+          ++nopen;
+        }
+        ++scan;
+      }
+      if (nopen == nmembers) break;
+      const int c = P->take();
+      if (c >= 0) P->copy(c);
+    }
+    job.unlock();
+  }
+  CK(err);
+  // 3. outputs
   CK(cudaMemcpyAsync(host_out, dev_out, out_bytes, cudaMemcpyDeviceToHost, S(stream)));
   CK(cudaStreamSynchronize(S(stream)));
   return DFX_OK;

@@ -543,6 +543,20 @@ __global__ void __launch_bounds__(256) in_im2col_kernel(const __grid_constant__ 
   }
 }
 
+// A member's input gate (DFX_OP_GATE): one thread waits for the host's flag, clears it
+// for the next query.  The member's IN kernel follows it in the graph.
+__global__ void gate_kernel(const __grid_constant__ dfx_gate_params P) {
+  if (threadIdx.x == 0) {
+    for (uint32_t tries = 0; ld_acquire_u32(P.flag) == 0u; ++tries) {
+      __nanosleep(256);
+      if (tries > (1u << 24)) __trap();                // ~4 s: never hang the GPU
+    }
+    *P.flag = 0u;
+    __threadfence();
+  }
+  griddep_launch();
+}
+
 // 16-bit NHWC -> fp32 samples in logical CHW order (also the flatten order).
 template <typename T>
 __global__ void out_kernel(const __grid_constant__ dfx_out_params P) {

@@ -104,6 +104,12 @@ GROUP_AUTO_MEMBERS = 6
 GROUP_MIN = int(os.environ.get("DFX_GROUP_MIN", "4"))          # matched layers for a pair to group
 # e2e queries gather their inputs on a host thread pool, overlapping the H2D (A/B switch)
 E2E_GATHER = os.environ.get("DFX_E2E_GATHER", "1") != "0"
+# end to end with per-member input gates (dfx_execute_gated): the graph is launched
+# first and every member starts as soon as its own input is on the device (the
+# longest chain gathered and sent first).  Measured no gain (fp16x2 e2e 3.24 ms
+# gathered-then-launched vs 3.27 ms gated: the graph launch call now precedes the
+# gather on the host, and the gates add a kernel per chain).  Off (DFX_E2E_GATED=1)
+E2E_GATED = os.environ.get("DFX_E2E_GATED", "0") == "1"
 
 
 def gemm_slots(bn: int, tiles: int, sm_count: int = 148, m2: int = 0, planes: int = 1) -> int:
@@ -787,10 +793,17 @@ class ExecInstance:
         self._se_scratch_used = 0
         self.dev_in = rt.malloc(max(self.in_bytes, 16))
         self.dev_out = rt.malloc(max(self.out_bytes, 16))
+        # per-member input gates: device flags, a pinned 1, a copy stream
+        self.gated = E2E_GATED and E2E_GATHER
+        self.gate_flags = rt.malloc(4 * max(len(progs), 4))
+        self.gate_one = rt.host_alloc(16)
+        C.c_uint32.from_address(self.gate_one).value = 1
+        self.copy_stream = rt.stream_create()
         self.host_in = rt.host_alloc(max(self.in_bytes, 16))
         self.host_out = rt.host_alloc(max(self.out_bytes, 16))
         rt.memset(self.act, 0, self.act_bytes, self.stream)
         rt.memset(self.se_sync, 0, max(self.se_count, 1) * 16, self.stream)
+        rt.memset(self.gate_flags, 0, 4 * max(len(progs), 4), self.stream)
         rt.memset(self.counters, 0, max(4 * n_ctr, 16), self.stream)
         self.gemm_count = 0
         self.kernel_nodes = 0
@@ -833,6 +846,9 @@ class ExecInstance:
             ind = tuple(prog.input_dims) if len(prog.input_dims) == 3 else (prog.input_dims[0], 1, 1)
             pin = rt.InParams(self.dev_in + self.in_off[m], self._view(m, prog, "<input>", n),
                               *ic, *ind, getattr(prog, "input_split", 0))
+            if self.gated:                             # the member waits for its input (dfx_execute_gated)
+                gp = rt.GateParams(self.gate_flags + 4 * m)
+                items.append((rt.OP_GATE, gp, dict(member=m, kind="gate", flops=0, bytes=0)))
             items.append((rt.OP_IN, pin, dict(member=m, kind="in", flops=0, bytes=self.in_sizes[m] * 3 // 2)))
             for L in prog.launches:
                 if L.index in self.plans[m].skip:      # absorbed by the GEMM before it
@@ -906,6 +922,10 @@ class ExecInstance:
                 if pos[m] == len(items) and seq:
                     prev_tail = tail[m]
         assert all(p == len(c) for p, c in zip(pos, chains)), "grouped GEMM matching left a chain blocked"
+        chain: dict[int, float] = {}
+        for mm, (op_, _, info_) in zip(self._node_member, self.nodes):
+            chain[mm] = chain.get(mm, 0.0) + _node_cost_us(info_)
+        self.gate_order = sorted(range(len(progs)), key=lambda mm: (-chain.get(mm, 0.0), mm))
         if NODE_PRIORITY and self.dag.mode == "concurrent" and max(self.batch) <= PRIORITY_MAX_BATCH:
             self._prioritise(g)
         self._keep = [p for _, p, _ in self.nodes]
@@ -1073,7 +1093,7 @@ class ExecInstance:
                 group.append(nodes[i + 1][:2])
                 i += 1
             i += 1
-            if kinds is not None and info["kind"] not in kinds:
+            if op == rt.OP_GATE or (kinds is not None and info["kind"] not in kinds):
                 continue
             g = rt.Graph()
             last = None
@@ -1303,6 +1323,7 @@ class ExecInstance:
         H2D).  DFX_E2E_GATHER=0: one-thread staging + dfx_execute."""
         if not E2E_GATHER:
             self.stage_inputs(xs)
+            self.open_gates()
             self.graph.execute(self.host_in, self.dev_in, self.in_bytes, self.host_out, self.dev_out,
                                self.out_bytes, self.stream)
             return self.read_outputs()
@@ -1316,6 +1337,25 @@ class ExecInstance:
                 total += a.nbytes
             if total != self.in_sizes[m]:
                 raise ValueError(f"member {m}: {total} input bytes, expected {self.in_sizes[m]}")
+        if self.gated:
+            # sources member by member, the longest chain first (its branch starts first)
+            per = []
+            at = 0
+            for m, x in enumerate(xs):
+                k = len(x) if isinstance(x, (list, tuple)) else 1
+                per.append(keep[at:at + k])
+                at += k
+            order = self.gate_order
+            lst = [(m, a) for m in order for a in per[m]]
+            srcs = (C.c_void_p * len(lst))(*[a.ctypes.data for _, a in lst])
+            sizes = (C.c_size_t * len(lst))(*[a.nbytes for _, a in lst])
+            smem = (C.c_int * len(lst))(*[m for m, _ in lst])
+            moff = (C.c_size_t * len(xs))(*self.in_off[:len(xs)])
+            mbytes = (C.c_size_t * len(xs))(*self.in_sizes)
+            self.graph.execute_gated(srcs, sizes, smem, moff, mbytes, self.host_in, self.dev_in, self.gate_flags,
+                                     self.gate_one, self.host_out, self.dev_out, self.out_bytes, self.stream,
+                                     self.copy_stream)
+            return self.read_outputs()
         srcs = (C.c_void_p * len(keep))(*[a.ctypes.data for a in keep])
         sizes = (C.c_size_t * len(keep))(*[a.nbytes for a in keep])
         self.graph.execute_gather(srcs, sizes, self.host_in, self.dev_in, self.host_out, self.dev_out,
@@ -1327,7 +1367,14 @@ class ExecInstance:
         rt.h2d(self.dev_in, self.host_in, self.in_bytes, self.stream)
         rt.stream_sync(self.stream)
 
+    def open_gates(self):
+        """Every member's gate open (inputs already resident: device-timed steps,
+        profiling, the manager's replays): 0x01010101 in each flag, stream-ordered."""
+        if self.gated:
+            rt.memset(self.gate_flags, 1, 4 * max(len(self.dag.programs), 4), self.stream)
+
     def launch_graph(self):
+        self.open_gates()
         self.graph.launch(self.stream)
 
     def sync(self):
@@ -1341,8 +1388,10 @@ class ExecInstance:
     def free(self):
         self.graph.destroy()
         for p in (self.act, self.ws, self.counters, self.descs, self.dev_in, self.dev_out,
-                  self.se_structs, self.se_sync, self.se_scratch, self.se_pooled):
+                  self.se_structs, self.se_sync, self.se_scratch, self.se_pooled, self.gate_flags):
             rt.free(p)
+        rt.host_free(self.gate_one)
+        rt.stream_destroy(self.copy_stream)
         rt.host_free(self.host_in)
         rt.host_free(self.host_out)
         rt.stream_destroy(self.stream)

@@ -20,7 +20,7 @@ PKG = Path(__file__).resolve().parent
 LIB_PATH = PKG / "libdfx.so"
 
 (OP_GEMM, OP_SPLITK, OP_DWCONV, OP_POOL, OP_GAP, OP_EW, OP_IN, OP_OUT, OP_SE, OP_LN, OP_TOKENS,
- OP_ATTN, OP_DWSE) = range(1, 14)
+ OP_ATTN, OP_DWSE, OP_GATE) = range(1, 15)
 ACT = {None: 0, "relu": 1, "hardswish": 2, "hardsigmoid": 3, "silu": 4, "sigmoid": 5, "gelu": 6}
 BIN_NONE, BIN_ADD, BIN_SCALE = 0, 1, 2
 DT_BF16, DT_F16, DT_BF16X2, DT_F16X2 = 0, 1, 2, 3
@@ -103,6 +103,10 @@ class OutParams(C.Structure):
     _fields_ = [("inp", View), ("dst", vp)]
 
 
+class GateParams(C.Structure):
+    _fields_ = [("flag", vp), ("_pad", i32 * 2)]
+
+
 class SeParams(C.Structure):
     _fields_ = [("inp", View), ("out", View), ("w1", vp), ("b1", vp), ("w2", vp), ("b2", vp),
                 ("cr", i32), ("act1", i32), ("act2", i32), ("apply", i32), ("pooled", vp)]
@@ -135,12 +139,12 @@ STRUCTS = {
     "dfx_gap_params": GapParams, "dfx_ew_params": EwParams, "dfx_in_params": InParams,
     "dfx_out_params": OutParams, "dfx_se_params": SeParams, "dfx_ln_params": LnParams,
     "dfx_tokens_params": TokensParams, "dfx_attn_params": AttnParams, "dfx_dwse_params": DwseParams,
-    "dfx_se_fuse": SeFuse,
+    "dfx_se_fuse": SeFuse, "dfx_gate_params": GateParams,
 }
 OP_PARAMS = {OP_GEMM: GemmLaunch, OP_SPLITK: SplitKParams, OP_DWCONV: DwconvParams,
              OP_POOL: PoolParams, OP_GAP: GapParams, OP_EW: EwParams, OP_IN: InParams,
              OP_OUT: OutParams, OP_SE: SeParams, OP_LN: LnParams, OP_TOKENS: TokensParams,
-             OP_ATTN: AttnParams, OP_DWSE: DwseParams}
+             OP_ATTN: AttnParams, OP_DWSE: DwseParams, OP_GATE: GateParams}
 
 # every symbol include/dfx.h declares (tests check the .so exports all of them)
 EXPORTS = (
@@ -151,7 +155,8 @@ EXPORTS = (
     "dfx_stream_sync", "dfx_event_create", "dfx_event_destroy", "dfx_event_record",
     "dfx_event_elapsed", "dfx_tmap_act", "dfx_tmap_weights", "dfx_launch", "dfx_graph_create",
     "dfx_graph_add", "dfx_graph_set_priority", "dfx_graph_instantiate", "dfx_graph_launch", "dfx_graph_node_count",
-    "dfx_graph_destroy", "dfx_execute", "dfx_execute_gather", "dfx_nvtx_range_push", "dfx_nvtx_range_pop",
+    "dfx_graph_destroy", "dfx_execute", "dfx_execute_gather", "dfx_execute_gated", "dfx_nvtx_range_push",
+    "dfx_nvtx_range_pop",
 )
 
 _lock = threading.Lock()
@@ -349,6 +354,13 @@ class Graph:
         """srcs / sizes: ctypes arrays of host pointers and byte counts."""
         call("dfx_execute_gather", vp(self.ptr), srcs, sizes, C.c_int(len(srcs)), vp(host_in),
              vp(dev_in), vp(host_out), vp(dev_out), C.c_size_t(out_bytes), vp(stream))
+
+    def execute_gated(self, srcs, sizes, src_member, member_off, member_bytes, host_in, dev_in, flags, one,
+                      host_out, dev_out, out_bytes, stream, copy_stream):
+        """dfx_execute_gated: graph launched first, members' inputs staged behind it."""
+        call("dfx_execute_gated", vp(self.ptr), srcs, sizes, src_member, C.c_int(len(srcs)), member_off,
+             member_bytes, C.c_int(len(member_off)), vp(host_in), vp(dev_in), vp(flags), vp(one),
+             vp(host_out), vp(dev_out), C.c_size_t(out_bytes), vp(stream), vp(copy_stream))
 
     def destroy(self):
         if self.ptr:

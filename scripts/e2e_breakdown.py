@@ -8,7 +8,7 @@ from paper_2410_21120_b200.executor import Tensor
 
 models = bench.build_models(list(zoo.NORTH_STAR))
 dag = fuse.fuse_models(models)
-img = fuse.load_fused(dag)
+img = fuse.load_fused(dag, precision=sys.argv[1] if len(sys.argv) > 1 else "fp16x2")
 xs = {g.model_id: Tensor(g.input_spec, np.random.default_rng(i).standard_normal((3, 224, 224)).astype(np.float32))
       for i, (g, _) in enumerate(models)}
 for _ in range(20):
