@@ -211,10 +211,13 @@ typedef struct __attribute__((aligned(64))) dfx_gemm_launch {
                                       bit 3: cluster split-K -- the desc0.splits (2..8)
                                       CTAs of an output tile form a cluster and reduce
                                       their partials over DSMEM (no workspace, no
-                                      splitk launch) */
+                                      splitk launch);
+                                      bit 5: weight tiles with an L2 evict_first
+                                      policy (each read by <= 2 CTAs) */
   int32_t m2;                      /* any problem has m2 = 1 (sizes smem / TMEM) */
   int32_t se_cr;                   /* desc0.se != NULL: its hidden width (sizes smem) */
-  int32_t _pad[6];
+  int32_t max_ctas;                /* persistent launch: grid cap (0 = 1-2 CTAs per SM) */
+  int32_t _pad[5];
   dfx_gemm_desc desc0;             /* the problem when ndesc == 1 */
 } dfx_gemm_launch;
 

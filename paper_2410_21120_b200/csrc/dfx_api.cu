@@ -250,7 +250,9 @@ int config_for(int op, const void* params, size_t size, LaunchCfg* c) {
         c->smem = dfx::gemm_smem_bytes(p->bn_max, p->nslots, 0, planes) + 1024 +
                   ((p->flags & 4) ? 8 * dfx::kEpiStageWarpBytes : 0) +
                   (p->desc0.cout <= dfx::kPersistVecMax ? 2 * ((p->desc0.cout + 15) & ~15) * 4 : 0);
-        c->grid = dim3(unsigned(std::min<int64_t>(p->total_tiles, int64_t(per_sm) * g_sm_count)));
+        int64_t cap = int64_t(per_sm) * g_sm_count;
+        if (p->max_ctas > 0) cap = std::min<int64_t>(cap, p->max_ctas);
+        c->grid = dim3(unsigned(std::min<int64_t>(p->total_tiles, cap)));
         c->block = dim3(64 + 128 * groups);
       } else {
         c->smem = dfx::gemm_smem_bytes(p->bn_max, p->nslots, p->m2 ? 1 : 0, planes) + 1024;

@@ -407,6 +407,44 @@ DFX_DEV void tma_load_2d(void* dst, const void* tmap, uint64_t* bar, int c0, int
       : "memory");
 }
 
+// L2 policy for operands read once per query (batch-1 weights): evict_first, so
+// streaming hundreds of MB of weights does not push the concurrent members'
+// L2-resident activations out to HBM.
+DFX_DEV uint64_t l2_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+
+DFX_DEV void tma_load_2d_hint(void* dst, const void* tmap, uint64_t* bar, int c0, int c1, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(dst)),
+      "l"(tmap), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "l"(pol)
+      : "memory");
+}
+
+DFX_DEV void tma_load_3d_hint(void* dst, const void* tmap, uint64_t* bar, int c0, int c1, int c2,
+                              uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%3, %4, %5}], [%2], %6;" ::"r"(smem_u32(dst)),
+      "l"(tmap), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "l"(pol)
+      : "memory");
+}
+
+// weight (B) tile of one k-step; pol != 0: with that L2 policy
+template <int planes>
+DFX_DEV void tma_load_w(void* dst, const void* tmap, uint64_t* bar, int c0, int c1, uint64_t pol) {
+  if constexpr (planes == 2) {      // one 3-D box: the k-step's hi rows, then its lo rows
+    if (pol) tma_load_3d_hint(dst, tmap, bar, c0, c1, 0, pol);
+    else tma_load_3d(dst, tmap, bar, c0, c1, 0);
+  } else {
+    if (pol) tma_load_2d_hint(dst, tmap, bar, c0, c1, pol);
+    else tma_load_2d(dst, tmap, bar, c0, c1);
+  }
+}
+
 // Non-tensor bulk copy global -> own CTA's shared memory (16-B aligned, size % 16 == 0).
 DFX_DEV void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
   asm volatile(

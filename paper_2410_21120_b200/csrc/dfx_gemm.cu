@@ -213,6 +213,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     const uint32_t tx_per_k = (box_a_bytes + uint32_t(sub_b)) * planes;
     const void* tma = gd->tmap_a;
     const void* tmb = gd->tmap_b;
+    // flags bit 5: every weight tile is read by one or two CTAs (batch-1 layers)
+    const uint64_t wpol = (L.flags & 32) ? l2_evict_first() : 0;
     // Weights are static: the first nslots stages' B tiles are requested before
     // the programmatic dependency resolves, overlapping the predecessor's tail.
     const int npre = min(nslots, st_end - st_begin);
@@ -222,12 +224,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       const int k0 = st * kpack;
       const int nk = min(kpack, ksteps - k0);
       mbar_arrive_expect_tx(&hdr->full[it], nk * tx_per_k);
-      for (int j = 0; j < nk; ++j) {
-        if constexpr (planes == 2)       // one 3-D box: the k-step's hi rows, then its lo rows
-          tma_load_3d(b_dst + 2 * j * sub_b, tmb, &hdr->full[it], (k0 + j) * cb, co_base, 0);
-        else
-          tma_load_2d(b_dst + j * sub_b, tmb, &hdr->full[it], (k0 + j) * cb, co_base);
-      }
+      for (int j = 0; j < nk; ++j)       // split: one 3-D box, the k-step's hi rows then lo rows
+        tma_load_w<planes>(b_dst + j * b_kstride * sub_b, tmb, &hdr->full[it], (k0 + j) * cb, co_base, wpol);
       if (it < 8) DFX_TL(30 + it);                 // B prefetch of stage `it` issued (30..37)
     }
     DFX_TL(1);                                     // weight prefetch issued
@@ -293,10 +291,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                           pb[h] + rc, n0h[h]);
             }
           }
-        if constexpr (planes == 2)
-          tma_load_3d(b_dst + 2 * j * sub_b, tmb, &hdr->full[slot], (k0 + j) * cb, co_base, 0);
-        else
-          tma_load_2d(b_dst + j * sub_b, tmb, &hdr->full[slot], (k0 + j) * cb, co_base);
+        tma_load_w<planes>(b_dst + j * b_kstride * sub_b, tmb, &hdr->full[slot], (k0 + j) * cb, co_base, wpol);
         if (++cblk == cblocks) {
           cblk = 0;
           if (++sc == S) {

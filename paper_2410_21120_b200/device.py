@@ -22,6 +22,7 @@ from __future__ import annotations
 import ctypes as C
 import math
 import os
+import sys
 import threading
 import time
 import weakref
@@ -89,6 +90,13 @@ SE_UNSTAGED_BATCH = int(os.environ.get("DFX_SE_UNSTAGED_BATCH", "8"))
 NODE_PRIORITY = os.environ.get("DFX_PRIORITY", "1") != "0"
 PRIORITY_MAX_BATCH = 2
 SLACK_SPLIT_MAX = int(os.environ.get("DFX_SLACK_SPLIT_MAX", "0"))
+# ... applied only to members whose estimated chain is below this fraction of the
+# longest one (A/B: the members with the most slack give up SMs)
+SLACK_FRAC = float(os.environ.get("DFX_SLACK_FRAC", "1.0"))
+SLACK_SMS = int(os.environ.get("DFX_SLACK_SMS", "0"))
+# batch-1 weight tiles (each read by one or two CTAs) loaded with an L2 evict_first
+# policy, so weight streaming does not evict the members' activations (A/B)
+W_EVICT_FIRST = os.environ.get("DFX_W_EVICT_FIRST", "0") == "1"
 # persistent GEMM for grids above this many waves (A/B knob)
 PERSIST_MIN_WAVES = float(os.environ.get("DFX_PERSIST_MIN_WAVES", "2"))
 GEMM_EARLY_PDL = os.environ.get("DFX_GEMM_EARLY_PDL", "0") == "1"            # A/B switch
@@ -736,11 +744,20 @@ class ExecInstance:
         # A/B (DFX_SLACK_SPLIT_MAX=k): at small batch, members off the critical chain
         # split K at most k ways, leaving SMs to the longest chain
         caps = [0] * len(progs)
-        if SLACK_SPLIT_MAX and dag.mode == "concurrent" and max(batch) <= PRIORITY_MAX_BATCH:
+        # A/B (DFX_SLACK_SMS=k): the same members instead run every GEMM unsplit on
+        # the persistent kernel with at most k CTAs, so they never hold more than
+        # ~k SMs while the critical chain's kernels wait for free SMs
+        self.sm_budget = [0] * len(progs)
+        if (SLACK_SPLIT_MAX or SLACK_SMS) and dag.mode == "concurrent" and max(batch) <= PRIORITY_MAX_BATCH:
             est = [sum(_NODE_BASE_US.get(L.kind, 2.5) for L in p.launches) if n > 0 else 0
                    for p, n in zip(progs, batch)]
             crit = est.index(max(est))
-            caps = [0 if i == crit else SLACK_SPLIT_MAX for i in range(len(progs))]
+            slack = [i != crit and e < SLACK_FRAC * est[crit] for i, e in enumerate(est)]
+            caps = [(1 if SLACK_SMS else SLACK_SPLIT_MAX) if s else 0 for s in slack]
+            self.sm_budget = [SLACK_SMS if s else 0 for s in slack]
+            if os.environ.get("DFX_SLACK_DEBUG"):
+                print(f"slack caps: est {[round(e) for e in est]} caps {caps} sms {self.sm_budget}",
+                      file=sys.stderr)
         # fused SE grids meet at a grid-wide barrier: the members that may run one at the
         # same time share the SMs (concurrent mode; sequential members never overlap)
         se_members = sum(1 for p, n in zip(progs, batch) if 0 < n <= 2 and any(L.kind == SE for L in p.launches))
@@ -1203,8 +1220,10 @@ class ExecInstance:
                 gl.flags |= 8                # cluster split-K (DSMEM reduction, no splitk node)
                 need = 128 * (t["bn"] + 4) * 4          # the fp32 partial tile parks in the slots
                 gl.nslots = max(gl.nslots, -(-need // slot_bytes))
+            budget = self.sm_budget[m] if t.get("dw") is None and not csplit else 0
             if GEMM_PERSIST and not gl.m2 and t["splits"] == 1 and \
-                    t["tiles"] > PERSIST_MIN_WAVES * self.dag.sm_count:
+                    (t["tiles"] > PERSIST_MIN_WAVES * self.dag.sm_count or budget):
+                gl.max_ctas = budget
                 gl.flags |= 2                # persistent kernel for multi-wave layers
                 # bn > 64: one CTA per SM, as deep a ring as smem allows; bn <= 64: two
                 # CTAs per SM (dfx_api.cu), 4 slots each
@@ -1215,6 +1234,8 @@ class ExecInstance:
                                            // slot_bytes))
                 else:
                     gl.nslots = 4 if planes == 1 else 2
+            if W_EVICT_FIRST and not gl.flags & 2 and t["mt_n"] * t["mt_p"] * t["mt_q"] <= 2:
+                gl.flags |= 32               # weights read by <= 2 CTAs each: L2 evict_first
             if GEMM_DRAIN_STAGED:
                 gl.flags |= 4                # smem-transposed epilogue drain (A/B)
             if GEMM_EARLY_PDL:

@@ -7,6 +7,7 @@ from paper_2410_21120_b200.device import DeviceDag
 ap = argparse.ArgumentParser()
 ap.add_argument("--batch", type=int, default=1)
 ap.add_argument("--set", choices=("north", "eight"), default="north")
+ap.add_argument("--precision", default="fp16x2")
 a = ap.parse_args()
 names = zoo.NORTH_STAR if a.set == "north" else zoo.EIGHT_MODEL
 models = [zoo.build(n) for n in names]
@@ -23,12 +24,12 @@ def timeit(dag, batch, K=30):
 
 
 for (g, w), name in zip(models, names):
-    d = DeviceDag([(g, w)])
+    d = DeviceDag([(g, w)], precision=a.precision)
     ms, nodes = timeit(d, (a.batch,))
     print(f"{name:22s} alone: {ms:7.3f} ms  nodes {nodes:5d}  {ms / nodes * 1e3:6.2f} us/node", flush=True)
-d = DeviceDag(models)
+d = DeviceDag(models, precision=a.precision)
 ms, nodes = timeit(d, tuple([a.batch] * len(models)))
 print(f"{'fused (concurrent)':22s}      {ms:7.3f} ms  nodes {nodes:5d}")
-d = DeviceDag(models, mode="sequential")
+d = DeviceDag(models, mode="sequential", precision=a.precision)
 ms, nodes = timeit(d, tuple([a.batch] * len(models)))
 print(f"{'fused (sequential)':22s}      {ms:7.3f} ms  nodes {nodes:5d}")
