@@ -779,6 +779,9 @@ def run_ours(args):
         "roofline": roofline,
         "cpu_baseline": cpu_baseline,
         "parity_rel_err": parity,
+        # logits that came out inf / NaN during the whole run (fp16 stores do not
+        # saturate, so any activation overflow would show here; dfx_nonfinite_count)
+        "nonfinite_logits": fuse.nonfinite_outputs(),
         "clocks": clk,
         "sharded_batch32": sharded,
         "other_configs": extra,

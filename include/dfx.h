@@ -365,6 +365,11 @@ int dfx_init(int device);
 int dfx_device_info(int device, int* sm_count, int* cc_major, int* cc_minor,
                     size_t* total_mem);
 int dfx_mem_info(size_t* free_bytes, size_t* total_bytes);
+/* Logits that came out non-finite (inf / NaN) on `device` since the last reset:
+ * fp16 stores do not saturate, so an activation overflow anywhere in a member
+ * reaches its output as inf / NaN and is counted here by the output kernel
+ * (reset != 0: read and zero). */
+int dfx_nonfinite_count(int device, unsigned long long* count, int reset);
 
 /* NVTX ranges (header-only NVTX3: free unless a profiler is attached).  The library
  * marks swap-in, graph instantiation and execution itself; the Python layer marks

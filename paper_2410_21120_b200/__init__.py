@@ -22,7 +22,7 @@ _EXPORTS = {
     "Tensor": "executor", "run": "executor", "run_batch": "executor",
     # fusion compiler
     "FusedDag": "fuse", "InitPreamble": "fuse", "SubGraph": "fuse", "execute_fused": "fuse",
-    "fuse_models": "fuse", "swap_subgraph": "fuse", "load_fused": "fuse", "unload": "fuse",
+    "fuse_models": "fuse", "swap_subgraph": "fuse", "load_fused": "fuse", "unload": "fuse", "nonfinite_outputs": "fuse",
     # repository (read side)
     "Repository": "repo", "ModelManifest": "repo",
     # memory / load accounting

@@ -19,6 +19,7 @@
 #include <nvtx3/nvToolsExt.h>   // header-only NVTX3: ranges cost nothing without a tool attached
 
 #include "dfx_common.cuh"
+#include "dfx_dw.cuh"
 #include "dfx_epi.cuh"
 
 namespace dfx {
@@ -30,6 +31,8 @@ template <typename T, int ACT1> __global__ void ew_vec_kernel(const __grid_const
 template <typename T> __global__ void dwconv_kernel(const __grid_constant__ dfx_dwconv_params P);
 template <typename T, int K, int S, int QV, int ACT>
 __global__ void dwconv_tile_kernel(const __grid_constant__ dfx_dwconv_params P);
+template <typename T, int S, int ACT>
+__global__ void dwconv_col_kernel(const __grid_constant__ dfx_dwconv_params P);
 template <typename T> __global__ void pool_kernel(const __grid_constant__ dfx_pool_params P);
 template <typename T> __global__ void gap_kernel(const __grid_constant__ dfx_gap_params P);
 template <typename T> __global__ void in_kernel(const __grid_constant__ dfx_in_params P);
@@ -87,6 +90,45 @@ const void* se_func(int dt, int cl, int ipi = 1) {
                        : reinterpret_cast<const void*>(&dfx::se_kernel<__nv_bfloat16, 8, 1>);
 }
 
+template <typename T, int A>
+const void* dwconv_col_func_a(int s) {
+  return s == 1 ? reinterpret_cast<const void*>(&dfx::dwconv_col_kernel<T, 1, A>)
+                : reinterpret_cast<const void*>(&dfx::dwconv_col_kernel<T, 2, A>);
+}
+template <typename T>
+const void* dwconv_col_func_t(int s, int act) {
+  switch (act) {
+    case DFX_ACT_RELU: return dwconv_col_func_a<T, DFX_ACT_RELU>(s);
+    case DFX_ACT_HARDSWISH: return dwconv_col_func_a<T, DFX_ACT_HARDSWISH>(s);
+    case DFX_ACT_SILU: return dwconv_col_func_a<T, DFX_ACT_SILU>(s);
+    default: return dwconv_col_func_a<T, DFX_ACT_NONE>(s);
+  }
+}
+const void* dwconv_col_func(int dt, int s, int act) {
+  switch (dt) {
+    case DFX_F16: return dwconv_col_func_t<__half>(s, act);
+    case DFX_BF16: return dwconv_col_func_t<__nv_bfloat16>(s, act);
+    case DFX_F16X2: return dwconv_col_func_t<dfx::f16x2>(s, act);
+    case DFX_BF16X2: return dwconv_col_func_t<dfx::bf16x2>(s, act);
+    default: return nullptr;
+  }
+}
+// column-strip depthwise kernel for 3x3 layers (dfx_dw.cu); DFX_DW_COL=0: the tile
+// kernel everywhere (A/B)
+int dw_col_waves() {            // DFX_DW_COL_WAVES: grid size target of the strip split (A/B)
+  static const int w = [] {
+    const char* e = std::getenv("DFX_DW_COL_WAVES");
+    return e ? std::max(1, std::atoi(e)) : 2;
+  }();
+  return w;
+}
+bool dw_col_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("DFX_DW_COL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
 template <typename T, int A>
 const void* dwconv_tile_func_a(int k, int s, int qv) {
 #define DFX_DW_CASE(K, S)                                                                    \
@@ -316,6 +358,15 @@ int config_for(int op, const void* params, size_t size, LaunchCfg* c) {
                          (st == 1 || st == 2) && (p->in.c & 7) == 0 &&
                          ((p->in.coff | p->out.coff | p->in.pitch) & 7) == 0 &&
                          int64_t(p->out.n) * p->out.h * p->out.w * p->in.c < (int64_t(1) << 34);
+      if (tiled && k == 3 && dw_col_enabled()) {
+        const int cg = p->in.c / 8;
+        const int ns = dfx::dw_col_strips(p->out.n, p->out.h, p->out.w, cg, dw_col_waves());
+        const int64_t items = int64_t(p->out.n) * p->out.w * cg;
+        c->func = dwconv_col_func(p->in.dtype, st, p->epi.act1);
+        c->grid = dim3(unsigned(cdiv(items, dfx::kDwColThreads)), unsigned(ns));
+        c->block = dim3(dfx::kDwColThreads);
+        return DFX_OK;
+      }
       if (tiled) {
         // outputs per thread: as many as keep >= 2 waves of 256-thread blocks
         const int64_t rows = int64_t(p->out.n) * p->out.h * (p->in.c / 8);

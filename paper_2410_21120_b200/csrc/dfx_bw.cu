@@ -557,6 +557,10 @@ __global__ void gate_kernel(const __grid_constant__ dfx_gate_params P) {
   griddep_launch();
 }
 
+// Non-finite logits written by out_kernel since the last reset (per device): an
+// fp16 overflow anywhere upstream arrives here as inf / NaN (dfx_common.cuh).
+__device__ unsigned long long g_nonfinite_outputs;
+
 // 16-bit NHWC -> fp32 samples in logical CHW order (also the flatten order).
 template <typename T>
 __global__ void out_kernel(const __grid_constant__ dfx_out_params P) {
@@ -571,7 +575,9 @@ __global__ void out_kernel(const __grid_constant__ dfx_out_params P) {
     const int64_t r = idx - int64_t(n) * per;
     const int c = int(r / hw);
     const int s = int(r - int64_t(c) * hw);
-    P.dst[idx] = ldv1<T>(v, view_pixel_index(v, int64_t(n) * hw + s, c));
+    const float y = ldv1<T>(v, view_pixel_index(v, int64_t(n) * hw + s, c));
+    P.dst[idx] = y;
+    if (!isfinite(y)) atomicAdd(&g_nonfinite_outputs, 1ull);
   }
 }
 
@@ -590,3 +596,14 @@ DFX_INSTANTIATE(out_kernel, dfx_out_params)
 #undef DFX_INSTANTIATE
 
 }  // namespace dfx
+
+extern "C" int dfx_nonfinite_count(int device, unsigned long long* count, int reset) {
+  if (!count) return DFX_E_ARG;
+  if (cudaSetDevice(device) != cudaSuccess) return DFX_E_CUDA;
+  if (cudaMemcpyFromSymbol(count, dfx::g_nonfinite_outputs, sizeof(*count)) != cudaSuccess) return DFX_E_CUDA;
+  if (reset) {
+    const unsigned long long zero = 0;
+    if (cudaMemcpyToSymbol(dfx::g_nonfinite_outputs, &zero, sizeof(zero)) != cudaSuccess) return DFX_E_CUDA;
+  }
+  return 0;
+}

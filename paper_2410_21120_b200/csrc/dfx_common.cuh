@@ -98,8 +98,10 @@ template <bool P = false> DFX_DEV void act8(int act, float* v) {
 }
 
 // ---------------------------------------------------------------- storage types
-// Activations and GEMM operands are 16-bit: bf16 or IEEE half (saturating stores,
-// so an out-of-range value clamps to +-65504 instead of becoming inf).
+// Activations and GEMM operands are 16-bit: bf16 or IEEE half.  Half stores round
+// to nearest WITHOUT saturation: a value beyond the fp16 range becomes +-inf (a
+// split value hi + lo becomes NaN), propagates to the logits, and out_kernel counts
+// it (dfx_nonfinite_count) -- an overflow is never a silently clamped, finite logit.
 //
 // Split precision (f16x2 / bf16x2, dtypes DFX_F16X2 / DFX_BF16X2): every value is
 // stored as TWO 16-bit planes, x = hi + lo with hi = rn16(x), lo = rn16(x - hi),
@@ -129,12 +131,11 @@ template <> struct Elt<__nv_bfloat16> {
 template <> struct Elt<__half> {
   static constexpr int kDtype = DFX_F16;
   static constexpr bool kSplit = false;
-  static DFX_DEV float sat(float v) { return fminf(fmaxf(v, -65504.0f), 65504.0f); }
   static DFX_DEV float to_f(__half v) { return __half2float(v); }
-  static DFX_DEV __half from_f(float v) { return __float2half_rn(sat(v)); }
-  static DFX_DEV uint32_t pack2(float a, float b) {   // one F2FP.SATFINITE: a low, b high
+  static DFX_DEV __half from_f(float v) { return __float2half_rn(v); }
+  static DFX_DEV uint32_t pack2(float a, float b) {   // one F2FP: a low, b high
     uint32_t r;
-    asm("cvt.rn.satfinite.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(b), "f"(a));
+    asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(b), "f"(a));
     return r;
   }
   static DFX_DEV float2 unpack2(uint32_t u) { return __half22float2(*reinterpret_cast<__half2*>(&u)); }

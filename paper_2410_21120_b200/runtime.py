@@ -148,7 +148,7 @@ OP_PARAMS = {OP_GEMM: GemmLaunch, OP_SPLITK: SplitKParams, OP_DWCONV: DwconvPara
 
 # every symbol include/dfx.h declares (tests check the .so exports all of them)
 EXPORTS = (
-    "dfx_last_error", "dfx_abi_version", "dfx_sizeof", "dfx_init", "dfx_device_info", "dfx_mem_info",
+    "dfx_last_error", "dfx_abi_version", "dfx_sizeof", "dfx_init", "dfx_device_info", "dfx_mem_info", "dfx_nonfinite_count",
     "dfx_malloc", "dfx_free", "dfx_memset", "dfx_pool_malloc", "dfx_pool_free", "dfx_pool_trim", "dfx_pool_stats", "dfx_host_alloc", "dfx_host_free",
     "dfx_host_register", "dfx_host_unregister", "dfx_memcpy_h2d", "dfx_memcpy_d2h",
     "dfx_memcpy_d2d", "dfx_arena_upload", "dfx_stream_create", "dfx_stream_destroy",
@@ -282,6 +282,14 @@ def stream_sync(stream) -> None:
 
 def stream_destroy(stream) -> None:
     call("dfx_stream_destroy", vp(stream))
+
+
+def nonfinite_count(device: int = 0, reset: bool = False) -> int:
+    """Non-finite logits the output kernels wrote on ``device`` since the last reset
+    (an fp16 overflow upstream becomes inf / NaN instead of a clamped value)."""
+    n = C.c_ulonglong()
+    call("dfx_nonfinite_count", C.c_int(device), C.byref(n), C.c_int(1 if reset else 0))
+    return n.value
 
 
 def mem_info() -> tuple[int, int]:

@@ -64,13 +64,15 @@ def test_conv_layer(cin, h, w, cout, k, s, p, n):
     assert rel(got, ref) < TOL
 
 
-# depthwise conv: the tiled kernel (square 3x3 / 5x5, stride 1 / 2, C % 8 == 0;
-# 1, 2 or 4 outputs per thread by grid size, ragged last pixel group) and the
+# depthwise conv: 3x3 layers on the column-strip kernel (dfx_dw.cu: whole columns
+# or row strips by grid size, stride 1 / 2, odd sizes), 5x5 on the tiled kernel
+# (1, 2 or 4 outputs per thread by grid size, ragged last pixel group), and the
 # generic kernel (C = 12)
 DW_CASES = [
     # c, h, w, k, stride, n
     (16, 9, 11, 3, 1, 2), (32, 56, 56, 3, 1, 8), (24, 17, 23, 3, 2, 3), (72, 28, 28, 5, 2, 16),
     (40, 14, 13, 5, 1, 4), (96, 112, 112, 3, 2, 2), (12, 10, 10, 3, 1, 2),
+    (1056, 14, 14, 3, 1, 32), (3840, 7, 7, 3, 1, 8), (48, 15, 15, 3, 2, 16), (64, 112, 112, 3, 1, 4),
 ]
 
 
