@@ -217,7 +217,10 @@ typedef struct __attribute__((aligned(64))) dfx_gemm_launch {
   int32_t m2;                      /* any problem has m2 = 1 (sizes smem / TMEM) */
   int32_t se_cr;                   /* desc0.se != NULL: its hidden width (sizes smem) */
   int32_t max_ctas;                /* persistent launch: grid cap (0 = 1-2 CTAs per SM) */
-  int32_t _pad[5];
+  uint32_t l2_pf_units;            /* sizes of l2_pf[0] | l2_pf[1] << 16, in 256-B units */
+  const void* l2_pf[2];            /* weights of the member's next launches: each CTA
+                                      prefetches its slice into L2 before its dependency
+                                      resolves (batch-1 weight streaming off the chain) */
   dfx_gemm_desc desc0;             /* the problem when ndesc == 1 */
 } dfx_gemm_launch;
 

@@ -69,6 +69,11 @@ extern "C" int dfx_debug_timeline(unsigned long long* out, int n) {
 
 namespace dfx {
 
+// L2 prefetch of a global range (16-B aligned, size % 16 == 0): no smem, no barrier
+DFX_DEV void l2_prefetch_bulk(const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
+
 struct GemmHeader {
   uint64_t full[kMaxSlots];
   uint64_t empty[kMaxSlots];
@@ -148,6 +153,18 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(gd->tmap_a);
     tma_prefetch_desc(gd->tmap_b);
+  }
+  if (warp == 1 && lane == 0 && L.l2_pf_units) {
+    // the member's next weight blobs -> L2, one slice per CTA, while this launch
+    // (and its predecessor) run: the next layer's weight TMA then hits L2
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      const uint64_t bytes = uint64_t((L.l2_pf_units >> (16 * r)) & 0xFFFFu) << 8;
+      if (bytes == 0 || L.l2_pf[r] == nullptr) continue;
+      const uint64_t per = ((bytes + gridDim.x - 1) / gridDim.x + 255) & ~uint64_t(255);
+      const uint64_t off = per * blockIdx.x;
+      if (off < bytes) l2_prefetch_bulk(static_cast<const char*>(L.l2_pf[r]) + off, uint32_t(min(per, bytes - off)));
+    }
   }
   tc_fence_before();
   __syncthreads();

@@ -97,6 +97,11 @@ SLACK_SMS = int(os.environ.get("DFX_SLACK_SMS", "0"))
 # batch-1 weight tiles (each read by one or two CTAs) loaded with an L2 evict_first
 # policy, so weight streaming does not evict the members' activations (A/B)
 W_EVICT_FIRST = os.environ.get("DFX_W_EVICT_FIRST", "0") == "1"
+# batch <= 2: every GEMM launch prefetches the member's NEXT weight blobs (the next
+# GEMM's weights, and the SE's FC weights when an SE launch comes first) into L2
+# (dfx_gemm_launch.l2_pf), so a dependent layer's weight TMA hits L2 (A/B)
+L2_PREFETCH = os.environ.get("DFX_L2_PREFETCH", "1") != "0"
+L2_PREFETCH_MAX_BATCH = 2
 # persistent GEMM for grids above this many waves (A/B knob)
 PERSIST_MIN_WAVES = float(os.environ.get("DFX_PERSIST_MIN_WAVES", "2"))
 GEMM_EARLY_PDL = os.environ.get("DFX_GEMM_EARLY_PDL", "0") == "1"            # A/B switch
@@ -1128,6 +1133,44 @@ class ExecInstance:
             out.append(dict(info, op=op, ms=ms, split=len(group) > 1))
         return out
 
+    def _set_l2_prefetch(self, gl, m, prog: MemberProgram, L) -> None:
+        """Ranges for dfx_gemm_launch.l2_pf: the weight blob of the member's next GEMM
+        launch and, when an SE launch comes before it, the SE's blobs (one span),
+        each capped at 16 MB (256-B units in 16 bits)."""
+        arena, skip = self.dag.arena, self.plans[m].skip
+        after = False
+        se_span = gemm_span = None
+        for X in prog.launches:
+            if X.index == L.index:
+                after = True
+                continue
+            if not after or X.index in skip:
+                continue
+            if X.kind == SE and se_span is None and gemm_span is None:
+                keys = [k for k in X.blobs.values()]
+                lo = min(arena.addr(m, k) for k in keys)
+                hi = max(arena.addr(m, k) + prog.blobs[k].nbytes for k in keys)
+                total = sum(prog.blobs[k].nbytes for k in keys)
+                if hi - lo > 2 * total:          # not adjacent in the segment: the largest blob
+                    k = max(keys, key=lambda k: prog.blobs[k].nbytes)
+                    lo, hi = arena.addr(m, k), arena.addr(m, k) + prog.blobs[k].nbytes
+                se_span = (lo, hi - lo)
+            if X.kind == GEMM:
+                k = X.blobs["weight"]
+                gemm_span = (arena.addr(m, k), prog.blobs[k].nbytes)
+                break
+        units, ptrs = 0, []
+        for span in (gemm_span, se_span):
+            if span is None:
+                continue
+            u = min(span[1] >> 8, 0xFFFF)
+            if u:
+                units |= u << (16 * len(ptrs))
+                ptrs.append(span[0])
+        gl.l2_pf_units = units
+        for i, a in enumerate(ptrs):
+            gl.l2_pf[i] = a
+
     def _params(self, m, prog: MemberProgram, L, n, host_descs):
         arena = self.dag.arena
         src = self._view(m, prog, L.src, n)
@@ -1236,6 +1279,8 @@ class ExecInstance:
                     gl.nslots = 4 if planes == 1 else 2
             if W_EVICT_FIRST and not gl.flags & 2 and t["mt_n"] * t["mt_p"] * t["mt_q"] <= 2:
                 gl.flags |= 32               # weights read by <= 2 CTAs each: L2 evict_first
+            if L2_PREFETCH and n <= L2_PREFETCH_MAX_BATCH:
+                self._set_l2_prefetch(gl, m, prog, L)
             if GEMM_DRAIN_STAGED:
                 gl.flags |= 4                # smem-transposed epilogue drain (A/B)
             if GEMM_EARLY_PDL:

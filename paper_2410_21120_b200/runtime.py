@@ -65,7 +65,7 @@ class SeFuse(C.Structure):
 
 class GemmLaunch(C.Structure):
     _fields_ = [("descs", vp), ("ndesc", i32), ("total_tiles", i32), ("bn_max", i32),
-                ("dtype", i32), ("nslots", i32), ("flags", i32), ("m2", i32), ("se_cr", i32), ("max_ctas", i32), ("_pad", i32 * 5),
+                ("dtype", i32), ("nslots", i32), ("flags", i32), ("m2", i32), ("se_cr", i32), ("max_ctas", i32), ("l2_pf_units", C.c_uint32), ("l2_pf", vp * 2),
                 ("desc0", GemmDesc)]
 
 
