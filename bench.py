@@ -510,10 +510,10 @@ def ncu_traffic():
     for f in sorted((ROOT / "profiles").glob("*traffic*.json"), reverse=True):
         try:
             d = json.loads(f.read_text())
-            return d.get("dram_bytes_per_gemm_launch"), f.name
+            return d.get("dram_bytes_per_gemm_launch"), f.name, d.get("note")
         except Exception:  # noqa: BLE001
             continue
-    return None, None
+    return None, None, None
 
 
 # ----------------------------------------------------------------------------- our arm
@@ -716,9 +716,10 @@ def run_ours(args):
         "dominant_class": dom,
     }
 
-    traffic, traffic_src = ncu_traffic()
+    traffic, traffic_src, traffic_note = ncu_traffic()
     roofline["traffic"] = traffic
     roofline["traffic_source"] = traffic_src
+    roofline["traffic_note"] = traffic_note
     roofline["algorithmic_bytes_per_gemm_launch"] = g["bytes"] / max(g["launches"], 1)
     extra = modes = None
     if not args.skip_extra and world == 1:
