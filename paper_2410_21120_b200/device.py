@@ -102,6 +102,7 @@ W_EVICT_FIRST = os.environ.get("DFX_W_EVICT_FIRST", "0") == "1"
 # (dfx_gemm_launch.l2_pf), so a dependent layer's weight TMA hits L2 (A/B)
 L2_PREFETCH = os.environ.get("DFX_L2_PREFETCH", "1") != "0"
 L2_PREFETCH_MAX_BATCH = 2
+L2_PREFETCH_DEPTH = int(os.environ.get("DFX_L2_PREFETCH_DEPTH", "1"))   # A/B: 2 = one launch further
 # persistent GEMM for grids above this many waves (A/B knob)
 PERSIST_MIN_WAVES = float(os.environ.get("DFX_PERSIST_MIN_WAVES", "2"))
 GEMM_EARLY_PDL = os.environ.get("DFX_GEMM_EARLY_PDL", "0") == "1"            # A/B switch
@@ -1135,38 +1136,50 @@ class ExecInstance:
 
     def _set_l2_prefetch(self, gl, m, prog: MemberProgram, L) -> None:
         """Ranges for dfx_gemm_launch.l2_pf: the weight blob of the member's next GEMM
-        launch and, when an SE launch comes before it, the SE's blobs (one span),
-        each capped at 16 MB (256-B units in 16 bits)."""
+        launch and the next SE launch's blobs (one span) when it comes before that
+        GEMM; else (DFX_L2_PREFETCH_DEPTH=2) the weight-bearing launch after the next
+        GEMM.  Each capped at 16 MB (256-B units in 16 bits)."""
         arena, skip = self.dag.arena, self.plans[m].skip
+
+        def span(X):
+            if X.kind == GEMM:
+                k = X.blobs["weight"]
+                return arena.addr(m, k), prog.blobs[k].nbytes
+            keys = list(X.blobs.values())
+            lo = min(arena.addr(m, k) for k in keys)
+            hi = max(arena.addr(m, k) + prog.blobs[k].nbytes for k in keys)
+            total = sum(prog.blobs[k].nbytes for k in keys)
+            if hi - lo > 2 * total:              # not adjacent in the segment: the largest blob
+                k = max(keys, key=lambda k: prog.blobs[k].nbytes)
+                lo, hi = arena.addr(m, k), arena.addr(m, k) + prog.blobs[k].nbytes
+            return lo, hi - lo
+
         after = False
-        se_span = gemm_span = None
+        gemm_span = se_span = extra = None
         for X in prog.launches:
             if X.index == L.index:
                 after = True
                 continue
-            if not after or X.index in skip:
+            if not after or X.index in skip or X.kind not in (GEMM, SE):
                 continue
-            if X.kind == SE and se_span is None and gemm_span is None:
-                keys = [k for k in X.blobs.values()]
-                lo = min(arena.addr(m, k) for k in keys)
-                hi = max(arena.addr(m, k) + prog.blobs[k].nbytes for k in keys)
-                total = sum(prog.blobs[k].nbytes for k in keys)
-                if hi - lo > 2 * total:          # not adjacent in the segment: the largest blob
-                    k = max(keys, key=lambda k: prog.blobs[k].nbytes)
-                    lo, hi = arena.addr(m, k), arena.addr(m, k) + prog.blobs[k].nbytes
-                se_span = (lo, hi - lo)
-            if X.kind == GEMM:
-                k = X.blobs["weight"]
-                gemm_span = (arena.addr(m, k), prog.blobs[k].nbytes)
+            if gemm_span is None:
+                if X.kind == SE:
+                    se_span = se_span or span(X)
+                else:
+                    gemm_span = span(X)
+                    if se_span is not None or L2_PREFETCH_DEPTH < 2:
+                        break
+            else:
+                extra = span(X)
                 break
         units, ptrs = 0, []
-        for span in (gemm_span, se_span):
-            if span is None:
+        for sp in (gemm_span, se_span or extra):
+            if sp is None:
                 continue
-            u = min(span[1] >> 8, 0xFFFF)
+            u = min(sp[1] >> 8, 0xFFFF)
             if u:
                 units |= u << (16 * len(ptrs))
-                ptrs.append(span[0])
+                ptrs.append(sp[0])
         gl.l2_pf_units = units
         for i, a in enumerate(ptrs):
             gl.l2_pf[i] = a
