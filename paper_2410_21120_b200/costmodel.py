@@ -6,7 +6,8 @@ exactly (/root/reference/pkg/src/dagfuse/costmodel.py:252-274, 358-373) so
 ``FusedDag.total_mem_estimate_mib`` is identical to the reference's.  The
 calibration/replay machinery of the reference (Table IV, scenario replays)
 is out of scope: on B200 the swap-in time and peak HBM are *measured*
-(``device.WeightArena.upload`` and ``measured_peak``), not simulated.
+(``device.WeightArena.upload``; cudaMemGetInfo samples in the bench and the
+manager), not simulated.
 """
 
 from __future__ import annotations
@@ -94,7 +95,3 @@ def estimate_memory(manifests: Sequence, mode: str, ct: CostTable = DEFAULT_COST
                    ct.per_model_overhead_mib)
     return MemoryEstimate(ct.context_base_mib, weights, acts, over)
 
-
-def measured_peak(before_free: int, low_water_free: int) -> int:
-    """Peak device bytes of a run from two cudaMemGetInfo samples."""
-    return max(before_free - low_water_free, 0)
