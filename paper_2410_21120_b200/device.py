@@ -94,6 +94,7 @@ SLACK_SPLIT_MAX = int(os.environ.get("DFX_SLACK_SPLIT_MAX", "0"))
 # longest one (A/B: the members with the most slack give up SMs)
 SLACK_FRAC = float(os.environ.get("DFX_SLACK_FRAC", "1.0"))
 SLACK_SMS = int(os.environ.get("DFX_SLACK_SMS", "0"))
+SLACK_DELAY = float(os.environ.get("DFX_SLACK_DELAY", "0"))
 # batch-1 weight tiles (each read by one or two CTAs) loaded with an L2 evict_first
 # policy, so weight streaming does not evict the members' activations (A/B)
 W_EVICT_FIRST = os.environ.get("DFX_W_EVICT_FIRST", "0") == "1"
@@ -754,6 +755,12 @@ class ExecInstance:
         # the persistent kernel with at most k CTAs, so they never hold more than
         # ~k SMs while the critical chain's kernels wait for free SMs
         self.sm_budget = [0] * len(progs)
+        self.sm_budget_slack = [False] * len(progs)
+        if SLACK_DELAY > 0 and dag.mode == "concurrent" and max(batch) <= PRIORITY_MAX_BATCH:
+            est = [sum(_NODE_BASE_US.get(L.kind, 2.5) for L in p.launches) if n > 0 else 0
+                   for p, n in zip(progs, batch)]
+            crit = est.index(max(est))
+            self.sm_budget_slack = [i != crit and e < SLACK_FRAC * est[crit] for i, e in enumerate(est)]
         if (SLACK_SPLIT_MAX or SLACK_SMS) and dag.mode == "concurrent" and max(batch) <= PRIORITY_MAX_BATCH:
             est = [sum(_NODE_BASE_US.get(L.kind, 2.5) for L in p.launches) if n > 0 else 0
                    for p, n in zip(progs, batch)]
@@ -914,6 +921,17 @@ class ExecInstance:
             return nid
 
         order = [m for m in range(len(chains)) if chains[m]]
+        # A/B (DFX_SLACK_DELAY=f): the members with slack (DFX_SLACK_FRAC) start only
+        # once the critical member's chain is f of the way through (a graph edge from
+        # that node to their first node), so their big-grid layers meet its late,
+        # narrow layers instead of its wide early ones
+        delay_after, delayed = None, set()
+        if SLACK_DELAY > 0 and self.dag.mode == "concurrent" and any(self.sm_budget_slack):
+            crit = max(order, key=lambda mm: len(chains[mm]))
+            delayed = {mm for mm in order if self.sm_budget_slack[mm]}
+            delay_after = (crit, int(SLACK_DELAY * len(chains[crit])))
+            order = [crit] + [mm for mm in order if mm != crit]
+        delay_nid = None
         progressed = True
         while progressed:
             progressed = False
@@ -938,8 +956,13 @@ class ExecInstance:
                                   tiling=info["tiling"], geom=info["geom"])
                         add(rt.OP_GEMM, gl, gi, [m, b])
                         pos[b] += 1
+                    elif i == 0 and m in delayed and delay_nid is not None:
+                        tail[m] = delay_nid              # start after the critical chain's node
+                        add(op, params, info, [m])
                     else:
                         add(op, params, info, [m])
+                    if delay_after is not None and (m, i) == delay_after:
+                        delay_nid = tail[m]
                     pos[m] += 1
                     progressed = True
                 if pos[m] == len(items) and seq:
