@@ -78,8 +78,12 @@ const void* gemm_func(int dt, int m2) {
 }
 
 const void* se_func(int dt, int cl, int ipi = 1) {
-  if (dt == DFX_F16X2) return reinterpret_cast<const void*>(&dfx::se_kernel<dfx::f16x2, 16, 1>);
-  if (dt == DFX_BF16X2) return reinterpret_cast<const void*>(&dfx::se_kernel<dfx::bf16x2, 16, 1>);
+  if (dt == DFX_F16X2)
+    return ipi == 4 ? reinterpret_cast<const void*>(&dfx::se_kernel<dfx::f16x2, 16, 4>)
+                    : reinterpret_cast<const void*>(&dfx::se_kernel<dfx::f16x2, 16, 1>);
+  if (dt == DFX_BF16X2)
+    return ipi == 4 ? reinterpret_cast<const void*>(&dfx::se_kernel<dfx::bf16x2, 16, 4>)
+                    : reinterpret_cast<const void*>(&dfx::se_kernel<dfx::bf16x2, 16, 1>);
   if (ipi == 4)
     return dt == DFX_F16 ? reinterpret_cast<const void*>(&dfx::se_kernel<__half, 16, 4>)
                          : reinterpret_cast<const void*>(&dfx::se_kernel<__nv_bfloat16, 16, 4>);
@@ -459,7 +463,11 @@ int config_for(int op, const void* params, size_t size, LaunchCfg* c) {
       // images).  Off by default: the lost pooling/scaling parallelism costs more than
       // the weight traffic saves (EfficientNetV2-L batch 32 6.73 vs 6.07 ms)
       static const int ipi_env = getenv("DFX_SE_IPI") ? atoi(getenv("DFX_SE_IPI")) : 1;
-      const int ipi = (ipi_env == 4 && cl == 16 && p->in.n >= 8 && !dfx::dtype_split(p->in.dtype)) ? 4 : 1;
+      // split precision (DFX_SE_IPI_SPLIT=4, A/B): the hi + lo FC slices double the
+      // per-image L2 weight traffic that 4 images per cluster amortise
+      static const int ipi_split_env = getenv("DFX_SE_IPI_SPLIT") ? atoi(getenv("DFX_SE_IPI_SPLIT")) : 1;
+      const int ipi = (cl == 16 && p->in.n >= 8 &&
+                       (dfx::dtype_split(p->in.dtype) ? ipi_split_env == 4 : ipi_env == 4)) ? 4 : 1;
       const bool split = dfx::dtype_split(p->in.dtype);       // hi + lo FC slices, no x tile
       if (split) cl = 16;
       c->func = se_func(p->in.dtype, cl, ipi);
@@ -636,6 +644,9 @@ int dfx_init(int device) {
                             kIm2colSmemLimit));
     CK(cudaFuncSetAttribute(se_func(dt, 16), cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     CK(cudaFuncSetAttribute(se_func(dt, 16), cudaFuncAttributeMaxDynamicSharedMemorySize, dfx::kSeSmemBudget));
+    CK(cudaFuncSetAttribute(se_func(dt, 16, 4), cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    CK(cudaFuncSetAttribute(se_func(dt, 16, 4), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            dfx::kSeSmemBudget));
   }
   return get_encode();
 }

@@ -596,6 +596,8 @@ DFX_SE_INST(__nv_bfloat16, 16, 4)
 DFX_SE_INST(__half, 16, 4)
 DFX_SE_INST(f16x2, 16, 1)
 DFX_SE_INST(bf16x2, 16, 1)
+DFX_SE_INST(f16x2, 16, 4)
+DFX_SE_INST(bf16x2, 16, 4)
 #undef DFX_SE_INST
 
 }  // namespace dfx
