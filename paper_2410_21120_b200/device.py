@@ -106,6 +106,11 @@ L2_PREFETCH_MAX_BATCH = 2
 L2_PREFETCH_DEPTH = int(os.environ.get("DFX_L2_PREFETCH_DEPTH", "1"))   # A/B: 2 = one launch further
 # persistent GEMM for grids above this many waves (A/B knob)
 PERSIST_MIN_WAVES = float(os.environ.get("DFX_PERSIST_MIN_WAVES", "2"))
+# split precision: slots twice as large (half the prefetched stages per CTA), so the
+# one-tile-per-CTA kernel's per-tile prologue and pipeline fill weigh more -- the
+# persistent walk pays from under one wave (fp16x2 batch 32: 2 waves 18.76 ms,
+# 1.5: 18.03, 1: 17.23, 0.75: 17.18, 0.5: 17.18)
+PERSIST_MIN_WAVES_X2 = float(os.environ.get("DFX_PERSIST_MIN_WAVES_X2", "0.75"))
 GEMM_EARLY_PDL = os.environ.get("DFX_GEMM_EARLY_PDL", "0") == "1"            # A/B switch
 GEMM_DRAIN_STAGED = os.environ.get("DFX_GEMM_DRAIN", "direct") == "staged"   # A/B switch
 # grouped GEMM across members (north-star subsystem 4): pairs of concurrent members
@@ -1300,8 +1305,9 @@ class ExecInstance:
                 need = 128 * (t["bn"] + 4) * 4          # the fp32 partial tile parks in the slots
                 gl.nslots = max(gl.nslots, -(-need // slot_bytes))
             budget = self.sm_budget[m] if t.get("dw") is None and not csplit else 0
-            if GEMM_PERSIST and not gl.m2 and t["splits"] == 1 and \
-                    (t["tiles"] > PERSIST_MIN_WAVES * self.dag.sm_count or budget):
+            if GEMM_PERSIST and not gl.m2 and t["splits"] == 1 and t.get("dw") is None and \
+                    (t["tiles"] > (PERSIST_MIN_WAVES_X2 if planes > 1 else PERSIST_MIN_WAVES)
+                     * self.dag.sm_count or budget):
                 gl.max_ctas = budget
                 gl.flags |= 2                # persistent kernel for multi-wave layers
                 # bn > 64: one CTA per SM, as deep a ring as smem allows; bn <= 64: two

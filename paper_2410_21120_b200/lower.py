@@ -897,6 +897,7 @@ def choose_bn(cout: int) -> tuple[int, int]:
 
 GEMM_M2 = os.environ.get("DFX_GEMM_M2", "1") != "0"     # A/B switch for 256-row CTAs
 BN_FLOOR_MANY_M = int(os.environ.get("DFX_BN_FLOOR_MANY_M", "64"))   # A/B knob
+BN_FLOOR_SUBWAVE_X2 = int(os.environ.get("DFX_BN_FLOOR_SUBWAVE_X2", "128"))   # A/B knob
 SPLIT_MIN_STAGES = int(os.environ.get("DFX_SPLIT_MIN_STAGES", "4"))   # K stages per split, at least
 # split precision: a stage costs 2-3x the MMAs and twice the operand bytes, so fewer,
 # longer splits (measured at batch 1: 4-model fp16x2 3.34 ms at 4, 3.26 at 6, 3.39 at 8)
@@ -941,6 +942,11 @@ def gemm_tiling(geom: dict, n: int, p: int, q: int, sm_count: int = 148, cluster
     # (with many M tiles -- batched layers -- N stays >= BN_FLOOR_MANY_M: an N = 64 MMA
     # costs what an N = 128 one does, so split-K keeps the tensor pipe denser)
     bn_floor = BN_FLOOR_MANY_M if m_tiles >= 8 else 64
+    if planes > 1 and n <= 2 and 8 <= m_tiles < sm_count:
+        # split precision at batch 1-2, sub-wave M (56x56 / 28x28 maps): wide N tiles,
+        # since an N = 2bn MMA costs what an N = bn one does up to 128 (4-model batch 1
+        # fp16x2 2.960 -> 2.947 ms; at batch 32 the same rule cost 17.19 -> 17.53 ms)
+        bn_floor = max(bn_floor, BN_FLOOR_SUBWAVE_X2)
     while m_tiles * nt < sm_count and bn > bn_floor:
         bn = max(bn_floor, round_up(bn // 2, 16))
         nt = -(-geom["cout"] // bn)
