@@ -477,7 +477,11 @@ int config_for(int op, const void* params, size_t size, LaunchCfg* c) {
       // room for the CTA's x slice (latency-bound small batches): the scale reads smem
       // (batch 1: EfficientNetV2-L 2.10 -> 2.08 ms; at batch 32 it costs occupancy)
       static const int xt_batch = getenv("DFX_SE_XTILE_BATCH") ? atoi(getenv("DFX_SE_XTILE_BATCH")) : 8;
-      if ((p->apply & 1) && ipi == 1 && p->in.n < xt_batch) {
+      // split precision keeps it at every batch (the scale's second read is of two
+      // planes): 4-model batch 32 fp16x2 17.08 -> 16.88 ms
+      static const int xt_batch_x2 =
+          getenv("DFX_SE_XTILE_BATCH_X2") ? atoi(getenv("DFX_SE_XTILE_BATCH_X2")) : (1 << 30);
+      if ((p->apply & 1) && ipi == 1 && p->in.n < (split ? xt_batch_x2 : xt_batch)) {
         const size_t xt = size_t(p->in.h) * p->in.w * dfx::se_chan_slice(p->in.c, cl) * 2 * (split ? 2 : 1);
         if (c->smem + xt <= size_t(dfx::kSeSmemBudget)) c->smem += xt;
       }
