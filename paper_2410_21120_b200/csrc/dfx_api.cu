@@ -291,7 +291,10 @@ int config_for(int op, const void* params, size_t size, LaunchCfg* c) {
         c->func = DFX_PICK(gemm_persist_kernel, p->dtype);
         // narrow tiles (bn <= 64): two CTAs per SM with one epilogue group each (two
         // producers / MMA issuers per SM); else one CTA per SM with two groups
-        const int per_sm = (p->bn_max <= 64 && !p->desc0.pre_mode) ? 2 : 1;   // pre_mode: 2 groups
+        // DFX_PERSIST_ONE_CTA_X2=1 (A/B): split precision keeps one CTA per SM with a
+        // deeper ring (its slots are twice as large: 2 CTAs x 2 slots otherwise)
+        static const bool one_x2 = getenv("DFX_PERSIST_ONE_CTA_X2") && atoi(getenv("DFX_PERSIST_ONE_CTA_X2")) == 1;
+        const int per_sm = (p->bn_max <= 64 && !p->desc0.pre_mode && !(planes == 2 && one_x2)) ? 2 : 1;
         const int groups = 3 - per_sm;
         c->smem = dfx::gemm_smem_bytes(p->bn_max, p->nslots, 0, planes) + 1024 +
                   ((p->flags & 4) ? 8 * dfx::kEpiStageWarpBytes : 0) +

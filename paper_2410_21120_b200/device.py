@@ -111,6 +111,7 @@ PERSIST_MIN_WAVES = float(os.environ.get("DFX_PERSIST_MIN_WAVES", "2"))
 # persistent walk pays from under one wave (fp16x2 batch 32: 2 waves 18.76 ms,
 # 1.5: 18.03, 1: 17.23, 0.75: 17.18, 0.5: 17.18)
 PERSIST_MIN_WAVES_X2 = float(os.environ.get("DFX_PERSIST_MIN_WAVES_X2", "0.75"))
+PERSIST_ONE_CTA_X2 = os.environ.get("DFX_PERSIST_ONE_CTA_X2", "0") == "1"   # A/B (dfx_api.cu reads it too)
 GEMM_EARLY_PDL = os.environ.get("DFX_GEMM_EARLY_PDL", "0") == "1"            # A/B switch
 GEMM_DRAIN_STAGED = os.environ.get("DFX_GEMM_DRAIN", "direct") == "staged"   # A/B switch
 # grouped GEMM across members (north-star subsystem 4): pairs of concurrent members
@@ -1317,6 +1318,8 @@ class ExecInstance:
                     gl.nslots = max(2, min(8, (GEMM_SMEM_LIMIT - GEMM_SMEM_FIXED - vec
                                                - (8 * 2560 if GEMM_DRAIN_STAGED else 0))
                                            // slot_bytes))
+                elif planes > 1 and PERSIST_ONE_CTA_X2:      # one CTA per SM, deeper ring (A/B)
+                    gl.nslots = max(2, min(8, (GEMM_SMEM_LIMIT - GEMM_SMEM_FIXED) // slot_bytes))
                 else:
                     gl.nslots = 4 if planes == 1 else 2
             if W_EVICT_FIRST and not gl.flags & 2 and t["mt_n"] * t["mt_p"] * t["mt_q"] <= 2:
